@@ -1,0 +1,134 @@
+"""Parity cases shared by the golden generator, the oracle tests and the GPU tests.
+
+Each case names one Hybrid-Fortran app, its module scalars and the synthetic
+fills of its module arrays (value = offset + scale * u(seed, flat),
+flat = the logical row-major index over the declared dims). The golden fixtures
+under tests/golden/ hold what the REFERENCE INTERPRETER produced for these
+inputs (oracle/_ref/hft_ref, see tests/golden/make_golden.py).
+"""
+from dataclasses import dataclass, field
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parents[1]
+REF_APPS = Path("/root/reference/proj/tests/data/apps")  # generation time only
+OWN_APPS = REPO / "apps"
+
+
+@dataclass
+class App:
+    name: str
+    sources: list          # (root, relative path); root "ref" or "own"
+    module: str            # state module
+    arrays: dict           # name -> tuple of declared-dim expressions (for shapes)
+    outputs: list          # arrays/scalars compared after the run
+    families: list = field(default_factory=list)
+    entry: str = "main"
+    backend: str = "cuda"
+
+
+APPS = {
+    "diffusion": App(
+        "diffusion", [("ref", "diffusion/diffusion.h90")], "diff_state",
+        {"t_old": ("nz", "nx", "ny"), "t_new": ("nz", "nx", "ny")},
+        ["t_old", "t_new"]),
+    "damping": App(
+        "damping", [("ref", "damping/damping.h90")], "svar",
+        {"dens_ref_f": ("nz_mn:nz_mx", "nx_mn:nx_mx", "ny_mn:ny_mx"),
+         "dens_ptb_damp": ("nz_mn:nz_mx", "nx_mn:nx_mx", "ny_mn:ny_mx"),
+         "dens_ptb_bnd": ("nz_mn:nz_mx", "nx_mn:nx_mx", "ny_mn:ny_mx", "2")},
+        ["dens_ptb_damp", "dens_ref_f", "dens_ptb_bnd"],
+        families=[("AT_TIGHT_STENCIL", "DOM_TIGHT_STENCIL"),
+                  ("AT4_TIGHT_STENCIL", "DOM4_TIGHT_STENCIL")]),
+    "bounded": App(
+        "bounded", [("ref", "bounded/bounded.h90")], "b_state",
+        {"a": ("nx", "ny"), "b": ("nx", "ny")}, ["a", "b"]),
+    "surface_flux": App(
+        "surface_flux",
+        [("ref", "surface_flux/sf_state.h90"), ("ref", "surface_flux/surface_flux.h90"),
+         ("ref", "surface_flux/driver.h90")], "sf_state",
+        {"cover_frac": ("ntlm", "nx", "ny"), "wind_speed": ("nx", "ny"),
+         "flx_sum_x": ("nx", "ny"), "flx_sum_y": ("nx", "ny")},
+        ["cover_frac", "wind_speed", "flx_sum_x", "flx_sum_y"]),
+    "reduction": App(
+        "reduction", [("ref", "reduction/reduction.h90")], "red_state",
+        {"y": ("nz", "nx", "ny")}, ["total", "y"], backend="acc"),
+    "dycore": App(
+        "dycore", [("own", "dycore/dyn_state.h90"), ("own", "dycore/dycore.h90")], "dyn_state",
+        {n: ("nz", "nx", "ny") for n in ("rho", "th", "u", "v", "w", "p")},
+        ["th", "u", "v", "w", "p", "rho"]),
+}
+
+# Synthetic-state conventions; seeds are fixed per field.
+DYCORE_SCALARS = {"dt": 0.1, "rdx": 2.0, "rdy": 2.0, "rdz": 20.0, "cs2": 1.0,
+                  "grav": 0.0327, "th0": 300.0}
+DYCORE_FILLS = {  # name: (seed, offset, scale)
+    "rho": (7, 1.0, 0.1), "th": (8, 300.0, 1.0), "u": (9, -0.01, 0.02),
+    "v": (10, -0.01, 0.02), "w": (11, -0.002, 0.004), "p": (12, -0.005, 0.01)}
+
+
+@dataclass
+class Case:
+    name: str
+    app: str
+    ints: dict
+    reals: dict
+    fills: dict            # name -> (seed, offset, scale)
+    unset: list = field(default_factory=list)
+    gpu_check: bool = True  # also run run_gpu_simulated and require equality
+    order: str = "shuffled"
+
+
+def _diff(name, nx, ny, nz, nsteps, seed=1, off=280.0, scale=10.0, coef=0.1):
+    return Case(name, "diffusion", dict(nx=nx, ny=ny, nz=nz, nsteps=nsteps), dict(coef=coef),
+                {"t_old": (seed, off, scale)}, unset=["t_new"])
+
+
+def _dyc(name, nx, ny, nz, nsteps, gpu_check=True):
+    return Case(name, "dycore", dict(nx=nx, ny=ny, nz=nz, nsteps=nsteps), dict(DYCORE_SCALARS),
+                dict(DYCORE_FILLS), gpu_check=gpu_check)
+
+
+CASES = [
+    # SURVEY §8(c) anchor: sum(t_old) after 10 steps == 2054.7107351501668
+    _diff("diffusion_16x16x16_s10_anchor", 16, 16, 16, 10, seed=0, off=0.0, scale=1.0),
+    _diff("diffusion_37x21x9_s3", 37, 21, 9, 3),
+    _diff("diffusion_1x1x3_s2", 1, 1, 3, 2),
+    _diff("diffusion_31x5x3_s2", 31, 5, 3, 2),
+    _diff("diffusion_32x5x3_s2", 32, 5, 3, 2),
+    _diff("diffusion_33x5x3_s2", 33, 5, 3, 2),
+    _diff("diffusion_67x5x3_s2", 67, 5, 3, 2),
+    _diff("diffusion_67x1x3_s2", 67, 1, 3, 2),
+    _diff("diffusion_40x36x58_s1", 40, 36, 58, 1),
+    Case("damping_37x21x9", "damping",
+         dict(nx_mn=-1, nx_mx=35, ny_mn=0, ny_mx=20, nz_mn=1, nz_mx=9),
+         dict(tratio_bnd=0.3, mtratio_bnd=0.7),
+         {"dens_ref_f": (2, 1.0, 1.0), "dens_ptb_bnd": (3, -0.005, 0.01)}, unset=["dens_ptb_damp"]),
+    Case("damping_1x1x1", "damping",
+         dict(nx_mn=1, nx_mx=1, ny_mn=1, ny_mx=1, nz_mn=1, nz_mx=1),
+         dict(tratio_bnd=0.3, mtratio_bnd=0.7),
+         {"dens_ref_f": (2, 1.0, 1.0), "dens_ptb_bnd": (3, -0.005, 0.01)}, unset=["dens_ptb_damp"]),
+    Case("damping_70x9x58_neg", "damping",
+         dict(nx_mn=-3, nx_mx=66, ny_mn=-2, ny_mx=6, nz_mn=0, nz_mx=57),
+         dict(tratio_bnd=0.3, mtratio_bnd=0.7),
+         {"dens_ref_f": (2, 1.0, 1.0), "dens_ptb_bnd": (3, -0.005, 0.01)}, unset=["dens_ptb_damp"]),
+    Case("bounded_37x21", "bounded", dict(nx=37, ny=21), {},
+         {"a": (4, 0.0, 1.0), "b": (6, -1.0, 0.5)}),
+    Case("bounded_3x3", "bounded", dict(nx=3, ny=3), {},
+         {"a": (4, 0.0, 1.0), "b": (6, -1.0, 0.5)}),
+    Case("bounded_67x34", "bounded", dict(nx=67, ny=34), {},
+         {"a": (4, 0.0, 1.0), "b": (6, -1.0, 0.5)}),
+    Case("surface_flux_37x21_t1", "surface_flux", dict(nx=37, ny=21, tile_land=1), {},
+         {"cover_frac": (5, 0.0, 1.0)}, unset=["wind_speed", "flx_sum_x", "flx_sum_y"]),
+    Case("surface_flux_33x7_t3", "surface_flux", dict(nx=33, ny=7, tile_land=3), {},
+         {"cover_frac": (5, 0.0, 1.0)}, unset=["wind_speed", "flx_sum_x", "flx_sum_y"]),
+    Case("reduction_37x21x9", "reduction", dict(nx=37, ny=21, nz=9), dict(total=0.0),
+         {"y": (6, 0.0, 1.0)}),
+    Case("reduction_67x5x58", "reduction", dict(nx=67, ny=5, nz=58), dict(total=0.0),
+         {"y": (6, 0.0, 1.0)}),
+    _dyc("dycore_13x7x10_s3", 13, 7, 10, 3),
+    _dyc("dycore_24x20x12_s2", 24, 20, 12, 2),
+    _dyc("dycore_1x5x2_s2", 1, 5, 2, 2),
+    _dyc("dycore_33x3x58_s1", 33, 3, 58, 1),
+    _dyc("dycore_13x7x10_s100", 13, 7, 10, 100, gpu_check=False),
+]
+CASE_BY_NAME = {c.name: c for c in CASES}
