@@ -1,0 +1,360 @@
+#!/usr/bin/env python3
+"""Benchmark: one ASUCA-style dry dynamical-core timestep (flux-limited advection,
+pressure gradient + divergence, HE-VI vertically implicit Thomas solve) per step.
+
+Workload (BASELINE.json configs[1]): 512 x 512 x 58 per GPU, fp64, synthetic state
+(SURVEY §8(d) SplitMix64 fields). Metric: grid-point updates per second per timestep
+(nx*ny*nz / t_step, whole job) and the HBM-roofline fraction of the dominant kernel.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun, one rank per GPU: a 2-D (px x py) horizontal block
+decomposition with NCCL halo exchange, WEAK scaling (a 512 x 512 x 58 tile per GPU).
+`--impl reference` times the reference's own CPU path (oracle/_ref/hft_ref: the
+reference interpreter built from /root/reference/proj/src) on the host cores.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+NX, NY, NZ = 512, 512, 58
+METRIC = "grid-point updates/sec per timestep"
+UNIT = "grid-point updates/s"
+GRIDS = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
+# compulsory HBM bytes per grid point and step of each native kernel:
+# advect reads th,u,v,w and writes th' (5 x 8 B); acoustic reads rho,th,u,v,w,p and
+# writes u',v',w',p' (10 x 8 B)
+BYTES_PER_POINT = {"dycore_advect": 40, "dycore_acoustic": 80}
+L2_BYTES = 126 * 2**20
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.3)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[q] for r in self.rows for q in range(4)
+                          if r[2 + q].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def make_state(eng, d, px, py):
+    """Bind the synthetic state of this rank's tile (global-flat-indexed fields)."""
+    from paper_1710_08616_b200 import synthetic
+    gnx, gny = NX * px, NY * py
+    box = [(0, NZ), (d.i0, d.i0 + d.nx), (d.j0, d.j0 + d.ny)]
+    arrs = {k: synthetic.field((NZ, gnx, gny), *v, box=box, order="F")
+            for k, v in synthetic.DYCORE_FILLS.items()}
+    for k, v in dict(nx=int(d.nx), ny=int(d.ny), nz=NZ, nsteps=1).items():
+        eng.set(k, v)
+    for k, v in synthetic.DYCORE_SCALARS.items():
+        eng.set(k, v)
+    for k, a in arrs.items():
+        eng.bind(k, a, pin=True)
+    return arrs
+
+
+def cpu_baseline_port(seconds_budget=20.0):
+    """The C restatement (oracle/, KIJ storage, OpenMP over j on every host core) timed on
+    a bounded sample of the same workload: whole 512x512x58 dycore steps."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle
+    from paper_1710_08616_b200 import synthetic
+    cores = os.cpu_count() or 1
+    oracle.set_threads(cores)
+    a = {k: synthetic.field((NZ, NX, NY), *v, order="F") for k, v in synthetic.DYCORE_FILLS.items()}
+    oracle.dycore_run(1, synthetic.DYCORE_SCALARS, a["rho"], a["th"], a["u"], a["v"], a["w"],
+                      a["p"])  # warm (scratch allocation, page faults)
+    steps, t0 = 0, time.perf_counter()
+    while True:
+        oracle.dycore_run(1, synthetic.DYCORE_SCALARS, a["rho"], a["th"], a["u"], a["v"],
+                          a["w"], a["p"])
+        steps += 1
+        el = time.perf_counter() - t0
+        if el > seconds_budget / 2 or steps >= 20:
+            break
+    return {"value": NX * NY * NZ * steps / el, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{steps} full dycore steps of {NX}x{NY}x{NZ} (oracle/hfb_oracle.c, "
+                      f"KIJ order, OpenMP {cores} threads), {el:.2f} s"}
+
+
+def bench_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_1710_08616_b200 as hfb
+
+    rank, world, local = dist_env()
+    n = args.gpus
+    if world != n:
+        raise SystemExit(f"--gpus {n} but WORLD_SIZE={world}")
+    if n not in GRIDS:
+        raise SystemExit("--gpus must be 1, 2, 4 or 8")
+    px, py = GRIDS[n]
+    torch.cuda.set_device(local)
+    if n > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    eng = hfb.Engine("dycore", device=local)
+    d = hfb.decomp_init(NX * px, NY * py, NZ, px, py, rank, halo=2)
+    if n > 1:
+        obj = [hfb.runtime.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        eng.set_decomposition(d, obj[0])
+    arrs = make_state(eng, d, px, py)
+    for k in arrs:
+        eng.copy_to_device(k)
+    eng.synchronize()
+
+    # ---- device-resident timed region: K timesteps ------------------------------------
+    stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
+    for _ in range(args.warmup):
+        eng.enqueue("dycore_step")
+    eng.synchronize()
+    eng.profile(True, clear=True)
+    eng.profile(True)
+
+    def barrier():
+        if n > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    t_ev0 = torch.cuda.Event(enable_timing=True)
+    t_ev1 = torch.cuda.Event(enable_timing=True)
+    launches = 0
+    barrier()
+    with ClockSampler(local) as clocks:
+        t_ev0.record(stream)
+        for _ in range(args.steps):
+            launches += eng.enqueue("dycore_step").native_launches
+        t_ev1.record(stream)
+        eng.synchronize()
+    barrier()
+    ms = t_ev0.elapsed_time(t_ev1)
+    eng.profile(False)
+    kt = {k: eng.kernel_time(k) for k in BYTES_PER_POINT}
+    if n > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    pts_step = NX * NY * NZ * n
+    value = pts_step * args.steps / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (live CUDA events over the timed region) -------
+    hbm, src = peaks()
+    dom = max(kt, key=lambda k: kt[k][0])
+    dom_ms, dom_n = kt[dom]
+    pts_local = int(d.nx) * int(d.ny) * NZ
+    alg_bytes = BYTES_PER_POINT[dom] * pts_local
+    achieved = alg_bytes / (dom_ms / dom_n / 1e3) / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get(dom)
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": traffic, "kernel": dom,
+                "peak_source": src, "algorithmic_bytes_per_launch": alg_bytes,
+                "kernel_ms_avg": round(dom_ms / dom_n, 5),
+                "share_of_step": round(dom_ms / ms, 3),
+                "kernels": {k: {"ms_avg": round(v[0] / max(v[1], 1), 5),
+                                "GBps": round(BYTES_PER_POINT[k] * pts_local /
+                                              (v[0] / max(v[1], 1) / 1e3) / 1e9, 1)}
+                            for k, v in kt.items()}}
+
+    # ---- end to end through the public API with host buffers --------------------------
+    # one e2e step = one call of the program's `main` entry (transferHere copy-in of the six
+    # state arrays from pinned host memory, `nsteps` timesteps, copy-out), as the
+    # generated host code does (codegen.cpp:570-600)
+    e2e_nsteps = 100
+    eng2 = hfb.Engine("dycore", device=local)
+    if n > 1:
+        obj = [hfb.runtime.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        eng2.set_decomposition(d, obj[0])
+    arrs2 = make_state(eng2, d, px, py)
+    eng2.set("nsteps", e2e_nsteps)
+    eng2.run("main")  # warm-up call
+    arrs2 = make_state(eng2, d, px, py)
+    eng2.set("nsteps", e2e_nsteps)
+    e2e_calls = max(1, min(3, args.steps // 10))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_calls):
+        eng2.run("main")
+    t1 = time.perf_counter()
+    e2e_s = t1 - t0
+    if n > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    field_bytes = pts_local * 8
+    h2d = 6 * field_bytes
+    d2h = 6 * field_bytes
+    e2e = {"value": pts_step * e2e_nsteps * e2e_calls / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "step": f"one `main` call through the C ABI: copy-in of 6 pinned host fields, "
+                   f"{e2e_nsteps} timesteps, copy-out", "timesteps_per_step": e2e_nsteps,
+           "calls": e2e_calls}
+    halo = eng.halo_bytes()
+    eng2.close()
+    eng.close()
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": n,
+               "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic (SplitMix64 fields, SURVEY §8(d))",
+               "config": {"workload": f"dycore+HE-VI {NX}x{NY}x{NZ} per GPU (BASELINE configs[1])",
+                          "global_grid": [NX * px, NY * py, NZ], "decomposition": f"{px}x{py}",
+                          "l2": f"inputs larger than L2: {6 * NX * NY * NZ * 8 / 2**30:.2f} GiB "
+                                f"state + {5 * NX * NY * NZ * 8 / 2**30:.2f} GiB outputs per step "
+                                f"vs 126 MB L2"},
+               "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
+               "clocks": clocks.summary(), "halo_bytes": halo}
+        out["cpu_baseline"] = cpu_baseline_port() if n == 1 else None
+        print(json.dumps(out), flush=True)
+    if n > 1:
+        dist.destroy_process_group()
+
+
+def bench_reference(args):
+    """The reference's own CPU path: its binary64 interpreter (oracle/_ref/hft_ref, compiled
+    from /root/reference/proj/src) running this repo's dycore app (apps/dycore, the
+    reference dialect) through run_reference. It is single-threaded by design
+    (SPEC.md:476), so every host core runs one independent interpreter over its own
+    SAMPLE_NX x SAMPLE_NY x 58 column block of the workload; a step is one timestep of
+    all blocks."""
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    hft = ROOT / "oracle" / "_ref" / "hft_ref"
+    if not hft.exists():
+        subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "ref"], check=True)
+    from paper_1710_08616_b200 import synthetic
+    cores = os.cpu_count() or 1
+    sx, sy = 16, 16
+    tmp = Path(tempfile.mkdtemp(prefix="hftref_"))
+    scen = tmp / "dycore.sc"
+    lines = [f"source {ROOT / 'apps/dycore/dyn_state.h90'}",
+             f"source {ROOT / 'apps/dycore/dycore.h90'}", "mode ref", "entry main",
+             "max_steps 2000000000", f"int dyn_state nx {sx}", f"int dyn_state ny {sy}",
+             f"int dyn_state nz {NZ}", "int dyn_state nsteps 1"]
+    lines += [f"real dyn_state {k} {float(v).hex()}" for k, v in synthetic.DYCORE_SCALARS.items()]
+    lines += [f"fill dyn_state {k} {s} {float(o).hex()} {float(c).hex()}"
+              for k, (s, o, c) in synthetic.DYCORE_FILLS.items()]
+    scen.write_text("\n".join(lines) + "\n")
+
+    def one_step():
+        procs = [subprocess.Popen([str(hft), str(scen)], stdout=subprocess.DEVNULL)
+                 for _ in range(cores)]
+        for p in procs:
+            if p.wait() != 0:
+                raise RuntimeError("reference interpreter failed")
+
+    for _ in range(args.warmup):
+        one_step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one_step()
+    el = time.perf_counter() - t0
+    value = cores * sx * sy * NZ * args.steps / el
+    sample = (f"{cores} concurrent reference interpreters (run_reference, 1 thread each), "
+              f"each one timestep of a {sx}x{sy}x{NZ} block of the {NX}x{NY}x{NZ} workload")
+    out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (SplitMix64 fields, SURVEY §8(d))", "impl": "reference",
+           "config": {"workload": f"dycore+HE-VI {NX}x{NY}x{NZ} per GPU (BASELINE configs[1])"},
+           "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cores,
+                            "kind": "reference", "sample": sample},
+           "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_ours(args)
+
+
+if __name__ == "__main__":
+    main()

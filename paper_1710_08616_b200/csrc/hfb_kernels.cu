@@ -1,0 +1,666 @@
+// hfb_kernels.cu — sm_100a kernels of the Hybrid-Fortran timestep hot path.
+//
+// Every kernel maps one thread to one (i,j) column of the domain and marches K
+// sequentially (K is executed sequentially, I/J are the parallel
+// domain), over the I-fastest device order of hfb_layout.cuh, so each warp touches
+// 32 consecutive i of one row per access (fully coalesced 256-B requests).
+//
+// Bit-exactness: compiled with -fmad=false (no FMA contraction), IEEE division and
+// sqrt; every expression is written in the reference's left-associative evaluation
+// order (parser.cpp:174-211, interp.cpp:661-770), so results equal the reference
+// interpreter's binary64 results bit for bit.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "hfb_kernels.cuh"
+
+namespace hfb {
+
+namespace {
+
+inline dim3 span_grid(const Span& sp, dim3 block, unsigned z = 1) {
+  int64_t ex = sp.ihi - sp.ilo + 1, ey = sp.jhi - sp.jlo + 1;
+  return dim3(static_cast<unsigned>((ex + block.x - 1) / block.x),
+              static_cast<unsigned>((ey + block.y - 1) / block.y), z);
+}
+
+inline bool span_empty(const Span& sp) { return sp.ihi < sp.ilo || sp.jhi < sp.jlo; }
+
+}  // namespace
+
+// ============================================================================
+// relayout: dense host order (any dim permutation) <-> device layout.
+// One 32x32 tile of the (I, F) plane per block, F = the host-fastest role;
+// smem transpose so both global sides are coalesced.
+// ============================================================================
+namespace {
+struct RelayoutArgs {
+  const double* src;
+  double* dst;
+  Relayout r;
+  int r1, r2;  // the two roles enumerated by blockIdx.z
+  bool to_device;
+};
+
+__global__ void __launch_bounds__(256) k_relayout(RelayoutArgs a) {
+  __shared__ double tile[32][33];
+  const Relayout& r = a.r;
+  const int F = r.fast;
+  const int64_t z = blockIdx.z;
+  const int64_t n1 = r.ext[a.r1];
+  const int64_t c1 = z % n1, c2 = z / n1;
+  const int64_t hrest = c1 * r.hs[a.r1] + c2 * r.hs[a.r2];
+  const int64_t drest = c1 * r.ds[a.r1] + c2 * r.ds[a.r2];
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int64_t f0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  if (F == kRoleI) {
+    // host already I-fastest: straight coalesced copy of rows (blockIdx.y over J*...)
+    for (int rr = ty; rr < 32; rr += 8) {
+      int64_t i = i0 + tx, f = f0 + rr;  // here "f" walks J
+      if (i < r.ext[kRoleI] && f < r.ext[kRoleJ]) {
+        int64_t h = i * r.hs[kRoleI] + f * r.hs[kRoleJ] + hrest;
+        int64_t d = i + f * r.ds[kRoleJ] + drest;
+        if (a.to_device)
+          a.dst[d] = a.src[h];
+        else
+          a.dst[h] = a.src[d];
+      }
+    }
+    return;
+  }
+  if (a.to_device) {
+    for (int rr = ty; rr < 32; rr += 8) {  // read along F (host-contiguous)
+      int64_t i = i0 + rr, f = f0 + tx;
+      if (i < r.ext[kRoleI] && f < r.ext[F]) tile[rr][tx] = a.src[i * r.hs[kRoleI] + f + hrest];
+    }
+    __syncthreads();
+    for (int rr = ty; rr < 32; rr += 8) {  // write along I (device-contiguous)
+      int64_t i = i0 + tx, f = f0 + rr;
+      if (i < r.ext[kRoleI] && f < r.ext[F]) a.dst[i + f * r.ds[F] + drest] = tile[tx][rr];
+    }
+  } else {
+    for (int rr = ty; rr < 32; rr += 8) {  // read along I (device)
+      int64_t i = i0 + tx, f = f0 + rr;
+      if (i < r.ext[kRoleI] && f < r.ext[F]) tile[rr][tx] = a.src[i + f * r.ds[F] + drest];
+    }
+    __syncthreads();
+    for (int rr = ty; rr < 32; rr += 8) {  // write along F (host)
+      int64_t i = i0 + rr, f = f0 + tx;
+      if (i < r.ext[kRoleI] && f < r.ext[F]) a.dst[i * r.hs[kRoleI] + f + hrest] = tile[tx][rr];
+    }
+  }
+}
+}  // namespace
+
+cudaError_t launch_relayout(const double* src, double* dst, const Relayout& r, bool to_device,
+                            cudaStream_t s) {
+  RelayoutArgs a{src, dst, r, 0, 0, to_device};
+  int F = r.fast;
+  int rest[3], n = 0;
+  int second = (F == kRoleI) ? kRoleJ : F;
+  for (int role = 0; role < 4; ++role)
+    if (role != kRoleI && role != second) rest[n++] = role;
+  a.r1 = rest[0];
+  a.r2 = rest[1];
+  int64_t gz = r.ext[a.r1] * r.ext[a.r2];
+  if (r.ext[kRoleI] <= 0 || r.ext[second] <= 0 || gz <= 0) return cudaSuccess;
+  if (gz > 65535) return cudaErrorInvalidConfiguration;
+  dim3 block(32, 8);
+  dim3 grid(static_cast<unsigned>((r.ext[kRoleI] + 31) / 32),
+            static_cast<unsigned>((r.ext[second] + 31) / 32), static_cast<unsigned>(gz));
+  k_relayout<<<grid, block, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// diffusion.h90:23-41 — 7-point stencil with the Dirichlet copy on the GLOBAL
+// boundary; K neighbours live in registers (k-1, k, k+1 rotate), I/J neighbours
+// come from L1 (each is loaded by the adjacent threads of the same warp/block).
+// hfk1 (t_old = t_new) is fused away: the step result goes to out1 and, when the
+// caller needs both arrays materialised, to out2.
+// ============================================================================
+namespace {
+struct DiffArgs {
+  const double* __restrict__ src;
+  double* __restrict__ o1;
+  double* __restrict__ o2;
+  Grid3 g;
+  int nz, kchunk;
+  double coef;
+  Span sp;
+};
+
+__global__ void __launch_bounds__(256) k_diffusion(DiffArgs a) {
+  const int64_t i = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t j = a.sp.jlo + static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y;
+  if (i > a.sp.ihi || j > a.sp.jhi) return;
+  const int kb = 1 + static_cast<int>(blockIdx.z) * a.kchunk;
+  const int ke = min(a.nz, kb + a.kchunk - 1);
+  const int64_t gi = i + a.sp.i0, gj = j + a.sp.j0;
+  const bool hb = (gi == 1) | (gi == a.sp.gnx) | (gj == 1) | (gj == a.sp.gny);
+  const int64_t P = a.g.plane, W = a.g.pitch;
+  const int64_t col = (j - 1) * W + (i - 1);
+  const double* __restrict__ src = a.src + col;
+  double* o1 = a.o1 + col;
+  double* o2 = a.o2 ? a.o2 + col : nullptr;
+  const int nz = a.nz;
+  const double coef = a.coef;
+  double km1 = (kb > 1) ? __ldg(src + (kb - 2) * P) : 0.0;
+  double k0 = __ldg(src + (kb - 1) * P);
+#pragma unroll 4
+  for (int k = kb; k <= ke; ++k) {
+    const double kp1 = (k < nz) ? __ldg(src + static_cast<int64_t>(k) * P) : 0.0;
+    double out;
+    if (hb || k == 1 || k == nz) {
+      out = k0;
+    } else {
+      const double* c = src + static_cast<int64_t>(k - 1) * P;
+      double s = km1 + kp1;
+      s = s + __ldg(c - 1);
+      s = s + __ldg(c + 1);
+      s = s + __ldg(c - W);
+      s = s + __ldg(c + W);
+      s = s - 6.0 * k0;
+      out = k0 + coef * s;
+    }
+    const int64_t off = static_cast<int64_t>(k - 1) * P;
+    o1[off] = out;
+    if (o2) o2[off] = out;
+    km1 = k0;
+    k0 = kp1;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_copy_columns(const double* __restrict__ src,
+                                                      double* __restrict__ dst, Grid3 g, int nz,
+                                                      Span sp) {
+  const int64_t i = sp.ilo + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t j = sp.jlo + static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y;
+  if (i > sp.ihi || j > sp.jhi) return;
+  const int64_t col = (j - 1) * g.pitch + (i - 1);
+  for (int k = 0; k < nz; ++k) dst[col + k * g.plane] = src[col + k * g.plane];
+}
+}  // namespace
+
+cudaError_t launch_diffusion(const double* t_old, double* out1, double* out2, Grid3 g,
+                             int64_t nz, double coef, const Span& sp, cudaStream_t s) {
+  if (span_empty(sp) || nz <= 0) return cudaSuccess;
+  dim3 block(32, 8);
+  int64_t cols = (sp.ihi - sp.ilo + 1) * (sp.jhi - sp.jlo + 1);
+  // Small grids cannot fill 148 SMs with one thread per column: split K into chunks
+  // (each chunk re-reads its two boundary planes) until ~4 waves of columns exist.
+  int64_t target = 148LL * 2048 * 2;
+  int kchunks = 1;
+  while (cols * kchunks < target && nz / (kchunks * 2) >= 8) kchunks *= 2;
+  int kchunk = static_cast<int>((nz + kchunks - 1) / kchunks);
+  kchunks = static_cast<int>((nz + kchunk - 1) / kchunk);
+  DiffArgs a{t_old, out1, out2, g, static_cast<int>(nz), kchunk, coef, sp};
+  k_diffusion<<<span_grid(sp, block, kchunks), block, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_columns(const double* src, double* dst, Grid3 g, int64_t nz,
+                                const Span& sp, cudaStream_t s) {
+  if (span_empty(sp) || nz <= 0) return cudaSuccess;
+  dim3 block(32, 8);
+  k_copy_columns<<<span_grid(sp, block), block, 0, s>>>(src, dst, g, static_cast<int>(nz), sp);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// damping.h90:38-48 — pointwise: d = (m*(r + b1) + t*(r + b2)) - r.
+// One thread per (i, j, k) element (no reuse to exploit; pure streaming).
+// ============================================================================
+namespace {
+__global__ void __launch_bounds__(256) k_damping(const double* __restrict__ ref,
+                                                 const double* __restrict__ b1,
+                                                 const double* __restrict__ b2,
+                                                 double* __restrict__ d, Grid3 g, double m,
+                                                 double t, Span sp) {
+  const int64_t i = sp.ilo + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t j = sp.jlo + static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y;
+  if (i > sp.ihi || j > sp.jhi) return;
+  const int64_t idx = g.at(i - 1, j - 1, blockIdx.z);
+  const double r = __ldg(ref + idx);
+  d[idx] = (m * (r + __ldg(b1 + idx)) + t * (r + __ldg(b2 + idx))) - r;
+}
+}  // namespace
+
+cudaError_t launch_damping(const double* ref, const double* bnd1, const double* bnd2,
+                           double* damp, Grid3 g, int64_t nk, double mtratio, double tratio,
+                           const Span& sp, cudaStream_t s) {
+  if (span_empty(sp) || nk <= 0) return cudaSuccess;
+  if (nk > 65535) return cudaErrorInvalidConfiguration;
+  dim3 block(32, 8);
+  k_damping<<<span_grid(sp, block, static_cast<unsigned>(nk)), block, 0, s>>>(
+      ref, bnd1, bnd2, damp, g, mtratio, tratio, sp);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// bounded.h90:19-21 — 2-D 5-point average.
+// ============================================================================
+namespace {
+__global__ void __launch_bounds__(256) k_bounded(const double* __restrict__ a,
+                                                 double* __restrict__ b, int64_t W, Span sp) {
+  const int64_t i = sp.ilo + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t j = sp.jlo + static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y;
+  if (i > sp.ihi || j > sp.jhi) return;
+  const double* c = a + (j - 1) * W + (i - 1);
+  b[(j - 1) * W + (i - 1)] =
+      0.25 * (((__ldg(c - 1) + __ldg(c + 1)) + __ldg(c - W)) + __ldg(c + W));
+}
+}  // namespace
+
+cudaError_t launch_bounded(const double* a, double* b, int64_t pitch, const Span& sp,
+                           cudaStream_t s) {
+  if (span_empty(sp)) return cudaSuccess;
+  dim3 block(32, 8);
+  k_bounded<<<span_grid(sp, block), block, 0, s>>>(a, b, pitch, sp);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// surface flux: driver.h90:3-17 (setup shift) and surface_flux.h90:3-48 (tile
+// physics, privatised temporaries kept in registers instead of DOM(nx,ny,ntlm)
+// device arrays — SURVEY §2.2 S5).
+// ============================================================================
+namespace {
+__global__ void __launch_bounds__(256) k_sf_setup(double* __restrict__ cf, Grid3 g, int ntlm,
+                                                  Span sp) {
+  const int64_t i = sp.ilo + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t j = sp.jlo + static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y;
+  if (i > sp.ihi || j > sp.jhi) return;
+  for (int lt = 0; lt < ntlm; ++lt) {
+    const int64_t idx = g.at(i - 1, j - 1, lt);
+    cf[idx] = cf[idx] - 0.5;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sf_tile(const double* __restrict__ cover,
+                                                 double* __restrict__ fx,
+                                                 double* __restrict__ fy,
+                                                 double* __restrict__ sw, int64_t W, Span sp) {
+  const int64_t i = sp.ilo + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t j = sp.jlo + static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y;
+  if (i > sp.ihi || j > sp.jhi) return;
+  const int64_t idx = (j - 1) * W + (i - 1);
+  const double cf = __ldg(cover + idx);
+  double taux, tauy, uf;
+  if (cf > 0.0) {
+    taux = 0.1 * cf;
+    tauy = 0.2 * cf * cf;
+    uf = sqrt(sqrt(taux * taux + tauy * tauy));
+  } else {
+    taux = 0.0;
+    tauy = 0.0;
+    uf = 0.0;
+  }
+  fx[idx] = taux;
+  fy[idx] = tauy;
+  sw[idx] = uf;
+}
+}  // namespace
+
+cudaError_t launch_sf_setup(double* cover_frac, Grid3 g, int64_t ntlm, const Span& sp,
+                            cudaStream_t s) {
+  if (span_empty(sp)) return cudaSuccess;
+  dim3 block(32, 8);
+  k_sf_setup<<<span_grid(sp, block), block, 0, s>>>(cover_frac, g, static_cast<int>(ntlm), sp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sf_tile(const double* cover_lt, double* flx_x, double* flx_y, double* swind,
+                           int64_t pitch, const Span& sp, cudaStream_t s) {
+  if (span_empty(sp)) return cudaSuccess;
+  dim3 block(32, 8);
+  k_sf_tile<<<span_grid(sp, block), block, 0, s>>>(cover_lt, flx_x, flx_y, swind, pitch, sp);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// reduction.h90:21-25 — deterministic fp64 sum: fixed block count, each block sums
+// a fixed contiguous range of (k, j) rows, warp-shuffle + smem tree inside the
+// block; a single block folds the partials in index order. Same bits every run;
+// within 1e-12 relative of the reference's sequential order.
+// ============================================================================
+namespace {
+constexpr int kRedBlocks = 148 * 8;
+constexpr int kRedThreads = 256;
+
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double warp_part[kRedThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) warp_part[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    r = lane < kRedThreads / 32 ? warp_part[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+  }
+  return r;  // valid in thread 0
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_sum_rows(const double* __restrict__ y, Grid3 g,
+                                                          int64_t nz, Span sp,
+                                                          double* __restrict__ partials) {
+  const int64_t ni = sp.ihi - sp.ilo + 1, nj = sp.jhi - sp.jlo + 1;
+  const int64_t rows = nz * nj;
+  const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
+  double acc = 0.0;
+  for (int64_t r = r0; r < r1; ++r) {
+    const int64_t k = r / nj, jj = r % nj;
+    const double* row = y + g.at(sp.ilo - 1, sp.jlo - 1 + jj, k);
+    for (int64_t ii = threadIdx.x; ii < ni; ii += kRedThreads) acc += __ldg(row + ii);
+  }
+  const double s = block_sum(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_sum_partials(const double* __restrict__ partials,
+                                                              int n, double total,
+                                                              double* __restrict__ result) {
+  double acc = 0.0;
+  for (int t = threadIdx.x; t < n; t += kRedThreads) acc += partials[t];
+  const double s = block_sum(acc);
+  if (threadIdx.x == 0) *result = total + s;
+}
+}  // namespace
+
+int64_t reduce_partials_needed() { return kRedBlocks; }
+
+cudaError_t launch_grid_sum(const double* y, Grid3 g, int64_t nz, const Span& sp,
+                            double* partials, double* result, double total, cudaStream_t s) {
+  if (span_empty(sp) || nz <= 0) {
+    k_sum_partials<<<1, kRedThreads, 0, s>>>(partials, 0, total, result);
+    return cudaGetLastError();
+  }
+  k_sum_rows<<<kRedBlocks, kRedThreads, 0, s>>>(y, g, nz, sp, partials);
+  k_sum_partials<<<1, kRedThreads, 0, s>>>(partials, kRedBlocks, total, result);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// apps/dycore/dycore.h90
+// ============================================================================
+DynConst make_dyn_const(double dt, double rdx, double rdy, double rdz, double cs2, double grav,
+                        double th0) {
+  DynConst c;
+  c.dt = dt;
+  c.rdx = rdx;
+  c.rdy = rdy;
+  c.rdz = rdz;
+  c.cs2 = cs2;
+  c.grav = grav;
+  c.th0 = th0;
+  c.dt_rdx = dt * rdx;                    // `dt * rdx * (...)`
+  c.dt_rdy = dt * rdy;
+  c.dt_rdz = dt * rdz;                    // `dt * rdz * (...) / rf`
+  c.dt_cs2 = dt * cs2;                    // `dt * cs2 * (...)`
+  c.dt_cs2_rdz = dt * cs2 * rdz;          // `dt * cs2 * rdz * (...)`
+  c.beta_num = dt * dt * cs2 * rdz * rdz; // `dt * dt * cs2 * rdz * rdz / rf`
+  c.dt_grav = dt * grav;                  // `dt * grav * (...) / th0`
+  return c;
+}
+
+namespace {
+__device__ __forceinline__ double minmod(double a, double b) {
+  // dycore.h90 `minmod`
+  if (a * b <= 0.0) return 0.0;
+  if (fabs(a) < fabs(b)) return a;
+  return b;
+}
+
+// Upwind limited flux through face f (between cells f and f+1) of a dimension with
+// n cells: walls at f = 0 and f = n (dycore.h90 regions 1-3).
+__device__ __forceinline__ double face_flux(int64_t f, int64_t n, double vel, double tm1,
+                                            double t0, double tp1, double tp2) {
+  if (f == 0 || f == n) return 0.0;
+  if (vel >= 0.0) {
+    const double s = (f == 1) ? 0.0 : minmod(t0 - tm1, tp1 - t0);
+    return vel * (t0 + 0.5 * s);
+  }
+  const double s = (f + 1 == n) ? 0.0 : minmod(tp1 - t0, tp2 - tp1);
+  return vel * (tp1 - 0.5 * s);
+}
+
+struct AdvArgs {
+  DynIn in;
+  double* __restrict__ thn;
+  Grid3 g;
+  int nz;
+  DynConst c;
+  Span sp;
+};
+
+// Regions 1-4 fused: the x/y/z face fluxes are recomputed per cell from theta
+// (each face is computed by both adjacent cells with identical inputs, so the bits
+// match the materialised fx/fy/fz of the reference), then the flux divergence with
+// the velocity-divergence correction. K-window of theta in registers.
+__global__ void __launch_bounds__(128) k_dyn_advect(AdvArgs a) {
+  const int64_t i = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t j = a.sp.jlo + static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y;
+  if (i > a.sp.ihi || j > a.sp.jhi) return;
+  const int64_t gi = i + a.sp.i0, gj = j + a.sp.j0, gnx = a.sp.gnx, gny = a.sp.gny;
+  const int64_t P = a.g.plane, W = a.g.pitch;
+  const int64_t col = (j - 1) * W + (i - 1);
+  const double* __restrict__ th = a.in.th + col;
+  const double* __restrict__ u = a.in.u + col;
+  const double* __restrict__ v = a.in.v + col;
+  const double* __restrict__ w = a.in.w + col;
+  double* __restrict__ thn = a.thn + col;
+  const int nz = a.nz;
+  const DynConst& c = a.c;
+
+  double tkm1 = 0.0;
+  double tk = __ldg(th);
+  double tkp1 = nz >= 2 ? __ldg(th + P) : 0.0;
+  double tkp2 = nz >= 3 ? __ldg(th + 2 * P) : 0.0;
+  double fzm = 0.0;   // fz(k-1), fz(0) = 0 (ground)
+  double wkm1 = 0.0;  // w(k-1)
+  for (int k = 1; k <= nz; ++k) {
+    const int64_t off = static_cast<int64_t>(k - 1) * P;
+    const double wk = __ldg(w + off);
+    const double fzk = face_flux(k, nz, wk, tkm1, tk, tkp1, tkp2);
+    const double* r = th + off;
+    const double xm2 = __ldg(r - 2), xm1 = __ldg(r - 1), xp1 = __ldg(r + 1), xp2 = __ldg(r + 2);
+    const double ym2 = __ldg(r - 2 * W), ym1 = __ldg(r - W), yp1 = __ldg(r + W),
+                 yp2 = __ldg(r + 2 * W);
+    const double ui = __ldg(u + off), uim1 = __ldg(u + off - 1);
+    const double vj = __ldg(v + off), vjm1 = __ldg(v + off - W);
+    const double fxe = face_flux(gi, gnx, ui, xm1, tk, xp1, xp2);
+    const double fxw = face_flux(gi - 1, gnx, uim1, xm2, xm1, tk, xp1);
+    const double fyn = face_flux(gj, gny, vj, ym1, tk, yp1, yp2);
+    const double fys = face_flux(gj - 1, gny, vjm1, ym2, ym1, tk, yp1);
+    const double ue = (gi == gnx) ? 0.0 : ui;
+    const double uw = (gi == 1) ? 0.0 : uim1;
+    const double vnf = (gj == gny) ? 0.0 : vj;
+    const double vs = (gj == 1) ? 0.0 : vjm1;
+    const double wt = (k == nz) ? 0.0 : wk;
+    const double wb = (k == 1) ? 0.0 : wkm1;
+    double flux = c.rdx * (fxe - fxw) + c.rdy * (fyn - fys);
+    flux = flux + c.rdz * (fzk - fzm);
+    double div = c.rdx * (ue - uw) + c.rdy * (vnf - vs);
+    div = div + c.rdz * (wt - wb);
+    thn[off] = tk - c.dt * (flux - tk * div);
+    fzm = fzk;
+    wkm1 = wk;
+    tkm1 = tk;
+    tk = tkp1;
+    tkp1 = tkp2;
+    tkp2 = (k + 3 <= nz) ? __ldg(th + static_cast<int64_t>(k + 2) * P) : 0.0;
+  }
+}
+
+struct AcoArgs {
+  DynIn in;
+  DynOut out;
+  Grid3 g;
+  int nz;
+  DynConst c;
+  Span sp;
+};
+
+// Regions 5-7 fused: horizontal pressure gradient (new u, v), the pressure after the
+// horizontal divergence (ps; the western/southern new velocities are recomputed from
+// p and u/v instead of being re-read), and the HE-VI Thomas sweep for w with the
+// pressure update. Per-thread Thomas coefficients cp/dp and ps stay on chip in
+// shared memory ([k][thread], conflict-free); one forward and one backward K sweep.
+__global__ void __launch_bounds__(64) k_dyn_acoustic(AcoArgs a) {
+  extern __shared__ double smem[];
+  const int T = blockDim.x * blockDim.y;
+  const int t = threadIdx.y * blockDim.x + threadIdx.x;
+  const int64_t i = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t j = a.sp.jlo + static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y;
+  if (i > a.sp.ihi || j > a.sp.jhi) return;
+  const int nz = a.nz;
+  double* cps = smem + t;
+  double* dps = smem + static_cast<int64_t>(nz) * T + t;
+  double* pss = smem + 2 * static_cast<int64_t>(nz) * T + t;
+  const int64_t gi = i + a.sp.i0, gj = j + a.sp.j0;
+  const bool east = gi == a.sp.gnx, west = gi == 1, north = gj == a.sp.gny, south = gj == 1;
+  const int64_t P = a.g.plane, W = a.g.pitch;
+  const int64_t col = (j - 1) * W + (i - 1);
+  const double* __restrict__ rho = a.in.rho + col;
+  const double* __restrict__ th = a.in.th + col;
+  const double* __restrict__ u = a.in.u + col;
+  const double* __restrict__ v = a.in.v + col;
+  const double* __restrict__ w = a.in.w + col;
+  const double* __restrict__ p = a.in.p + col;
+  double* __restrict__ un = a.out.u + col;
+  double* __restrict__ vn = a.out.v + col;
+  double* __restrict__ wn = a.out.w + col;
+  double* __restrict__ pn = a.out.p + col;
+  const DynConst& c = a.c;
+
+  double rho_prev = 0.0, th_prev = 0.0, ps_prev = 0.0, cp_prev = 0.0, dp_prev = 0.0;
+  for (int k = 1; k <= nz; ++k) {
+    const int64_t off = static_cast<int64_t>(k - 1) * P;
+    const double pk = __ldg(p + off);
+    const double pe = __ldg(p + off + 1), pw = __ldg(p + off - 1);
+    const double pnn = __ldg(p + off + W), psth = __ldg(p + off - W);
+    const double uk = __ldg(u + off), ukw = __ldg(u + off - 1);
+    const double vk = __ldg(v + off), vks = __ldg(v + off - W);
+    const double unk = east ? 0.0 : uk - c.dt_rdx * (pe - pk);
+    const double vnk = north ? 0.0 : vk - c.dt_rdy * (pnn - pk);
+    const double uw = west ? 0.0 : ukw - c.dt_rdx * (pk - pw);
+    const double vs = south ? 0.0 : vks - c.dt_rdy * (pk - psth);
+    const double psk = pk - c.dt_cs2 * (c.rdx * (unk - uw) + c.rdy * (vnk - vs));
+    un[off] = unk;
+    vn[off] = vnk;
+    pss[static_cast<int64_t>(k - 1) * T] = psk;
+    const double rhok = __ldg(rho + off), thk = __ldg(th + off);
+    if (k >= 2) {
+      const int kf = k - 1;  // face kf + 1/2 between levels kf and kf + 1
+      const double rf = 0.5 * (rho_prev + rhok);
+      const double beta = c.beta_num / rf;
+      double dd = __ldg(w + static_cast<int64_t>(kf - 1) * P) - c.dt_rdz * (psk - ps_prev) / rf;
+      dd = dd + c.dt_grav * (0.5 * (th_prev + thk) - c.th0) / c.th0;
+      const double bb = 1.0 + 2.0 * beta;
+      double cpk, dpk;
+      if (kf == 1) {
+        cpk = -beta / bb;
+        dpk = dd / bb;
+      } else {
+        const double m = bb + beta * cp_prev;
+        cpk = -beta / m;
+        dpk = (dd + beta * dp_prev) / m;
+      }
+      cps[static_cast<int64_t>(kf - 1) * T] = cpk;
+      dps[static_cast<int64_t>(kf - 1) * T] = dpk;
+      cp_prev = cpk;
+      dp_prev = dpk;
+    }
+    rho_prev = rhok;
+    th_prev = thk;
+    ps_prev = psk;
+  }
+  // backward sweep: w at faces nz-1 .. 1 (w(nz) = 0 is the lid), pressure update
+  wn[static_cast<int64_t>(nz - 1) * P] = 0.0;
+  double wk1 = 0.0;  // w(k+1)
+  for (int k = nz - 1; k >= 1; --k) {
+    const double dpk = dps[static_cast<int64_t>(k - 1) * T];
+    const double wk = (k == nz - 1) ? dpk : dpk - cps[static_cast<int64_t>(k - 1) * T] * wk1;
+    wn[static_cast<int64_t>(k - 1) * P] = wk;
+    pn[static_cast<int64_t>(k) * P] = pss[static_cast<int64_t>(k) * T] - c.dt_cs2_rdz * (wk1 - wk);
+    wk1 = wk;
+  }
+  pn[0] = pss[0] - c.dt_cs2_rdz * wk1;
+}
+}  // namespace
+
+cudaError_t launch_dycore_advect(const DynIn& in, double* thn, Grid3 g, int64_t nz,
+                                 const DynConst& c, const Span& sp, cudaStream_t s) {
+  if (span_empty(sp) || nz <= 0) return cudaSuccess;
+  dim3 block(32, 4);
+  AdvArgs a{in, thn, g, static_cast<int>(nz), c, sp};
+  k_dyn_advect<<<span_grid(sp, block), block, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dycore_acoustic(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
+                                   const DynConst& c, const Span& sp, cudaStream_t s) {
+  if (span_empty(sp) || nz < 2) return cudaSuccess;
+  dim3 block(32, 2);
+  size_t smem = 3 * static_cast<size_t>(nz) * block.x * block.y * sizeof(double);
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_dyn_acoustic,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  AcoArgs a{in, out, g, static_cast<int>(nz), c, sp};
+  k_dyn_acoustic<<<span_grid(sp, block), block, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// halo pack/unpack: box {ilo, ihi, jlo, jhi} (local 1-based) x all K levels
+// ============================================================================
+namespace {
+__global__ void __launch_bounds__(256) k_pack_box(const double* __restrict__ field,
+                                                  double* __restrict__ buf, Grid3 g,
+                                                  int64_t bi0, int64_t bj0, int64_t nbi,
+                                                  int64_t nbj, int64_t total) {
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t ii = t % nbi, rest = t / nbi, jj = rest % nbj, k = rest / nbj;
+    buf[t] = field[g.at(bi0 - 1 + ii, bj0 - 1 + jj, k)];
+  }
+}
+__global__ void __launch_bounds__(256) k_unpack_box(double* __restrict__ field,
+                                                    const double* __restrict__ buf, Grid3 g,
+                                                    int64_t bi0, int64_t bj0, int64_t nbi,
+                                                    int64_t nbj, int64_t total) {
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t ii = t % nbi, rest = t / nbi, jj = rest % nbj, k = rest / nbj;
+    field[g.at(bi0 - 1 + ii, bj0 - 1 + jj, k)] = buf[t];
+  }
+}
+}  // namespace
+
+cudaError_t launch_pack_box(const double* field, double* buf, Grid3 g, int64_t nk,
+                            const int64_t box[4], bool pack, cudaStream_t s) {
+  const int64_t nbi = box[1] - box[0] + 1, nbj = box[3] - box[2] + 1;
+  if (nbi <= 0 || nbj <= 0 || nk <= 0) return cudaSuccess;
+  const int64_t total = nbi * nbj * nk;
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  if (pack)
+    k_pack_box<<<blocks, 256, 0, s>>>(field, buf, g, box[0], box[2], nbi, nbj, total);
+  else
+    k_unpack_box<<<blocks, 256, 0, s>>>(const_cast<double*>(field), buf, g, box[0], box[2], nbi,
+                                        nbj, total);
+  return cudaGetLastError();
+}
+
+}  // namespace hfb

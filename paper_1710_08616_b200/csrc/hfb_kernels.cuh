@@ -1,0 +1,83 @@
+// hfb_kernels.cuh — launchers of the sm_100a kernels (internal C++ interface).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hfb_layout.cuh"
+
+namespace hfb {
+
+// Tile of a launch in 1-based LOCAL coordinates plus the tile's global placement,
+// so boundary predicates always test GLOBAL indices (diffusion.h90:25 tests i == nx
+// on the global domain).
+struct Span {
+  int64_t ilo, ihi, jlo, jhi;   // inclusive, local 1-based
+  int64_t i0 = 0, j0 = 0;       // global offset (global i = local i + i0)
+  int64_t gnx = 0, gny = 0;     // global extents
+};
+
+// ---- relayout: caller's host order <-> device layout -------------------------
+// ext/hs per role (I, J, K, L): extents and host strides in elements; the device side
+// uses the Layout strides. `fast` is the role with host stride 1.
+struct Relayout {
+  int64_t ext[4];
+  int64_t hs[4];
+  int64_t ds[4];
+  int fast;
+};
+cudaError_t launch_relayout(const double* src, double* dst, const Relayout& r, bool to_device,
+                            cudaStream_t s);
+
+// ---- diffusion.h90 (hfk0 + hfk1 fused: write the step result to one or two outputs)
+cudaError_t launch_diffusion(const double* t_old, double* out1, double* out2, Grid3 g,
+                             int64_t nz, double coef, const Span& sp, cudaStream_t s);
+// hfk1_diffuse_step alone (t_old = t_new over the span)
+cudaError_t launch_copy_columns(const double* src, double* dst, Grid3 g, int64_t nz,
+                                const Span& sp, cudaStream_t s);
+
+// ---- damping.h90 ---------------------------------------------------------------
+cudaError_t launch_damping(const double* ref, const double* bnd1, const double* bnd2,
+                           double* damp, Grid3 g, int64_t nk, double mtratio, double tratio,
+                           const Span& sp, cudaStream_t s);
+
+// ---- bounded.h90 -----------------------------------------------------------------
+cudaError_t launch_bounded(const double* a, double* b, int64_t pitch, const Span& sp,
+                           cudaStream_t s);
+
+// ---- surface flux (driver.h90 setup, surface_flux.h90 tile physics) ----------------
+cudaError_t launch_sf_setup(double* cover_frac, Grid3 g, int64_t ntlm, const Span& sp,
+                            cudaStream_t s);
+cudaError_t launch_sf_tile(const double* cover_lt, double* flx_x, double* flx_y, double* swind,
+                           int64_t pitch, const Span& sp, cudaStream_t s);
+
+// ---- reduction.h90: deterministic two-level fp64 sum ------------------------------
+// partials must hold >= reduce_partials_needed() doubles; result = total + sum.
+int64_t reduce_partials_needed();
+cudaError_t launch_grid_sum(const double* y, Grid3 g, int64_t nz, const Span& sp,
+                            double* partials, double* result, double total, cudaStream_t s);
+
+// ---- apps/dycore/dycore.h90 --------------------------------------------------------
+struct DynConst {
+  double dt, rdx, rdy, rdz, cs2, grav, th0;
+  // products formed exactly as the reference evaluates them (left-associative)
+  double dt_rdx, dt_rdy, dt_rdz, dt_cs2, dt_cs2_rdz, beta_num, dt_grav;
+};
+DynConst make_dyn_const(double dt, double rdx, double rdy, double rdz, double cs2, double grav,
+                        double th0);
+struct DynIn {
+  const double *rho, *th, *u, *v, *w, *p;
+};
+struct DynOut {
+  double *th, *u, *v, *w, *p;
+};
+cudaError_t launch_dycore_advect(const DynIn& in, double* thn, Grid3 g, int64_t nz,
+                                 const DynConst& c, const Span& sp, cudaStream_t s);
+cudaError_t launch_dycore_acoustic(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
+                                   const DynConst& c, const Span& sp, cudaStream_t s);
+
+// ---- halo pack/unpack for the 2-D decomposition -------------------------------------
+cudaError_t launch_pack_box(const double* field, double* buf, Grid3 g, int64_t nk,
+                            const int64_t box[4], bool pack, cudaStream_t s);
+
+}  // namespace hfb

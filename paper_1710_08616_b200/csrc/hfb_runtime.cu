@@ -1,0 +1,1444 @@
+// hfb_runtime.cu — host runtime behind include/hfb.h.
+//
+// Plays the part of the reference's executor for GPU programs
+// (/root/reference/proj/src/interp.cpp: Executor::exec_transfer :1369-1415,
+// exec_launch :1417-1475, slot_side residency :397-411) but runs native sm_100a
+// kernels instead of interpreting the generated CUDA-Fortran: a context holds the
+// MachineState-equivalent (module scalars + caller-owned host buffers), the device
+// copies in the I-fastest layout (hfb_layout.cuh), the residency state machine, and
+// the app programs, whose entries follow the generated host code
+// (transfers at `transferHere` routines, codegen.cpp:570-600; kernel launches per
+// @parallelRegion, codegen.cpp:397-449).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cctype>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hfb.h"
+#include "hfb_kernels.cuh"
+#include "hfb_layout.cuh"
+
+using namespace hfb;
+
+namespace {
+
+thread_local std::string g_last_error = "";
+
+// An hft::Error analogue: kind (status) + message.
+struct Fail {
+  hfb_status code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(hfb_status code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  throw Fail{code, buf};
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(HFB_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+std::string lower(const char* s) {
+  std::string r = s ? s : "";
+  for (char& c : r) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+  return r;
+}
+
+template <class F>
+hfb_status guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return HFB_OK;
+  } catch (const Fail& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return HFB_RUNTIME;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Program description: the built-in apps' modules (declarations as in the .h90)
+// ---------------------------------------------------------------------------
+enum class SType { Int, Real };
+
+struct ScalarDecl {
+  std::string name;
+  SType type;
+  bool is_param = false;
+  double param = 0.0;
+};
+
+struct ArrayDecl {
+  std::string name;
+  std::vector<std::pair<std::string, std::string>> dims;  // (lower expr, upper expr)
+  std::vector<Role> roles;
+  bool pingpong = false;  // state array the timestep rewrites in full (double-buffered)
+};
+
+struct AppDecl {
+  std::string app, module;
+  std::vector<ScalarDecl> scalars;
+  std::vector<ArrayDecl> arrays;
+};
+
+std::vector<std::pair<std::string, std::string>> dims3(const char* a, const char* b,
+                                                       const char* c) {
+  return {{"1", a}, {"1", b}, {"1", c}};
+}
+
+const std::vector<AppDecl>& app_table() {
+  static const std::vector<AppDecl> apps = [] {
+    std::vector<AppDecl> v;
+    const std::vector<Role> KIJ = {kRoleK, kRoleI, kRoleJ};
+    const std::vector<Role> IJ = {kRoleI, kRoleJ};
+    // diffusion.h90:1-10
+    v.push_back({"diffusion",
+                 "diff_state",
+                 {{"nx", SType::Int}, {"ny", SType::Int}, {"nz", SType::Int},
+                  {"nsteps", SType::Int}, {"coef", SType::Real}},
+                 {{"t_old", dims3("nz", "nx", "ny"), KIJ, true},
+                  {"t_new", dims3("nz", "nx", "ny"), KIJ, false}}});
+    // damping.h90:1-14
+    {
+      std::vector<std::pair<std::string, std::string>> d3 = {
+          {"nz_mn", "nz_mx"}, {"nx_mn", "nx_mx"}, {"ny_mn", "ny_mx"}};
+      auto d4 = d3;
+      d4.push_back({"1", "2"});
+      v.push_back({"damping",
+                   "svar",
+                   {{"nx_mn", SType::Int}, {"nx_mx", SType::Int}, {"ny_mn", SType::Int},
+                    {"ny_mx", SType::Int}, {"nz_mn", SType::Int}, {"nz_mx", SType::Int},
+                    {"tratio_bnd", SType::Real}, {"mtratio_bnd", SType::Real}},
+                   {{"dens_ref_f", d3, KIJ},
+                    {"dens_ptb_damp", d3, KIJ},
+                    {"dens_ptb_bnd", d4, {kRoleK, kRoleI, kRoleJ, kRoleL}}}});
+    }
+    // bounded.h90:1-7
+    v.push_back({"bounded",
+                 "b_state",
+                 {{"nx", SType::Int}, {"ny", SType::Int}},
+                 {{"a", {{"1", "nx"}, {"1", "ny"}}, IJ}, {"b", {{"1", "nx"}, {"1", "ny"}}, IJ}}});
+    // sf_state.h90:1-11 (cover_frac's tile dim rides the K role)
+    v.push_back({"surface_flux",
+                 "sf_state",
+                 {{"ntlm", SType::Int, true, 4.0},
+                  {"nx", SType::Int},
+                  {"ny", SType::Int},
+                  {"tile_land", SType::Int}},
+                 {{"cover_frac", dims3("ntlm", "nx", "ny"), KIJ},
+                  {"wind_speed", {{"1", "nx"}, {"1", "ny"}}, IJ},
+                  {"flx_sum_x", {{"1", "nx"}, {"1", "ny"}}, IJ},
+                  {"flx_sum_y", {{"1", "nx"}, {"1", "ny"}}, IJ}}});
+    // reduction.h90:1-8
+    v.push_back({"reduction",
+                 "red_state",
+                 {{"nx", SType::Int}, {"ny", SType::Int}, {"nz", SType::Int},
+                  {"total", SType::Real}},
+                 {{"y", dims3("nz", "nx", "ny"), KIJ}}});
+    // apps/dycore/dyn_state.h90
+    v.push_back({"dycore",
+                 "dyn_state",
+                 {{"nx", SType::Int}, {"ny", SType::Int}, {"nz", SType::Int},
+                  {"nsteps", SType::Int}, {"dt", SType::Real}, {"rdx", SType::Real},
+                  {"rdy", SType::Real}, {"rdz", SType::Real}, {"cs2", SType::Real},
+                  {"grav", SType::Real}, {"th0", SType::Real}},
+                 {{"rho", dims3("nz", "nx", "ny"), KIJ, false},
+                  {"th", dims3("nz", "nx", "ny"), KIJ, true},
+                  {"u", dims3("nz", "nx", "ny"), KIJ, true},
+                  {"v", dims3("nz", "nx", "ny"), KIJ, true},
+                  {"w", dims3("nz", "nx", "ny"), KIJ, true},
+                  {"p", dims3("nz", "nx", "ny"), KIJ, true}}});
+    return v;
+  }();
+  return apps;
+}
+
+// ---------------------------------------------------------------------------
+// State
+// ---------------------------------------------------------------------------
+enum Residency { kHost = 0, kDevice = 1, kBoth = 2 };  // interp.hpp:30
+
+struct Scalar {
+  SType type;
+  int64_t i = 0;
+  double r = 0.0;
+  bool init = false;
+};
+
+struct Slot {
+  std::string module, name;
+  const ArrayDecl* decl = nullptr;
+  // host side (caller-owned)
+  double* host = nullptr;
+  int rank = 0;
+  int64_t lower[4] = {1, 1, 1, 1}, upper[4] = {1, 1, 1, 1}, hstride[4] = {0, 0, 0, 0};
+  int64_t count = 0;
+  bool pinned = false;
+  // device side
+  Layout lay;
+  double* dev[2] = {nullptr, nullptr};
+  int cur = 0;
+  bool has_device = false;
+  Residency res = kHost;
+  cudaStream_t stream = nullptr;  // owning context's stream
+
+  double* d() const { return dev[cur] + lay.origin_off; }
+  double* d_alt() const { return dev[1 - cur] + lay.origin_off; }
+};
+
+}  // namespace
+
+struct hfb_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  const AppDecl* app = nullptr;
+  std::map<std::string, Scalar> scalars;  // key: name (single module per app)
+  std::map<std::string, Slot> slots;
+  double* staging = nullptr;
+  size_t staging_bytes = 0;
+  double* red_partials = nullptr;
+  double* red_result = nullptr;
+  double* red_host = nullptr;
+  hfb_decomp decomp{};
+  bool decomposed = false;
+  int64_t halo_bytes = 0;
+  // NCCL (multi-process decomposition)
+  void* nccl_comm = nullptr;
+  double* halo_send = nullptr;
+  double* halo_recv = nullptr;
+  size_t halo_cap = 0;
+  // CUDA graph cache for hfb_run_graph
+  cudaGraphExec_t graph_exec = nullptr;
+  std::string graph_key;
+  hfb_launch_stats graph_stats{};
+  // per-kernel CUDA-event timing (hfb_profile)
+  bool prof = false;
+  bool capturing = false;
+  struct Timed {
+    std::string name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Timed> pending;
+  std::vector<cudaEvent_t> free_events;
+  std::map<std::string, std::pair<double, int64_t>> kernel_ms;  // name -> (ms, launches)
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// small helpers on the context
+// ---------------------------------------------------------------------------
+Scalar& scalar_ref(hfb_ctx* c, const std::string& module, const std::string& name) {
+  if (!c->app) fail(HFB_CONFIG, "no program loaded (hfb_load_program)");
+  if (module != c->app->module)
+    fail(HFB_CONFIG, "unknown module '%s' (program '%s' has module '%s')", module.c_str(),
+         c->app->app.c_str(), c->app->module.c_str());
+  auto it = c->scalars.find(name);
+  if (it == c->scalars.end())
+    fail(HFB_CONFIG, "'%s' is not a scalar of module '%s'", name.c_str(), module.c_str());
+  return it->second;
+}
+
+int64_t ival(hfb_ctx* c, const char* name) {
+  auto it = c->scalars.find(name);
+  if (it == c->scalars.end() || !it->second.init)
+    fail(HFB_RUNTIME, "read of unset variable '%s'", name);  // interp.cpp:549
+  return it->second.type == SType::Int ? it->second.i : static_cast<int64_t>(it->second.r);
+}
+
+double rval(hfb_ctx* c, const char* name) {
+  auto it = c->scalars.find(name);
+  if (it == c->scalars.end() || !it->second.init)
+    fail(HFB_RUNTIME, "read of unset variable '%s'", name);
+  return it->second.type == SType::Real ? it->second.r : static_cast<double>(it->second.i);
+}
+
+int64_t eval_dim(hfb_ctx* c, const std::string& e) {
+  if (!e.empty() && (std::isdigit(static_cast<unsigned char>(e[0])) || e[0] == '-'))
+    return std::stoll(e);
+  return ival(c, e.c_str());
+}
+
+Slot& slot_ref(hfb_ctx* c, const std::string& module, const std::string& name) {
+  if (!c->app) fail(HFB_CONFIG, "no program loaded (hfb_load_program)");
+  if (module != c->app->module)
+    fail(HFB_CONFIG, "unknown module '%s'", module.c_str());
+  auto it = c->slots.find(name);
+  if (it == c->slots.end())
+    fail(HFB_CONFIG, "'%s' is not an array of module '%s'", name.c_str(), module.c_str());
+  return it->second;
+}
+
+Slot& slot(hfb_ctx* c, const char* name) { return slot_ref(c, c->app->module, name); }
+
+// declared bounds vs the bound buffer
+void check_bounds(hfb_ctx* c, Slot& s) {
+  if (!s.host) fail(HFB_CONFIG, "array '%s' of module '%s' is not bound", s.name.c_str(),
+                    s.module.c_str());
+  for (size_t d = 0; d < s.decl->dims.size(); ++d) {
+    int64_t lo = eval_dim(c, s.decl->dims[d].first), hi = eval_dim(c, s.decl->dims[d].second);
+    if (lo != s.lower[d] || hi != s.upper[d])
+      fail(HFB_RUNTIME,
+           "array '%s' is bound with bounds [%lld:%lld] in dimension %zu but declared "
+           "[%lld:%lld]",
+           s.name.c_str(), (long long)s.lower[d], (long long)s.upper[d], d + 1, (long long)lo,
+           (long long)hi);
+  }
+}
+
+void role_extents(const Slot& s, int64_t ext[4], int64_t hs[4]) {
+  for (int r = 0; r < 4; ++r) {
+    ext[r] = 1;
+    hs[r] = 0;
+  }
+  for (int d = 0; d < s.rank; ++d) {
+    Role r = s.decl->roles[d];
+    ext[r] = s.upper[d] - s.lower[d] + 1;
+    hs[r] = s.hstride[d];
+  }
+}
+
+void ensure_device(hfb_ctx* c, Slot& s, bool second) {
+  if (!s.dev[0]) {
+    int64_t ext[4], hs[4];
+    role_extents(s, ext, hs);
+    s.lay = Layout::make(ext[kRoleI], ext[kRoleJ], ext[kRoleK], ext[kRoleL]);
+  }
+  for (int b = 0; b < (second ? 2 : 1); ++b) {
+    if (s.dev[b]) continue;
+    size_t bytes = static_cast<size_t>(s.lay.alloc_elems) * sizeof(double);
+    cuda_check(cudaMalloc(&s.dev[b], bytes), "cudaMalloc(device array)");
+    cuda_check(cudaMemsetAsync(s.dev[b], 0, bytes, c->stream), "cudaMemsetAsync");
+  }
+}
+
+void ensure_staging(hfb_ctx* c, size_t bytes) {
+  if (c->staging_bytes >= bytes) return;
+  if (c->staging) cudaFree(c->staging);
+  c->staging = nullptr;
+  cuda_check(cudaMalloc(&c->staging, bytes), "cudaMalloc(staging)");
+  c->staging_bytes = bytes;
+}
+
+Relayout relayout_of(const Slot& s) {
+  Relayout r{};
+  role_extents(s, r.ext, r.hs);
+  r.ds[kRoleI] = 1;
+  r.ds[kRoleJ] = s.lay.pitch;
+  r.ds[kRoleK] = s.lay.plane;
+  r.ds[kRoleL] = s.lay.volume;
+  r.fast = kRoleI;
+  for (int role = 0; role < 4; ++role)
+    if (r.hs[role] == 1 && r.ext[role] > 1) r.fast = role;
+  if (r.hs[kRoleI] == 1 || r.ext[kRoleI] == 1) {
+    // keep I as the copy axis when it is host-contiguous (or trivially so)
+    if (r.hs[kRoleI] == 1) r.fast = kRoleI;
+  }
+  if (r.fast != kRoleI && r.ext[r.fast] <= 1) r.fast = kRoleI;
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// transfers (interp.cpp:1369-1415)
+// ---------------------------------------------------------------------------
+void do_device_allocate(hfb_ctx* c, Slot& s) {
+  check_bounds(c, s);
+  if (!s.has_device) {
+    ensure_device(c, s, false);
+    s.has_device = true;  // init flags cleared: contents undefined until written
+  }
+}
+
+void do_copy_to_device(hfb_ctx* c, Slot& s) {
+  check_bounds(c, s);
+  if (s.res == kDevice)
+    fail(HFB_RESIDENCY, "copy-in of '%s' would overwrite newer device data", s.name.c_str());
+  ensure_device(c, s, false);
+  size_t bytes = static_cast<size_t>(s.count) * sizeof(double);
+  ensure_staging(c, bytes);
+  cuda_check(cudaMemcpyAsync(c->staging, s.host, bytes, cudaMemcpyHostToDevice, c->stream),
+             "cudaMemcpyAsync(H2D)");
+  cuda_check(launch_relayout(c->staging, s.d(), relayout_of(s), true, c->stream),
+             "relayout(H2D)");
+  s.has_device = true;
+  s.res = kBoth;
+}
+
+void do_copy_from_device(hfb_ctx* c, Slot& s) {
+  if (!s.has_device)
+    fail(HFB_RESIDENCY, "copy-out of '%s', which was never transferred to the device",
+         s.name.c_str());
+  if (s.res == kHost)
+    fail(HFB_RESIDENCY, "copy-out of '%s' would overwrite newer host data", s.name.c_str());
+  size_t bytes = static_cast<size_t>(s.count) * sizeof(double);
+  ensure_staging(c, bytes);
+  cuda_check(launch_relayout(s.d(), c->staging, relayout_of(s), false, c->stream),
+             "relayout(D2H)");
+  cuda_check(cudaMemcpyAsync(s.host, c->staging, bytes, cudaMemcpyDeviceToHost, c->stream),
+             "cudaMemcpyAsync(D2H)");
+  cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  s.res = kBoth;
+}
+
+// device-code access checks (slot_side, interp.cpp:397-411)
+void dev_read(hfb_ctx* c, const char* name) {
+  Slot& s = slot(c, name);
+  if (!s.has_device)
+    fail(HFB_RESIDENCY, "array '%s' has no device copy (missing transfer)", name);
+  if (s.res == kHost)
+    fail(HFB_RESIDENCY, "device copy of '%s' is stale (host copy was modified)", name);
+}
+void dev_write(hfb_ctx* c, const char* name) {
+  Slot& s = slot(c, name);
+  if (!s.has_device)
+    fail(HFB_RESIDENCY, "array '%s' has no device copy (missing transfer)", name);
+}
+void dev_written(hfb_ctx* c, const char* name) { slot(c, name).res = kDevice; }
+
+// ---------------------------------------------------------------------------
+// launch contract accounting (codegen.cpp:421-434; interp.cpp:1417-1475)
+// ---------------------------------------------------------------------------
+struct Stats {
+  int64_t launches = 0, threads = 0, guard_returns = 0, native = 0;
+};
+
+// one generated launch over a region with extents ex x ey and block bx x by
+void count_launch(Stats& st, int64_t ex, int64_t ey, int64_t bx = 32, int64_t by = 4) {
+  // cugridSize = ceiling(real(extent) / real(B)); non-positive grids are rejected
+  auto ceil_div = [](int64_t e, int64_t b) -> int64_t {
+    double q = static_cast<double>(e) / static_cast<double>(b);
+    return static_cast<int64_t>(std::ceil(q));
+  };
+  int64_t gx = ceil_div(ex, bx), gy = ceil_div(ey, by);
+  if (gx < 1 || gy < 1)
+    fail(HFB_RUNTIME, "launch configuration dimensions must be positive");  // interp.cpp:1425
+  int64_t total = gx * bx * gy * by;
+  st.launches += 1;
+  st.threads += total;
+  st.guard_returns += total - ex * ey;
+}
+
+Span full_span(hfb_ctx* c, int64_t ni, int64_t nj) {
+  Span sp;
+  sp.ilo = 1;
+  sp.ihi = ni;
+  sp.jlo = 1;
+  sp.jhi = nj;
+  if (c->decomposed) {
+    sp.i0 = c->decomp.i0;
+    sp.j0 = c->decomp.j0;
+    sp.gnx = c->decomp.global_nx;
+    sp.gny = c->decomp.global_ny;
+  } else {
+    sp.gnx = ni;
+    sp.gny = nj;
+  }
+  return sp;
+}
+
+Grid3 grid_of(const Slot& s) { return Grid3{s.lay.pitch, s.lay.plane}; }
+
+cudaEvent_t take_event(hfb_ctx* c) {
+  if (!c->free_events.empty()) {
+    cudaEvent_t e = c->free_events.back();
+    c->free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+  return e;
+}
+
+// Launch one native kernel (or a fixed group of `n`), with optional CUDA-event timing
+// on the context stream (never during graph capture).
+template <class F>
+void launch(hfb_ctx* c, Stats& st, const char* name, F&& f, int n = 1) {
+  const bool timed = c->prof && !c->capturing;
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (timed) {
+    a = take_event(c);
+    cuda_check(cudaEventRecord(a, c->stream), "cudaEventRecord");
+  }
+  cuda_check(f(), name);
+  if (timed) {
+    b = take_event(c);
+    cuda_check(cudaEventRecord(b, c->stream), "cudaEventRecord");
+    c->pending.push_back({name, a, b});
+  }
+  st.native += n;
+}
+
+void resolve_timings(hfb_ctx* c) {
+  for (auto& t : c->pending) {
+    cuda_check(cudaEventSynchronize(t.b), "cudaEventSynchronize");
+    float ms = 0.f;
+    cuda_check(cudaEventElapsedTime(&ms, t.a, t.b), "cudaEventElapsedTime");
+    auto& acc = c->kernel_ms[t.name];
+    acc.first += ms;
+    acc.second += 1;
+    c->free_events.push_back(t.a);
+    c->free_events.push_back(t.b);
+  }
+  c->pending.clear();
+}
+
+void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width);
+
+// ---------------------------------------------------------------------------
+// app: diffusion (diffusion.h90)
+// ---------------------------------------------------------------------------
+void diffusion_step(hfb_ctx* c, Stats& st, bool write_t_new) {
+  int64_t nx = ival(c, "nx"), ny = ival(c, "ny"), nz = ival(c, "nz");
+  double coef = rval(c, "coef");
+  dev_read(c, "t_old");
+  dev_write(c, "t_new");
+  Slot& to = slot(c, "t_old");
+  Slot& tn = slot(c, "t_new");
+  ensure_device(c, to, true);
+  halo_exchange(c, {"t_old"}, 1);
+  Span sp = full_span(c, nx, ny);
+  // hfk0 (stencil into the alternate t_old buffer [+ t_new]) then hfk1 fused away
+  launch(c, st, "hfk0_diffuse_step", [&] { return launch_diffusion(to.d(), to.d_alt(), write_t_new ? tn.d() : nullptr, grid_of(to), nz,
+                            coef, sp, c->stream); });
+  to.cur = 1 - to.cur;
+  count_launch(st, nx, ny);
+  count_launch(st, nx, ny);
+  dev_written(c, "t_new");
+  dev_written(c, "t_old");
+}
+
+void diffusion_entry(hfb_ctx* c, const std::string& r, Stats& st) {
+  if (r == "main" || r == "simulation_run") {
+    int64_t nsteps = ival(c, "nsteps");
+    for (const char* n : {"t_new", "t_old"}) do_copy_to_device(c, slot(c, n));
+    for (int64_t s = 0; s < nsteps; ++s) diffusion_step(c, st, s == nsteps - 1);
+    for (const char* n : {"t_new", "t_old"}) do_copy_from_device(c, slot(c, n));
+  } else if (r == "diffuse_step") {
+    diffusion_step(c, st, true);
+  } else {
+    fail(HFB_CONFIG, "program 'diffusion' has no entry '%s'", r.c_str());
+  }
+}
+
+// ---------------------------------------------------------------------------
+// app: damping (damping.h90)
+// ---------------------------------------------------------------------------
+void damping_kernel(hfb_ctx* c, Stats& st) {
+  int64_t nx = ival(c, "nx_mx") - ival(c, "nx_mn") + 1;
+  int64_t ny = ival(c, "ny_mx") - ival(c, "ny_mn") + 1;
+  int64_t nz = ival(c, "nz_mx") - ival(c, "nz_mn") + 1;
+  double t = rval(c, "tratio_bnd"), m = rval(c, "mtratio_bnd");
+  count_launch(st, nx, ny);
+  dev_read(c, "dens_ref_f");
+  dev_read(c, "dens_ptb_bnd");
+  dev_write(c, "dens_ptb_damp");
+  Slot& ref = slot(c, "dens_ref_f");
+  Slot& bnd = slot(c, "dens_ptb_bnd");
+  Slot& dmp = slot(c, "dens_ptb_damp");
+  Span sp = full_span(c, nx, ny);
+  launch(c, st, "hfk0_lateral_and_upper_damping", [&] { return launch_damping(ref.d(), bnd.d(), bnd.d() + bnd.lay.volume, dmp.d(), grid_of(ref), nz,
+                          m, t, sp, c->stream); });
+  dev_written(c, "dens_ptb_damp");
+}
+
+void damping_entry(hfb_ctx* c, const std::string& r, Stats& st) {
+  const char* names[] = {"dens_ptb_bnd", "dens_ptb_damp", "dens_ref_f"};
+  if (r == "main") {
+    for (const char* n : names) do_copy_to_device(c, slot(c, n));
+    damping_kernel(c, st);
+    for (const char* n : names) do_copy_from_device(c, slot(c, n));
+  } else if (r == "lateral_and_upper_damping") {
+    damping_kernel(c, st);
+  } else {
+    fail(HFB_CONFIG, "program 'damping' has no entry '%s'", r.c_str());
+  }
+}
+
+// ---------------------------------------------------------------------------
+// app: bounded (bounded.h90)
+// ---------------------------------------------------------------------------
+void bounded_kernel(hfb_ctx* c, Stats& st) {
+  int64_t nx = ival(c, "nx"), ny = ival(c, "ny");
+  count_launch(st, (nx - 1) - 2 + 1, (ny - 1) - 2 + 1);
+  dev_read(c, "a");
+  dev_write(c, "b");
+  Slot& a = slot(c, "a");
+  Slot& b = slot(c, "b");
+  halo_exchange(c, {"a"}, 1);
+  Span sp = full_span(c, nx, ny);
+  // startAt(2,2), endAt(nx-1, ny-1) on the GLOBAL domain
+  sp.ilo = std::max<int64_t>(1, 2 - sp.i0);
+  sp.ihi = std::min<int64_t>(nx, sp.gnx - 1 - sp.i0);
+  sp.jlo = std::max<int64_t>(1, 2 - sp.j0);
+  sp.jhi = std::min<int64_t>(ny, sp.gny - 1 - sp.j0);
+  launch(c, st, "hfk0_interior_update", [&] { return launch_bounded(a.d(), b.d(), a.lay.pitch, sp, c->stream); });
+  dev_written(c, "b");
+}
+
+void bounded_entry(hfb_ctx* c, const std::string& r, Stats& st) {
+  if (r == "main" || r == "simulation_run") {
+    for (const char* n : {"a", "b"}) do_copy_to_device(c, slot(c, n));
+    bounded_kernel(c, st);
+    for (const char* n : {"a", "b"}) do_copy_from_device(c, slot(c, n));
+  } else if (r == "interior_update") {
+    bounded_kernel(c, st);
+  } else {
+    fail(HFB_CONFIG, "program 'bounded' has no entry '%s'", r.c_str());
+  }
+}
+
+// ---------------------------------------------------------------------------
+// app: surface_flux (sf_state.h90, surface_flux.h90, driver.h90)
+// ---------------------------------------------------------------------------
+void sf_tile_kernel(hfb_ctx* c, Stats& st) {
+  int64_t nx = ival(c, "nx"), ny = ival(c, "ny"), lt = ival(c, "tile_land");
+  int64_t ntlm = ival(c, "ntlm");
+  count_launch(st, nx, ny);
+  dev_read(c, "cover_frac");
+  for (const char* n : {"flx_sum_x", "flx_sum_y", "wind_speed"}) dev_write(c, n);
+  if (lt < 1 || lt > ntlm)
+    fail(HFB_RUNTIME, "index %lld out of bounds [1, %lld] in dimension 1 of 'cover_frac'",
+         (long long)lt, (long long)ntlm);
+  Slot& cf = slot(c, "cover_frac");
+  Span sp = full_span(c, nx, ny);
+  launch(c, st, "hfk0_sf_slab_flx_tile_run", [&] { return launch_sf_tile(cf.d() + (lt - 1) * cf.lay.plane, slot(c, "flx_sum_x").d(),
+                          slot(c, "flx_sum_y").d(), slot(c, "wind_speed").d(), cf.lay.pitch, sp,
+                          c->stream); });
+  for (const char* n : {"flx_sum_x", "flx_sum_y", "wind_speed"}) dev_written(c, n);
+}
+
+void sf_entry(hfb_ctx* c, const std::string& r, Stats& st) {
+  const char* names[] = {"cover_frac", "flx_sum_x", "flx_sum_y", "wind_speed"};
+  if (r == "main" || r == "simulation_run") {
+    for (const char* n : names) do_copy_to_device(c, slot(c, n));
+    if (r == "main") {
+      // driver.h90 setup(): the host-side coverage shift, executed on the device copy
+      // right after it arrives (same final state; no host compute on the product path)
+      Slot& cf = slot(c, "cover_frac");
+      int64_t nx = ival(c, "nx"), ny = ival(c, "ny");
+      launch(c, st, "sf_setup", [&] { return launch_sf_setup(cf.d(), grid_of(cf), ival(c, "ntlm"), full_span(c, nx, ny),
+                               c->stream); });
+    }
+    sf_tile_kernel(c, st);
+    for (const char* n : names) do_copy_from_device(c, slot(c, n));
+  } else if (r == "physics_run" || r == "sf_slab_flx_tile_run" || r == "physics_main") {
+    sf_tile_kernel(c, st);
+  } else {
+    fail(HFB_CONFIG, "program 'surface_flux' has no device entry '%s'", r.c_str());
+  }
+}
+
+// ---------------------------------------------------------------------------
+// app: reduction (reduction.h90) — OpenACC-style reduction kernel
+// ---------------------------------------------------------------------------
+void allreduce_sum(hfb_ctx* c, double* dev_value);
+
+void reduction_kernel(hfb_ctx* c, Stats& st) {
+  int64_t nx = ival(c, "nx"), ny = ival(c, "ny"), nz = ival(c, "nz");
+  double total = rval(c, "total");
+  dev_read(c, "y");
+  Slot& y = slot(c, "y");
+  if (!c->red_partials) {
+    cuda_check(cudaMalloc(&c->red_partials, sizeof(double) * (reduce_partials_needed() + 2)),
+               "cudaMalloc(partials)");
+    c->red_result = c->red_partials + reduce_partials_needed();
+    cuda_check(cudaMallocHost(&c->red_host, sizeof(double)), "cudaMallocHost");
+  }
+  Span sp = full_span(c, nx, ny);
+  bool multi = c->decomposed && c->decomp.px * c->decomp.py > 1;
+  launch(c, st, "grid_total", [&] { return launch_grid_sum(y.d(), grid_of(y), nz, sp, c->red_partials, c->red_result,
+                           multi ? 0.0 : total, c->stream); }, 2);
+  if (multi) allreduce_sum(c, c->red_result);
+  cuda_check(cudaMemcpyAsync(c->red_host, c->red_result, sizeof(double), cudaMemcpyDeviceToHost,
+                             c->stream),
+             "cudaMemcpyAsync(total)");
+  cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  Scalar& tot = c->scalars["total"];
+  tot.r = multi ? total + *c->red_host : *c->red_host;
+  tot.init = true;
+  // acc kernels: one virtual launch over the (j, i) iteration space (interp.cpp:1080-1114)
+  st.launches += 1;
+  st.threads += nx * ny;
+}
+
+void reduction_entry(hfb_ctx* c, const std::string& r, Stats& st) {
+  if (r == "main" || r == "simulation_run") {
+    do_copy_to_device(c, slot(c, "y"));
+    Scalar& tot = c->scalars["total"];
+    tot.r = 0.0;  // reduction.h90:34 `total = 0.0_r_size`
+    tot.init = true;
+    reduction_kernel(c, st);
+    do_copy_from_device(c, slot(c, "y"));
+  } else if (r == "grid_total") {
+    reduction_kernel(c, st);
+  } else {
+    fail(HFB_CONFIG, "program 'reduction' has no entry '%s'", r.c_str());
+  }
+}
+
+// ---------------------------------------------------------------------------
+// app: dycore (apps/dycore/dycore.h90)
+// ---------------------------------------------------------------------------
+void dycore_step(hfb_ctx* c, Stats& st) {
+  int64_t nx = ival(c, "nx"), ny = ival(c, "ny"), nz = ival(c, "nz");
+  if (nz < 2) fail(HFB_RUNTIME, "dycore_step needs nz >= 2 (got %lld)", (long long)nz);
+  DynConst k = make_dyn_const(rval(c, "dt"), rval(c, "rdx"), rval(c, "rdy"), rval(c, "rdz"),
+                              rval(c, "cs2"), rval(c, "grav"), rval(c, "th0"));
+  for (const char* n : {"th", "u", "v", "w", "p", "rho"}) dev_read(c, n);
+  Slot &rho = slot(c, "rho"), &th = slot(c, "th"), &u = slot(c, "u"), &v = slot(c, "v"),
+       &w = slot(c, "w"), &p = slot(c, "p");
+  for (Slot* s : {&th, &u, &v, &w, &p}) ensure_device(c, *s, true);
+  halo_exchange(c, {"th", "u", "v", "p"}, kHalo);
+  DynIn in{rho.d(), th.d(), u.d(), v.d(), w.d(), p.d()};
+  DynOut out{th.d_alt(), u.d_alt(), v.d_alt(), w.d_alt(), p.d_alt()};
+  Span sp = full_span(c, nx, ny);
+  launch(c, st, "dycore_advect", [&] { return launch_dycore_advect(in, out.th, grid_of(th), nz, k, sp, c->stream); });
+  launch(c, st, "dycore_acoustic", [&] { return launch_dycore_acoustic(in, out, grid_of(th), nz, k, sp, c->stream); });
+  for (Slot* s : {&th, &u, &v, &w, &p}) s->cur = 1 - s->cur;
+  // the generated code's 8 launches (dycore.h90 regions; region 1 spans i = 0..nx,
+  // region 2 spans j = 0..ny)
+  count_launch(st, nx + 1, ny);
+  count_launch(st, nx, ny + 1);
+  for (int r = 0; r < 6; ++r) count_launch(st, nx, ny);
+  for (const char* n : {"th", "u", "v", "w", "p"}) dev_written(c, n);
+}
+
+void dycore_entry(hfb_ctx* c, const std::string& r, Stats& st) {
+  const char* names[] = {"p", "rho", "th", "u", "v", "w"};
+  if (r == "main" || r == "simulation_run") {
+    int64_t nsteps = ival(c, "nsteps");
+    for (const char* n : names) do_copy_to_device(c, slot(c, n));
+    for (int64_t s = 0; s < nsteps; ++s) dycore_step(c, st);
+    for (const char* n : names) do_copy_from_device(c, slot(c, n));
+  } else if (r == "dycore_step") {
+    dycore_step(c, st);
+  } else {
+    fail(HFB_CONFIG, "program 'dycore' has no entry '%s'", r.c_str());
+  }
+}
+
+using EntryFn = void (*)(hfb_ctx*, const std::string&, Stats&);
+EntryFn entry_fn(const std::string& app) {
+  if (app == "diffusion") return diffusion_entry;
+  if (app == "damping") return damping_entry;
+  if (app == "bounded") return bounded_entry;
+  if (app == "surface_flux") return sf_entry;
+  if (app == "reduction") return reduction_entry;
+  if (app == "dycore") return dycore_entry;
+  return nullptr;
+}
+
+bool entry_has_transfers(const std::string& app, const std::string& r) {
+  if (r == "main" || r == "simulation_run") return true;
+  (void)app;
+  return false;
+}
+
+std::string routine_name(const char* entry) {
+  std::string r = lower(entry);
+  if (r.rfind("hfd_", 0) == 0) r = r.substr(4);
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// multi-GPU: NCCL loaded lazily (only a decomposed context with >1 rank needs it)
+// ---------------------------------------------------------------------------
+struct NcclApi {
+  void* h = nullptr;
+  int (*CommInitRank)(void**, int, const void* /*ncclUniqueId by value*/, int) = nullptr;
+  int (*Send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*CommDestroy)(void*) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+
+void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width);
+
+}  // namespace
+
+// ncclUniqueId is a 128-byte struct passed by value; declare a matching type.
+struct NcclId {
+  char internal[128];
+};
+typedef int (*nccl_init_fn)(void**, int, NcclId, int);
+
+namespace {
+
+NcclApi& nccl() {
+  static NcclApi api;
+  if (!api.h) {
+    api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!api.h) fail(HFB_CUDA, "cannot load libnccl.so.2: %s", dlerror());
+    auto sym = [](const char* n) {
+      void* p = dlsym(nccl().h, n);
+      if (!p) fail(HFB_CUDA, "libnccl.so.2 lacks %s", n);
+      return p;
+    };
+    api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+    api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+    api.GetErrorString =
+        reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+  }
+  return api;
+}
+
+void nccl_check(int rc, const char* what) {
+  if (rc != 0) fail(HFB_CUDA, "%s: %s", what, nccl().GetErrorString(rc));
+}
+
+constexpr int kNcclFloat64 = 8;  // ncclDouble
+constexpr int kNcclSum = 0;
+
+// Two-phase halo update of `fields` (all share one layout): east/west faces first,
+// then north/south faces spanning the I halo so corners arrive too.
+void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width) {
+  if (!c->decomposed || c->decomp.px * c->decomp.py <= 1) return;
+  if (!c->nccl_comm) fail(HFB_CONFIG, "decomposed context without a communicator");
+  (void)width;  // the face boxes always carry the full halo ring (kHalo)
+  NcclApi& api = nccl();
+  const hfb_decomp& d = c->decomp;
+  const int nbr[4] = {d.west, d.east, d.south, d.north};
+  for (int phase = 0; phase < 2; ++phase) {
+    // per side: pack all fields' send boxes contiguously
+    size_t need = 0;
+    int64_t sbox[4][4], rbox[4][4];
+    size_t count[4] = {0, 0, 0, 0};
+    for (int s = 2 * phase; s < 2 * phase + 2; ++s) {
+      hfb_decomp_faces(&d, s, sbox[s], rbox[s]);
+      if (nbr[s] < 0) continue;
+      for (const char* f : fields) {
+        Slot& sl = slot(c, f);
+        int64_t nk = sl.lay.nk * sl.lay.nl;
+        count[s] += static_cast<size_t>((sbox[s][1] - sbox[s][0] + 1) *
+                                        (sbox[s][3] - sbox[s][2] + 1) * nk);
+      }
+      need += count[s];
+    }
+    if (need == 0) continue;
+    if (c->halo_cap < need) {
+      if (c->halo_send) cudaFree(c->halo_send);
+      if (c->halo_recv) cudaFree(c->halo_recv);
+      cuda_check(cudaMalloc(&c->halo_send, need * sizeof(double)), "cudaMalloc(halo)");
+      cuda_check(cudaMalloc(&c->halo_recv, need * sizeof(double)), "cudaMalloc(halo)");
+      c->halo_cap = need;
+    }
+    size_t off = 0;
+    size_t base[4] = {0, 0, 0, 0};
+    for (int s = 2 * phase; s < 2 * phase + 2; ++s) {
+      base[s] = off;
+      if (nbr[s] < 0) continue;
+      for (const char* f : fields) {
+        Slot& sl = slot(c, f);
+        int64_t fk = sl.lay.nk * sl.lay.nl;
+        cuda_check(launch_pack_box(sl.d(), c->halo_send + off, grid_of(sl), fk, sbox[s], true,
+                                   c->stream),
+                   "halo pack");
+        off += static_cast<size_t>((sbox[s][1] - sbox[s][0] + 1) * (sbox[s][3] - sbox[s][2] + 1) *
+                                   fk);
+      }
+    }
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    for (int s = 2 * phase; s < 2 * phase + 2; ++s) {
+      if (nbr[s] < 0) continue;
+      nccl_check(api.Send(c->halo_send + base[s], count[s], kNcclFloat64, nbr[s], c->nccl_comm,
+                          c->stream),
+                 "ncclSend");
+      nccl_check(api.Recv(c->halo_recv + base[s], count[s], kNcclFloat64, nbr[s], c->nccl_comm,
+                          c->stream),
+                 "ncclRecv");
+    }
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
+    for (int s = 2 * phase; s < 2 * phase + 2; ++s) {
+      if (nbr[s] < 0) continue;
+      size_t o = base[s];
+      for (const char* f : fields) {
+        Slot& sl = slot(c, f);
+        int64_t fk = sl.lay.nk * sl.lay.nl;
+        cuda_check(launch_pack_box(sl.d(), c->halo_recv + o, grid_of(sl), fk, rbox[s], false,
+                                   c->stream),
+                   "halo unpack");
+        o += static_cast<size_t>((rbox[s][1] - rbox[s][0] + 1) * (rbox[s][3] - rbox[s][2] + 1) *
+                                 fk);
+      }
+      c->halo_bytes += static_cast<int64_t>(2 * count[s] * sizeof(double));
+    }
+  }
+}
+
+void allreduce_sum(hfb_ctx* c, double* dev_value) {
+  NcclApi& api = nccl();
+  nccl_check(api.AllReduce(dev_value, dev_value, 1, kNcclFloat64, kNcclSum, c->nccl_comm,
+                           c->stream),
+             "ncclAllReduce");
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* hfb_last_error(void) { return g_last_error.c_str(); }
+int hfb_abi_version(void) { return 1; }
+
+hfb_status hfb_create(int device, hfb_ctx** out) {
+  return guarded([&] {
+    if (!out) fail(HFB_CONFIG, "null output pointer");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+      fail(HFB_CUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
+    if (device < 0 || device >= n) fail(HFB_CONFIG, "device %d out of range [0, %d)", device, n);
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    auto c = std::make_unique<hfb_ctx>();
+    c->device = device;
+    cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    *out = c.release();
+  });
+}
+
+void hfb_destroy(hfb_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& [n, s] : c->slots) {
+    for (double* p : s.dev)
+      if (p) cudaFree(p);
+    if (s.pinned && s.host) cudaHostUnregister(s.host);
+  }
+  if (c->staging) cudaFree(c->staging);
+  if (c->red_partials) cudaFree(c->red_partials);
+  if (c->red_host) cudaFreeHost(c->red_host);
+  if (c->halo_send) cudaFree(c->halo_send);
+  if (c->halo_recv) cudaFree(c->halo_recv);
+  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  if (c->nccl_comm) nccl().CommDestroy(c->nccl_comm);
+  for (auto& t : c->pending) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (cudaEvent_t e : c->free_events) cudaEventDestroy(e);
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+hfb_status hfb_load_program(hfb_ctx* c, const char* app) {
+  return guarded([&] {
+    if (!c) fail(HFB_CONFIG, "null context");
+    std::string a = lower(app);
+    const AppDecl* found = nullptr;
+    for (const AppDecl& d : app_table())
+      if (d.app == a) found = &d;
+    if (!found) fail(HFB_CONFIG, "unknown program '%s'", a.c_str());
+    if (c->app) fail(HFB_CONFIG, "context already holds program '%s'", c->app->app.c_str());
+    c->app = found;
+    for (const ScalarDecl& s : found->scalars) {
+      Scalar v;
+      v.type = s.type;
+      if (s.is_param) {
+        v.i = static_cast<int64_t>(s.param);
+        v.r = s.param;
+        v.init = true;
+      }
+      c->scalars[s.name] = v;
+    }
+    for (const ArrayDecl& ad : found->arrays) {
+      Slot s;
+      s.module = found->module;
+      s.name = ad.name;
+      s.decl = &ad;
+      s.stream = c->stream;
+      c->slots[ad.name] = s;
+    }
+  });
+}
+
+hfb_status hfb_set_scalar_i64(hfb_ctx* c, const char* module, const char* name, int64_t v) {
+  return guarded([&] {
+    Scalar& s = scalar_ref(c, lower(module), lower(name));
+    s.i = v;
+    s.r = static_cast<double>(v);
+    s.init = true;
+  });
+}
+
+hfb_status hfb_set_scalar_f64(hfb_ctx* c, const char* module, const char* name, double v) {
+  return guarded([&] {
+    Scalar& s = scalar_ref(c, lower(module), lower(name));
+    s.r = v;
+    s.i = static_cast<int64_t>(v);
+    s.init = true;
+  });
+}
+
+hfb_status hfb_get_scalar_i64(hfb_ctx* c, const char* module, const char* name, int64_t* v) {
+  return guarded([&] {
+    Scalar& s = scalar_ref(c, lower(module), lower(name));
+    if (!s.init) fail(HFB_RUNTIME, "read of unset variable '%s'", name);
+    *v = s.type == SType::Int ? s.i : static_cast<int64_t>(s.r);
+  });
+}
+
+hfb_status hfb_get_scalar_f64(hfb_ctx* c, const char* module, const char* name, double* v) {
+  return guarded([&] {
+    Scalar& s = scalar_ref(c, lower(module), lower(name));
+    if (!s.init) fail(HFB_RUNTIME, "read of unset variable '%s'", name);
+    *v = s.type == SType::Real ? s.r : static_cast<double>(s.i);
+  });
+}
+
+hfb_status hfb_bind_array(hfb_ctx* c, const char* module, const char* name, int rank,
+                          const int64_t* lo, const int64_t* hi, double* host,
+                          const int64_t* strides, unsigned flags) {
+  return guarded([&] {
+    Slot& s = slot_ref(c, lower(module), lower(name));
+    if (!host) fail(HFB_CONFIG, "null host buffer for '%s'", name);
+    if (rank != static_cast<int>(s.decl->dims.size()))
+      fail(HFB_RUNTIME, "array '%s' has rank %zu but is bound with rank %d", name,
+           s.decl->dims.size(), rank);
+    if (s.has_device) {
+      // rebinding keeps the device copy only if the shape is unchanged
+      for (int d = 0; d < rank; ++d)
+        if (lo[d] != s.lower[d] || hi[d] != s.upper[d])
+          fail(HFB_CONFIG, "rebinding '%s' with a different shape after a transfer", name);
+    }
+    int64_t count = 1;
+    int64_t ext[4];
+    for (int d = 0; d < rank; ++d) {
+      ext[d] = hi[d] - lo[d] + 1;
+      if (ext[d] < 1) fail(HFB_RUNTIME, "non-positive extent for '%s'", name);
+      count *= ext[d];
+    }
+    int64_t st[4];
+    if (strides) {
+      for (int d = 0; d < rank; ++d) st[d] = strides[d];
+      // dense in some permutation: sorting dims by stride must give exact products
+      int order[4] = {0, 1, 2, 3};
+      std::sort(order, order + rank, [&](int a, int b) { return st[a] < st[b]; });
+      int64_t expect = 1;
+      for (int q = 0; q < rank; ++q) {
+        int d = order[q];
+        if (ext[d] > 1 && st[d] != expect)
+          fail(HFB_CONFIG, "host buffer of '%s' is not dense (stride %lld, expected %lld)", name,
+               (long long)st[d], (long long)expect);
+        if (ext[d] == 1) st[d] = 0;
+        expect *= ext[d];
+      }
+    } else {
+      int64_t acc = 1;
+      for (int d = rank - 1; d >= 0; --d) {  // ArrayValue order: last subscript fastest
+        st[d] = ext[d] > 1 ? acc : 0;
+        acc *= ext[d];
+      }
+    }
+    if (s.pinned && s.host && s.host != host) {
+      cudaHostUnregister(s.host);
+      s.pinned = false;
+    }
+    s.host = host;
+    s.rank = rank;
+    s.count = count;
+    for (int d = 0; d < rank; ++d) {
+      s.lower[d] = lo[d];
+      s.upper[d] = hi[d];
+      s.hstride[d] = st[d];
+    }
+    if ((flags & HFB_BIND_PIN) && !s.pinned) {
+      cudaSetDevice(c->device);
+      cudaError_t e = cudaHostRegister(host, static_cast<size_t>(count) * sizeof(double),
+                                       cudaHostRegisterDefault);
+      if (e == cudaSuccess)
+        s.pinned = true;
+      else
+        cudaGetLastError();  // already pinned or not pinnable: transfers still work
+    }
+  });
+}
+
+hfb_status hfb_residency(hfb_ctx* c, const char* module, const char* name, int* residency,
+                         int* has_device) {
+  return guarded([&] {
+    Slot& s = slot_ref(c, lower(module), lower(name));
+    if (residency) *residency = s.res;
+    if (has_device) *has_device = s.has_device ? 1 : 0;
+  });
+}
+
+hfb_status hfrt_device_allocate(hfb_ctx* c, const char* module, const char* name) {
+  return guarded([&] {
+    cudaSetDevice(c->device);
+    do_device_allocate(c, slot_ref(c, lower(module), lower(name)));
+  });
+}
+
+hfb_status hfrt_copy_to_device(hfb_ctx* c, const char* module, const char* name) {
+  return guarded([&] {
+    cudaSetDevice(c->device);
+    do_copy_to_device(c, slot_ref(c, lower(module), lower(name)));
+  });
+}
+
+hfb_status hfrt_copy_from_device(hfb_ctx* c, const char* module, const char* name) {
+  return guarded([&] {
+    cudaSetDevice(c->device);
+    do_copy_from_device(c, slot_ref(c, lower(module), lower(name)));
+  });
+}
+
+hfb_status hfb_mark_host_modified(hfb_ctx* c, const char* module, const char* name) {
+  return guarded([&] {
+    Slot& s = slot_ref(c, lower(module), lower(name));
+    if (s.has_device) s.res = kHost;
+  });
+}
+
+static hfb_status run_impl(hfb_ctx* c, const char* entry, hfb_launch_stats* stats, bool sync,
+                           bool allow_transfers) {
+  return guarded([&] {
+    if (!c || !c->app) fail(HFB_CONFIG, "no program loaded");
+    cudaSetDevice(c->device);
+    std::string r = routine_name(entry);
+    if (!allow_transfers && entry_has_transfers(c->app->app, r))
+      fail(HFB_CONFIG, "entry '%s' performs host transfers; use hfb_run", entry);
+    Stats st;
+    entry_fn(c->app->app)(c, r, st);
+    if (sync) cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    if (stats) {
+      stats->launches = st.launches;
+      stats->threads = st.threads;
+      stats->guard_returns = st.guard_returns;
+      stats->native_launches = st.native;
+    }
+  });
+}
+
+hfb_status hfb_run(hfb_ctx* c, const char* entry, hfb_launch_stats* stats) {
+  return run_impl(c, entry, stats, true, true);
+}
+
+hfb_status hfb_enqueue(hfb_ctx* c, const char* entry, hfb_launch_stats* stats) {
+  return run_impl(c, entry, stats, false, false);
+}
+
+hfb_status hfb_synchronize(hfb_ctx* c) {
+  return guarded([&] { cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize"); });
+}
+
+void* hfb_stream(hfb_ctx* c) { return c ? c->stream : nullptr; }
+
+hfb_status hfb_run_graph(hfb_ctx* c, const char* entry, int64_t steps, hfb_launch_stats* stats) {
+  return guarded([&] {
+    if (!c || !c->app) fail(HFB_CONFIG, "no program loaded");
+    if (steps < 1) return;
+    cudaSetDevice(c->device);
+    std::string r = routine_name(entry);
+    if (entry_has_transfers(c->app->app, r))
+      fail(HFB_CONFIG, "entry '%s' performs host transfers; cannot be graph-captured", entry);
+    if (c->decomposed && c->decomp.px * c->decomp.py > 1)
+      fail(HFB_CONFIG, "graph replay of decomposed contexts is not supported");
+    // Capture `steps` steps; an even step count returns every double buffer to its
+    // starting side, so the graph can be replayed; odd counts are re-captured.
+    std::string key = r + ":" + std::to_string(steps);
+    // no allocation may happen during capture: materialise every double buffer first
+    for (auto& [n, s] : c->slots)
+      if (s.decl->pingpong && s.has_device) ensure_device(c, s, true);
+    cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    std::map<std::string, int> cur0;
+    for (auto& [n, s] : c->slots) cur0[n] = s.cur;
+    if (c->graph_key != key || steps % 2) {
+      if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+      c->graph_exec = nullptr;
+      c->graph_key.clear();
+      Stats st;
+      cudaGraph_t g;
+      cuda_check(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal),
+                 "cudaStreamBeginCapture");
+      c->capturing = true;
+      try {
+        for (int64_t s = 0; s < steps; ++s) entry_fn(c->app->app)(c, r, st);
+        c->capturing = false;
+      } catch (...) {
+        c->capturing = false;
+        cudaStreamEndCapture(c->stream, &g);
+        for (auto& [n, s] : c->slots) s.cur = cur0[n];
+        throw;
+      }
+      cuda_check(cudaStreamEndCapture(c->stream, &g), "cudaStreamEndCapture");
+      cuda_check(cudaGraphInstantiate(&c->graph_exec, g, 0), "cudaGraphInstantiate");
+      cudaGraphDestroy(g);
+      c->graph_key = key;
+      c->graph_stats = hfb_launch_stats{st.launches, st.threads, st.guard_returns, st.native};
+      // capture recorded the launches without running them: roll the buffer sides back
+      for (auto& [n, s] : c->slots) s.cur = cur0[n];
+    }
+    cuda_check(cudaGraphLaunch(c->graph_exec, c->stream), "cudaGraphLaunch");
+    // advance the double-buffer sides exactly as the captured steps did
+    for (int64_t s = 0; s < steps; ++s)
+      for (auto& [n, sl] : c->slots)
+        if (sl.decl->pingpong && sl.dev[1]) sl.cur = 1 - sl.cur;
+    cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    if (stats) *stats = c->graph_stats;
+  });
+}
+
+hfb_status hfb_device_array(hfb_ctx* c, const char* module, const char* name, hfb_array* out) {
+  return guarded([&] {
+    Slot& s = slot_ref(c, lower(module), lower(name));
+    if (!s.has_device)
+      fail(HFB_RESIDENCY, "array '%s' has no device copy (missing transfer)", name);
+    hfb_array a{};
+    a.origin = s.d();
+    a.pitch = s.lay.pitch;
+    a.plane = s.lay.plane;
+    a.volume = s.lay.volume;
+    a.rank = s.rank;
+    for (int d = 0; d < 4; ++d) {
+      a.lower[d] = s.lower[d];
+      a.upper[d] = s.upper[d];
+    }
+    int packed = 0;
+    for (int d = 0; d < s.rank; ++d) packed |= static_cast<int>(s.decl->roles[d]) << (2 * d);
+    a.roles = packed;
+    a.slot = &s;
+    *out = a;
+  });
+}
+
+// ---- generated-kernel ABI --------------------------------------------------
+// The thread set of a launch: per axis (blockidx-1)*blockdim + threadidx (+start-1)
+// for blockidx in 1..grid, threadidx in 1..block; guard `it > end` (codegen.cpp:495-512).
+static Span launch_span(hfb_dim3 grid, hfb_dim3 block, int64_t istart, int64_t iend,
+                        int64_t jstart, int64_t jend) {
+  if (grid.x < 1 || grid.y < 1 || grid.z < 1 || block.x < 1 || block.y < 1 || block.z < 1)
+    fail(HFB_RUNTIME, "launch configuration dimensions must be positive");
+  Span sp;
+  sp.ilo = istart;
+  sp.jlo = jstart;
+  sp.ihi = std::min<int64_t>(iend, istart - 1 + static_cast<int64_t>(grid.x) * block.x);
+  sp.jhi = std::min<int64_t>(jend, jstart - 1 + static_cast<int64_t>(grid.y) * block.y);
+  return sp;
+}
+
+static cudaStream_t stream_of(void* s, const hfb_array& a) {
+  if (s) return static_cast<cudaStream_t>(s);
+  return a.slot ? static_cast<const Slot*>(a.slot)->stream : nullptr;
+}
+
+hfb_status hfk0_diffuse_step(hfb_dim3 grid, hfb_dim3 block, double coef, int32_t k, int32_t nx,
+                             int32_t ny, int32_t nz, hfb_array t_new, hfb_array t_old,
+                             void* stream) {
+  (void)k;
+  return guarded([&] {
+    Span sp = launch_span(grid, block, 1, nx, 1, ny);
+    sp.gnx = nx;
+    sp.gny = ny;
+    cuda_check(launch_diffusion(t_old.origin, t_new.origin, nullptr,
+                                Grid3{t_old.pitch, t_old.plane}, nz, coef, sp,
+                                stream_of(stream, t_old)),
+               "hfk0_diffuse_step");
+  });
+}
+
+hfb_status hfk1_diffuse_step(hfb_dim3 grid, hfb_dim3 block, int32_t k, int32_t nx, int32_t ny,
+                             int32_t nz, hfb_array t_new, hfb_array t_old, void* stream) {
+  (void)k;
+  return guarded([&] {
+    Span sp = launch_span(grid, block, 1, nx, 1, ny);
+    cuda_check(launch_copy_columns(t_new.origin, t_old.origin, Grid3{t_old.pitch, t_old.plane},
+                                   nz, sp, stream_of(stream, t_old)),
+               "hfk1_diffuse_step");
+  });
+}
+
+hfb_status hfk0_lateral_and_upper_damping(hfb_dim3 grid, hfb_dim3 block, int32_t k,
+                                          double mtratio_bnd, int32_t nx_mn, int32_t nx_mx,
+                                          int32_t ny_mn, int32_t ny_mx, int32_t nz_mn,
+                                          int32_t nz_mx, double tratio_bnd,
+                                          hfb_array dens_ptb_bnd, hfb_array dens_ptb_damp,
+                                          hfb_array dens_ref_f, void* stream) {
+  (void)k;
+  return guarded([&] {
+    // i = (blockidx-1)*B + threadidx + nx_mn - 1, in array-relative 1-based terms
+    Span sp = launch_span(grid, block, 1, nx_mx - nx_mn + 1, 1, ny_mx - ny_mn + 1);
+    cuda_check(launch_damping(dens_ref_f.origin, dens_ptb_bnd.origin,
+                              dens_ptb_bnd.origin + dens_ptb_bnd.volume, dens_ptb_damp.origin,
+                              Grid3{dens_ref_f.pitch, dens_ref_f.plane}, nz_mx - nz_mn + 1,
+                              mtratio_bnd, tratio_bnd, sp, stream_of(stream, dens_ref_f)),
+               "hfk0_lateral_and_upper_damping");
+  });
+}
+
+hfb_status hfk0_interior_update(hfb_dim3 grid, hfb_dim3 block, int32_t nx, int32_t ny,
+                                hfb_array a, hfb_array b, void* stream) {
+  return guarded([&] {
+    Span sp = launch_span(grid, block, 2, nx - 1, 2, ny - 1);
+    cuda_check(launch_bounded(a.origin, b.origin, a.pitch, sp, stream_of(stream, a)),
+               "hfk0_interior_update");
+  });
+}
+
+hfb_status hfk0_sf_slab_flx_tile_run(hfb_dim3 grid, hfb_dim3 block, int32_t nx, int32_t ny,
+                                     int32_t tile_land, hfb_array cover_frac,
+                                     hfb_array flx_sum_x, hfb_array flx_sum_y,
+                                     hfb_array swind, void* stream) {
+  return guarded([&] {
+    Span sp = launch_span(grid, block, 1, nx, 1, ny);
+    int64_t ntlm = cover_frac.upper[0] - cover_frac.lower[0] + 1;
+    if (tile_land < 1 || tile_land > ntlm)
+      fail(HFB_RUNTIME, "index %d out of bounds [1, %lld] in dimension 1 of 'cover_frac'",
+           tile_land, (long long)ntlm);
+    cuda_check(launch_sf_tile(cover_frac.origin + (tile_land - 1) * cover_frac.plane,
+                              flx_sum_x.origin, flx_sum_y.origin, swind.origin, cover_frac.pitch,
+                              sp, stream_of(stream, cover_frac)),
+               "hfk0_sf_slab_flx_tile_run");
+  });
+}
+
+// ---- decomposition -----------------------------------------------------------
+hfb_status hfb_decomp_init(hfb_decomp* d) {
+  return guarded([&] {
+    if (!d) fail(HFB_CONFIG, "null decomposition");
+    if (d->px < 1 || d->py < 1) fail(HFB_CONFIG, "process grid must be positive");
+    if (d->rank < 0 || d->rank >= d->px * d->py) fail(HFB_CONFIG, "rank out of range");
+    if (d->halo < 0 || d->halo > kHalo) fail(HFB_CONFIG, "halo width must be in [0, %d]", kHalo);
+    if (d->global_nx < d->px || d->global_ny < d->py)
+      fail(HFB_CONFIG, "grid %lldx%lld cannot be split %dx%d", (long long)d->global_nx,
+           (long long)d->global_ny, d->px, d->py);
+    d->rx = d->rank % d->px;
+    d->ry = d->rank / d->px;
+    auto split = [](int64_t n, int p, int r, int64_t* off, int64_t* len) {
+      int64_t base = n / p, rem = n % p;
+      *len = base + (r < rem ? 1 : 0);
+      *off = r * base + std::min<int64_t>(r, rem);
+    };
+    split(d->global_nx, d->px, d->rx, &d->i0, &d->nx);
+    split(d->global_ny, d->py, d->ry, &d->j0, &d->ny);
+    if (d->halo > 0 && (d->nx < d->halo || d->ny < d->halo))
+      fail(HFB_CONFIG, "tile %lldx%lld is narrower than the halo", (long long)d->nx,
+           (long long)d->ny);
+    d->west = d->rx > 0 ? d->rank - 1 : -1;
+    d->east = d->rx < d->px - 1 ? d->rank + 1 : -1;
+    d->south = d->ry > 0 ? d->rank - d->px : -1;
+    d->north = d->ry < d->py - 1 ? d->rank + d->px : -1;
+  });
+}
+
+hfb_status hfb_decomp_faces(const hfb_decomp* d, int32_t side, int64_t send_box[4],
+                            int64_t recv_box[4]) {
+  return guarded([&] {
+    if (!d) fail(HFB_CONFIG, "null decomposition");
+    const int64_t H = d->halo, nx = d->nx, ny = d->ny;
+    int64_t sb[4], rb[4];
+    switch (side) {
+      case 0:  // west: send my first H columns, receive the H columns left of me
+        sb[0] = 1; sb[1] = H; sb[2] = 1; sb[3] = ny;
+        rb[0] = 1 - H; rb[1] = 0; rb[2] = 1; rb[3] = ny;
+        break;
+      case 1:  // east
+        sb[0] = nx - H + 1; sb[1] = nx; sb[2] = 1; sb[3] = ny;
+        rb[0] = nx + 1; rb[1] = nx + H; rb[2] = 1; rb[3] = ny;
+        break;
+      case 2:  // south, spanning the I halo (corners)
+        sb[0] = 1 - H; sb[1] = nx + H; sb[2] = 1; sb[3] = H;
+        rb[0] = 1 - H; rb[1] = nx + H; rb[2] = 1 - H; rb[3] = 0;
+        break;
+      case 3:  // north
+        sb[0] = 1 - H; sb[1] = nx + H; sb[2] = ny - H + 1; sb[3] = ny;
+        rb[0] = 1 - H; rb[1] = nx + H; rb[2] = ny + 1; rb[3] = ny + H;
+        break;
+      default:
+        fail(HFB_CONFIG, "side must be 0..3");
+    }
+    const int nb[4] = {d->west, d->east, d->south, d->north};
+    if (nb[side] < 0 || H == 0) {
+      sb[1] = sb[0] - 1;
+      rb[1] = rb[0] - 1;
+    }
+    for (int q = 0; q < 4; ++q) {
+      send_box[q] = sb[q];
+      recv_box[q] = rb[q];
+    }
+  });
+}
+
+hfb_status hfb_set_decomposition(hfb_ctx* c, const hfb_decomp* d, const void* nccl_id) {
+  return guarded([&] {
+    if (!c) fail(HFB_CONFIG, "null context");
+    hfb_decomp dd = *d;
+    hfb_status st = hfb_decomp_init(&dd);
+    if (st != HFB_OK) fail(st, "%s", g_last_error.c_str());
+    c->decomp = dd;
+    c->decomposed = true;
+    if (dd.px * dd.py > 1) {
+      if (!nccl_id) fail(HFB_CONFIG, "a multi-rank decomposition needs the NCCL unique id");
+      cudaSetDevice(c->device);
+      NcclApi& api = nccl();
+      (void)api;
+      auto init = reinterpret_cast<nccl_init_fn>(dlsym(api.h, "ncclCommInitRank"));
+      if (!init) fail(HFB_CUDA, "libnccl.so.2 lacks ncclCommInitRank");
+      NcclId id;
+      std::memcpy(id.internal, nccl_id, sizeof id.internal);
+      nccl_check(init(&c->nccl_comm, dd.px * dd.py, id, dd.rank), "ncclCommInitRank");
+    }
+  });
+}
+
+int64_t hfb_halo_bytes(hfb_ctx* c) { return c ? c->halo_bytes : 0; }
+
+hfb_status hfb_profile(hfb_ctx* c, int enable) {
+  return guarded([&] {
+    if (!c) fail(HFB_CONFIG, "null context");
+    resolve_timings(c);
+    if (enable < 0) c->kernel_ms.clear();
+    c->prof = enable > 0;
+  });
+}
+
+hfb_status hfb_kernel_time(hfb_ctx* c, const char* kernel, double* total_ms, int64_t* count) {
+  return guarded([&] {
+    if (!c) fail(HFB_CONFIG, "null context");
+    resolve_timings(c);
+    auto it = c->kernel_ms.find(kernel ? kernel : "");
+    *total_ms = it == c->kernel_ms.end() ? 0.0 : it->second.first;
+    *count = it == c->kernel_ms.end() ? 0 : it->second.second;
+  });
+}
+
+hfb_status hfb_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    auto get = reinterpret_cast<int (*)(NcclId*)>(dlsym(nccl().h, "ncclGetUniqueId"));
+    if (!get) fail(HFB_CUDA, "libnccl.so.2 lacks ncclGetUniqueId");
+    NcclId id;
+    nccl_check(get(&id), "ncclGetUniqueId");
+    std::memcpy(out128, id.internal, sizeof id.internal);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,291 @@
+"""Python host mirror of the reference's executor interface, over the C ABI (include/hfb.h).
+
+The reference runs a Hybrid-Fortran program with
+
+    Program p(units); MachineState st = p.prepare_state(); ...
+    LaunchStats s = run_gpu_simulated(p, st, "hfd_main");      # interp.hpp:113-122
+
+Here the same shape of call runs the program's kernels natively on a B200:
+
+    eng = Engine("diffusion")                     # Program + MachineState (+ device)
+    eng.set("nx", 128); ...; eng.bind("t_old", a)  # module scalars / ObjectSlot host buffers
+    stats = eng.run("main")                        # LaunchStats (launches/threads/guard_returns)
+
+Errors are raised as HfbError with the reference's ErrKind name (diagnostics.hpp:21-32).
+There is no fallback: if libhfb.so or a CUDA device is missing, Engine() raises.
+"""
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libhfb.so"
+CSRC = PKG / "csrc"
+
+KINDS = {0: "ok", 10: "config", 15: "runtime", 16: "residency", 17: "race", 18: "validation",
+         19: "io", 30: "cuda"}
+
+# exported C-ABI symbols (include/hfb.h); the CPU test checks each one resolves
+EXPORTS = [
+    "hfb_last_error", "hfb_abi_version", "hfb_create", "hfb_destroy", "hfb_load_program",
+    "hfb_set_scalar_i64", "hfb_set_scalar_f64", "hfb_get_scalar_i64", "hfb_get_scalar_f64",
+    "hfb_bind_array", "hfb_residency", "hfrt_device_allocate", "hfrt_copy_to_device",
+    "hfrt_copy_from_device", "hfb_mark_host_modified", "hfb_run", "hfb_enqueue",
+    "hfb_synchronize", "hfb_stream", "hfb_run_graph", "hfb_device_array", "hfk0_diffuse_step",
+    "hfk1_diffuse_step", "hfk0_lateral_and_upper_damping", "hfk0_interior_update",
+    "hfk0_sf_slab_flx_tile_run", "hfb_decomp_init", "hfb_decomp_faces", "hfb_set_decomposition",
+    "hfb_halo_bytes", "hfb_nccl_unique_id", "hfb_profile", "hfb_kernel_time",
+]
+
+# module of each built-in program (the apps' state modules)
+MODULES = {"diffusion": "diff_state", "damping": "svar", "bounded": "b_state",
+           "surface_flux": "sf_state", "reduction": "red_state", "dycore": "dyn_state"}
+
+
+class HfbError(RuntimeError):
+    def __init__(self, code, msg):
+        self.code = code
+        self.kind = KINDS.get(code, "unknown")
+        super().__init__(f"[{self.kind}] {msg}")
+
+
+@dataclass
+class LaunchStats:
+    launches: int
+    threads: int
+    guard_returns: int
+    native_launches: int
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("launches", ctypes.c_int64), ("threads", ctypes.c_int64),
+                ("guard_returns", ctypes.c_int64), ("native_launches", ctypes.c_int64)]
+
+
+class Decomp(ctypes.Structure):
+    _fields_ = [("global_nx", ctypes.c_int64), ("global_ny", ctypes.c_int64),
+                ("nz", ctypes.c_int64), ("px", ctypes.c_int32), ("py", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("halo", ctypes.c_int32), ("rx", ctypes.c_int32),
+                ("ry", ctypes.c_int32), ("i0", ctypes.c_int64), ("j0", ctypes.c_int64),
+                ("nx", ctypes.c_int64), ("ny", ctypes.c_int64), ("west", ctypes.c_int32),
+                ("east", ctypes.c_int32), ("south", ctypes.c_int32), ("north", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def build(verbose=False):
+    """Compile the sm_100a kernels + C ABI into paper_1710_08616_b200/libhfb.so."""
+    subprocess.run(["make", "-s", "-C", str(CSRC), "-j4"], check=True,
+                   stdout=None if verbose else subprocess.DEVNULL)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            build()
+        L = ctypes.CDLL(str(LIB_PATH))
+        c = ctypes
+        P, S, i64, dbl = c.c_void_p, c.c_char_p, c.c_int64, c.c_double
+        L.hfb_last_error.restype = S
+        L.hfb_create.argtypes = [c.c_int, c.POINTER(P)]
+        L.hfb_destroy.argtypes = [P]
+        L.hfb_destroy.restype = None
+        L.hfb_load_program.argtypes = [P, S]
+        L.hfb_set_scalar_i64.argtypes = [P, S, S, i64]
+        L.hfb_set_scalar_f64.argtypes = [P, S, S, dbl]
+        L.hfb_get_scalar_i64.argtypes = [P, S, S, c.POINTER(i64)]
+        L.hfb_get_scalar_f64.argtypes = [P, S, S, c.POINTER(dbl)]
+        L.hfb_bind_array.argtypes = [P, S, S, c.c_int, c.POINTER(i64), c.POINTER(i64), P,
+                                     c.POINTER(i64), c.c_uint]
+        L.hfb_residency.argtypes = [P, S, S, c.POINTER(c.c_int), c.POINTER(c.c_int)]
+        for n in ("hfrt_device_allocate", "hfrt_copy_to_device", "hfrt_copy_from_device",
+                  "hfb_mark_host_modified"):
+            getattr(L, n).argtypes = [P, S, S]
+        L.hfb_run.argtypes = [P, S, c.POINTER(_Stats)]
+        L.hfb_enqueue.argtypes = [P, S, c.POINTER(_Stats)]
+        L.hfb_synchronize.argtypes = [P]
+        L.hfb_stream.argtypes = [P]
+        L.hfb_stream.restype = P
+        L.hfb_run_graph.argtypes = [P, S, i64, c.POINTER(_Stats)]
+        L.hfb_decomp_init.argtypes = [c.POINTER(Decomp)]
+        L.hfb_decomp_faces.argtypes = [c.POINTER(Decomp), c.c_int32, c.POINTER(i64),
+                                       c.POINTER(i64)]
+        L.hfb_set_decomposition.argtypes = [P, c.POINTER(Decomp), P]
+        L.hfb_halo_bytes.argtypes = [P]
+        L.hfb_halo_bytes.restype = i64
+        L.hfb_nccl_unique_id.argtypes = [P]
+        L.hfb_profile.argtypes = [P, c.c_int]
+        L.hfb_kernel_time.argtypes = [P, S, c.POINTER(dbl), c.POINTER(i64)]
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise HfbError(rc, lib().hfb_last_error().decode())
+
+
+def _b(s):
+    return s.encode() if isinstance(s, str) else s
+
+
+def decomp_init(global_nx, global_ny, nz, px, py, rank, halo=2):
+    d = Decomp(global_nx, global_ny, nz, px, py, rank, halo)
+    _check(lib().hfb_decomp_init(ctypes.byref(d)))
+    return d
+
+
+def decomp_faces(d, side):
+    sb = (ctypes.c_int64 * 4)()
+    rb = (ctypes.c_int64 * 4)()
+    _check(lib().hfb_decomp_faces(ctypes.byref(d), side, sb, rb))
+    return tuple(sb), tuple(rb)
+
+
+class Engine:
+    """One context = the reference's (Program, MachineState) pair on one GPU."""
+
+    def __init__(self, app, device=0):
+        self.app = app
+        self.module = MODULES.get(app, app)
+        h = ctypes.c_void_p()
+        _check(lib().hfb_create(device, ctypes.byref(h)))
+        self._h = h
+        self._bound = {}
+        _check(lib().hfb_load_program(h, _b(app)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hfb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # --- MachineState --------------------------------------------------------------
+    def set(self, name, value):
+        if isinstance(value, (int, np.integer)) and not isinstance(value, bool):
+            _check(lib().hfb_set_scalar_i64(self._h, _b(self.module), _b(name), int(value)))
+        else:
+            _check(lib().hfb_set_scalar_f64(self._h, _b(self.module), _b(name), float(value)))
+
+    def get(self, name, integer=False):
+        if integer:
+            v = ctypes.c_int64()
+            _check(lib().hfb_get_scalar_i64(self._h, _b(self.module), _b(name), ctypes.byref(v)))
+        else:
+            v = ctypes.c_double()
+            _check(lib().hfb_get_scalar_f64(self._h, _b(self.module), _b(name), ctypes.byref(v)))
+        return v.value
+
+    def bind(self, name, array, lower=None, pin=False):
+        """Bind a float64 host array shaped by the declared dims (any dense order)."""
+        a = array
+        if a.dtype != np.float64:
+            raise TypeError("module arrays are real(r_size) = float64")
+        rank = a.ndim
+        lower = tuple(lower) if lower is not None else (1,) * rank
+        upper = tuple(l + n - 1 for l, n in zip(lower, a.shape))
+        strides = (ctypes.c_int64 * rank)(*[s // 8 for s in a.strides])
+        lo = (ctypes.c_int64 * rank)(*lower)
+        hi = (ctypes.c_int64 * rank)(*upper)
+        _check(lib().hfb_bind_array(self._h, _b(self.module), _b(name), rank, lo, hi,
+                                    a.ctypes.data, strides, 1 if pin else 0))
+        self._bound[name] = a  # keep the buffer alive
+
+    # --- transfers (hfrt_*) -----------------------------------------------------------
+    def device_allocate(self, name):
+        _check(lib().hfrt_device_allocate(self._h, _b(self.module), _b(name)))
+
+    def copy_to_device(self, name):
+        _check(lib().hfrt_copy_to_device(self._h, _b(self.module), _b(name)))
+
+    def copy_from_device(self, name):
+        _check(lib().hfrt_copy_from_device(self._h, _b(self.module), _b(name)))
+
+    def mark_host_modified(self, name):
+        _check(lib().hfb_mark_host_modified(self._h, _b(self.module), _b(name)))
+
+    def residency(self, name):
+        r, d = ctypes.c_int(), ctypes.c_int()
+        _check(lib().hfb_residency(self._h, _b(self.module), _b(name), ctypes.byref(r),
+                                   ctypes.byref(d)))
+        return ("host", "device", "both")[r.value], bool(d.value)
+
+    # --- entries ------------------------------------------------------------------
+    def run(self, entry="main"):
+        st = _Stats()
+        _check(lib().hfb_run(self._h, _b(entry), ctypes.byref(st)))
+        return LaunchStats(st.launches, st.threads, st.guard_returns, st.native_launches)
+
+    def enqueue(self, entry):
+        st = _Stats()
+        _check(lib().hfb_enqueue(self._h, _b(entry), ctypes.byref(st)))
+        return LaunchStats(st.launches, st.threads, st.guard_returns, st.native_launches)
+
+    def run_graph(self, entry, steps):
+        st = _Stats()
+        _check(lib().hfb_run_graph(self._h, _b(entry), int(steps), ctypes.byref(st)))
+        return LaunchStats(st.launches, st.threads, st.guard_returns, st.native_launches)
+
+    def synchronize(self):
+        _check(lib().hfb_synchronize(self._h))
+
+    @property
+    def stream(self):
+        return lib().hfb_stream(self._h)
+
+    def set_decomposition(self, d, nccl_id=None):
+        buf = None
+        if nccl_id is not None:
+            buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        _check(lib().hfb_set_decomposition(self._h, ctypes.byref(d), buf))
+
+    def halo_bytes(self):
+        return lib().hfb_halo_bytes(self._h)
+
+    def profile(self, enable=True, clear=False):
+        """CUDA-event timing of every native launch (on the context stream)."""
+        _check(lib().hfb_profile(self._h, -1 if clear else (1 if enable else 0)))
+
+    def kernel_time(self, kernel):
+        """(total device ms, launches) accumulated for one native kernel."""
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        _check(lib().hfb_kernel_time(self._h, _b(kernel), ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
+
+
+def nccl_unique_id():
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().hfb_nccl_unique_id(buf))
+    return buf.raw
+
+
+def run_gpu(app, scalars, arrays, entry="main", device=0, lower=None):
+    """run_gpu_simulated(program, state, entry) analogue: runs `entry` of `app` with the
+    given module scalars and host arrays (updated in place); returns (LaunchStats, scalars)."""
+    with Engine(app, device) as eng:
+        for k, v in scalars.items():
+            eng.set(k, v)
+        for k, a in arrays.items():
+            eng.bind(k, a, lower=(lower or {}).get(k))
+        stats = eng.run(entry)
+        out = {}
+        for k, v in scalars.items():
+            out[k] = eng.get(k, integer=isinstance(v, (int, np.integer)))
+        return stats, out

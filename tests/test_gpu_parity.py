@@ -1,0 +1,230 @@
+"""Parity of the B200 path (libhfb.so through the C ABI) with the reference.
+
+* every golden case (fixtures produced by the reference interpreter itself): bit-exact
+  outputs, and LaunchStats equal to the reference's simulated launches;
+* larger seeded inputs against the CPU restatement (oracle/), bit-exact;
+* full-size (BASELINE configs) single steps against the oracle, bit-exact;
+* the drop-in surface: per-step entries, residency errors, the generated-kernel ABI,
+  graph replay.
+"""
+import numpy as np
+import pytest
+
+import paper_1710_08616_b200 as hfb
+from cases import APPS, CASES, CASE_BY_NAME, DYCORE_FILLS, DYCORE_SCALARS, Case
+from golden_io import bits_equal, decl, load_golden, make_inputs, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def run_engine(case, arrs, entry="main"):
+    app = APPS[case.app]
+    with hfb.Engine(case.app) as eng:
+        for k, v in case.ints.items():
+            eng.set(k, int(v))
+        for k, v in case.reals.items():
+            eng.set(k, float(v))
+        for name, a in arrs.items():
+            _, lower = decl(case.app, name, case.ints)
+            eng.bind(name, a, lower=lower)
+        stats = eng.run(entry)
+        scal = {}
+        if case.app == "reduction":
+            scal["total"] = eng.get("total")
+    return stats, scal
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: c.name)
+@pytest.mark.parametrize("order", ["C", "F"])
+def test_golden_case(case, order):
+    meta, out, init, extra = load_golden(case.name)
+    arrs = make_inputs(case, order=order)
+    stats, scal = run_engine(case, arrs)
+    for name in APPS[case.app].outputs:
+        if name == "total":
+            ref = float(out["total"].reshape(()))
+            assert abs(scal["total"] - ref) <= 1e-12 * abs(ref), (scal["total"], ref)
+        else:
+            assert bits_equal(arrs[name], out[name]), f"{case.name}: {name} differs"
+    if "gpu_launches" in meta and case.app != "reduction":
+        assert stats.launches == meta["gpu_launches"]
+        assert stats.threads == meta["gpu_threads"]
+        assert stats.guard_returns == meta["gpu_guard_returns"]
+    assert stats.native_launches > 0
+
+
+def _oracle_vs_gpu(case, order="C"):
+    a_gpu = make_inputs(case, order=order)
+    a_ora = {k: v.copy(order="A") for k, v in a_gpu.items()}
+    run_oracle(case, a_ora)
+    run_engine(case, a_gpu)
+    for name in APPS[case.app].outputs:
+        if name in a_gpu:
+            assert bits_equal(a_gpu[name], a_ora[name]), f"{case.name}: {name} differs"
+
+
+LARGE = [
+    Case("diffusion_128x128x58_s10", "diffusion", dict(nx=128, ny=128, nz=58, nsteps=10),
+         dict(coef=0.1), {"t_old": (1, 280.0, 10.0)}, unset=["t_new"]),
+    Case("diffusion_333x77x58_s3", "diffusion", dict(nx=333, ny=77, nz=58, nsteps=3),
+         dict(coef=0.1), {"t_old": (1, 280.0, 10.0)}, unset=["t_new"]),
+    Case("damping_260x131x58", "damping",
+         dict(nx_mn=-1, nx_mx=258, ny_mn=0, ny_mx=130, nz_mn=1, nz_mx=58),
+         dict(tratio_bnd=0.3, mtratio_bnd=0.7),
+         {"dens_ref_f": (2, 1.0, 1.0), "dens_ptb_bnd": (3, -0.005, 0.01)}),
+    Case("bounded_1024x515", "bounded", dict(nx=1024, ny=515), {},
+         {"a": (4, 0.0, 1.0), "b": (6, -1.0, 0.5)}),
+    Case("surface_flux_1024x1024", "surface_flux", dict(nx=1024, ny=1024, tile_land=2), {},
+         {"cover_frac": (5, 0.0, 1.0)}),
+    Case("dycore_128x96x58_s5", "dycore", dict(nx=128, ny=96, nz=58, nsteps=5),
+         dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
+    Case("dycore_77x203x31_s3", "dycore", dict(nx=77, ny=203, nz=31, nsteps=3),
+         dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
+]
+
+
+@pytest.mark.parametrize("case", LARGE, ids=lambda c: c.name)
+def test_large_vs_oracle(case):
+    _oracle_vs_gpu(case)
+
+
+def test_reduction_large_tolerance():
+    case = Case("reduction_512x512x58", "reduction", dict(nx=512, ny=512, nz=58),
+                dict(total=0.0), {"y": (6, 0.0, 1.0)})
+    arrs = make_inputs(case)
+    ref = run_oracle(case, {k: v.copy() for k, v in arrs.items()})
+    _, scal = run_engine(case, arrs)
+    assert abs(scal["total"] - ref["total"]) <= 1e-12 * abs(ref["total"])
+
+
+@pytest.mark.parametrize("nx,ny", [(512, 512)])
+def test_full_size_dycore_step(nx, ny):
+    """BASELINE configs C2 / C4: one full step, bit-exact against the oracle."""
+    case = Case(f"dycore_{nx}x{ny}x58_s1", "dycore", dict(nx=nx, ny=ny, nz=58, nsteps=1),
+                dict(DYCORE_SCALARS), dict(DYCORE_FILLS))
+    _oracle_vs_gpu(case)
+
+
+def test_full_size_diffusion_step():
+    case = Case("diffusion_1581x1301x58_s1", "diffusion", dict(nx=1581, ny=1301, nz=58, nsteps=1),
+                dict(coef=0.1), {"t_old": (1, 280.0, 10.0)}, unset=["t_new"])
+    _oracle_vs_gpu(case)
+
+
+# ---------------------------------------------------------------------------
+# drop-in surface: per-step entries, residency, generated-kernel ABI, graphs
+# ---------------------------------------------------------------------------
+
+def _diffusion_engine(nx=40, ny=36, nz=58, nsteps=3):
+    case = Case("d", "diffusion", dict(nx=nx, ny=ny, nz=nz, nsteps=nsteps), dict(coef=0.1),
+                {"t_old": (1, 280.0, 10.0)}, unset=["t_new"])
+    arrs = make_inputs(case)
+    eng = hfb.Engine("diffusion")
+    for k, v in case.ints.items():
+        eng.set(k, v)
+    eng.set("coef", 0.1)
+    for k, a in arrs.items():
+        eng.bind(k, a)
+    return case, arrs, eng
+
+
+def test_missing_transfer_is_a_residency_error():
+    # deleting transferHere -> "[residency] array 't_old' has no device copy"
+    case, arrs, eng = _diffusion_engine()
+    with pytest.raises(hfb.HfbError) as e:
+        eng.run("hfd_diffuse_step")
+    assert e.value.kind == "residency" and "t_old" in str(e.value)
+    with pytest.raises(hfb.HfbError) as e:
+        eng.copy_from_device("t_old")
+    assert e.value.kind == "residency" and "never transferred" in str(e.value)
+    eng.close()
+
+
+def test_per_step_entry_matches_simulation_run():
+    case, arrs, eng = _diffusion_engine(nsteps=3)
+    ref = {k: v.copy() for k, v in arrs.items()}
+    run_oracle(case, ref)
+    eng.copy_to_device("t_old")
+    eng.copy_to_device("t_new")
+    for _ in range(3):
+        st = eng.run("diffuse_step")
+        assert st.launches == 2
+    assert eng.residency("t_old") == ("device", True)
+    with pytest.raises(hfb.HfbError) as e:  # device data is newer
+        eng.copy_to_device("t_old")
+    assert e.value.kind == "residency"
+    eng.copy_from_device("t_old")
+    eng.copy_from_device("t_new")
+    assert bits_equal(arrs["t_old"], ref["t_old"]) and bits_equal(arrs["t_new"], ref["t_new"])
+    eng.mark_host_modified("t_old")
+    with pytest.raises(hfb.HfbError) as e:  # stale device copy
+        eng.run("diffuse_step")
+    assert e.value.kind == "residency"
+    eng.close()
+
+
+def test_graph_replay_matches_step_loop():
+    case = Case("g", "dycore", dict(nx=96, ny=64, nz=58, nsteps=6), dict(DYCORE_SCALARS),
+                dict(DYCORE_FILLS))
+    arrs = make_inputs(case)
+    ref = {k: v.copy() for k, v in arrs.items()}
+    run_oracle(case, ref)
+    with hfb.Engine("dycore") as eng:
+        for k, v in case.ints.items():
+            eng.set(k, v)
+        for k, v in case.reals.items():
+            eng.set(k, v)
+        for k, a in arrs.items():
+            eng.bind(k, a)
+        for k in arrs:
+            eng.copy_to_device(k)
+        st = eng.run_graph("dycore_step", 2)
+        assert st.native_launches == 4
+        eng.run_graph("dycore_step", 2)
+        eng.run_graph("dycore_step", 2)
+        for k in arrs:
+            eng.copy_from_device(k)
+    for k in ("th", "u", "v", "w", "p"):
+        assert bits_equal(arrs[k], ref[k]), k
+
+
+def test_errors_mirror_reference_kinds():
+    with pytest.raises(hfb.HfbError) as e:
+        hfb.Engine("no_such_app")
+    assert e.value.kind == "config"
+    case, arrs, eng = _diffusion_engine()
+    with pytest.raises(hfb.HfbError) as e:
+        eng.run("no_such_entry")
+    assert e.value.kind == "config"
+    eng.set("nx", 41)  # bound buffers no longer match the declaration
+    with pytest.raises(hfb.HfbError) as e:
+        eng.run("main")
+    assert e.value.kind == "runtime"
+    eng.close()
+    # bounded with nx = 2: ceiling(0/32) = 0 blocks -> the reference rejects the launch
+    with hfb.Engine("bounded") as eng:
+        eng.set("nx", 2)
+        eng.set("ny", 5)
+        a = np.ones((2, 5))
+        b = np.zeros((2, 5))
+        eng.bind("a", a)
+        eng.bind("b", b)
+        with pytest.raises(hfb.HfbError) as e:
+            eng.run("main")
+        assert e.value.kind == "runtime"
+
+
+def test_pinned_binding_and_fortran_order_equal():
+    case = CASE_BY_NAME["dycore_24x20x12_s2"]
+    meta, out, init, extra = load_golden(case.name)
+    arrs = make_inputs(case, order="F")
+    with hfb.Engine("dycore") as eng:
+        for k, v in case.ints.items():
+            eng.set(k, v)
+        for k, v in case.reals.items():
+            eng.set(k, v)
+        for k, a in arrs.items():
+            eng.bind(k, a, pin=True)
+        eng.run("main")
+    for k in ("th", "u", "v", "w", "p"):
+        assert bits_equal(arrs[k], out[k])
