@@ -442,7 +442,37 @@ struct AdvArgs {
 // Regions 1-4 fused: the x/y/z face fluxes are recomputed per cell from theta
 // (each face is computed by both adjacent cells with identical inputs, so the bits
 // match the materialised fx/fy/fz of the reference), then the flux divergence with
-// the velocity-divergence correction. K-window of theta in registers.
+// the velocity-divergence correction. K-window of theta in registers; the next
+// level's 13 loads are issued before the current level is computed (software
+// pipelining: two levels of loads in flight per thread).
+struct AdvLevel {
+  double xm2, xm1, xp1, xp2, ym2, ym1, yp1, yp2, ui, uim1, vj, vjm1, w, tkp2;
+};
+
+__device__ __forceinline__ AdvLevel adv_load(const double* __restrict__ th,
+                                             const double* __restrict__ u,
+                                             const double* __restrict__ v,
+                                             const double* __restrict__ w, int64_t off,
+                                             int64_t W, int64_t off_kp2, bool has_kp2) {
+  AdvLevel L;
+  const double* r = th + off;
+  L.xm2 = __ldg(r - 2);
+  L.xm1 = __ldg(r - 1);
+  L.xp1 = __ldg(r + 1);
+  L.xp2 = __ldg(r + 2);
+  L.ym2 = __ldg(r - 2 * W);
+  L.ym1 = __ldg(r - W);
+  L.yp1 = __ldg(r + W);
+  L.yp2 = __ldg(r + 2 * W);
+  L.ui = __ldg(u + off);
+  L.uim1 = __ldg(u + off - 1);
+  L.vj = __ldg(v + off);
+  L.vjm1 = __ldg(v + off - W);
+  L.w = __ldg(w + off);
+  L.tkp2 = has_kp2 ? __ldg(th + off_kp2) : 0.0;
+  return L;
+}
+
 __global__ void __launch_bounds__(128) k_dyn_advect(AdvArgs a) {
   const int64_t i = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t j = a.sp.jlo + static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y;
@@ -457,44 +487,44 @@ __global__ void __launch_bounds__(128) k_dyn_advect(AdvArgs a) {
   double* __restrict__ thn = a.thn + col;
   const int nz = a.nz;
   const DynConst& c = a.c;
+  const bool east = gi == gnx, west = gi == 1, north = gj == gny, south = gj == 1;
 
   double tkm1 = 0.0;
   double tk = __ldg(th);
   double tkp1 = nz >= 2 ? __ldg(th + P) : 0.0;
-  double tkp2 = nz >= 3 ? __ldg(th + 2 * P) : 0.0;
   double fzm = 0.0;   // fz(k-1), fz(0) = 0 (ground)
   double wkm1 = 0.0;  // w(k-1)
+  AdvLevel cur = adv_load(th, u, v, w, 0, W, 2 * P, nz >= 3);
   for (int k = 1; k <= nz; ++k) {
-    const int64_t off = static_cast<int64_t>(k - 1) * P;
-    const double wk = __ldg(w + off);
+    AdvLevel nxt;
+    if (k < nz) {
+      const int64_t o = static_cast<int64_t>(k) * P;
+      nxt = adv_load(th, u, v, w, o, W, static_cast<int64_t>(k + 2) * P, k + 3 <= nz);
+    }
+    const double tkp2 = cur.tkp2;
+    const double wk = cur.w;
     const double fzk = face_flux(k, nz, wk, tkm1, tk, tkp1, tkp2);
-    const double* r = th + off;
-    const double xm2 = __ldg(r - 2), xm1 = __ldg(r - 1), xp1 = __ldg(r + 1), xp2 = __ldg(r + 2);
-    const double ym2 = __ldg(r - 2 * W), ym1 = __ldg(r - W), yp1 = __ldg(r + W),
-                 yp2 = __ldg(r + 2 * W);
-    const double ui = __ldg(u + off), uim1 = __ldg(u + off - 1);
-    const double vj = __ldg(v + off), vjm1 = __ldg(v + off - W);
-    const double fxe = face_flux(gi, gnx, ui, xm1, tk, xp1, xp2);
-    const double fxw = face_flux(gi - 1, gnx, uim1, xm2, xm1, tk, xp1);
-    const double fyn = face_flux(gj, gny, vj, ym1, tk, yp1, yp2);
-    const double fys = face_flux(gj - 1, gny, vjm1, ym2, ym1, tk, yp1);
-    const double ue = (gi == gnx) ? 0.0 : ui;
-    const double uw = (gi == 1) ? 0.0 : uim1;
-    const double vnf = (gj == gny) ? 0.0 : vj;
-    const double vs = (gj == 1) ? 0.0 : vjm1;
+    const double fxe = face_flux(gi, gnx, cur.ui, cur.xm1, tk, cur.xp1, cur.xp2);
+    const double fxw = face_flux(gi - 1, gnx, cur.uim1, cur.xm2, cur.xm1, tk, cur.xp1);
+    const double fyn = face_flux(gj, gny, cur.vj, cur.ym1, tk, cur.yp1, cur.yp2);
+    const double fys = face_flux(gj - 1, gny, cur.vjm1, cur.ym2, cur.ym1, tk, cur.yp1);
+    const double ue = east ? 0.0 : cur.ui;
+    const double uw = west ? 0.0 : cur.uim1;
+    const double vnf = north ? 0.0 : cur.vj;
+    const double vs = south ? 0.0 : cur.vjm1;
     const double wt = (k == nz) ? 0.0 : wk;
     const double wb = (k == 1) ? 0.0 : wkm1;
     double flux = c.rdx * (fxe - fxw) + c.rdy * (fyn - fys);
     flux = flux + c.rdz * (fzk - fzm);
     double div = c.rdx * (ue - uw) + c.rdy * (vnf - vs);
     div = div + c.rdz * (wt - wb);
-    thn[off] = tk - c.dt * (flux - tk * div);
+    thn[static_cast<int64_t>(k - 1) * P] = tk - c.dt * (flux - tk * div);
     fzm = fzk;
     wkm1 = wk;
     tkm1 = tk;
     tk = tkp1;
     tkp1 = tkp2;
-    tkp2 = (k + 3 <= nz) ? __ldg(th + static_cast<int64_t>(k + 2) * P) : 0.0;
+    cur = nxt;
   }
 }
 
@@ -507,12 +537,39 @@ struct AcoArgs {
   Span sp;
 };
 
+struct AcoLevel {
+  double pk, pe, pw, pnn, psth, uk, ukw, vk, vks, rho, th, w;
+};
+
+__device__ __forceinline__ AcoLevel aco_load(const DynIn& in, int64_t col, int64_t off,
+                                             int64_t W) {
+  AcoLevel L;
+  const double* p = in.p + col + off;
+  L.pk = __ldg(p);
+  L.pe = __ldg(p + 1);
+  L.pw = __ldg(p - 1);
+  L.pnn = __ldg(p + W);
+  L.psth = __ldg(p - W);
+  L.uk = __ldg(in.u + col + off);
+  L.ukw = __ldg(in.u + col + off - 1);
+  L.vk = __ldg(in.v + col + off);
+  L.vks = __ldg(in.v + col + off - W);
+  L.rho = __ldg(in.rho + col + off);
+  L.th = __ldg(in.th + col + off);
+  L.w = __ldg(in.w + col + off);
+  return L;
+}
+
 // Regions 5-7 fused: horizontal pressure gradient (new u, v), the pressure after the
 // horizontal divergence (ps; the western/southern new velocities are recomputed from
 // p and u/v instead of being re-read), and the HE-VI Thomas sweep for w with the
-// pressure update. Per-thread Thomas coefficients cp/dp and ps stay on chip in
-// shared memory ([k][thread], conflict-free); one forward and one backward K sweep.
-__global__ void __launch_bounds__(64) k_dyn_acoustic(AcoArgs a) {
+// pressure update, in one forward and one backward K sweep per column.
+// On-chip budget: the Thomas coefficient cp(k) stays in shared memory ([k][thread],
+// conflict-free); dp(k) and ps(k) make an L2 round trip through the OUTPUT arrays
+// themselves (wn and pn hold dp and ps after the forward sweep and are overwritten
+// with the final w and p in the backward sweep, so DRAM sees only the final values).
+// This keeps shared memory at nz*8 B per thread, i.e. ~15 resident warps per SM.
+__global__ void __launch_bounds__(128) k_dyn_acoustic(AcoArgs a) {
   extern __shared__ double smem[];
   const int T = blockDim.x * blockDim.y;
   const int t = threadIdx.y * blockDim.x + threadIdx.x;
@@ -521,47 +578,38 @@ __global__ void __launch_bounds__(64) k_dyn_acoustic(AcoArgs a) {
   if (i > a.sp.ihi || j > a.sp.jhi) return;
   const int nz = a.nz;
   double* cps = smem + t;
-  double* dps = smem + static_cast<int64_t>(nz) * T + t;
-  double* pss = smem + 2 * static_cast<int64_t>(nz) * T + t;
   const int64_t gi = i + a.sp.i0, gj = j + a.sp.j0;
   const bool east = gi == a.sp.gnx, west = gi == 1, north = gj == a.sp.gny, south = gj == 1;
   const int64_t P = a.g.plane, W = a.g.pitch;
   const int64_t col = (j - 1) * W + (i - 1);
-  const double* __restrict__ rho = a.in.rho + col;
-  const double* __restrict__ th = a.in.th + col;
-  const double* __restrict__ u = a.in.u + col;
-  const double* __restrict__ v = a.in.v + col;
-  const double* __restrict__ w = a.in.w + col;
-  const double* __restrict__ p = a.in.p + col;
-  double* __restrict__ un = a.out.u + col;
-  double* __restrict__ vn = a.out.v + col;
-  double* __restrict__ wn = a.out.w + col;
-  double* __restrict__ pn = a.out.p + col;
+  double* un = a.out.u + col;
+  double* vn = a.out.v + col;
+  double* wn = a.out.w + col;  // holds dp(k) between the sweeps
+  double* pn = a.out.p + col;  // holds ps(k) between the sweeps
   const DynConst& c = a.c;
 
-  double rho_prev = 0.0, th_prev = 0.0, ps_prev = 0.0, cp_prev = 0.0, dp_prev = 0.0;
+  double rho_prev = 0.0, th_prev = 0.0, ps_prev = 0.0, w_prev = 0.0, cp_prev = 0.0,
+         dp_prev = 0.0;
+  AcoLevel cur = aco_load(a.in, col, 0, W);
   for (int k = 1; k <= nz; ++k) {
+    AcoLevel nxt;
+    if (k < nz) nxt = aco_load(a.in, col, static_cast<int64_t>(k) * P, W);
     const int64_t off = static_cast<int64_t>(k - 1) * P;
-    const double pk = __ldg(p + off);
-    const double pe = __ldg(p + off + 1), pw = __ldg(p + off - 1);
-    const double pnn = __ldg(p + off + W), psth = __ldg(p + off - W);
-    const double uk = __ldg(u + off), ukw = __ldg(u + off - 1);
-    const double vk = __ldg(v + off), vks = __ldg(v + off - W);
-    const double unk = east ? 0.0 : uk - c.dt_rdx * (pe - pk);
-    const double vnk = north ? 0.0 : vk - c.dt_rdy * (pnn - pk);
-    const double uw = west ? 0.0 : ukw - c.dt_rdx * (pk - pw);
-    const double vs = south ? 0.0 : vks - c.dt_rdy * (pk - psth);
+    const double pk = cur.pk;
+    const double unk = east ? 0.0 : cur.uk - c.dt_rdx * (cur.pe - pk);
+    const double vnk = north ? 0.0 : cur.vk - c.dt_rdy * (cur.pnn - pk);
+    const double uw = west ? 0.0 : cur.ukw - c.dt_rdx * (pk - cur.pw);
+    const double vs = south ? 0.0 : cur.vks - c.dt_rdy * (pk - cur.psth);
     const double psk = pk - c.dt_cs2 * (c.rdx * (unk - uw) + c.rdy * (vnk - vs));
     un[off] = unk;
     vn[off] = vnk;
-    pss[static_cast<int64_t>(k - 1) * T] = psk;
-    const double rhok = __ldg(rho + off), thk = __ldg(th + off);
+    pn[off] = psk;
     if (k >= 2) {
       const int kf = k - 1;  // face kf + 1/2 between levels kf and kf + 1
-      const double rf = 0.5 * (rho_prev + rhok);
+      const double rf = 0.5 * (rho_prev + cur.rho);
       const double beta = c.beta_num / rf;
-      double dd = __ldg(w + static_cast<int64_t>(kf - 1) * P) - c.dt_rdz * (psk - ps_prev) / rf;
-      dd = dd + c.dt_grav * (0.5 * (th_prev + thk) - c.th0) / c.th0;
+      double dd = w_prev - c.dt_rdz * (psk - ps_prev) / rf;
+      dd = dd + c.dt_grav * (0.5 * (th_prev + cur.th) - c.th0) / c.th0;
       const double bb = 1.0 + 2.0 * beta;
       double cpk, dpk;
       if (kf == 1) {
@@ -573,25 +621,37 @@ __global__ void __launch_bounds__(64) k_dyn_acoustic(AcoArgs a) {
         dpk = (dd + beta * dp_prev) / m;
       }
       cps[static_cast<int64_t>(kf - 1) * T] = cpk;
-      dps[static_cast<int64_t>(kf - 1) * T] = dpk;
+      wn[static_cast<int64_t>(kf - 1) * P] = dpk;
       cp_prev = cpk;
       dp_prev = dpk;
     }
-    rho_prev = rhok;
-    th_prev = thk;
+    rho_prev = cur.rho;
+    th_prev = cur.th;
+    w_prev = cur.w;
     ps_prev = psk;
+    cur = nxt;
   }
-  // backward sweep: w at faces nz-1 .. 1 (w(nz) = 0 is the lid), pressure update
+  // backward sweep: w at faces nz-1 .. 1 (w(nz) = 0 is the lid), pressure update.
+  // dp(k) / ps(k+1) were written by this thread (same-thread RAW through L2: plain
+  // loads, not the read-only path); they are fetched one level ahead.
   wn[static_cast<int64_t>(nz - 1) * P] = 0.0;
   double wk1 = 0.0;  // w(k+1)
+  double dpk = wn[static_cast<int64_t>(nz - 2) * P];
+  double psk1 = pn[static_cast<int64_t>(nz - 1) * P];
   for (int k = nz - 1; k >= 1; --k) {
-    const double dpk = dps[static_cast<int64_t>(k - 1) * T];
+    double dp_next = 0.0, ps_next = 0.0;
+    if (k >= 2) {
+      dp_next = wn[static_cast<int64_t>(k - 2) * P];
+      ps_next = pn[static_cast<int64_t>(k - 1) * P];
+    }
     const double wk = (k == nz - 1) ? dpk : dpk - cps[static_cast<int64_t>(k - 1) * T] * wk1;
     wn[static_cast<int64_t>(k - 1) * P] = wk;
-    pn[static_cast<int64_t>(k) * P] = pss[static_cast<int64_t>(k) * T] - c.dt_cs2_rdz * (wk1 - wk);
+    pn[static_cast<int64_t>(k) * P] = psk1 - c.dt_cs2_rdz * (wk1 - wk);
     wk1 = wk;
+    dpk = dp_next;
+    psk1 = ps_next;
   }
-  pn[0] = pss[0] - c.dt_cs2_rdz * wk1;
+  pn[0] = pn[0] - c.dt_cs2_rdz * wk1;
 }
 }  // namespace
 
@@ -607,9 +667,23 @@ cudaError_t launch_dycore_advect(const DynIn& in, double* thn, Grid3 g, int64_t 
 cudaError_t launch_dycore_acoustic(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                    const DynConst& c, const Span& sp, cudaStream_t s) {
   if (span_empty(sp) || nz < 2) return cudaSuccess;
-  dim3 block(32, 2);
-  size_t smem = 3 * static_cast<size_t>(nz) * block.x * block.y * sizeof(double);
-  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  // pick the block height that maximises resident warps under the shared-memory budget
+  // (cp: nz doubles per thread) and the 128-thread launch bound
+  const size_t smem_cap = 227 * 1024;
+  int best_by = 1, best_warps = 0;
+  for (int by = 1; by <= 4; ++by) {
+    size_t per_block = static_cast<size_t>(nz) * 32 * by * sizeof(double);
+    if (per_block > smem_cap) break;
+    int blocks = static_cast<int>(std::min<size_t>(smem_cap / (per_block + 1024), 32 / by));
+    int warps = blocks * by;
+    if (warps >= best_warps) {
+      best_warps = warps;
+      best_by = by;
+    }
+  }
+  if (best_warps == 0) return cudaErrorInvalidConfiguration;
+  dim3 block(32, best_by);
+  size_t smem = static_cast<size_t>(nz) * block.x * block.y * sizeof(double);
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(k_dyn_acoustic,
