@@ -1,0 +1,258 @@
+// hfb_dycore_tmem.cu — the HE-VI acoustic kernel, B200 edition.
+//
+// Same arithmetic as dycore.h90 regions 5-7 (see k_dyn_acoustic in hfb_kernels.cu for
+// the line-by-line mapping), different machine organisation:
+//
+//   * A CTA owns a 32 x 4 tile of (i,j) columns (warp w = row j0+w, lane = i0+lane) and
+//     marches K. Each K-plane of the six input fields the tile needs (p with its
+//     one-cell ring, u with i-1, v with j-1, rho, th, w) is staged into shared memory by
+//     LDGSTS (cp.async, 16-B chunks, L1 bypass) through a kStages-deep ring, so ~6 planes
+//     per CTA are in flight while the current one is computed (no per-thread register
+//     prefetch, no redundant L1 traffic for the horizontal neighbours).
+//   * The Thomas sweep needs cp(k), dp(k) for the back substitution and ps(k) for the
+//     pressure update: 3 x nz doubles per column. cp and dp live in TENSOR MEMORY: each
+//     thread owns one TMEM lane (warp w -> lanes 32w..32w+31) and writes its
+//     coefficients with tcgen05.st; the back substitution reads four levels per
+//     tcgen05.ld. ps lives in shared memory. Nothing makes a round trip through L2/HBM:
+//     DRAM traffic is exactly the compulsory 10 x 8 B per grid point.
+//   * Budget per CTA: 256 TMEM columns (cp: 0..127, dp: 128..255; nz <= 65), ring
+//     kStages x 7 KB, ps nz x 1 KB -> two CTAs (8 warps) per SM share the 512 TMEM
+//     columns and ~200 KB of shared memory.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "hfb_kernels.cuh"
+#include "hfb_sm100.cuh"
+
+namespace hfb {
+
+namespace {
+
+constexpr int kTX = 32, kTY = 4, kThreads = kTX * kTY;
+constexpr int kStages = 6;
+// per-stage plane tiles (doubles): p rows j0-1..j0+4, cols i0-2..i0+33 (36);
+// u rows j0..j0+3, cols i0-2..i0+31 (34); v rows j0-1..j0+3, cols i0..i0+31 (32);
+// rho/th/w rows j0..j0+3, cols i0..i0+31 (32)
+constexpr int kPW = 36, kPR = kTY + 2;
+constexpr int kUW = 34, kUR = kTY;
+constexpr int kVW = 32, kVR = kTY + 1;
+constexpr int kSW = 32, kSR = kTY;
+constexpr int kOffP = 0;
+constexpr int kOffU = kOffP + kPW * kPR;
+constexpr int kOffV = kOffU + kUW * kUR;
+constexpr int kOffRho = kOffV + kVW * kVR;
+constexpr int kOffTh = kOffRho + kSW * kSR;
+constexpr int kOffW = kOffTh + kSW * kSR;
+constexpr int kStageDoubles = kOffW + kSW * kSR;  // 896
+constexpr int kChunks = kStageDoubles / 2;         // 16-B chunks per stage (448)
+constexpr int kChunksPerThread = (kChunks + kThreads - 1) / kThreads;  // 4
+constexpr int kTmemCols = 256;
+constexpr int kDpCol = 128;
+
+struct AcoTmemArgs {
+  DynIn in;
+  DynOut out;
+  Grid3 g;
+  int nz;
+  int64_t nj;       // tile extents of the arrays (rows valid: -2 .. nj+1)
+  int64_t row_lo, row_hi;  // valid element range inside a row: [-kIOff, pitch-kIOff-1]
+  DynConst c;
+  Span sp;
+};
+
+__global__ void __launch_bounds__(kThreads, 2) k_dyn_acoustic_tmem(AcoTmemArgs a) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ uint32_t tmem_base_slot;
+  double* ring = smem;                                   // kStages * kStageDoubles
+  double* ps_s = smem + kStages * kStageDoubles;         // nz * kThreads
+
+  const int lane = threadIdx.x, warp = threadIdx.y;
+  const int t = warp * kTX + lane;
+  const int64_t i0 = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * kTX;  // 1-based local
+  const int64_t j0 = a.sp.jlo + static_cast<int64_t>(blockIdx.y) * kTY;
+  const int64_t i = i0 + lane, j = j0 + warp;
+  const bool active = i <= a.sp.ihi && j <= a.sp.jhi;
+  const int nz = a.nz;
+  const int64_t P = a.g.plane, W = a.g.pitch;
+  const DynConst& c = a.c;
+
+  // ---- TMEM allocation (warp 0), address broadcast through shared memory ----------
+  if (warp == 0) sm100::tmem_alloc(&tmem_base_slot, kTmemCols);
+  sm100::tmem_fence_before();
+  __syncthreads();
+  sm100::tmem_fence_after();
+  const uint32_t tmem = tmem_base_slot + (static_cast<uint32_t>(32 * warp) << 16);
+
+  // ---- this thread's copy chunks: (global source at plane 0, smem byte offset) -----
+  const double* src[kChunksPerThread];
+  uint32_t dst[kChunksPerThread];
+  bool ok[kChunksPerThread];
+  const uint32_t ring_u32 = sm100::smem_u32(ring);
+#pragma unroll
+  for (int q = 0; q < kChunksPerThread; ++q) {
+    const int ch = t + q * kThreads;
+    ok[q] = false;
+    src[q] = a.in.p;
+    dst[q] = 0;
+    if (ch >= kChunks) continue;
+    const int e = ch * 2;  // first double of the chunk inside the stage
+    const double* base;
+    int64_t row, col;      // 0-based local row (j') and column (i') of the chunk start
+    if (e < kOffU) {
+      base = a.in.p; row = (j0 - 2) + e / kPW; col = (i0 - 3) + e % kPW;
+    } else if (e < kOffV) {
+      base = a.in.u; row = (j0 - 1) + (e - kOffU) / kUW; col = (i0 - 3) + (e - kOffU) % kUW;
+    } else if (e < kOffRho) {
+      base = a.in.v; row = (j0 - 2) + (e - kOffV) / kVW; col = (i0 - 1) + (e - kOffV) % kVW;
+    } else if (e < kOffTh) {
+      base = a.in.rho; row = (j0 - 1) + (e - kOffRho) / kSW; col = (i0 - 1) + (e - kOffRho) % kSW;
+    } else if (e < kOffW) {
+      base = a.in.th; row = (j0 - 1) + (e - kOffTh) / kSW; col = (i0 - 1) + (e - kOffTh) % kSW;
+    } else {
+      base = a.in.w; row = (j0 - 1) + (e - kOffW) / kSW; col = (i0 - 1) + (e - kOffW) % kSW;
+    }
+    ok[q] = row >= -kHalo && row <= a.nj - 1 + kHalo && col >= a.row_lo && col + 1 <= a.row_hi;
+    src[q] = base + row * W + col;
+    dst[q] = ring_u32 + static_cast<uint32_t>(e) * 8u;
+  }
+  auto issue = [&](int k) {  // stage the 0-based level k into ring slot k % kStages
+    if (k < nz) {
+      const uint32_t so = static_cast<uint32_t>((k % kStages) * kStageDoubles * 8);
+      const int64_t go = static_cast<int64_t>(k) * P;
+#pragma unroll
+      for (int q = 0; q < kChunksPerThread; ++q)
+        if (ok[q]) sm100::cp_async16(dst[q] + so, src[q] + go);
+    }
+    sm100::cp_async_commit();
+  };
+
+  const int64_t col = (j - 1) * W + (i - 1);
+  double* un = a.out.u + col;
+  double* vn = a.out.v + col;
+  double* wn = a.out.w + col;
+  double* pn = a.out.p + col;
+  const bool east = i + a.sp.i0 == a.sp.gnx, west = i + a.sp.i0 == 1;
+  const bool north = j + a.sp.j0 == a.sp.gny, south = j + a.sp.j0 == 1;
+
+#pragma unroll 1
+  for (int k = 0; k < kStages - 1; ++k) issue(k);
+
+  double rho_prev = 0.0, th_prev = 0.0, ps_prev = 0.0, w_prev = 0.0, cp_prev = 0.0,
+         dp_prev = 0.0;
+#pragma unroll 1
+  for (int k = 0; k < nz; ++k) {  // 0-based level; dialect level kk = k + 1
+    issue(k + kStages - 1);
+    sm100::cp_async_wait<kStages - 1>();
+    __syncthreads();
+    const double* S = ring + (k % kStages) * kStageDoubles;
+    const double* Pp = S + kOffP + (warp + 1) * kPW + (lane + 2);
+    const double pk = Pp[0], pe = Pp[1], pw = Pp[-1], pnn = Pp[kPW], psth = Pp[-kPW];
+    const double* Up = S + kOffU + warp * kUW + (lane + 2);
+    const double uk = Up[0], ukw = Up[-1];
+    const double* Vp = S + kOffV + (warp + 1) * kVW + lane;
+    const double vk = Vp[0], vks = Vp[-kVW];
+    const double rhok = S[kOffRho + warp * kSW + lane];
+    const double thk = S[kOffTh + warp * kSW + lane];
+    const double wk = S[kOffW + warp * kSW + lane];
+
+    const double unk = east ? 0.0 : uk - c.dt_rdx * (pe - pk);
+    const double vnk = north ? 0.0 : vk - c.dt_rdy * (pnn - pk);
+    const double uw = west ? 0.0 : ukw - c.dt_rdx * (pk - pw);
+    const double vs = south ? 0.0 : vks - c.dt_rdy * (pk - psth);
+    const double psk = pk - c.dt_cs2 * (c.rdx * (unk - uw) + c.rdy * (vnk - vs));
+    if (active) {
+      un[static_cast<int64_t>(k) * P] = unk;
+      vn[static_cast<int64_t>(k) * P] = vnk;
+    }
+    ps_s[k * kThreads + t] = psk;
+    if (k >= 1) {
+      const int f = k - 1;  // 0-based face between levels k-1 and k (dialect kf = k)
+      const double rf = 0.5 * (rho_prev + rhok);
+      const double beta = c.beta_num / rf;
+      double dd = w_prev - c.dt_rdz * (psk - ps_prev) / rf;
+      dd = dd + c.dt_grav * (0.5 * (th_prev + thk) - c.th0) / c.th0;
+      const double bb = 1.0 + 2.0 * beta;
+      double cpk, dpk;
+      if (f == 0) {
+        cpk = -beta / bb;
+        dpk = dd / bb;
+      } else {
+        const double m = bb + beta * cp_prev;
+        cpk = -beta / m;
+        dpk = (dd + beta * dp_prev) / m;
+      }
+      sm100::tmem_st_f64(tmem + 2 * f, cpk);
+      sm100::tmem_st_f64(tmem + kDpCol + 2 * f, dpk);
+      cp_prev = cpk;
+      dp_prev = dpk;
+    }
+    rho_prev = rhok;
+    th_prev = thk;
+    w_prev = wk;
+    ps_prev = psk;
+    __syncthreads();  // the slot is refilled by the next iteration's issue()
+  }
+  sm100::cp_async_wait<0>();
+  sm100::tmem_wait_st();
+
+  // ---- back substitution: faces nz-2 .. 0 (w(nz) = 0 is the lid), four per TMEM load
+  if (active) wn[static_cast<int64_t>(nz - 1) * P] = 0.0;
+  double wk1 = 0.0;  // w at the face above
+  const int nf = nz - 1;
+#pragma unroll 1
+  for (int cb = (nf - 1) / 4; cb >= 0; --cb) {
+    double cpv[4], dpv[4];
+    sm100::tmem_ld_4f64(tmem + 8 * cb, cpv);
+    sm100::tmem_ld_4f64(tmem + kDpCol + 8 * cb, dpv);
+#pragma unroll
+    for (int q = 3; q >= 0; --q) {
+      const int f = 4 * cb + q;
+      if (f >= nf) continue;
+      const double wk = (f == nf - 1) ? dpv[q] : dpv[q] - cpv[q] * wk1;
+      const double pk1 = ps_s[(f + 1) * kThreads + t] - c.dt_cs2_rdz * (wk1 - wk);
+      if (active) {
+        wn[static_cast<int64_t>(f) * P] = wk;
+        pn[static_cast<int64_t>(f + 1) * P] = pk1;
+      }
+      wk1 = wk;
+    }
+  }
+  if (active) pn[0] = ps_s[t] - c.dt_cs2_rdz * wk1;
+
+  sm100::tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) sm100::tmem_dealloc(tmem_base_slot, kTmemCols);
+}
+
+}  // namespace
+
+bool dycore_acoustic_tmem_fits(int64_t nz) { return nz >= 2 && nz - 1 <= 64; }
+
+cudaError_t launch_dycore_acoustic_tmem(const DynIn& in, const DynOut& out, Grid3 g,
+                                        int64_t nz, int64_t nj, const DynConst& c,
+                                        const Span& sp, cudaStream_t s) {
+  if (sp.ihi < sp.ilo || sp.jhi < sp.jlo) return cudaSuccess;
+  if (!dycore_acoustic_tmem_fits(nz)) return cudaErrorInvalidValue;
+  // at most two CTAs per SM: they share the SM's 512 TMEM columns (256 each); a third
+  // CTA would block in tcgen05.alloc, so small-nz launches pad their shared memory
+  const size_t smem = std::max<size_t>((static_cast<size_t>(kStages) * kStageDoubles +
+                                        static_cast<size_t>(nz) * kThreads) * sizeof(double),
+                                       80 * 1024);
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_dyn_acoustic_tmem,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  AcoTmemArgs a{in, out, g, static_cast<int>(nz), nj, -kIOff, g.pitch - kIOff - 1, c, sp};
+  dim3 block(kTX, kTY);
+  dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
+            static_cast<unsigned>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY));
+  k_dyn_acoustic_tmem<<<grid, block, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace hfb

@@ -73,8 +73,15 @@ struct DynOut {
 };
 cudaError_t launch_dycore_advect(const DynIn& in, double* thn, Grid3 g, int64_t nz,
                                  const DynConst& c, const Span& sp, cudaStream_t s);
+// generic version: Thomas scratch dp/ps through an L2 round trip, cp in shared memory
 cudaError_t launch_dycore_acoustic(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                    const DynConst& c, const Span& sp, cudaStream_t s);
+// sm_100a version (hfb_dycore_tmem.cu): cp.async plane ring + TMEM Thomas scratch;
+// nj = rows of the arrays (for halo-row bounds); requires nz - 1 <= 64
+bool dycore_acoustic_tmem_fits(int64_t nz);
+cudaError_t launch_dycore_acoustic_tmem(const DynIn& in, const DynOut& out, Grid3 g,
+                                        int64_t nz, int64_t nj, const DynConst& c,
+                                        const Span& sp, cudaStream_t s);
 
 // ---- halo pack/unpack for the 2-D decomposition -------------------------------------
 cudaError_t launch_pack_box(const double* field, double* buf, Grid3 g, int64_t nk,

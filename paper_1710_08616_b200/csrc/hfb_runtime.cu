@@ -16,6 +16,7 @@
 #include <cctype>
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -230,6 +231,7 @@ struct hfb_ctx {
   cudaGraphExec_t graph_exec = nullptr;
   std::string graph_key;
   hfb_launch_stats graph_stats{};
+  bool force_generic = getenv("HFB_GENERIC_KERNELS") != nullptr;  // A/B switch
   // per-kernel CUDA-event timing (hfb_profile)
   bool prof = false;
   bool capturing = false;
@@ -712,7 +714,14 @@ void dycore_step(hfb_ctx* c, Stats& st) {
   DynOut out{th.d_alt(), u.d_alt(), v.d_alt(), w.d_alt(), p.d_alt()};
   Span sp = full_span(c, nx, ny);
   launch(c, st, "dycore_advect", [&] { return launch_dycore_advect(in, out.th, grid_of(th), nz, k, sp, c->stream); });
-  launch(c, st, "dycore_acoustic", [&] { return launch_dycore_acoustic(in, out, grid_of(th), nz, k, sp, c->stream); });
+  if (dycore_acoustic_tmem_fits(nz) && !c->force_generic)
+    launch(c, st, "dycore_acoustic", [&] {
+      return launch_dycore_acoustic_tmem(in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
+    });
+  else
+    launch(c, st, "dycore_acoustic", [&] {
+      return launch_dycore_acoustic(in, out, grid_of(th), nz, k, sp, c->stream);
+    });
   for (Slot* s : {&th, &u, &v, &w, &p}) s->cur = 1 - s->cur;
   // the generated code's 8 launches (dycore.h90 regions; region 1 spans i = 0..nx,
   // region 2 spans j = 0..ny)

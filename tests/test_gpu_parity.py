@@ -80,6 +80,13 @@ LARGE = [
          dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
     Case("dycore_77x203x31_s3", "dycore", dict(nx=77, ny=203, nz=31, nsteps=3),
          dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
+    # nz - 1 > 64: beyond the TMEM budget, served by the generic (L2 round-trip) kernel
+    Case("dycore_40x30x80_s2", "dycore", dict(nx=40, ny=30, nz=80, nsteps=2),
+         dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
+    Case("dycore_33x9x65_s2", "dycore", dict(nx=33, ny=9, nz=65, nsteps=2),
+         dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
+    Case("dycore_31x7x2_s3", "dycore", dict(nx=31, ny=7, nz=2, nsteps=3),
+         dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
 ]
 
 
@@ -95,6 +102,13 @@ def test_reduction_large_tolerance():
     ref = run_oracle(case, {k: v.copy() for k, v in arrs.items()})
     _, scal = run_engine(case, arrs)
     assert abs(scal["total"] - ref["total"]) <= 1e-12 * abs(ref["total"])
+
+
+def test_generic_kernels_match(monkeypatch):
+    """The portable acoustic kernel (HFB_GENERIC_KERNELS=1) gives the same bits."""
+    monkeypatch.setenv("HFB_GENERIC_KERNELS", "1")
+    _oracle_vs_gpu(Case("dycore_70x45x58_s2", "dycore", dict(nx=70, ny=45, nz=58, nsteps=2),
+                        dict(DYCORE_SCALARS), dict(DYCORE_FILLS)))
 
 
 @pytest.mark.parametrize("nx,ny", [(512, 512)])
