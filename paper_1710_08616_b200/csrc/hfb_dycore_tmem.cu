@@ -255,4 +255,279 @@ cudaError_t launch_dycore_acoustic_tmem(const DynIn& in, const DynOut& out, Grid
   return cudaGetLastError();
 }
 
+
+// ===========================================================================
+// The whole dycore timestep in ONE kernel (dycore.h90 regions 1-8): flux-limited
+// advection of theta + horizontal pressure gradient + divergence + HE-VI Thomas
+// sweep, reading rho, th, u, v, w, p once and writing th', u', v', w', p' once:
+// 88 compulsory bytes per grid point (the two-kernel split needs 120).
+// Advection is independent of the Thomas recurrence, so its arithmetic fills the
+// latency of the division chain (the acoustic kernel alone is bound by fp64 latency).
+// ===========================================================================
+namespace {
+
+// fused stage: th rows j0-2..j0+5 (8) x cols i0-2..i0+33 (36); u 4 x 34; v 5 x 32;
+// w 4 x 32; p 6 x 36; rho 4 x 32
+constexpr int kFThW = 36, kFThR = kTY + 4;
+constexpr int kFOffTh = 0;
+constexpr int kFOffU = kFOffTh + kFThW * kFThR;
+constexpr int kFOffV = kFOffU + kUW * kUR;
+constexpr int kFOffW = kFOffV + kVW * kVR;
+constexpr int kFOffP = kFOffW + kSW * kSR;
+constexpr int kFOffRho = kFOffP + kPW * kPR;
+constexpr int kFStageDoubles = kFOffRho + kSW * kSR;  // 1056
+constexpr int kFChunks = kFStageDoubles / 2;          // 528
+constexpr int kFChunksPerThread = (kFChunks + kThreads - 1) / kThreads;  // 5
+constexpr int kFStages = 6;
+
+// minmod and the limited upwind face flux, branch-free (both upwind candidates are
+// formed and one is selected: identical bits to the branching dialect code, no warp
+// divergence on the sign of the face velocity)
+__device__ __forceinline__ double minmod_sel(double a, double b) {
+  const double m = fabs(a) < fabs(b) ? a : b;
+  return (a * b <= 0.0) ? 0.0 : m;
+}
+__device__ __forceinline__ double face_flux_sel(int64_t f, int64_t n, double vel, double tm1,
+                                                double t0, double tp1, double tp2) {
+  const double d0 = t0 - tm1, d1 = tp1 - t0, d2 = tp2 - tp1;
+  const double sp = (f == 1) ? 0.0 : minmod_sel(d0, d1);
+  const double sm = (f + 1 == n) ? 0.0 : minmod_sel(d1, d2);
+  const double fp = vel * (t0 + 0.5 * sp);
+  const double fm = vel * (tp1 - 0.5 * sm);
+  const double fv = vel >= 0.0 ? fp : fm;
+  return (f == 0 || f == n) ? 0.0 : fv;
+}
+
+struct StepTmemArgs {
+  DynIn in;
+  DynOut out;
+  Grid3 g;
+  int nz;
+  int64_t nj;
+  int64_t row_lo, row_hi;
+  DynConst c;
+  Span sp;
+};
+
+__global__ void __launch_bounds__(kThreads, 2) k_dyn_step_tmem(StepTmemArgs a) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ uint32_t tmem_base_slot;
+  double* ring = smem;
+  double* ps_s = smem + kFStages * kFStageDoubles;
+
+  const int lane = threadIdx.x, warp = threadIdx.y;
+  const int t = warp * kTX + lane;
+  const int64_t i0 = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * kTX;
+  const int64_t j0 = a.sp.jlo + static_cast<int64_t>(blockIdx.y) * kTY;
+  const int64_t i = i0 + lane, j = j0 + warp;
+  const bool active = i <= a.sp.ihi && j <= a.sp.jhi;
+  const int nz = a.nz;
+  const int64_t P = a.g.plane, W = a.g.pitch;
+  const DynConst& c = a.c;
+  const int64_t gi = i + a.sp.i0, gj = j + a.sp.j0, gnx = a.sp.gnx, gny = a.sp.gny;
+
+  if (warp == 0) sm100::tmem_alloc(&tmem_base_slot, kTmemCols);
+  sm100::tmem_fence_before();
+  __syncthreads();
+  sm100::tmem_fence_after();
+  const uint32_t tmem = tmem_base_slot + (static_cast<uint32_t>(32 * warp) << 16);
+
+  const double* src[kFChunksPerThread];
+  uint32_t dst[kFChunksPerThread];
+  bool ok[kFChunksPerThread];
+  const uint32_t ring_u32 = sm100::smem_u32(ring);
+#pragma unroll
+  for (int q = 0; q < kFChunksPerThread; ++q) {
+    const int ch = t + q * kThreads;
+    ok[q] = false;
+    src[q] = a.in.p;
+    dst[q] = 0;
+    if (ch >= kFChunks) continue;
+    const int e = ch * 2;
+    const double* base;
+    int64_t row, col;  // 0-based local (j', i') of the chunk start
+    if (e < kFOffU) {
+      base = a.in.th; row = (j0 - 3) + e / kFThW; col = (i0 - 3) + e % kFThW;
+    } else if (e < kFOffV) {
+      base = a.in.u; row = (j0 - 1) + (e - kFOffU) / kUW; col = (i0 - 3) + (e - kFOffU) % kUW;
+    } else if (e < kFOffW) {
+      base = a.in.v; row = (j0 - 2) + (e - kFOffV) / kVW; col = (i0 - 1) + (e - kFOffV) % kVW;
+    } else if (e < kFOffP) {
+      base = a.in.w; row = (j0 - 1) + (e - kFOffW) / kSW; col = (i0 - 1) + (e - kFOffW) % kSW;
+    } else if (e < kFOffRho) {
+      base = a.in.p; row = (j0 - 2) + (e - kFOffP) / kPW; col = (i0 - 3) + (e - kFOffP) % kPW;
+    } else {
+      base = a.in.rho; row = (j0 - 1) + (e - kFOffRho) / kSW; col = (i0 - 1) + (e - kFOffRho) % kSW;
+    }
+    ok[q] = row >= -kHalo && row <= a.nj - 1 + kHalo && col >= a.row_lo && col + 1 <= a.row_hi;
+    src[q] = base + row * W + col;
+    dst[q] = ring_u32 + static_cast<uint32_t>(e) * 8u;
+  }
+  auto issue = [&](int k) {
+    if (k < nz) {
+      const uint32_t so = static_cast<uint32_t>((k % kFStages) * kFStageDoubles * 8);
+      const int64_t go = static_cast<int64_t>(k) * P;
+#pragma unroll
+      for (int q = 0; q < kFChunksPerThread; ++q)
+        if (ok[q]) sm100::cp_async16(dst[q] + so, src[q] + go);
+    }
+    sm100::cp_async_commit();
+  };
+
+  const int64_t col = (j - 1) * W + (i - 1);
+  double* thn = a.out.th + col;
+  double* un = a.out.u + col;
+  double* vn = a.out.v + col;
+  double* wn = a.out.w + col;
+  double* pn = a.out.p + col;
+  const bool east = gi == gnx, west = gi == 1, north = gj == gny, south = gj == 1;
+  const int thc = (warp + 2) * kFThW + (lane + 2);  // this column inside a th plane tile
+
+#pragma unroll 1
+  for (int k = 0; k < kFStages - 1; ++k) issue(k);
+
+  double rho_prev = 0.0, th_prev = 0.0, ps_prev = 0.0, w_prev = 0.0, cp_prev = 0.0,
+         dp_prev = 0.0, fz_prev = 0.0;
+#pragma unroll 1
+  for (int k = 0; k < nz; ++k) {  // 0-based level; dialect level kk = k + 1
+    issue(k + kFStages - 1);
+    sm100::cp_async_wait<kFStages - 4>();  // levels <= k+2 have landed (own copies)
+    __syncthreads();                       // ... and everyone else's
+    const int kk = k + 1;
+    const double* S = ring + (k % kFStages) * kFStageDoubles;
+    const double* T0 = S + kFOffTh + thc;
+    const double tk = T0[0];
+    const double tkp1 = (kk + 1 <= nz) ? ring[((k + 1) % kFStages) * kFStageDoubles + kFOffTh + thc] : 0.0;
+    const double tkp2 = (kk + 2 <= nz) ? ring[((k + 2) % kFStages) * kFStageDoubles + kFOffTh + thc] : 0.0;
+    const double xm2 = T0[-2], xm1 = T0[-1], xp1 = T0[1], xp2 = T0[2];
+    const double ym2 = T0[-2 * kFThW], ym1 = T0[-kFThW], yp1 = T0[kFThW], yp2 = T0[2 * kFThW];
+    const double* Up = S + kFOffU + warp * kUW + (lane + 2);
+    const double ui = Up[0], uim1 = Up[-1];
+    const double* Vp = S + kFOffV + (warp + 1) * kVW + lane;
+    const double vj = Vp[0], vjm1 = Vp[-kVW];
+    const double wk = S[kFOffW + warp * kSW + lane];
+    const double* Pp = S + kFOffP + (warp + 1) * kPW + (lane + 2);
+    const double pk = Pp[0], pe = Pp[1], pw = Pp[-1], pnn = Pp[kPW], psth = Pp[-kPW];
+    const double rhok = S[kFOffRho + warp * kSW + lane];
+
+    // ---- advection (regions 1-4) --------------------------------------------------
+    const double fzk = face_flux_sel(kk, nz, wk, th_prev, tk, tkp1, tkp2);
+    const double fxe = face_flux_sel(gi, gnx, ui, xm1, tk, xp1, xp2);
+    const double fxw = face_flux_sel(gi - 1, gnx, uim1, xm2, xm1, tk, xp1);
+    const double fyn = face_flux_sel(gj, gny, vj, ym1, tk, yp1, yp2);
+    const double fys = face_flux_sel(gj - 1, gny, vjm1, ym2, ym1, tk, yp1);
+    const double ue = east ? 0.0 : ui;
+    const double uwf = west ? 0.0 : uim1;
+    const double vnf = north ? 0.0 : vj;
+    const double vsf = south ? 0.0 : vjm1;
+    const double wt = (kk == nz) ? 0.0 : wk;
+    const double wb = (kk == 1) ? 0.0 : w_prev;
+    double flux = c.rdx * (fxe - fxw) + c.rdy * (fyn - fys);
+    flux = flux + c.rdz * (fzk - fz_prev);
+    double div = c.rdx * (ue - uwf) + c.rdy * (vnf - vsf);
+    div = div + c.rdz * (wt - wb);
+    const double thk_new = tk - c.dt * (flux - tk * div);
+
+    // ---- pressure gradient + divergence (regions 5-6) ------------------------------
+    const double unk = east ? 0.0 : ui - c.dt_rdx * (pe - pk);
+    const double vnk = north ? 0.0 : vj - c.dt_rdy * (pnn - pk);
+    const double uw = west ? 0.0 : uim1 - c.dt_rdx * (pk - pw);
+    const double vs = south ? 0.0 : vjm1 - c.dt_rdy * (pk - psth);
+    const double psk = pk - c.dt_cs2 * (c.rdx * (unk - uw) + c.rdy * (vnk - vs));
+    if (active) {
+      const int64_t o = static_cast<int64_t>(k) * P;
+      thn[o] = thk_new;
+      un[o] = unk;
+      vn[o] = vnk;
+    }
+    ps_s[k * kThreads + t] = psk;
+    // ---- HE-VI forward elimination (region 7) --------------------------------------
+    if (k >= 1) {
+      const int f = k - 1;
+      const double rf = 0.5 * (rho_prev + rhok);
+      const double beta = c.beta_num / rf;
+      double dd = w_prev - c.dt_rdz * (psk - ps_prev) / rf;
+      dd = dd + c.dt_grav * (0.5 * (th_prev + tk) - c.th0) / c.th0;
+      const double bb = 1.0 + 2.0 * beta;
+      double cpk, dpk;
+      if (f == 0) {
+        cpk = -beta / bb;
+        dpk = dd / bb;
+      } else {
+        const double m = bb + beta * cp_prev;
+        cpk = -beta / m;
+        dpk = (dd + beta * dp_prev) / m;
+      }
+      sm100::tmem_st_f64(tmem + 2 * f, cpk);
+      sm100::tmem_st_f64(tmem + kDpCol + 2 * f, dpk);
+      cp_prev = cpk;
+      dp_prev = dpk;
+    }
+    rho_prev = rhok;
+    th_prev = tk;
+    w_prev = wk;
+    ps_prev = psk;
+    fz_prev = fzk;
+    __syncthreads();
+  }
+  sm100::cp_async_wait<0>();
+  sm100::tmem_wait_st();
+
+  // ---- back substitution + pressure update (region 7), four faces per TMEM load ----
+  if (active) wn[static_cast<int64_t>(nz - 1) * P] = 0.0;
+  double wk1 = 0.0;
+  const int nf = nz - 1;
+#pragma unroll 1
+  for (int cb = (nf - 1) / 4; cb >= 0; --cb) {
+    double cpv[4], dpv[4];
+    sm100::tmem_ld_4f64(tmem + 8 * cb, cpv);
+    sm100::tmem_ld_4f64(tmem + kDpCol + 8 * cb, dpv);
+#pragma unroll
+    for (int q = 3; q >= 0; --q) {
+      const int f = 4 * cb + q;
+      if (f >= nf) continue;
+      const double wk = (f == nf - 1) ? dpv[q] : dpv[q] - cpv[q] * wk1;
+      const double pk1 = ps_s[(f + 1) * kThreads + t] - c.dt_cs2_rdz * (wk1 - wk);
+      if (active) {
+        wn[static_cast<int64_t>(f) * P] = wk;
+        pn[static_cast<int64_t>(f + 1) * P] = pk1;
+      }
+      wk1 = wk;
+    }
+  }
+  if (active) pn[0] = ps_s[t] - c.dt_cs2_rdz * wk1;
+
+  sm100::tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) sm100::tmem_dealloc(tmem_base_slot, kTmemCols);
+}
+
+}  // namespace
+
+bool dycore_step_tmem_fits(int64_t nz) { return nz >= 2 && nz - 1 <= 64; }
+
+cudaError_t launch_dycore_step_tmem(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
+                                    int64_t nj, const DynConst& c, const Span& sp,
+                                    cudaStream_t s) {
+  if (sp.ihi < sp.ilo || sp.jhi < sp.jlo) return cudaSuccess;
+  if (!dycore_step_tmem_fits(nz)) return cudaErrorInvalidValue;
+  const size_t smem = std::max<size_t>((static_cast<size_t>(kFStages) * kFStageDoubles +
+                                        static_cast<size_t>(nz) * kThreads) * sizeof(double),
+                                       80 * 1024);
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_dyn_step_tmem,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  StepTmemArgs a{in, out, g, static_cast<int>(nz), nj, -kIOff, g.pitch - kIOff - 1, c, sp};
+  dim3 block(kTX, kTY);
+  dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
+            static_cast<unsigned>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY));
+  k_dyn_step_tmem<<<grid, block, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 }  // namespace hfb

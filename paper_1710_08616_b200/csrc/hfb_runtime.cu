@@ -231,7 +231,9 @@ struct hfb_ctx {
   cudaGraphExec_t graph_exec = nullptr;
   std::string graph_key;
   hfb_launch_stats graph_stats{};
-  bool force_generic = getenv("HFB_GENERIC_KERNELS") != nullptr;  // A/B switch
+  // A/B switches: portable kernels only / the two-kernel (advect + acoustic) split
+  bool force_generic = getenv("HFB_GENERIC_KERNELS") != nullptr;
+  bool force_split = getenv("HFB_SPLIT_STEP") != nullptr;
   // per-kernel CUDA-event timing (hfb_profile)
   bool prof = false;
   bool capturing = false;
@@ -713,15 +715,24 @@ void dycore_step(hfb_ctx* c, Stats& st) {
   DynIn in{rho.d(), th.d(), u.d(), v.d(), w.d(), p.d()};
   DynOut out{th.d_alt(), u.d_alt(), v.d_alt(), w.d_alt(), p.d_alt()};
   Span sp = full_span(c, nx, ny);
-  launch(c, st, "dycore_advect", [&] { return launch_dycore_advect(in, out.th, grid_of(th), nz, k, sp, c->stream); });
-  if (dycore_acoustic_tmem_fits(nz) && !c->force_generic)
-    launch(c, st, "dycore_acoustic", [&] {
-      return launch_dycore_acoustic_tmem(in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
+  if (dycore_step_tmem_fits(nz) && !c->force_generic && !c->force_split) {
+    launch(c, st, "dycore_step", [&] {
+      return launch_dycore_step_tmem(in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
     });
-  else
-    launch(c, st, "dycore_acoustic", [&] {
-      return launch_dycore_acoustic(in, out, grid_of(th), nz, k, sp, c->stream);
+  } else {
+    launch(c, st, "dycore_advect", [&] {
+      return launch_dycore_advect(in, out.th, grid_of(th), nz, k, sp, c->stream);
     });
+    if (dycore_acoustic_tmem_fits(nz) && !c->force_generic)
+      launch(c, st, "dycore_acoustic", [&] {
+        return launch_dycore_acoustic_tmem(in, out, grid_of(th), nz, th.lay.nj, k, sp,
+                                           c->stream);
+      });
+    else
+      launch(c, st, "dycore_acoustic", [&] {
+        return launch_dycore_acoustic(in, out, grid_of(th), nz, k, sp, c->stream);
+      });
+  }
   for (Slot* s : {&th, &u, &v, &w, &p}) s->cur = 1 - s->cur;
   // the generated code's 8 launches (dycore.h90 regions; region 1 spans i = 0..nx,
   // region 2 spans j = 0..ny)

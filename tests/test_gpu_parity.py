@@ -104,6 +104,13 @@ def test_reduction_large_tolerance():
     assert abs(scal["total"] - ref["total"]) <= 1e-12 * abs(ref["total"])
 
 
+def test_split_step_matches(monkeypatch):
+    """The two-kernel step (advect + TMEM acoustic; HFB_SPLIT_STEP=1) gives the same bits."""
+    monkeypatch.setenv("HFB_SPLIT_STEP", "1")
+    _oracle_vs_gpu(Case("dycore_70x45x58_s2", "dycore", dict(nx=70, ny=45, nz=58, nsteps=2),
+                        dict(DYCORE_SCALARS), dict(DYCORE_FILLS)))
+
+
 def test_generic_kernels_match(monkeypatch):
     """The portable acoustic kernel (HFB_GENERIC_KERNELS=1) gives the same bits."""
     monkeypatch.setenv("HFB_GENERIC_KERNELS", "1")
@@ -193,7 +200,7 @@ def test_graph_replay_matches_step_loop():
         for k in arrs:
             eng.copy_to_device(k)
         st = eng.run_graph("dycore_step", 2)
-        assert st.native_launches == 4
+        assert st.native_launches == 2  # one fused kernel per timestep
         eng.run_graph("dycore_step", 2)
         eng.run_graph("dycore_step", 2)
         for k in arrs:
