@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 
 #include "hfb_kernels.cuh"
 #include "hfb_sm100.cuh"
@@ -303,6 +305,7 @@ struct StepTmemArgs {
   DynOut out;
   Grid3 g;
   int nz;
+  int debug_skip;  // profiling experiments only: 1 = no advection, 2 = no acoustic, 3 = neither
   int64_t nj;
   int64_t row_lo, row_hi;
   DynConst c;
@@ -522,11 +525,322 @@ cudaError_t launch_dycore_step_tmem(const DynIn& in, const DynOut& out, Grid3 g,
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  StepTmemArgs a{in, out, g, static_cast<int>(nz), nj, -kIOff, g.pitch - kIOff - 1, c, sp};
+  StepTmemArgs a{in, out, g, static_cast<int>(nz), 0, nj, -kIOff, g.pitch - kIOff - 1, c, sp};
   dim3 block(kTX, kTY);
   dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
             static_cast<unsigned>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY));
   k_dyn_step_tmem<<<grid, block, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+
+// ===========================================================================
+// Warp-specialised fused timestep: the same 32 x 4 column tile and cp.async plane ring,
+// but 8 warps per CTA — warps 0-3 run the acoustic/HE-VI part (they own the TMEM lanes
+// holding the Thomas coefficients), warps 4-7 run the flux-limited advection of the same
+// four rows. The two halves share every staged plane, split the fp64 work roughly in
+// half and, with 2 CTAs per SM, double the resident warps (16) that hide the fp64
+// dependency latency (the single-role kernel is bound by `stall_wait`).
+// Tiles that touch no global boundary (all but a thin rim) take a boundary-free
+// instantiation of the level body: no wall/limiter special cases, no selects for them.
+// ===========================================================================
+namespace {
+
+constexpr int kWsThreads = 2 * kThreads;  // 256
+// ring depth: 6 planes x 8.25 KB (+ ps, nz x 1 KB, in shared memory: measured faster than
+// an L2 round trip of ps with a 10-deep ring)
+constexpr int kWsStages = 6;
+constexpr int kWsChunksPerThread = (kFChunks + kWsThreads - 1) / kWsThreads;  // 3
+
+// Limited upwind face flux with ONE minmod: the upwind side's slope pair and base value
+// are selected first. vel*(tp1 - 0.5*s) == vel*(tp1 + (-0.5)*s) bit for bit (exact
+// negation), so this equals the dialect's two-branch form. kCheck adds the wall and
+// first/last-face cases (face index f of n cells).
+template <bool kCheck>
+__device__ __forceinline__ double face_flux_up(int64_t f, int64_t n, double vel, double tm1,
+                                               double t0, double tp1, double tp2) {
+  const double d0 = t0 - tm1, d1 = tp1 - t0, d2 = tp2 - tp1;
+  const bool up = vel >= 0.0;
+  const double x = up ? d0 : d1, y = up ? d1 : d2;
+  const double m = fabs(x) < fabs(y) ? x : y;
+  double sl = (x * y <= 0.0) ? 0.0 : m;
+  if (kCheck) sl = (up ? f == 1 : f + 1 == n) ? 0.0 : sl;
+  const double base = up ? t0 : tp1;
+  const double h = up ? 0.5 : -0.5;
+  const double fv = vel * (base + h * sl);
+  if (kCheck) return (f == 0 || f == n) ? 0.0 : fv;
+  return fv;
+}
+
+__global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ uint32_t tmem_base_slot;
+  double* ring = smem;
+  double* ps_s = smem + kWsStages * kFStageDoubles;  // nz x 128 (ps of each column)
+
+  const int lane = threadIdx.x, warp = threadIdx.y;  // blockDim = (32, 8)
+  const bool acoustic = warp < kTY;
+  const int row = acoustic ? warp : warp - kTY;       // tile row served by this warp
+  const int tid = warp * kTX + lane;                  // 0..255 (copy issue)
+  const int t = row * kTX + lane;                     // 0..127 (column within the tile)
+  const int64_t i0 = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * kTX;
+  const int64_t j0 = a.sp.jlo + static_cast<int64_t>(blockIdx.y) * kTY;
+  const int64_t i = i0 + lane, j = j0 + row;
+  const bool active = i <= a.sp.ihi && j <= a.sp.jhi;
+  const int nz = a.nz;
+  const int64_t P = a.g.plane, W = a.g.pitch;
+  const DynConst& c = a.c;
+  const int64_t gi = i + a.sp.i0, gj = j + a.sp.j0, gnx = a.sp.gnx, gny = a.sp.gny;
+  // CTA-uniform: every column of the tile is >= 3 cells from every global wall
+  const int64_t gi0 = i0 + a.sp.i0, gj0 = j0 + a.sp.j0;
+  const bool interior = gi0 >= 3 && gi0 + kTX - 1 <= gnx - 2 && gj0 >= 3 &&
+                        gj0 + kTY - 1 <= gny - 2 && i0 + kTX - 1 <= a.sp.ihi &&
+                        j0 + kTY - 1 <= a.sp.jhi;
+
+  if (warp == 0) sm100::tmem_alloc(&tmem_base_slot, kTmemCols);
+  sm100::tmem_fence_before();
+  __syncthreads();
+  sm100::tmem_fence_after();
+  const uint32_t tmem = tmem_base_slot + (static_cast<uint32_t>(32 * row) << 16);
+
+  const double* src[kWsChunksPerThread];
+  uint32_t dst[kWsChunksPerThread];
+  bool ok[kWsChunksPerThread];
+  const uint32_t ring_u32 = sm100::smem_u32(ring);
+#pragma unroll
+  for (int q = 0; q < kWsChunksPerThread; ++q) {
+    const int ch = tid + q * kWsThreads;
+    ok[q] = false;
+    src[q] = a.in.p;
+    dst[q] = 0;
+    if (ch >= kFChunks) continue;
+    const int e = ch * 2;
+    const double* base;
+    int64_t r, cc;  // 0-based local (j', i') of the chunk start
+    if (e < kFOffU) {
+      base = a.in.th; r = (j0 - 3) + e / kFThW; cc = (i0 - 3) + e % kFThW;
+    } else if (e < kFOffV) {
+      base = a.in.u; r = (j0 - 1) + (e - kFOffU) / kUW; cc = (i0 - 3) + (e - kFOffU) % kUW;
+    } else if (e < kFOffW) {
+      base = a.in.v; r = (j0 - 2) + (e - kFOffV) / kVW; cc = (i0 - 1) + (e - kFOffV) % kVW;
+    } else if (e < kFOffP) {
+      base = a.in.w; r = (j0 - 1) + (e - kFOffW) / kSW; cc = (i0 - 1) + (e - kFOffW) % kSW;
+    } else if (e < kFOffRho) {
+      base = a.in.p; r = (j0 - 2) + (e - kFOffP) / kPW; cc = (i0 - 3) + (e - kFOffP) % kPW;
+    } else {
+      base = a.in.rho; r = (j0 - 1) + (e - kFOffRho) / kSW; cc = (i0 - 1) + (e - kFOffRho) % kSW;
+    }
+    ok[q] = r >= -kHalo && r <= a.nj - 1 + kHalo && cc >= a.row_lo && cc + 1 <= a.row_hi;
+    src[q] = base + r * W + cc;
+    dst[q] = ring_u32 + static_cast<uint32_t>(e) * 8u;
+  }
+  // levels are issued in order, once each: sources advance by one plane per call and the
+  // ring offset rotates (no per-level multiplies or modulo)
+  uint32_t so = 0;
+  constexpr uint32_t kStageBytes = kFStageDoubles * 8;
+  int issued = 0;
+  auto issue = [&]() {
+    if (issued < nz) {
+#pragma unroll
+      for (int q = 0; q < kWsChunksPerThread; ++q) {
+        if (ok[q]) sm100::cp_async16(dst[q] + so, src[q]);
+        src[q] += P;
+      }
+    }
+    sm100::cp_async_commit();
+    ++issued;
+    so = so == (kWsStages - 1) * kStageBytes ? 0u : so + kStageBytes;
+  };
+
+  const int64_t col = (j - 1) * W + (i - 1);
+  double* out_th = a.out.th + col;  // running pointers (advance one plane per level)
+  double* out_u = a.out.u + col;
+  double* out_v = a.out.v + col;
+  const bool east = gi == gnx, west = gi == 1, north = gj == gny, south = gj == 1;
+  const int thc = (row + 2) * kFThW + (lane + 2);
+
+#pragma unroll 1
+  for (int k = 0; k < kWsStages - 1; ++k) issue();
+
+  // role state carried along K
+  double th_prev = 0.0, w_prev = 0.0;              // both roles
+  double rho_prev = 0.0, ps_prev = 0.0, cp_prev = 0.0, dp_prev = 0.0;  // acoustic
+  double fz_prev = 0.0;                            // advection
+  double pend_beta = 0.0, pend_bb = 1.0, pend_dd = 0.0;  // face awaiting its recursion step
+  int s0 = 0;  // ring slot of level k
+
+  // Thomas forward recursion for face f (dialect face kf = f + 1) from the pending
+  // coefficients; cp/dp go to this thread's TMEM lane
+  auto thomas_step = [&](int f) {
+    double cpk, dpk;
+    if (f == 0) {
+      cpk = -pend_beta / pend_bb;
+      dpk = pend_dd / pend_bb;
+    } else {
+      const double m = pend_bb + pend_beta * cp_prev;
+      cpk = -pend_beta / m;
+      dpk = (pend_dd + pend_beta * dp_prev) / m;
+    }
+    sm100::tmem_st_f64(tmem + 2 * f, cpk);
+    sm100::tmem_st_f64(tmem + kDpCol + 2 * f, dpk);
+    cp_prev = cpk;
+    dp_prev = dpk;
+  };
+
+  auto level = [&](int k, auto interior_tag) {
+    constexpr bool kIn = decltype(interior_tag)::value;
+    const int kk = k + 1;
+    const int s1 = s0 == kWsStages - 1 ? 0 : s0 + 1;
+    const int s2 = s1 == kWsStages - 1 ? 0 : s1 + 1;
+    const double* S = ring + s0 * kFStageDoubles;
+    const double tk = S[kFOffTh + thc];
+    const double* Up = S + kFOffU + row * kUW + (lane + 2);
+    const double ui = Up[0], uim1 = Up[-1];
+    const double* Vp = S + kFOffV + (row + 1) * kVW + lane;
+    const double vj = Vp[0], vjm1 = Vp[-kVW];
+    const double wk = S[kFOffW + row * kSW + lane];
+    if (acoustic && (a.debug_skip & 2) == 0) {
+      const double* Pp = S + kFOffP + (row + 1) * kPW + (lane + 2);
+      const double pk = Pp[0], pe = Pp[1], pw = Pp[-1], pnn = Pp[kPW], psth = Pp[-kPW];
+      const double rhok = S[kFOffRho + row * kSW + lane];
+      const double unk0 = ui - c.dt_rdx * (pe - pk);
+      const double vnk0 = vj - c.dt_rdy * (pnn - pk);
+      const double uw0 = uim1 - c.dt_rdx * (pk - pw);
+      const double vs0 = vjm1 - c.dt_rdy * (pk - psth);
+      const double unk = (!kIn && east) ? 0.0 : unk0;
+      const double vnk = (!kIn && north) ? 0.0 : vnk0;
+      const double uw = (!kIn && west) ? 0.0 : uw0;
+      const double vs = (!kIn && south) ? 0.0 : vs0;
+      const double psk = pk - c.dt_cs2 * (c.rdx * (unk - uw) + c.rdy * (vnk - vs));
+      if (kIn || active) {
+        *out_u = unk;
+        *out_v = vnk;
+      }
+      ps_s[k * kThreads + t] = psk;
+      // The Thomas recursion for face f = k-2 (its coefficients were formed in the
+      // previous iteration) runs here, independent of this iteration's coefficient
+      // formation for face k-1: the two division chains overlap instead of adding up.
+      if (k >= 2) thomas_step(k - 2);
+      if (k >= 1) {
+        const double rf = 0.5 * (rho_prev + rhok);
+        const double beta = c.beta_num / rf;
+        double dd = w_prev - c.dt_rdz * (psk - ps_prev) / rf;
+        dd = dd + c.dt_grav * (0.5 * (th_prev + tk) - c.th0) / c.th0;
+        pend_beta = beta;
+        pend_bb = 1.0 + 2.0 * beta;
+        pend_dd = dd;
+      }
+      rho_prev = rhok;
+      ps_prev = psk;
+    } else if (!acoustic && (a.debug_skip & 1) == 0) {
+      const double* T0 = S + kFOffTh + thc;
+      const double tkp1 = (kk + 1 <= nz) ? ring[s1 * kFStageDoubles + kFOffTh + thc] : 0.0;
+      const double tkp2 = (kk + 2 <= nz) ? ring[s2 * kFStageDoubles + kFOffTh + thc] : 0.0;
+      const double xm2 = T0[-2], xm1 = T0[-1], xp1 = T0[1], xp2 = T0[2];
+      const double ym2 = T0[-2 * kFThW], ym1 = T0[-kFThW], yp1 = T0[kFThW], yp2 = T0[2 * kFThW];
+      const double fzk = face_flux_up<true>(kk, nz, wk, th_prev, tk, tkp1, tkp2);
+      const double fxe = face_flux_up<!kIn>(gi, gnx, ui, xm1, tk, xp1, xp2);
+      const double fxw = face_flux_up<!kIn>(gi - 1, gnx, uim1, xm2, xm1, tk, xp1);
+      const double fyn = face_flux_up<!kIn>(gj, gny, vj, ym1, tk, yp1, yp2);
+      const double fys = face_flux_up<!kIn>(gj - 1, gny, vjm1, ym2, ym1, tk, yp1);
+      const double ue = (!kIn && east) ? 0.0 : ui;
+      const double uwf = (!kIn && west) ? 0.0 : uim1;
+      const double vnf = (!kIn && north) ? 0.0 : vj;
+      const double vsf = (!kIn && south) ? 0.0 : vjm1;
+      const double wt = (kk == nz) ? 0.0 : wk;
+      const double wb = (kk == 1) ? 0.0 : w_prev;
+      double flux = c.rdx * (fxe - fxw) + c.rdy * (fyn - fys);
+      flux = flux + c.rdz * (fzk - fz_prev);
+      double div = c.rdx * (ue - uwf) + c.rdy * (vnf - vsf);
+      div = div + c.rdz * (wt - wb);
+      if (kIn || active) *out_th = tk - c.dt * (flux - tk * div);
+      fz_prev = fzk;
+    }
+    th_prev = tk;
+    w_prev = wk;
+    s0 = s1;
+    out_th += P;
+    out_u += P;
+    out_v += P;
+  };
+
+#pragma unroll 1
+  for (int k = 0; k < nz; ++k) {
+    // levels <= k+2 have landed (own copies; issued up to k+kWsStages-2) ...
+    sm100::cp_async_wait<kWsStages - 4>();
+    // ... and everyone else's; every warp has also finished level k-1, so its slot
+    // can be refilled now (one barrier per level)
+    __syncthreads();
+    issue();
+    if (interior)
+      level(k, std::true_type{});
+    else
+      level(k, std::false_type{});
+  }
+  if (acoustic && nz >= 2) thomas_step(nz - 2);  // drain the last face
+  sm100::cp_async_wait<0>();
+
+  if (acoustic) {
+    sm100::tmem_wait_st();
+    double* wn = a.out.w + col + static_cast<int64_t>(nz - 1) * P;  // running pointers
+    double* pn = a.out.p + col + static_cast<int64_t>(nz - 1) * P;
+    if (active) *wn = 0.0;
+    double wk1 = 0.0;
+    const int nf = nz - 1;
+    const double* psp = ps_s + (nz - 1) * kThreads + t;  // ps(f+1)
+#pragma unroll 1
+    for (int cb = (nf - 1) / 4; cb >= 0; --cb) {
+      double cpv[4], dpv[4];
+      sm100::tmem_ld_4f64(tmem + 8 * cb, cpv);
+      sm100::tmem_ld_4f64(tmem + kDpCol + 8 * cb, dpv);
+#pragma unroll
+      for (int q = 3; q >= 0; --q) {
+        const int f = 4 * cb + q;
+        if (f >= nf) continue;
+        wn -= P;
+        const double wkk = (f == nf - 1) ? dpv[q] : dpv[q] - cpv[q] * wk1;
+        const double pk1 = *psp - c.dt_cs2_rdz * (wk1 - wkk);
+        if (active) {
+          *wn = wkk;
+          *pn = pk1;
+        }
+        pn -= P;
+        psp -= kThreads;
+        wk1 = wkk;
+      }
+    }
+    if (active) *pn = *psp - c.dt_cs2_rdz * wk1;
+  }
+  sm100::tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) sm100::tmem_dealloc(tmem_base_slot, kTmemCols);
+}
+
+}  // namespace
+
+cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
+                                  int64_t nj, const DynConst& c, const Span& sp,
+                                  cudaStream_t s) {
+  if (sp.ihi < sp.ilo || sp.jhi < sp.jlo) return cudaSuccess;
+  if (!dycore_step_tmem_fits(nz)) return cudaErrorInvalidValue;
+  const size_t smem = std::max<size_t>((static_cast<size_t>(kWsStages) * kFStageDoubles +
+                                        static_cast<size_t>(nz) * kThreads) * sizeof(double),
+                                       80 * 1024);
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_dyn_step_ws,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  static const int debug_skip = getenv("HFB_DEBUG_SKIP") ? atoi(getenv("HFB_DEBUG_SKIP")) : 0;
+  StepTmemArgs a{in, out, g, static_cast<int>(nz), debug_skip, nj, -kIOff, g.pitch - kIOff - 1,
+                 c, sp};
+  dim3 block(kTX, 2 * kTY);
+  dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
+            static_cast<unsigned>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY));
+  k_dyn_step_ws<<<grid, block, smem, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -87,6 +87,10 @@ bool dycore_step_tmem_fits(int64_t nz);
 cudaError_t launch_dycore_step_tmem(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                     int64_t nj, const DynConst& c, const Span& sp,
                                     cudaStream_t s);
+// warp-specialised variant (acoustic warps + advection warps per tile)
+cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
+                                  int64_t nj, const DynConst& c, const Span& sp,
+                                  cudaStream_t s);
 
 // ---- halo pack/unpack for the 2-D decomposition -------------------------------------
 cudaError_t launch_pack_box(const double* field, double* buf, Grid3 g, int64_t nk,

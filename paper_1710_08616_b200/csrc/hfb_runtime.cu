@@ -234,6 +234,7 @@ struct hfb_ctx {
   // A/B switches: portable kernels only / the two-kernel (advect + acoustic) split
   bool force_generic = getenv("HFB_GENERIC_KERNELS") != nullptr;
   bool force_split = getenv("HFB_SPLIT_STEP") != nullptr;
+  bool force_single_role = getenv("HFB_SINGLE_ROLE") != nullptr;
   // per-kernel CUDA-event timing (hfb_profile)
   bool prof = false;
   bool capturing = false;
@@ -716,9 +717,14 @@ void dycore_step(hfb_ctx* c, Stats& st) {
   DynOut out{th.d_alt(), u.d_alt(), v.d_alt(), w.d_alt(), p.d_alt()};
   Span sp = full_span(c, nx, ny);
   if (dycore_step_tmem_fits(nz) && !c->force_generic && !c->force_split) {
-    launch(c, st, "dycore_step", [&] {
-      return launch_dycore_step_tmem(in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
-    });
+    if (c->force_single_role)
+      launch(c, st, "dycore_step", [&] {
+        return launch_dycore_step_tmem(in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
+      });
+    else
+      launch(c, st, "dycore_step", [&] {
+        return launch_dycore_step_ws(in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
+      });
   } else {
     launch(c, st, "dycore_advect", [&] {
       return launch_dycore_advect(in, out.th, grid_of(th), nz, k, sp, c->stream);

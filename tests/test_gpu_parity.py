@@ -111,6 +111,13 @@ def test_split_step_matches(monkeypatch):
                         dict(DYCORE_SCALARS), dict(DYCORE_FILLS)))
 
 
+def test_single_role_fused_matches(monkeypatch):
+    """The single-role fused kernel (HFB_SINGLE_ROLE=1) gives the same bits."""
+    monkeypatch.setenv("HFB_SINGLE_ROLE", "1")
+    _oracle_vs_gpu(Case("dycore_70x45x58_s2", "dycore", dict(nx=70, ny=45, nz=58, nsteps=2),
+                        dict(DYCORE_SCALARS), dict(DYCORE_FILLS)))
+
+
 def test_generic_kernels_match(monkeypatch):
     """The portable acoustic kernel (HFB_GENERIC_KERNELS=1) gives the same bits."""
     monkeypatch.setenv("HFB_GENERIC_KERNELS", "1")

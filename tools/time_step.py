@@ -1,0 +1,34 @@
+#!/usr/bin/env python3
+"""ms per dycore step (CUDA events on the engine stream) for quick A/B experiments."""
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import torch  # noqa: E402
+
+import paper_1710_08616_b200 as hfb  # noqa: E402
+from paper_1710_08616_b200 import synthetic  # noqa: E402
+
+nx, ny, nz = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (512, 512, 58)))
+eng = hfb.Engine("dycore")
+for k, v in dict(nx=nx, ny=ny, nz=nz, nsteps=1).items():
+    eng.set(k, v)
+for k, v in synthetic.DYCORE_SCALARS.items():
+    eng.set(k, v)
+arrs = {k: synthetic.field((nz, nx, ny), *v, order="F") for k, v in synthetic.DYCORE_FILLS.items()}
+for k, a in arrs.items():
+    eng.bind(k, a)
+    eng.copy_to_device(k)
+s = torch.cuda.ExternalStream(eng.stream)
+for _ in range(5):
+    eng.enqueue("dycore_step")
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+n = 40
+e0.record(s)
+for _ in range(n):
+    eng.enqueue("dycore_step")
+e1.record(s)
+eng.synchronize()
+ms = e0.elapsed_time(e1) / n
+print(f"{nx}x{ny}x{nz}: {ms:.4f} ms/step  {nx*ny*nz/ms/1e6:.3e} pt/s  {88*nx*ny*nz/ms/1e6:.0f} GB/s(alg)")
