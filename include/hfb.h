@@ -180,8 +180,18 @@ hfb_status hfb_decomp_faces(const hfb_decomp* d, int32_t side, int64_t send_box[
                             int64_t recv_box[4]);
 /* Attach a decomposition to a context: kernels then test boundaries on GLOBAL
  * indices and stencil entries exchange halos before each stencil launch.
- * `nccl_id` is the 128-byte ncclUniqueId shared by all ranks (NULL with px*py == 1). */
+ * `nccl_id` is the 128-byte ncclUniqueId shared by all ranks (one process per rank), or
+ * NULL when the rank will join an in-process group (hfb_group_create). */
 hfb_status hfb_set_decomposition(hfb_ctx* ctx, const hfb_decomp* d, const void* nccl_id);
+/* In-process rank group: contexts (ranks 0..n-1 of one decomposition, set with a NULL
+ * NCCL id) driven by one host thread, halos pulled by device-to-device copies. Runs the
+ * decomposed path without NCCL, e.g. several tiles on one GPU. hfb_group_run executes
+ * `entry` on every rank in lockstep (main/simulation_run: copy-in on all ranks, nsteps x
+ * step on every rank, copy-out). */
+typedef struct hfb_group hfb_group;
+hfb_status hfb_group_create(hfb_ctx* const* ctxs, int n, hfb_group** out);
+void hfb_group_destroy(hfb_group* group);
+hfb_status hfb_group_run(hfb_group* group, const char* entry, hfb_launch_stats* stats);
 /* halo bytes moved by this context so far (for NVLink accounting) */
 int64_t hfb_halo_bytes(hfb_ctx* ctx);
 /* 128-byte ncclUniqueId for hfb_set_decomposition (rank 0 creates, all ranks share) */

@@ -3,8 +3,8 @@
 The product is libhfb.so (CUDA sm_100a kernels + the C ABI of include/hfb.h);
 this package is the Python host mirror of the reference executor's interface.
 """
-from .runtime import (EXPORTS, Engine, HfbError, LaunchStats, MODULES, build, decomp_faces,
+from .runtime import (EXPORTS, Engine, Group, HfbError, LaunchStats, MODULES, build, decomp_faces,
                       decomp_init, lib, run_gpu)
 
-__all__ = ["Engine", "HfbError", "LaunchStats", "MODULES", "EXPORTS", "build", "lib", "run_gpu",
+__all__ = ["Engine", "Group", "HfbError", "LaunchStats", "MODULES", "EXPORTS", "build", "lib", "run_gpu",
            "decomp_init", "decomp_faces"]

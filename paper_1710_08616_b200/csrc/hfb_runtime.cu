@@ -208,6 +208,10 @@ struct Slot {
 
 }  // namespace
 
+struct hfb_group {
+  std::vector<hfb_ctx*> ranks;
+};
+
 struct hfb_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -221,6 +225,12 @@ struct hfb_ctx {
   double* red_host = nullptr;
   hfb_decomp decomp{};
   bool decomposed = false;
+  // in-process rank group (all ranks' contexts driven by one host thread; halos are
+  // pulled by device copies instead of NCCL): used to exercise the decomposed path
+  // bit-for-bit on a single GPU
+  struct hfb_group* group = nullptr;
+  int64_t steps_done = 0;    // per-step entries completed (pull-side buffer selection)
+  double red_local = 0.0;    // this rank's partial of a group reduction
   int64_t halo_bytes = 0;
   // NCCL (multi-process decomposition)
   void* nccl_comm = nullptr;
@@ -670,16 +680,21 @@ void reduction_kernel(hfb_ctx* c, Stats& st) {
   }
   Span sp = full_span(c, nx, ny);
   bool multi = c->decomposed && c->decomp.px * c->decomp.py > 1;
+  bool local_group = multi && c->group != nullptr;
   launch(c, st, "grid_total", [&] { return launch_grid_sum(y.d(), grid_of(y), nz, sp, c->red_partials, c->red_result,
                            multi ? 0.0 : total, c->stream); }, 2);
-  if (multi) allreduce_sum(c, c->red_result);
+  if (multi && !local_group) allreduce_sum(c, c->red_result);
   cuda_check(cudaMemcpyAsync(c->red_host, c->red_result, sizeof(double), cudaMemcpyDeviceToHost,
                              c->stream),
              "cudaMemcpyAsync(total)");
   cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
   Scalar& tot = c->scalars["total"];
-  tot.r = multi ? total + *c->red_host : *c->red_host;
-  tot.init = true;
+  if (local_group) {
+    c->red_local = *c->red_host;  // combined in rank order by hfb_group_run
+  } else {
+    tot.r = multi ? total + *c->red_host : *c->red_host;
+    tot.init = true;
+  }
   // acc kernels: one virtual launch over the (j, i) iteration space (interp.cpp:1080-1114)
   st.launches += 1;
   st.threads += nx * ny;
@@ -706,6 +721,9 @@ void reduction_entry(hfb_ctx* c, const std::string& r, Stats& st) {
 void dycore_step(hfb_ctx* c, Stats& st) {
   int64_t nx = ival(c, "nx"), ny = ival(c, "ny"), nz = ival(c, "nz");
   if (nz < 2) fail(HFB_RUNTIME, "dycore_step needs nz >= 2 (got %lld)", (long long)nz);
+  if (c->decomposed && c->decomp.px * c->decomp.py > 1 && c->decomp.halo < 2)
+    fail(HFB_CONFIG, "dycore_step needs a halo of 2 cells (limited advection), got %d",
+         c->decomp.halo);
   DynConst k = make_dyn_const(rval(c, "dt"), rval(c, "rdx"), rval(c, "rdy"), rval(c, "rdz"),
                               rval(c, "cs2"), rval(c, "grav"), rval(c, "th0"));
   for (const char* n : {"th", "u", "v", "w", "p", "rho"}) dev_read(c, n);
@@ -843,8 +861,14 @@ constexpr int kNcclSum = 0;
 
 // Two-phase halo update of `fields` (all share one layout): east/west faces first,
 // then north/south faces spanning the I halo so corners arrive too.
+void group_pull(hfb_ctx* c, const std::vector<const char*>& fields);
+
 void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width) {
   if (!c->decomposed || c->decomp.px * c->decomp.py <= 1) return;
+  if (c->group) {
+    group_pull(c, fields);
+    return;
+  }
   if (!c->nccl_comm) fail(HFB_CONFIG, "decomposed context without a communicator");
   (void)width;  // the face boxes always carry the full halo ring (kHalo)
   NcclApi& api = nccl();
@@ -914,6 +938,54 @@ void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width
       }
       c->halo_bytes += static_cast<int64_t>(2 * count[s] * sizeof(double));
     }
+  }
+}
+
+// In-process group: fill this rank's halo ring from the neighbours' interiors by device
+// copies (pack into a staging buffer on this stream, unpack into the halo). A neighbour
+// that already finished this step has flipped its double buffers; its previous state
+// is then the other buffer (untouched until its next step).
+void group_pull(hfb_ctx* c, const std::vector<const char*>& fields) {
+  const hfb_decomp& d = c->decomp;
+  const int nbr[4] = {d.west, d.east, d.south, d.north};
+  const int opposite[4] = {1, 0, 3, 2};
+  for (int phase = 0; phase < 2; ++phase) {
+    for (int s = 2 * phase; s < 2 * phase + 2; ++s) {
+      if (nbr[s] < 0) continue;
+      hfb_ctx* n = c->group->ranks[nbr[s]];
+      int64_t my_send[4], my_recv[4], n_send[4], n_recv[4];
+      hfb_decomp_faces(&d, s, my_send, my_recv);
+      hfb_decomp_faces(&n->decomp, opposite[s], n_send, n_recv);
+      for (const char* f : fields) {
+        Slot& mine = slot(c, f);
+        Slot& theirs = slot(n, f);
+        if (!theirs.has_device) fail(HFB_RESIDENCY, "rank %d has no device copy of '%s'", nbr[s], f);
+        const bool advanced = n->steps_done > c->steps_done;
+        const double* src = (advanced && theirs.decl->pingpong && theirs.dev[1])
+                                ? theirs.d_alt()
+                                : theirs.d();
+        const int64_t fk = mine.lay.nk * mine.lay.nl;
+        const size_t cnt = static_cast<size_t>((n_send[1] - n_send[0] + 1) *
+                                               (n_send[3] - n_send[2] + 1) * fk);
+        if (cnt == 0) continue;
+        if (c->halo_cap < cnt) {
+          if (c->halo_send) cudaFree(c->halo_send);
+          if (c->halo_recv) cudaFree(c->halo_recv);
+          cuda_check(cudaMalloc(&c->halo_send, cnt * sizeof(double)), "cudaMalloc(halo)");
+          cuda_check(cudaMalloc(&c->halo_recv, cnt * sizeof(double)), "cudaMalloc(halo)");
+          c->halo_cap = cnt;
+        }
+        cuda_check(launch_pack_box(src, c->halo_send, grid_of(theirs), fk, n_send, true,
+                                   c->stream),
+                   "group halo pack");
+        cuda_check(launch_pack_box(mine.d(), c->halo_send, grid_of(mine), fk, my_recv, false,
+                                   c->stream),
+                   "group halo unpack");
+        c->halo_bytes += static_cast<int64_t>(cnt * sizeof(double));
+      }
+    }
+    // the second phase reads the neighbours' I halos (corners): finish phase one everywhere
+    cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
   }
 }
 
@@ -1422,8 +1494,7 @@ hfb_status hfb_set_decomposition(hfb_ctx* c, const hfb_decomp* d, const void* nc
     if (st != HFB_OK) fail(st, "%s", g_last_error.c_str());
     c->decomp = dd;
     c->decomposed = true;
-    if (dd.px * dd.py > 1) {
-      if (!nccl_id) fail(HFB_CONFIG, "a multi-rank decomposition needs the NCCL unique id");
+    if (dd.px * dd.py > 1 && nccl_id) {  // NULL: the rank joins an in-process group
       cudaSetDevice(c->device);
       NcclApi& api = nccl();
       (void)api;
@@ -1437,6 +1508,114 @@ hfb_status hfb_set_decomposition(hfb_ctx* c, const hfb_decomp* d, const void* nc
 }
 
 int64_t hfb_halo_bytes(hfb_ctx* c) { return c ? c->halo_bytes : 0; }
+
+hfb_status hfb_group_create(hfb_ctx* const* ctxs, int n, hfb_group** out) {
+  return guarded([&] {
+    if (!ctxs || n < 1 || !out) fail(HFB_CONFIG, "bad group arguments");
+    auto g = std::make_unique<hfb_group>();
+    for (int r = 0; r < n; ++r) {
+      hfb_ctx* c = ctxs[r];
+      if (!c || !c->app) fail(HFB_CONFIG, "rank %d has no program", r);
+      if (!c->decomposed || c->decomp.rank != r || c->decomp.px * c->decomp.py != n)
+        fail(HFB_CONFIG, "rank %d: decomposition rank/size does not match the group", r);
+      if (c->app != ctxs[0]->app) fail(HFB_CONFIG, "ranks run different programs");
+      if (c->group) fail(HFB_CONFIG, "rank %d already belongs to a group", r);
+      g->ranks.push_back(c);
+    }
+    for (hfb_ctx* c : g->ranks) {
+      c->group = g.get();
+      c->steps_done = 0;
+    }
+    *out = g.release();
+  });
+}
+
+void hfb_group_destroy(hfb_group* g) {
+  if (!g) return;
+  for (hfb_ctx* c : g->ranks) c->group = nullptr;
+  delete g;
+}
+
+// Lockstep execution of one entry on every rank of an in-process group. Per-step
+// entries run rank by rank (each pulls its halos first); `main`/`simulation_run` are
+// unrolled into copy-in on all ranks, nsteps x (step on every rank), copy-out.
+hfb_status hfb_group_run(hfb_group* g, const char* entry, hfb_launch_stats* stats) {
+  return guarded([&] {
+    if (!g || g->ranks.empty()) fail(HFB_CONFIG, "empty group");
+    std::string r = routine_name(entry);
+    const std::string& app = g->ranks[0]->app->app;
+    Stats st;
+    auto each = [&](const std::function<void(hfb_ctx*)>& f) {
+      for (hfb_ctx* c : g->ranks) {
+        cudaSetDevice(c->device);
+        f(c);
+        cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+      }
+    };
+    const bool outer = r == "main" || r == "simulation_run";
+    std::vector<std::string> transfers;
+    std::string step;
+    if (app == "dycore") {
+      transfers = {"p", "rho", "th", "u", "v", "w"};
+      step = "dycore_step";
+    } else if (app == "diffusion") {
+      transfers = {"t_new", "t_old"};
+      step = "diffuse_step";
+    } else if (app == "bounded") {
+      transfers = {"a", "b"};
+      step = "interior_update";
+    } else if (app == "damping") {
+      transfers = {"dens_ptb_bnd", "dens_ptb_damp", "dens_ref_f"};
+      step = "lateral_and_upper_damping";
+    } else if (app == "surface_flux") {
+      transfers = {"cover_frac", "flx_sum_x", "flx_sum_y", "wind_speed"};
+      step = "physics_run";
+    } else if (app == "reduction") {
+      transfers = {"y"};
+      step = "grid_total";
+    }
+    if (outer && app == "surface_flux" && r == "main")
+      fail(HFB_CONFIG, "group runs of surface_flux start at simulation_run");
+    if (!outer) step = r;
+    int64_t nsteps = 1;
+    if (outer && (app == "dycore" || app == "diffusion")) nsteps = ival(g->ranks[0], "nsteps");
+    if (outer) each([&](hfb_ctx* c) {
+      for (const std::string& n : transfers) do_copy_to_device(c, slot(c, n.c_str()));
+      if (app == "reduction") {
+        c->scalars["total"].r = 0.0;
+        c->scalars["total"].init = true;
+      }
+    });
+    double total0 = app == "reduction" ? rval(g->ranks[0], "total") : 0.0;
+    for (int64_t s = 0; s < nsteps; ++s) {
+      each([&](hfb_ctx* c) {
+        Stats local;
+        if (app == "diffusion" && step == "diffuse_step")
+          diffusion_step(c, local, !outer || s == nsteps - 1);
+        else
+          entry_fn(app)(c, step, local);
+        if (c == g->ranks[0]) st = Stats{st.launches + local.launches, st.threads + local.threads,
+                                         st.guard_returns + local.guard_returns,
+                                         st.native + local.native};
+        else
+          st.native += local.native;
+      });
+      for (hfb_ctx* c : g->ranks) c->steps_done += 1;
+    }
+    if (app == "reduction") {
+      double sum = 0.0;
+      for (hfb_ctx* c : g->ranks) sum += c->red_local;  // rank order: deterministic
+      for (hfb_ctx* c : g->ranks) {
+        c->scalars["total"].r = total0 + sum;
+        c->scalars["total"].init = true;
+      }
+    }
+    if (outer) each([&](hfb_ctx* c) {
+      for (const std::string& n : transfers) do_copy_from_device(c, slot(c, n.c_str()));
+    });
+    if (stats) *stats = hfb_launch_stats{st.launches, st.threads, st.guard_returns, st.native};
+  });
+}
 
 hfb_status hfb_profile(hfb_ctx* c, int enable) {
   return guarded([&] {

@@ -39,6 +39,7 @@ EXPORTS = [
     "hfk1_diffuse_step", "hfk0_lateral_and_upper_damping", "hfk0_interior_update",
     "hfk0_sf_slab_flx_tile_run", "hfb_decomp_init", "hfb_decomp_faces", "hfb_set_decomposition",
     "hfb_halo_bytes", "hfb_nccl_unique_id", "hfb_profile", "hfb_kernel_time",
+    "hfb_group_create", "hfb_group_destroy", "hfb_group_run",
 ]
 
 # module of each built-in program (the apps' state modules)
@@ -122,6 +123,10 @@ def lib():
         L.hfb_nccl_unique_id.argtypes = [P]
         L.hfb_profile.argtypes = [P, c.c_int]
         L.hfb_kernel_time.argtypes = [P, S, c.POINTER(dbl), c.POINTER(i64)]
+        L.hfb_group_create.argtypes = [c.POINTER(P), c.c_int, c.POINTER(P)]
+        L.hfb_group_destroy.argtypes = [P]
+        L.hfb_group_destroy.restype = None
+        L.hfb_group_run.argtypes = [P, S, c.POINTER(_Stats)]
         _lib = L
     return _lib
 
@@ -268,6 +273,34 @@ class Engine:
         ms, n = ctypes.c_double(), ctypes.c_int64()
         _check(lib().hfb_kernel_time(self._h, _b(kernel), ctypes.byref(ms), ctypes.byref(n)))
         return ms.value, n.value
+
+
+class Group:
+    """In-process rank group (hfb_group_*): every rank's Engine on this host thread, halos
+    exchanged by device copies. Engines must carry decomposition ranks 0..n-1."""
+
+    def __init__(self, engines):
+        self.engines = list(engines)
+        arr = (ctypes.c_void_p * len(self.engines))(*[e._h.value for e in self.engines])
+        h = ctypes.c_void_p()
+        _check(lib().hfb_group_create(arr, len(self.engines), ctypes.byref(h)))
+        self._h = h
+
+    def run(self, entry="main"):
+        st = _Stats()
+        _check(lib().hfb_group_run(self._h, _b(entry), ctypes.byref(st)))
+        return LaunchStats(st.launches, st.threads, st.guard_returns, st.native_launches)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hfb_group_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
 
 
 def nccl_unique_id():
