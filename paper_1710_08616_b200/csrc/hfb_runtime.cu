@@ -1599,8 +1599,8 @@ hfb_status hfb_group_run(hfb_group* g, const char* entry, hfb_launch_stats* stat
                                          st.native + local.native};
         else
           st.native += local.native;
+        c->steps_done += 1;  // later ranks of this step pull this rank's previous state
       });
-      for (hfb_ctx* c : g->ranks) c->steps_done += 1;
     }
     if (app == "reduction") {
       double sum = 0.0;

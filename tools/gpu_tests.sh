@@ -1,0 +1,3 @@
+# full GPU test suite + smoke
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider --maxfail=20 2>&1 | tail -25
