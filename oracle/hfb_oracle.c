@@ -387,3 +387,37 @@ int ora_dycore_run(int64_t nsteps, const ora_dyn_params* prm, ora_view rho, ora_
   }
   return 0;
 }
+
+/* apps/dycore/dycore.h90 column_physics: per column, one K pass */
+void ora_column_physics(const ora_dyn_params* q, double ch, double rrelax, ora_view rho,
+                        ora_view th, ora_view u, ora_view v, ora_view tsfc, ora_view colm) {
+  const int64_t nx = q->nx, ny = q->ny, nz = q->nz;
+  const double dt = q->dt, rdz = q->rdz;
+#pragma omp parallel for schedule(static)
+  for (int64_t j = 1; j <= ny; ++j)
+    for (int64_t i = 1; i <= nx; ++i) {
+      double cs = 0.0, cm = 0.0;
+      for (int64_t k = 1; k <= nz; ++k) {
+        AT(th, k, i, j) = AT(th, k, i, j) - dt * rrelax * (AT(th, k, i, j) - AT(colm, 0, i, j));
+        if (k == 1) {
+          double wspd = sqrt(AT(u, k, i, j) * AT(u, k, i, j) + AT(v, k, i, j) * AT(v, k, i, j));
+          AT(th, k, i, j) = AT(th, k, i, j) + dt * ch * wspd * (AT(tsfc, 0, i, j) - AT(th, k, i, j)) *
+                                                   rdz / AT(rho, k, i, j);
+        }
+        cs = cs + AT(rho, k, i, j) * AT(th, k, i, j);
+        cm = cm + AT(rho, k, i, j);
+      }
+      AT(colm, 0, i, j) = cs / cm;
+    }
+}
+
+int ora_full_run(int64_t nsteps, const ora_dyn_params* prm, double ch, double rrelax,
+                 ora_view rho, ora_view th, ora_view u, ora_view v, ora_view w, ora_view p,
+                 ora_view tsfc, ora_view colm) {
+  for (int64_t s = 0; s < nsteps; ++s) {
+    int rc = ora_dycore_step(prm, rho, th, u, v, w, p);
+    if (rc) return rc;
+    ora_column_physics(prm, ch, rrelax, rho, th, u, v, tsfc, colm);
+  }
+  return 0;
+}

@@ -57,6 +57,8 @@ def lib():
         L.ora_grid_total.restype = dbl
         L.ora_dycore_run.argtypes = [i64, ctypes.POINTER(DynParams), V, V, V, V, V, V]
         L.ora_dycore_run.restype = ctypes.c_int
+        L.ora_full_run.argtypes = [i64, ctypes.POINTER(DynParams), dbl, dbl] + [V] * 8
+        L.ora_full_run.restype = ctypes.c_int
         L.ora_fill.argtypes = [ctypes.c_void_p, i64, ctypes.c_uint64, dbl, dbl]
         L.ora_splitmix64.argtypes = [ctypes.c_uint64]
         L.ora_splitmix64.restype = ctypes.c_uint64
@@ -142,3 +144,15 @@ def dycore_run(nsteps, params, rho, th, u, v, w, p):
                               view(v), view(w), view(p))
     if rc:
         raise RuntimeError(f"ora_dycore_run failed ({rc})")
+
+
+def full_run(nsteps, params, rho, th, u, v, w, p, tsfc, colm):
+    """simulation_run_full: nsteps x (dycore_step; column_physics)."""
+    nz, nx, ny = th.shape
+    prm = DynParams(nx, ny, nz, params["dt"], params["rdx"], params["rdy"], params["rdz"],
+                    params["cs2"], params["grav"], params["th0"])
+    rc = lib().ora_full_run(nsteps, ctypes.byref(prm), params["ch"], params["rrelax"],
+                            view(rho), view(th), view(u), view(v), view(w), view(p),
+                            view(tsfc), view(colm))
+    if rc:
+        raise RuntimeError(f"ora_full_run failed ({rc})")

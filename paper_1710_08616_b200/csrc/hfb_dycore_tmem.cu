@@ -306,6 +306,10 @@ struct StepTmemArgs {
   Grid3 g;
   int nz;
   int debug_skip;  // profiling experiments only: 1 = no advection, 2 = no acoustic, 3 = neither
+  // column physics fused into the advection warps (full_step); null when off
+  const double* tsfc;
+  double* colm;
+  double dt_rrelax, dt_ch;
   int64_t nj;
   int64_t row_lo, row_hi;
   DynConst c;
@@ -525,7 +529,8 @@ cudaError_t launch_dycore_step_tmem(const DynIn& in, const DynOut& out, Grid3 g,
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  StepTmemArgs a{in, out, g, static_cast<int>(nz), 0, nj, -kIOff, g.pitch - kIOff - 1, c, sp};
+  StepTmemArgs a{in,  out,     g,   static_cast<int>(nz), 0, nullptr, nullptr, 0.0, 0.0, nj,
+                 -kIOff, g.pitch - kIOff - 1, c, sp};
   dim3 block(kTX, kTY);
   dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
             static_cast<unsigned>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY));
@@ -572,6 +577,7 @@ __device__ __forceinline__ double face_flux_up(int64_t f, int64_t n, double vel,
   return fv;
 }
 
+template <bool kPhys>
 __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
   extern __shared__ __align__(128) double smem[];
   __shared__ uint32_t tmem_base_slot;
@@ -666,6 +672,11 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
   double th_prev = 0.0, w_prev = 0.0;              // both roles
   double rho_prev = 0.0, ps_prev = 0.0, cp_prev = 0.0, dp_prev = 0.0;  // acoustic
   double fz_prev = 0.0;                            // advection
+  double phys_cs = 0.0, phys_cm = 0.0, colm_ij = 0.0, tsfc_ij = 0.0;  // column physics
+  if (kPhys && !acoustic && active) {
+    colm_ij = a.colm[(j - 1) * W + (i - 1)];
+    tsfc_ij = a.tsfc[(j - 1) * W + (i - 1)];
+  }
   double pend_beta = 0.0, pend_bb = 1.0, pend_dd = 0.0;  // face awaiting its recursion step
   int s0 = 0;  // ring slot of level k
 
@@ -753,7 +764,21 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
       flux = flux + c.rdz * (fzk - fz_prev);
       double div = c.rdx * (ue - uwf) + c.rdy * (vnf - vsf);
       div = div + c.rdz * (wt - wb);
-      if (kIn || active) *out_th = tk - c.dt * (flux - tk * div);
+      double thv = tk - c.dt * (flux - tk * div);
+      if (kPhys) {  // column_physics (dycore.h90), applied to the new theta of this level
+        thv = thv - a.dt_rrelax * (thv - colm_ij);
+        if (kk == 1) {  // new u, v at the lowest level (region 5), recomputed from the plane
+          const double* Pp = S + kFOffP + (row + 1) * kPW + (lane + 2);
+          const double un1 = (!kIn && east) ? 0.0 : ui - c.dt_rdx * (Pp[1] - Pp[0]);
+          const double vn1 = (!kIn && north) ? 0.0 : vj - c.dt_rdy * (Pp[kPW] - Pp[0]);
+          const double wspd = sqrt(un1 * un1 + vn1 * vn1);
+          thv = thv + a.dt_ch * wspd * (tsfc_ij - thv) * c.rdz / S[kFOffRho + row * kSW + lane];
+        }
+        const double rhok = S[kFOffRho + row * kSW + lane];
+        phys_cs = phys_cs + rhok * thv;
+        phys_cm = phys_cm + rhok;
+      }
+      if (kIn || active) *out_th = thv;
       fz_prev = fzk;
     }
     th_prev = tk;
@@ -779,6 +804,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
   }
   if (acoustic && nz >= 2) thomas_step(nz - 2);  // drain the last face
   sm100::cp_async_wait<0>();
+  if (kPhys && !acoustic && active) a.colm[(j - 1) * W + (i - 1)] = phys_cs / phys_cm;
 
   if (acoustic) {
     sm100::tmem_wait_st();
@@ -820,27 +846,29 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
 
 cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                   int64_t nj, const DynConst& c, const Span& sp,
-                                  cudaStream_t s) {
+                                  cudaStream_t s, const PhysArgs* phys) {
   if (sp.ihi < sp.ilo || sp.jhi < sp.jlo) return cudaSuccess;
   if (!dycore_step_tmem_fits(nz)) return cudaErrorInvalidValue;
   const size_t smem = std::max<size_t>((static_cast<size_t>(kWsStages) * kFStageDoubles +
                                         static_cast<size_t>(nz) * kThreads) * sizeof(double),
                                        80 * 1024);
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_dyn_step_ws,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+  auto kern = phys ? k_dyn_step_ws<true> : k_dyn_step_ws<false>;
+  static size_t configured[2] = {0, 0};
+  if (smem > configured[phys ? 1 : 0]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    configured = smem;
+    configured[phys ? 1 : 0] = smem;
   }
   static const int debug_skip = getenv("HFB_DEBUG_SKIP") ? atoi(getenv("HFB_DEBUG_SKIP")) : 0;
-  StepTmemArgs a{in, out, g, static_cast<int>(nz), debug_skip, nj, -kIOff, g.pitch - kIOff - 1,
-                 c, sp};
+  StepTmemArgs a{in, out, g, static_cast<int>(nz), debug_skip,
+                 phys ? phys->tsfc : nullptr, phys ? phys->colm : nullptr,
+                 phys ? phys->dt_rrelax : 0.0, phys ? phys->dt_ch : 0.0,
+                 nj, -kIOff, g.pitch - kIOff - 1, c, sp};
   dim3 block(kTX, 2 * kTY);
   dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
             static_cast<unsigned>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY));
-  k_dyn_step_ws<<<grid, block, smem, s>>>(a);
+  kern<<<grid, block, smem, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -698,6 +698,52 @@ cudaError_t launch_dycore_acoustic(const DynIn& in, const DynOut& out, Grid3 g, 
 }
 
 // ============================================================================
+// apps/dycore/dycore.h90 column_physics — one thread per column, one K pass:
+// relaxation toward the previous column mean, bulk surface heat flux at k = 1, the new
+// density-weighted column mean (sequential column sum, the dialect's order).
+// ============================================================================
+namespace {
+__global__ void __launch_bounds__(128) k_column_physics(const double* __restrict__ rho,
+                                                        double* __restrict__ th,
+                                                        const double* __restrict__ u,
+                                                        const double* __restrict__ v, Grid3 g,
+                                                        int nz, DynConst c, PhysArgs ph,
+                                                        Span sp) {
+  const int64_t i = sp.ilo + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t j = sp.jlo + static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y;
+  if (i > sp.ihi || j > sp.jhi) return;
+  const int64_t col = (j - 1) * g.pitch + (i - 1);
+  const double cmean = ph.colm[col];
+  double cs = 0.0, cm = 0.0;
+  for (int k = 0; k < nz; ++k) {
+    const int64_t o = col + static_cast<int64_t>(k) * g.plane;
+    const double r = __ldg(rho + o);
+    double t = th[o];
+    t = t - ph.dt_rrelax * (t - cmean);
+    if (k == 0) {
+      const double uu = __ldg(u + o), vv = __ldg(v + o);
+      const double wspd = sqrt(uu * uu + vv * vv);
+      t = t + ph.dt_ch * wspd * (__ldg(ph.tsfc + col) - t) * c.rdz / r;
+    }
+    th[o] = t;
+    cs = cs + r * t;
+    cm = cm + r;
+  }
+  ph.colm[col] = cs / cm;
+}
+}  // namespace
+
+cudaError_t launch_column_physics(const double* rho, double* th, const double* u,
+                                  const double* v, Grid3 g, int64_t nz, const DynConst& c,
+                                  const PhysArgs& ph, const Span& sp, cudaStream_t s) {
+  if (span_empty(sp) || nz <= 0) return cudaSuccess;
+  dim3 block(32, 4);
+  k_column_physics<<<span_grid(sp, block), block, 0, s>>>(rho, th, u, v, g,
+                                                          static_cast<int>(nz), c, ph, sp);
+  return cudaGetLastError();
+}
+
+// ============================================================================
 // halo pack/unpack: box {ilo, ihi, jlo, jhi} (local 1-based) x all K levels
 // ============================================================================
 namespace {

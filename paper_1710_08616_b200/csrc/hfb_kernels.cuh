@@ -87,10 +87,22 @@ bool dycore_step_tmem_fits(int64_t nz);
 cudaError_t launch_dycore_step_tmem(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                     int64_t nj, const DynConst& c, const Span& sp,
                                     cudaStream_t s);
-// warp-specialised variant (acoustic warps + advection warps per tile)
+// column physics (dycore.h90 column_physics): surface field, previous column mean
+// (updated in place), and the products dt*rrelax, dt*ch as the dialect forms them
+struct PhysArgs {
+  const double* tsfc;
+  double* colm;
+  double dt_rrelax, dt_ch;
+};
+// warp-specialised variant (acoustic warps + advection warps per tile); with `phys` the
+// column physics is fused into the advection warps (the full timestep in one kernel)
 cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                   int64_t nj, const DynConst& c, const Span& sp,
-                                  cudaStream_t s);
+                                  cudaStream_t s, const PhysArgs* phys = nullptr);
+// standalone column physics on the current state (th updated in place)
+cudaError_t launch_column_physics(const double* rho, double* th, const double* u,
+                                  const double* v, Grid3 g, int64_t nz, const DynConst& c,
+                                  const PhysArgs& ph, const Span& sp, cudaStream_t s);
 
 // ---- halo pack/unpack for the 2-D decomposition -------------------------------------
 cudaError_t launch_pack_box(const double* field, double* buf, Grid3 g, int64_t nk,

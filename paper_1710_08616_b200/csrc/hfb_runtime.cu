@@ -161,13 +161,16 @@ const std::vector<AppDecl>& app_table() {
                  {{"nx", SType::Int}, {"ny", SType::Int}, {"nz", SType::Int},
                   {"nsteps", SType::Int}, {"dt", SType::Real}, {"rdx", SType::Real},
                   {"rdy", SType::Real}, {"rdz", SType::Real}, {"cs2", SType::Real},
-                  {"grav", SType::Real}, {"th0", SType::Real}},
+                  {"grav", SType::Real}, {"th0", SType::Real}, {"ch", SType::Real},
+                  {"rrelax", SType::Real}},
                  {{"rho", dims3("nz", "nx", "ny"), KIJ, false},
                   {"th", dims3("nz", "nx", "ny"), KIJ, true},
                   {"u", dims3("nz", "nx", "ny"), KIJ, true},
                   {"v", dims3("nz", "nx", "ny"), KIJ, true},
                   {"w", dims3("nz", "nx", "ny"), KIJ, true},
-                  {"p", dims3("nz", "nx", "ny"), KIJ, true}}});
+                  {"p", dims3("nz", "nx", "ny"), KIJ, true},
+                  {"tsfc", {{"1", "nx"}, {"1", "ny"}}, IJ, false},
+                  {"colm", {{"1", "nx"}, {"1", "ny"}}, IJ, false}}});
     return v;
   }();
   return apps;
@@ -718,7 +721,28 @@ void reduction_entry(hfb_ctx* c, const std::string& r, Stats& st) {
 // ---------------------------------------------------------------------------
 // app: dycore (apps/dycore/dycore.h90)
 // ---------------------------------------------------------------------------
-void dycore_step(hfb_ctx* c, Stats& st) {
+PhysArgs phys_args(hfb_ctx* c, Slot& tsfc, Slot& colm) {
+  const double dt = rval(c, "dt");
+  return PhysArgs{tsfc.d(), colm.d(), dt * rval(c, "rrelax"), dt * rval(c, "ch")};
+}
+
+// column_physics on the current state (standalone kernel)
+void column_physics(hfb_ctx* c, Stats& st) {
+  int64_t nx = ival(c, "nx"), ny = ival(c, "ny"), nz = ival(c, "nz");
+  for (const char* n : {"rho", "th", "u", "v", "tsfc", "colm"}) dev_read(c, n);
+  DynConst k = make_dyn_const(rval(c, "dt"), rval(c, "rdx"), rval(c, "rdy"), rval(c, "rdz"),
+                              rval(c, "cs2"), rval(c, "grav"), rval(c, "th0"));
+  Slot &rho = slot(c, "rho"), &th = slot(c, "th"), &u = slot(c, "u"), &v = slot(c, "v");
+  PhysArgs ph = phys_args(c, slot(c, "tsfc"), slot(c, "colm"));
+  launch(c, st, "column_physics", [&] {
+    return launch_column_physics(rho.d(), th.d(), u.d(), v.d(), grid_of(th), nz, k, ph,
+                                 full_span(c, nx, ny), c->stream);
+  });
+  count_launch(st, nx, ny);
+  for (const char* n : {"th", "colm"}) dev_written(c, n);
+}
+
+void dycore_step(hfb_ctx* c, Stats& st, bool with_physics = false) {
   int64_t nx = ival(c, "nx"), ny = ival(c, "ny"), nz = ival(c, "nz");
   if (nz < 2) fail(HFB_RUNTIME, "dycore_step needs nz >= 2 (got %lld)", (long long)nz);
   if (c->decomposed && c->decomp.px * c->decomp.py > 1 && c->decomp.halo < 2)
@@ -727,6 +751,8 @@ void dycore_step(hfb_ctx* c, Stats& st) {
   DynConst k = make_dyn_const(rval(c, "dt"), rval(c, "rdx"), rval(c, "rdy"), rval(c, "rdz"),
                               rval(c, "cs2"), rval(c, "grav"), rval(c, "th0"));
   for (const char* n : {"th", "u", "v", "w", "p", "rho"}) dev_read(c, n);
+  if (with_physics)
+    for (const char* n : {"tsfc", "colm"}) dev_read(c, n);
   Slot &rho = slot(c, "rho"), &th = slot(c, "th"), &u = slot(c, "u"), &v = slot(c, "v"),
        &w = slot(c, "w"), &p = slot(c, "p");
   for (Slot* s : {&th, &u, &v, &w, &p}) ensure_device(c, *s, true);
@@ -734,12 +760,20 @@ void dycore_step(hfb_ctx* c, Stats& st) {
   DynIn in{rho.d(), th.d(), u.d(), v.d(), w.d(), p.d()};
   DynOut out{th.d_alt(), u.d_alt(), v.d_alt(), w.d_alt(), p.d_alt()};
   Span sp = full_span(c, nx, ny);
+  bool fused_physics = false;
   if (dycore_step_tmem_fits(nz) && !c->force_generic && !c->force_split) {
     if (c->force_single_role)
       launch(c, st, "dycore_step", [&] {
         return launch_dycore_step_tmem(in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
       });
-    else
+    else if (with_physics) {
+      PhysArgs ph = phys_args(c, slot(c, "tsfc"), slot(c, "colm"));
+      launch(c, st, "full_step", [&] {
+        return launch_dycore_step_ws(in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream,
+                                     &ph);
+      });
+      fused_physics = true;
+    } else
       launch(c, st, "dycore_step", [&] {
         return launch_dycore_step_ws(in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
       });
@@ -764,6 +798,14 @@ void dycore_step(hfb_ctx* c, Stats& st) {
   count_launch(st, nx, ny + 1);
   for (int r = 0; r < 6; ++r) count_launch(st, nx, ny);
   for (const char* n : {"th", "u", "v", "w", "p"}) dev_written(c, n);
+  if (with_physics) {
+    if (fused_physics) {
+      count_launch(st, nx, ny);  // the generated code's column_physics launch
+      dev_written(c, "colm");
+    } else {
+      column_physics(c, st);
+    }
+  }
 }
 
 void dycore_entry(hfb_ctx* c, const std::string& r, Stats& st) {
@@ -775,6 +817,16 @@ void dycore_entry(hfb_ctx* c, const std::string& r, Stats& st) {
     for (const char* n : names) do_copy_from_device(c, slot(c, n));
   } else if (r == "dycore_step") {
     dycore_step(c, st);
+  } else if (r == "main_full" || r == "simulation_run_full") {
+    int64_t nsteps = ival(c, "nsteps");
+    const char* full_names[] = {"colm", "p", "rho", "th", "tsfc", "u", "v", "w"};
+    for (const char* n : full_names) do_copy_to_device(c, slot(c, n));
+    for (int64_t s = 0; s < nsteps; ++s) dycore_step(c, st, true);
+    for (const char* n : full_names) do_copy_from_device(c, slot(c, n));
+  } else if (r == "full_step") {
+    dycore_step(c, st, true);
+  } else if (r == "column_physics") {
+    column_physics(c, st);
   } else {
     fail(HFB_CONFIG, "program 'dycore' has no entry '%s'", r.c_str());
   }
@@ -792,7 +844,8 @@ EntryFn entry_fn(const std::string& app) {
 }
 
 bool entry_has_transfers(const std::string& app, const std::string& r) {
-  if (r == "main" || r == "simulation_run") return true;
+  if (r == "main" || r == "simulation_run" || r == "main_full" || r == "simulation_run_full")
+    return true;
   (void)app;
   return false;
 }
@@ -1552,10 +1605,14 @@ hfb_status hfb_group_run(hfb_group* g, const char* entry, hfb_launch_stats* stat
         cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
       }
     };
-    const bool outer = r == "main" || r == "simulation_run";
+    const bool full = r == "main_full" || r == "simulation_run_full";
+    const bool outer = r == "main" || r == "simulation_run" || full;
     std::vector<std::string> transfers;
     std::string step;
-    if (app == "dycore") {
+    if (app == "dycore" && full) {
+      transfers = {"colm", "p", "rho", "th", "tsfc", "u", "v", "w"};
+      step = "full_step";
+    } else if (app == "dycore") {
       transfers = {"p", "rho", "th", "u", "v", "w"};
       step = "dycore_step";
     } else if (app == "diffusion") {

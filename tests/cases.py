@@ -24,6 +24,11 @@ class App:
     families: list = field(default_factory=list)
     entry: str = "main"
     backend: str = "cuda"
+    program: str = ""      # runtime program name (default: the app name)
+
+    @property
+    def prog(self):
+        return self.program or self.name
 
 
 APPS = {
@@ -56,6 +61,13 @@ APPS = {
         "dycore", [("own", "dycore/dyn_state.h90"), ("own", "dycore/dycore.h90")], "dyn_state",
         {n: ("nz", "nx", "ny") for n in ("rho", "th", "u", "v", "w", "p")},
         ["th", "u", "v", "w", "p", "rho"]),
+    # the full timestep: dycore + column physics (entry main_full)
+    "dycore_full": App(
+        "dycore_full", [("own", "dycore/dyn_state.h90"), ("own", "dycore/dycore.h90")],
+        "dyn_state",
+        dict({n: ("nz", "nx", "ny") for n in ("rho", "th", "u", "v", "w", "p")},
+             tsfc=("nx", "ny"), colm=("nx", "ny")),
+        ["th", "u", "v", "w", "p", "colm"], entry="main_full", program="dycore"),
 }
 
 # Synthetic-state conventions; seeds are fixed per field.
@@ -64,6 +76,8 @@ DYCORE_SCALARS = {"dt": 0.1, "rdx": 2.0, "rdy": 2.0, "rdz": 20.0, "cs2": 1.0,
 DYCORE_FILLS = {  # name: (seed, offset, scale)
     "rho": (7, 1.0, 0.1), "th": (8, 300.0, 1.0), "u": (9, -0.01, 0.02),
     "v": (10, -0.01, 0.02), "w": (11, -0.002, 0.004), "p": (12, -0.005, 0.01)}
+PHYS_SCALARS = {"ch": 0.05, "rrelax": 0.01}
+PHYS_FILLS = {"tsfc": (13, 300.0, 2.0), "colm": (14, 300.0, 0.5)}
 
 
 @dataclass
@@ -86,6 +100,12 @@ def _diff(name, nx, ny, nz, nsteps, seed=1, off=280.0, scale=10.0, coef=0.1):
 def _dyc(name, nx, ny, nz, nsteps, gpu_check=True):
     return Case(name, "dycore", dict(nx=nx, ny=ny, nz=nz, nsteps=nsteps), dict(DYCORE_SCALARS),
                 dict(DYCORE_FILLS), gpu_check=gpu_check)
+
+
+def _full(name, nx, ny, nz, nsteps, gpu_check=True):
+    return Case(name, "dycore_full", dict(nx=nx, ny=ny, nz=nz, nsteps=nsteps),
+                dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS),
+                gpu_check=gpu_check)
 
 
 CASES = [
@@ -130,5 +150,9 @@ CASES = [
     _dyc("dycore_1x5x2_s2", 1, 5, 2, 2),
     _dyc("dycore_33x3x58_s1", 33, 3, 58, 1),
     _dyc("dycore_13x7x10_s100", 13, 7, 10, 100, gpu_check=False),
+    _full("full_13x7x10_s3", 13, 7, 10, 3),
+    _full("full_24x20x12_s2", 24, 20, 12, 2),
+    _full("full_1x5x2_s2", 1, 5, 2, 2),
+    _full("full_33x3x58_s1", 33, 3, 58, 1),
 ]
 CASE_BY_NAME = {c.name: c for c in CASES}

@@ -8,19 +8,21 @@ import numpy as np
 import pytest
 
 import paper_1710_08616_b200 as hfb
-from cases import APPS, DYCORE_FILLS, DYCORE_SCALARS, Case
+from cases import APPS, DYCORE_FILLS, DYCORE_SCALARS, PHYS_FILLS, PHYS_SCALARS, Case
 from golden_io import bits_equal, decl, make_inputs, run_oracle
 
 pytestmark = pytest.mark.gpu
 
 # which declared dims are (i, j) for each array of an app
 IJ_DIMS = {"diffusion": (1, 2), "dycore": (1, 2), "reduction": (1, 2), "bounded": (0, 1),
-           "damping": (1, 2), "surface_flux": None}
+           "damping": (1, 2), "surface_flux": None, "dycore_full": (1, 2)}
 
 
 def tile_slices(app, name, arr, d):
     if app == "surface_flux":
         ij = (1, 2) if name == "cover_frac" else (0, 1)
+    elif arr.ndim == 2:
+        ij = (0, 1)
     else:
         ij = IJ_DIMS[app]
     sl = [slice(None)] * arr.ndim
@@ -48,14 +50,15 @@ def global_extent(case):
     return case.ints["nx"], case.ints["ny"]
 
 
-def run_decomposed(case, px, py, entry="main", halo=2):
+def run_decomposed(case, px, py, entry=None, halo=2):
+    entry = entry or APPS[case.app].entry
     garr = make_inputs(case)
     gnx, gny = global_extent(case)
     nz = case.ints.get("nz", 1)
     engines, tiles, decomps = [], [], []
     for r in range(px * py):
         d = hfb.decomp_init(gnx, gny, nz, px, py, r, halo=halo)
-        eng = hfb.Engine(case.app)
+        eng = hfb.Engine(APPS[case.app].prog)
         eng.set_decomposition(d)
         ints = tile_ints(case, d)
         for k, v in ints.items():
@@ -98,6 +101,16 @@ def test_dycore_decomposed_equals_single(px, py):
         assert bits_equal(out[k], ref[k]), f"{px}x{py}: {k} differs"
     assert halo_bytes > 0
     assert stats.native_launches == 3 * px * py
+
+
+def test_full_step_decomposed_equals_single():
+    case = Case("f", "dycore_full", dict(nx=70, ny=45, nz=58, nsteps=3),
+                dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS))
+    garr, out, _, _, _ = run_decomposed(case, 2, 2)
+    ref = {k: v.copy() for k, v in garr.items()}
+    run_oracle(case, ref)
+    for k in ("th", "u", "v", "w", "p", "colm"):
+        assert bits_equal(out[k], ref[k]), k
 
 
 def test_dycore_decomposed_ragged_tiles_generic_kernel(monkeypatch):

@@ -11,15 +11,17 @@ import numpy as np
 import pytest
 
 import paper_1710_08616_b200 as hfb
-from cases import APPS, CASES, CASE_BY_NAME, DYCORE_FILLS, DYCORE_SCALARS, Case
+from cases import (APPS, CASES, CASE_BY_NAME, DYCORE_FILLS, DYCORE_SCALARS, PHYS_FILLS,
+                   PHYS_SCALARS, Case)
 from golden_io import bits_equal, decl, load_golden, make_inputs, run_oracle
 
 pytestmark = pytest.mark.gpu
 
 
-def run_engine(case, arrs, entry="main"):
+def run_engine(case, arrs, entry=None):
     app = APPS[case.app]
-    with hfb.Engine(case.app) as eng:
+    entry = entry or app.entry
+    with hfb.Engine(app.prog) as eng:
         for k, v in case.ints.items():
             eng.set(k, int(v))
         for k, v in case.reals.items():
@@ -87,6 +89,10 @@ LARGE = [
          dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
     Case("dycore_31x7x2_s3", "dycore", dict(nx=31, ny=7, nz=2, nsteps=3),
          dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
+    Case("full_128x96x58_s3", "dycore_full", dict(nx=128, ny=96, nz=58, nsteps=3),
+         dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS)),
+    Case("full_45x37x80_s2", "dycore_full", dict(nx=45, ny=37, nz=80, nsteps=2),
+         dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS)),
 ]
 
 
@@ -109,6 +115,20 @@ def test_split_step_matches(monkeypatch):
     monkeypatch.setenv("HFB_SPLIT_STEP", "1")
     _oracle_vs_gpu(Case("dycore_70x45x58_s2", "dycore", dict(nx=70, ny=45, nz=58, nsteps=2),
                         dict(DYCORE_SCALARS), dict(DYCORE_FILLS)))
+
+
+def test_full_step_split_path_matches(monkeypatch):
+    """dycore kernels + the standalone column-physics kernel (HFB_SPLIT_STEP=1)."""
+    monkeypatch.setenv("HFB_SPLIT_STEP", "1")
+    _oracle_vs_gpu(Case("full_70x45x58_s2", "dycore_full", dict(nx=70, ny=45, nz=58, nsteps=2),
+                        dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS)))
+
+
+def test_full_size_full_timestep_c3():
+    """BASELINE configs[2]: full timestep with column physics, 1024 x 1024 x 58, one step."""
+    _oracle_vs_gpu(Case("full_1024x1024x58_s1", "dycore_full",
+                        dict(nx=1024, ny=1024, nz=58, nsteps=1),
+                        dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS)))
 
 
 def test_single_role_fused_matches(monkeypatch):
