@@ -37,7 +37,8 @@ GRIDS = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
 # the fused step reads rho,th,u,v,w,p and writes th',u',v',w',p' (11 x 8 B); the split
 # variant's advect reads th,u,v,w / writes th' (5 x 8 B) and acoustic reads
 # rho,th,u,v,w,p / writes u',v',w',p' (10 x 8 B)
-BYTES_PER_POINT = {"dycore_step": 88, "dycore_advect": 40, "dycore_acoustic": 80}
+BYTES_PER_POINT = {"dycore_step": 88, "full_step": 88, "dycore_advect": 40,
+                   "dycore_acoustic": 80, "hfk0_diffuse_step": 24}
 L2_BYTES = 126 * 2**20
 
 
@@ -122,6 +123,63 @@ def make_state(eng, d, px, py):
     for k, a in arrs.items():
         eng.bind(k, a, pin=True)
     return arrs
+
+
+def secondary(local, steps=10, warmup=3):
+    """Single-GPU, device-resident timings of the other BASELINE configs (reported beside
+    the headline; same CUDA-event method, per-kernel times from hfb_profile)."""
+    import torch
+    import paper_1710_08616_b200 as hfb
+    from paper_1710_08616_b200 import synthetic
+    hbm, _ = peaks()
+    out = {}
+    runs = [("C1 dycore step 128x128x58", "dycore", "dycore_step", 128, 128),
+            ("C3 full timestep + column physics 1024x1024x58", "dycore", "full_step", 1024, 1024),
+            ("C4 dycore step 1581x1301x58 (1 GPU)", "dycore", "dycore_step", 1581, 1301),
+            ("reference kernel: diffusion step 1581x1301x58", "diffusion", "diffuse_step",
+             1581, 1301)]
+    for label, prog, entry, nx, ny in runs:
+        eng = hfb.Engine(prog, device=local)
+        shape = (NZ, nx, ny)
+        for k, v in dict(nx=nx, ny=ny, nz=NZ, nsteps=1).items():
+            eng.set(k, v)
+        if prog == "dycore":
+            for k, v in dict(synthetic.DYCORE_SCALARS, ch=0.05, rrelax=0.01).items():
+                eng.set(k, v)
+            arrs = {k: synthetic.field(shape, *v, order="F")
+                    for k, v in synthetic.DYCORE_FILLS.items()}
+            if entry == "full_step":
+                arrs["tsfc"] = synthetic.field((nx, ny), 13, 300.0, 2.0, order="F")
+                arrs["colm"] = synthetic.field((nx, ny), 14, 300.0, 0.5, order="F")
+            bpp = 88
+        else:
+            eng.set("coef", 0.1)
+            arrs = {"t_old": synthetic.field(shape, 1, 280.0, 10.0, order="F"),
+                    "t_new": np.zeros(shape, order="F")}
+            bpp = 24
+        for k, a in arrs.items():
+            eng.bind(k, a)
+            eng.copy_to_device(k)
+        stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
+        for _ in range(warmup):
+            eng.enqueue(entry)
+        eng.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            eng.enqueue(entry)
+        e1.record(stream)
+        eng.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        pts = nx * ny * NZ
+        out[label] = {"ms_per_step": round(ms, 4), "value": round(pts / (ms / 1e3), 1),
+                      "unit": UNIT, "alg_bytes_per_point": bpp,
+                      "achieved_GBps": round(bpp * pts / (ms / 1e3) / 1e9, 1),
+                      "frac_of_measured_hbm": round(bpp * pts / (ms / 1e3) / 1e9 / hbm, 4),
+                      "steps": steps}
+        eng.close()
+        del arrs
+    return out
 
 
 def cpu_baseline_port(seconds_budget=20.0):
@@ -282,6 +340,8 @@ def bench_ours(args):
                "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
                "clocks": clocks.summary(), "halo_bytes": halo}
         out["cpu_baseline"] = cpu_baseline_port() if n == 1 else None
+        if n == 1 and not args.no_secondary:
+            out["other_configs"] = secondary(local)
         print(json.dumps(out), flush=True)
     if n > 1:
         dist.destroy_process_group()
@@ -349,6 +409,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the single-GPU timings of the other BASELINE configs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "hfb_kernels.cuh"
 
@@ -132,6 +133,11 @@ struct DiffArgs {
   Span sp;
 };
 
+// K is processed in chunks of kDiffChunk levels: all loads of a chunk (its center
+// column plus the four horizontal neighbours of every level) are issued before any
+// arithmetic, so ~40 independent loads per thread are in flight (the one-level
+// version is bound by load latency: long_scoreboard 87%).
+template <int kDiffChunk>
 __global__ void __launch_bounds__(256) k_diffusion(DiffArgs a) {
   const int64_t i = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t j = a.sp.jlo + static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y;
@@ -147,29 +153,46 @@ __global__ void __launch_bounds__(256) k_diffusion(DiffArgs a) {
   double* o2 = a.o2 ? a.o2 + col : nullptr;
   const int nz = a.nz;
   const double coef = a.coef;
-  double km1 = (kb > 1) ? __ldg(src + (kb - 2) * P) : 0.0;
-  double k0 = __ldg(src + (kb - 1) * P);
-#pragma unroll 4
-  for (int k = kb; k <= ke; ++k) {
-    const double kp1 = (k < nz) ? __ldg(src + static_cast<int64_t>(k) * P) : 0.0;
-    double out;
-    if (hb || k == 1 || k == nz) {
-      out = k0;
-    } else {
-      const double* c = src + static_cast<int64_t>(k - 1) * P;
-      double s = km1 + kp1;
-      s = s + __ldg(c - 1);
-      s = s + __ldg(c + 1);
-      s = s + __ldg(c - W);
-      s = s + __ldg(c + W);
-      s = s - 6.0 * k0;
-      out = k0 + coef * s;
+#pragma unroll 1
+  for (int k0 = kb; k0 <= ke; k0 += kDiffChunk) {
+    double cc[kDiffChunk + 2];  // levels k0-1 .. k0+kDiffChunk
+    double xw[kDiffChunk], xe[kDiffChunk], ys[kDiffChunk], yn[kDiffChunk];
+#pragma unroll
+    for (int q = 0; q < kDiffChunk + 2; ++q) {
+      const int k = k0 - 1 + q;
+      cc[q] = (k >= 1 && k <= nz) ? __ldg(src + static_cast<int64_t>(k - 1) * P) : 0.0;
     }
-    const int64_t off = static_cast<int64_t>(k - 1) * P;
-    o1[off] = out;
-    if (o2) o2[off] = out;
-    km1 = k0;
-    k0 = kp1;
+#pragma unroll
+    for (int q = 0; q < kDiffChunk; ++q) {
+      const int k = k0 + q;
+      const bool need = !hb && k > 1 && k < nz && k <= ke;
+      const double* c = src + static_cast<int64_t>(k - 1) * P;
+      xw[q] = need ? __ldg(c - 1) : 0.0;
+      xe[q] = need ? __ldg(c + 1) : 0.0;
+      ys[q] = need ? __ldg(c - W) : 0.0;
+      yn[q] = need ? __ldg(c + W) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kDiffChunk; ++q) {
+      const int k = k0 + q;
+      if (k > ke) break;
+      const double c0 = cc[q + 1];
+      double out;
+      if (hb || k == 1 || k == nz) {
+        out = c0;
+      } else {
+        double s = cc[q] + cc[q + 2];
+        s = s + xw[q];
+        s = s + xe[q];
+        s = s + ys[q];
+        s = s + yn[q];
+        s = s - 6.0 * c0;
+        out = c0 + coef * s;
+      }
+      const int64_t off = static_cast<int64_t>(k - 1) * P;
+      o1[off] = out;
+      if (o2) o2[off] = out;
+    }
   }
 }
 
@@ -197,7 +220,14 @@ cudaError_t launch_diffusion(const double* t_old, double* out1, double* out2, Gr
   int kchunk = static_cast<int>((nz + kchunks - 1) / kchunks);
   kchunks = static_cast<int>((nz + kchunk - 1) / kchunk);
   DiffArgs a{t_old, out1, out2, g, static_cast<int>(nz), kchunk, coef, sp};
-  k_diffusion<<<span_grid(sp, block, kchunks), block, 0, s>>>(a);
+  static const int chunk = getenv("HFB_DIFF_CHUNK") ? atoi(getenv("HFB_DIFF_CHUNK")) : 2;
+  dim3 grid = span_grid(sp, block, kchunks);
+  switch (chunk) {
+    case 1: k_diffusion<1><<<grid, block, 0, s>>>(a); break;
+    case 4: k_diffusion<4><<<grid, block, 0, s>>>(a); break;
+    case 8: k_diffusion<8><<<grid, block, 0, s>>>(a); break;
+    default: k_diffusion<2><<<grid, block, 0, s>>>(a); break;
+  }
   return cudaGetLastError();
 }
 

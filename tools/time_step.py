@@ -10,25 +10,37 @@ import torch  # noqa: E402
 import paper_1710_08616_b200 as hfb  # noqa: E402
 from paper_1710_08616_b200 import synthetic  # noqa: E402
 
+import numpy as np  # noqa: E402
+
 nx, ny, nz = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (512, 512, 58)))
-eng = hfb.Engine("dycore")
+app = sys.argv[4] if len(sys.argv) > 4 else "dycore"
+eng = hfb.Engine(app)
 for k, v in dict(nx=nx, ny=ny, nz=nz, nsteps=1).items():
     eng.set(k, v)
-for k, v in synthetic.DYCORE_SCALARS.items():
-    eng.set(k, v)
-arrs = {k: synthetic.field((nz, nx, ny), *v, order="F") for k, v in synthetic.DYCORE_FILLS.items()}
+if app == "dycore":
+    for k, v in synthetic.DYCORE_SCALARS.items():
+        eng.set(k, v)
+    arrs = {k: synthetic.field((nz, nx, ny), *v, order="F")
+            for k, v in synthetic.DYCORE_FILLS.items()}
+    entry, bpp = "dycore_step", 88
+else:
+    eng.set("coef", 0.1)
+    arrs = {"t_old": synthetic.field((nz, nx, ny), 1, 280.0, 10.0, order="F"),
+            "t_new": np.zeros((nz, nx, ny), order="F")}
+    entry, bpp = "diffuse_step", 24
 for k, a in arrs.items():
     eng.bind(k, a)
     eng.copy_to_device(k)
 s = torch.cuda.ExternalStream(eng.stream)
 for _ in range(5):
-    eng.enqueue("dycore_step")
+    eng.enqueue(entry)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 n = 40
 e0.record(s)
 for _ in range(n):
-    eng.enqueue("dycore_step")
+    eng.enqueue(entry)
 e1.record(s)
 eng.synchronize()
 ms = e0.elapsed_time(e1) / n
-print(f"{nx}x{ny}x{nz}: {ms:.4f} ms/step  {nx*ny*nz/ms/1e6:.3e} pt/s  {88*nx*ny*nz/ms/1e6:.0f} GB/s(alg)")
+print(f"{app} {nx}x{ny}x{nz}: {ms:.4f} ms/step  {nx*ny*nz/ms*1e3:.3e} pt/s  "
+      f"{bpp*nx*ny*nz/ms/1e6:.0f} GB/s(alg)")
