@@ -134,6 +134,8 @@ def secondary(local, steps=10, warmup=3):
     hbm, _ = peaks()
     out = {}
     runs = [("C1 dycore step 128x128x58", "dycore", "dycore_step", 128, 128),
+            ("C2 dycore with Wicker-Skamarock RK3 (3 stages) 512x512x58", "dycore", "rk3_step",
+             512, 512),
             ("C3 full timestep + column physics 1024x1024x58", "dycore", "full_step", 1024, 1024),
             ("C4 dycore step 1581x1301x58 (1 GPU)", "dycore", "dycore_step", 1581, 1301),
             ("reference kernel: diffusion step 1581x1301x58", "diffusion", "diffuse_step",
@@ -151,7 +153,9 @@ def secondary(local, steps=10, warmup=3):
             if entry == "full_step":
                 arrs["tsfc"] = synthetic.field((nx, ny), 13, 300.0, 2.0, order="F")
                 arrs["colm"] = synthetic.field((nx, ny), 14, 300.0, 0.5, order="F")
-            bpp = 88
+            # RK3: stage 1 as the single step (88 B/pt); stages 2-3 also read the base
+            # th, u, v, w, p (128 B/pt each)
+            bpp = 88 + 2 * 128 if entry == "rk3_step" else 88
         else:
             eng.set("coef", 0.1)
             arrs = {"t_old": synthetic.field(shape, 1, 280.0, 10.0, order="F"),

@@ -209,11 +209,16 @@ static int s3_alloc(int id, scratch3* s, int64_t k0, int64_t k1, int64_t i0, int
   return s->p != NULL;
 }
 
-int ora_dycore_step(const ora_dyn_params* q, ora_view rho, ora_view th, ora_view u, ora_view v,
-                    ora_view w, ora_view p) {
+/* One evaluation of the dynamics at the current state (th, u, v, w, p) applied with
+ * step `dt` to the base state (thb, ub, vb, wb, pb); the result replaces the current
+ * state. dycore_step is the stage with base == current and dt = q->dt; rk3_step runs
+ * three stages with dt/3, dt/2, dt from the state at the start of the step. */
+static int dycore_stage(const ora_dyn_params* q, double dt, ora_view rho, ora_view th,
+                        ora_view u, ora_view v, ora_view w, ora_view p, ora_view thb,
+                        ora_view ub, ora_view vb, ora_view wb, ora_view pb) {
   const int64_t nx = q->nx, ny = q->ny, nz = q->nz;
-  const double dt = q->dt, rdx = q->rdx, rdy = q->rdy, rdz = q->rdz, cs2 = q->cs2,
-               grav = q->grav, th0 = q->th0;
+  const double rdx = q->rdx, rdy = q->rdy, rdz = q->rdz, cs2 = q->cs2, grav = q->grav,
+               th0 = q->th0;
   if (nz < 2) return -1;
   scratch3 fx, fy, fz, thn, un, vn, ps, wn, pn;
   int ok = s3_alloc(0, &fx, 1, nz, 0, nx, 1, ny) & s3_alloc(1, &fy, 1, nz, 1, nx, 0, ny) &
@@ -303,7 +308,7 @@ int ora_dycore_step(const ora_dyn_params* q, ora_view rho, ora_view th, ora_view
         flux = flux + rdz * (*s3(&fz, k, i, j) - *s3(&fz, k - 1, i, j));
         double div = rdx * (ue - uw) + rdy * (vnf - vs);
         div = div + rdz * (wt - wb);
-        *s3(&thn, k, i, j) = t - dt * (flux - t * div);
+        *s3(&thn, k, i, j) = AT(thb, k, i, j) - dt * (flux - t * div);
       }
   /* region 5: horizontal pressure gradient */
 #pragma omp parallel for schedule(static)
@@ -311,9 +316,9 @@ int ora_dycore_step(const ora_dyn_params* q, ora_view rho, ora_view th, ora_view
     for (int64_t i = 1; i <= nx; ++i)
       for (int64_t k = 1; k <= nz; ++k) {
         *s3(&un, k, i, j) =
-            (i == nx) ? 0.0 : AT(u, k, i, j) - dt * rdx * (AT(p, k, i + 1, j) - AT(p, k, i, j));
+            (i == nx) ? 0.0 : AT(ub, k, i, j) - dt * rdx * (AT(p, k, i + 1, j) - AT(p, k, i, j));
         *s3(&vn, k, i, j) =
-            (j == ny) ? 0.0 : AT(v, k, i, j) - dt * rdy * (AT(p, k, i, j + 1) - AT(p, k, i, j));
+            (j == ny) ? 0.0 : AT(vb, k, i, j) - dt * rdy * (AT(p, k, i, j + 1) - AT(p, k, i, j));
       }
   /* region 6: pressure after the horizontal divergence */
 #pragma omp parallel for schedule(static)
@@ -322,7 +327,7 @@ int ora_dycore_step(const ora_dyn_params* q, ora_view rho, ora_view th, ora_view
       for (int64_t k = 1; k <= nz; ++k) {
         double uw = (i == 1) ? 0.0 : *s3(&un, k, i - 1, j);
         double vs = (j == 1) ? 0.0 : *s3(&vn, k, i, j - 1);
-        *s3(&ps, k, i, j) = AT(p, k, i, j) - dt * cs2 * (rdx * (*s3(&un, k, i, j) - uw) +
+        *s3(&ps, k, i, j) = AT(pb, k, i, j) - dt * cs2 * (rdx * (*s3(&un, k, i, j) - uw) +
                                                           rdy * (*s3(&vn, k, i, j) - vs));
       }
   /* region 7: HE-VI Thomas sweep per column, then the pressure update */
@@ -336,7 +341,7 @@ int ora_dycore_step(const ora_dyn_params* q, ora_view rho, ora_view th, ora_view
         for (int64_t k = 1; k <= nz - 1; ++k) {
           double rf = 0.5 * (AT(rho, k, i, j) + AT(rho, k + 1, i, j));
           double beta = dt * dt * cs2 * rdz * rdz / rf;
-          double dd = AT(w, k, i, j) - dt * rdz * (*s3(&ps, k + 1, i, j) - *s3(&ps, k, i, j)) / rf;
+          double dd = AT(wb, k, i, j) - dt * rdz * (*s3(&ps, k + 1, i, j) - *s3(&ps, k, i, j)) / rf;
           dd = dd + dt * grav * (0.5 * (AT(th, k, i, j) + AT(th, k + 1, i, j)) - th0) / th0;
           double bb = 1.0 + 2.0 * beta;
           if (k == 1) {
@@ -376,6 +381,60 @@ int ora_dycore_step(const ora_dyn_params* q, ora_view rho, ora_view th, ora_view
         AT(w, k, i, j) = *s3(&wn, k, i, j);
         AT(p, k, i, j) = *s3(&pn, k, i, j);
       }
+  return 0;
+}
+
+int ora_dycore_step(const ora_dyn_params* q, ora_view rho, ora_view th, ora_view u, ora_view v,
+                    ora_view w, ora_view p) {
+  return dycore_stage(q, q->dt, rho, th, u, v, w, p, th, u, v, w, p);
+}
+
+/* dycore.h90 rk3_step: base copies (routine locals), three stages */
+static double* g_base[5];
+static size_t g_base_n;
+
+int ora_rk3_step(const ora_dyn_params* q, ora_view rho, ora_view th, ora_view u, ora_view v,
+                 ora_view w, ora_view p) {
+  const int64_t nx = q->nx, ny = q->ny, nz = q->nz;
+  const size_t n = (size_t)(nx * ny * nz);
+  if (g_base_n < n) {
+    for (int f = 0; f < 5; ++f) {
+      free(g_base[f]);
+      g_base[f] = (double*)malloc(sizeof(double) * n);
+      if (!g_base[f]) return -2;
+    }
+    g_base_n = n;
+  }
+  /* base views: (k, i, j) dense, j fastest */
+  ora_view bv[5];
+  for (int f = 0; f < 5; ++f) {
+    bv[f].p = g_base[f];
+    bv[f].sk = nx * ny;
+    bv[f].si = ny;
+    bv[f].sj = 1;
+    bv[f].sl = 0;
+    bv[f].off = -(bv[f].sk + bv[f].si + bv[f].sj);
+  }
+  ora_view cur[5] = {th, u, v, w, p};
+#pragma omp parallel for schedule(static)
+  for (int64_t j = 1; j <= ny; ++j)
+    for (int64_t i = 1; i <= nx; ++i)
+      for (int64_t k = 1; k <= nz; ++k)
+        for (int f = 0; f < 5; ++f) AT(bv[f], k, i, j) = AT(cur[f], k, i, j);
+  const double dts[3] = {q->dt / 3.0, q->dt / 2.0, q->dt};
+  for (int s = 0; s < 3; ++s) {
+    int rc = dycore_stage(q, dts[s], rho, th, u, v, w, p, bv[0], bv[1], bv[2], bv[3], bv[4]);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+int ora_rk3_run(int64_t nsteps, const ora_dyn_params* prm, ora_view rho, ora_view th, ora_view u,
+                ora_view v, ora_view w, ora_view p) {
+  for (int64_t s = 0; s < nsteps; ++s) {
+    int rc = ora_rk3_step(prm, rho, th, u, v, w, p);
+    if (rc) return rc;
+  }
   return 0;
 }
 

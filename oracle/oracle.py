@@ -57,6 +57,8 @@ def lib():
         L.ora_grid_total.restype = dbl
         L.ora_dycore_run.argtypes = [i64, ctypes.POINTER(DynParams), V, V, V, V, V, V]
         L.ora_dycore_run.restype = ctypes.c_int
+        L.ora_rk3_run.argtypes = [i64, ctypes.POINTER(DynParams), V, V, V, V, V, V]
+        L.ora_rk3_run.restype = ctypes.c_int
         L.ora_full_run.argtypes = [i64, ctypes.POINTER(DynParams), dbl, dbl] + [V] * 8
         L.ora_full_run.restype = ctypes.c_int
         L.ora_fill.argtypes = [ctypes.c_void_p, i64, ctypes.c_uint64, dbl, dbl]
@@ -156,3 +158,14 @@ def full_run(nsteps, params, rho, th, u, v, w, p, tsfc, colm):
                             view(tsfc), view(colm))
     if rc:
         raise RuntimeError(f"ora_full_run failed ({rc})")
+
+
+def rk3_run(nsteps, params, rho, th, u, v, w, p):
+    """simulation_run_rk3: nsteps x rk3_step."""
+    nz, nx, ny = th.shape
+    prm = DynParams(nx, ny, nz, params["dt"], params["rdx"], params["rdy"], params["rdz"],
+                    params["cs2"], params["grav"], params["th0"])
+    rc = lib().ora_rk3_run(nsteps, ctypes.byref(prm), view(rho), view(th), view(u), view(v),
+                           view(w), view(p))
+    if rc:
+        raise RuntimeError(f"ora_rk3_run failed ({rc})")

@@ -310,6 +310,8 @@ struct StepTmemArgs {
   const double* tsfc;
   double* colm;
   double dt_rrelax, dt_ch;
+  // RK3 stages 2-3: the state at the start of the step (th, u, v, w, p; rho unused)
+  DynIn base;
   int64_t nj;
   int64_t row_lo, row_hi;
   DynConst c;
@@ -529,8 +531,8 @@ cudaError_t launch_dycore_step_tmem(const DynIn& in, const DynOut& out, Grid3 g,
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  StepTmemArgs a{in,  out,     g,   static_cast<int>(nz), 0, nullptr, nullptr, 0.0, 0.0, nj,
-                 -kIOff, g.pitch - kIOff - 1, c, sp};
+  StepTmemArgs a{in,  out,     g,      static_cast<int>(nz), 0, nullptr, nullptr, 0.0, 0.0,
+                 DynIn{}, nj, -kIOff, g.pitch - kIOff - 1, c, sp};
   dim3 block(kTX, kTY);
   dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
             static_cast<unsigned>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY));
@@ -577,8 +579,9 @@ __device__ __forceinline__ double face_flux_up(int64_t f, int64_t n, double vel,
   return fv;
 }
 
-template <bool kPhys>
+template <bool kPhys, bool kRK>
 __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
+  static_assert(!(kPhys && kRK), "column physics is not fused into RK stages");
   extern __shared__ __align__(128) double smem[];
   __shared__ uint32_t tmem_base_slot;
   double* ring = smem;
@@ -673,6 +676,29 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
   double rho_prev = 0.0, ps_prev = 0.0, cp_prev = 0.0, dp_prev = 0.0;  // acoustic
   double fz_prev = 0.0;                            // advection
   double phys_cs = 0.0, phys_cm = 0.0, colm_ij = 0.0, tsfc_ij = 0.0;  // column physics
+  // RK stage: base-state values of this column (one level prefetched in registers)
+  struct BaseLevel {
+    double th, u, uw, v, vs, p, w;
+  };
+  auto base_load = [&](int k) {
+    BaseLevel b{};
+    if (kRK && k < nz && active) {
+      const int64_t o = col + static_cast<int64_t>(k) * P;
+      if (acoustic) {
+        b.u = __ldg(a.base.u + o);
+        b.uw = __ldg(a.base.u + o - 1);
+        b.v = __ldg(a.base.v + o);
+        b.vs = __ldg(a.base.v + o - W);
+        b.p = __ldg(a.base.p + o);
+        b.w = __ldg(a.base.w + o);
+      } else {
+        b.th = __ldg(a.base.th + o);
+      }
+    }
+    return b;
+  };
+  BaseLevel bcur = base_load(0);
+  double wb_prev = 0.0;  // base w of the previous level (RK: the HE-VI right-hand side)
   if (kPhys && !acoustic && active) {
     colm_ij = a.colm[(j - 1) * W + (i - 1)];
     tsfc_ij = a.tsfc[(j - 1) * W + (i - 1)];
@@ -700,6 +726,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
 
   auto level = [&](int k, auto interior_tag) {
     constexpr bool kIn = decltype(interior_tag)::value;
+    const BaseLevel bnext = base_load(k + 1);
     const int kk = k + 1;
     const int s1 = s0 == kWsStages - 1 ? 0 : s0 + 1;
     const int s2 = s1 == kWsStages - 1 ? 0 : s1 + 1;
@@ -714,15 +741,16 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
       const double* Pp = S + kFOffP + (row + 1) * kPW + (lane + 2);
       const double pk = Pp[0], pe = Pp[1], pw = Pp[-1], pnn = Pp[kPW], psth = Pp[-kPW];
       const double rhok = S[kFOffRho + row * kSW + lane];
-      const double unk0 = ui - c.dt_rdx * (pe - pk);
-      const double vnk0 = vj - c.dt_rdy * (pnn - pk);
-      const double uw0 = uim1 - c.dt_rdx * (pk - pw);
-      const double vs0 = vjm1 - c.dt_rdy * (pk - psth);
+      // PGF applied to the base momentum (RK) or the current one (single stage)
+      const double unk0 = (kRK ? bcur.u : ui) - c.dt_rdx * (pe - pk);
+      const double vnk0 = (kRK ? bcur.v : vj) - c.dt_rdy * (pnn - pk);
+      const double uw0 = (kRK ? bcur.uw : uim1) - c.dt_rdx * (pk - pw);
+      const double vs0 = (kRK ? bcur.vs : vjm1) - c.dt_rdy * (pk - psth);
       const double unk = (!kIn && east) ? 0.0 : unk0;
       const double vnk = (!kIn && north) ? 0.0 : vnk0;
       const double uw = (!kIn && west) ? 0.0 : uw0;
       const double vs = (!kIn && south) ? 0.0 : vs0;
-      const double psk = pk - c.dt_cs2 * (c.rdx * (unk - uw) + c.rdy * (vnk - vs));
+      const double psk = (kRK ? bcur.p : pk) - c.dt_cs2 * (c.rdx * (unk - uw) + c.rdy * (vnk - vs));
       if (kIn || active) {
         *out_u = unk;
         *out_v = vnk;
@@ -735,7 +763,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
       if (k >= 1) {
         const double rf = 0.5 * (rho_prev + rhok);
         const double beta = c.beta_num / rf;
-        double dd = w_prev - c.dt_rdz * (psk - ps_prev) / rf;
+        double dd = (kRK ? wb_prev : w_prev) - c.dt_rdz * (psk - ps_prev) / rf;
         dd = dd + c.dt_grav * (0.5 * (th_prev + tk) - c.th0) / c.th0;
         pend_beta = beta;
         pend_bb = 1.0 + 2.0 * beta;
@@ -743,6 +771,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
       }
       rho_prev = rhok;
       ps_prev = psk;
+      if (kRK) wb_prev = bcur.w;
     } else if (!acoustic && (a.debug_skip & 1) == 0) {
       const double* T0 = S + kFOffTh + thc;
       const double tkp1 = (kk + 1 <= nz) ? ring[s1 * kFStageDoubles + kFOffTh + thc] : 0.0;
@@ -764,7 +793,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
       flux = flux + c.rdz * (fzk - fz_prev);
       double div = c.rdx * (ue - uwf) + c.rdy * (vnf - vsf);
       div = div + c.rdz * (wt - wb);
-      double thv = tk - c.dt * (flux - tk * div);
+      double thv = (kRK ? bcur.th : tk) - c.dt * (flux - tk * div);
       if (kPhys) {  // column_physics (dycore.h90), applied to the new theta of this level
         thv = thv - a.dt_rrelax * (thv - colm_ij);
         if (kk == 1) {  // new u, v at the lowest level (region 5), recomputed from the plane
@@ -787,6 +816,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
     out_th += P;
     out_u += P;
     out_v += P;
+    bcur = bnext;
   };
 
 #pragma unroll 1
@@ -846,25 +876,29 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
 
 cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                   int64_t nj, const DynConst& c, const Span& sp,
-                                  cudaStream_t s, const PhysArgs* phys) {
+                                  cudaStream_t s, const PhysArgs* phys, const DynIn* base) {
   if (sp.ihi < sp.ilo || sp.jhi < sp.jlo) return cudaSuccess;
   if (!dycore_step_tmem_fits(nz)) return cudaErrorInvalidValue;
+  if (phys && base) return cudaErrorInvalidValue;
   const size_t smem = std::max<size_t>((static_cast<size_t>(kWsStages) * kFStageDoubles +
                                         static_cast<size_t>(nz) * kThreads) * sizeof(double),
                                        80 * 1024);
-  auto kern = phys ? k_dyn_step_ws<true> : k_dyn_step_ws<false>;
-  static size_t configured[2] = {0, 0};
-  if (smem > configured[phys ? 1 : 0]) {
+  const int variant = phys ? 1 : base ? 2 : 0;
+  void (*kern)(StepTmemArgs) = variant == 1   ? k_dyn_step_ws<true, false>
+                               : variant == 2 ? k_dyn_step_ws<false, true>
+                                              : k_dyn_step_ws<false, false>;
+  static size_t configured[3] = {0, 0, 0};
+  if (smem > configured[variant]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    configured[phys ? 1 : 0] = smem;
+    configured[variant] = smem;
   }
   static const int debug_skip = getenv("HFB_DEBUG_SKIP") ? atoi(getenv("HFB_DEBUG_SKIP")) : 0;
   StepTmemArgs a{in, out, g, static_cast<int>(nz), debug_skip,
                  phys ? phys->tsfc : nullptr, phys ? phys->colm : nullptr,
                  phys ? phys->dt_rrelax : 0.0, phys ? phys->dt_ch : 0.0,
-                 nj, -kIOff, g.pitch - kIOff - 1, c, sp};
+                 base ? *base : DynIn{}, nj, -kIOff, g.pitch - kIOff - 1, c, sp};
   dim3 block(kTX, 2 * kTY);
   dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
             static_cast<unsigned>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY));

@@ -96,9 +96,11 @@ struct PhysArgs {
 };
 // warp-specialised variant (acoustic warps + advection warps per tile); with `phys` the
 // column physics is fused into the advection warps (the full timestep in one kernel)
+// with `base` it is an RK stage: tendencies at `in`, applied to the base state
 cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                   int64_t nj, const DynConst& c, const Span& sp,
-                                  cudaStream_t s, const PhysArgs* phys = nullptr);
+                                  cudaStream_t s, const PhysArgs* phys = nullptr,
+                                  const DynIn* base = nullptr);
 // standalone column physics on the current state (th updated in place)
 cudaError_t launch_column_physics(const double* rho, double* th, const double* u,
                                   const double* v, Grid3 g, int64_t nz, const DynConst& c,

@@ -199,14 +199,16 @@ struct Slot {
   bool pinned = false;
   // device side
   Layout lay;
-  double* dev[2] = {nullptr, nullptr};
+  double* dev[3] = {nullptr, nullptr, nullptr};  // [2] only for RK3 stage states
   int cur = 0;
   bool has_device = false;
   Residency res = kHost;
   cudaStream_t stream = nullptr;  // owning context's stream
 
   double* d() const { return dev[cur] + lay.origin_off; }
-  double* d_alt() const { return dev[1 - cur] + lay.origin_off; }
+  int alt() const { return cur == 0 ? 1 : 0; }
+  double* d_alt() const { return dev[alt()] + lay.origin_off; }
+  double* d_buf(int b) const { return dev[b] + lay.origin_off; }
 };
 
 }  // namespace
@@ -244,6 +246,7 @@ struct hfb_ctx {
   cudaGraphExec_t graph_exec = nullptr;
   std::string graph_key;
   hfb_launch_stats graph_stats{};
+  std::map<std::string, int> graph_cur0, graph_cur1;
   // A/B switches: portable kernels only / the two-kernel (advect + acoustic) split
   bool force_generic = getenv("HFB_GENERIC_KERNELS") != nullptr;
   bool force_split = getenv("HFB_SPLIT_STEP") != nullptr;
@@ -335,13 +338,14 @@ void role_extents(const Slot& s, int64_t ext[4], int64_t hs[4]) {
   }
 }
 
-void ensure_device(hfb_ctx* c, Slot& s, bool second) {
+void ensure_device(hfb_ctx* c, Slot& s, bool second, int nbuf = 0) {
   if (!s.dev[0]) {
     int64_t ext[4], hs[4];
     role_extents(s, ext, hs);
     s.lay = Layout::make(ext[kRoleI], ext[kRoleJ], ext[kRoleK], ext[kRoleL]);
   }
-  for (int b = 0; b < (second ? 2 : 1); ++b) {
+  const int want = nbuf ? nbuf : (second ? 2 : 1);
+  for (int b = 0; b < want; ++b) {
     if (s.dev[b]) continue;
     size_t bytes = static_cast<size_t>(s.lay.alloc_elems) * sizeof(double);
     cuda_check(cudaMalloc(&s.dev[b], bytes), "cudaMalloc(device array)");
@@ -537,7 +541,7 @@ void diffusion_step(hfb_ctx* c, Stats& st, bool write_t_new) {
   // hfk0 (stencil into the alternate t_old buffer [+ t_new]) then hfk1 fused away
   launch(c, st, "hfk0_diffuse_step", [&] { return launch_diffusion(to.d(), to.d_alt(), write_t_new ? tn.d() : nullptr, grid_of(to), nz,
                             coef, sp, c->stream); });
-  to.cur = 1 - to.cur;
+  to.cur = to.alt();
   count_launch(st, nx, ny);
   count_launch(st, nx, ny);
   dev_written(c, "t_new");
@@ -791,7 +795,7 @@ void dycore_step(hfb_ctx* c, Stats& st, bool with_physics = false) {
         return launch_dycore_acoustic(in, out, grid_of(th), nz, k, sp, c->stream);
       });
   }
-  for (Slot* s : {&th, &u, &v, &w, &p}) s->cur = 1 - s->cur;
+  for (Slot* s : {&th, &u, &v, &w, &p}) s->cur = s->alt();
   // the generated code's 8 launches (dycore.h90 regions; region 1 spans i = 0..nx,
   // region 2 spans j = 0..ny)
   count_launch(st, nx + 1, ny);
@@ -806,6 +810,60 @@ void dycore_step(hfb_ctx* c, Stats& st, bool with_physics = false) {
       column_physics(c, st);
     }
   }
+}
+
+// dycore.h90 rk3_step: Wicker-Skamarock RK3 with three native stage launches.
+// Buffers per prognostic field: base (the state at the start of the step, left intact),
+// s1 and s2 (stage states); the new state ends in s1.
+void rk3_step(hfb_ctx* c, Stats& st) {
+  int64_t nx = ival(c, "nx"), ny = ival(c, "ny"), nz = ival(c, "nz");
+  if (!dycore_step_tmem_fits(nz))
+    fail(HFB_CONFIG, "rk3_step is implemented for 2 <= nz <= 65 (got %lld)", (long long)nz);
+  if (c->decomposed && c->decomp.px * c->decomp.py > 1 && c->decomp.halo < 2)
+    fail(HFB_CONFIG, "rk3_step needs a halo of 2 cells, got %d", c->decomp.halo);
+  if (c->group)  // stage states are overwritten within a step: needs true rank lockstep
+    fail(HFB_CONFIG, "rk3_step runs decomposed with one process per rank (NCCL), not in "
+                     "an in-process group");
+  const double dt = rval(c, "dt");
+  for (const char* n : {"th", "u", "v", "w", "p", "rho"}) dev_read(c, n);
+  Slot &rho = slot(c, "rho"), &th = slot(c, "th"), &u = slot(c, "u"), &v = slot(c, "v"),
+       &w = slot(c, "w"), &p = slot(c, "p");
+  Slot* prog[5] = {&th, &u, &v, &w, &p};
+  for (Slot* s : prog) ensure_device(c, *s, true, 3);
+  const int b = th.cur;
+  for (Slot* s : prog)
+    if (s->cur != b) fail(HFB_RUNTIME, "prognostic buffers out of step");
+  const int s1 = (b + 1) % 3, s2 = (b + 2) % 3;
+  auto state = [&](int buf) {
+    return DynIn{rho.d(), th.d_buf(buf), u.d_buf(buf), v.d_buf(buf), w.d_buf(buf), p.d_buf(buf)};
+  };
+  auto outs = [&](int buf) {
+    return DynOut{th.d_buf(buf), u.d_buf(buf), v.d_buf(buf), w.d_buf(buf), p.d_buf(buf)};
+  };
+  const DynIn base = state(b);
+  const double dts[3] = {dt / 3.0, dt / 2.0, dt};  // dycore.h90 rk3_step `dtf`
+  const int cur_of[3] = {b, s1, s2}, out_of[3] = {s1, s2, s1};
+  Span sp = full_span(c, nx, ny);
+  // the generated code's launches: the base copy region, then 8 regions per stage
+  count_launch(st, nx, ny);
+  for (int g = 0; g < 3; ++g) {
+    // halos of the stage state (the current buffers of this stage)
+    for (Slot* s : prog) s->cur = cur_of[g];
+    halo_exchange(c, {"th", "u", "v", "p"}, kHalo);
+    DynConst k = make_dyn_const(dts[g], rval(c, "rdx"), rval(c, "rdy"), rval(c, "rdz"),
+                                rval(c, "cs2"), rval(c, "grav"), rval(c, "th0"));
+    const DynIn in = state(cur_of[g]);
+    const DynOut out = outs(out_of[g]);
+    launch(c, st, "rk3_stage", [&] {
+      return launch_dycore_step_ws(in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream,
+                                   nullptr, g == 0 ? nullptr : &base);
+    });
+    count_launch(st, nx + 1, ny);
+    count_launch(st, nx, ny + 1);
+    for (int r = 0; r < 6; ++r) count_launch(st, nx, ny);
+  }
+  for (Slot* s : prog) s->cur = s1;
+  for (const char* n : {"th", "u", "v", "w", "p"}) dev_written(c, n);
 }
 
 void dycore_entry(hfb_ctx* c, const std::string& r, Stats& st) {
@@ -825,6 +883,13 @@ void dycore_entry(hfb_ctx* c, const std::string& r, Stats& st) {
     for (const char* n : full_names) do_copy_from_device(c, slot(c, n));
   } else if (r == "full_step") {
     dycore_step(c, st, true);
+  } else if (r == "rk3_step") {
+    rk3_step(c, st);
+  } else if (r == "main_rk3" || r == "simulation_run_rk3") {
+    int64_t nsteps = ival(c, "nsteps");
+    for (const char* n : names) do_copy_to_device(c, slot(c, n));
+    for (int64_t s = 0; s < nsteps; ++s) rk3_step(c, st);
+    for (const char* n : names) do_copy_from_device(c, slot(c, n));
   } else if (r == "column_physics") {
     column_physics(c, st);
   } else {
@@ -844,7 +909,8 @@ EntryFn entry_fn(const std::string& app) {
 }
 
 bool entry_has_transfers(const std::string& app, const std::string& r) {
-  if (r == "main" || r == "simulation_run" || r == "main_full" || r == "simulation_run_full")
+  if (r == "main" || r == "simulation_run" || r == "main_full" || r == "simulation_run_full" ||
+      r == "main_rk3" || r == "simulation_run_rk3")
     return true;
   (void)app;
   return false;
@@ -1317,13 +1383,13 @@ hfb_status hfb_run_graph(hfb_ctx* c, const char* entry, int64_t steps, hfb_launc
     // Capture `steps` steps; an even step count returns every double buffer to its
     // starting side, so the graph can be replayed; odd counts are re-captured.
     std::string key = r + ":" + std::to_string(steps);
-    // no allocation may happen during capture: materialise every double buffer first
+    // no allocation may happen during capture: materialise every buffer first
     for (auto& [n, s] : c->slots)
-      if (s.decl->pingpong && s.has_device) ensure_device(c, s, true);
+      if (s.decl->pingpong && s.has_device) ensure_device(c, s, true, r == "rk3_step" ? 3 : 0);
     cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
     std::map<std::string, int> cur0;
     for (auto& [n, s] : c->slots) cur0[n] = s.cur;
-    if (c->graph_key != key || steps % 2) {
+    if (c->graph_key != key || c->graph_cur0 != cur0) {
       if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
       c->graph_exec = nullptr;
       c->graph_key.clear();
@@ -1345,15 +1411,15 @@ hfb_status hfb_run_graph(hfb_ctx* c, const char* entry, int64_t steps, hfb_launc
       cuda_check(cudaGraphInstantiate(&c->graph_exec, g, 0), "cudaGraphInstantiate");
       cudaGraphDestroy(g);
       c->graph_key = key;
+      c->graph_cur0 = cur0;
+      c->graph_cur1.clear();
+      for (auto& [n, s] : c->slots) c->graph_cur1[n] = s.cur;  // buffer sides after the steps
       c->graph_stats = hfb_launch_stats{st.launches, st.threads, st.guard_returns, st.native};
-      // capture recorded the launches without running them: roll the buffer sides back
-      for (auto& [n, s] : c->slots) s.cur = cur0[n];
+      // a graph whose steps do not return every buffer to its side is single-use
+      if (c->graph_cur1 != cur0) c->graph_key += ":once";
     }
     cuda_check(cudaGraphLaunch(c->graph_exec, c->stream), "cudaGraphLaunch");
-    // advance the double-buffer sides exactly as the captured steps did
-    for (int64_t s = 0; s < steps; ++s)
-      for (auto& [n, sl] : c->slots)
-        if (sl.decl->pingpong && sl.dev[1]) sl.cur = 1 - sl.cur;
+    for (auto& [n, sl] : c->slots) sl.cur = c->graph_cur1[n];
     cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
     if (stats) *stats = c->graph_stats;
   });

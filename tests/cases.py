@@ -61,6 +61,11 @@ APPS = {
         "dycore", [("own", "dycore/dyn_state.h90"), ("own", "dycore/dycore.h90")], "dyn_state",
         {n: ("nz", "nx", "ny") for n in ("rho", "th", "u", "v", "w", "p")},
         ["th", "u", "v", "w", "p", "rho"]),
+    # the dynamics with Wicker-Skamarock RK3 (entry main_rk3)
+    "dycore_rk3": App(
+        "dycore_rk3", [("own", "dycore/dyn_state.h90"), ("own", "dycore/dycore.h90")],
+        "dyn_state", {n: ("nz", "nx", "ny") for n in ("rho", "th", "u", "v", "w", "p")},
+        ["th", "u", "v", "w", "p"], entry="main_rk3", program="dycore"),
     # the full timestep: dycore + column physics (entry main_full)
     "dycore_full": App(
         "dycore_full", [("own", "dycore/dyn_state.h90"), ("own", "dycore/dycore.h90")],
@@ -106,6 +111,11 @@ def _full(name, nx, ny, nz, nsteps, gpu_check=True):
     return Case(name, "dycore_full", dict(nx=nx, ny=ny, nz=nz, nsteps=nsteps),
                 dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS),
                 gpu_check=gpu_check)
+
+
+def _rk3(name, nx, ny, nz, nsteps, gpu_check=True):
+    return Case(name, "dycore_rk3", dict(nx=nx, ny=ny, nz=nz, nsteps=nsteps),
+                dict(DYCORE_SCALARS), dict(DYCORE_FILLS), gpu_check=gpu_check)
 
 
 CASES = [
@@ -154,5 +164,9 @@ CASES = [
     _full("full_24x20x12_s2", 24, 20, 12, 2),
     _full("full_1x5x2_s2", 1, 5, 2, 2),
     _full("full_33x3x58_s1", 33, 3, 58, 1),
+    _rk3("rk3_13x7x10_s2", 13, 7, 10, 2),
+    _rk3("rk3_24x20x12_s1", 24, 20, 12, 1),
+    _rk3("rk3_1x5x2_s2", 1, 5, 2, 2),
+    _rk3("rk3_33x3x58_s1", 33, 3, 58, 1),
 ]
 CASE_BY_NAME = {c.name: c for c in CASES}

@@ -68,6 +68,8 @@ def run_oracle(case, arrs):
                 "total_accsim": oracle.grid_total(a["y"], 0.0, mode=1)}
     elif case.app == "dycore":
         oracle.dycore_run(i["nsteps"], r, a["rho"], a["th"], a["u"], a["v"], a["w"], a["p"])
+    elif case.app == "dycore_rk3":
+        oracle.rk3_run(i["nsteps"], r, a["rho"], a["th"], a["u"], a["v"], a["w"], a["p"])
     elif case.app == "dycore_full":
         oracle.full_run(i["nsteps"], r, a["rho"], a["th"], a["u"], a["v"], a["w"], a["p"],
                         a["tsfc"], a["colm"])

@@ -89,6 +89,10 @@ LARGE = [
          dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
     Case("dycore_31x7x2_s3", "dycore", dict(nx=31, ny=7, nz=2, nsteps=3),
          dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
+    Case("rk3_128x96x58_s2", "dycore_rk3", dict(nx=128, ny=96, nz=58, nsteps=2),
+         dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
+    Case("rk3_77x41x31_s3", "dycore_rk3", dict(nx=77, ny=41, nz=31, nsteps=3),
+         dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
     Case("full_128x96x58_s3", "dycore_full", dict(nx=128, ny=96, nz=58, nsteps=3),
          dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS)),
     Case("full_45x37x80_s2", "dycore_full", dict(nx=45, ny=37, nz=80, nsteps=2),
@@ -230,6 +234,34 @@ def test_graph_replay_matches_step_loop():
         assert st.native_launches == 2  # one fused kernel per timestep
         eng.run_graph("dycore_step", 2)
         eng.run_graph("dycore_step", 2)
+        for k in arrs:
+            eng.copy_from_device(k)
+    for k in ("th", "u", "v", "w", "p"):
+        assert bits_equal(arrs[k], ref[k]), k
+
+
+def test_rk3_graph_replay_and_mixed_steps():
+    """RK3 steps (3 buffers per field) in a CUDA graph, mixed with single-stage steps."""
+    case = Case("g", "dycore", dict(nx=96, ny=64, nz=58, nsteps=1), dict(DYCORE_SCALARS),
+                dict(DYCORE_FILLS))
+    arrs = make_inputs(case)
+    import oracle
+    ref = {k: v.copy() for k, v in arrs.items()}
+    oracle.rk3_run(2, DYCORE_SCALARS, *(ref[k] for k in ("rho", "th", "u", "v", "w", "p")))
+    oracle.dycore_run(1, DYCORE_SCALARS, *(ref[k] for k in ("rho", "th", "u", "v", "w", "p")))
+    oracle.rk3_run(3, DYCORE_SCALARS, *(ref[k] for k in ("rho", "th", "u", "v", "w", "p")))
+    with hfb.Engine("dycore") as eng:
+        for k, v in case.ints.items():
+            eng.set(k, v)
+        for k, v in case.reals.items():
+            eng.set(k, v)
+        for k, a in arrs.items():
+            eng.bind(k, a)
+            eng.copy_to_device(k)
+        st = eng.run_graph("rk3_step", 2)
+        assert st.launches == 50 and st.native_launches == 6
+        eng.run("dycore_step")
+        eng.run_graph("rk3_step", 3)
         for k in arrs:
             eng.copy_from_device(k)
     for k in ("th", "u", "v", "w", "p"):
