@@ -26,6 +26,7 @@
 
 #include "hfb_kernels.cuh"
 #include "hfb_sm100.cuh"
+#include "hfb_fp64.cuh"
 
 namespace hfb {
 
@@ -705,11 +706,18 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
   }
   double pend_beta = 0.0, pend_bb = 1.0, pend_dd = 0.0;  // face awaiting its recursion step
   int s0 = 0;  // ring slot of level k
+  const fp64::Recip rth0 = fp64::recip(c.th0);
 
   // Thomas forward recursion for face f (dialect face kf = f + 1) from the pending
-  // coefficients; cp/dp go to this thread's TMEM lane
-  auto thomas_step = [&](int f) {
-    double cpk, dpk;
+  // coefficients (quotients by m share one reciprocal; `ok` guards the fast path)
+  auto thomas_fast = [&](int f, double& cpk, double& dpk, bool& ok) {
+    const double m = f == 0 ? pend_bb : pend_bb + pend_beta * cp_prev;
+    const double num = f == 0 ? pend_dd : pend_dd + pend_beta * dp_prev;
+    const fp64::Recip rm = fp64::recip(m);
+    cpk = fp64::quot(-pend_beta, rm, ok);
+    dpk = fp64::quot(num, rm, ok);
+  };
+  auto thomas_div = [&](int f, double& cpk, double& dpk) {  // the dialect's divisions
     if (f == 0) {
       cpk = -pend_beta / pend_bb;
       dpk = pend_dd / pend_bb;
@@ -718,6 +726,9 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
       cpk = -pend_beta / m;
       dpk = (pend_dd + pend_beta * dp_prev) / m;
     }
+  };
+  // cp/dp of face f go to this thread's TMEM lane
+  auto thomas_commit = [&](int f, double cpk, double dpk) {
     sm100::tmem_st_f64(tmem + 2 * f, cpk);
     sm100::tmem_st_f64(tmem + kDpCol + 2 * f, dpk);
     cp_prev = cpk;
@@ -759,12 +770,30 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
       // The Thomas recursion for face f = k-2 (its coefficients were formed in the
       // previous iteration) runs here, independent of this iteration's coefficient
       // formation for face k-1: the two division chains overlap instead of adding up.
-      if (k >= 2) thomas_step(k - 2);
+      bool ok = true;
+      double cpk = 0.0, dpk = 0.0, beta = 0.0, dd = 0.0;
+      if (k >= 2) thomas_fast(k - 2, cpk, dpk, ok);
+      const double w_rhs = kRK ? wb_prev : w_prev;
+      const double n_ps = c.dt_rdz * (psk - ps_prev);
+      const double n_th = c.dt_grav * (0.5 * (th_prev + tk) - c.th0);
       if (k >= 1) {
         const double rf = 0.5 * (rho_prev + rhok);
-        const double beta = c.beta_num / rf;
-        double dd = (kRK ? wb_prev : w_prev) - c.dt_rdz * (psk - ps_prev) / rf;
-        dd = dd + c.dt_grav * (0.5 * (th_prev + tk) - c.th0) / c.th0;
+        const fp64::Recip rr = fp64::recip(rf);
+        beta = fp64::quot(c.beta_num, rr, ok);
+        dd = w_rhs - fp64::quot(n_ps, rr, ok);
+        dd = dd + fp64::quot(n_th, rth0, ok);
+      }
+      if (__builtin_expect(!ok, 0)) {  // a range check failed: the dialect's divisions
+        if (k >= 2) thomas_div(k - 2, cpk, dpk);
+        if (k >= 1) {
+          const double rf = 0.5 * (rho_prev + rhok);
+          beta = c.beta_num / rf;
+          dd = w_rhs - n_ps / rf;
+          dd = dd + n_th / c.th0;
+        }
+      }
+      if (k >= 2) thomas_commit(k - 2, cpk, dpk);
+      if (k >= 1) {
         pend_beta = beta;
         pend_bb = 1.0 + 2.0 * beta;
         pend_dd = dd;
@@ -832,7 +861,13 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
     else
       level(k, std::false_type{});
   }
-  if (acoustic && nz >= 2) thomas_step(nz - 2);  // drain the last face
+  if (acoustic && nz >= 2) {  // drain the last face
+    bool ok = true;
+    double cpk, dpk;
+    thomas_fast(nz - 2, cpk, dpk, ok);
+    if (!ok) thomas_div(nz - 2, cpk, dpk);
+    thomas_commit(nz - 2, cpk, dpk);
+  }
   sm100::cp_async_wait<0>();
   if (kPhys && !acoustic && active) a.colm[(j - 1) * W + (i - 1)] = phys_cs / phys_cm;
 

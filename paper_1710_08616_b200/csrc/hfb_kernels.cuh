@@ -101,6 +101,12 @@ cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, i
                                   int64_t nj, const DynConst& c, const Span& sp,
                                   cudaStream_t s, const PhysArgs* phys = nullptr,
                                   const DynIn* base = nullptr);
+// the same step fed by TMA through mbarriers (hfb_dycore_tma.cu): measured slower than the
+// cp.async-fed launch_dycore_step_ws, kept as the HFB_TMA_STEP=1 variant
+cudaError_t launch_dycore_step_tma(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
+                                   int64_t nj, const DynConst& c, const Span& sp,
+                                   cudaStream_t s, const PhysArgs* phys = nullptr,
+                                   const DynIn* base = nullptr);
 // standalone column physics on the current state (th updated in place)
 cudaError_t launch_column_physics(const double* rho, double* th, const double* u,
                                   const double* v, Grid3 g, int64_t nz, const DynConst& c,

@@ -251,6 +251,7 @@ struct hfb_ctx {
   bool force_generic = getenv("HFB_GENERIC_KERNELS") != nullptr;
   bool force_split = getenv("HFB_SPLIT_STEP") != nullptr;
   bool force_single_role = getenv("HFB_SINGLE_ROLE") != nullptr;
+  bool force_tma = getenv("HFB_TMA_STEP") != nullptr;
   // per-kernel CUDA-event timing (hfb_profile)
   bool prof = false;
   bool capturing = false;
@@ -746,6 +747,15 @@ void column_physics(hfb_ctx* c, Stats& st) {
   for (const char* n : {"th", "colm"}) dev_written(c, n);
 }
 
+// the fused warp-specialised step: cp.async-fed (product) or its TMA twin (measured
+// slower, hfb_dycore_tma.cu)
+cudaError_t launch_step(hfb_ctx* c, const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
+                        int64_t nj, const DynConst& k, const Span& sp, cudaStream_t s,
+                        const PhysArgs* phys = nullptr, const DynIn* base = nullptr) {
+  return c->force_tma ? launch_dycore_step_tma(in, out, g, nz, nj, k, sp, s, phys, base)
+                      : launch_dycore_step_ws(in, out, g, nz, nj, k, sp, s, phys, base);
+}
+
 void dycore_step(hfb_ctx* c, Stats& st, bool with_physics = false) {
   int64_t nx = ival(c, "nx"), ny = ival(c, "ny"), nz = ival(c, "nz");
   if (nz < 2) fail(HFB_RUNTIME, "dycore_step needs nz >= 2 (got %lld)", (long long)nz);
@@ -773,13 +783,13 @@ void dycore_step(hfb_ctx* c, Stats& st, bool with_physics = false) {
     else if (with_physics) {
       PhysArgs ph = phys_args(c, slot(c, "tsfc"), slot(c, "colm"));
       launch(c, st, "full_step", [&] {
-        return launch_dycore_step_ws(in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream,
+        return launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream,
                                      &ph);
       });
       fused_physics = true;
     } else
       launch(c, st, "dycore_step", [&] {
-        return launch_dycore_step_ws(in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
+        return launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
       });
   } else {
     launch(c, st, "dycore_advect", [&] {
@@ -855,7 +865,7 @@ void rk3_step(hfb_ctx* c, Stats& st) {
     const DynIn in = state(cur_of[g]);
     const DynOut out = outs(out_of[g]);
     launch(c, st, "rk3_stage", [&] {
-      return launch_dycore_step_ws(in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream,
+      return launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream,
                                    nullptr, g == 0 ? nullptr : &base);
     });
     count_launch(st, nx + 1, ny);

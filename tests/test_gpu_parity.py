@@ -142,6 +142,38 @@ def test_single_role_fused_matches(monkeypatch):
                         dict(DYCORE_SCALARS), dict(DYCORE_FILLS)))
 
 
+@pytest.mark.parametrize("app", ["dycore", "dycore_full", "dycore_rk3"])
+def test_tma_step_matches(monkeypatch, app):
+    """The TMA-fed twin of the fused step (HFB_TMA_STEP=1) gives the same bits."""
+    monkeypatch.setenv("HFB_TMA_STEP", "1")
+    reals = dict(DYCORE_SCALARS, **PHYS_SCALARS) if app == "dycore_full" else dict(DYCORE_SCALARS)
+    fills = dict(DYCORE_FILLS, **PHYS_FILLS) if app == "dycore_full" else dict(DYCORE_FILLS)
+    _oracle_vs_gpu(Case(f"{app}_70x45x58_s2", app, dict(nx=70, ny=45, nz=58, nsteps=2),
+                        reals, fills))
+
+
+@pytest.mark.parametrize("app", ["dycore", "dycore_rk3"])
+@pytest.mark.parametrize("edge", ["th_eq_th0", "zero_w_p", "tiny"])
+def test_division_fast_path_edges(app, edge):
+    """HE-VI quotients share reciprocals (hfb_fp64.cuh) behind a range check; inputs that
+    fail it (zero numerators: theta == th0 makes dt*grav*(theta-th0) exactly 0, a resting
+    state makes the pressure-difference numerator 0; tiny magnitudes) take the dialect's
+    divisions. Bit-exact either way."""
+    fills = dict(DYCORE_FILLS)
+    reals = dict(DYCORE_SCALARS)
+    if edge == "th_eq_th0":
+        fills["th"] = (8, 300.0, 0.0)
+    elif edge == "zero_w_p":
+        for k in ("u", "v", "w", "p"):
+            fills[k] = (fills[k][0], 0.0, 0.0)
+    else:  # tiny pressure perturbations at rest: tiny and subnormal quotients
+        for k in ("u", "v", "w"):
+            fills[k] = (fills[k][0], 0.0, 0.0)
+        fills["p"] = (12, 0.0, 1e-300)
+    _oracle_vs_gpu(Case(f"{app}_{edge}_40x36x20_s2", app, dict(nx=40, ny=36, nz=20, nsteps=2),
+                        reals, fills))
+
+
 def test_generic_kernels_match(monkeypatch):
     """The portable acoustic kernel (HFB_GENERIC_KERNELS=1) gives the same bits."""
     monkeypatch.setenv("HFB_GENERIC_KERNELS", "1")
