@@ -13,8 +13,9 @@
 //     Thomas sweep; each thread owns one TMEM lane for its column's cp(k), dp(k).
 //   * warps 4-7 (ADVECTION) run the flux-limited advection of theta for the same rows
 //     (they read levels k..k+2 of th for the vertical faces).
-//   * one CTA barrier per level frees the slot of level k-1 for level k-1+kStages; a
-//     warp waits on a slot's mbarrier (parity = pass over the ring) before reading it.
+//   * warp 0 waits on the slot mbarrier of the newest level needed (parity = pass over
+//     the ring); one CTA barrier per level then publishes it and frees the slot of
+//     level k-1 for level k-1+kStages (the same sync structure as the cp.async twin).
 //   * MEASURED (512x512x58, B200): this kernel is SLOWER than its cp.async twin (0.414 vs
 //     0.379 ms per step) although its data-movement skeleton is faster (0.219 vs 0.235
 //     ms with both roles' arithmetic skipped), so the cp.async kernel stays the product
@@ -36,6 +37,7 @@
 #include "hfb_fp64.cuh"
 #include "hfb_kernels.cuh"
 #include "hfb_sm100.cuh"
+#include "hfb_tmap.cuh"
 
 namespace hfb {
 
@@ -239,7 +241,6 @@ __global__ void __launch_bounds__(kThreadsTma, 2)
     };
 
     int s0 = 0;
-    uint32_t ph0 = 0;  // parity of the current pass over the ring (slot s0)
     auto level = [&](int k, auto interior_tag) {
       constexpr bool kIn = decltype(interior_tag)::value;
       const BaseLevel bnext = base_load(k + 1);
@@ -351,29 +352,21 @@ __global__ void __launch_bounds__(kThreadsTma, 2)
       out_u += P;
       out_v += P;
       bcur = bnext;
-      if (s1 == 0) ph0 ^= 1u;
       s0 = s1;
     };
 
-    // the advection needs levels k+1 and k+2 too (its z faces); it waits for them
-    // one level at a time so that every slot is waited for exactly once per pass
-    if (!acoustic) {
-      sm100::mbar_wait(full0, 0);
-      if (nz > 1) sm100::mbar_wait(full0 + 8, 0);
-    }
+    // Warp 0 alone waits for the newest level anyone reads at level k (k+2: the
+    // advection's z faces; levels are waited in order, once each), then the CTA barrier
+    // publishes it to every warp (mbarrier acquire by warp 0, then bar.sync) and frees
+    // the slot of level k-1 for level k-1+kStages.
 #pragma unroll 1
     for (int k = 0; k < nz; ++k) {
-      if (k >= 1) {
-        // every warp is done with level k-1: its slot takes level k-1+kStages
-        __syncthreads();
-        if (tma_lane && k - 1 + kStages < nz) issue(k - 1 + kStages);
+      if (warp == 0) {
+        for (int l = k == 0 ? 0 : k + 2; l <= k + 2 && l < nz; ++l)
+          sm100::mbar_wait(full0 + 8 * (l % kStages), (l / kStages) & 1);
       }
-      if (acoustic) {
-        sm100::mbar_wait(full0 + 8 * s0, ph0);
-      } else if (k + 2 < nz) {
-        const int l = k + 2;
-        sm100::mbar_wait(full0 + 8 * (l % kStages), (l / kStages) & 1);
-      }
+      __syncthreads();
+      if (tma_lane && k >= 1 && k - 1 + kStages < nz) issue(k - 1 + kStages);
       if (interior)
         level(k, std::true_type{});
       else
@@ -425,7 +418,10 @@ __global__ void __launch_bounds__(kThreadsTma, 2)
   if (warp == 0) sm100::tmem_dealloc(tmem_base_slot, kTmemCols);
 }
 
+}  // namespace
+
 // ---- host: tensor maps ------------------------------------------------------------
+namespace {
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* p = nullptr;
@@ -439,10 +435,10 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 3-D map over a whole device array allocation (pitch x (nj + 2 halo rows) x nz), box
-// (bw, bh, 1); `origin` is the array's interior origin (Slot::d())
-bool make_map(CUtensorMap* m, const double* origin, Grid3 g, int64_t nj, int64_t nz, int bw,
-              int bh) {
+}  // namespace
+
+bool make_box_map(CUtensorMap* m, const double* origin, Grid3 g, int64_t nj, int64_t nz, int bw,
+                  int bh) {
   auto fn = encode_fn();
   if (!fn) return false;
   const double* base = origin - (kHalo * g.pitch + kIOff);
@@ -457,7 +453,6 @@ bool make_map(CUtensorMap* m, const double* origin, Grid3 g, int64_t nj, int64_t
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-}  // namespace
 
 cudaError_t launch_dycore_step_tma(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                    int64_t nj, const DynConst& c, const Span& sp,
@@ -466,12 +461,12 @@ cudaError_t launch_dycore_step_tma(const DynIn& in, const DynOut& out, Grid3 g, 
   if (!dycore_step_tmem_fits(nz)) return cudaErrorInvalidValue;
   if (phys && base) return cudaErrorInvalidValue;
   TmaMaps maps;
-  const bool ok = make_map(&maps.m[kMapTh], in.th, g, nj, nz, kThW, kThR) &&
-                  make_map(&maps.m[kMapU], in.u, g, nj, nz, kUW, kUR) &&
-                  make_map(&maps.m[kMapV], in.v, g, nj, nz, kVW, kVR) &&
-                  make_map(&maps.m[kMapW], in.w, g, nj, nz, kWW, kWR) &&
-                  make_map(&maps.m[kMapP], in.p, g, nj, nz, kPW, kPR) &&
-                  make_map(&maps.m[kMapRho], in.rho, g, nj, nz, kRW, kRR);
+  const bool ok = make_box_map(&maps.m[kMapTh], in.th, g, nj, nz, kThW, kThR) &&
+                  make_box_map(&maps.m[kMapU], in.u, g, nj, nz, kUW, kUR) &&
+                  make_box_map(&maps.m[kMapV], in.v, g, nj, nz, kVW, kVR) &&
+                  make_box_map(&maps.m[kMapW], in.w, g, nj, nz, kWW, kWR) &&
+                  make_box_map(&maps.m[kMapP], in.p, g, nj, nz, kPW, kPR) &&
+                  make_box_map(&maps.m[kMapRho], in.rho, g, nj, nz, kRW, kRR);
   if (!ok) return cudaErrorInvalidValue;
   // two CTAs per SM share its 512 TMEM columns; small-nz launches pad shared memory
   // so that a third CTA never blocks in tcgen05.alloc

@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "hfb_kernels.cuh"
@@ -645,22 +646,28 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
     dst[q] = ring_u32 + static_cast<uint32_t>(e) * 8u;
   }
   // levels are issued in order, once each: sources advance by one plane per call and the
-  // ring offset rotates (no per-level multiplies or modulo)
+  // ring offset rotates (no per-level multiplies or modulo). 528 chunks per level over
+  // 256 threads: two each, and a third for the first 16 threads (warp 0 only, so the
+  // other warps carry no third pointer).
+  static_assert(kFChunks > 2 * kWsThreads && kFChunks <= 2 * kWsThreads + kTX, "chunk split");
   uint32_t so = 0;
   constexpr uint32_t kStageBytes = kFStageDoubles * 8;
-  int issued = 0;
-  auto issue = [&]() {
-    if (issued < nz) {
+  auto issue = [&](bool copy) {
+    if (copy) {
 #pragma unroll
-      for (int q = 0; q < kWsChunksPerThread; ++q) {
+      for (int q = 0; q < 2; ++q) {
         if (ok[q]) sm100::cp_async16(dst[q] + so, src[q]);
         src[q] += P;
       }
+      if (warp == 0) {
+        if (ok[2]) sm100::cp_async16(dst[2] + so, src[2]);
+        src[2] += P;
+      }
     }
     sm100::cp_async_commit();
-    ++issued;
     so = so == (kWsStages - 1) * kStageBytes ? 0u : so + kStageBytes;
   };
+
 
   const int64_t col = (j - 1) * W + (i - 1);
   double* out_th = a.out.th + col;  // running pointers (advance one plane per level)
@@ -670,7 +677,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
   const int thc = (row + 2) * kFThW + (lane + 2);
 
 #pragma unroll 1
-  for (int k = 0; k < kWsStages - 1; ++k) issue();
+  for (int k = 0; k < kWsStages - 1; ++k) issue(k < nz);
 
   // role state carried along K
   double th_prev = 0.0, w_prev = 0.0;              // both roles
@@ -710,9 +717,10 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
 
   // Thomas forward recursion for face f (dialect face kf = f + 1) from the pending
   // coefficients (quotients by m share one reciprocal; `ok` guards the fast path)
-  auto thomas_fast = [&](int f, double& cpk, double& dpk, bool& ok) {
-    const double m = f == 0 ? pend_bb : pend_bb + pend_beta * cp_prev;
-    const double num = f == 0 ? pend_dd : pend_dd + pend_beta * dp_prev;
+  auto thomas_fast = [&](int f, double& cpk, double& dpk, bool& ok, bool not_first) {
+    const bool first = !not_first && f == 0;
+    const double m = first ? pend_bb : pend_bb + pend_beta * cp_prev;
+    const double num = first ? pend_dd : pend_dd + pend_beta * dp_prev;
     const fp64::Recip rm = fp64::recip(m);
     cpk = fp64::quot(-pend_beta, rm, ok);
     dpk = fp64::quot(num, rm, ok);
@@ -735,8 +743,11 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
     dp_prev = dpk;
   };
 
-  auto level = [&](int k, auto interior_tag) {
+  // kMid: 3 <= k < nz - 5 — no vertical boundary cases (faces kk+1/2 with
+  // 2 <= kk <= nz-2, Thomas face k-2 >= 1) and the copy of level k+5 always exists
+  auto level = [&](int k, auto interior_tag, auto mid_tag) {
     constexpr bool kIn = decltype(interior_tag)::value;
+    constexpr bool kMid = decltype(mid_tag)::value;
     const BaseLevel bnext = base_load(k + 1);
     const int kk = k + 1;
     const int s1 = s0 == kWsStages - 1 ? 0 : s0 + 1;
@@ -772,11 +783,11 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
       // formation for face k-1: the two division chains overlap instead of adding up.
       bool ok = true;
       double cpk = 0.0, dpk = 0.0, beta = 0.0, dd = 0.0;
-      if (k >= 2) thomas_fast(k - 2, cpk, dpk, ok);
+      if (kMid || k >= 2) thomas_fast(k - 2, cpk, dpk, ok, kMid);
       const double w_rhs = kRK ? wb_prev : w_prev;
       const double n_ps = c.dt_rdz * (psk - ps_prev);
       const double n_th = c.dt_grav * (0.5 * (th_prev + tk) - c.th0);
-      if (k >= 1) {
+      if (kMid || k >= 1) {
         const double rf = 0.5 * (rho_prev + rhok);
         const fp64::Recip rr = fp64::recip(rf);
         beta = fp64::quot(c.beta_num, rr, ok);
@@ -792,8 +803,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
           dd = dd + n_th / c.th0;
         }
       }
-      if (k >= 2) thomas_commit(k - 2, cpk, dpk);
-      if (k >= 1) {
+      if (kMid || k >= 2) thomas_commit(k - 2, cpk, dpk);
+      if (kMid || k >= 1) {
         pend_beta = beta;
         pend_bb = 1.0 + 2.0 * beta;
         pend_dd = dd;
@@ -803,11 +814,13 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
       if (kRK) wb_prev = bcur.w;
     } else if (!acoustic && (a.debug_skip & 1) == 0) {
       const double* T0 = S + kFOffTh + thc;
-      const double tkp1 = (kk + 1 <= nz) ? ring[s1 * kFStageDoubles + kFOffTh + thc] : 0.0;
-      const double tkp2 = (kk + 2 <= nz) ? ring[s2 * kFStageDoubles + kFOffTh + thc] : 0.0;
+      const double tkp1 =
+          (kMid || kk + 1 <= nz) ? ring[s1 * kFStageDoubles + kFOffTh + thc] : 0.0;
+      const double tkp2 =
+          (kMid || kk + 2 <= nz) ? ring[s2 * kFStageDoubles + kFOffTh + thc] : 0.0;
       const double xm2 = T0[-2], xm1 = T0[-1], xp1 = T0[1], xp2 = T0[2];
       const double ym2 = T0[-2 * kFThW], ym1 = T0[-kFThW], yp1 = T0[kFThW], yp2 = T0[2 * kFThW];
-      const double fzk = face_flux_up<true>(kk, nz, wk, th_prev, tk, tkp1, tkp2);
+      const double fzk = face_flux_up<!kMid>(kk, nz, wk, th_prev, tk, tkp1, tkp2);
       const double fxe = face_flux_up<!kIn>(gi, gnx, ui, xm1, tk, xp1, xp2);
       const double fxw = face_flux_up<!kIn>(gi - 1, gnx, uim1, xm2, xm1, tk, xp1);
       const double fyn = face_flux_up<!kIn>(gj, gny, vj, ym1, tk, yp1, yp2);
@@ -816,8 +829,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
       const double uwf = (!kIn && west) ? 0.0 : uim1;
       const double vnf = (!kIn && north) ? 0.0 : vj;
       const double vsf = (!kIn && south) ? 0.0 : vjm1;
-      const double wt = (kk == nz) ? 0.0 : wk;
-      const double wb = (kk == 1) ? 0.0 : w_prev;
+      const double wt = (!kMid && kk == nz) ? 0.0 : wk;
+      const double wb = (!kMid && kk == 1) ? 0.0 : w_prev;
       double flux = c.rdx * (fxe - fxw) + c.rdy * (fyn - fys);
       flux = flux + c.rdz * (fzk - fz_prev);
       double div = c.rdx * (ue - uwf) + c.rdy * (vnf - vsf);
@@ -855,16 +868,24 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
     // ... and everyone else's; every warp has also finished level k-1, so its slot
     // can be refilled now (one barrier per level)
     __syncthreads();
-    issue();
-    if (interior)
-      level(k, std::true_type{});
-    else
-      level(k, std::false_type{});
+    if (k >= 3 && k < nz - 5) {
+      issue(true);
+      if (interior)
+        level(k, std::true_type{}, std::true_type{});
+      else
+        level(k, std::false_type{}, std::true_type{});
+    } else {
+      issue(k + kWsStages - 1 < nz);
+      if (interior)
+        level(k, std::true_type{}, std::false_type{});
+      else
+        level(k, std::false_type{}, std::false_type{});
+    }
   }
   if (acoustic && nz >= 2) {  // drain the last face
     bool ok = true;
     double cpk, dpk;
-    thomas_fast(nz - 2, cpk, dpk, ok);
+    thomas_fast(nz - 2, cpk, dpk, ok, false);
     if (!ok) thomas_div(nz - 2, cpk, dpk);
     thomas_commit(nz - 2, cpk, dpk);
   }
