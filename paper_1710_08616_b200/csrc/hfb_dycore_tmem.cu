@@ -670,8 +670,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
 
 
   const int64_t col = (j - 1) * W + (i - 1);
-  double* out_th = a.out.th + col;  // running pointers (advance one plane per level)
-  double* out_u = a.out.u + col;
+  // running output pointers (advance one plane per level): acoustic u', v'; advection th'
+  double* out_a = (acoustic ? a.out.u : a.out.th) + col;
   double* out_v = a.out.v + col;
   const bool east = gi == gnx, west = gi == 1, north = gj == gny, south = gj == 1;
   const int thc = (row + 2) * kFThW + (lane + 2);
@@ -774,7 +774,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
       const double vs = (!kIn && south) ? 0.0 : vs0;
       const double psk = (kRK ? bcur.p : pk) - c.dt_cs2 * (c.rdx * (unk - uw) + c.rdy * (vnk - vs));
       if (kIn || active) {
-        *out_u = unk;
+        *out_a = unk;
         *out_v = vnk;
       }
       ps_s[k * kThreads + t] = psk;
@@ -849,39 +849,41 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
         phys_cs = phys_cs + rhok * thv;
         phys_cm = phys_cm + rhok;
       }
-      if (kIn || active) *out_th = thv;
+      if (kIn || active) *out_a = thv;
       fz_prev = fzk;
     }
     th_prev = tk;
     w_prev = wk;
     s0 = s1;
-    out_th += P;
-    out_u += P;
-    out_v += P;
+    out_a += P;
+    if (acoustic) out_v += P;
     bcur = bnext;
   };
 
-#pragma unroll 1
-  for (int k = 0; k < nz; ++k) {
-    // levels <= k+2 have landed (own copies; issued up to k+kWsStages-2) ...
+  // one level: levels <= k+2 have landed (own copies; issued up to k+kWsStages-2), the
+  // barrier makes everyone's visible and tells that every warp has finished level k-1,
+  // so its slot is refilled with level k+kWsStages-1 (one barrier per level)
+  auto step = [&](int k, auto in_tag, auto mid_tag) {
     sm100::cp_async_wait<kWsStages - 4>();
-    // ... and everyone else's; every warp has also finished level k-1, so its slot
-    // can be refilled now (one barrier per level)
     __syncthreads();
-    if (k >= 3 && k < nz - 5) {
-      issue(true);
-      if (interior)
-        level(k, std::true_type{}, std::true_type{});
-      else
-        level(k, std::false_type{}, std::true_type{});
-    } else {
-      issue(k + kWsStages - 1 < nz);
-      if (interior)
-        level(k, std::true_type{}, std::false_type{});
-      else
-        level(k, std::false_type{}, std::false_type{});
-    }
-  }
+    issue(decltype(mid_tag)::value || k + kWsStages - 1 < nz);
+    level(k, in_tag, mid_tag);
+  };
+  // K phases: [0, 3) and [nz-5, nz) with the vertical boundary cases, [3, nz-5) without
+  const int mid_lo = nz >= 3 ? 3 : nz, mid_hi = nz - 5 > mid_lo ? nz - 5 : mid_lo;
+  auto sweep = [&](auto in_tag) {
+    int k = 0;
+#pragma unroll 1
+    for (; k < mid_lo; ++k) step(k, in_tag, std::false_type{});
+#pragma unroll 1
+    for (; k < mid_hi; ++k) step(k, in_tag, std::true_type{});
+#pragma unroll 1
+    for (; k < nz; ++k) step(k, in_tag, std::false_type{});
+  };
+  if (interior)
+    sweep(std::true_type{});
+  else
+    sweep(std::false_type{});
   if (acoustic && nz >= 2) {  // drain the last face
     bool ok = true;
     double cpk, dpk;
