@@ -107,6 +107,11 @@ cudaError_t launch_dycore_step_tma(const DynIn& in, const DynOut& out, Grid3 g, 
                                    int64_t nj, const DynConst& c, const Span& sp,
                                    cudaStream_t s, const PhysArgs* phys = nullptr,
                                    const DynIn* base = nullptr);
+// two columns per thread, one CTA (32 x 8 tile) per SM (hfb_dycore_ws2.cu)
+cudaError_t launch_dycore_step_ws2(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
+                                   int64_t nj, const DynConst& c, const Span& sp,
+                                   cudaStream_t s, const PhysArgs* phys = nullptr,
+                                   const DynIn* base = nullptr);
 // standalone column physics on the current state (th updated in place)
 cudaError_t launch_column_physics(const double* rho, double* th, const double* u,
                                   const double* v, Grid3 g, int64_t nz, const DynConst& c,

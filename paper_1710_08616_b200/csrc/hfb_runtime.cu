@@ -252,6 +252,7 @@ struct hfb_ctx {
   bool force_split = getenv("HFB_SPLIT_STEP") != nullptr;
   bool force_single_role = getenv("HFB_SINGLE_ROLE") != nullptr;
   bool force_tma = getenv("HFB_TMA_STEP") != nullptr;
+  bool force_ws2 = getenv("HFB_WS2_STEP") != nullptr;
   // per-kernel CUDA-event timing (hfb_profile)
   bool prof = false;
   bool capturing = false;
@@ -752,6 +753,7 @@ void column_physics(hfb_ctx* c, Stats& st) {
 cudaError_t launch_step(hfb_ctx* c, const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                         int64_t nj, const DynConst& k, const Span& sp, cudaStream_t s,
                         const PhysArgs* phys = nullptr, const DynIn* base = nullptr) {
+  if (c->force_ws2) return launch_dycore_step_ws2(in, out, g, nz, nj, k, sp, s, phys, base);
   return c->force_tma ? launch_dycore_step_tma(in, out, g, nz, nj, k, sp, s, phys, base)
                       : launch_dycore_step_ws(in, out, g, nz, nj, k, sp, s, phys, base);
 }

@@ -143,9 +143,11 @@ def test_single_role_fused_matches(monkeypatch):
 
 
 @pytest.mark.parametrize("app", ["dycore", "dycore_full", "dycore_rk3"])
-def test_tma_step_matches(monkeypatch, app):
-    """The TMA-fed twin of the fused step (HFB_TMA_STEP=1) gives the same bits."""
-    monkeypatch.setenv("HFB_TMA_STEP", "1")
+@pytest.mark.parametrize("variant", ["HFB_TMA_STEP", "HFB_WS2_STEP"])
+def test_step_variant_matches(monkeypatch, app, variant):
+    """The measured alternatives of the fused step give the same bits: the TMA-fed twin
+    (HFB_TMA_STEP=1) and the two-columns-per-thread kernel (HFB_WS2_STEP=1)."""
+    monkeypatch.setenv(variant, "1")
     reals = dict(DYCORE_SCALARS, **PHYS_SCALARS) if app == "dycore_full" else dict(DYCORE_SCALARS)
     fills = dict(DYCORE_FILLS, **PHYS_FILLS) if app == "dycore_full" else dict(DYCORE_FILLS)
     _oracle_vs_gpu(Case(f"{app}_70x45x58_s2", app, dict(nx=70, ny=45, nz=58, nsteps=2),
