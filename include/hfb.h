@@ -197,6 +197,37 @@ int64_t hfb_halo_bytes(hfb_ctx* ctx);
 /* 128-byte ncclUniqueId for hfb_set_decomposition (rank 0 creates, all ranks share) */
 hfb_status hfb_nccl_unique_id(void* out128);
 
+/* --- state images and scenario files ------------------ */
+/* HFBSTAT1 image of the context's MachineState: program, every scalar (with its set
+ * flag), every bound array in the reference's ArrayValue order (row-major, last subscript
+ * fastest, interp.cpp:485-494; independent of device layout and host order), FNV-1a
+ * trailer. Arrays whose device copy is newer are read back without changing residency.
+ * The format is documented in csrc/hfb_runtime.cu and mirrored by state.py. */
+hfb_status hfb_save_state(hfb_ctx* ctx, const char* path);
+/* Restore an image (checkpoint/resume): loads the program when none is loaded (else it
+ * must match), sets every scalar, and writes every array into its bound host buffer
+ * (same bounds required) or into a context-owned pinned buffer it binds. Restored arrays
+ * are host-newer (a later copy-in transfers them). A corrupt image is HFB_IO. */
+hfb_status hfb_load_state(hfb_ctx* ctx, const char* path);
+/* the host buffer bound to an array (the caller's or a context-owned one), its bounds and
+ * element strides per dim (unused dims: bounds 1, stride 0) */
+hfb_status hfb_host_array(hfb_ctx* ctx, const char* module, const char* name, double** host,
+                          int* rank, int64_t lower[4], int64_t upper[4], int64_t strides[4]);
+/* checksums of an array's newest copy in ArrayValue order: the fp64 sum in that order
+ * and the FNV-1a 64 hash of its raw little-endian bytes (either output may be NULL) */
+hfb_status hfb_array_checksum(hfb_ctx* ctx, const char* module, const char* name, double* sum,
+                              uint64_t* bits);
+/* Scenario file (text; the reference's harness input): `program`, `entry`,
+ * `set` scalars, optional `array` bounds, `fill` patterns (const v | ramp a b |
+ * splitmix seed offset scale, the reference SplitMix64 over the ArrayValue flat index,
+ * interp.cpp:22-28) and `expect` checksums (array sum value rel_tol | array bits hex |
+ * scalar value v rel_tol). Filled arrays are bound to context-owned buffers (or the
+ * caller's, if bound with the same bounds), the entry runs, then every expectation is
+ * checked: HFB_VALIDATION names the first that fails. `report` (may be NULL) receives one
+ * line per expectation. */
+hfb_status hfb_run_scenario(hfb_ctx* ctx, const char* path, hfb_launch_stats* stats,
+                            char* report, size_t report_len);
+
 /* --- measurement --------------------------------------------------------------------- */
 /* enable (1) / disable (0) CUDA-event timing of every native launch on the context
  * stream; -1 also clears the accumulated times */

@@ -197,6 +197,7 @@ struct Slot {
   int64_t lower[4] = {1, 1, 1, 1}, upper[4] = {1, 1, 1, 1}, hstride[4] = {0, 0, 0, 0};
   int64_t count = 0;
   bool pinned = false;
+  double* owned = nullptr;  // context-owned host buffer (hfb_load_state / scenarios)
   // device side
   Layout lay;
   double* dev[3] = {nullptr, nullptr, nullptr};  // [2] only for RK3 stage states
@@ -1135,7 +1136,7 @@ void allreduce_sum(hfb_ctx* c, double* dev_value) {
 extern "C" {
 
 const char* hfb_last_error(void) { return g_last_error.c_str(); }
-int hfb_abi_version(void) { return 1; }
+int hfb_abi_version(void) { return 2; }  // 2: state images, scenarios
 
 hfb_status hfb_create(int device, hfb_ctx** out) {
   return guarded([&] {
@@ -1161,6 +1162,7 @@ void hfb_destroy(hfb_ctx* c) {
     for (double* p : s.dev)
       if (p) cudaFree(p);
     if (s.pinned && s.host) cudaHostUnregister(s.host);
+    if (s.owned) cudaFreeHost(s.owned);
   }
   if (c->staging) cudaFree(c->staging);
   if (c->red_partials) cudaFree(c->red_partials);
@@ -1290,6 +1292,10 @@ hfb_status hfb_bind_array(hfb_ctx* c, const char* module, const char* name, int 
     if (s.pinned && s.host && s.host != host) {
       cudaHostUnregister(s.host);
       s.pinned = false;
+    }
+    if (s.owned && s.owned != host) {  // a caller buffer replaces a context-owned one
+      cudaFreeHost(s.owned);
+      s.owned = nullptr;
     }
     s.host = host;
     s.rank = rank;
@@ -1779,6 +1785,536 @@ hfb_status hfb_nccl_unique_id(void* out128) {
     nccl_check(get(&id), "ncclGetUniqueId");
     std::memcpy(out128, id.internal, sizeof id.internal);
   });
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// State I/O and scenario files.
+//
+// The reference's harness input is "a scenario file naming the program, array shapes,
+// fill patterns (constant, linear ramp, seeded pseudo-random with stated algorithm and
+// seed), and expected-checksum entries" (never implemented: scenario.cpp:1
+// is a placeholder). HFBSTAT1 images are the matching binary MachineState dump: program,
+// scalars, array bounds and data in the reference's ArrayValue order (row-major, last
+// subscript fastest, interp.cpp:485-494), so an image is independent of the device
+// layout and of the caller's host order, and the oracle (tests/, oracle/) reads and
+// writes the same bytes (paper_1710_08616_b200/state.py).
+//
+// HFBSTAT1 (little-endian): "HFBSTAT1" | u32 version=1 | str program | str module |
+//   u32 nscalars | { str name | u8 type (0 int, 1 real) | u8 set | 8-byte value } |
+//   u32 narrays | { str name | u32 rank | i64 lower[rank] | i64 upper[rank] |
+//                   f64 data[count] } | u64 FNV-1a 64 of every preceding byte
+// where str = u32 length + bytes.
+// ===========================================================================
+namespace {
+
+constexpr char kStateMagic[8] = {'H', 'F', 'B', 'S', 'T', 'A', 'T', '1'};
+
+uint64_t fnv1a(uint64_t h, const void* p, size_t n) {
+  const unsigned char* b = static_cast<const unsigned char*>(p);
+  for (size_t q = 0; q < n; ++q) {
+    h ^= b[q];
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+constexpr uint64_t kFnvBasis = 0xcbf29ce484222325ull;
+
+void rowmajor_strides(const Slot& s, int64_t st[4]) {
+  int64_t acc = 1;
+  for (int d = s.rank - 1; d >= 0; --d) {
+    const int64_t e = s.upper[d] - s.lower[d] + 1;
+    st[d] = e > 1 ? acc : 0;
+    acc *= e;
+  }
+}
+
+// visit every element: f(flat index in ArrayValue order, element offset in the host buffer)
+template <class F>
+void for_each_element(const Slot& s, F&& f) {
+  int64_t ext[4] = {1, 1, 1, 1}, idx[4] = {0, 0, 0, 0};
+  for (int d = 0; d < s.rank; ++d) ext[d] = s.upper[d] - s.lower[d] + 1;
+  for (int64_t flat = 0; flat < s.count; ++flat) {
+    int64_t off = 0;
+    for (int d = 0; d < s.rank; ++d) off += idx[d] * s.hstride[d];
+    f(flat, off);
+    for (int d = s.rank - 1; d >= 0; --d) {  // odometer, last subscript fastest
+      if (++idx[d] < ext[d]) break;
+      idx[d] = 0;
+    }
+  }
+}
+
+// the newest copy of a bound array in ArrayValue order; residency is left unchanged
+std::vector<double> read_newest(hfb_ctx* c, Slot& s) {
+  check_bounds(c, s);
+  std::vector<double> out(static_cast<size_t>(s.count));
+  if (s.has_device && s.res == kDevice) {
+    Slot t = s;
+    rowmajor_strides(s, t.hstride);
+    const size_t bytes = static_cast<size_t>(s.count) * sizeof(double);
+    ensure_staging(c, bytes);
+    cuda_check(launch_relayout(s.d(), c->staging, relayout_of(t), false, c->stream),
+               "relayout(D2H)");
+    cuda_check(cudaMemcpyAsync(out.data(), c->staging, bytes, cudaMemcpyDeviceToHost, c->stream),
+               "cudaMemcpyAsync(D2H)");
+    cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  } else {
+    for_each_element(s, [&](int64_t flat, int64_t off) { out[flat] = s.host[off]; });
+  }
+  return out;
+}
+
+// write ArrayValue-ordered data into the slot's host buffer, binding a context-owned one
+// (pinned) when none is bound; the host copy becomes the newest
+void write_host(hfb_ctx* c, Slot& s, int rank, const int64_t* lo, const int64_t* hi,
+                const double* data) {
+  if (!s.host) {
+    int64_t count = 1;
+    for (int d = 0; d < rank; ++d) count *= hi[d] - lo[d] + 1;
+    double* buf = nullptr;
+    cudaSetDevice(c->device);
+    cuda_check(cudaMallocHost(&buf, static_cast<size_t>(count) * sizeof(double)),
+               "cudaMallocHost(state array)");
+    s.owned = buf;
+    hfb_status rc = hfb_bind_array(c, s.module.c_str(), s.name.c_str(), rank, lo, hi, buf,
+                                   nullptr, 0);
+    if (rc != HFB_OK) fail(rc, "%s", hfb_last_error());
+  } else {
+    if (rank != s.rank) fail(HFB_RUNTIME, "array '%s': rank %d vs bound rank %d", s.name.c_str(),
+                             rank, s.rank);
+    for (int d = 0; d < rank; ++d)
+      if (lo[d] != s.lower[d] || hi[d] != s.upper[d])
+        fail(HFB_RUNTIME, "array '%s' is bound with bounds [%lld:%lld] in dimension %d, the "
+                          "state has [%lld:%lld]", s.name.c_str(), (long long)s.lower[d],
+             (long long)s.upper[d], d + 1, (long long)lo[d], (long long)hi[d]);
+  }
+  for_each_element(s, [&](int64_t flat, int64_t off) { s.host[off] = data[flat]; });
+  if (s.has_device) s.res = kHost;  // host newer than the device copy
+}
+
+struct Writer {
+  FILE* f;
+  uint64_t h = kFnvBasis;
+  void put(const void* p, size_t n) {
+    if (fwrite(p, 1, n, f) != n) fail(HFB_IO, "write error");
+    h = fnv1a(h, p, n);
+  }
+  template <class T>
+  void pod(T v) { put(&v, sizeof v); }
+  void str(const std::string& s) {
+    pod<uint32_t>(static_cast<uint32_t>(s.size()));
+    put(s.data(), s.size());
+  }
+};
+
+struct Reader {
+  FILE* f;
+  std::string path;
+  uint64_t h = kFnvBasis;
+  void get(void* p, size_t n) {
+    if (fread(p, 1, n, f) != n) fail(HFB_IO, "'%s': truncated state image", path.c_str());
+    h = fnv1a(h, p, n);
+  }
+  template <class T>
+  T pod() {
+    T v;
+    get(&v, sizeof v);
+    return v;
+  }
+  std::string str() {
+    const uint32_t n = pod<uint32_t>();
+    if (n > 4096) fail(HFB_IO, "'%s': corrupt state image (name length %u)", path.c_str(), n);
+    std::string s(n, '\0');
+    get(&s[0], n);
+    return s;
+  }
+};
+
+struct FileCloser {
+  FILE* f;
+  ~FileCloser() {
+    if (f) fclose(f);
+  }
+};
+
+void save_state(hfb_ctx* c, const char* path) {
+  if (!c || !c->app) fail(HFB_CONFIG, "no program loaded");
+  cudaSetDevice(c->device);
+  FILE* f = fopen(path, "wb");
+  if (!f) fail(HFB_IO, "cannot open '%s' for writing", path);
+  FileCloser fc{f};
+  Writer w{f};
+  w.put(kStateMagic, 8);
+  w.pod<uint32_t>(1);
+  w.str(c->app->app);
+  w.str(c->app->module);
+  w.pod<uint32_t>(static_cast<uint32_t>(c->scalars.size()));
+  for (const auto& [name, v] : c->scalars) {
+    w.str(name);
+    w.pod<uint8_t>(v.type == SType::Int ? 0 : 1);
+    w.pod<uint8_t>(v.init ? 1 : 0);
+    if (v.type == SType::Int)
+      w.pod<int64_t>(v.i);
+    else
+      w.pod<double>(v.r);
+  }
+  uint32_t nbound = 0;
+  for (const auto& [name, s] : c->slots) nbound += s.host ? 1 : 0;
+  w.pod<uint32_t>(nbound);
+  for (auto& [name, s] : c->slots) {
+    if (!s.host) continue;
+    std::vector<double> data = read_newest(c, s);
+    w.str(name);
+    w.pod<uint32_t>(static_cast<uint32_t>(s.rank));
+    for (int d = 0; d < s.rank; ++d) w.pod<int64_t>(s.lower[d]);
+    for (int d = 0; d < s.rank; ++d) w.pod<int64_t>(s.upper[d]);
+    w.put(data.data(), data.size() * sizeof(double));
+  }
+  const uint64_t sum = w.h;
+  if (fwrite(&sum, 1, sizeof sum, f) != sizeof sum) fail(HFB_IO, "write error on '%s'", path);
+  if (fflush(f) != 0) fail(HFB_IO, "write error on '%s'", path);
+}
+
+void load_state(hfb_ctx* c, const char* path) {
+  if (!c) fail(HFB_CONFIG, "null context");
+  FILE* f = fopen(path, "rb");
+  if (!f) fail(HFB_IO, "cannot open '%s'", path);
+  FileCloser fc{f};
+  Reader r{f, path};
+  char magic[8];
+  r.get(magic, 8);
+  if (std::memcmp(magic, kStateMagic, 8) != 0) fail(HFB_IO, "'%s' is not an HFBSTAT1 image", path);
+  const uint32_t version = r.pod<uint32_t>();
+  if (version != 1) fail(HFB_IO, "'%s': unsupported state image version %u", path, version);
+  const std::string app = r.str(), module = r.str();
+  if (!c->app) {
+    hfb_status rc = hfb_load_program(c, app.c_str());
+    if (rc != HFB_OK) fail(rc, "%s", hfb_last_error());
+  } else if (c->app->app != app) {
+    fail(HFB_CONFIG, "state image of program '%s' loaded into a context holding '%s'",
+         app.c_str(), c->app->app.c_str());
+  }
+  if (module != c->app->module) fail(HFB_IO, "'%s': module '%s' is not '%s'", path,
+                                     module.c_str(), c->app->module.c_str());
+  // read everything first, apply after the checksum verified
+  struct SV { std::string name; uint8_t type, set; int64_t i; double r; };
+  std::vector<SV> scal(r.pod<uint32_t>());
+  for (SV& v : scal) {
+    v.name = r.str();
+    v.type = r.pod<uint8_t>();
+    v.set = r.pod<uint8_t>();
+    if (v.type == 0) v.i = r.pod<int64_t>(); else v.r = r.pod<double>();
+  }
+  struct AV { std::string name; int rank; int64_t lo[4], hi[4]; std::vector<double> data; };
+  std::vector<AV> arrs(r.pod<uint32_t>());
+  for (AV& a : arrs) {
+    a.name = r.str();
+    a.rank = static_cast<int>(r.pod<uint32_t>());
+    if (a.rank < 1 || a.rank > 4) fail(HFB_IO, "'%s': array '%s' has rank %d", path,
+                                       a.name.c_str(), a.rank);
+    int64_t count = 1;
+    for (int d = 0; d < a.rank; ++d) a.lo[d] = r.pod<int64_t>();
+    for (int d = 0; d < a.rank; ++d) {
+      a.hi[d] = r.pod<int64_t>();
+      if (a.hi[d] < a.lo[d]) fail(HFB_IO, "'%s': array '%s' has an empty dimension", path,
+                                  a.name.c_str());
+      count *= a.hi[d] - a.lo[d] + 1;
+    }
+    if (count > (int64_t(1) << 34)) fail(HFB_IO, "'%s': array '%s' too large", path, a.name.c_str());
+    a.data.resize(static_cast<size_t>(count));
+    r.get(a.data.data(), a.data.size() * sizeof(double));
+  }
+  const uint64_t expect = r.h;
+  uint64_t stored = 0;
+  if (fread(&stored, 1, sizeof stored, f) != sizeof stored || stored != expect)
+    fail(HFB_IO, "'%s': checksum mismatch (corrupt or truncated state image)", path);
+  for (const SV& v : scal) {
+    auto it = c->scalars.find(v.name);
+    if (it == c->scalars.end()) fail(HFB_IO, "'%s': unknown scalar '%s'", path, v.name.c_str());
+    Scalar& s = it->second;
+    if ((s.type == SType::Int) != (v.type == 0))
+      fail(HFB_IO, "'%s': scalar '%s' has the wrong type", path, v.name.c_str());
+    s.init = v.set != 0;
+    if (v.type == 0) { s.i = v.i; s.r = static_cast<double>(v.i); }
+    else { s.r = v.r; s.i = static_cast<int64_t>(v.r); }
+  }
+  for (const AV& a : arrs) {
+    Slot& s = slot_ref(c, c->app->module, a.name);
+    if (a.rank != static_cast<int>(s.decl->dims.size()))
+      fail(HFB_IO, "'%s': array '%s' has rank %d, declared %zu", path, a.name.c_str(), a.rank,
+           s.decl->dims.size());
+    write_host(c, s, a.rank, a.lo, a.hi, a.data.data());
+  }
+}
+
+// ---- scenario files -------------------------------------------------------------------
+//   program <app>            entry <routine>          set <scalar> <value>
+//   array <name> <dims...>   (dims: lo:hi or n; default: the declaration, evaluated)
+//   fill <name> const <v> | ramp <a> <b> | splitmix <seed> <offset> <scale>
+//   expect <array> sum <value> <rel_tol> | expect <array> bits <hex>
+//   expect <scalar> value <value> <rel_tol>
+// '#' starts a comment. splitmix: offset + scale * u, u = (splitmix64((seed << 40) + flat)
+// >> 11) * 2^-53 with the reference's SplitMix64 (interp.cpp:22-28) over the ArrayValue
+// flat index; ramp: a + b * flat.
+uint64_t splitmix64(uint64_t x) {  // interp.cpp:22-28
+  x += 0x9E3779B97F4A7C15ull;
+  uint64_t z = x;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+std::vector<std::string> split_ws(const std::string& line) {
+  std::vector<std::string> t;
+  size_t q = 0;
+  while (q < line.size()) {
+    while (q < line.size() && std::isspace(static_cast<unsigned char>(line[q]))) ++q;
+    if (q >= line.size() || line[q] == '#') break;
+    size_t e = q;
+    while (e < line.size() && !std::isspace(static_cast<unsigned char>(line[e]))) ++e;
+    t.push_back(line.substr(q, e - q));
+    q = e;
+  }
+  return t;
+}
+
+double num(const std::string& s, const char* what, int ln) {
+  char* end = nullptr;
+  double v = std::strtod(s.c_str(), &end);
+  if (s.empty() || *end != '\0') fail(HFB_IO, "scenario line %d: bad %s '%s'", ln, what, s.c_str());
+  return v;
+}
+
+void run_scenario(hfb_ctx* c, const char* path, hfb_launch_stats* stats, std::string& report) {
+  if (!c) fail(HFB_CONFIG, "null context");
+  FILE* f = fopen(path, "r");
+  if (!f) fail(HFB_IO, "cannot open scenario '%s'", path);
+  std::vector<std::pair<int, std::vector<std::string>>> lines;
+  {
+    FileCloser fc{f};
+    char buf[4096];
+    int ln = 0;
+    while (fgets(buf, sizeof buf, f)) {
+      ++ln;
+      auto t = split_ws(buf);
+      if (!t.empty()) lines.push_back({ln, t});
+    }
+  }
+  std::string entry = "main";
+  struct Fill { std::string kind; double a = 0, b = 0; uint64_t seed = 0; };
+  std::map<std::string, std::vector<std::pair<int64_t, int64_t>>> shapes;
+  std::vector<std::pair<std::string, Fill>> fills;
+  struct Expect { int ln; std::string name, kind, a, b; };
+  std::vector<Expect> expects;
+  for (auto& lt : lines) {
+    const int ln = lt.first;
+    const std::vector<std::string>& t = lt.second;
+    const std::string& k = t[0];
+    auto need = [&](size_t n) {
+      if (t.size() != n) fail(HFB_IO, "scenario line %d: '%s' takes %zu fields", ln, k.c_str(),
+                              n - 1);
+    };
+    if (k == "program") {
+      need(2);
+      if (!c->app) {
+        hfb_status rc = hfb_load_program(c, t[1].c_str());
+        if (rc != HFB_OK) fail(rc, "%s", hfb_last_error());
+      } else if (c->app->app != lower(t[1].c_str())) {
+        fail(HFB_CONFIG, "scenario program '%s' in a context holding '%s'", t[1].c_str(),
+             c->app->app.c_str());
+      }
+    } else if (!c->app) {
+      fail(HFB_IO, "scenario line %d: 'program' must come first", ln);
+    } else if (k == "entry") {
+      need(2);
+      entry = t[1];
+    } else if (k == "set") {
+      need(3);
+      Scalar& s = scalar_ref(c, c->app->module, lower(t[1].c_str()));
+      const double v = num(t[2], "value", ln);
+      s.r = v;
+      s.i = static_cast<int64_t>(v);
+      if (s.type == SType::Int && static_cast<double>(s.i) != v)
+        fail(HFB_IO, "scenario line %d: integer scalar '%s' set to %s", ln, t[1].c_str(),
+             t[2].c_str());
+      s.init = true;
+    } else if (k == "array") {
+      if (t.size() < 3 || t.size() > 6) fail(HFB_IO, "scenario line %d: array <name> <dims>", ln);
+      std::vector<std::pair<int64_t, int64_t>> dims;
+      for (size_t q = 2; q < t.size(); ++q) {
+        const size_t colon = t[q].find(':');
+        if (colon == std::string::npos)
+          dims.push_back({1, static_cast<int64_t>(num(t[q], "extent", ln))});
+        else
+          dims.push_back({static_cast<int64_t>(num(t[q].substr(0, colon), "bound", ln)),
+                          static_cast<int64_t>(num(t[q].substr(colon + 1), "bound", ln))});
+      }
+      shapes[lower(t[1].c_str())] = dims;
+    } else if (k == "fill") {
+      if (t.size() < 3) fail(HFB_IO, "scenario line %d: fill <name> <kind> ...", ln);
+      Fill fl;
+      fl.kind = t[2];
+      if (fl.kind == "const") {
+        need(4);
+        fl.a = num(t[3], "value", ln);
+      } else if (fl.kind == "ramp") {
+        need(5);
+        fl.a = num(t[3], "value", ln);
+        fl.b = num(t[4], "value", ln);
+      } else if (fl.kind == "splitmix") {
+        need(6);
+        fl.seed = std::strtoull(t[3].c_str(), nullptr, 0);
+        fl.a = num(t[4], "offset", ln);
+        fl.b = num(t[5], "scale", ln);
+      } else {
+        fail(HFB_IO, "scenario line %d: unknown fill '%s'", ln, fl.kind.c_str());
+      }
+      fills.push_back({lower(t[1].c_str()), fl});
+    } else if (k == "expect") {
+      if (t.size() < 4 || t.size() > 5) fail(HFB_IO, "scenario line %d: expect <name> <kind> ...", ln);
+      expects.push_back({ln, lower(t[1].c_str()), t[2], t[3], t.size() > 4 ? t[4] : "0"});
+    } else {
+      fail(HFB_IO, "scenario line %d: unknown keyword '%s'", ln, k.c_str());
+    }
+  }
+  if (!c->app) fail(HFB_IO, "scenario '%s' names no program", path);
+  // bind every filled array to a context-owned buffer and fill it (ArrayValue order)
+  for (auto& [name, fl] : fills) {
+    Slot& s = slot_ref(c, c->app->module, name);
+    std::vector<std::pair<int64_t, int64_t>> dims;
+    auto it = shapes.find(name);
+    if (it != shapes.end()) {
+      dims = it->second;
+    } else {
+      for (auto& d : s.decl->dims) dims.push_back({eval_dim(c, d.first), eval_dim(c, d.second)});
+    }
+    const int rank = static_cast<int>(dims.size());
+    int64_t lo[4], hi[4], count = 1;
+    for (int d = 0; d < rank; ++d) {
+      lo[d] = dims[d].first;
+      hi[d] = dims[d].second;
+      count *= hi[d] - lo[d] + 1;
+    }
+    std::vector<double> data(static_cast<size_t>(count));
+    for (int64_t q = 0; q < count; ++q) {
+      if (fl.kind == "const") {
+        data[q] = fl.a;
+      } else if (fl.kind == "ramp") {
+        data[q] = fl.a + fl.b * static_cast<double>(q);
+      } else {
+        const double u =
+            static_cast<double>(splitmix64((fl.seed << 40) + static_cast<uint64_t>(q)) >> 11) *
+            0x1.0p-53;
+        data[q] = fl.a + fl.b * u;
+      }
+    }
+    // a caller buffer stays bound (same bounds required); a context-owned buffer of
+    // another size is replaced
+    if (s.owned && s.count != count) {
+      if (s.has_device) fail(HFB_CONFIG, "scenario reshapes '%s' after a transfer", name.c_str());
+      cudaFreeHost(s.owned);
+      s.owned = nullptr;
+      s.host = nullptr;
+    }
+    write_host(c, s, rank, lo, hi, data.data());
+  }
+  hfb_status rc = hfb_run(c, entry.c_str(), stats);
+  if (rc != HFB_OK) fail(rc, "%s", hfb_last_error());
+  // expectations
+  std::string first_fail;
+  char line[512];
+  for (const Expect& e : expects) {
+    bool ok = false;
+    if (e.kind == "sum" || e.kind == "bits") {
+      Slot& s = slot_ref(c, c->app->module, e.name);
+      std::vector<double> data = read_newest(c, s);
+      if (e.kind == "sum") {
+        double sum = 0.0;
+        for (double v : data) sum += v;
+        const double want = num(e.a, "value", e.ln), tol = num(e.b, "tolerance", e.ln);
+        ok = tol == 0.0 ? sum == want : std::fabs(sum - want) <= tol * std::fabs(want);
+        snprintf(line, sizeof line, "%s sum %.17g expected %.17g (rel tol %g) %s\n",
+                 e.name.c_str(), sum, want, tol, ok ? "ok" : "FAIL");
+      } else {
+        const uint64_t h = fnv1a(kFnvBasis, data.data(), data.size() * sizeof(double));
+        const uint64_t want = std::strtoull(e.a.c_str(), nullptr, 0);
+        ok = h == want;
+        snprintf(line, sizeof line, "%s bits 0x%016llx expected 0x%016llx %s\n", e.name.c_str(),
+                 (unsigned long long)h, (unsigned long long)want, ok ? "ok" : "FAIL");
+      }
+    } else if (e.kind == "value") {
+      const double v = rval(c, e.name.c_str());
+      const double want = num(e.a, "value", e.ln), tol = num(e.b, "tolerance", e.ln);
+      ok = tol == 0.0 ? v == want : std::fabs(v - want) <= tol * std::fabs(want);
+      snprintf(line, sizeof line, "%s value %.17g expected %.17g (rel tol %g) %s\n",
+               e.name.c_str(), v, want, tol, ok ? "ok" : "FAIL");
+    } else {
+      fail(HFB_IO, "scenario line %d: unknown expectation '%s'", e.ln, e.kind.c_str());
+    }
+    report += line;
+    if (!ok && first_fail.empty()) first_fail = line;
+  }
+  if (!first_fail.empty()) {
+    if (!first_fail.empty() && first_fail.back() == '\n') first_fail.pop_back();
+    fail(HFB_VALIDATION, "scenario '%s': %s", path, first_fail.c_str());
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+hfb_status hfb_save_state(hfb_ctx* c, const char* path) {
+  return guarded([&] { save_state(c, path); });
+}
+
+hfb_status hfb_load_state(hfb_ctx* c, const char* path) {
+  return guarded([&] { load_state(c, path); });
+}
+
+hfb_status hfb_host_array(hfb_ctx* c, const char* module, const char* name, double** host,
+                          int* rank, int64_t lower_out[4], int64_t upper_out[4],
+                          int64_t strides[4]) {
+  return guarded([&] {
+    Slot& s = slot_ref(c, lower(module), lower(name));
+    if (!s.host) fail(HFB_CONFIG, "array '%s' of module '%s' is not bound", name, module);
+    *host = s.host;
+    *rank = s.rank;
+    for (int d = 0; d < 4; ++d) {
+      lower_out[d] = d < s.rank ? s.lower[d] : 1;
+      upper_out[d] = d < s.rank ? s.upper[d] : 1;
+      strides[d] = d < s.rank ? s.hstride[d] : 0;
+    }
+  });
+}
+
+hfb_status hfb_array_checksum(hfb_ctx* c, const char* module, const char* name, double* sum,
+                              uint64_t* bits) {
+  return guarded([&] {
+    Slot& s = slot_ref(c, lower(module), lower(name));
+    cudaSetDevice(c->device);
+    std::vector<double> data = read_newest(c, s);
+    double acc = 0.0;
+    for (double v : data) acc += v;
+    if (sum) *sum = acc;
+    if (bits) *bits = fnv1a(kFnvBasis, data.data(), data.size() * sizeof(double));
+  });
+}
+
+hfb_status hfb_run_scenario(hfb_ctx* c, const char* path, hfb_launch_stats* stats, char* report,
+                            size_t report_len) {
+  std::string rep;
+  hfb_status rc = guarded([&] {
+    if (c) cudaSetDevice(c->device);
+    run_scenario(c, path, stats, rep);
+  });
+  if (report && report_len) {
+    std::strncpy(report, rep.c_str(), report_len - 1);
+    report[report_len - 1] = '\0';
+  }
+  return rc;
 }
 
 }  // extern "C"

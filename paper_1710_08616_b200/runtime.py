@@ -39,7 +39,8 @@ EXPORTS = [
     "hfk1_diffuse_step", "hfk0_lateral_and_upper_damping", "hfk0_interior_update",
     "hfk0_sf_slab_flx_tile_run", "hfb_decomp_init", "hfb_decomp_faces", "hfb_set_decomposition",
     "hfb_halo_bytes", "hfb_nccl_unique_id", "hfb_profile", "hfb_kernel_time",
-    "hfb_group_create", "hfb_group_destroy", "hfb_group_run",
+    "hfb_group_create", "hfb_group_destroy", "hfb_group_run", "hfb_save_state",
+    "hfb_load_state", "hfb_host_array", "hfb_array_checksum", "hfb_run_scenario",
 ]
 
 # module of each built-in program (the apps' state modules)
@@ -127,6 +128,12 @@ def lib():
         L.hfb_group_destroy.argtypes = [P]
         L.hfb_group_destroy.restype = None
         L.hfb_group_run.argtypes = [P, S, c.POINTER(_Stats)]
+        L.hfb_save_state.argtypes = [P, S]
+        L.hfb_load_state.argtypes = [P, S]
+        L.hfb_host_array.argtypes = [P, S, S, c.POINTER(c.POINTER(dbl)), c.POINTER(c.c_int),
+                                     c.POINTER(i64), c.POINTER(i64), c.POINTER(i64)]
+        L.hfb_array_checksum.argtypes = [P, S, S, c.POINTER(dbl), c.POINTER(c.c_uint64)]
+        L.hfb_run_scenario.argtypes = [P, S, c.POINTER(_Stats), c.c_char_p, c.c_size_t]
         _lib = L
     return _lib
 
@@ -163,7 +170,42 @@ class Engine:
         _check(lib().hfb_create(device, ctypes.byref(h)))
         self._h = h
         self._bound = {}
-        _check(lib().hfb_load_program(h, _b(app)))
+        if app is not None:
+            _check(lib().hfb_load_program(h, _b(app)))
+
+    @classmethod
+    def from_state(cls, path, device=0):
+        """A context restored from an HFBSTAT1 image (hfb_load_state): program, scalars
+        and arrays (in context-owned host buffers, see array())."""
+        eng = cls(None, device)
+        try:
+            _check(lib().hfb_load_state(eng._h, _b(str(path))))
+        except Exception:
+            eng.close()
+            raise
+        from .state import read_header
+        eng.app = read_header(path)["program"]
+        eng.module = MODULES.get(eng.app, eng.app)
+        return eng
+
+    @classmethod
+    def scenario(cls, path, device=0):
+        """Run a scenario file (hfb_run_scenario): returns (engine, LaunchStats, report);
+        a failed expectation raises HfbError('validation')."""
+        from .state import Scenario
+        sc = Scenario.parse(path)
+        eng = cls(None, device)
+        st = _Stats()
+        buf = ctypes.create_string_buffer(1 << 16)
+        rc = lib().hfb_run_scenario(eng._h, _b(str(path)), ctypes.byref(st), buf, len(buf))
+        eng.app = sc.program
+        eng.module = MODULES.get(sc.program, sc.program)
+        if rc != 0:
+            msg = lib().hfb_last_error().decode()
+            eng.close()
+            raise HfbError(rc, msg)
+        return eng, LaunchStats(st.launches, st.threads, st.guard_returns,
+                                st.native_launches), buf.value.decode()
 
     def close(self):
         if getattr(self, "_h", None):
@@ -212,6 +254,35 @@ class Engine:
         _check(lib().hfb_bind_array(self._h, _b(self.module), _b(name), rank, lo, hi,
                                     a.ctypes.data, strides, 1 if pin else 0))
         self._bound[name] = a  # keep the buffer alive
+
+    def array(self, name):
+        """numpy view (declared bounds' shape, host order) of an array's bound host buffer:
+        the caller's, or the context-owned one of a restored state / scenario."""
+        p = ctypes.POINTER(ctypes.c_double)()
+        rank = ctypes.c_int()
+        lo, hi, st = (ctypes.c_int64 * 4)(), (ctypes.c_int64 * 4)(), (ctypes.c_int64 * 4)()
+        _check(lib().hfb_host_array(self._h, _b(self.module), _b(name), ctypes.byref(p),
+                                    ctypes.byref(rank), lo, hi, st))
+        shape = tuple(hi[d] - lo[d] + 1 for d in range(rank.value))
+        count = int(np.prod(shape))
+        flat = np.ctypeslib.as_array(p, shape=(count,))
+        strides = tuple(8 * (st[d] if shape[d] > 1 else 1) for d in range(rank.value))
+        return np.lib.stride_tricks.as_strided(flat, shape=shape, strides=strides)
+
+    def save_state(self, path):
+        """HFBSTAT1 image of the MachineState (hfb_save_state); newest copies, residency
+        unchanged."""
+        _check(lib().hfb_save_state(self._h, _b(str(path))))
+
+    def load_state(self, path):
+        _check(lib().hfb_load_state(self._h, _b(str(path))))
+
+    def checksum(self, name):
+        """(fp64 sum, FNV-1a 64 of the bits) of an array's newest copy, ArrayValue order."""
+        s, b = ctypes.c_double(), ctypes.c_uint64()
+        _check(lib().hfb_array_checksum(self._h, _b(self.module), _b(name), ctypes.byref(s),
+                                        ctypes.byref(b)))
+        return s.value, b.value
 
     # --- transfers (hfrt_*) -----------------------------------------------------------
     def device_allocate(self, name):
