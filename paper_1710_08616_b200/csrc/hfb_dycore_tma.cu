@@ -85,6 +85,7 @@ struct TmaStepArgs {
   DynIn base;  // RK3 stages 2-3: the state at the start of the step
   DynConst c;
   Span sp;
+  int wait_warp;  // the warp that waits on the slot barriers
 };
 
 // limited upwind face flux (see face_flux_up in hfb_dycore_tmem.cu for the derivation)
@@ -355,22 +356,25 @@ __global__ void __launch_bounds__(kThreadsTma, 2)
       s0 = s1;
     };
 
-    // Warp 0 alone waits for the newest level anyone reads at level k (k+2: the
-    // advection's z faces; levels are waited in order, once each), then the CTA barrier
-    // publishes it to every warp (mbarrier acquire by warp 0, then bar.sync) and frees
-    // the slot of level k-1 for level k-1+kStages.
+    // One warp waits for the levels: k+3 at the END of level k (after its own work, so
+    // the ~90-cycle mbarrier wait overlaps the other warps' arithmetic instead of
+    // sitting on the critical path), levels 0-2 before the loop. The CTA barrier at the
+    // top of level k+1 then publishes k+3 to every warp (mbarrier acquire, bar.sync) —
+    // the newest level the advection reads there — and frees the slot of level k.
+    const bool waiter = warp == a.wait_warp;
+    if (waiter)
+      for (int l = 0; l < 3 && l < nz; ++l)
+        sm100::mbar_wait(full0 + 8 * (l % kStages), (l / kStages) & 1);
 #pragma unroll 1
     for (int k = 0; k < nz; ++k) {
-      if (warp == 0) {
-        for (int l = k == 0 ? 0 : k + 2; l <= k + 2 && l < nz; ++l)
-          sm100::mbar_wait(full0 + 8 * (l % kStages), (l / kStages) & 1);
-      }
       __syncthreads();
       if (tma_lane && k >= 1 && k - 1 + kStages < nz) issue(k - 1 + kStages);
       if (interior)
         level(k, std::true_type{});
       else
         level(k, std::false_type{});
+      if (waiter && k + 3 < nz)
+        sm100::mbar_wait(full0 + 8 * ((k + 3) % kStages), ((k + 3) / kStages) & 1);
     }
     if (acoustic && nz >= 2) {  // drain the last face
       bool ok = true;
@@ -488,7 +492,8 @@ cudaError_t launch_dycore_step_tma(const DynIn& in, const DynOut& out, Grid3 g, 
   TmaStepArgs a{out, g, static_cast<int>(nz), debug_skip,
                 phys ? phys->tsfc : nullptr, phys ? phys->colm : nullptr,
                 phys ? phys->dt_rrelax : 0.0, phys ? phys->dt_ch : 0.0,
-                base ? *base : DynIn{}, c, sp};
+                base ? *base : DynIn{}, c, sp,
+                getenv("HFB_TMA_WAITWARP") ? atoi(getenv("HFB_TMA_WAITWARP")) : 7};
   dim3 block(kTX, kWarps);
   dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
             static_cast<unsigned>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY));
