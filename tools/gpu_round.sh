@@ -1,10 +1,15 @@
-# full GPU check of the current tree: all gpu tests, smoke, bench line, launch list, ncu capture
+# full GPU check of the current tree: all gpu tests, smoke, bench line (+ reference arm),
+# launch list, ncu capture of the dominant kernel
 TAG=${1:-r}
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider 2>&1 | tail -5
+timeout 1200 python -m pytest tests -m gpu -q -x -p no:cacheprovider 2>&1 | tail -5
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
 timeout 600 python bench.py --steps 50 --warmup 5 > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; tail -3 gpurun_out/bench_$TAG.err
 cat gpurun_out/bench_$TAG.json
+if [ -n "$2" ]; then
+  timeout 600 python bench.py --impl reference --steps 10 --warmup 3 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err; tail -3 gpurun_out/bench_ref_$TAG.err
+  cat gpurun_out/bench_ref_$TAG.json
+fi
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python tools/profile_step.py --steps 5 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_dyn_step -s 1 -c 1 -o gpurun_out/prof_$TAG python tools/profile_step.py --steps 2 > gpurun_out/ncu_$TAG.log 2>&1
 tail -2 gpurun_out/ncu_$TAG.log
