@@ -197,6 +197,15 @@ int64_t hfb_halo_bytes(hfb_ctx* ctx);
 /* 128-byte ncclUniqueId for hfb_set_decomposition (rank 0 creates, all ranks share) */
 hfb_status hfb_nccl_unique_id(void* out128);
 
+/* --- reductions (reduction.h90 `reduce(+:total)`) ---------------------------------- */
+/* 0 (default): fast two-level tree sum, equal to the reference to 1e-12 relative
+ * (SPEC.md:473). 1: ordered — the reference's acc-simulated order (interp.cpp:1080-1173):
+ * one partial per (i,j) iteration summing k = 1..nz from the identity, combined in
+ * linear-id order (i fastest) starting from the initial value, i.e. bit-identical to
+ * run_gpu_simulated on the OpenACC backend. Ordered runs single-domain or in an
+ * in-process group (the tiles' partials are assembled in global order). */
+hfb_status hfb_set_reduction_order(hfb_ctx* ctx, int ordered);
+
 /* --- state images and scenario files ------------------ */
 /* HFBSTAT1 image of the context's MachineState: program, every scalar (with its set
  * flag), every bound array in the reference's ArrayValue order (row-major, last subscript

@@ -401,7 +401,55 @@ __global__ void __launch_bounds__(kRedThreads) k_sum_partials(const double* __re
   const double s = block_sum(acc);
   if (threadIdx.x == 0) *result = total + s;
 }
+
+// ---- ordered mode: the reference's acc-simulated order (interp.cpp:1080-1173) ---------
+// every (i,j) iteration is one virtual thread whose private `total` starts at the identity
+// and adds y(k,i,j) for k = 1..nz in order; the partials are then combined one by one,
+// in linear-id order (i fastest, then j), starting from the initial value of `total`.
+__global__ void __launch_bounds__(128) k_column_sums(const double* __restrict__ y, Grid3 g,
+                                                     int64_t nz, Span sp,
+                                                     double* __restrict__ col, int64_t ld) {
+  const int64_t i = sp.ilo + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t j = sp.jlo + static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y;
+  if (i > sp.ihi || j > sp.jhi) return;
+  const double* p = y + g.at(i - 1, j - 1, 0);
+  double acc = 0.0;  // identity_for("+") (interp.cpp:167-171)
+  for (int64_t k = 0; k < nz; ++k) acc += __ldg(p + k * g.plane);
+  col[(j - sp.jlo) * ld + (i - sp.ilo)] = acc;
+}
+
+__global__ void __launch_bounds__(32) k_ordered_total(const double* __restrict__ col, int64_t n,
+                                                      double total, double* __restrict__ result) {
+  if (threadIdx.x != 0) return;
+  double acc = total;
+  int64_t t = 0;
+  for (; t + 8 <= n; t += 8) {  // loads run ahead, the additions stay in order
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __ldg(col + t + q);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc += v[q];
+  }
+  for (; t < n; ++t) acc += __ldg(col + t);
+  *result = acc;
+}
 }  // namespace
+
+cudaError_t launch_column_sums(const double* y, Grid3 g, int64_t nz, const Span& sp, double* col,
+                               int64_t ld, cudaStream_t s) {
+  if (span_empty(sp)) return cudaSuccess;
+  dim3 block(32, 4);
+  dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + 31) / 32),
+            static_cast<unsigned>((sp.jhi - sp.jlo + 1 + 3) / 4));
+  k_column_sums<<<grid, block, 0, s>>>(y, g, nz, sp, col, ld);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ordered_total(const double* col, int64_t n, double total, double* result,
+                                 cudaStream_t s) {
+  k_ordered_total<<<1, 32, 0, s>>>(col, n, total, result);
+  return cudaGetLastError();
+}
 
 int64_t reduce_partials_needed() { return kRedBlocks; }
 

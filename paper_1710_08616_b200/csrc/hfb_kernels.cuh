@@ -56,6 +56,12 @@ cudaError_t launch_sf_tile(const double* cover_lt, double* flx_x, double* flx_y,
 int64_t reduce_partials_needed();
 cudaError_t launch_grid_sum(const double* y, Grid3 g, int64_t nz, const Span& sp,
                             double* partials, double* result, double total, cudaStream_t s);
+// ordered mode, the reference's acc-simulated order (interp.cpp:1080-1173): per-column
+// partials (k in order from 0) into col[(j-jlo)*ld + (i-ilo)], then one in-order pass
+cudaError_t launch_column_sums(const double* y, Grid3 g, int64_t nz, const Span& sp, double* col,
+                               int64_t ld, cudaStream_t s);
+cudaError_t launch_ordered_total(const double* col, int64_t n, double total, double* result,
+                                 cudaStream_t s);
 
 // ---- apps/dycore/dycore.h90 --------------------------------------------------------
 struct DynConst {

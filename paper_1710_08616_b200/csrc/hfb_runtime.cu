@@ -237,6 +237,10 @@ struct hfb_ctx {
   struct hfb_group* group = nullptr;
   int64_t steps_done = 0;    // per-step entries completed (pull-side buffer selection)
   double red_local = 0.0;    // this rank's partial of a group reduction
+  // ordered reductions (hfb_set_reduction_order): per-column partials of this tile
+  bool reduce_ordered = false;
+  double* red_cols = nullptr;
+  size_t red_cols_cap = 0;
   int64_t halo_bytes = 0;
   // NCCL (multi-process decomposition)
   void* nccl_comm = nullptr;
@@ -691,8 +695,34 @@ void reduction_kernel(hfb_ctx* c, Stats& st) {
   Span sp = full_span(c, nx, ny);
   bool multi = c->decomposed && c->decomp.px * c->decomp.py > 1;
   bool local_group = multi && c->group != nullptr;
-  launch(c, st, "grid_total", [&] { return launch_grid_sum(y.d(), grid_of(y), nz, sp, c->red_partials, c->red_result,
-                           multi ? 0.0 : total, c->stream); }, 2);
+  if (c->reduce_ordered) {
+    // the acc-simulated order (interp.cpp:1080-1173): column partials, then one in-order
+    // pass from the initial value; a group assembles the tiles' partials in global order
+    if (multi && !local_group)
+      fail(HFB_CONFIG, "ordered reductions run single-domain or in an in-process group");
+    const size_t need = static_cast<size_t>(nx) * static_cast<size_t>(ny);
+    if (c->red_cols_cap < need) {
+      if (c->red_cols) cudaFree(c->red_cols);
+      c->red_cols = nullptr;
+      cuda_check(cudaMalloc(&c->red_cols, need * sizeof(double)), "cudaMalloc(column sums)");
+      c->red_cols_cap = need;
+    }
+    launch(c, st, "grid_total", [&] {
+      return launch_column_sums(y.d(), grid_of(y), nz, sp, c->red_cols, nx, c->stream);
+    });
+    if (local_group) {  // combined in global (j, i) order by hfb_group_run
+      st.launches += 1;
+      st.threads += nx * ny;
+      return;
+    }
+    launch(c, st, "grid_total_ordered", [&] {
+      return launch_ordered_total(c->red_cols, static_cast<int64_t>(need), total, c->red_result,
+                                  c->stream);
+    });
+  } else {
+    launch(c, st, "grid_total", [&] { return launch_grid_sum(y.d(), grid_of(y), nz, sp, c->red_partials, c->red_result,
+                             multi ? 0.0 : total, c->stream); }, 2);
+  }
   if (multi && !local_group) allreduce_sum(c, c->red_result);
   cuda_check(cudaMemcpyAsync(c->red_host, c->red_result, sizeof(double), cudaMemcpyDeviceToHost,
                              c->stream),
@@ -1166,6 +1196,7 @@ void hfb_destroy(hfb_ctx* c) {
   }
   if (c->staging) cudaFree(c->staging);
   if (c->red_partials) cudaFree(c->red_partials);
+  if (c->red_cols) cudaFree(c->red_cols);
   if (c->red_host) cudaFreeHost(c->red_host);
   if (c->halo_send) cudaFree(c->halo_send);
   if (c->halo_recv) cudaFree(c->halo_recv);
@@ -1743,7 +1774,36 @@ hfb_status hfb_group_run(hfb_group* g, const char* entry, hfb_launch_stats* stat
         c->steps_done += 1;  // later ranks of this step pull this rank's previous state
       });
     }
-    if (app == "reduction") {
+    if (app == "reduction" && g->ranks[0]->reduce_ordered) {
+      // every rank's column partials into rank 0's global buffer in (j, i) order, then
+      // the in-order pass from the initial value (interp.cpp:1163-1173)
+      hfb_ctx* r0 = g->ranks[0];
+      const hfb_decomp& d0 = r0->decomp;
+      const size_t gcount = static_cast<size_t>(d0.global_nx) * static_cast<size_t>(d0.global_ny);
+      double* gcols = nullptr;
+      cudaSetDevice(r0->device);
+      for (hfb_ctx* c : g->ranks) cuda_check(cudaStreamSynchronize(c->stream), "sync");
+      cuda_check(cudaMalloc(&gcols, gcount * sizeof(double)), "cudaMalloc(global column sums)");
+      struct Free { double* p; ~Free() { cudaFree(p); } } free_g{gcols};
+      for (hfb_ctx* c : g->ranks)
+        cuda_check(cudaMemcpy2DAsync(gcols + c->decomp.j0 * d0.global_nx + c->decomp.i0,
+                                     d0.global_nx * sizeof(double), c->red_cols,
+                                     c->decomp.nx * sizeof(double), c->decomp.nx * sizeof(double),
+                                     c->decomp.ny, cudaMemcpyDefault, r0->stream),
+                   "cudaMemcpy2DAsync(column sums)");
+      cuda_check(launch_ordered_total(gcols, static_cast<int64_t>(gcount), total0, r0->red_result,
+                                      r0->stream),
+                 "ordered total");
+      st.native += 1;
+      cuda_check(cudaMemcpyAsync(r0->red_host, r0->red_result, sizeof(double),
+                                 cudaMemcpyDeviceToHost, r0->stream),
+                 "cudaMemcpyAsync(total)");
+      cuda_check(cudaStreamSynchronize(r0->stream), "cudaStreamSynchronize");
+      for (hfb_ctx* c : g->ranks) {
+        c->scalars["total"].r = *r0->red_host;
+        c->scalars["total"].init = true;
+      }
+    } else if (app == "reduction") {
       double sum = 0.0;
       for (hfb_ctx* c : g->ranks) sum += c->red_local;  // rank order: deterministic
       for (hfb_ctx* c : g->ranks) {
@@ -1755,6 +1815,13 @@ hfb_status hfb_group_run(hfb_group* g, const char* entry, hfb_launch_stats* stat
       for (const std::string& n : transfers) do_copy_from_device(c, slot(c, n.c_str()));
     });
     if (stats) *stats = hfb_launch_stats{st.launches, st.threads, st.guard_returns, st.native};
+  });
+}
+
+hfb_status hfb_set_reduction_order(hfb_ctx* c, int ordered) {
+  return guarded([&] {
+    if (!c) fail(HFB_CONFIG, "null context");
+    c->reduce_ordered = ordered != 0;
   });
 }
 
@@ -2051,6 +2118,7 @@ void load_state(hfb_ctx* c, const char* path) {
 
 // ---- scenario files -------------------------------------------------------------------
 //   program <app>            entry <routine>          set <scalar> <value>
+//   option reduction ordered|fast (hfb_set_reduction_order)
 //   array <name> <dims...>   (dims: lo:hi or n; default: the declaration, evaluated)
 //   fill <name> const <v> | ramp <a> <b> | splitmix <seed> <offset> <scale>
 //   expect <array> sum <value> <rel_tol> | expect <array> bits <hex>
@@ -2130,6 +2198,11 @@ void run_scenario(hfb_ctx* c, const char* path, hfb_launch_stats* stats, std::st
     } else if (k == "entry") {
       need(2);
       entry = t[1];
+    } else if (k == "option") {  // option reduction ordered|fast
+      need(3);
+      if (t[1] != "reduction" || (t[2] != "ordered" && t[2] != "fast"))
+        fail(HFB_IO, "scenario line %d: unknown option '%s %s'", ln, t[1].c_str(), t[2].c_str());
+      c->reduce_ordered = t[2] == "ordered";
     } else if (k == "set") {
       need(3);
       Scalar& s = scalar_ref(c, c->app->module, lower(t[1].c_str()));

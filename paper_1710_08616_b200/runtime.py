@@ -41,6 +41,7 @@ EXPORTS = [
     "hfb_halo_bytes", "hfb_nccl_unique_id", "hfb_profile", "hfb_kernel_time",
     "hfb_group_create", "hfb_group_destroy", "hfb_group_run", "hfb_save_state",
     "hfb_load_state", "hfb_host_array", "hfb_array_checksum", "hfb_run_scenario",
+    "hfb_set_reduction_order",
 ]
 
 # module of each built-in program (the apps' state modules)
@@ -128,6 +129,7 @@ def lib():
         L.hfb_group_destroy.argtypes = [P]
         L.hfb_group_destroy.restype = None
         L.hfb_group_run.argtypes = [P, S, c.POINTER(_Stats)]
+        L.hfb_set_reduction_order.argtypes = [P, c.c_int]
         L.hfb_save_state.argtypes = [P, S]
         L.hfb_load_state.argtypes = [P, S]
         L.hfb_host_array.argtypes = [P, S, S, c.POINTER(c.POINTER(dbl)), c.POINTER(c.c_int),
@@ -268,6 +270,11 @@ class Engine:
         flat = np.ctypeslib.as_array(p, shape=(count,))
         strides = tuple(8 * (st[d] if shape[d] > 1 else 1) for d in range(rank.value))
         return np.lib.stride_tricks.as_strided(flat, shape=shape, strides=strides)
+
+    def set_reduction_order(self, ordered=True):
+        """Ordered reductions: bit-identical to the reference's acc-simulated order
+        (hfb_set_reduction_order); default is the fast tree (1e-12 relative)."""
+        _check(lib().hfb_set_reduction_order(self._h, 1 if ordered else 0))
 
     def save_state(self, path):
         """HFBSTAT1 image of the MachineState (hfb_save_state); newest copies, residency

@@ -149,6 +149,7 @@ class Expect:
 class Scenario:
     program: str = ""
     entry: str = "main"
+    options: dict = field(default_factory=dict)  # e.g. {"reduction": "ordered"}
     sets: dict = field(default_factory=dict)     # scalar -> float (as written)
     shapes: dict = field(default_factory=dict)   # array -> [(lo, hi), ...]
     fills: list = field(default_factory=list)    # (array, kind, params)
@@ -169,6 +170,8 @@ class Scenario:
                 sc.program = t[1].lower()
             elif k == "entry":
                 sc.entry = t[1]
+            elif k == "option":
+                sc.options[t[1]] = t[2]
             elif k == "set":
                 sc.sets[t[1].lower()] = float(t[2])
             elif k == "array":

@@ -50,7 +50,7 @@ def global_extent(case):
     return case.ints["nx"], case.ints["ny"]
 
 
-def run_decomposed(case, px, py, entry=None, halo=2):
+def run_decomposed(case, px, py, entry=None, halo=2, ordered=False):
     entry = entry or APPS[case.app].entry
     garr = make_inputs(case)
     gnx, gny = global_extent(case)
@@ -60,6 +60,8 @@ def run_decomposed(case, px, py, entry=None, halo=2):
         d = hfb.decomp_init(gnx, gny, nz, px, py, r, halo=halo)
         eng = hfb.Engine(APPS[case.app].prog)
         eng.set_decomposition(d)
+        if ordered:
+            eng.set_reduction_order(True)
         ints = tile_ints(case, d)
         for k, v in ints.items():
             eng.set(k, int(v))
@@ -159,3 +161,14 @@ def test_reduction_decomposed_allreduce():
     ref = run_oracle(case, {k: v.copy() for k, v in garr.items()})["total"]
     assert len(set(totals)) == 1
     assert abs(totals[0] - ref) <= 1e-12 * abs(ref)
+
+
+@pytest.mark.parametrize("px,py", [(2, 2), (3, 1), (1, 4)])
+def test_reduction_decomposed_ordered_bit_exact(px, py):
+    """Ordered reductions in a group: the tiles' column partials are assembled in global
+    (j, i) order, so the total is bit-identical to the single-domain acc-simulated order."""
+    case = Case("r", "reduction", dict(nx=67, ny=45, nz=58), dict(total=0.0), {"y": (6, 0.0, 1.0)})
+    garr, out, totals, _, _ = run_decomposed(case, px, py, halo=0, ordered=True)
+    accsim = run_oracle(case, {k: v.copy() for k, v in garr.items()})["total_accsim"]
+    assert len(set(totals)) == 1
+    assert np.float64(totals[0]).view(np.uint64) == np.float64(accsim).view(np.uint64)

@@ -105,6 +105,44 @@ def test_large_vs_oracle(case):
     _oracle_vs_gpu(case)
 
 
+@pytest.mark.parametrize("name", ["reduction_37x21x9", "reduction_67x5x58"])
+def test_reduction_ordered_matches_reference_accsim(name):
+    """hfb_set_reduction_order(1): bit-identical to the REFERENCE's run_gpu_simulated total
+    on the OpenACC backend (golden out_accsim.total), not just within 1e-12."""
+    case = CASE_BY_NAME[name]
+    _, out, _, extra = load_golden(name)
+    arrs = make_inputs(case)
+    app = APPS[case.app]
+    with hfb.Engine(app.prog) as eng:
+        eng.set_reduction_order(True)
+        for k, v in case.ints.items():
+            eng.set(k, int(v))
+        for k, v in case.reals.items():
+            eng.set(k, float(v))
+        eng.bind("y", arrs["y"])
+        eng.run("main")
+        total = eng.get("total")
+    ref = float(extra["out_accsim.total"].reshape(()))
+    assert np.float64(total).view(np.uint64) == np.float64(ref).view(np.uint64), (total, ref)
+
+
+def test_reduction_ordered_full_size():
+    """512 x 512 x 58 ordered total == the oracle's acc-simulated order, bit for bit."""
+    case = Case("reduction_512x512x58", "reduction", dict(nx=512, ny=512, nz=58),
+                dict(total=0.0), {"y": (6, 0.0, 1.0)})
+    arrs = make_inputs(case)
+    ref = run_oracle(case, {k: v.copy() for k, v in arrs.items()})["total_accsim"]
+    with hfb.Engine("reduction") as eng:
+        eng.set_reduction_order(True)
+        for k, v in case.ints.items():
+            eng.set(k, int(v))
+        eng.set("total", 0.0)
+        eng.bind("y", arrs["y"])
+        eng.run("main")
+        total = eng.get("total")
+    assert np.float64(total).view(np.uint64) == np.float64(ref).view(np.uint64)
+
+
 def test_reduction_large_tolerance():
     case = Case("reduction_512x512x58", "reduction", dict(nx=512, ny=512, nz=58),
                 dict(total=0.0), {"y": (6, 0.0, 1.0)})
