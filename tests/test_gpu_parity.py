@@ -380,3 +380,32 @@ def test_pinned_binding_and_fortran_order_equal():
         eng.run("main")
     for k in ("th", "u", "v", "w", "p"):
         assert bits_equal(arrs[k], out[k])
+
+
+@pytest.mark.parametrize("app", ["diffusion", "dycore", "damping"])
+def test_layout_invariance_all_host_orders(app):
+    """SPEC.md:549 "identical results under any configured storage-order permutation":
+    the same logical arrays bound in every dim permutation of host memory order give
+    bit-identical results (the device layout is fixed; only the relayout changes)."""
+    import itertools
+    case = {"diffusion": CASE_BY_NAME["diffusion_37x21x9_s3"],
+            "dycore": CASE_BY_NAME["dycore_24x20x12_s2"],
+            "damping": CASE_BY_NAME["damping_37x21x9"]}[app]
+    base = make_inputs(case)
+    results = []
+    for perm in itertools.permutations(range(3)):
+        arrs = {}
+        for k, a in base.items():
+            p = perm + tuple(range(3, a.ndim))
+            inv = tuple(np.argsort(p))
+            # a fresh copy in permuted memory order (ascontiguousarray would alias `base`
+            # for the identity permutation and let the run overwrite the inputs)
+            arrs[k] = np.array(a.transpose(p), order="C", copy=True).transpose(inv)
+        run_engine(case, arrs)
+        results.append({k: np.ascontiguousarray(v) for k, v in arrs.items()})
+    for r in results[1:]:
+        for k in results[0]:
+            assert bits_equal(r[k], results[0][k]), k
+    _, out, _, _ = load_golden(case.name)
+    for k in APPS[case.app].outputs:
+        assert bits_equal(results[0][k], out[k]), k
