@@ -581,6 +581,12 @@ __device__ __forceinline__ double face_flux_up(int64_t f, int64_t n, double vel,
   return fv;
 }
 
+// which lateral boundary cases a tile's instantiation handles
+template <bool kX, bool kY>
+struct Chk {
+  static constexpr bool x = kX, y = kY;
+};
+
 template <bool kPhys, bool kRK>
 __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
   static_assert(!(kPhys && kRK), "column physics is not fused into RK stages");
@@ -604,9 +610,10 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
   const int64_t gi = i + a.sp.i0, gj = j + a.sp.j0, gnx = a.sp.gnx, gny = a.sp.gny;
   // CTA-uniform: every column of the tile is >= 3 cells from every global wall
   const int64_t gi0 = i0 + a.sp.i0, gj0 = j0 + a.sp.j0;
-  const bool interior = gi0 >= 3 && gi0 + kTX - 1 <= gnx - 2 && gj0 >= 3 &&
-                        gj0 + kTY - 1 <= gny - 2 && i0 + kTX - 1 <= a.sp.ihi &&
-                        j0 + kTY - 1 <= a.sp.jhi;
+  // CTA-uniform: which wall / partial-tile cases this tile needs (x: its columns, y: its
+  // rows); tiles >= 3 cells from the walls and fully inside the span need none
+  const bool chk_x = !(gi0 >= 3 && gi0 + kTX - 1 <= gnx - 2 && i0 + kTX - 1 <= a.sp.ihi);
+  const bool chk_y = !(gj0 >= 3 && gj0 + kTY - 1 <= gny - 2 && j0 + kTY - 1 <= a.sp.jhi);
 
   if (warp == 0) sm100::tmem_alloc(&tmem_base_slot, kTmemCols);
   sm100::tmem_fence_before();
@@ -745,8 +752,9 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
 
   // kMid: 3 <= k < nz - 5 — no vertical boundary cases (faces kk+1/2 with
   // 2 <= kk <= nz-2, Thomas face k-2 >= 1) and the copy of level k+5 always exists
-  auto level = [&](int k, auto interior_tag, auto mid_tag) {
-    constexpr bool kIn = decltype(interior_tag)::value;
+  auto level = [&](int k, auto chk_tag, auto mid_tag) {
+    constexpr bool kCX = decltype(chk_tag)::x, kCY = decltype(chk_tag)::y;
+    constexpr bool kIn = !kCX && !kCY;  // every lane active
     constexpr bool kMid = decltype(mid_tag)::value;
     const BaseLevel bnext = base_load(k + 1);
     const int kk = k + 1;
@@ -768,10 +776,10 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
       const double vnk0 = (kRK ? bcur.v : vj) - c.dt_rdy * (pnn - pk);
       const double uw0 = (kRK ? bcur.uw : uim1) - c.dt_rdx * (pk - pw);
       const double vs0 = (kRK ? bcur.vs : vjm1) - c.dt_rdy * (pk - psth);
-      const double unk = (!kIn && east) ? 0.0 : unk0;
-      const double vnk = (!kIn && north) ? 0.0 : vnk0;
-      const double uw = (!kIn && west) ? 0.0 : uw0;
-      const double vs = (!kIn && south) ? 0.0 : vs0;
+      const double unk = (kCX && east) ? 0.0 : unk0;
+      const double vnk = (kCY && north) ? 0.0 : vnk0;
+      const double uw = (kCX && west) ? 0.0 : uw0;
+      const double vs = (kCY && south) ? 0.0 : vs0;
       const double psk = (kRK ? bcur.p : pk) - c.dt_cs2 * (c.rdx * (unk - uw) + c.rdy * (vnk - vs));
       if (kIn || active) {
         *out_a = unk;
@@ -821,14 +829,14 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
       const double xm2 = T0[-2], xm1 = T0[-1], xp1 = T0[1], xp2 = T0[2];
       const double ym2 = T0[-2 * kFThW], ym1 = T0[-kFThW], yp1 = T0[kFThW], yp2 = T0[2 * kFThW];
       const double fzk = face_flux_up<!kMid>(kk, nz, wk, th_prev, tk, tkp1, tkp2);
-      const double fxe = face_flux_up<!kIn>(gi, gnx, ui, xm1, tk, xp1, xp2);
-      const double fxw = face_flux_up<!kIn>(gi - 1, gnx, uim1, xm2, xm1, tk, xp1);
-      const double fyn = face_flux_up<!kIn>(gj, gny, vj, ym1, tk, yp1, yp2);
-      const double fys = face_flux_up<!kIn>(gj - 1, gny, vjm1, ym2, ym1, tk, yp1);
-      const double ue = (!kIn && east) ? 0.0 : ui;
-      const double uwf = (!kIn && west) ? 0.0 : uim1;
-      const double vnf = (!kIn && north) ? 0.0 : vj;
-      const double vsf = (!kIn && south) ? 0.0 : vjm1;
+      const double fxe = face_flux_up<kCX>(gi, gnx, ui, xm1, tk, xp1, xp2);
+      const double fxw = face_flux_up<kCX>(gi - 1, gnx, uim1, xm2, xm1, tk, xp1);
+      const double fyn = face_flux_up<kCY>(gj, gny, vj, ym1, tk, yp1, yp2);
+      const double fys = face_flux_up<kCY>(gj - 1, gny, vjm1, ym2, ym1, tk, yp1);
+      const double ue = (kCX && east) ? 0.0 : ui;
+      const double uwf = (kCX && west) ? 0.0 : uim1;
+      const double vnf = (kCY && north) ? 0.0 : vj;
+      const double vsf = (kCY && south) ? 0.0 : vjm1;
       const double wt = (!kMid && kk == nz) ? 0.0 : wk;
       const double wb = (!kMid && kk == 1) ? 0.0 : w_prev;
       double flux = c.rdx * (fxe - fxw) + c.rdy * (fyn - fys);
@@ -840,8 +848,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
         thv = thv - a.dt_rrelax * (thv - colm_ij);
         if (kk == 1) {  // new u, v at the lowest level (region 5), recomputed from the plane
           const double* Pp = S + kFOffP + (row + 1) * kPW + (lane + 2);
-          const double un1 = (!kIn && east) ? 0.0 : ui - c.dt_rdx * (Pp[1] - Pp[0]);
-          const double vn1 = (!kIn && north) ? 0.0 : vj - c.dt_rdy * (Pp[kPW] - Pp[0]);
+          const double un1 = (kCX && east) ? 0.0 : ui - c.dt_rdx * (Pp[1] - Pp[0]);
+          const double vn1 = (kCY && north) ? 0.0 : vj - c.dt_rdy * (Pp[kPW] - Pp[0]);
           const double wspd = sqrt(un1 * un1 + vn1 * vn1);
           thv = thv + a.dt_ch * wspd * (tsfc_ij - thv) * c.rdz / S[kFOffRho + row * kSW + lane];
         }
@@ -880,10 +888,14 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
 #pragma unroll 1
     for (; k < nz; ++k) step(k, in_tag, std::false_type{});
   };
-  if (interior)
-    sweep(std::true_type{});
+  if (!chk_x && !chk_y)
+    sweep(Chk<false, false>{});
+  else if (!chk_y)
+    sweep(Chk<true, false>{});
+  else if (!chk_x)
+    sweep(Chk<false, true>{});
   else
-    sweep(std::false_type{});
+    sweep(Chk<true, true>{});
   if (acoustic && nz >= 2) {  // drain the last face
     bool ok = true;
     double cpk, dpk;

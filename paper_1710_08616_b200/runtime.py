@@ -23,7 +23,8 @@ from pathlib import Path
 import numpy as np
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libhfb.so"
+# HFB_LIB: another build of the library (A/B timing of kernel variants)
+LIB_PATH = Path(os.environ["HFB_LIB"]) if os.environ.get("HFB_LIB") else PKG / "libhfb.so"
 CSRC = PKG / "csrc"
 
 KINDS = {0: "ok", 10: "config", 15: "runtime", 16: "residency", 17: "race", 18: "validation",
