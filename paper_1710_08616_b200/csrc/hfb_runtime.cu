@@ -247,6 +247,12 @@ struct hfb_ctx {
   double* halo_send = nullptr;
   double* halo_recv = nullptr;
   size_t halo_cap = 0;
+  // halo exchange overlapped with the interior columns (decomposed stencil steps): the
+  // exchange runs on `comm` while the columns that never read the halo ring run on
+  // `stream`; the boundary strips follow the exchange (HFB_NO_OVERLAP=1 serialises)
+  cudaStream_t comm = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+  bool overlap = getenv("HFB_NO_OVERLAP") == nullptr;
   // CUDA graph cache for hfb_run_graph
   cudaGraphExec_t graph_exec = nullptr;
   std::string graph_key;
@@ -530,7 +536,59 @@ void resolve_timings(hfb_ctx* c) {
   c->pending.clear();
 }
 
-void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width);
+void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width,
+                   cudaStream_t s = nullptr);
+
+// Decomposed stencil step with the halo exchange overlapped: the exchange of `fields` goes
+// to the communication stream; the columns at least `r` (the stencil radius) cells inside
+// the tile — they never read the halo ring — are launched at once on the compute stream;
+// the four boundary strips follow once the halos landed. Every column is computed from
+// the same inputs either way, so the split is bit-identical to one full-span launch.
+// `run(span)` launches the step kernel over a span of the tile.
+template <class F>
+void exchange_and_run(hfb_ctx* c, const std::vector<const char*>& fields, int r, int64_t nx,
+                      int64_t ny, bool odd_ilo, F&& run) {
+  const Span full = full_span(c, nx, ny);
+  const bool multi = c->decomposed && c->decomp.px * c->decomp.py > 1;
+  if (!multi) {
+    run(full);
+    return;
+  }
+  // odd_ilo: spans must start at odd i (the fused dycore kernel's 16-B copy chunks begin
+  // 2 columns left of a tile: i - 3 must be even), so the east strip may be one column
+  // wider and an even interior start falls back to the serial order
+  const int64_t east_lo = (!odd_ilo || (nx - r + 1) % 2 == 1) ? nx - r + 1 : nx - r;
+  Span in = full;
+  in.ilo = r + 1;
+  in.ihi = east_lo - 1;
+  in.jlo = r + 1;
+  in.jhi = ny - r;
+  if (!c->overlap || c->capturing || (odd_ilo && in.ilo % 2 == 0) || in.ihi < in.ilo ||
+      in.jhi < in.jlo) {
+    halo_exchange(c, fields, r);
+    run(full);
+    return;
+  }
+  if (!c->comm) {
+    cuda_check(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming), "cudaEventCreate");
+  }
+  cuda_check(cudaEventRecord(c->ev_ready, c->stream), "cudaEventRecord");
+  cuda_check(cudaStreamWaitEvent(c->comm, c->ev_ready, 0), "cudaStreamWaitEvent");
+  halo_exchange(c, fields, r, c->comm);
+  cuda_check(cudaEventRecord(c->ev_halo, c->comm), "cudaEventRecord");
+  run(in);
+  cuda_check(cudaStreamWaitEvent(c->stream, c->ev_halo, 0), "cudaStreamWaitEvent");
+  Span south = full, north = full, west = full, east = full;
+  south.jhi = r;
+  north.jlo = ny - r + 1;
+  west.jlo = east.jlo = r + 1;
+  west.jhi = east.jhi = ny - r;
+  west.ihi = r;
+  east.ilo = east_lo;
+  for (const Span& sp : {south, north, west, east}) run(sp);
+}
 
 // ---------------------------------------------------------------------------
 // app: diffusion (diffusion.h90)
@@ -543,11 +601,13 @@ void diffusion_step(hfb_ctx* c, Stats& st, bool write_t_new) {
   Slot& to = slot(c, "t_old");
   Slot& tn = slot(c, "t_new");
   ensure_device(c, to, true);
-  halo_exchange(c, {"t_old"}, 1);
-  Span sp = full_span(c, nx, ny);
   // hfk0 (stencil into the alternate t_old buffer [+ t_new]) then hfk1 fused away
-  launch(c, st, "hfk0_diffuse_step", [&] { return launch_diffusion(to.d(), to.d_alt(), write_t_new ? tn.d() : nullptr, grid_of(to), nz,
-                            coef, sp, c->stream); });
+  exchange_and_run(c, {"t_old"}, 1, nx, ny, false, [&](const Span& sp) {
+    launch(c, st, "hfk0_diffuse_step", [&] {
+      return launch_diffusion(to.d(), to.d_alt(), write_t_new ? tn.d() : nullptr, grid_of(to),
+                              nz, coef, sp, c->stream);
+    });
+  });
   to.cur = to.alt();
   count_launch(st, nx, ny);
   count_launch(st, nx, ny);
@@ -803,41 +863,41 @@ void dycore_step(hfb_ctx* c, Stats& st, bool with_physics = false) {
   Slot &rho = slot(c, "rho"), &th = slot(c, "th"), &u = slot(c, "u"), &v = slot(c, "v"),
        &w = slot(c, "w"), &p = slot(c, "p");
   for (Slot* s : {&th, &u, &v, &w, &p}) ensure_device(c, *s, true);
-  halo_exchange(c, {"th", "u", "v", "p"}, kHalo);
   DynIn in{rho.d(), th.d(), u.d(), v.d(), w.d(), p.d()};
   DynOut out{th.d_alt(), u.d_alt(), v.d_alt(), w.d_alt(), p.d_alt()};
-  Span sp = full_span(c, nx, ny);
-  bool fused_physics = false;
-  if (dycore_step_tmem_fits(nz) && !c->force_generic && !c->force_split) {
-    if (c->force_single_role)
-      launch(c, st, "dycore_step", [&] {
-        return launch_dycore_step_tmem(in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
+  const bool fused = dycore_step_tmem_fits(nz) && !c->force_generic && !c->force_split;
+  const bool fused_physics = fused && !c->force_single_role && with_physics;
+  PhysArgs ph{};
+  if (fused_physics) ph = phys_args(c, slot(c, "tsfc"), slot(c, "colm"));
+  exchange_and_run(c, {"th", "u", "v", "p"}, kHalo, nx, ny, true, [&](const Span& sp) {
+    if (fused) {
+      if (c->force_single_role)
+        launch(c, st, "dycore_step", [&] {
+          return launch_dycore_step_tmem(in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
+        });
+      else if (fused_physics)
+        launch(c, st, "full_step", [&] {
+          return launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream, &ph);
+        });
+      else
+        launch(c, st, "dycore_step", [&] {
+          return launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
+        });
+    } else {
+      launch(c, st, "dycore_advect", [&] {
+        return launch_dycore_advect(in, out.th, grid_of(th), nz, k, sp, c->stream);
       });
-    else if (with_physics) {
-      PhysArgs ph = phys_args(c, slot(c, "tsfc"), slot(c, "colm"));
-      launch(c, st, "full_step", [&] {
-        return launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream,
-                                     &ph);
-      });
-      fused_physics = true;
-    } else
-      launch(c, st, "dycore_step", [&] {
-        return launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
-      });
-  } else {
-    launch(c, st, "dycore_advect", [&] {
-      return launch_dycore_advect(in, out.th, grid_of(th), nz, k, sp, c->stream);
-    });
-    if (dycore_acoustic_tmem_fits(nz) && !c->force_generic)
-      launch(c, st, "dycore_acoustic", [&] {
-        return launch_dycore_acoustic_tmem(in, out, grid_of(th), nz, th.lay.nj, k, sp,
-                                           c->stream);
-      });
-    else
-      launch(c, st, "dycore_acoustic", [&] {
-        return launch_dycore_acoustic(in, out, grid_of(th), nz, k, sp, c->stream);
-      });
-  }
+      if (dycore_acoustic_tmem_fits(nz) && !c->force_generic)
+        launch(c, st, "dycore_acoustic", [&] {
+          return launch_dycore_acoustic_tmem(in, out, grid_of(th), nz, th.lay.nj, k, sp,
+                                             c->stream);
+        });
+      else
+        launch(c, st, "dycore_acoustic", [&] {
+          return launch_dycore_acoustic(in, out, grid_of(th), nz, k, sp, c->stream);
+        });
+    }
+  });
   for (Slot* s : {&th, &u, &v, &w, &p}) s->cur = s->alt();
   // the generated code's 8 launches (dycore.h90 regions; region 1 spans i = 0..nx,
   // region 2 spans j = 0..ny)
@@ -886,20 +946,20 @@ void rk3_step(hfb_ctx* c, Stats& st) {
   const DynIn base = state(b);
   const double dts[3] = {dt / 3.0, dt / 2.0, dt};  // dycore.h90 rk3_step `dtf`
   const int cur_of[3] = {b, s1, s2}, out_of[3] = {s1, s2, s1};
-  Span sp = full_span(c, nx, ny);
   // the generated code's launches: the base copy region, then 8 regions per stage
   count_launch(st, nx, ny);
   for (int g = 0; g < 3; ++g) {
     // halos of the stage state (the current buffers of this stage)
     for (Slot* s : prog) s->cur = cur_of[g];
-    halo_exchange(c, {"th", "u", "v", "p"}, kHalo);
     DynConst k = make_dyn_const(dts[g], rval(c, "rdx"), rval(c, "rdy"), rval(c, "rdz"),
                                 rval(c, "cs2"), rval(c, "grav"), rval(c, "th0"));
     const DynIn in = state(cur_of[g]);
     const DynOut out = outs(out_of[g]);
-    launch(c, st, "rk3_stage", [&] {
-      return launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream,
-                                   nullptr, g == 0 ? nullptr : &base);
+    exchange_and_run(c, {"th", "u", "v", "p"}, kHalo, nx, ny, true, [&](const Span& sp) {
+      launch(c, st, "rk3_stage", [&] {
+        return launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream, nullptr,
+                           g == 0 ? nullptr : &base);
+      });
     });
     count_launch(st, nx + 1, ny);
     count_launch(st, nx, ny + 1);
@@ -980,8 +1040,6 @@ struct NcclApi {
   const char* (*GetErrorString)(int) = nullptr;
 };
 
-void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width);
-
 }  // namespace
 
 // ncclUniqueId is a 128-byte struct passed by value; declare a matching type.
@@ -1023,12 +1081,14 @@ constexpr int kNcclSum = 0;
 
 // Two-phase halo update of `fields` (all share one layout): east/west faces first,
 // then north/south faces spanning the I halo so corners arrive too.
-void group_pull(hfb_ctx* c, const std::vector<const char*>& fields);
+void group_pull(hfb_ctx* c, const std::vector<const char*>& fields, cudaStream_t st);
 
-void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width) {
+void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width,
+                   cudaStream_t st) {
   if (!c->decomposed || c->decomp.px * c->decomp.py <= 1) return;
+  if (!st) st = c->stream;
   if (c->group) {
-    group_pull(c, fields);
+    group_pull(c, fields, st);
     return;
   }
   if (!c->nccl_comm) fail(HFB_CONFIG, "decomposed context without a communicator");
@@ -1069,7 +1129,7 @@ void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width
         Slot& sl = slot(c, f);
         int64_t fk = sl.lay.nk * sl.lay.nl;
         cuda_check(launch_pack_box(sl.d(), c->halo_send + off, grid_of(sl), fk, sbox[s], true,
-                                   c->stream),
+                                   st),
                    "halo pack");
         off += static_cast<size_t>((sbox[s][1] - sbox[s][0] + 1) * (sbox[s][3] - sbox[s][2] + 1) *
                                    fk);
@@ -1079,10 +1139,10 @@ void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width
     for (int s = 2 * phase; s < 2 * phase + 2; ++s) {
       if (nbr[s] < 0) continue;
       nccl_check(api.Send(c->halo_send + base[s], count[s], kNcclFloat64, nbr[s], c->nccl_comm,
-                          c->stream),
+                          st),
                  "ncclSend");
       nccl_check(api.Recv(c->halo_recv + base[s], count[s], kNcclFloat64, nbr[s], c->nccl_comm,
-                          c->stream),
+                          st),
                  "ncclRecv");
     }
     nccl_check(api.GroupEnd(), "ncclGroupEnd");
@@ -1093,7 +1153,7 @@ void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width
         Slot& sl = slot(c, f);
         int64_t fk = sl.lay.nk * sl.lay.nl;
         cuda_check(launch_pack_box(sl.d(), c->halo_recv + o, grid_of(sl), fk, rbox[s], false,
-                                   c->stream),
+                                   st),
                    "halo unpack");
         o += static_cast<size_t>((rbox[s][1] - rbox[s][0] + 1) * (rbox[s][3] - rbox[s][2] + 1) *
                                  fk);
@@ -1107,7 +1167,7 @@ void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width
 // copies (pack into a staging buffer on this stream, unpack into the halo). A neighbour
 // that already finished this step has flipped its double buffers; its previous state
 // is then the other buffer (untouched until its next step).
-void group_pull(hfb_ctx* c, const std::vector<const char*>& fields) {
+void group_pull(hfb_ctx* c, const std::vector<const char*>& fields, cudaStream_t st) {
   const hfb_decomp& d = c->decomp;
   const int nbr[4] = {d.west, d.east, d.south, d.north};
   const int opposite[4] = {1, 0, 3, 2};
@@ -1138,16 +1198,16 @@ void group_pull(hfb_ctx* c, const std::vector<const char*>& fields) {
           c->halo_cap = cnt;
         }
         cuda_check(launch_pack_box(src, c->halo_send, grid_of(theirs), fk, n_send, true,
-                                   c->stream),
+                                   st),
                    "group halo pack");
         cuda_check(launch_pack_box(mine.d(), c->halo_send, grid_of(mine), fk, my_recv, false,
-                                   c->stream),
+                                   st),
                    "group halo unpack");
         c->halo_bytes += static_cast<int64_t>(cnt * sizeof(double));
       }
     }
     // the second phase reads the neighbours' I halos (corners): finish phase one everywhere
-    cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
   }
 }
 
@@ -1207,6 +1267,9 @@ void hfb_destroy(hfb_ctx* c) {
     cudaEventDestroy(t.b);
   }
   for (cudaEvent_t e : c->free_events) cudaEventDestroy(e);
+  if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+  if (c->comm) cudaStreamDestroy(c->comm);
   cudaStreamDestroy(c->stream);
   delete c;
 }

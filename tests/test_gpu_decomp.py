@@ -102,7 +102,8 @@ def test_dycore_decomposed_equals_single(px, py):
     for k in ("th", "u", "v", "w", "p", "rho"):
         assert bits_equal(out[k], ref[k]), f"{px}x{py}: {k} differs"
     assert halo_bytes > 0
-    assert stats.native_launches == 3 * px * py
+    # per rank and step: the interior launch while the halos travel + 4 boundary strips
+    assert stats.native_launches == 3 * px * py * 5
 
 
 def test_full_step_decomposed_equals_single():
@@ -172,3 +173,29 @@ def test_reduction_decomposed_ordered_bit_exact(px, py):
     accsim = run_oracle(case, {k: v.copy() for k, v in garr.items()})["total_accsim"]
     assert len(set(totals)) == 1
     assert np.float64(totals[0]).view(np.uint64) == np.float64(accsim).view(np.uint64)
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+@pytest.mark.parametrize("app", ["dycore", "dycore_full", "diffusion"])
+def test_overlapped_exchange_equals_serial(monkeypatch, app, overlap):
+    """Decomposed stencil steps run the interior columns while the halos travel, then the
+    boundary strips (HFB_NO_OVERLAP=1: exchange first, one full launch). Both are
+    bit-identical to the undecomposed oracle."""
+    if not overlap:
+        monkeypatch.setenv("HFB_NO_OVERLAP", "1")
+    if app == "diffusion":
+        case = Case("d", "diffusion", dict(nx=70, ny=45, nz=20, nsteps=3), dict(coef=0.1),
+                    {"t_old": (1, 280.0, 10.0)}, unset=["t_new"])
+        names = ("t_old", "t_new")
+    else:
+        reals = dict(DYCORE_SCALARS, **PHYS_SCALARS) if app == "dycore_full" else dict(DYCORE_SCALARS)
+        fills = dict(DYCORE_FILLS, **PHYS_FILLS) if app == "dycore_full" else dict(DYCORE_FILLS)
+        case = Case("x", app, dict(nx=70, ny=45, nz=20, nsteps=2), reals, fills)
+        names = APPS[app].outputs
+    garr, out, _, stats, _ = run_decomposed(case, 2, 2)
+    ref = {k: v.copy() for k, v in garr.items()}
+    run_oracle(case, ref)
+    for k in names:
+        assert bits_equal(out[k], ref[k]), k
+    steps = case.ints["nsteps"]
+    assert stats.native_launches == 4 * steps * (5 if overlap else 1)
