@@ -32,6 +32,11 @@ cudaError_t launch_relayout(const double* src, double* dst, const Relayout& r, b
 // ---- diffusion.h90 (hfk0 + hfk1 fused: write the step result to one or two outputs)
 cudaError_t launch_diffusion(const double* t_old, double* out1, double* out2, Grid3 g,
                              int64_t nz, double coef, const Span& sp, cudaStream_t s);
+// the same step with shared-memory plane staging (hfb_diffusion.cu); nj = rows of the
+// arrays (halo-row bounds)
+cudaError_t launch_diffusion_ring(const double* t_old, double* out1, double* out2, Grid3 g,
+                                  int64_t nz, int64_t nj, double coef, const Span& sp,
+                                  cudaStream_t s);
 // hfk1_diffuse_step alone (t_old = t_new over the span)
 cudaError_t launch_copy_columns(const double* src, double* dst, Grid3 g, int64_t nz,
                                 const Span& sp, cudaStream_t s);

@@ -604,8 +604,11 @@ void diffusion_step(hfb_ctx* c, Stats& st, bool write_t_new) {
   // hfk0 (stencil into the alternate t_old buffer [+ t_new]) then hfk1 fused away
   exchange_and_run(c, {"t_old"}, 1, nx, ny, false, [&](const Span& sp) {
     launch(c, st, "hfk0_diffuse_step", [&] {
-      return launch_diffusion(to.d(), to.d_alt(), write_t_new ? tn.d() : nullptr, grid_of(to),
-                              nz, coef, sp, c->stream);
+      if (c->force_generic)
+        return launch_diffusion(to.d(), to.d_alt(), write_t_new ? tn.d() : nullptr,
+                                grid_of(to), nz, coef, sp, c->stream);
+      return launch_diffusion_ring(to.d(), to.d_alt(), write_t_new ? tn.d() : nullptr,
+                                   grid_of(to), nz, to.lay.nj, coef, sp, c->stream);
     });
   });
   to.cur = to.alt();

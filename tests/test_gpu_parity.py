@@ -214,6 +214,14 @@ def test_division_fast_path_edges(app, edge):
                         reals, fills))
 
 
+def test_generic_diffusion_kernel_matches(monkeypatch):
+    """The L1-cached diffusion kernel (HFB_GENERIC_KERNELS=1; the product kernel stages
+    planes in shared memory, hfb_diffusion.cu) gives the same bits."""
+    monkeypatch.setenv("HFB_GENERIC_KERNELS", "1")
+    _oracle_vs_gpu(Case("diffusion_333x77x58_s3", "diffusion", dict(nx=333, ny=77, nz=58, nsteps=3),
+                        dict(coef=0.1), {"t_old": (1, 280.0, 10.0)}, unset=["t_new"]))
+
+
 def test_generic_kernels_match(monkeypatch):
     """The portable acoustic kernel (HFB_GENERIC_KERNELS=1) gives the same bits."""
     monkeypatch.setenv("HFB_GENERIC_KERNELS", "1")
