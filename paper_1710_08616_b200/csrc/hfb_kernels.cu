@@ -418,20 +418,41 @@ __global__ void __launch_bounds__(128) k_column_sums(const double* __restrict__ 
   col[(j - sp.jlo) * ld + (i - sp.ilo)] = acc;
 }
 
+// one warp: the partials are staged through shared memory in 1024-value chunks (coalesced,
+// the next chunk loaded while the current one is summed) and lane 0 adds them in order,
+// 32 values per batch read ahead of the dependent DADD chain (8.2 cycles per add on B200:
+// the chain is the floor of this mode, ~8.6 ms per 2 M columns)
 __global__ void __launch_bounds__(32) k_ordered_total(const double* __restrict__ col, int64_t n,
                                                       double total, double* __restrict__ result) {
-  if (threadIdx.x != 0) return;
+  constexpr int kChunk = 1024;
+  __shared__ double buf[2][kChunk];
+  const int lane = threadIdx.x;
+  auto load = [&](int b, int64_t t0) {
+#pragma unroll 4
+    for (int q = lane; q < kChunk; q += 32) buf[b][q] = (t0 + q < n) ? __ldg(col + t0 + q) : 0.0;
+  };
   double acc = total;
-  int64_t t = 0;
-  for (; t + 8 <= n; t += 8) {  // loads run ahead, the additions stay in order
-    double v[8];
+  load(0, 0);
+  __syncwarp();
+  int b = 0;
+  for (int64_t t0 = 0; t0 < n; t0 += kChunk) {
+    if (t0 + kChunk < n) load(b ^ 1, t0 + kChunk);
+    if (lane == 0) {
+      const int m = n - t0 < kChunk ? static_cast<int>(n - t0) : kChunk;
+      int q = 0;
+      for (; q + 32 <= m; q += 32) {
+        double v[32];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = __ldg(col + t + q);
+        for (int r = 0; r < 32; ++r) v[r] = buf[b][q + r];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc += v[q];
+        for (int r = 0; r < 32; ++r) acc += v[r];
+      }
+      for (; q < m; ++q) acc += buf[b][q];
+    }
+    __syncwarp();
+    b ^= 1;
   }
-  for (; t < n; ++t) acc += __ldg(col + t);
-  *result = acc;
+  if (lane == 0) *result = acc;
 }
 }  // namespace
 
