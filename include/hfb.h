@@ -61,6 +61,12 @@ void hfb_destroy(hfb_ctx* ctx);
  * (module parameters such as sf_state.ntlm pre-set, interp.cpp:1498-1518). */
 hfb_status hfb_load_program(hfb_ctx* ctx, const char* app);
 
+/* Programs can also be generated from Hybrid-Fortran sources (paper_1710_08616_b200/hfc,
+ * include/hfb_plugin.h): hfb_load_program(ctx, "<path>.so") loads such a program. */
+/* name and state module of the loaded program (NULL before hfb_load_program) */
+const char* hfb_program_name(hfb_ctx* ctx);
+const char* hfb_program_module(hfb_ctx* ctx);
+
 /* module scalars (MachineState::scalars; interp.hpp:40-47) */
 hfb_status hfb_set_scalar_i64(hfb_ctx* ctx, const char* module, const char* name, int64_t v);
 hfb_status hfb_set_scalar_f64(hfb_ctx* ctx, const char* module, const char* name, double v);

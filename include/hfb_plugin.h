@@ -1,0 +1,74 @@
+/* hfb_plugin.h — ABI between libhfb.so and programs compiled from Hybrid-Fortran sources
+ * by the code generator (paper_1710_08616_b200/hfc).
+ *
+ * The reference's backend turns a `.h90` program into CUDA-Fortran text
+ * (codegen.cpp:397-519: host wrappers hfd_<routine>, kernels hfk<i>_<routine>). Here the
+ * generator emits CUDA C++ for sm_100a, nvcc builds it into a shared object, and
+ * hfb_load_program(ctx, "<path>.so") loads it: the context then holds that program's
+ * module state (scalars, arrays in the engine's device layout) exactly as it holds a
+ * built-in app's, and hfb_run(ctx, entry, ...) runs the generated host driver.
+ */
+#ifndef HFB_PLUGIN_H
+#define HFB_PLUGIN_H
+
+#include <stdint.h>
+
+#include "hfb.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HFB_PLUGIN_ABI 1
+
+typedef struct {
+  const char* name;
+  int type; /* 0 integer(4), 1 real(r_size), 2 logical */
+} hfb_plugin_scalar;
+
+typedef struct {
+  const char* name;
+  int rank;
+  const char* lower[4]; /* literal or module scalar name, per dim */
+  const char* upper[4];
+  int roles[4];         /* 0 I, 1 J, 2 K, 3 L: the device storage order of each dim */
+} hfb_plugin_array;
+
+typedef struct {
+  int abi; /* HFB_PLUGIN_ABI */
+  const char* program;
+  const char* module;                 /* the state module */
+  const hfb_plugin_scalar* scalars;   /* terminated by name == NULL */
+  const hfb_plugin_array* arrays;     /* terminated by name == NULL */
+  const char* const* entries;         /* host routines, NULL-terminated */
+  const char* const* transfer_entries; /* entries that perform host transfers */
+  /* run a host routine; stats accumulate; returns an hfb_status */
+  int (*run)(hfb_ctx* ctx, const char* routine, hfb_launch_stats* stats, int allow_transfers);
+} hfb_plugin_desc;
+
+/* the one symbol a program plugin exports */
+const hfb_plugin_desc* hfb_plugin(void);
+
+/* --- services libhfb.so provides to generated code -------------------------------- */
+/* device view of an array: element(d0..) = origin[sum (d - lower[d]) * stride[d]] */
+typedef struct {
+  double* origin;
+  int64_t stride[4];
+  int64_t lower[4];
+} hfb_view;
+/* residency checks before a kernel reads (mode 0) or reads and writes (mode 2) a module
+ * array (interp.cpp:397-411); routine-local (scratch) arrays always pass */
+hfb_status hfb_plugin_prepare(hfb_ctx* ctx, const char* name, int mode);
+/* a kernel wrote the array: the device copy is the newest (interp.cpp:533-538) */
+hfb_status hfb_plugin_written(hfb_ctx* ctx, const char* name);
+/* device view of a module array (allocated on first use) or of a scratch array */
+hfb_status hfb_plugin_view(hfb_ctx* ctx, const char* name, hfb_view* out);
+/* context-owned device scratch array `key` (a routine-local array, possibly extended by
+ * the region domain; analysis.cpp:439-527), (re)allocated when its bounds change */
+hfb_status hfb_plugin_scratch(hfb_ctx* ctx, const char* key, int rank, const int64_t* lower,
+                              const int64_t* upper, const int* roles);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HFB_PLUGIN_H */

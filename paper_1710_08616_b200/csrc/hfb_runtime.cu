@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "../../include/hfb.h"
+#include "../../include/hfb_plugin.h"
 #include "hfb_kernels.cuh"
 #include "hfb_layout.cuh"
 
@@ -99,6 +100,7 @@ struct AppDecl {
   std::string app, module;
   std::vector<ScalarDecl> scalars;
   std::vector<ArrayDecl> arrays;
+  const hfb_plugin_desc* plugin = nullptr;  // generated program (include/hfb_plugin.h)
 };
 
 std::vector<std::pair<std::string, std::string>> dims3(const char* a, const char* b,
@@ -218,6 +220,17 @@ struct hfb_group {
   std::vector<hfb_ctx*> ranks;
 };
 
+namespace {
+// device scratch of generated programs: routine-local arrays (hfb_plugin_scratch)
+struct Scratch {
+  Layout lay;
+  double* dev = nullptr;
+  int rank = 0;
+  int64_t lower[4] = {1, 1, 1, 1}, upper[4] = {1, 1, 1, 1};
+  Role roles[4] = {kRoleI, kRoleJ, kRoleK, kRoleL};
+};
+}  // namespace
+
 struct hfb_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -247,6 +260,7 @@ struct hfb_ctx {
   double* halo_send = nullptr;
   double* halo_recv = nullptr;
   size_t halo_cap = 0;
+  std::map<std::string, Scratch> scratch;  // generated programs' routine-local arrays
   // halo exchange overlapped with the interior columns (decomposed stencil steps): the
   // exchange runs on `comm` while the columns that never read the halo ring run on
   // `stream`; the boundary strips follow the exchange (HFB_NO_OVERLAP=1 serialises)
@@ -1004,7 +1018,22 @@ void dycore_entry(hfb_ctx* c, const std::string& r, Stats& st) {
 }
 
 using EntryFn = void (*)(hfb_ctx*, const std::string&, Stats&);
-EntryFn entry_fn(const std::string& app) {
+// a generated program: its host driver (hfb_plugin_desc::run) runs the routine
+void plugin_entry(hfb_ctx* c, const std::string& r, Stats& st) {
+  hfb_launch_stats s{};
+  const int rc = c->app->plugin->run(c, r.c_str(), &s, 1);
+  st.launches += s.launches;
+  st.threads += s.threads;
+  st.guard_returns += s.guard_returns;
+  st.native += s.native_launches;
+  if (rc == HFB_CONFIG && g_last_error.empty())
+    fail(HFB_CONFIG, "program '%s' has no entry '%s'", c->app->app.c_str(), r.c_str());
+  if (rc != HFB_OK) fail(rc, "%s", g_last_error.c_str());
+}
+
+EntryFn entry_fn(const AppDecl* d) {
+  if (d->plugin) return plugin_entry;
+  const std::string& app = d->app;
   if (app == "diffusion") return diffusion_entry;
   if (app == "damping") return damping_entry;
   if (app == "bounded") return bounded_entry;
@@ -1014,7 +1043,13 @@ EntryFn entry_fn(const std::string& app) {
   return nullptr;
 }
 
-bool entry_has_transfers(const std::string& app, const std::string& r) {
+bool entry_has_transfers(const AppDecl* d, const std::string& r) {
+  if (d->plugin) {
+    for (const char* const* e = d->plugin->transfer_entries; *e; ++e)
+      if (r == *e) return true;
+    return false;
+  }
+  const std::string& app = d->app;
   if (r == "main" || r == "simulation_run" || r == "main_full" || r == "simulation_run_full" ||
       r == "main_rk3" || r == "simulation_run_rk3")
     return true;
@@ -1224,6 +1259,60 @@ void allreduce_sum(hfb_ctx* c, double* dev_value) {
 }  // namespace
 
 // ===========================================================================
+// generated programs (include/hfb_plugin.h)
+// ===========================================================================
+namespace {
+
+const AppDecl* load_plugin(const std::string& path) {
+  static std::map<std::string, std::unique_ptr<AppDecl>> registry;
+  auto it = registry.find(path);
+  if (it != registry.end()) return it->second.get();
+  void* h = dlopen(path.c_str(), RTLD_NOW | RTLD_LOCAL);
+  if (!h) fail(HFB_CONFIG, "cannot load program '%s': %s", path.c_str(), dlerror());
+  auto get = reinterpret_cast<const hfb_plugin_desc* (*)()>(dlsym(h, "hfb_plugin"));
+  if (!get) fail(HFB_CONFIG, "'%s' is not a program plugin (no hfb_plugin symbol)", path.c_str());
+  const hfb_plugin_desc* d = get();
+  if (!d || d->abi != HFB_PLUGIN_ABI)
+    fail(HFB_CONFIG, "'%s': plugin ABI %d, expected %d", path.c_str(), d ? d->abi : -1,
+         HFB_PLUGIN_ABI);
+  auto decl = std::make_unique<AppDecl>();
+  decl->app = lower(d->program);
+  decl->module = lower(d->module);
+  decl->plugin = d;
+  for (const hfb_plugin_scalar* sc = d->scalars; sc->name; ++sc)
+    decl->scalars.push_back({lower(sc->name), sc->type == 1 ? SType::Real : SType::Int});
+  for (const hfb_plugin_array* ar = d->arrays; ar->name; ++ar) {
+    ArrayDecl ad;
+    ad.name = lower(ar->name);
+    for (int q = 0; q < ar->rank; ++q) {
+      ad.dims.push_back({ar->lower[q], ar->upper[q]});
+      ad.roles.push_back(static_cast<Role>(ar->roles[q]));
+    }
+    decl->arrays.push_back(ad);
+  }
+  const AppDecl* out = decl.get();
+  registry[path] = std::move(decl);
+  return out;
+}
+
+bool is_scratch(const char* name) { return std::strchr(name, '.') != nullptr; }
+
+void fill_view(const Layout& lay, const Role* roles, int rank, const int64_t* lower,
+               double* origin, hfb_view* v) {
+  v->origin = origin;
+  for (int q = 0; q < 4; ++q) {
+    v->stride[q] = 0;
+    v->lower[q] = q < rank ? lower[q] : 1;
+  }
+  for (int q = 0; q < rank; ++q) {
+    const Role r = roles[q];
+    v->stride[q] = r == kRoleI ? 1 : r == kRoleJ ? lay.pitch : r == kRoleK ? lay.plane : lay.volume;
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
 // C ABI
 // ===========================================================================
 extern "C" {
@@ -1260,6 +1349,8 @@ void hfb_destroy(hfb_ctx* c) {
   if (c->staging) cudaFree(c->staging);
   if (c->red_partials) cudaFree(c->red_partials);
   if (c->red_cols) cudaFree(c->red_cols);
+  for (auto& kv : c->scratch)
+    if (kv.second.dev) cudaFree(kv.second.dev);
   if (c->red_host) cudaFreeHost(c->red_host);
   if (c->halo_send) cudaFree(c->halo_send);
   if (c->halo_recv) cudaFree(c->halo_recv);
@@ -1282,6 +1373,9 @@ hfb_status hfb_load_program(hfb_ctx* c, const char* app) {
     if (!c) fail(HFB_CONFIG, "null context");
     std::string a = lower(app);
     const AppDecl* found = nullptr;
+    const std::string path = app;
+    if (path.size() > 3 && path.compare(path.size() - 3, 3, ".so") == 0)
+      found = load_plugin(path);
     for (const AppDecl& d : app_table())
       if (d.app == a) found = &d;
     if (!found) fail(HFB_CONFIG, "unknown program '%s'", a.c_str());
@@ -1457,10 +1551,10 @@ static hfb_status run_impl(hfb_ctx* c, const char* entry, hfb_launch_stats* stat
     if (!c || !c->app) fail(HFB_CONFIG, "no program loaded");
     cudaSetDevice(c->device);
     std::string r = routine_name(entry);
-    if (!allow_transfers && entry_has_transfers(c->app->app, r))
+    if (!allow_transfers && entry_has_transfers(c->app, r))
       fail(HFB_CONFIG, "entry '%s' performs host transfers; use hfb_run", entry);
     Stats st;
-    entry_fn(c->app->app)(c, r, st);
+    entry_fn(c->app)(c, r, st);
     if (sync) cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
     if (stats) {
       stats->launches = st.launches;
@@ -1491,7 +1585,7 @@ hfb_status hfb_run_graph(hfb_ctx* c, const char* entry, int64_t steps, hfb_launc
     if (steps < 1) return;
     cudaSetDevice(c->device);
     std::string r = routine_name(entry);
-    if (entry_has_transfers(c->app->app, r))
+    if (entry_has_transfers(c->app, r))
       fail(HFB_CONFIG, "entry '%s' performs host transfers; cannot be graph-captured", entry);
     if (c->decomposed && c->decomp.px * c->decomp.py > 1)
       fail(HFB_CONFIG, "graph replay of decomposed contexts is not supported");
@@ -1514,7 +1608,7 @@ hfb_status hfb_run_graph(hfb_ctx* c, const char* entry, int64_t steps, hfb_launc
                  "cudaStreamBeginCapture");
       c->capturing = true;
       try {
-        for (int64_t s = 0; s < steps; ++s) entry_fn(c->app->app)(c, r, st);
+        for (int64_t s = 0; s < steps; ++s) entry_fn(c->app)(c, r, st);
         c->capturing = false;
       } catch (...) {
         c->capturing = false;
@@ -1831,7 +1925,7 @@ hfb_status hfb_group_run(hfb_group* g, const char* entry, hfb_launch_stats* stat
         if (app == "diffusion" && step == "diffuse_step")
           diffusion_step(c, local, !outer || s == nsteps - 1);
         else
-          entry_fn(app)(c, step, local);
+          entry_fn(g->ranks[0]->app)(c, step, local);
         if (c == g->ranks[0]) st = Stats{st.launches + local.launches, st.threads + local.threads,
                                          st.guard_returns + local.guard_returns,
                                          st.native + local.native};
@@ -1883,6 +1977,12 @@ hfb_status hfb_group_run(hfb_group* g, const char* entry, hfb_launch_stats* stat
     if (stats) *stats = hfb_launch_stats{st.launches, st.threads, st.guard_returns, st.native};
   });
 }
+
+const char* hfb_program_module(hfb_ctx* c) {
+  return c && c->app ? c->app->module.c_str() : nullptr;
+}
+
+const char* hfb_program_name(hfb_ctx* c) { return c && c->app ? c->app->app.c_str() : nullptr; }
 
 hfb_status hfb_set_reduction_order(hfb_ctx* c, int ordered) {
   return guarded([&] {
@@ -2454,6 +2554,73 @@ hfb_status hfb_run_scenario(hfb_ctx* c, const char* path, hfb_launch_stats* stat
     report[report_len - 1] = '\0';
   }
   return rc;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+hfb_status hfb_plugin_prepare(hfb_ctx* c, const char* name, int mode) {
+  return guarded([&] {
+    if (is_scratch(name)) return;
+    if (mode == 0)
+      dev_read(c, name);
+    else
+      dev_write(c, name);
+  });
+}
+
+hfb_status hfb_plugin_written(hfb_ctx* c, const char* name) {
+  return guarded([&] {
+    if (!is_scratch(name)) dev_written(c, name);
+  });
+}
+
+hfb_status hfb_plugin_view(hfb_ctx* c, const char* name, hfb_view* out) {
+  return guarded([&] {
+    if (is_scratch(name)) {
+      auto it = c->scratch.find(name);
+      if (it == c->scratch.end()) fail(HFB_CONFIG, "no scratch array '%s'", name);
+      const Scratch& sa = it->second;
+      fill_view(sa.lay, sa.roles, sa.rank, sa.lower, sa.dev + sa.lay.origin_off, out);
+      return;
+    }
+    Slot& s = slot(c, name);
+    if (!s.has_device) fail(HFB_RESIDENCY, "array '%s' has no device copy (missing transfer)", name);
+    Role roles[4];
+    for (int q = 0; q < s.rank; ++q) roles[q] = s.decl->roles[q];
+    fill_view(s.lay, roles, s.rank, s.lower, s.d(), out);
+  });
+}
+
+hfb_status hfb_plugin_scratch(hfb_ctx* c, const char* key, int rank, const int64_t* lower,
+                              const int64_t* upper, const int* roles) {
+  return guarded([&] {
+    if (rank < 1 || rank > 4) fail(HFB_CONFIG, "scratch '%s': rank %d", key, rank);
+    Scratch& sa = c->scratch[key];
+    bool same = sa.dev && sa.rank == rank;
+    int64_t ext[4] = {1, 1, 1, 1};
+    for (int q = 0; q < rank; ++q) {
+      if (upper[q] < lower[q]) fail(HFB_RUNTIME, "scratch '%s': empty dimension %d", key, q + 1);
+      same = same && sa.lower[q] == lower[q] && sa.upper[q] == upper[q] &&
+             sa.roles[q] == static_cast<Role>(roles[q]);
+      ext[roles[q]] *= upper[q] - lower[q] + 1;
+    }
+    if (same) return;
+    if (sa.dev) cudaFree(sa.dev);
+    sa.dev = nullptr;
+    sa.rank = rank;
+    for (int q = 0; q < rank; ++q) {
+      sa.lower[q] = lower[q];
+      sa.upper[q] = upper[q];
+      sa.roles[q] = static_cast<Role>(roles[q]);
+    }
+    sa.lay = Layout::make(ext[kRoleI], ext[kRoleJ], ext[kRoleK], ext[kRoleL]);
+    const size_t bytes = static_cast<size_t>(sa.lay.alloc_elems) * sizeof(double);
+    cudaSetDevice(c->device);
+    cuda_check(cudaMalloc(&sa.dev, bytes), "cudaMalloc(scratch)");
+    cuda_check(cudaMemsetAsync(sa.dev, 0, bytes, c->stream), "cudaMemsetAsync");
+  });
 }
 
 }  // extern "C"

@@ -42,7 +42,8 @@ EXPORTS = [
     "hfb_halo_bytes", "hfb_nccl_unique_id", "hfb_profile", "hfb_kernel_time",
     "hfb_group_create", "hfb_group_destroy", "hfb_group_run", "hfb_save_state",
     "hfb_load_state", "hfb_host_array", "hfb_array_checksum", "hfb_run_scenario",
-    "hfb_set_reduction_order",
+    "hfb_set_reduction_order", "hfb_program_name", "hfb_program_module", "hfb_plugin_prepare",
+    "hfb_plugin_written", "hfb_plugin_view", "hfb_plugin_scratch",
 ]
 
 # module of each built-in program (the apps' state modules)
@@ -131,6 +132,10 @@ def lib():
         L.hfb_group_destroy.restype = None
         L.hfb_group_run.argtypes = [P, S, c.POINTER(_Stats)]
         L.hfb_set_reduction_order.argtypes = [P, c.c_int]
+        L.hfb_program_name.argtypes = [P]
+        L.hfb_program_name.restype = S
+        L.hfb_program_module.argtypes = [P]
+        L.hfb_program_module.restype = S
         L.hfb_save_state.argtypes = [P, S]
         L.hfb_load_state.argtypes = [P, S]
         L.hfb_host_array.argtypes = [P, S, S, c.POINTER(c.POINTER(dbl)), c.POINTER(c.c_int),
@@ -174,7 +179,10 @@ class Engine:
         self._h = h
         self._bound = {}
         if app is not None:
-            _check(lib().hfb_load_program(h, _b(app)))
+            _check(lib().hfb_load_program(h, _b(str(app))))
+            if str(app).endswith(".so"):  # a program generated from .h90 sources (hfc)
+                self.app = lib().hfb_program_name(h).decode()
+                self.module = lib().hfb_program_module(h).decode()
 
     @classmethod
     def from_state(cls, path, device=0):
