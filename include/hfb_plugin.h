@@ -63,6 +63,10 @@ hfb_status hfb_plugin_prepare(hfb_ctx* ctx, const char* name, int mode);
 hfb_status hfb_plugin_written(hfb_ctx* ctx, const char* name);
 /* device view of a module array (allocated on first use) or of a scratch array */
 hfb_status hfb_plugin_view(hfb_ctx* ctx, const char* name, hfb_view* out);
+/* host view of a module array's bound host buffer for host-code element access (the
+ * generated host drivers); reads of a host copy older than the device copy fail, writes
+ * make the host copy the newest (interp.cpp:406-409) */
+hfb_status hfb_plugin_host(hfb_ctx* ctx, const char* name, int write, hfb_view* out);
 /* context-owned device scratch array `key` (a routine-local array, possibly extended by
  * the region domain; analysis.cpp:439-527), (re)allocated when its bounds change */
 hfb_status hfb_plugin_scratch(hfb_ctx* ctx, const char* key, int rank, const int64_t* lower,

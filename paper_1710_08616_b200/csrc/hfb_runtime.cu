@@ -2593,6 +2593,24 @@ hfb_status hfb_plugin_view(hfb_ctx* c, const char* name, hfb_view* out) {
   });
 }
 
+hfb_status hfb_plugin_host(hfb_ctx* c, const char* name, int write, hfb_view* out) {
+  return guarded([&] {
+    if (is_scratch(name))
+      fail(HFB_CONFIG, "host access to the routine-local array '%s' is not supported", name);
+    Slot& s = slot(c, name);
+    check_bounds(c, s);
+    // host-code access checks (slot_side, interp.cpp:406-409)
+    if (!write && s.res == kDevice)
+      fail(HFB_RESIDENCY, "host copy of '%s' is stale (device copy was modified)", name);
+    if (write && s.has_device) s.res = kHost;
+    out->origin = s.host;
+    for (int d = 0; d < 4; ++d) {
+      out->stride[d] = d < s.rank ? s.hstride[d] : 0;
+      out->lower[d] = d < s.rank ? s.lower[d] : 1;
+    }
+  });
+}
+
 hfb_status hfb_plugin_scratch(hfb_ctx* c, const char* key, int rank, const int64_t* lower,
                               const int64_t* upper, const int* roles) {
   return guarded([&] {

@@ -21,6 +21,18 @@ GEN_DIR = PKG / "gen"  # generated plugins (built by __graft_entry__.build, git-
 # programs of this repository generated at build time: name -> sources (repo-relative)
 BUILTIN_SOURCES = {
     "dycore_gen": ["apps/dycore/dyn_state.h90", "apps/dycore/dycore.h90"],
+    "kitchen_gen": ["apps/kitchen/kit_state.h90", "apps/kitchen/kitchen.h90"],
+}
+# the reference's own application corpus (proj/tests/data/apps), compiled when the reference
+# tree is present (this container); the sources are never copied into the repository
+REFERENCE_APPS = Path(os.environ.get("HFB_REFERENCE_APPS", "/root/reference/proj/tests/data/apps"))
+CORPUS_SOURCES = {
+    "diffusion_gen": ["diffusion/diffusion.h90"],
+    "damping_gen": ["damping/damping.h90"],
+    "bounded_gen": ["bounded/bounded.h90"],
+    "surface_flux_gen": ["surface_flux/sf_state.h90", "surface_flux/surface_flux.h90",
+                         "surface_flux/driver.h90"],
+    "reduction_gen": ["reduction/reduction.h90"],
 }
 INCLUDE = PKG.parent / "include"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

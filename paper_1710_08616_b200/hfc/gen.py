@@ -55,12 +55,21 @@ class Program:
             raise GenError("exactly one module with declarations (the state module) is "
                            f"supported, found {[m.name for m in state]}")
         self.state = state[0]
+        # module parameters are constants (inlined, not part of the MachineState)
+        self.params = {n: d for n, d in self.state.decls.items() if d.param is not None}
+        for n in self.params:
+            del self.state.decls[n]
         self.routines = {}
         for m in self.mods.values():
             for r in m.routines.values():
                 if r.name in self.routines:
                     raise GenError(f"routine {r.name} defined twice")
                 self.routines[r.name] = r
+        # target selection (SPEC §3.1 appliesTo): regions that do not apply to the GPU are
+        # not parallel regions of this target; their bodies run as ordinary statements
+        gpu = _gpu_routines(self.routines)
+        for r in self.routines.values():
+            r.body = _gpu_target(r.body, self.routines, gpu)
         for n, d in self.state.decls.items():
             if d.type == "dim3":
                 raise GenError("type(dim3) module objects are not supported")
@@ -68,6 +77,8 @@ class Program:
                 raise GenError(f"module array {n}: only real(r_size) arrays are supported")
             for lo, hi in d.dims:
                 for e in (lo, hi):
+                    if isinstance(e, Name) and e.name in self.params:
+                        continue
                     if not isinstance(e, (Num, Name)):
                         raise GenError(f"module array {n}: dims must be literals or scalar "
                                        "names (the engine evaluates them)")
@@ -188,6 +199,84 @@ class Program:
         return roles
 
 
+def _applies_gpu(s):
+    applies = [x.lower() for x in s.attrs.get("appliesto", [])]
+    return not applies or "gpu" in applies
+
+
+def region_bounds(s):
+    """(lower, upper) expressions per domain dimension (codegen.cpp:38-63)."""
+    lo, hi = [], []
+    for sz in s.attrs.get("domsize", []):
+        if ":" in sz:
+            a, b = sz.split(":")
+            lo.append(parse_expr(a, s.line))
+            hi.append(parse_expr(b, s.line))
+        else:
+            lo.append(Num("1", False))
+            hi.append(parse_expr(sz, s.line))
+    if "startat" in s.attrs:
+        lo = [parse_expr(x, s.line) for x in s.attrs["startat"]]
+    if "endat" in s.attrs:
+        hi = [parse_expr(x, s.line) for x in s.attrs["endat"]]
+    return lo, hi
+
+
+def _walk(stmts):
+    for s in stmts:
+        yield s
+        if isinstance(s, (Region, Do)):
+            yield from _walk(s.body)
+        elif isinstance(s, If):
+            for _, b in s.branches:
+                yield from _walk(b)
+
+
+def _gpu_routines(routines):
+    """Routines with GPU regions in scope: their own, or through the routines they call."""
+    gpu = {n for n, r in routines.items()
+           if any(isinstance(s, Region) and _applies_gpu(s) for s in _walk(r.body))}
+    changed = True
+    while changed:
+        changed = False
+        for n, r in routines.items():
+            if n not in gpu and any(isinstance(s, Call) and s.name in gpu for s in _walk(r.body)):
+                gpu.add(n)
+                changed = True
+    return gpu
+
+
+def _gpu_target(stmts, routines, gpu):
+    """GPU-target lowering of regions that do not apply to the GPU (codegen.cpp:297-312): a
+    CPU-only region over code that launches its own kernels runs its body once with the
+    iterators pinned to the region start; any other becomes plain host loops, the last
+    domain outermost (codegen.cpp:335-359)."""
+    out = []
+    for s in stmts:
+        if isinstance(s, Region):
+            s.body = _gpu_target(s.body, routines, gpu)
+            if not _applies_gpu(s):
+                names = [n.lower() for n in s.attrs.get("domname", [])]
+                lo, hi = region_bounds(s)
+                covers = any((isinstance(t, Region) and _applies_gpu(t)) or
+                             (isinstance(t, Call) and t.name in gpu) for t in _walk(s.body))
+                if covers:
+                    out += [Assign(Name(n), e, s.line) for n, e in zip(names, lo)]
+                    out += s.body
+                else:
+                    body = s.body
+                    for n, a, b in zip(names, lo, hi):  # innermost first
+                        body = [Do(n, a, b, body, s.line)]
+                    out += body
+                continue
+        elif isinstance(s, Do):
+            s.body = _gpu_target(s.body, routines, gpu)
+        elif isinstance(s, If):
+            s.branches = [(c, _gpu_target(b, routines, gpu)) for c, b in s.branches]
+        out.append(s)
+    return out
+
+
 def _iter_of(e, iters):
     """index of the domain iterator an index expression is (iterator +- constant)"""
     if isinstance(e, Name) and e.name in iters:
@@ -234,7 +323,7 @@ class Emitter:
             return v[1]
         if isinstance(e, Ref):
             v = sc.get(e.name)
-            if v is not None and v[0] in ("array", "xarray"):
+            if v is not None and v[0] in ("array", "xarray", "harray"):
                 return "real"
             if e.name in ("sqrt", "real"):
                 return "real"
@@ -271,16 +360,18 @@ class Emitter:
             v = sc.get(e.name)
             if v is None:
                 raise GenError(f"unknown name {e.name}")
-            if v[0] == "array":
+            if v[0] in ("array", "xarray", "harray"):
                 raise GenError(f"array {e.name} used without subscripts")
             return v[2]
         if isinstance(e, Ref):
             v = sc.get(e.name)
-            if v is not None and v[0] in ("array", "xarray"):
+            if v is not None and v[0] in ("array", "xarray", "harray"):
                 idx = [self.expr(a, sc) if self.etype(a, sc) == "int"
                        else f"static_cast<int64_t>({self.expr(a, sc)})" for a in e.args]
                 if v[0] == "xarray":  # extended local: domain iterators prepended
                     idx = list(sc.get("@iters")[2]) + idx
+                if v[0] == "harray":  # host code: the bound host buffer
+                    return f"hfc_host(R, {v[2]}, {int(bool(sc.get('@write')))}).at({', '.join(idx)})"
                 return f"{v[2]}.at({', '.join(idx)})"
             return self.intrinsic(e, sc)
         if isinstance(e, Un):
@@ -358,14 +449,14 @@ struct HArr {  // device view: element(d0..d3) = o[sum (d - lo) * s]
   double* o;
   int64_t s[4];
   int64_t lo[4];
-  __device__ __forceinline__ double& at(int64_t a) const { return o[(a - lo[0]) * s[0]]; }
-  __device__ __forceinline__ double& at(int64_t a, int64_t b) const {
+  __host__ __device__ __forceinline__ double& at(int64_t a) const { return o[(a - lo[0]) * s[0]]; }
+  __host__ __device__ __forceinline__ double& at(int64_t a, int64_t b) const {
     return o[(a - lo[0]) * s[0] + (b - lo[1]) * s[1]];
   }
-  __device__ __forceinline__ double& at(int64_t a, int64_t b, int64_t c) const {
+  __host__ __device__ __forceinline__ double& at(int64_t a, int64_t b, int64_t c) const {
     return o[(a - lo[0]) * s[0] + (b - lo[1]) * s[1] + (c - lo[2]) * s[2]];
   }
-  __device__ __forceinline__ double& at(int64_t a, int64_t b, int64_t c, int64_t d) const {
+  __host__ __device__ __forceinline__ double& at(int64_t a, int64_t b, int64_t c, int64_t d) const {
     return o[(a - lo[0]) * s[0] + (b - lo[1]) * s[1] + (c - lo[2]) * s[2] + (d - lo[3]) * s[3]];
   }
 };
@@ -405,6 +496,15 @@ struct Run {
     int rc_ = (call);                         \
     if (rc_ != HFB_OK) throw rc_;             \
   } while (0)
+
+// reduce(...) regions: the partials in linear-id order combined from the initial value, one
+// at a time (interp.cpp:1163-1173), by one thread
+__global__ void hfc_ordered(const double* __restrict__ p, int64_t n, double init, int is_mul,
+                            double* __restrict__ out) {
+  double acc = init;
+  for (int64_t t = 0; t < n; ++t) acc = is_mul ? acc * p[t] : acc + p[t];
+  *out = acc;
+}
 
 HArr hfc_view(const hfb_view& v) {
   HArr a;
@@ -490,6 +590,8 @@ class Gen:
 
     # -- scopes ----------------------------------------------------------------------------
     def module_scope(self, sc, host):
+        for n, d in self.p.params.items():
+            sc.set(n, "const", d.type, self.em.expr(d.param, Scope()))
         for n, d in self.p.state.decls.items():
             if d.dims:
                 continue
@@ -579,14 +681,17 @@ class Gen:
             rhs_t = em.etype(s.rhs, sc)
             if isinstance(s.lhs, Ref):
                 v = sc.get(s.lhs.name)
-                if v is None or v[0] not in ("array", "xarray"):
+                if v is None or v[0] not in ("array", "xarray", "harray"):
                     raise GenError(f"line {s.line}: assignment to non-array {s.lhs.name}(...)")
-                if not kernel:
-                    raise GenError(f"line {s.line}: array element writes outside parallel "
-                                   "regions are not supported by the generated backend")
                 if region_ctx is not None:
                     region_ctx["written"].add(s.lhs.name)
-                return [f"{ind}{em.expr(s.lhs, sc)} = {em.real(s.rhs, sc)};"]
+                rhs = em.real(s.rhs, sc)
+                if v[0] == "harray":  # host element write (marks the host copy newer)
+                    sc.set("@write", "meta", "", True)
+                    lhs = em.expr(s.lhs, sc)
+                    sc.names.pop("@write")
+                    return [f"{ind}{{ const double hfc_v = {rhs}; {lhs} = hfc_v; }}"]
+                return [f"{ind}{em.expr(s.lhs, sc)} = {rhs};"]
             n = s.lhs.name
             v = sc.get(n)
             if v is None:
@@ -597,10 +702,12 @@ class Gen:
                 val = f"static_cast<double>({val})"
             elif t == "int" and rhs_t == "real":
                 val = f"static_cast<int64_t>({val})"
+            if kind == "const":
+                raise GenError(f"line {s.line}: assignment to the parameter {n}")
             if kind == "mscalar":
                 if kernel:
                     raise GenError(f"line {s.line}: module scalar {n} written inside a kernel "
-                                   "(reductions are not generated)")
+                                   "outside a reduce(...) region")
                 setter = "hfc_seti" if t == "int" else "hfc_setr" if t == "real" else "hfc_setl"
                 return [f"{ind}{setter}(R, \"{n}\", {val});"]
             return [f"{ind}{c} = {val};"]
@@ -635,19 +742,44 @@ class Gen:
                 for a, formal in zip(s.args, callee.args):
                     d = callee.decls[formal]
                     if d.intent in ("out", "inout"):
+                        if isinstance(a, Ref) and sc.get(a.name) is not None and \
+                                sc.get(a.name)[0] in ("array", "xarray"):
+                            if region_ctx is not None:
+                                region_ctx["written"].add(a.name)
+                            args.append(em.expr(a, sc))  # the element, by reference
+                            continue
                         if not isinstance(a, Name):
                             raise GenError(f"line {s.line}: intent(out) argument must be a "
-                                           "variable")
+                                           "variable or an array element")
                         args.append(sc.get(a.name)[2])
                     else:
                         args.append(em.real(a, sc) if d.type == "real" else em.expr(a, sc))
                 args += [sc.get(n)[2] for n in self.dev_mod_sc[s.name]]
                 return [f"{ind}dev_{s.name}({', '.join(args)});"]
-            if s.args:
-                raise GenError(f"line {s.line}: host routines with arguments are not supported")
-            if s.name not in self.p.routines:
+            callee = self.p.routines.get(s.name)
+            if callee is None:
                 raise GenError(f"line {s.line}: call of unknown routine {s.name}")
-            return [f"{ind}host_{s.name}(R);"]
+            if len(s.args) != len(callee.args):
+                raise GenError(f"line {s.line}: {s.name} takes {len(callee.args)} arguments")
+            args = ["R"]
+            for a, formal in zip(s.args, callee.args):
+                d = callee.decls.get(formal)
+                if d is None:
+                    raise GenError(f"{s.name}: undeclared argument {formal}")
+                if d.dims:  # array dummy: the actual array's runtime name
+                    if not isinstance(a, Name) or sc.get(a.name) is None or \
+                            sc.get(a.name)[0] != "harray":
+                        raise GenError(f"line {s.line}: array argument {formal} needs an array")
+                    args.append(sc.get(a.name)[2])
+                elif d.intent in ("out", "inout"):
+                    v = sc.get(a.name) if isinstance(a, Name) else None
+                    if v is None or v[0] != "scalar":
+                        raise GenError(f"line {s.line}: intent(out) argument must be a local "
+                                       "variable")
+                    args.append(v[2])
+                else:
+                    args.append(em.real(a, sc) if d.type == "real" else em.expr(a, sc))
+            return [f"{ind}host_{s.name}({', '.join(args)});"]
         if isinstance(s, Region):
             if kernel:
                 raise GenError(f"line {s.line}: nested parallel regions")
@@ -657,26 +789,20 @@ class Gen:
     # -- a parallel region: kernel + launch -------------------------------------------------
     def region(self, s, hsc, ind, R):
         r = R["routine"]
+        red = None  # (op, module scalar): the OpenACC-style reduction, acc-simulated order
         if "reduce" in s.attrs:
-            raise GenError(f"{r.name}:{s.line}: reduce(...) regions are not generated "
-                           "(codegen.cpp:399-403)")
+            if len(s.attrs["reduce"]) != 1 or ":" not in s.attrs["reduce"][0]:
+                raise GenError(f"{r.name}:{s.line}: one reduce(op:var) is supported")
+            op, var = [x.strip().lower() for x in s.attrs["reduce"][0].split(":")]
+            v = hsc.get(var)
+            if op not in ("+", "*") or v is None or v[0] != "mscalar" or v[1] != "real":
+                raise GenError(f"{r.name}:{s.line}: reduce needs + or * on a real module scalar")
+            red = (op, var)
         names = [n.lower() for n in s.attrs.get("domname", [])]
         sizes = s.attrs.get("domsize", [])
         if len(names) not in (1, 2) or len(names) != len(sizes):
             raise GenError(f"{r.name}:{s.line}: domName/domSize must name 1 or 2 dims")
-        lo, hi = [], []
-        for k, sz in enumerate(sizes):
-            if ":" in sz:
-                a, b = sz.split(":")
-                lo.append(parse_expr(a, s.line))
-                hi.append(parse_expr(b, s.line))
-            else:
-                lo.append(Num("1", False))
-                hi.append(parse_expr(sz, s.line))
-        if "startat" in s.attrs:
-            lo = [parse_expr(x, s.line) for x in s.attrs["startat"]]
-        if "endat" in s.attrs:
-            hi = [parse_expr(x, s.line) for x in s.attrs["endat"]]
+        lo, hi = region_bounds(s)
         idx = self.kcount.get(r.name, 0)
         self.kcount[r.name] = idx + 1
         kname = f"hfk{idx}_{r.name}"
@@ -715,7 +841,7 @@ class Gen:
                     read_scalars.append(e.name)
             elif isinstance(e, Ref):
                 v = hsc.get(e.name)
-                if v is not None and v[0] == "array" and e.name not in used_arrays:
+                if v is not None and v[0] == "harray" and e.name not in used_arrays:
                     used_arrays.append(e.name)
                 for a in e.args:
                     scan_e(a)
@@ -731,7 +857,7 @@ class Gen:
         params, args = [], []
         for a in used_arrays:
             params.append(f"HArr {a}")
-            args.append(hsc.get(a)[2])
+            args.append(f"hfc_array(R, {hsc.get(a)[2]})")
             ksc.set(a, "xarray" if a in self.extended else "array", "real", a)
         for k, n in enumerate(names):
             ksc.set(n, "scalar", "int", n)
@@ -743,7 +869,7 @@ class Gen:
             v = hsc.get(n)
             if v is None:
                 raise GenError(f"{r.name}:{s.line}: unknown name {n} in a parallel region")
-            if v[0] == "array":
+            if v[0] in ("harray", "const"):
                 continue
             if v[0] == "mscalar":
                 continue  # module scalars travel as m_<name>
@@ -752,6 +878,10 @@ class Gen:
             args.append(v[2])
             ksc.set(n, "scalar", v[1], n)
         mod_sc = self.mod_scalars_of(s.body, lo + hi, local_names=set(r.decls) | set(names))
+        if red:
+            mod_sc = [n for n in mod_sc if n != red[1]]
+            params += ["double* hfc_red", "int64_t hfc_ex"]
+            args += ["hfc_red_buf", "ex"]
         for n in mod_sc:
             t = self.p.state.decls[n].type
             params.append(f"{self.ctype(t)} m_{n}")
@@ -763,6 +893,10 @@ class Gen:
             v = hsc.get(n)
             if v is None:
                 raise GenError(f"{r.name}:{s.line}: unknown name {n}")
+            if red and n == red[1]:  # the thread's private accumulator from the identity
+                ksc.set(n, "scalar", "real", n)
+                kloc.append(f"  double {n} = {'1.0' if red[0] == '*' else '0.0'};")
+                continue
             if v[0] == "mscalar":
                 raise GenError(f"{r.name}:{s.line}: module scalar {n} written in a region")
             ksc.set(n, "scalar", v[1], n)
@@ -781,6 +915,11 @@ class Gen:
         body += kloc
         rctx = {"written": set()}
         body += self.stmts(s.body, ksc, "  ", kernel=True, region_ctx=rctx)
+        if red:  # partial of iteration (i, j) at its linear id, i fastest (interp.cpp:1127)
+            lin = f"({names[0]} - ({lo_c[0]}))"
+            if len(names) == 2:
+                lin = f"({names[1]} - ({lo_c[1]})) * hfc_ex + {lin}"
+            body.append(f"  hfc_red[{lin}] = {red[1]};")
         sig = f"__global__ void __launch_bounds__(128) {kname}({', '.join(params)})"
         self.kernels.append((sig, body))
         # host launch (grid ceiling(extent / B), block (32, 4, 1): codegen.cpp:421-434)
@@ -789,38 +928,65 @@ class Gen:
         out = [f"{ind}{{  // {kname}: region at line {s.line}"]
         for a in used_arrays:
             mode = 2 if a in rctx["written"] else 0
-            out.append(f"{ind}  hfc_prepare(R, \"{self.rt_names.get(a, a)}\", {mode});")
+            out.append(f"{ind}  hfc_prepare(R, {hsc.get(a)[2]}, {mode});")
         out.append(f"{ind}  const int64_t ex = ({hhi[0]}) - ({hlo[0]}) + 1;")
         out.append(f"{ind}  const int64_t ey = " + (f"({hhi[1]}) - ({hlo[1]}) + 1;" if len(names) == 2
                                                      else "1;"))
-        out.append(f"{ind}  hfc_count(R, ex, ey);")
+        if red:  # acc kernels: one virtual launch over the iteration space (interp.cpp:1114)
+            out.append(f"{ind}  double* hfc_red_buf = hfc_red_alloc(R, \"{r.name}.@red{s.line}\", "
+                       "ex * ey);")
+            out.append(f"{ind}  R.st->launches += 1;")
+            out.append(f"{ind}  R.st->threads += ex * ey;")
+        else:
+            out.append(f"{ind}  hfc_count(R, ex, ey);")
         out.append(f"{ind}  if (ex > 0 && ey > 0) {{")
         out.append(f"{ind}    dim3 grid(static_cast<unsigned>((ex + 31) / 32), "
                    f"static_cast<unsigned>((ey + 3) / 4), 1), block(32, 4, 1);")
         out.append(f"{ind}    {kname}<<<grid, block, 0, R.stream>>>({', '.join(args)});")
         out.append(f"{ind}    HFC_CHECK(hfc_launched(R));")
         out.append(f"{ind}  }}")
+        if red:  # partials combined in linear-id order from the initial value (:1163-1173)
+            out.append(f"{ind}  hfc_setr(R, \"{red[1]}\", hfc_red_finish(R, hfc_red_buf, ex * ey, "
+                       f"hfc_getr(R, \"{red[1]}\"), {int(red[0] == '*')}));")
         for a in sorted(rctx["written"]):
-            out.append(f"{ind}  hfc_written(R, \"{self.rt_names.get(a, a)}\");")
+            out.append(f"{ind}  hfc_written(R, {hsc.get(a)[2]});")
         out.append(f"{ind}}}")
         return out
 
     # -- host routines ------------------------------------------------------------------------
+    def host_signature(self, r):
+        params = ["Run& R"]
+        for a in r.args:
+            d = r.decls.get(a)
+            if d is None:
+                raise GenError(f"{r.name}: undeclared argument {a}")
+            if d.dims:
+                params.append(f"const char* a_{a}")
+            elif d.intent in ("out", "inout"):
+                params.append(f"{self.ctype(d.type)}& a_{a}")
+            else:
+                params.append(f"{self.ctype(d.type)} a_{a}")
+        return f"void host_{r.name}({', '.join(params)})"
+
     def gen_host(self, r):
         sc = Scope()
         self.module_scope(sc, host=True)
         body = []
         locs = self.local_arrays(r)
+        for n, d in self.p.state.decls.items():
+            if d.dims:
+                sc.set(n, "harray", "real", f"\"{n}\"")
         for n, d in r.decls.items():
             if n in r.args:
+                if d.dims:
+                    sc.set(n, "harray", "real", f"a_{n}")
+                else:
+                    sc.set(n, "scalar", d.type, f"a_{n}")
                 continue
             if d.dims:
                 continue
             sc.set(n, "scalar", d.type, f"l_{n}")
             body.append(f"  {self.ctype(d.type)} l_{n} = {self.zero(d.type)};")
-        for n, d in self.p.state.decls.items():
-            if d.dims:
-                sc.set(n, "array", "real", f"hfc_array(R, \"{n}\")")
         self.extended = {n for n, v in locs.items() if v[2]}
         self.rt_names = {n: f"{r.name}.{n}" for n in locs}
         for n, (d, dims, extended, dn) in locs.items():
@@ -832,7 +998,7 @@ class Gen:
             body.append(f"  {{ const int64_t lo[] = {{{lo}}}, hi[] = {{{hi}}}; "
                         f"const int roles[] = {{{rl}}};")
             body.append(f"    hfc_scratch(R, \"{key}\", {len(dims)}, lo, hi, roles); }}")
-            sc.set(n, "array", "real", f"hfc_array(R, \"{key}\")")
+            sc.set(n, "harray", "real", f"\"{key}\"")
         transfers = []
         for dd in r.domdeps:
             if "transferhere" in dd.attrs.get("attribute", []):
@@ -846,7 +1012,7 @@ class Gen:
         body += self.stmts(r.body, sc, "  ", kernel=False, R=R)
         for n in transfers:
             body.append(f"  HFC_CHECK(hfc_copy_out(R, \"{n}\"));")
-        self.hostfns.append((r.name, body))
+        self.hostfns.append((self.host_signature(r), body))
 
     def local_roles(self, r, n, dims, extended):
         rank = len(dims)
@@ -935,9 +1101,9 @@ class Gen:
             lines += body
             lines.append("}")
         for n in host_names:
-            lines.append(f"void host_{n}(Run& R);")
-        for n, body in self.hostfns:
-            lines.append(f"void host_{n}(Run& R) {{")
+            lines.append(self.host_signature(self.p.routines[n]) + ";")
+        for sig, body in self.hostfns:
+            lines.append(sig + " {")
             lines += body
             lines.append("}")
         lines.append(self.descriptor(host_names))
@@ -961,6 +1127,7 @@ class Gen:
             roles = ", ".join(str(x) for x in self.p.module_roles[n])
             out.append(f"  {{\"{n}\", {len(d.dims)}, {{{los}}}, {{{his}}}, {{{roles}}}}},")
         out.append("  {nullptr, 0, {}, {}, {}}};")
+        host_names = [n for n in host_names if not self.p.routines[n].args]
         out.append("const char* kEntries[] = {")
         for n in host_names:
             out.append(f"  \"{n}\",")
@@ -1004,6 +1171,11 @@ class Gen:
     def dimtext(self, e):
         if isinstance(e, Num):
             return e.text
+        if isinstance(e, Name) and e.name in self.p.params:
+            pv = self.p.params[e.name].param
+            if isinstance(pv, Num) and not pv.is_real:
+                return pv.text
+            raise GenError(f"parameter {e.name} used as an array bound must be an integer literal")
         if isinstance(e, Name):
             return e.name
         raise GenError("array dims must be literals or scalar names")
@@ -1037,6 +1209,13 @@ void hfc_scratch(Run& R, const char* key, int rank, const int64_t* lo, const int
                  const int* roles) {
   HFC_CHECK(hfb_plugin_scratch(R.ctx, key, rank, lo, hi, roles));
 }
+// host-side element access (host routines): the bound host buffer; write = 1 makes the
+// host copy the newest
+HArr hfc_host(Run& R, const char* n, int write) {
+  hfb_view v;
+  HFC_CHECK(hfb_plugin_host(R.ctx, n, write, &v));
+  return hfc_view(v);
+}
 int hfc_copy_in(Run& R, const char* n) {
   if (!R.allow_transfers) return HFB_CONFIG;
   return hfrt_copy_to_device(R.ctx, kMod, n);
@@ -1053,6 +1232,25 @@ void hfc_count(Run& R, int64_t ex, int64_t ey) {
 int hfc_launched(Run& R) {
   R.st->native_launches += 1;
   return cudaGetLastError() == cudaSuccess ? HFB_OK : HFB_CUDA;
+}
+double* hfc_red_alloc(Run& R, const char* key, int64_t n) {
+  const int64_t lo[] = {1}, hi[] = {n + 1};
+  const int roles[] = {0};
+  HFC_CHECK(hfb_plugin_scratch(R.ctx, key, 1, lo, hi, roles));
+  hfb_view v;
+  HFC_CHECK(hfb_plugin_view(R.ctx, key, &v));
+  return v.origin;
+}
+double hfc_red_finish(Run& R, double* partials, int64_t n, double init, int is_mul) {
+  hfc_ordered<<<1, 1, 0, R.stream>>>(partials, n, init, is_mul, partials + n);
+  HFC_CHECK(hfc_launched(R));
+  double out = 0.0;
+  if (cudaMemcpyAsync(&out, partials + n, sizeof(double), cudaMemcpyDeviceToHost, R.stream) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(R.stream) != cudaSuccess)
+    throw static_cast<int>(HFB_CUDA);
+  R.st->native_launches -= 1;  // the combine is part of the one virtual launch
+  return out;
 }
 """
 

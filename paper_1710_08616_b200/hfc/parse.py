@@ -96,6 +96,7 @@ class Decl:
     type: str       # 'int' | 'real' | 'logical'
     dims: list      # [(lo_expr, hi_expr)] ; empty for scalars
     intent: str = ""
+    param: object = None  # value expression of a `parameter`
 
 
 @dataclass
@@ -340,7 +341,8 @@ def parse_attrs(s, line):
 
 
 _DECL = re.compile(r"^(integer\s*\(\s*4\s*\)|real\s*\(\s*r_size\s*\)|logical|type\s*\(\s*dim3\s*\))"
-                   r"\s*(,\s*intent\s*\(\s*(in|out|inout)\s*\))?\s*::\s*(.*)$", re.I)
+                   r"\s*(,\s*intent\s*\(\s*(in|out|inout)\s*\))?(\s*,\s*parameter)?\s*::\s*(.*)$",
+                   re.I)
 
 
 def parse_decl(text, line):
@@ -351,13 +353,19 @@ def parse_decl(text, line):
     typ = "int" if t.startswith("integer") else "real" if t.startswith("real") else (
         "logical" if t == "logical" else "dim3")
     intent = (m.group(3) or "").lower()
+    is_param = m.group(4) is not None
     out = []
-    for item in split_top(m.group(4)):
-        mm = re.match(r"(\w+)\s*(\((.*)\))?$", item.strip(), re.S)
+    for item in split_top(m.group(5)):
+        mm = re.match(r"(\w+)\s*(\((.*)\))?\s*(=\s*(.*))?$", item.strip(), re.S)
         if not mm:
             raise ParseError(f"line {line}: bad declaration {item!r}")
         dims = parse_dims(mm.group(3), line) if mm.group(3) else []
-        out.append(Decl(mm.group(1).lower(), typ, dims, intent))
+        d = Decl(mm.group(1).lower(), typ, dims, intent)
+        if is_param:
+            if mm.group(5) is None or dims:
+                raise ParseError(f"line {line}: a parameter needs a scalar value")
+            d.param = parse_expr(mm.group(5), line)
+        out.append(d)
     return out
 
 

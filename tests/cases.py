@@ -73,6 +73,13 @@ APPS = {
         dict({n: ("nz", "nx", "ny") for n in ("rho", "th", "u", "v", "w", "p")},
              tsfc=("nx", "ny"), colm=("nx", "ny")),
         ["th", "u", "v", "w", "p", "colm"], entry="main_full", program="dycore"),
+    # feature coverage of the code generator (hfc); not a built-in program of the engine
+    "kitchen": App(
+        "kitchen", [("own", "kitchen/kit_state.h90"), ("own", "kitchen/kitchen.h90")],
+        "kit_state",
+        {"a": ("nz", "nx", "ny"), "b": ("nz", "nx", "ny"), "c": ("nx", "ny"),
+         "halo": ("0:nz", "0:nx", "ny")},
+        ["a", "b", "c", "halo", "alpha", "total_host"], program="kitchen_gen"),
 }
 
 # Synthetic-state conventions; seeds are fixed per field.
@@ -170,3 +177,20 @@ CASES = [
     _rk3("rk3_33x3x58_s1", 33, 3, 58, 1),
 ]
 CASE_BY_NAME = {c.name: c for c in CASES}
+
+
+def _kit(name, nx, ny, nz, nsteps, shift):
+    return Case(name, "kitchen", dict(nx=nx, ny=ny, nz=nz, nsteps=nsteps, shift=shift),
+                dict(alpha=0.7, total_host=0.0),
+                {"a": (21, -0.5, 1.0), "b": (22, 0.0, 2.0), "c": (23, 0.0, 1.0),
+                 "halo": (24, 0.0, 1.0)})
+
+
+# programs run only through generated code (hfc plugins); goldens by the reference itself
+HFC_CASES = [
+    _kit("kitchen_13x7x5_s2", 13, 7, 5, 2, 1),
+    _kit("kitchen_37x21x9_s3", 37, 21, 9, 3, 4),
+    _kit("kitchen_3x3x3_s1", 3, 3, 3, 1, 0),
+    _kit("kitchen_33x4x12_s2", 33, 4, 12, 2, -2),
+]
+CASE_BY_NAME.update({c.name: c for c in HFC_CASES})

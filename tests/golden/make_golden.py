@@ -23,7 +23,7 @@ import numpy as np
 
 HERE = Path(__file__).resolve().parent
 sys.path.insert(0, str(HERE.parent))
-from cases import APPS, CASES, OWN_APPS, REF_APPS, REPO  # noqa: E402
+from cases import APPS, CASES, HFC_CASES, OWN_APPS, REF_APPS, REPO  # noqa: E402
 from hfb_dump import read_dump  # noqa: E402
 
 HFT_REF = REPO / "oracle" / "_ref" / "hft_ref"
@@ -76,7 +76,7 @@ def same_bits(a, b):
 def main(names):
     if not HFT_REF.exists():
         subprocess.run(["make", "-C", str(REPO / "oracle"), "ref"], check=True)
-    cases = [c for c in CASES if not names or c.name in names]
+    cases = [c for c in CASES + HFC_CASES if not names or c.name in names]
     with tempfile.TemporaryDirectory() as tmp:
         for case in cases:
             app = APPS[case.app]
