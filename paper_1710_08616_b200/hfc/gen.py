@@ -843,7 +843,8 @@ class Gen:
                 v = hsc.get(e.name)
                 if v is not None and v[0] == "harray" and e.name not in used_arrays:
                     used_arrays.append(e.name)
-                for a in e.args:
+                # real(x, kind): the kind argument is not a value
+                for a in (e.args[:1] if e.name == "real" and v is None else e.args):
                     scan_e(a)
             elif isinstance(e, Bin):
                 scan_e(e.a)
@@ -898,7 +899,8 @@ class Gen:
                 kloc.append(f"  double {n} = {'1.0' if red[0] == '*' else '0.0'};")
                 continue
             if v[0] == "mscalar":
-                raise GenError(f"{r.name}:{s.line}: module scalar {n} written in a region")
+                raise GenError(f"{r.name}:{s.line}: module scalar {n} written in a region "
+                               "outside a reduce(...) clause")
             ksc.set(n, "scalar", v[1], n)
             kloc.append(f"  {self.ctype(v[1])} {n} = {self.zero(v[1])};")
         lo_c = [self.em.expr(e, ksc) for e in lo]
