@@ -1244,6 +1244,10 @@ double* hfc_red_alloc(Run& R, const char* key, int64_t n) {
   return v.origin;
 }
 double hfc_red_finish(Run& R, double* partials, int64_t n, double init, int is_mul) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(R.stream, &cap);
+  if (cap != cudaStreamCaptureStatusNone)  // the result is needed on the host now
+    throw static_cast<int>(HFB_CONFIG);
   hfc_ordered<<<1, 1, 0, R.stream>>>(partials, n, init, is_mul, partials + n);
   HFC_CHECK(hfc_launched(R));
   double out = 0.0;

@@ -137,3 +137,48 @@ def test_generated_reference_corpus_matches_reference(case):
     assert stats.threads == meta["gpu_threads"]
     assert stats.guard_returns == meta["gpu_guard_returns"]
     assert stats.native_launches >= 1
+
+
+def test_generated_program_graph_replay():
+    """hfb_run_graph captures the generated host driver's launches (after one warm step has
+    materialised the scratch arrays) and replays them: 1 enqueued + 2 replayed steps equal
+    the reference's 3 steps, with the same launch accounting per step."""
+    case = [c for c in DYCORE_CASES if c.name == "dycore_13x7x10_s3"][0]
+    arrs = make_inputs(case)
+    with hfb.Engine(str(GEN)) as eng:
+        for k, v in case.ints.items():
+            eng.set(k, int(v))
+        for k, v in case.reals.items():
+            eng.set(k, float(v))
+        for name, a in arrs.items():
+            eng.bind(name, a)
+        for name in arrs:
+            eng.copy_to_device(name)
+        one = eng.enqueue("dycore_step")
+        eng.synchronize()
+        two = eng.run_graph("dycore_step", 2)
+        for name in arrs:
+            eng.copy_from_device(name)
+    assert two.launches == 2 * one.launches and two.threads == 2 * one.threads
+    _, out, _, _ = load_golden(case.name)
+    for name in APPS[case.app].outputs:
+        assert bits_equal(arrs[name], out[name]), name
+
+
+def test_generated_reduction_refuses_graph_capture():
+    so = hfc.GEN_DIR / "reduction_gen.so"
+    if not so.exists():
+        pytest.skip("reduction_gen.so not built")
+    case = [c for c in CORPUS if c.app == "reduction"][0]
+    arrs = make_inputs(case)
+    with hfb.Engine(str(so)) as eng:
+        for k, v in case.ints.items():
+            eng.set(k, int(v))
+        for k, v in case.reals.items():
+            eng.set(k, float(v))
+        for name, a in arrs.items():
+            eng.bind(name, a)
+        eng.copy_to_device("y")
+        eng.run("grid_total")  # warm (allocates the partials)
+        with pytest.raises(hfb.HfbError):
+            eng.run_graph("grid_total", 1)
