@@ -9,7 +9,10 @@ Workload (BASELINE.json configs[1]): 512 x 512 x 58 per GPU, fp64, synthetic sta
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 N > 1 runs under torchrun, one rank per GPU: a 2-D (px x py) horizontal block
-decomposition with NCCL halo exchange, WEAK scaling (a 512 x 512 x 58 tile per GPU).
+decomposition, WEAK scaling (a 512 x 512 x 58 tile per GPU). The halo exchange uses the
+peer-memory transport (push kernels storing into the neighbours' halo rings over
+NVLink/NVSwitch, CUDA IPC-mapped buffers, release/acquire flags); `--transport nccl`
+selects NCCL send/recv instead.
 `--impl reference` times the reference's own CPU path (oracle/_ref/hft_ref: the
 reference interpreter built from /root/reference/proj/src) on the host cores.
 """
@@ -107,6 +110,20 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def decompose(eng, d, n, transport, dist):
+    """Attach the rank's tile; NCCL needs the shared unique id now, the peer transport
+    maps the neighbours' buffers once the state is bound (Engine.attach_peers)."""
+    if n == 1:
+        return
+    if transport == "nccl":
+        import paper_1710_08616_b200 as hfb
+        obj = [hfb.runtime.nccl_unique_id() if d.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        eng.set_decomposition(d, obj[0])
+    else:
+        eng.set_decomposition(d)
 
 
 def make_state(eng, d, px, py):
@@ -222,16 +239,23 @@ def bench_ours(args):
     if n not in GRIDS:
         raise SystemExit("--gpus must be 1, 2, 4 or 8")
     px, py = GRIDS[n]
+    # HFB_BENCH_ONE_GPU=1 (testing only): every rank on cuda:0, gloo for the host-side
+    # collectives — exercises the multi-rank path (peer transport) on a one-GPU box
+    one_gpu = os.environ.get("HFB_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if n > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     eng = hfb.Engine("dycore", device=local)
     d = hfb.decomp_init(NX * px, NY * py, NZ, px, py, rank, halo=2)
-    if n > 1:
-        obj = [hfb.runtime.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        eng.set_decomposition(d, obj[0])
+    decompose(eng, d, n, args.transport, dist)
     arrs = make_state(eng, d, px, py)
+    if n > 1 and args.transport == "peer":
+        eng.attach_peers()
     for k in arrs:
         eng.copy_to_device(k)
     eng.synchronize()
@@ -265,7 +289,7 @@ def bench_ours(args):
     kt = {k: eng.kernel_time(k) for k in BYTES_PER_POINT}
     kt = {k: v for k, v in kt.items() if v[1] > 0}
     if n > 1:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device="cpu" if one_gpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     pts_step = NX * NY * NZ * n
@@ -276,8 +300,12 @@ def bench_ours(args):
     dom = max(kt, key=lambda k: kt[k][0])
     dom_ms, dom_n = kt[dom]
     pts_local = int(d.nx) * int(d.ny) * NZ
+    # one step of the tile is one launch (N=1) or the interior launch plus four boundary
+    # strips (decomposed, halo exchange overlapped): the kernel's device time per STEP
+    # moves the tile's algorithmic bytes
     alg_bytes = BYTES_PER_POINT[dom] * pts_local
-    achieved = alg_bytes / (dom_ms / dom_n / 1e3) / 1e9
+    per_step = dom_ms / args.steps
+    achieved = alg_bytes / (per_step / 1e3) / 1e9
     traffic = None
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists():
@@ -285,11 +313,12 @@ def bench_ours(args):
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": traffic, "kernel": dom,
                 "peak_source": src, "algorithmic_bytes_per_launch": alg_bytes,
-                "kernel_ms_avg": round(dom_ms / dom_n, 5),
+                "launches_per_step": dom_n // args.steps,
+                "kernel_ms_avg": round(per_step, 5),
                 "share_of_step": round(dom_ms / ms, 3),
-                "kernels": {k: {"ms_avg": round(v[0] / max(v[1], 1), 5),
+                "kernels": {k: {"ms_avg": round(v[0] / args.steps, 5),
                                 "GBps": round(BYTES_PER_POINT[k] * pts_local /
-                                              (v[0] / max(v[1], 1) / 1e3) / 1e9, 1)}
+                                              (v[0] / args.steps / 1e3) / 1e9, 1)}
                             for k, v in kt.items()}}
 
     # ---- end to end through the public API with host buffers --------------------------
@@ -298,11 +327,10 @@ def bench_ours(args):
     # generated host code does (codegen.cpp:570-600)
     e2e_nsteps = 100
     eng2 = hfb.Engine("dycore", device=local)
-    if n > 1:
-        obj = [hfb.runtime.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        eng2.set_decomposition(d, obj[0])
+    decompose(eng2, d, n, args.transport, dist)
     arrs2 = make_state(eng2, d, px, py)
+    if n > 1 and args.transport == "peer":
+        eng2.attach_peers()
     eng2.set("nsteps", e2e_nsteps)
     eng2.run("main")  # warm-up call
     arrs2 = make_state(eng2, d, px, py)
@@ -315,7 +343,7 @@ def bench_ours(args):
     t1 = time.perf_counter()
     e2e_s = t1 - t0
     if n > 1:
-        t = torch.tensor([e2e_s], device="cuda")
+        t = torch.tensor([e2e_s], device="cpu" if one_gpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     field_bytes = pts_local * 8
@@ -338,6 +366,7 @@ def bench_ours(args):
                "data": "synthetic (SplitMix64 fields, SURVEY §8(d))",
                "config": {"workload": f"dycore+HE-VI {NX}x{NY}x{NZ} per GPU (BASELINE configs[1])",
                           "global_grid": [NX * px, NY * py, NZ], "decomposition": f"{px}x{py}",
+                          "transport": args.transport if n > 1 else None,
                           "l2": f"inputs larger than L2: {6 * NX * NY * NZ * 8 / 2**30:.2f} GiB "
                                 f"state + {5 * NX * NY * NZ * 8 / 2**30:.2f} GiB outputs per step "
                                 f"vs 126 MB L2"},
@@ -413,6 +442,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="halo exchange for N > 1 (peer: P2P stores + flags; nccl: send/recv)")
     ap.add_argument("--no-secondary", action="store_true",
                     help="skip the single-GPU timings of the other BASELINE configs")
     args = ap.parse_args()

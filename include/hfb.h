@@ -202,6 +202,16 @@ hfb_status hfb_group_run(hfb_group* group, const char* entry, hfb_launch_stats* 
 int64_t hfb_halo_bytes(hfb_ctx* ctx);
 /* 128-byte ncclUniqueId for hfb_set_decomposition (rank 0 creates, all ranks share) */
 hfb_status hfb_nccl_unique_id(void* out128);
+/* Peer-memory transport (one process per rank, NVLink/NVSwitch P2P; replaces NCCL for
+ * the halo exchange and the reduction): after hfb_set_decomposition (NULL id) and
+ * binding every array, each rank exports a blob (its device buffers' CUDA IPC handles,
+ * layouts and a signal block; `buf` NULL queries the length), the caller all-gathers
+ * the blobs (e.g. torch.distributed) and every rank attaches all of them. Halo updates
+ * are then one push kernel storing the boundary cells straight into the neighbours'
+ * halo rings (corners included, single phase) plus a release/acquire flag; reductions
+ * sum the ranks' partials in rank order (deterministic). */
+hfb_status hfb_peer_export(hfb_ctx* ctx, void* buf, size_t cap, size_t* len);
+hfb_status hfb_peer_attach(hfb_ctx* ctx, int n, const void* const* blobs, const size_t* lens);
 
 /* --- reductions (reduction.h90 `reduce(+:total)`) ---------------------------------- */
 /* 0 (default): fast two-level tree sum, equal to the reference to 1e-12 relative

@@ -882,4 +882,102 @@ cudaError_t launch_pack_box(const double* field, double* buf, Grid3 g, int64_t n
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// peer-memory halo transport
+// ---------------------------------------------------------------------------
+namespace {
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys_f64(double* p, double v) {
+  asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// blockIdx.y: box; threads stride over the box's cells, i fastest (rows of the face are
+// contiguous on both sides)
+__global__ void __launch_bounds__(256) k_peer_push(const __grid_constant__ PeerPush p) {
+  const PeerBox& b = p.box[blockIdx.y];
+  const int64_t total = b.nbi * b.nbj * b.nk;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t ii = t % b.nbi, rest = t / b.nbi, jj = rest % b.nbj, k = rest / b.nbj;
+    b.dst[b.gd.at(b.di0 - 1 + ii, b.dj0 - 1 + jj, k)] =
+        b.src[b.gs.at(b.si0 - 1 + ii, b.sj0 - 1 + jj, k)];
+  }
+}
+
+struct FlagList {
+  uint64_t* f[16];
+};
+
+__global__ void k_peer_signal(FlagList fl, int n, uint64_t epoch) {
+  // every push of this stream completed before this kernel started (stream order); the
+  // system-scope fence makes them visible to whoever acquires the flag
+  __threadfence_system();
+  for (int q = 0; q < n; ++q) st_release_sys(fl.f[q], epoch);
+}
+
+__global__ void k_peer_wait(FlagList fl, int n, uint64_t epoch) {
+  const int q = threadIdx.x;
+  if (q < n)
+    while (ld_acquire_sys(fl.f[q]) < epoch) __nanosleep(128);
+}
+
+__global__ void k_peer_allreduce(const __grid_constant__ PeerReduce r) {
+  const double v = *r.value;
+  const int par = static_cast<int>(r.epoch & 1);
+  for (int q = 0; q < r.n; ++q) st_relaxed_sys_f64(r.slots[q] + par * 64 + r.rank, v);
+  __threadfence_system();
+  for (int q = 0; q < r.n; ++q) st_release_sys(r.flags[q] + r.rank, r.epoch);
+  for (int q = 0; q < r.n; ++q)
+    while (ld_acquire_sys(r.my_flags + q) < r.epoch) __nanosleep(128);
+  double acc = 0.0;  // rank order: every rank computes the identical total
+  for (int q = 0; q < r.n; ++q) acc += r.my_slots[par * 64 + q];
+  *r.value = acc;
+}
+
+}  // namespace
+
+cudaError_t launch_peer_push(const PeerPush& p, cudaStream_t s) {
+  if (p.n <= 0) return cudaSuccess;
+  int64_t most = 0;
+  for (int q = 0; q < p.n; ++q)
+    most = std::max(most, p.box[q].nbi * p.box[q].nbj * p.box[q].nk);
+  if (most == 0) return cudaSuccess;
+  const unsigned bx = static_cast<unsigned>(std::min<int64_t>((most + 255) / 256, 64));
+  k_peer_push<<<dim3(bx, static_cast<unsigned>(p.n)), 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_signal(uint64_t* const* flags, int n, uint64_t epoch, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  if (n > 16) return cudaErrorInvalidValue;
+  FlagList fl{};
+  for (int q = 0; q < n; ++q) fl.f[q] = flags[q];
+  k_peer_signal<<<1, 1, 0, s>>>(fl, n, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_wait(const uint64_t* const* flags, int n, uint64_t epoch,
+                             cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  if (n > 16) return cudaErrorInvalidValue;
+  FlagList fl{};
+  for (int q = 0; q < n; ++q) fl.f[q] = const_cast<uint64_t*>(flags[q]);
+  k_peer_wait<<<1, 32, 0, s>>>(fl, n, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_allreduce(const PeerReduce& r, cudaStream_t s) {
+  if (r.n < 1 || r.n > 64) return cudaErrorInvalidValue;
+  k_peer_allreduce<<<1, 1, 0, s>>>(r);
+  return cudaGetLastError();
+}
+
 }  // namespace hfb

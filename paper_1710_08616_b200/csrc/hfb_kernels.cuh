@@ -132,4 +132,40 @@ cudaError_t launch_column_physics(const double* rho, double* th, const double* u
 cudaError_t launch_pack_box(const double* field, double* buf, Grid3 g, int64_t nk,
                             const int64_t box[4], bool pack, cudaStream_t s);
 
+// ---- peer-memory halo transport (NVLink / NVSwitch P2P stores) -----------------------
+// one box: interior cells of a local field stored straight into a neighbour's halo ring
+// (the neighbour's buffer is mapped into this process by CUDA IPC); (i, j) are 1-based
+// tile-local, the same k range on both sides
+struct PeerBox {
+  const double* src;   // local field origin
+  double* dst;         // remote field origin (the neighbour's layout)
+  Grid3 gs, gd;
+  int64_t si0, sj0;    // first source cell
+  int64_t di0, dj0;    // where it lands on the neighbour
+  int64_t nbi, nbj, nk;
+};
+constexpr int kMaxPeerBoxes = 64;
+struct PeerPush {
+  PeerBox box[kMaxPeerBoxes];
+  int n;
+};
+cudaError_t launch_peer_push(const PeerPush& p, cudaStream_t s);
+// release `epoch` into each remote flag (system scope, after the pushes on this stream)
+cudaError_t launch_peer_signal(uint64_t* const* flags, int n, uint64_t epoch, cudaStream_t s);
+// wait until every local flag reached `epoch` (acquire, system scope)
+cudaError_t launch_peer_wait(const uint64_t* const* flags, int n, uint64_t epoch,
+                             cudaStream_t s);
+// deterministic all-reduce of one double over n ranks through peer memory: my value goes
+// to slot [parity][rank] of every rank, then every rank sums slots 0..n-1 in rank order
+struct PeerReduce {
+  double* value;               // in: this rank's partial; out: the total
+  double* slots[64];           // every rank's slot array (remote, or local for self)
+  uint64_t* flags[64];         // every rank's reduction flag array
+  double* my_slots;            // this rank's slot array
+  uint64_t* my_flags;          // this rank's reduction flags
+  int n, rank;
+  uint64_t epoch;
+};
+cudaError_t launch_peer_allreduce(const PeerReduce& r, cudaStream_t s);
+
 }  // namespace hfb

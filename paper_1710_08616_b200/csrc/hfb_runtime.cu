@@ -221,6 +221,22 @@ struct hfb_group {
 };
 
 namespace {
+// peer-memory transport: a neighbour's field buffers and signal block, mapped into this
+// process by CUDA IPC (hfb_peer_attach)
+struct PeerField {
+  double* base[3] = {nullptr, nullptr, nullptr};
+  int nbuf = 0;
+  int64_t pitch = 0, plane = 0, origin_off = 0;
+};
+struct PeerRank {
+  int64_t nx = 0, ny = 0;
+  uint64_t* sig = nullptr;
+  std::map<std::string, PeerField> fields;
+};
+// signal block layout (uint64 words): [0, 9) halo flags by the sender's offset from the
+// receiver, [16, 80) reduction flags by sender rank, then 2 x 64 doubles of reduction
+// slots (parity of the reduction epoch)
+constexpr int kSigHalo = 0, kSigRed = 16, kSigSlots = 80, kSigWords = 80 + 128;
 // device scratch of generated programs: routine-local arrays (hfb_plugin_scratch)
 struct Scratch {
   Layout lay;
@@ -261,6 +277,13 @@ struct hfb_ctx {
   double* halo_recv = nullptr;
   size_t halo_cap = 0;
   std::map<std::string, Scratch> scratch;  // generated programs' routine-local arrays
+  // peer-memory halo transport (hfb_peer_export / hfb_peer_attach): halos are stored
+  // straight into the neighbours' buffers over NVLink, flags signal their arrival
+  bool peer = false;
+  uint64_t* peer_sig = nullptr;
+  uint64_t halo_epoch = 0, red_epoch = 0;
+  std::vector<PeerRank> peers;
+  std::vector<void*> ipc_opened;
   // halo exchange overlapped with the interior columns (decomposed stencil steps): the
   // exchange runs on `comm` while the columns that never read the halo ring run on
   // `stream`; the boundary strips follow the exchange (HFB_NO_OVERLAP=1 serialises)
@@ -1121,10 +1144,79 @@ constexpr int kNcclSum = 0;
 // then north/south faces spanning the I halo so corners arrive too.
 void group_pull(hfb_ctx* c, const std::vector<const char*>& fields, cudaStream_t st);
 
+// Peer-memory halo update: ONE push kernel stores this tile's boundary cells of every
+// field into the halo rings of its (up to 8) neighbours — corners go straight to the
+// diagonal neighbours, so there is a single phase —, a one-thread kernel releases the
+// exchange epoch into each neighbour's flag, and a wait kernel acquires the flags of the
+// neighbours that write into this tile. Everything is stream-ordered: the caller's
+// stream sees the halos when the wait kernel retires. Lockstep is structural: a rank
+// pushes exchange e only after its step e-1 (and so its reads of the halos exchange e-2
+// wrote into the same buffers) has completed, and it cannot start step e before every
+// neighbour's push e arrived.
+void peer_exchange(hfb_ctx* c, const std::vector<const char*>& fields, cudaStream_t st) {
+  const hfb_decomp& d = c->decomp;
+  const int64_t H = d.halo;
+  if (H == 0) return;
+  const uint64_t epoch = ++c->halo_epoch;
+  PeerPush push{};
+  std::vector<uint64_t*> remote_flags;
+  std::vector<const uint64_t*> my_flags;
+  for (int dy = -1; dy <= 1; ++dy)
+    for (int dx = -1; dx <= 1; ++dx) {
+      if (dx == 0 && dy == 0) continue;
+      const int rx = d.rx + dx, ry = d.ry + dy;
+      if (rx < 0 || rx >= d.px || ry < 0 || ry >= d.py) continue;
+      const int nr = ry * d.px + rx;
+      PeerRank& pr = c->peers.at(nr);
+      // my boundary cells -> the neighbour's halo (its tile-local coordinates)
+      const int64_t si0 = dx < 0 ? 1 : dx == 0 ? 1 : d.nx - H + 1;
+      const int64_t nbi = dx == 0 ? d.nx : H;
+      const int64_t di0 = dx < 0 ? pr.nx + 1 : dx == 0 ? 1 : 1 - H;
+      const int64_t sj0 = dy < 0 ? 1 : dy == 0 ? 1 : d.ny - H + 1;
+      const int64_t nbj = dy == 0 ? d.ny : H;
+      const int64_t dj0 = dy < 0 ? pr.ny + 1 : dy == 0 ? 1 : 1 - H;
+      for (const char* f : fields) {
+        Slot& sl = slot(c, f);
+        auto it = pr.fields.find(f);
+        if (it == pr.fields.end() || sl.cur >= it->second.nbuf || !it->second.base[sl.cur])
+          fail(HFB_CONFIG, "peer transport: buffer %d of '%s' on rank %d is not mapped "
+               "(export after binding every array)", sl.cur, f, nr);
+        if (push.n == kMaxPeerBoxes) fail(HFB_CONFIG, "peer transport: too many halo boxes");
+        const PeerField& rf = it->second;
+        PeerBox& b = push.box[push.n++];
+        b.src = sl.d();
+        b.dst = rf.base[sl.cur] + rf.origin_off;
+        b.gs = grid_of(sl);
+        b.gd = Grid3{rf.pitch, rf.plane};
+        b.si0 = si0;
+        b.sj0 = sj0;
+        b.di0 = di0;
+        b.dj0 = dj0;
+        b.nbi = nbi;
+        b.nbj = nbj;
+        b.nk = sl.lay.nk * sl.lay.nl;
+        c->halo_bytes += 2 * nbi * nbj * b.nk * static_cast<int64_t>(sizeof(double));
+      }
+      // I am at offset (-dx, -dy) from the receiver
+      remote_flags.push_back(pr.sig + kSigHalo + (1 - dy) * 3 + (1 - dx));
+      my_flags.push_back(c->peer_sig + kSigHalo + (dy + 1) * 3 + (dx + 1));
+    }
+  cuda_check(launch_peer_push(push, st), "peer halo push");
+  cuda_check(launch_peer_signal(remote_flags.data(), static_cast<int>(remote_flags.size()), epoch,
+                                st),
+             "peer signal");
+  cuda_check(launch_peer_wait(my_flags.data(), static_cast<int>(my_flags.size()), epoch, st),
+             "peer wait");
+}
+
 void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width,
                    cudaStream_t st) {
   if (!c->decomposed || c->decomp.px * c->decomp.py <= 1) return;
   if (!st) st = c->stream;
+  if (c->peer) {
+    peer_exchange(c, fields, st);
+    return;
+  }
   if (c->group) {
     group_pull(c, fields, st);
     return;
@@ -1250,6 +1342,23 @@ void group_pull(hfb_ctx* c, const std::vector<const char*>& fields, cudaStream_t
 }
 
 void allreduce_sum(hfb_ctx* c, double* dev_value) {
+  if (c->peer) {  // deterministic: every rank sums the partials in rank order
+    const hfb_decomp& d = c->decomp;
+    PeerReduce r{};
+    r.value = dev_value;
+    r.n = d.px * d.py;
+    r.rank = d.rank;
+    r.epoch = ++c->red_epoch;
+    for (int q = 0; q < r.n; ++q) {
+      uint64_t* base = q == d.rank ? c->peer_sig : c->peers.at(q).sig;
+      r.slots[q] = reinterpret_cast<double*>(base + kSigSlots);
+      r.flags[q] = base + kSigRed;
+    }
+    r.my_slots = reinterpret_cast<double*>(c->peer_sig + kSigSlots);
+    r.my_flags = c->peer_sig + kSigRed;
+    cuda_check(launch_peer_allreduce(r, c->stream), "peer all-reduce");
+    return;
+  }
   NcclApi& api = nccl();
   nccl_check(api.AllReduce(dev_value, dev_value, 1, kNcclFloat64, kNcclSum, c->nccl_comm,
                            c->stream),
@@ -1354,6 +1463,8 @@ void hfb_destroy(hfb_ctx* c) {
   if (c->red_host) cudaFreeHost(c->red_host);
   if (c->halo_send) cudaFree(c->halo_send);
   if (c->halo_recv) cudaFree(c->halo_recv);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (c->peer_sig) cudaFree(c->peer_sig);
   if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
   if (c->nccl_comm) nccl().CommDestroy(c->nccl_comm);
   for (auto& t : c->pending) {
@@ -1445,8 +1556,8 @@ hfb_status hfb_bind_array(hfb_ctx* c, const char* module, const char* name, int 
     if (rank != static_cast<int>(s.decl->dims.size()))
       fail(HFB_RUNTIME, "array '%s' has rank %zu but is bound with rank %d", name,
            s.decl->dims.size(), rank);
-    if (s.has_device) {
-      // rebinding keeps the device copy only if the shape is unchanged
+    if (s.has_device || s.dev[0]) {
+      // rebinding keeps the device buffers only if the shape is unchanged
       for (int d = 0; d < rank; ++d)
         if (lo[d] != s.lower[d] || hi[d] != s.upper[d])
           fail(HFB_CONFIG, "rebinding '%s' with a different shape after a transfer", name);
@@ -2017,6 +2128,130 @@ hfb_status hfb_nccl_unique_id(void* out128) {
     NcclId id;
     nccl_check(get(&id), "ncclGetUniqueId");
     std::memcpy(out128, id.internal, sizeof id.internal);
+  });
+}
+
+}  // extern "C"
+
+// ---- peer-memory transport: export / attach ----------------------------------------
+namespace {
+
+constexpr char kPeerMagic[8] = {'H', 'F', 'B', 'P', 'E', 'E', 'R', '1'};
+struct PeerBlobHead {
+  char magic[8];
+  int32_t rank, nranks, device, nfields;
+  int64_t nx, ny;
+  cudaIpcMemHandle_t sig;
+};
+struct PeerBlobField {
+  char name[48];
+  int32_t nbuf, pad;
+  int64_t pitch, plane, origin_off;
+  cudaIpcMemHandle_t h[3];
+};
+
+}  // namespace
+
+extern "C" {
+
+hfb_status hfb_peer_export(hfb_ctx* c, void* buf, size_t cap, size_t* len) {
+  return guarded([&] {
+    if (!c || !c->app) fail(HFB_CONFIG, "no program loaded");
+    if (!c->decomposed || c->decomp.px * c->decomp.py <= 1)
+      fail(HFB_CONFIG, "peer transport needs a multi-rank decomposition");
+    if (c->group) fail(HFB_CONFIG, "in-process groups exchange halos by device copies");
+    cudaSetDevice(c->device);
+    if (!c->peer_sig) {
+      cuda_check(cudaMalloc(&c->peer_sig, kSigWords * sizeof(uint64_t)), "cudaMalloc(signals)");
+      cuda_check(cudaMemset(c->peer_sig, 0, kSigWords * sizeof(uint64_t)), "cudaMemset");
+    }
+    // every bound array gets its device buffers now (double-buffered fields: all three
+    // stage buffers), so the neighbours can map them before the first step
+    std::vector<PeerBlobField> fs;
+    for (auto& [name, s] : c->slots) {
+      if (!s.host) continue;
+      check_bounds(c, s);
+      ensure_device(c, s, s.decl->pingpong, s.decl->pingpong ? 3 : 1);
+      PeerBlobField f{};
+      if (name.size() >= sizeof f.name) fail(HFB_CONFIG, "array name '%s' too long", name.c_str());
+      std::strncpy(f.name, name.c_str(), sizeof f.name - 1);
+      for (int b = 0; b < 3; ++b) {
+        if (!s.dev[b]) break;
+        cuda_check(cudaIpcGetMemHandle(&f.h[b], s.dev[b]), "cudaIpcGetMemHandle");
+        f.nbuf = b + 1;
+      }
+      f.pitch = s.lay.pitch;
+      f.plane = s.lay.plane;
+      f.origin_off = s.lay.origin_off;
+      fs.push_back(f);
+    }
+    cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    PeerBlobHead h{};
+    std::memcpy(h.magic, kPeerMagic, 8);
+    h.rank = c->decomp.rank;
+    h.nranks = c->decomp.px * c->decomp.py;
+    h.device = c->device;
+    h.nfields = static_cast<int32_t>(fs.size());
+    h.nx = c->decomp.nx;
+    h.ny = c->decomp.ny;
+    cuda_check(cudaIpcGetMemHandle(&h.sig, c->peer_sig), "cudaIpcGetMemHandle(signals)");
+    const size_t need = sizeof h + fs.size() * sizeof(PeerBlobField);
+    *len = need;
+    if (!buf) return;
+    if (cap < need) fail(HFB_CONFIG, "peer blob needs %zu bytes", need);
+    std::memcpy(buf, &h, sizeof h);
+    if (!fs.empty())
+      std::memcpy(static_cast<char*>(buf) + sizeof h, fs.data(), fs.size() * sizeof(PeerBlobField));
+  });
+}
+
+hfb_status hfb_peer_attach(hfb_ctx* c, int n, const void* const* blobs, const size_t* lens) {
+  return guarded([&] {
+    if (!c || !c->peer_sig) fail(HFB_CONFIG, "hfb_peer_export first");
+    const hfb_decomp& d = c->decomp;
+    if (n != d.px * d.py) fail(HFB_CONFIG, "%d blobs for %d ranks", n, d.px * d.py);
+    cudaSetDevice(c->device);
+    std::vector<PeerRank> peers(static_cast<size_t>(n));
+    std::vector<bool> seen(static_cast<size_t>(n), false);
+    auto open = [&](const cudaIpcMemHandle_t& hd) {
+      void* p = nullptr;
+      cuda_check(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess),
+                 "cudaIpcOpenMemHandle");
+      c->ipc_opened.push_back(p);
+      return p;
+    };
+    for (int q = 0; q < n; ++q) {
+      if (lens[q] < sizeof(PeerBlobHead)) fail(HFB_CONFIG, "peer blob %d truncated", q);
+      PeerBlobHead h;
+      std::memcpy(&h, blobs[q], sizeof h);
+      if (std::memcmp(h.magic, kPeerMagic, 8) != 0) fail(HFB_CONFIG, "blob %d is not a peer blob", q);
+      if (h.nranks != n || h.rank < 0 || h.rank >= n || seen[h.rank])
+        fail(HFB_CONFIG, "blob %d: rank %d of %d (duplicate or out of range)", q, h.rank, h.nranks);
+      seen[h.rank] = true;
+      if (lens[q] != sizeof h + static_cast<size_t>(h.nfields) * sizeof(PeerBlobField))
+        fail(HFB_CONFIG, "peer blob %d has a bad length", q);
+      if (h.rank == d.rank) continue;
+      PeerRank& pr = peers[h.rank];
+      pr.nx = h.nx;
+      pr.ny = h.ny;
+      pr.sig = static_cast<uint64_t*>(open(h.sig));
+      const int rx = h.rank % d.px, ry = h.rank / d.px;
+      if (std::abs(rx - d.rx) > 1 || std::abs(ry - d.ry) > 1) continue;  // not a neighbour
+      const char* fp = static_cast<const char*>(blobs[q]) + sizeof h;
+      for (int f = 0; f < h.nfields; ++f) {
+        PeerBlobField bf;
+        std::memcpy(&bf, fp + f * sizeof bf, sizeof bf);
+        PeerField pf;
+        pf.nbuf = bf.nbuf;
+        pf.pitch = bf.pitch;
+        pf.plane = bf.plane;
+        pf.origin_off = bf.origin_off;
+        for (int b = 0; b < bf.nbuf && b < 3; ++b) pf.base[b] = static_cast<double*>(open(bf.h[b]));
+        pr.fields[bf.name] = pf;
+      }
+    }
+    c->peers = std::move(peers);
+    c->peer = true;
   });
 }
 

@@ -44,6 +44,7 @@ EXPORTS = [
     "hfb_load_state", "hfb_host_array", "hfb_array_checksum", "hfb_run_scenario",
     "hfb_set_reduction_order", "hfb_program_name", "hfb_program_module", "hfb_plugin_prepare",
     "hfb_plugin_written", "hfb_plugin_view", "hfb_plugin_scratch", "hfb_plugin_host",
+    "hfb_peer_export", "hfb_peer_attach",
 ]
 
 # module of each built-in program (the apps' state modules)
@@ -142,6 +143,8 @@ def lib():
                                      c.POINTER(i64), c.POINTER(i64), c.POINTER(i64)]
         L.hfb_array_checksum.argtypes = [P, S, S, c.POINTER(dbl), c.POINTER(c.c_uint64)]
         L.hfb_run_scenario.argtypes = [P, S, c.POINTER(_Stats), c.c_char_p, c.c_size_t]
+        L.hfb_peer_export.argtypes = [P, P, c.c_size_t, c.POINTER(c.c_size_t)]
+        L.hfb_peer_attach.argtypes = [P, c.c_int, c.POINTER(P), c.POINTER(c.c_size_t)]
         _lib = L
     return _lib
 
@@ -347,6 +350,30 @@ class Engine:
         if nccl_id is not None:
             buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
         _check(lib().hfb_set_decomposition(self._h, ctypes.byref(d), buf))
+
+    def peer_export(self):
+        """This rank's peer-transport blob (CUDA IPC handles of its device buffers)."""
+        n = ctypes.c_size_t()
+        _check(lib().hfb_peer_export(self._h, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        _check(lib().hfb_peer_export(self._h, buf, n.value, ctypes.byref(n)))
+        return buf.raw[:n.value]
+
+    def peer_attach(self, blobs):
+        """Map every rank's blob (all ranks, in any order) and switch to the peer transport."""
+        keep = [ctypes.create_string_buffer(bytes(b), len(b)) for b in blobs]
+        ptrs = (ctypes.c_void_p * len(keep))(*[ctypes.addressof(k) for k in keep])
+        lens = (ctypes.c_size_t * len(keep))(*[len(b) for b in blobs])
+        _check(lib().hfb_peer_attach(self._h, len(keep), ptrs, lens))
+
+    def attach_peers(self, group=None):
+        """Collective over torch.distributed: export, all-gather, attach, barrier."""
+        import torch.distributed as dist
+        mine = self.peer_export()
+        blobs = [None] * dist.get_world_size(group)
+        dist.all_gather_object(blobs, mine, group=group)
+        self.peer_attach(blobs)
+        dist.barrier(group)
 
     def halo_bytes(self):
         return lib().hfb_halo_bytes(self._h)

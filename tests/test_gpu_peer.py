@@ -1,0 +1,127 @@
+"""The peer-memory transport (hfb_peer_export / hfb_peer_attach): one PROCESS per rank,
+the ranks' device buffers mapped into each other by CUDA IPC, halos stored straight into
+the neighbours' halo rings by one push kernel (corners to the diagonal neighbours) with a
+release/acquire flag per neighbour, reductions summed in rank order through peer memory.
+On a multi-GPU node the stores travel over NVLink/NVSwitch; here every rank's process
+shares the one GPU (CUDA IPC works within a device, NCCL refuses duplicate GPUs), which
+exercises the same kernels, flags and handle plumbing. The assembled tiles must equal
+the undecomposed oracle bit for bit."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_1710_08616_b200 as hfb
+from cases import APPS, DYCORE_FILLS, DYCORE_SCALARS, PHYS_FILLS, PHYS_SCALARS, Case
+from golden_io import bits_equal, decl, make_inputs, run_oracle
+from test_gpu_decomp import global_extent, tile_ints, tile_slices
+
+pytestmark = pytest.mark.gpu
+
+PEER_CASES = {
+    "dycore": Case("p_dycore", "dycore", dict(nx=70, ny=45, nz=20, nsteps=3),
+                   dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
+    "dycore_full": Case("p_full", "dycore_full", dict(nx=70, ny=45, nz=20, nsteps=2),
+                        dict(DYCORE_SCALARS, **PHYS_SCALARS),
+                        dict(DYCORE_FILLS, **PHYS_FILLS)),
+    "diffusion": Case("p_diff", "diffusion", dict(nx=40, ny=36, nz=12, nsteps=3),
+                      dict(coef=0.1), {"t_old": (1, 280.0, 10.0)}, unset=["t_new"]),
+    "reduction": Case("p_red", "reduction", dict(nx=67, ny=45, nz=20), dict(total=0.0),
+                      {"y": (6, 0.0, 1.0)}),
+}
+HALO = {"dycore": 2, "dycore_full": 2, "diffusion": 1, "reduction": 0}
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def worker(rank, world, port, name, px, py, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        case = PEER_CASES[name]
+        garr = make_inputs(case)
+        gnx, gny = global_extent(case)
+        d = hfb.decomp_init(gnx, gny, case.ints.get("nz", 1), px, py, rank, halo=HALO[name])
+        eng = hfb.Engine(APPS[case.app].prog, device=0)
+        eng.set_decomposition(d)
+        ints = tile_ints(case, d)
+        for k, v in ints.items():
+            eng.set(k, int(v))
+        for k, v in case.reals.items():
+            eng.set(k, float(v))
+        tiles = {}
+        for n, a in garr.items():
+            tiles[n] = np.ascontiguousarray(a[tile_slices(case.app, n, a, d)])
+            _, lower = decl(case.app, n, ints)
+            eng.bind(n, tiles[n], lower=lower)
+        eng.attach_peers()
+        stats = eng.run(APPS[case.app].entry)
+        total = eng.get("total") if case.app == "reduction" else None
+        q.put((rank, {k: (int(d.i0), int(d.j0)) for k in tiles}, tiles, total,
+               eng.halo_bytes(), stats.native_launches, None))
+        dist.barrier()
+        eng.close()
+    except Exception as e:  # report instead of hanging the parent
+        q.put((rank, None, None, None, 0, 0, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def run_peer(name, px, py):
+    world = px * py
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker, args=(r, world, port, name, px, py, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        parts = [q.get(timeout=300) for _ in range(world)]
+        for p in procs:
+            p.join(timeout=120)
+    finally:
+        for p in procs:  # a hung rank (e.g. a flag never released) must not outlive the test
+            if p.is_alive():
+                p.kill()
+    errors = [e for *_, e in parts if e]
+    assert not errors, errors
+    for p in procs:
+        assert p.exitcode == 0
+    case = PEER_CASES[name]
+    garr = make_inputs(case)
+    out = {k: np.empty_like(v) for k, v in garr.items()}
+    gnx, gny = global_extent(case)
+    for rank, _, tiles, _, _, _, _ in parts:
+        d = hfb.decomp_init(gnx, gny, case.ints.get("nz", 1), px, py, rank, halo=HALO[name])
+        for k, t in tiles.items():
+            out[k][tile_slices(case.app, k, out[k], d)] = t
+    return case, garr, out, parts
+
+
+@pytest.mark.parametrize("name,px,py", [("dycore", 2, 1), ("dycore", 2, 2), ("dycore", 4, 2),
+                                        ("dycore_full", 2, 2), ("diffusion", 2, 2)])
+def test_peer_transport_equals_single_domain(name, px, py):
+    case, garr, out, parts = run_peer(name, px, py)
+    ref = {k: v.copy() for k, v in garr.items()}
+    run_oracle(case, ref)
+    names = APPS[case.app].outputs if case.app != "diffusion" else ("t_old", "t_new")
+    for k in names:
+        assert bits_equal(out[k], ref[k]), f"{name} {px}x{py}: {k} differs"
+    assert all(p[4] > 0 for p in parts)  # every rank pushed halo bytes
+
+
+def test_peer_reduction_is_rank_ordered_and_identical_everywhere():
+    case, garr, _, parts = run_peer("reduction", 2, 2)
+    totals = [p[3] for p in parts]
+    assert len({np.float64(t).view(np.uint64) for t in totals}) == 1
+    ref = run_oracle(case, {k: v.copy() for k, v in garr.items()})["total"]
+    assert abs(totals[0] - ref) <= 1e-12 * abs(ref)
