@@ -587,8 +587,9 @@ struct Chk {
   static constexpr bool x = kX, y = kY;
 };
 
-template <bool kPhys, bool kRK>
-__global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
+template <bool kPhys, bool kRK, bool kRemote>
+__global__ void __launch_bounds__(kWsThreads, 2)
+    k_dyn_step_ws(StepTmemArgs a, const __grid_constant__ RemoteHalo rem) {
   static_assert(!(kPhys && kRK), "column physics is not fused into RK stages");
   extern __shared__ __align__(128) double smem[];
   __shared__ uint32_t tmem_base_slot;
@@ -682,6 +683,30 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
   double* out_v = a.out.v + col;
   const bool east = gi == gnx, west = gi == 1, north = gj == gny, south = gj == 1;
   const int thc = (row + 2) * kFThW + (lane + 2);
+  // kRemote: the neighbours (up to 3: edge, edge, corner) whose halo ring holds this
+  // column, and the column's offset in each neighbour's buffers
+  int rq[3] = {0, 0, 0}, nrem = 0;
+  int64_t roff[3] = {0, 0, 0};
+  if constexpr (kRemote) {
+    if (active)
+      for (int q = 0; q < rem.n; ++q) {
+        const bool in_i = rem.dx[q] < 0 ? i <= rem.h : rem.dx[q] > 0 ? i > rem.nx - rem.h : true;
+        const bool in_j = rem.dy[q] < 0 ? j <= rem.h : rem.dy[q] > 0 ? j > rem.ny - rem.h : true;
+        if (in_i && in_j && nrem < 3) {
+          rq[nrem] = q;
+          roff[nrem] = rem.g[q].at(i + rem.shift_i[q] - 1, j + rem.shift_j[q] - 1, 0);
+          ++nrem;
+        }
+      }
+  }
+  // store one output value of level k (0-based) of this column into the neighbours
+  auto remote = [&](double* const* base, int k, double v) {
+    if constexpr (kRemote) {
+#pragma unroll 1
+      for (int r = 0; r < nrem; ++r)
+        base[rq[r]][roff[r] + static_cast<int64_t>(k) * rem.g[rq[r]].plane] = v;
+    }
+  };
 
 #pragma unroll 1
   for (int k = 0; k < kWsStages - 1; ++k) issue(k < nz);
@@ -785,6 +810,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
         *out_a = unk;
         *out_v = vnk;
       }
+      remote(rem.u, k, unk);
+      remote(rem.v, k, vnk);
       ps_s[k * kThreads + t] = psk;
       // The Thomas recursion for face f = k-2 (its coefficients were formed in the
       // previous iteration) runs here, independent of this iteration's coefficient
@@ -858,6 +885,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
         phys_cm = phys_cm + rhok;
       }
       if (kIn || active) *out_a = thv;
+      remote(rem.th, k, thv);
       fz_prev = fzk;
     }
     th_prev = tk;
@@ -930,12 +958,15 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
           *wn = wkk;
           *pn = pk1;
         }
+        remote(rem.p, f + 1, pk1);
         pn -= P;
         psp -= kThreads;
         wk1 = wkk;
       }
     }
-    if (active) *pn = *psp - c.dt_cs2_rdz * wk1;
+    const double p0 = *psp - c.dt_cs2_rdz * wk1;
+    if (active) *pn = p0;
+    remote(rem.p, 0, p0);
   }
   sm100::tmem_fence_before();
   __syncthreads();
@@ -946,18 +977,22 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_dyn_step_ws(StepTmemArgs a) {
 
 cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                   int64_t nj, const DynConst& c, const Span& sp,
-                                  cudaStream_t s, const PhysArgs* phys, const DynIn* base) {
+                                  cudaStream_t s, const PhysArgs* phys, const DynIn* base,
+                                  const RemoteHalo* remote) {
   if (sp.ihi < sp.ilo || sp.jhi < sp.jlo) return cudaSuccess;
   if (!dycore_step_tmem_fits(nz)) return cudaErrorInvalidValue;
   if (phys && base) return cudaErrorInvalidValue;
+  if (remote && base) return cudaErrorInvalidValue;  // RK stages exchange by push
   const size_t smem = std::max<size_t>((static_cast<size_t>(kWsStages) * kFStageDoubles +
                                         static_cast<size_t>(nz) * kThreads) * sizeof(double),
                                        80 * 1024);
-  const int variant = phys ? 1 : base ? 2 : 0;
-  void (*kern)(StepTmemArgs) = variant == 1   ? k_dyn_step_ws<true, false>
-                               : variant == 2 ? k_dyn_step_ws<false, true>
-                                              : k_dyn_step_ws<false, false>;
-  static size_t configured[3] = {0, 0, 0};
+  const int variant = (phys ? 1 : base ? 2 : 0) + (remote ? 3 : 0);
+  void (*kern)(StepTmemArgs, RemoteHalo) = variant == 1   ? k_dyn_step_ws<true, false, false>
+                                           : variant == 2 ? k_dyn_step_ws<false, true, false>
+                                           : variant == 3 ? k_dyn_step_ws<false, false, true>
+                                           : variant == 4 ? k_dyn_step_ws<true, false, true>
+                                                          : k_dyn_step_ws<false, false, false>;
+  static size_t configured[5] = {0, 0, 0, 0, 0};
   if (smem > configured[variant]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -972,7 +1007,8 @@ cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, i
   dim3 block(kTX, 2 * kTY);
   dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
             static_cast<unsigned>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY));
-  kern<<<grid, block, smem, s>>>(a);
+  static const RemoteHalo none{};
+  kern<<<grid, block, smem, s>>>(a, remote ? *remote : none);
   return cudaGetLastError();
 }
 

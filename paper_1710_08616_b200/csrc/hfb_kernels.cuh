@@ -108,10 +108,25 @@ struct PhysArgs {
 // warp-specialised variant (acoustic warps + advection warps per tile); with `phys` the
 // column physics is fused into the advection warps (the full timestep in one kernel)
 // with `base` it is an RK stage: tendencies at `in`, applied to the base state
+// Peer transport, fused: the step's outputs of the cells within `h` of a tile edge are
+// also stored straight into the neighbours' next-step halo rings (their output buffers,
+// mapped by CUDA IPC) — the halo exchange of the next step rides on this step's epilogue
+struct RemoteHalo {
+  int n;                           // neighbour directions
+  int dx[8], dy[8];
+  int64_t shift_i[8], shift_j[8];  // neighbour (i, j) = local (i, j) + shift
+  Grid3 g[8];                      // the neighbour's layout
+  double* th[8];                   // the neighbour's output buffers (origins)
+  double* u[8];
+  double* v[8];
+  double* p[8];
+  int64_t nx, ny, h;               // this tile
+};
 cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                   int64_t nj, const DynConst& c, const Span& sp,
                                   cudaStream_t s, const PhysArgs* phys = nullptr,
-                                  const DynIn* base = nullptr);
+                                  const DynIn* base = nullptr,
+                                  const RemoteHalo* remote = nullptr);
 // the same step fed by TMA through mbarriers (hfb_dycore_tma.cu): measured slower than the
 // cp.async-fed launch_dycore_step_ws, kept as the HFB_TMA_STEP=1 variant
 cudaError_t launch_dycore_step_tma(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,

@@ -280,6 +280,10 @@ struct hfb_ctx {
   // peer-memory halo transport (hfb_peer_export / hfb_peer_attach): halos are stored
   // straight into the neighbours' buffers over NVLink, flags signal their arrival
   bool peer = false;
+  // the current buffers' halo rings were stored by the neighbours' previous step (fused
+  // remote epilogue): the next exchange only waits for their flags
+  bool peer_fused = false;
+  int64_t peer_pushes = 0, peer_handoffs = 0;  // exchanges by push kernel / by epilogue
   uint64_t* peer_sig = nullptr;
   uint64_t halo_epoch = 0, red_epoch = 0;
   std::vector<PeerRank> peers;
@@ -442,6 +446,7 @@ void do_device_allocate(hfb_ctx* c, Slot& s) {
 
 void do_copy_to_device(hfb_ctx* c, Slot& s) {
   check_bounds(c, s);
+  c->peer_fused = false;
   if (s.res == kDevice)
     fail(HFB_RESIDENCY, "copy-in of '%s' would overwrite newer device data", s.name.c_str());
   ensure_device(c, s, false);
@@ -575,6 +580,8 @@ void resolve_timings(hfb_ctx* c) {
 
 void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width,
                    cudaStream_t s = nullptr);
+RemoteHalo remote_halo(hfb_ctx* c, const std::vector<Slot*>& f4);
+void peer_signal(hfb_ctx* c, cudaStream_t st);
 
 // Decomposed stencil step with the halo exchange overlapped: the exchange of `fields` goes
 // to the communication stream; the columns at least `r` (the stencil radius) cells inside
@@ -588,7 +595,7 @@ void exchange_and_run(hfb_ctx* c, const std::vector<const char*>& fields, int r,
   const Span full = full_span(c, nx, ny);
   const bool multi = c->decomposed && c->decomp.px * c->decomp.py > 1;
   if (!multi) {
-    run(full);
+    run(full, false);
     return;
   }
   // odd_ilo: spans must start at odd i (the fused dycore kernel's 16-B copy chunks begin
@@ -603,7 +610,7 @@ void exchange_and_run(hfb_ctx* c, const std::vector<const char*>& fields, int r,
   if (!c->overlap || c->capturing || (odd_ilo && in.ilo % 2 == 0) || in.ihi < in.ilo ||
       in.jhi < in.jlo) {
     halo_exchange(c, fields, r);
-    run(full);
+    run(full, true);
     return;
   }
   if (!c->comm) {
@@ -615,7 +622,7 @@ void exchange_and_run(hfb_ctx* c, const std::vector<const char*>& fields, int r,
   cuda_check(cudaStreamWaitEvent(c->comm, c->ev_ready, 0), "cudaStreamWaitEvent");
   halo_exchange(c, fields, r, c->comm);
   cuda_check(cudaEventRecord(c->ev_halo, c->comm), "cudaEventRecord");
-  run(in);
+  run(in, false);
   cuda_check(cudaStreamWaitEvent(c->stream, c->ev_halo, 0), "cudaStreamWaitEvent");
   Span south = full, north = full, west = full, east = full;
   south.jhi = r;
@@ -624,7 +631,7 @@ void exchange_and_run(hfb_ctx* c, const std::vector<const char*>& fields, int r,
   west.jhi = east.jhi = ny - r;
   west.ihi = r;
   east.ilo = east_lo;
-  for (const Span& sp : {south, north, west, east}) run(sp);
+  for (const Span& sp : {south, north, west, east}) run(sp, true);
 }
 
 // ---------------------------------------------------------------------------
@@ -639,7 +646,7 @@ void diffusion_step(hfb_ctx* c, Stats& st, bool write_t_new) {
   Slot& tn = slot(c, "t_new");
   ensure_device(c, to, true);
   // hfk0 (stencil into the alternate t_old buffer [+ t_new]) then hfk1 fused away
-  exchange_and_run(c, {"t_old"}, 1, nx, ny, false, [&](const Span& sp) {
+  exchange_and_run(c, {"t_old"}, 1, nx, ny, false, [&](const Span& sp, bool) {
     launch(c, st, "hfk0_diffuse_step", [&] {
       if (c->force_generic)
         return launch_diffusion(to.d(), to.d_alt(), write_t_new ? tn.d() : nullptr,
@@ -909,7 +916,14 @@ void dycore_step(hfb_ctx* c, Stats& st, bool with_physics = false) {
   const bool fused_physics = fused && !c->force_single_role && with_physics;
   PhysArgs ph{};
   if (fused_physics) ph = phys_args(c, slot(c, "tsfc"), slot(c, "colm"));
-  exchange_and_run(c, {"th", "u", "v", "p"}, kHalo, nx, ny, true, [&](const Span& sp) {
+  // peer transport: the boundary strips store their outputs straight into the
+  // neighbours' halo rings (the next step's exchange rides on this step's epilogue)
+  const bool remote_ok = c->peer && fused && !c->force_single_role && !c->force_tma &&
+                         !c->force_ws2;
+  RemoteHalo rh{};
+  if (remote_ok) rh = remote_halo(c, {&th, &u, &v, &p});
+  exchange_and_run(c, {"th", "u", "v", "p"}, kHalo, nx, ny, true, [&](const Span& sp, bool edge) {
+    const RemoteHalo* rem = remote_ok && edge ? &rh : nullptr;
     if (fused) {
       if (c->force_single_role)
         launch(c, st, "dycore_step", [&] {
@@ -917,11 +931,15 @@ void dycore_step(hfb_ctx* c, Stats& st, bool with_physics = false) {
         });
       else if (fused_physics)
         launch(c, st, "full_step", [&] {
-          return launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream, &ph);
+          return rem ? launch_dycore_step_ws(in, out, grid_of(th), nz, th.lay.nj, k, sp,
+                                             c->stream, &ph, nullptr, rem)
+                     : launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream, &ph);
         });
       else
         launch(c, st, "dycore_step", [&] {
-          return launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
+          return rem ? launch_dycore_step_ws(in, out, grid_of(th), nz, th.lay.nj, k, sp,
+                                             c->stream, nullptr, nullptr, rem)
+                     : launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
         });
     } else {
       launch(c, st, "dycore_advect", [&] {
@@ -938,6 +956,10 @@ void dycore_step(hfb_ctx* c, Stats& st, bool with_physics = false) {
         });
     }
   });
+  if (c->peer && c->decomp.px * c->decomp.py > 1) {
+    if (remote_ok) peer_signal(c, c->stream);  // after the whole step: see peer_exchange
+    c->peer_fused = remote_ok;
+  }
   for (Slot* s : {&th, &u, &v, &w, &p}) s->cur = s->alt();
   // the generated code's 8 launches (dycore.h90 regions; region 1 spans i = 0..nx,
   // region 2 spans j = 0..ny)
@@ -995,7 +1017,7 @@ void rk3_step(hfb_ctx* c, Stats& st) {
                                 rval(c, "cs2"), rval(c, "grav"), rval(c, "th0"));
     const DynIn in = state(cur_of[g]);
     const DynOut out = outs(out_of[g]);
-    exchange_and_run(c, {"th", "u", "v", "p"}, kHalo, nx, ny, true, [&](const Span& sp) {
+    exchange_and_run(c, {"th", "u", "v", "p"}, kHalo, nx, ny, true, [&](const Span& sp, bool) {
       launch(c, st, "rk3_stage", [&] {
         return launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream, nullptr,
                            g == 0 ? nullptr : &base);
@@ -1153,11 +1175,90 @@ void group_pull(hfb_ctx* c, const std::vector<const char*>& fields, cudaStream_t
 // pushes exchange e only after its step e-1 (and so its reads of the halos exchange e-2
 // wrote into the same buffers) has completed, and it cannot start step e before every
 // neighbour's push e arrived.
+// the neighbour directions of this tile (dx, dy, rank)
+struct Nbr {
+  int dx, dy, rank;
+};
+std::vector<Nbr> peer_neighbours(const hfb_decomp& d) {
+  std::vector<Nbr> out;
+  for (int dy = -1; dy <= 1; ++dy)
+    for (int dx = -1; dx <= 1; ++dx) {
+      if (dx == 0 && dy == 0) continue;
+      const int rx = d.rx + dx, ry = d.ry + dy;
+      if (rx < 0 || rx >= d.px || ry < 0 || ry >= d.py) continue;
+      out.push_back({dx, dy, ry * d.px + rx});
+    }
+  return out;
+}
+
+void peer_wait(hfb_ctx* c, cudaStream_t st) {
+  std::vector<const uint64_t*> mine;
+  for (const Nbr& n : peer_neighbours(c->decomp))
+    mine.push_back(c->peer_sig + kSigHalo + (n.dy + 1) * 3 + (n.dx + 1));
+  cuda_check(launch_peer_wait(mine.data(), static_cast<int>(mine.size()), c->halo_epoch, st),
+             "peer wait");
+}
+
+// release the next epoch to every neighbour (I am at offset (-dx, -dy) from each)
+void peer_signal(hfb_ctx* c, cudaStream_t st) {
+  const uint64_t epoch = ++c->halo_epoch;
+  std::vector<uint64_t*> flags;
+  for (const Nbr& n : peer_neighbours(c->decomp))
+    flags.push_back(c->peers.at(n.rank).sig + kSigHalo + (1 - n.dy) * 3 + (1 - n.dx));
+  cuda_check(launch_peer_signal(flags.data(), static_cast<int>(flags.size()), epoch, st),
+             "peer signal");
+}
+
+// where this tile's edge cells land in each neighbour's OUTPUT buffers (the buffer the
+// current step writes: the neighbours flip their double buffers in lockstep)
+RemoteHalo remote_halo(hfb_ctx* c, const std::vector<Slot*>& f4) {
+  const hfb_decomp& d = c->decomp;
+  RemoteHalo rh{};
+  rh.nx = d.nx;
+  rh.ny = d.ny;
+  rh.h = d.halo;
+  const char* names[4] = {"th", "u", "v", "p"};
+  for (const Nbr& n : peer_neighbours(d)) {
+    PeerRank& pr = c->peers.at(n.rank);
+    const int q = rh.n++;
+    rh.dx[q] = n.dx;
+    rh.dy[q] = n.dy;
+    rh.shift_i[q] = n.dx < 0 ? pr.nx : n.dx > 0 ? -d.nx : 0;
+    rh.shift_j[q] = n.dy < 0 ? pr.ny : n.dy > 0 ? -d.ny : 0;
+    double** dst[4] = {rh.th, rh.u, rh.v, rh.p};
+    for (int fi = 0; fi < 4; ++fi) {
+      const int b = f4[fi]->alt();
+      auto it = pr.fields.find(names[fi]);
+      if (it == pr.fields.end() || b >= it->second.nbuf || !it->second.base[b])
+        fail(HFB_CONFIG, "peer transport: buffer %d of '%s' on rank %d is not mapped", b,
+             names[fi], n.rank);
+      const PeerField& rf = it->second;
+      if (fi == 0) rh.g[q] = Grid3{rf.pitch, rf.plane};
+      else if (rf.pitch != rh.g[q].pitch || rf.plane != rh.g[q].plane)
+        fail(HFB_CONFIG, "peer transport: rank %d's fields differ in layout", n.rank);
+      dst[fi][q] = rf.base[b] + rf.origin_off;
+    }
+  }
+  return rh;
+}
+
 void peer_exchange(hfb_ctx* c, const std::vector<const char*>& fields, cudaStream_t st) {
   const hfb_decomp& d = c->decomp;
   const int64_t H = d.halo;
   if (H == 0) return;
+  if (c->peer_fused) {  // the neighbours' previous step stored these halos already
+    peer_wait(c, st);
+    ++c->peer_handoffs;
+    for (const Nbr& n : peer_neighbours(d))
+      for (const char* f : fields) {
+        Slot& sl = slot(c, f);
+        c->halo_bytes += 2 * (n.dx == 0 ? d.nx : H) * (n.dy == 0 ? d.ny : H) * sl.lay.nk *
+                         sl.lay.nl * static_cast<int64_t>(sizeof(double));
+      }
+    return;
+  }
   const uint64_t epoch = ++c->halo_epoch;
+  ++c->peer_pushes;
   PeerPush push{};
   std::vector<uint64_t*> remote_flags;
   std::vector<const uint64_t*> my_flags;
@@ -1653,6 +1754,7 @@ hfb_status hfb_mark_host_modified(hfb_ctx* c, const char* module, const char* na
   return guarded([&] {
     Slot& s = slot_ref(c, lower(module), lower(name));
     if (s.has_device) s.res = kHost;
+    c->peer_fused = false;
   });
 }
 
@@ -1665,6 +1767,9 @@ static hfb_status run_impl(hfb_ctx* c, const char* entry, hfb_launch_stats* stat
     if (!allow_transfers && entry_has_transfers(c->app, r))
       fail(HFB_CONFIG, "entry '%s' performs host transfers; use hfb_run", entry);
     Stats st;
+    // only consecutive dycore steps keep the fused halo hand-off; any other entry may
+    // change the exchanged fields' buffers
+    if (r != "dycore_step" && r != "full_step") c->peer_fused = false;
     entry_fn(c->app)(c, r, st);
     if (sync) cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
     if (stats) {
@@ -2202,6 +2307,14 @@ hfb_status hfb_peer_export(hfb_ctx* c, void* buf, size_t cap, size_t* len) {
     std::memcpy(buf, &h, sizeof h);
     if (!fs.empty())
       std::memcpy(static_cast<char*>(buf) + sizeof h, fs.data(), fs.size() * sizeof(PeerBlobField));
+  });
+}
+
+hfb_status hfb_peer_stats(hfb_ctx* c, int64_t* pushes, int64_t* handoffs) {
+  return guarded([&] {
+    if (!c) fail(HFB_CONFIG, "null context");
+    if (pushes) *pushes = c->peer_pushes;
+    if (handoffs) *handoffs = c->peer_handoffs;
   });
 }
 

@@ -44,7 +44,7 @@ EXPORTS = [
     "hfb_load_state", "hfb_host_array", "hfb_array_checksum", "hfb_run_scenario",
     "hfb_set_reduction_order", "hfb_program_name", "hfb_program_module", "hfb_plugin_prepare",
     "hfb_plugin_written", "hfb_plugin_view", "hfb_plugin_scratch", "hfb_plugin_host",
-    "hfb_peer_export", "hfb_peer_attach",
+    "hfb_peer_export", "hfb_peer_attach", "hfb_peer_stats",
 ]
 
 # module of each built-in program (the apps' state modules)
@@ -145,6 +145,7 @@ def lib():
         L.hfb_run_scenario.argtypes = [P, S, c.POINTER(_Stats), c.c_char_p, c.c_size_t]
         L.hfb_peer_export.argtypes = [P, P, c.c_size_t, c.POINTER(c.c_size_t)]
         L.hfb_peer_attach.argtypes = [P, c.c_int, c.POINTER(P), c.POINTER(c.c_size_t)]
+        L.hfb_peer_stats.argtypes = [P, c.POINTER(i64), c.POINTER(i64)]
         _lib = L
     return _lib
 
@@ -374,6 +375,12 @@ class Engine:
         dist.all_gather_object(blobs, mine, group=group)
         self.peer_attach(blobs)
         dist.barrier(group)
+
+    def peer_stats(self):
+        """(halo updates by push kernel, halo updates handed off by the step epilogue)"""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().hfb_peer_stats(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
 
     def halo_bytes(self):
         return lib().hfb_halo_bytes(self._h)

@@ -41,7 +41,7 @@ def free_port():
         return s.getsockname()[1]
 
 
-def worker(rank, world, port, name, px, py, q):
+def worker(rank, world, port, name, px, py, q, per_step=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -62,9 +62,18 @@ def worker(rank, world, port, name, px, py, q):
             _, lower = decl(case.app, n, ints)
             eng.bind(n, tiles[n], lower=lower)
         eng.attach_peers()
-        stats = eng.run(APPS[case.app].entry)
+        if per_step:  # the bench's device-resident path: copy-in, n enqueued steps, copy-out
+            for n in tiles:
+                eng.copy_to_device(n)
+            for _ in range(case.ints["nsteps"]):
+                stats = eng.enqueue("dycore_step")
+            eng.synchronize()
+            for n in tiles:
+                eng.copy_from_device(n)
+        else:
+            stats = eng.run(APPS[case.app].entry)
         total = eng.get("total") if case.app == "reduction" else None
-        q.put((rank, {k: (int(d.i0), int(d.j0)) for k in tiles}, tiles, total,
+        q.put((rank, eng.peer_stats(), tiles, total,
                eng.halo_bytes(), stats.native_launches, None))
         dist.barrier()
         eng.close()
@@ -75,12 +84,12 @@ def worker(rank, world, port, name, px, py, q):
         dist.destroy_process_group()
 
 
-def run_peer(name, px, py):
+def run_peer(name, px, py, per_step=False):
     world = px * py
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=worker, args=(r, world, port, name, px, py, q))
+    procs = [ctx.Process(target=worker, args=(r, world, port, name, px, py, q, per_step))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -116,7 +125,12 @@ def test_peer_transport_equals_single_domain(name, px, py):
     names = APPS[case.app].outputs if case.app != "diffusion" else ("t_old", "t_new")
     for k in names:
         assert bits_equal(out[k], ref[k]), f"{name} {px}x{py}: {k} differs"
-    assert all(p[4] > 0 for p in parts)  # every rank pushed halo bytes
+    assert all(p[4] > 0 for p in parts)  # every rank moved halo bytes
+    n = case.ints["nsteps"]
+    # dycore: the first step after the copy-in pushes, the next ones are handed off by the
+    # previous step's epilogue; diffusion pushes every step
+    want = (1, n - 1) if case.app.startswith("dycore") else (n, 0)
+    assert all(p[1] == want for p in parts), [p[1] for p in parts]
 
 
 def test_peer_reduction_is_rank_ordered_and_identical_everywhere():
@@ -125,3 +139,20 @@ def test_peer_reduction_is_rank_ordered_and_identical_everywhere():
     assert len({np.float64(t).view(np.uint64) for t in totals}) == 1
     ref = run_oracle(case, {k: v.copy() for k, v in garr.items()})["total"]
     assert abs(totals[0] - ref) <= 1e-12 * abs(ref)
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+def test_peer_fused_halo_hand_off_per_step_entries(monkeypatch, overlap):
+    """Consecutive dycore_step entries hand the halos over in the step kernel's epilogue
+    (boundary strips store into the neighbours' next-step halo rings; the next exchange
+    only waits for their flags). Without overlap the single full-span launch carries the
+    remote epilogue. Both equal the undecomposed oracle bit for bit."""
+    if not overlap:
+        monkeypatch.setenv("HFB_NO_OVERLAP", "1")
+    case, garr, out, parts = run_peer("dycore", 2, 2, per_step=True)
+    ref = {k: v.copy() for k, v in garr.items()}
+    run_oracle(case, ref)
+    for k in ("th", "u", "v", "w", "p"):
+        assert bits_equal(out[k], ref[k]), k
+    # the first step after the copy-in pushes, the following ones are handed off
+    assert all(p[1] == (1, case.ints["nsteps"] - 1) for p in parts), [p[1] for p in parts]
