@@ -15,7 +15,8 @@ pytestmark = pytest.mark.gpu
 
 # which declared dims are (i, j) for each array of an app
 IJ_DIMS = {"diffusion": (1, 2), "dycore": (1, 2), "reduction": (1, 2), "bounded": (0, 1),
-           "damping": (1, 2), "surface_flux": None, "dycore_full": (1, 2)}
+           "damping": (1, 2), "surface_flux": None, "dycore_full": (1, 2),
+           "dycore_rk3": (1, 2)}
 
 
 def tile_slices(app, name, arr, d):

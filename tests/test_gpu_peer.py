@@ -27,12 +27,14 @@ PEER_CASES = {
     "dycore_full": Case("p_full", "dycore_full", dict(nx=70, ny=45, nz=20, nsteps=2),
                         dict(DYCORE_SCALARS, **PHYS_SCALARS),
                         dict(DYCORE_FILLS, **PHYS_FILLS)),
+    "dycore_rk3": Case("p_rk3", "dycore_rk3", dict(nx=70, ny=45, nz=20, nsteps=2),
+                       dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
     "diffusion": Case("p_diff", "diffusion", dict(nx=40, ny=36, nz=12, nsteps=3),
                       dict(coef=0.1), {"t_old": (1, 280.0, 10.0)}, unset=["t_new"]),
     "reduction": Case("p_red", "reduction", dict(nx=67, ny=45, nz=20), dict(total=0.0),
                       {"y": (6, 0.0, 1.0)}),
 }
-HALO = {"dycore": 2, "dycore_full": 2, "diffusion": 1, "reduction": 0}
+HALO = {"dycore": 2, "dycore_full": 2, "dycore_rk3": 2, "diffusion": 1, "reduction": 0}
 
 
 def free_port():
@@ -117,7 +119,8 @@ def run_peer(name, px, py, per_step=False):
 
 
 @pytest.mark.parametrize("name,px,py", [("dycore", 2, 1), ("dycore", 2, 2), ("dycore", 4, 2),
-                                        ("dycore_full", 2, 2), ("diffusion", 2, 2)])
+                                        ("dycore_full", 2, 2), ("dycore_rk3", 2, 2),
+                                        ("diffusion", 2, 2)])
 def test_peer_transport_equals_single_domain(name, px, py):
     case, garr, out, parts = run_peer(name, px, py)
     ref = {k: v.copy() for k, v in garr.items()}
@@ -129,7 +132,8 @@ def test_peer_transport_equals_single_domain(name, px, py):
     n = case.ints["nsteps"]
     # dycore: the first step after the copy-in pushes, the next ones are handed off by the
     # previous step's epilogue; diffusion pushes every step
-    want = (1, n - 1) if case.app.startswith("dycore") else (n, 0)
+    want = ((3 * n, 0) if case.app == "dycore_rk3"  # RK stages push (3 per step)
+            else (1, n - 1) if case.app.startswith("dycore") else (n, 0))
     assert all(p[1] == want for p in parts), [p[1] for p in parts]
 
 

@@ -1,11 +1,5 @@
-timeout 100 python tools/debug_tma.py 512 512 58 | tr '\n' ' '; echo
-timeout 100 python tools/debug_tma.py 70 45 58 | tr '\n' ' '; echo
-timeout 100 python tools/debug_tma.py 33 9 7 | tr '\n' ' '; echo
-for r in 1 2 3; do
-  for L in ab/libhfb_base.so ab/libhfb_k3.so; do
+for r in 1 2; do
+  for L in ab/libhfb_base.so ab/libhfb_cur.so; do
     echo -n "$L 512: "; HFB_LIB=$L timeout 120 python tools/time_step.py 512 512 58 2>&1 | tail -1
   done
-done
-for L in ab/libhfb_base.so ab/libhfb_k3.so; do
-  echo -n "$L C4: "; HFB_LIB=$L timeout 120 python tools/time_step.py 1581 1301 58 2>&1 | tail -1
 done
