@@ -45,6 +45,16 @@ BYTES_PER_POINT = {"dycore_step": 88, "full_step": 88, "dycore_advect": 40,
 L2_BYTES = 126 * 2**20
 
 
+def cpu_model():
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -223,6 +233,7 @@ def cpu_baseline_port(seconds_budget=20.0):
         if el > seconds_budget / 2 or steps >= 20:
             break
     return {"value": NX * NY * NZ * steps / el, "unit": UNIT, "cores": cores, "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"{steps} full dycore steps of {NX}x{NY}x{NZ} (oracle/hfb_oracle.c, "
                       f"KIJ order, OpenMP {cores} threads), {el:.2f} s"}
 
@@ -312,6 +323,7 @@ def bench_ours(args):
         traffic = json.loads(tp.read_text()).get(dom)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": traffic, "kernel": dom,
+                "frac_of_nominal_8TBps": round(achieved / 8000.0, 4),
                 "peak_source": src, "algorithmic_bytes_per_launch": alg_bytes,
                 "launches_per_step": dom_n // args.steps,
                 "kernel_ms_avg": round(per_step, 5),
@@ -372,6 +384,10 @@ def bench_ours(args):
                                 f"vs 126 MB L2"},
                "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
                "clocks": clocks.summary(), "halo_bytes": halo}
+        if n > 1:  # rank 0's halo traffic (sent + received) per step and its rate
+            hps = halo / (args.warmup + args.steps)
+            out["halo"] = {"bytes_per_step_rank0": int(hps),
+                           "GBps_rank0": round(hps / (ms / args.steps / 1e3) / 1e9, 2)}
         out["cpu_baseline"] = cpu_baseline_port() if n == 1 else None
         if n == 1 and not args.no_secondary:
             out["other_configs"] = secondary(local)

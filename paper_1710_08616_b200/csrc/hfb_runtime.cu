@@ -26,10 +26,23 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/hfb.h"
 #include "../../include/hfb_plugin.h"
 #include "hfb_kernels.cuh"
 #include "hfb_layout.cuh"
+
+namespace {
+// NVTX ranges (header-only NVTX3: free unless a tool such as ncu/nsys is attached): one
+// per native launch, entry, transfer and halo update (SURVEY §5 tracing)
+struct NvtxRange {
+  explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
 
 using namespace hfb;
 
@@ -445,6 +458,7 @@ void do_device_allocate(hfb_ctx* c, Slot& s) {
 }
 
 void do_copy_to_device(hfb_ctx* c, Slot& s) {
+  NvtxRange nr("hfrt_copy_to_device");
   check_bounds(c, s);
   c->peer_fused = false;
   if (s.res == kDevice)
@@ -461,6 +475,7 @@ void do_copy_to_device(hfb_ctx* c, Slot& s) {
 }
 
 void do_copy_from_device(hfb_ctx* c, Slot& s) {
+  NvtxRange nr("hfrt_copy_from_device");
   if (!s.has_device)
     fail(HFB_RESIDENCY, "copy-out of '%s', which was never transferred to the device",
          s.name.c_str());
@@ -549,6 +564,7 @@ cudaEvent_t take_event(hfb_ctx* c) {
 // on the context stream (never during graph capture).
 template <class F>
 void launch(hfb_ctx* c, Stats& st, const char* name, F&& f, int n = 1) {
+  NvtxRange nr(name);
   const bool timed = c->prof && !c->capturing;
   cudaEvent_t a = nullptr, b = nullptr;
   if (timed) {
@@ -1243,6 +1259,7 @@ RemoteHalo remote_halo(hfb_ctx* c, const std::vector<Slot*>& f4) {
 }
 
 void peer_exchange(hfb_ctx* c, const std::vector<const char*>& fields, cudaStream_t st) {
+  NvtxRange nr("halo:peer");
   const hfb_decomp& d = c->decomp;
   const int64_t H = d.halo;
   if (H == 0) return;
@@ -1323,6 +1340,7 @@ void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width
     return;
   }
   if (!c->nccl_comm) fail(HFB_CONFIG, "decomposed context without a communicator");
+  NvtxRange nr("halo:nccl");
   (void)width;  // the face boxes always carry the full halo ring (kHalo)
   NcclApi& api = nccl();
   const hfb_decomp& d = c->decomp;
@@ -1766,6 +1784,7 @@ static hfb_status run_impl(hfb_ctx* c, const char* entry, hfb_launch_stats* stat
     std::string r = routine_name(entry);
     if (!allow_transfers && entry_has_transfers(c->app, r))
       fail(HFB_CONFIG, "entry '%s' performs host transfers; use hfb_run", entry);
+    NvtxRange nr(r.c_str());
     Stats st;
     // only consecutive dycore steps keep the fused halo hand-off; any other entry may
     // change the exchanged fields' buffers
