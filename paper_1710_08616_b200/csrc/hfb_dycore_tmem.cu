@@ -318,6 +318,9 @@ struct StepTmemArgs {
   int64_t row_lo, row_hi;
   DynConst c;
   Span sp;
+  // tile order of the warp-specialised kernel (1-D grid): the rim first, then the tiles
+  // of the rectangle [tx_lo, tx_hi] x [ty_lo, ty_hi] that need no boundary cases
+  int ntx, nty, tx_lo, tx_hi, ty_lo, ty_hi;
 };
 
 __global__ void __launch_bounds__(kThreads, 2) k_dyn_step_tmem(StepTmemArgs a) {
@@ -601,8 +604,38 @@ __global__ void __launch_bounds__(kWsThreads, 2)
   const int row = acoustic ? warp : warp - kTY;       // tile row served by this warp
   const int tid = warp * kTX + lane;                  // 0..255 (copy issue)
   const int t = row * kTX + lane;                     // 0..127 (column within the tile)
-  const int64_t i0 = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * kTX;
-  const int64_t j0 = a.sp.jlo + static_cast<int64_t>(blockIdx.y) * kTY;
+  // CTA -> tile: the rim first, then the boundary-free tiles, so co-resident CTAs mostly
+  // run the same instantiation (the variants' code does not compete for the instruction
+  // cache) and the tail of the grid is made of the fast interior tiles
+  int tx, ty;
+  {
+    const int nix = a.tx_hi - a.tx_lo + 1, niy = a.ty_hi - a.ty_lo + 1;
+    const int nin = (nix > 0 && niy > 0) ? nix * niy : 0;
+    const int nrim = a.ntx * a.nty - nin;
+    const int b = static_cast<int>(blockIdx.x);
+    if (b >= nrim) {
+      tx = a.tx_lo + (b - nrim) % nix;
+      ty = a.ty_lo + (b - nrim) / nix;
+    } else {
+      const int e = b;
+      const int bottom = (nin ? a.ty_lo : a.nty) * a.ntx;
+      const int top = nin ? (a.nty - 1 - a.ty_hi) * a.ntx : 0;
+      if (e < bottom) {
+        tx = e % a.ntx;
+        ty = e / a.ntx;
+      } else if (e < bottom + top) {
+        tx = (e - bottom) % a.ntx;
+        ty = a.ty_hi + 1 + (e - bottom) / a.ntx;
+      } else {
+        const int left = a.tx_lo, side = a.ntx - nix, r3 = e - bottom - top;
+        ty = a.ty_lo + r3 / side;
+        const int r = r3 % side;
+        tx = r < left ? r : a.tx_hi + 1 + (r - left);
+      }
+    }
+  }
+  const int64_t i0 = a.sp.ilo + static_cast<int64_t>(tx) * kTX;
+  const int64_t j0 = a.sp.jlo + static_cast<int64_t>(ty) * kTY;
   const int64_t i = i0 + lane, j = j0 + row;
   const bool active = i <= a.sp.ihi && j <= a.sp.jhi;
   const int nz = a.nz;
@@ -1004,9 +1037,28 @@ cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, i
                  phys ? phys->tsfc : nullptr, phys ? phys->colm : nullptr,
                  phys ? phys->dt_rrelax : 0.0, phys ? phys->dt_ch : 0.0,
                  base ? *base : DynIn{}, nj, -kIOff, g.pitch - kIOff - 1, c, sp};
+  const int ntx = static_cast<int>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX);
+  const int nty = static_cast<int>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY);
+  // the boundary-free tile rectangle (the kernel's chk_x / chk_y criteria)
+  auto interior = [&](int n, int64_t lo, int64_t hi, int64_t off, int64_t gn, int w, int* a0,
+                      int* a1) {
+    *a0 = 0;
+    *a1 = -1;
+    for (int t = 0; t < n; ++t) {
+      const int64_t l0 = lo + static_cast<int64_t>(t) * w, g0 = l0 + off;
+      if (g0 >= 3 && g0 + w - 1 <= gn - 2 && l0 + w - 1 <= hi) {
+        if (*a1 < *a0) *a0 = t;
+        *a1 = t;
+      }
+    }
+  };
+  a.ntx = ntx;
+  a.nty = nty;
+  interior(ntx, sp.ilo, sp.ihi, sp.i0, sp.gnx, kTX, &a.tx_lo, &a.tx_hi);
+  interior(nty, sp.jlo, sp.jhi, sp.j0, sp.gny, kTY, &a.ty_lo, &a.ty_hi);
+  if (a.tx_hi < a.tx_lo || a.ty_hi < a.ty_lo) a.tx_lo = a.ty_lo = 0, a.tx_hi = a.ty_hi = -1;
   dim3 block(kTX, 2 * kTY);
-  dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
-            static_cast<unsigned>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY));
+  dim3 grid(static_cast<unsigned>(ntx * nty));
   static const RemoteHalo none{};
   kern<<<grid, block, smem, s>>>(a, remote ? *remote : none);
   return cudaGetLastError();
