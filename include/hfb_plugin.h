@@ -67,6 +67,16 @@ hfb_status hfb_plugin_view(hfb_ctx* ctx, const char* name, hfb_view* out);
  * generated host drivers); reads of a host copy older than the device copy fail, writes
  * make the host copy the newest (interp.cpp:406-409) */
 hfb_status hfb_plugin_host(hfb_ctx* ctx, const char* name, int write, hfb_view* out);
+/* the same without a call per element: the host view plus the array's residency word
+ * (0 host newer, 1 device newer, 2 both equal) and its has-a-device-copy flag; generated
+ * host code checks a read against residency 1 (then calls hfb_plugin_host for the
+ * error) and sets residency 0 on a write when a device copy exists — slot_side's rules */
+typedef struct {
+  hfb_view view;
+  int32_t* residency;
+  const int32_t* has_device;
+} hfb_host_ref;
+hfb_status hfb_plugin_host_ref(hfb_ctx* ctx, const char* name, hfb_host_ref* out);
 /* context-owned device scratch array `key` (a routine-local array, possibly extended by
  * the region domain; analysis.cpp:439-527), (re)allocated when its bounds change */
 hfb_status hfb_plugin_scratch(hfb_ctx* ctx, const char* key, int rank, const int64_t* lower,

@@ -194,7 +194,7 @@ const std::vector<AppDecl>& app_table() {
 // ---------------------------------------------------------------------------
 // State
 // ---------------------------------------------------------------------------
-enum Residency { kHost = 0, kDevice = 1, kBoth = 2 };  // interp.hpp:30
+enum Residency : int32_t { kHost = 0, kDevice = 1, kBoth = 2 };  // interp.hpp:30
 
 struct Scalar {
   SType type;
@@ -217,7 +217,7 @@ struct Slot {
   Layout lay;
   double* dev[3] = {nullptr, nullptr, nullptr};  // [2] only for RK3 stage states
   int cur = 0;
-  bool has_device = false;
+  int32_t has_device = 0;  // a device copy exists (bool; int32 for hfb_plugin_host_ref)
   Residency res = kHost;
   cudaStream_t stream = nullptr;  // owning context's stream
 
@@ -2975,6 +2975,23 @@ hfb_status hfb_plugin_host(hfb_ctx* c, const char* name, int write, hfb_view* ou
       out->stride[d] = d < s.rank ? s.hstride[d] : 0;
       out->lower[d] = d < s.rank ? s.lower[d] : 1;
     }
+  });
+}
+
+hfb_status hfb_plugin_host_ref(hfb_ctx* c, const char* name, hfb_host_ref* out) {
+  return guarded([&] {
+    if (is_scratch(name))
+      fail(HFB_CONFIG, "host access to the routine-local array '%s' is not supported", name);
+    Slot& s = slot(c, name);
+    check_bounds(c, s);
+    out->view.origin = s.host;
+    for (int d = 0; d < 4; ++d) {
+      out->view.stride[d] = d < s.rank ? s.hstride[d] : 0;
+      out->view.lower[d] = d < s.rank ? s.lower[d] : 1;
+    }
+    static_assert(sizeof(s.res) == sizeof(int32_t), "residency word");
+    out->residency = reinterpret_cast<int32_t*>(&s.res);
+    out->has_device = &s.has_device;
   });
 }
 

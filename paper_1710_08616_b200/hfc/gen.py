@@ -370,8 +370,9 @@ class Emitter:
                        else f"static_cast<int64_t>({self.expr(a, sc)})" for a in e.args]
                 if v[0] == "xarray":  # extended local: domain iterators prepended
                     idx = list(sc.get("@iters")[2]) + idx
-                if v[0] == "harray":  # host code: the bound host buffer
-                    return f"hfc_host(R, {v[2]}, {int(bool(sc.get('@write')))}).at({', '.join(idx)})"
+                if v[0] == "harray":  # host code: the bound host buffer (cached reference)
+                    fn = "hfc_wr" if sc.get("@write") else "hfc_rd"
+                    return f"{fn}(R, {sc.get('@href:' + e.name)[2]}, {v[2]}).at({', '.join(idx)})"
                 return f"{v[2]}.at({', '.join(idx)})"
             return self.intrinsic(e, sc)
         if isinstance(e, Un):
@@ -978,10 +979,14 @@ class Gen:
         for n, d in self.p.state.decls.items():
             if d.dims:
                 sc.set(n, "harray", "real", f"\"{n}\"")
+                sc.set("@href:" + n, "meta", "", f"h_{n}")
+                body.append(f"  HRef h_{n};")
         for n, d in r.decls.items():
             if n in r.args:
                 if d.dims:
                     sc.set(n, "harray", "real", f"a_{n}")
+                    sc.set("@href:" + n, "meta", "", f"ha_{n}")
+                    body.append(f"  HRef ha_{n};")
                 else:
                     sc.set(n, "scalar", d.type, f"a_{n}")
                 continue
@@ -1001,6 +1006,8 @@ class Gen:
                         f"const int roles[] = {{{rl}}};")
             body.append(f"    hfc_scratch(R, \"{key}\", {len(dims)}, lo, hi, roles); }}")
             sc.set(n, "harray", "real", f"\"{key}\"")
+            sc.set("@href:" + n, "meta", "", f"hl_{n}")
+            body.append(f"  HRef hl_{n};")
         transfers = []
         for dd in r.domdeps:
             if "transferhere" in dd.attrs.get("attribute", []):
@@ -1217,6 +1224,27 @@ HArr hfc_host(Run& R, const char* n, int write) {
   hfb_view v;
   HFC_CHECK(hfb_plugin_host(R.ctx, n, write, &v));
   return hfc_view(v);
+}
+// per host-routine invocation: one cached reference per array, fetched on first access
+struct HRef {
+  hfb_host_ref r;
+  bool ok = false;
+};
+inline HArr hfc_rd(Run& R, HRef& h, const char* n) {
+  if (!h.ok) {
+    HFC_CHECK(hfb_plugin_host_ref(R.ctx, n, &h.r));
+    h.ok = true;
+  }
+  if (*h.r.residency == 1) return hfc_host(R, n, 0);  // raises the stale-copy error
+  return hfc_view(h.r.view);
+}
+inline HArr hfc_wr(Run& R, HRef& h, const char* n) {
+  if (!h.ok) {
+    HFC_CHECK(hfb_plugin_host_ref(R.ctx, n, &h.r));
+    h.ok = true;
+  }
+  if (*h.r.has_device) *h.r.residency = 0;  // the host copy is now the newest
+  return hfc_view(h.r.view);
 }
 int hfc_copy_in(Run& R, const char* n) {
   if (!R.allow_transfers) return HFB_CONFIG;

@@ -43,7 +43,7 @@ EXPORTS = [
     "hfb_group_create", "hfb_group_destroy", "hfb_group_run", "hfb_save_state",
     "hfb_load_state", "hfb_host_array", "hfb_array_checksum", "hfb_run_scenario",
     "hfb_set_reduction_order", "hfb_program_name", "hfb_program_module", "hfb_plugin_prepare",
-    "hfb_plugin_written", "hfb_plugin_view", "hfb_plugin_scratch", "hfb_plugin_host",
+    "hfb_plugin_written", "hfb_plugin_view", "hfb_plugin_scratch", "hfb_plugin_host", "hfb_plugin_host_ref",
     "hfb_peer_export", "hfb_peer_attach", "hfb_peer_stats",
 ]
 

@@ -182,3 +182,27 @@ def test_generated_reduction_refuses_graph_capture():
         eng.run("grid_total")  # warm (allocates the partials)
         with pytest.raises(hfb.HfbError):
             eng.run_graph("grid_total", 1)
+
+
+def test_generated_host_update_marks_host_copy_newer():
+    """surface_flux's setup() updates cover_frac on the host (driver.h90:9-16); after a
+    copy-in that makes the device copy stale, so a kernel reading it is the reference's
+    residency error (interp.cpp:402-403); copying in again repairs it."""
+    so = hfc.GEN_DIR / "surface_flux_gen.so"
+    if not so.exists():
+        pytest.skip("surface_flux_gen.so not built")
+    case = [c for c in CORPUS if c.app == "surface_flux"][0]
+    arrs = make_inputs(case)
+    with hfb.Engine(str(so)) as eng:
+        for k, v in case.ints.items():
+            eng.set(k, int(v))
+        for name, a in arrs.items():
+            eng.bind(name, a)
+        for name in arrs:
+            eng.copy_to_device(name)
+        eng.run("setup")
+        with pytest.raises(hfb.HfbError) as ei:
+            eng.run("physics_run")
+        assert ei.value.kind == "residency" and "cover_frac" in str(ei.value)
+        eng.copy_to_device("cover_frac")
+        eng.run("physics_run")

@@ -69,7 +69,7 @@ def test_reference_corpus_translates(name):
     if name == "surface_flux_gen":
         # appliesTo(CPU) wrapper over GPU kernels: iterators pinned to the region start
         assert "l_i = INT64_C(1);" in code
-        assert "hfc_host(R, \"cover_frac\", 1)" in code  # setup's host update
+        assert "hfc_wr(R, h_cover_frac, \"cover_frac\")" in code  # setup's host update
 
 
 STATE = """module st
