@@ -35,6 +35,13 @@
 //   dump <module> <name>              (array or scalar)
 //   out <path>
 //   repeat <n>                        (run the entry n times; for timing only)
+//   app <program|plugin.so>           (mode b200: the engine program to run)
+//   array <module> <name> <lo> <hi> [<lo> <hi> ...]   (mode b200 without sources: the
+//                                     MachineState is built from the directives alone)
+//
+// Built with -DHFB_ADAPTER (oracle/_ref/hft_ref_b200), `mode b200` runs the entry on a
+// B200 through integration/hfb_adapter.hpp — the reference-side drop-in for
+// run_gpu_simulated — on the same MachineState the interpreter modes use.
 #include <algorithm>
 #include <array>
 #include <chrono>
@@ -55,6 +62,9 @@
 #include "hft/macro.hpp"
 #include "hft/parser.hpp"
 #include "hft/tokenize.hpp"
+#ifdef HFB_ADAPTER
+#include "hfb_adapter.hpp"
+#endif
 
 using namespace hft;
 
@@ -90,6 +100,12 @@ struct Scenario {
   std::vector<std::pair<std::string, std::string>> dumps;
   std::string out;
   int repeat = 1;
+  std::string app;
+  struct ArraySpec {
+    std::string module, name;
+    std::vector<long long> lo, hi;
+  };
+  std::vector<ArraySpec> arrays;
 };
 
 std::string read_text(const std::string& path) {
@@ -175,6 +191,17 @@ Scenario parse_scenario(const std::string& path) {
       ls >> sc.out;
     } else if (cmd == "repeat") {
       ls >> sc.repeat;
+    } else if (cmd == "app") {
+      ls >> sc.app;
+    } else if (cmd == "array") {
+      Scenario::ArraySpec a;
+      ls >> a.module >> a.name;
+      long long lo, hi;
+      while (ls >> lo >> hi) {
+        a.lo.push_back(lo);
+        a.hi.push_back(hi);
+      }
+      sc.arrays.push_back(a);
     } else {
       fail(ErrKind::Config, "unknown scenario directive '" + cmd + "'");
     }
@@ -252,6 +279,24 @@ void put_str(std::ofstream& o, const std::string& s) {
   o.write(s.data(), static_cast<std::streamsize>(s.size()));
 }
 
+// mode b200 without sources: the MachineState from the scenario's own declarations
+interp::MachineState state_from_directives(const Scenario& sc) {
+  interp::MachineState st;
+  for (const ScalarSet& s : sc.scalars) st.scalars[to_lower(s.module)][to_lower(s.name)] = {};
+  for (const Scenario::ArraySpec& d : sc.arrays) {
+    auto arr = std::make_shared<interp::ArrayValue>();
+    arr->type = ast::BaseType::Real;
+    arr->lower = d.lo;
+    arr->upper = d.hi;
+    arr->reals.assign(arr->size(), 0.0);
+    arr->init.assign(arr->size(), 0);
+    interp::ObjectSlot slot;
+    slot.host = std::move(arr);
+    st.arrays[to_lower(d.module)][to_lower(d.name)] = std::move(slot);
+  }
+  return st;
+}
+
 int run(const Scenario& sc) {
   std::vector<std::unique_ptr<ast::Unit>> units;
   for (const std::string& p : sc.sources)
@@ -291,7 +336,8 @@ int run(const Scenario& sc) {
     prog = std::make_unique<interp::Program>(std::move(units));
   }
 
-  interp::MachineState st = prog->prepare_state();
+  const bool own_state = sc.mode == "b200" && sc.sources.empty();
+  interp::MachineState st = own_state ? state_from_directives(sc) : prog->prepare_state();
   for (const ScalarSet& s : sc.scalars) {
     interp::ScalarValue* v = st.find_scalar(s.module, s.name);
     if (!v) fail(ErrKind::Config, "unknown scalar " + s.module + "." + s.name);
@@ -304,7 +350,7 @@ int run(const Scenario& sc) {
     }
     v->initialized = true;
   }
-  allocate_arrays(*prog, st);
+  if (!own_state) allocate_arrays(*prog, st);
   for (const FillSpec& f : sc.fills) {
     interp::ObjectSlot* slot = st.find_slot(f.module, f.name);
     if (!slot) fail(ErrKind::Config, "unknown array " + f.module + "." + f.name);
@@ -326,7 +372,13 @@ int run(const Scenario& sc) {
   interp::LaunchStats stats;
   auto t0 = std::chrono::steady_clock::now();
   for (int r = 0; r < sc.repeat; ++r) {
-    if (sc.mode == "gpu")
+    if (sc.mode == "b200") {
+#ifdef HFB_ADAPTER
+      stats = hfb_adapter::run_gpu(sc.app, st, sc.entry);
+#else
+      fail(ErrKind::Config, "mode b200 needs the hft_ref_b200 build (-DHFB_ADAPTER)");
+#endif
+    } else if (sc.mode == "gpu")
       stats = interp::run_gpu_simulated(*prog, st, sc.entry, opts);
     else if (sc.mode == "cpu")
       stats = interp::run_cpu_generated(*prog, st, sc.entry, opts);

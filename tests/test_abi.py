@@ -66,3 +66,21 @@ def test_decomposition_host_logic():
     assert s_east[2:] == r_west[2:]
     with pytest.raises(hfb.HfbError):
         hfb.decomp_init(3, 3, 58, 4, 1, 0)
+
+
+def test_reference_adapter_builds_and_maps_errors(tmp_path):
+    """integration/hfb_adapter.hpp compiles against the reference's headers (the `b200`
+    oracle target); without a GPU its run_gpu surfaces the engine's HFB_CUDA status as the
+    reference's own hft::Error[runtime] (exit code 10 + ErrKind::Runtime)."""
+    import subprocess
+    exe = ROOT / "oracle" / "_ref" / "hft_ref_b200"
+    if not exe.exists():
+        pytest.skip("hft_ref_b200 not built (needs /root/reference at build time)")
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present: tests/test_gpu_adapter.py covers the adapter")
+    sc = tmp_path / "s.sc"
+    sc.write_text("mode b200\napp dycore\nentry main\nint dyn_state nx 4\n")
+    r = subprocess.run([str(exe), str(sc)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 15, (r.returncode, r.stderr)
+    assert "hft::Error[runtime] no CUDA device" in r.stderr
