@@ -221,8 +221,9 @@ hfb_status hfb_peer_stats(hfb_ctx* ctx, int64_t* pushes, int64_t* handoffs);
  * (SPEC.md:473). 1: ordered — the reference's acc-simulated order (interp.cpp:1080-1173):
  * one partial per (i,j) iteration summing k = 1..nz from the identity, combined in
  * linear-id order (i fastest) starting from the initial value, i.e. bit-identical to
- * run_gpu_simulated on the OpenACC backend. Ordered runs single-domain or in an
- * in-process group (the tiles' partials are assembled in global order). */
+ * run_gpu_simulated on the OpenACC backend. Ordered runs single-domain, in an
+ * in-process group, or one process per rank over the peer transport (the tiles' column
+ * partials are assembled in global order on every rank). */
 hfb_status hfb_set_reduction_order(hfb_ctx* ctx, int ordered);
 
 /* --- state images and scenario files ------------------ */

@@ -244,6 +244,7 @@ struct PeerField {
 struct PeerRank {
   int64_t nx = 0, ny = 0;
   uint64_t* sig = nullptr;
+  double* gather = nullptr;  // 2 x global_nx x global_ny: ordered-reduction partials
   std::map<std::string, PeerField> fields;
 };
 // signal block layout (uint64 words): [0, 9) halo flags by the sender's offset from the
@@ -298,6 +299,7 @@ struct hfb_ctx {
   bool peer_fused = false;
   int64_t peer_pushes = 0, peer_handoffs = 0;  // exchanges by push kernel / by epilogue
   uint64_t* peer_sig = nullptr;
+  double* peer_gather = nullptr;  // this rank's gather buffer (ordered reductions)
   uint64_t halo_epoch = 0, red_epoch = 0;
   std::vector<PeerRank> peers;
   std::vector<void*> ipc_opened;
@@ -803,6 +805,7 @@ void sf_entry(hfb_ctx* c, const std::string& r, Stats& st) {
 // app: reduction (reduction.h90) — OpenACC-style reduction kernel
 // ---------------------------------------------------------------------------
 void allreduce_sum(hfb_ctx* c, double* dev_value);
+const double* peer_gather(hfb_ctx* c, int64_t nx, int64_t ny);
 
 void reduction_kernel(hfb_ctx* c, Stats& st) {
   int64_t nx = ival(c, "nx"), ny = ival(c, "ny"), nz = ival(c, "nz");
@@ -821,8 +824,9 @@ void reduction_kernel(hfb_ctx* c, Stats& st) {
   if (c->reduce_ordered) {
     // the acc-simulated order (interp.cpp:1080-1173): column partials, then one in-order
     // pass from the initial value; a group assembles the tiles' partials in global order
-    if (multi && !local_group)
-      fail(HFB_CONFIG, "ordered reductions run single-domain or in an in-process group");
+    if (multi && !local_group && !c->peer)
+      fail(HFB_CONFIG, "ordered reductions run single-domain, in an in-process group or over "
+                       "the peer transport");
     const size_t need = static_cast<size_t>(nx) * static_cast<size_t>(ny);
     if (c->red_cols_cap < need) {
       if (c->red_cols) cudaFree(c->red_cols);
@@ -838,15 +842,18 @@ void reduction_kernel(hfb_ctx* c, Stats& st) {
       st.threads += nx * ny;
       return;
     }
+    // over the peer transport every rank gathers all tiles' partials in global order
+    const double* cols = multi ? peer_gather(c, nx, ny) : c->red_cols;
+    const int64_t count = multi ? c->decomp.global_nx * c->decomp.global_ny
+                                : static_cast<int64_t>(need);
     launch(c, st, "grid_total_ordered", [&] {
-      return launch_ordered_total(c->red_cols, static_cast<int64_t>(need), total, c->red_result,
-                                  c->stream);
+      return launch_ordered_total(cols, count, total, c->red_result, c->stream);
     });
   } else {
     launch(c, st, "grid_total", [&] { return launch_grid_sum(y.d(), grid_of(y), nz, sp, c->red_partials, c->red_result,
                              multi ? 0.0 : total, c->stream); }, 2);
   }
-  if (multi && !local_group) allreduce_sum(c, c->red_result);
+  if (multi && !local_group && !c->reduce_ordered) allreduce_sum(c, c->red_result);
   cuda_check(cudaMemcpyAsync(c->red_host, c->red_result, sizeof(double), cudaMemcpyDeviceToHost,
                              c->stream),
              "cudaMemcpyAsync(total)");
@@ -855,7 +862,7 @@ void reduction_kernel(hfb_ctx* c, Stats& st) {
   if (local_group) {
     c->red_local = *c->red_host;  // combined in rank order by hfb_group_run
   } else {
-    tot.r = multi ? total + *c->red_host : *c->red_host;
+    tot.r = multi && !c->reduce_ordered ? total + *c->red_host : *c->red_host;
     tot.init = true;
   }
   // acc kernels: one virtual launch over the (j, i) iteration space (interp.cpp:1080-1114)
@@ -1460,6 +1467,44 @@ void group_pull(hfb_ctx* c, const std::vector<const char*>& fields, cudaStream_t
   }
 }
 
+// ordered reductions over the peer transport: this tile's column partials are stored into
+// every rank's gather buffer at their global (j, i) positions (parity of the reduction
+// epoch), flags released; once every rank's flag arrived the buffer holds the whole
+// plane in the acc-simulated combine order (linear id, i fastest)
+const double* peer_gather(hfb_ctx* c, int64_t nx, int64_t ny) {
+  const hfb_decomp& d = c->decomp;
+  const int n = d.px * d.py;
+  const int64_t G = d.global_nx * d.global_ny;
+  const uint64_t epoch = ++c->red_epoch;
+  const int64_t par = static_cast<int64_t>(epoch & 1) * G;
+  if (n > 16) fail(HFB_CONFIG, "peer ordered reductions support up to 16 ranks");
+  PeerPush push{};
+  std::vector<uint64_t*> flags;
+  std::vector<const uint64_t*> mine;
+  for (int q = 0; q < n; ++q) {
+    double* base = q == d.rank ? c->peer_gather : c->peers.at(q).gather;
+    uint64_t* sig = q == d.rank ? c->peer_sig : c->peers.at(q).sig;
+    PeerBox& b = push.box[push.n++];
+    b.src = c->red_cols;
+    b.dst = base + par;
+    b.gs = Grid3{nx, 0};
+    b.gd = Grid3{d.global_nx, 0};
+    b.si0 = 1;
+    b.sj0 = 1;
+    b.di0 = d.i0 + 1;
+    b.dj0 = d.j0 + 1;
+    b.nbi = nx;
+    b.nbj = ny;
+    b.nk = 1;
+    flags.push_back(sig + kSigRed + d.rank);
+    mine.push_back(c->peer_sig + kSigRed + q);
+  }
+  cuda_check(launch_peer_push(push, c->stream), "peer gather push");
+  cuda_check(launch_peer_signal(flags.data(), n, epoch, c->stream), "peer signal");
+  cuda_check(launch_peer_wait(mine.data(), n, epoch, c->stream), "peer wait");
+  return c->peer_gather + par;
+}
+
 void allreduce_sum(hfb_ctx* c, double* dev_value) {
   if (c->peer) {  // deterministic: every rank sums the partials in rank order
     const hfb_decomp& d = c->decomp;
@@ -1584,6 +1629,7 @@ void hfb_destroy(hfb_ctx* c) {
   if (c->halo_recv) cudaFree(c->halo_recv);
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (c->peer_sig) cudaFree(c->peer_sig);
+  if (c->peer_gather) cudaFree(c->peer_gather);
   if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
   if (c->nccl_comm) nccl().CommDestroy(c->nccl_comm);
   for (auto& t : c->pending) {
@@ -2266,6 +2312,7 @@ struct PeerBlobHead {
   int32_t rank, nranks, device, nfields;
   int64_t nx, ny;
   cudaIpcMemHandle_t sig;
+  cudaIpcMemHandle_t gather;
 };
 struct PeerBlobField {
   char name[48];
@@ -2288,6 +2335,11 @@ hfb_status hfb_peer_export(hfb_ctx* c, void* buf, size_t cap, size_t* len) {
     if (!c->peer_sig) {
       cuda_check(cudaMalloc(&c->peer_sig, kSigWords * sizeof(uint64_t)), "cudaMalloc(signals)");
       cuda_check(cudaMemset(c->peer_sig, 0, kSigWords * sizeof(uint64_t)), "cudaMemset");
+      // ordered reductions: every rank's column partials in global (j, i) order, two
+      // parities (a 2-D plane per rank: small next to the 3-D fields)
+      const size_t g = 2 * static_cast<size_t>(c->decomp.global_nx * c->decomp.global_ny);
+      cuda_check(cudaMalloc(&c->peer_gather, g * sizeof(double)), "cudaMalloc(gather)");
+      cuda_check(cudaMemset(c->peer_gather, 0, g * sizeof(double)), "cudaMemset");
     }
     // every bound array gets its device buffers now (double-buffered fields: all three
     // stage buffers), so the neighbours can map them before the first step
@@ -2319,6 +2371,7 @@ hfb_status hfb_peer_export(hfb_ctx* c, void* buf, size_t cap, size_t* len) {
     h.nx = c->decomp.nx;
     h.ny = c->decomp.ny;
     cuda_check(cudaIpcGetMemHandle(&h.sig, c->peer_sig), "cudaIpcGetMemHandle(signals)");
+    cuda_check(cudaIpcGetMemHandle(&h.gather, c->peer_gather), "cudaIpcGetMemHandle(gather)");
     const size_t need = sizeof h + fs.size() * sizeof(PeerBlobField);
     *len = need;
     if (!buf) return;
@@ -2367,6 +2420,7 @@ hfb_status hfb_peer_attach(hfb_ctx* c, int n, const void* const* blobs, const si
       pr.nx = h.nx;
       pr.ny = h.ny;
       pr.sig = static_cast<uint64_t*>(open(h.sig));
+      pr.gather = static_cast<double*>(open(h.gather));
       const int rx = h.rank % d.px, ry = h.rank / d.px;
       if (std::abs(rx - d.rx) > 1 || std::abs(ry - d.ry) > 1) continue;  // not a neighbour
       const char* fp = static_cast<const char*>(blobs[q]) + sizeof h;

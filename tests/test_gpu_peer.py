@@ -43,7 +43,7 @@ def free_port():
         return s.getsockname()[1]
 
 
-def worker(rank, world, port, name, px, py, q, per_step=False):
+def worker(rank, world, port, name, px, py, q, per_step=False, ordered=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -53,6 +53,8 @@ def worker(rank, world, port, name, px, py, q, per_step=False):
         d = hfb.decomp_init(gnx, gny, case.ints.get("nz", 1), px, py, rank, halo=HALO[name])
         eng = hfb.Engine(APPS[case.app].prog, device=0)
         eng.set_decomposition(d)
+        if ordered:
+            eng.set_reduction_order(True)
         ints = tile_ints(case, d)
         for k, v in ints.items():
             eng.set(k, int(v))
@@ -86,12 +88,12 @@ def worker(rank, world, port, name, px, py, q, per_step=False):
         dist.destroy_process_group()
 
 
-def run_peer(name, px, py, per_step=False):
+def run_peer(name, px, py, per_step=False, ordered=False):
     world = px * py
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=worker, args=(r, world, port, name, px, py, q, per_step))
+    procs = [ctx.Process(target=worker, args=(r, world, port, name, px, py, q, per_step, ordered))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -160,3 +162,14 @@ def test_peer_fused_halo_hand_off_per_step_entries(monkeypatch, overlap):
         assert bits_equal(out[k], ref[k]), k
     # the first step after the copy-in pushes, the following ones are handed off
     assert all(p[1] == (1, case.ints["nsteps"] - 1) for p in parts), [p[1] for p in parts]
+
+
+@pytest.mark.parametrize("px,py", [(2, 2), (3, 1)])
+def test_peer_ordered_reduction_bit_exact(px, py):
+    """Ordered reductions across processes: every rank gathers all tiles' column partials
+    into global (j, i) order through peer memory and combines them in the acc-simulated
+    order — the total is bit-identical to run_gpu_simulated's on every rank."""
+    case, garr, _, parts = run_peer("reduction", px, py, ordered=True)
+    accsim = run_oracle(case, {k: v.copy() for k, v in garr.items()})["total_accsim"]
+    for p in parts:
+        assert np.float64(p[3]).view(np.uint64) == np.float64(accsim).view(np.uint64)
