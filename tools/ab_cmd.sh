@@ -1,5 +1,9 @@
+timeout 100 python tools/debug_tma.py 512 512 58 | tr '\n' ' '; echo
+HFB_LIB=ab/libhfb_persist.so timeout 100 python tools/debug_tma.py 512 512 58 | tr '\n' ' '; echo
+HFB_LIB=ab/libhfb_persist.so timeout 100 python tools/debug_tma.py 70 45 58 | tr '\n' ' '; echo
 for r in 1 2; do
-for v in "HFB_DEBUG_SKIP=0" "HFB_DEBUG_SKIP=16" "HFB_DEBUG_SKIP=3" "HFB_DEBUG_SKIP=19"; do
-  echo -n "[$v] "; env $v timeout 120 python tools/time_step.py 512 512 58 2>&1 | tail -1
-done
+  for L in ab/libhfb_cur.so ab/libhfb_persist.so; do
+    echo -n "$L 512: "; HFB_LIB=$L timeout 120 python tools/time_step.py 512 512 58 2>&1 | tail -1
+    echo -n "$L C4: "; HFB_LIB=$L timeout 120 python tools/time_step.py 1581 1301 58 2>&1 | tail -1
+  done
 done
