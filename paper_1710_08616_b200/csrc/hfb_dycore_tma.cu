@@ -481,12 +481,9 @@ cudaError_t launch_dycore_step_tma(const DynIn& in, const DynOut& out, Grid3 g, 
   void (*kern)(const TmaMaps, const TmaStepArgs) = variant == 1   ? k_dyn_step_tma<true, false>
                                                    : variant == 2 ? k_dyn_step_tma<false, true>
                                                                   : k_dyn_step_tma<false, false>;
-  static size_t configured[3] = {0, 0, 0};
-  if (smem > configured[variant]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+  {
+    cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
-    configured[variant] = smem;
   }
   static const int debug_skip = getenv("HFB_DEBUG_SKIP") ? atoi(getenv("HFB_DEBUG_SKIP")) : 0;
   TmaStepArgs a{out, g, static_cast<int>(nz), debug_skip,

@@ -243,13 +243,9 @@ cudaError_t launch_dycore_acoustic_tmem(const DynIn& in, const DynOut& out, Grid
   const size_t smem = std::max<size_t>((static_cast<size_t>(kStages) * kStageDoubles +
                                         static_cast<size_t>(nz) * kThreads) * sizeof(double),
                                        80 * 1024);
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_dyn_acoustic_tmem,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+  {
+    cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(k_dyn_acoustic_tmem), smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   AcoTmemArgs a{in, out, g, static_cast<int>(nz), nj, -kIOff, g.pitch - kIOff - 1, c, sp};
   dim3 block(kTX, kTY);
@@ -528,13 +524,9 @@ cudaError_t launch_dycore_step_tmem(const DynIn& in, const DynOut& out, Grid3 g,
   const size_t smem = std::max<size_t>((static_cast<size_t>(kFStages) * kFStageDoubles +
                                         static_cast<size_t>(nz) * kThreads) * sizeof(double),
                                        80 * 1024);
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_dyn_step_tmem,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+  {
+    cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(k_dyn_step_tmem), smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   StepTmemArgs a{in,  out,     g,      static_cast<int>(nz), 0, nullptr, nullptr, 0.0, 0.0,
                  DynIn{}, nj, -kIOff, g.pitch - kIOff - 1, c, sp};
@@ -1025,12 +1017,9 @@ cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, i
                                            : variant == 3 ? k_dyn_step_ws<false, false, true>
                                            : variant == 4 ? k_dyn_step_ws<true, false, true>
                                                           : k_dyn_step_ws<false, false, false>;
-  static size_t configured[5] = {0, 0, 0, 0, 0};
-  if (smem > configured[variant]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+  {
+    cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
-    configured[variant] = smem;
   }
   static const int debug_skip = getenv("HFB_DEBUG_SKIP") ? atoi(getenv("HFB_DEBUG_SKIP")) : 0;
   StepTmemArgs a{in, out, g, static_cast<int>(nz), debug_skip,

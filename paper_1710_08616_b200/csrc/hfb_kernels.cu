@@ -12,6 +12,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <cstdlib>
 
 #include "hfb_kernels.cuh"
@@ -783,13 +786,9 @@ cudaError_t launch_dycore_acoustic(const DynIn& in, const DynOut& out, Grid3 g, 
   if (best_warps == 0) return cudaErrorInvalidConfiguration;
   dim3 block(32, best_by);
   size_t smem = static_cast<size_t>(nz) * block.x * block.y * sizeof(double);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_dyn_acoustic,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+  if (smem > 48 * 1024) {
+    cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(k_dyn_acoustic), smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   AcoArgs a{in, out, g, static_cast<int>(nz), c, sp};
   k_dyn_acoustic<<<span_grid(sp, block), block, smem, s>>>(a);
@@ -880,6 +879,21 @@ cudaError_t launch_pack_box(const double* field, double* buf, Grid3 g, int64_t n
     k_unpack_box<<<blocks, 256, 0, s>>>(const_cast<double*>(field), buf, g, box[0], box[2], nbi,
                                         nbj, total);
   return cudaGetLastError();
+}
+
+cudaError_t ensure_dynamic_smem(const void* kernel, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{dev, kernel}];
+  if (smem <= have) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+  if (e == cudaSuccess) have = smem;
+  return e;
 }
 
 // ---------------------------------------------------------------------------

@@ -147,6 +147,11 @@ cudaError_t launch_column_physics(const double* rho, double* th, const double* u
 cudaError_t launch_pack_box(const double* field, double* buf, Grid3 g, int64_t nk,
                             const int64_t box[4], bool pack, cudaStream_t s);
 
+// ---- launch attributes ----------------------------------------------------------------
+// Opt a kernel into `smem` bytes of dynamic shared memory on the CURRENT device (the
+// attribute is per device context): remembered per (device, kernel), thread-safe.
+cudaError_t ensure_dynamic_smem(const void* kernel, size_t smem);
+
 // ---- peer-memory halo transport (NVLink / NVSwitch P2P stores) -----------------------
 // one box: interior cells of a local field stored straight into a neighbour's halo ring
 // (the neighbour's buffer is mapped into this process by CUDA IPC); (i, j) are 1-based

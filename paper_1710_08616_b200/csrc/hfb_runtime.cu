@@ -2393,6 +2393,7 @@ hfb_status hfb_peer_stats(hfb_ctx* c, int64_t* pushes, int64_t* handoffs) {
 hfb_status hfb_peer_attach(hfb_ctx* c, int n, const void* const* blobs, const size_t* lens) {
   return guarded([&] {
     if (!c || !c->peer_sig) fail(HFB_CONFIG, "hfb_peer_export first");
+    if (c->peer) fail(HFB_CONFIG, "peers are already attached to this context");
     const hfb_decomp& d = c->decomp;
     if (n != d.px * d.py) fail(HFB_CONFIG, "%d blobs for %d ranks", n, d.px * d.py);
     cudaSetDevice(c->device);
