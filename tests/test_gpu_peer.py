@@ -31,10 +31,17 @@ PEER_CASES = {
                        dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
     "diffusion": Case("p_diff", "diffusion", dict(nx=40, ny=36, nz=12, nsteps=3),
                       dict(coef=0.1), {"t_old": (1, 280.0, 10.0)}, unset=["t_new"]),
+    "bounded": Case("p_bnd", "bounded", dict(nx=37, ny=21), {},
+                    {"a": (4, 0.0, 1.0), "b": (6, -1.0, 0.5)}),
+    "damping": Case("p_damp", "damping",
+                    dict(nx_mn=-1, nx_mx=35, ny_mn=0, ny_mx=20, nz_mn=1, nz_mx=9),
+                    dict(tratio_bnd=0.3, mtratio_bnd=0.7),
+                    {"dens_ref_f": (2, 1.0, 1.0), "dens_ptb_bnd": (3, -0.005, 0.01)}),
     "reduction": Case("p_red", "reduction", dict(nx=67, ny=45, nz=20), dict(total=0.0),
                       {"y": (6, 0.0, 1.0)}),
 }
-HALO = {"dycore": 2, "dycore_full": 2, "dycore_rk3": 2, "diffusion": 1, "reduction": 0}
+HALO = {"dycore": 2, "dycore_full": 2, "dycore_rk3": 2, "diffusion": 1, "reduction": 0,
+        "bounded": 1, "damping": 0}
 
 
 def free_port():
@@ -122,16 +129,21 @@ def run_peer(name, px, py, per_step=False, ordered=False):
 
 @pytest.mark.parametrize("name,px,py", [("dycore", 2, 1), ("dycore", 2, 2), ("dycore", 4, 2),
                                         ("dycore_full", 2, 2), ("dycore_rk3", 2, 2),
-                                        ("diffusion", 2, 2)])
+                                        ("diffusion", 2, 2), ("dycore", 3, 2),
+                                        ("bounded", 2, 3), ("damping", 2, 2)])
 def test_peer_transport_equals_single_domain(name, px, py):
     case, garr, out, parts = run_peer(name, px, py)
     ref = {k: v.copy() for k, v in garr.items()}
     run_oracle(case, ref)
-    names = APPS[case.app].outputs if case.app != "diffusion" else ("t_old", "t_new")
+    names = {"diffusion": ("t_old", "t_new"), "damping": ("dens_ptb_damp",)}.get(
+        case.app, APPS[case.app].outputs)
     for k in names:
         assert bits_equal(out[k], ref[k]), f"{name} {px}x{py}: {k} differs"
+    if HALO[name] == 0:  # pointwise: no exchange at all
+        assert all(p[1] == (0, 0) and p[4] == 0 for p in parts)
+        return
     assert all(p[4] > 0 for p in parts)  # every rank moved halo bytes
-    n = case.ints["nsteps"]
+    n = case.ints.get("nsteps", 1)
     # dycore: the first step after the copy-in pushes, the next ones are handed off by the
     # previous step's epilogue; diffusion pushes every step
     want = ((3 * n, 0) if case.app == "dycore_rk3"  # RK stages push (3 per step)
