@@ -165,6 +165,8 @@ def secondary(local, steps=10, warmup=3):
              512, 512),
             ("C3 full timestep + column physics 1024x1024x58", "dycore", "full_step", 1024, 1024),
             ("C4 dycore step 1581x1301x58 (1 GPU)", "dycore", "dycore_step", 1581, 1301),
+            ("north star: full timestep (dycore + HE-VI + column physics) 1581x1301x58 "
+             "(1 GPU)", "dycore", "full_step", 1581, 1301),
             ("reference kernel: diffusion step 1581x1301x58", "diffusion", "diffuse_step",
              1581, 1301)]
     for label, prog, entry, nx, ny in runs:
@@ -207,6 +209,7 @@ def secondary(local, steps=10, warmup=3):
                       "unit": UNIT, "alg_bytes_per_point": bpp,
                       "achieved_GBps": round(bpp * pts / (ms / 1e3) / 1e9, 1),
                       "frac_of_measured_hbm": round(bpp * pts / (ms / 1e3) / 1e9 / hbm, 4),
+                      "frac_of_nominal_8TBps": round(bpp * pts / (ms / 1e3) / 1e9 / 8000.0, 4),
                       "steps": steps}
         eng.close()
         del arrs
