@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(kWsThreads, 2)
   double th_prev = 0.0, w_prev = 0.0;              // both roles
   double rho_prev = 0.0, ps_prev = 0.0, cp_prev = 0.0, dp_prev = 0.0;  // acoustic
   double fz_prev = 0.0;                            // advection
-  double phys_cs = 0.0, phys_cm = 0.0, colm_ij = 0.0, tsfc_ij = 0.0;  // column physics
+  double phys_cs = 0.0, phys_cm = 0.0, colm_ij = 0.0;  // column physics
   // RK stage: base-state values of this column (one level prefetched in registers)
   struct BaseLevel {
     double th, u, uw, v, vs, p, w;
@@ -766,7 +766,6 @@ __global__ void __launch_bounds__(kWsThreads, 2)
   double wb_prev = 0.0;  // base w of the previous level (RK: the HE-VI right-hand side)
   if (kPhys && !acoustic && active) {
     colm_ij = a.colm[(j - 1) * W + (i - 1)];
-    tsfc_ij = a.tsfc[(j - 1) * W + (i - 1)];
   }
   double pend_beta = 0.0, pend_bb = 1.0, pend_dd = 0.0;  // face awaiting its recursion step
   int s0 = 0;  // ring slot of level k
@@ -898,11 +897,14 @@ __global__ void __launch_bounds__(kWsThreads, 2)
       double thv = (kRK ? bcur.th : tk) - c.dt * (flux - tk * div);
       if (kPhys) {  // column_physics (dycore.h90), applied to the new theta of this level
         thv = thv - a.dt_rrelax * (thv - colm_ij);
-        if (kk == 1) {  // new u, v at the lowest level (region 5), recomputed from the plane
+        // (only the first K phase holds level 1: the mid instantiation carries no branch, and
+        // tsfc is read where it is used instead of living in a register for the sweep)
+        if (!kMid && kk == 1) {  // new u, v at the lowest level (region 5), from the plane
           const double* Pp = S + kFOffP + (row + 1) * kPW + (lane + 2);
           const double un1 = (kCX && east) ? 0.0 : ui - c.dt_rdx * (Pp[1] - Pp[0]);
           const double vn1 = (kCY && north) ? 0.0 : vj - c.dt_rdy * (Pp[kPW] - Pp[0]);
           const double wspd = sqrt(un1 * un1 + vn1 * vn1);
+          const double tsfc_ij = active ? a.tsfc[(j - 1) * W + (i - 1)] : 0.0;
           thv = thv + a.dt_ch * wspd * (tsfc_ij - thv) * c.rdz / S[kFOffRho + row * kSW + lane];
         }
         const double rhok = S[kFOffRho + row * kSW + lane];

@@ -1,8 +1,4 @@
-HFB_LIB=ab/libhfb_ld.so timeout 100 python tools/debug_tma.py 512 512 58 | tr '\n' ' '; echo
-HFB_LIB=ab/libhfb_ld.so timeout 100 python tools/debug_tma.py 70 45 58 | tr '\n' ' '; echo
-for r in 1 2; do
-  for L in ab/libhfb_now.so ab/libhfb_ld.so; do
-    echo -n "$L 512: "; HFB_LIB=$L timeout 120 python tools/time_step.py 512 512 58 2>&1 | tail -1
-    echo -n "$L C4: "; HFB_LIB=$L timeout 120 python tools/time_step.py 1581 1301 58 2>&1 | tail -1
-  done
+for r in 1 2 3; do
+  echo -n "C4 dyc: "; timeout 120 python tools/time_step.py 1581 1301 58 2>&1 | tail -1
+  echo -n "C4 full: "; timeout 120 python tools/time_step.py 1581 1301 58 full 2>&1 | tail -1
 done

@@ -14,6 +14,9 @@ import numpy as np  # noqa: E402
 
 nx, ny, nz = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (512, 512, 58)))
 app = sys.argv[4] if len(sys.argv) > 4 else "dycore"
+full = app == "full"  # the full timestep: dycore + column physics (full_step)
+if full:
+    app = "dycore"
 eng = hfb.Engine(app)
 for k, v in dict(nx=nx, ny=ny, nz=nz, nsteps=1).items():
     eng.set(k, v)
@@ -23,6 +26,12 @@ if app == "dycore":
     arrs = {k: synthetic.field((nz, nx, ny), *v, order="F")
             for k, v in synthetic.DYCORE_FILLS.items()}
     entry, bpp = "dycore_step", 88
+    if full:
+        eng.set("ch", 0.05)
+        eng.set("rrelax", 0.01)
+        arrs["tsfc"] = synthetic.field((nx, ny), 13, 300.0, 2.0, order="F")
+        arrs["colm"] = synthetic.field((nx, ny), 14, 300.0, 0.5, order="F")
+        entry = "full_step"
 else:
     eng.set("coef", 0.1)
     arrs = {"t_old": synthetic.field((nz, nx, ny), 1, 280.0, 10.0, order="F"),
