@@ -1,7 +1,4 @@
-for L in ab/libhfb_cr1.so ab/libhfb_cr2.so; do HFB_LIB=$L timeout 100 python tools/debug_tma.py 70 45 58 | tr '\n' ' '; echo; done
-for r in 1 2; do
-  for L in ab/libhfb_cr0.so ab/libhfb_cr1.so ab/libhfb_cr2.so; do
-    echo -n "$L 512: "; HFB_LIB=$L timeout 120 python tools/time_step.py 512 512 58 2>&1 | tail -1
-    echo -n "$L C4 full: "; HFB_LIB=$L timeout 120 python tools/time_step.py 1581 1301 58 full 2>&1 | tail -1
-  done
+# scratch A/B script for gpurun (edited per experiment); see ab_libs.sh for the library A/B
+for L in ab/libhfb_now.so; do
+  echo -n "$L 512: "; HFB_LIB=$L timeout 120 python tools/time_step.py 512 512 58 2>&1 | tail -1
 done
