@@ -22,6 +22,7 @@ import hashlib
 from dataclasses import dataclass, field
 
 from .parse import (Assign, Bin, Call, Decl, Do, If, Logical, Name, Num, ParseError, Ref,
+                    Return, Stop,
                     Region, Un, parse_expr, parse_program)
 
 ROLE_I, ROLE_J, ROLE_K, ROLE_L = 0, 1, 2, 3
@@ -490,6 +491,10 @@ struct Run {
   cudaStream_t stream;
   int allow_transfers;
   int rc = HFB_OK;
+  unsigned long long* ret = nullptr;  // kernel threads that left through a `return`
+};
+struct HfcStop {  // `stop`: the run ends normally (interp.cpp StopSignal)
+  int code;
 };
 
 #define HFC_CHECK(call)                       \
@@ -678,6 +683,15 @@ class Gen:
 
     def stmt(self, s, sc, ind, kernel, R, region_ctx):
         em = self.em
+        if isinstance(s, Return):
+            if kernel and region_ctx is not None:  # a kernel thread leaves: a guard return
+                region_ctx["ret"] = True
+                return [f"{ind}{{ atomicAdd(hfc_ret, 1ULL); return; }}"]
+            return [f"{ind}return;"]
+        if isinstance(s, Stop):
+            if kernel:
+                raise GenError(f"line {s.line}: stop inside device code is not supported")
+            return [f"{ind}throw HfcStop{{{s.code}}};"]
         if isinstance(s, Assign):
             rhs_t = em.etype(s.rhs, sc)
             if isinstance(s.lhs, Ref):
@@ -923,6 +937,9 @@ class Gen:
             if len(names) == 2:
                 lin = f"({names[1]} - ({lo_c[1]})) * hfc_ex + {lin}"
             body.append(f"  hfc_red[{lin}] = {red[1]};")
+        if rctx.get("ret"):  # user returns counted on the device (exec_launch guard_returns)
+            params.append("unsigned long long* hfc_ret")
+            args.append("hfc_ret_counter(R)")
         sig = f"__global__ void __launch_bounds__(128) {kname}({', '.join(params)})"
         self.kernels.append((sig, body))
         # host launch (grid ceiling(extent / B), block (32, 4, 1): codegen.cpp:421-434)
@@ -1246,6 +1263,20 @@ inline HArr hfc_wr(Run& R, HRef& h, const char* n) {
   if (*h.r.has_device) *h.r.residency = 0;  // the host copy is now the newest
   return hfc_view(h.r.view);
 }
+// the run's early-return counter (one device word, zeroed once per run)
+unsigned long long* hfc_ret_counter(Run& R) {
+  if (!R.ret) {
+    const int64_t lo[] = {1}, hi[] = {1};
+    const int roles[] = {0};
+    HFC_CHECK(hfb_plugin_scratch(R.ctx, "@run.ret", 1, lo, hi, roles));
+    hfb_view v;
+    HFC_CHECK(hfb_plugin_view(R.ctx, "@run.ret", &v));
+    R.ret = reinterpret_cast<unsigned long long*>(v.origin);
+    if (cudaMemsetAsync(R.ret, 0, sizeof(unsigned long long), R.stream) != cudaSuccess)
+      throw static_cast<int>(HFB_CUDA);
+  }
+  return R.ret;
+}
 int hfc_copy_in(Run& R, const char* n) {
   if (!R.allow_transfers) return HFB_CONFIG;
   return hfrt_copy_to_device(R.ctx, kMod, n);
@@ -1293,7 +1324,18 @@ namespace {
 int run_entry(hfb_ctx* ctx, const char* routine, hfb_launch_stats* stats, int allow_transfers) {
   Run R{ctx, stats, static_cast<cudaStream_t>(hfb_stream(ctx)), allow_transfers};
   try {
-    dispatch(R, routine);
+    try {
+      dispatch(R, routine);
+    } catch (const HfcStop&) {
+      // the program stopped: the run ends here, state as left (run_program, interp.cpp)
+    }
+    if (R.ret) {  // kernel threads that returned early count as guard returns
+      unsigned long long n = 0;
+      if (cudaMemcpyAsync(&n, R.ret, sizeof n, cudaMemcpyDeviceToHost, R.stream) != cudaSuccess ||
+          cudaStreamSynchronize(R.stream) != cudaSuccess)
+        return HFB_CUDA;
+      R.st->guard_returns += static_cast<int64_t>(n);
+    }
   } catch (int rc) {
     return rc;
   }

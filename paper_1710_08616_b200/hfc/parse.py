@@ -84,6 +84,17 @@ class If:
 
 
 @dataclass
+class Return:       # leaves the routine (a kernel thread: counted like a guard return)
+    line: int
+
+
+@dataclass
+class Stop:         # ends the program run (interp.cpp StopSignal)
+    code: int
+    line: int
+
+
+@dataclass
 class Region:
     attrs: dict     # domname: [..], domsize: [(lo, hi) exprs], startat, endat, reduce
     body: list
@@ -507,6 +518,11 @@ class Parser:
                     self.next()
                     branches.append((None, body))
                 return If(branches, ln)
+        if low == "return":
+            return Return(ln)
+        m = re.match(r"stop(\s+(\d+))?$", low)
+        if m:
+            return Stop(int(m.group(2)) if m.group(2) else 0, ln)
         m = re.match(r"call\s+(\w+)\s*(\((.*)\))?$", low)
         if m:
             args = [parse_expr(a, ln) for a in split_top(m.group(3) or "")] if m.group(3) else []

@@ -188,3 +188,33 @@ def test_plugin_descriptor(name, module, entries):
     # routines taking arguments are not entries (physics_main(i, j, swind))
     assert "physics_main" not in got
     assert set(_strings(d.transfer_entries)) <= got
+
+
+def test_return_and_stop_statements():
+    from paper_1710_08616_b200.hfc.parse import Return, Stop
+    body = """  subroutine run()
+    use st, only : nx, ny, a
+    implicit none
+    @domainDependant{attribute(autoDom, present)}
+    a
+    @end domainDependant
+    @parallelRegion{domName(i,j), domSize(nx,ny)}
+    if (i .EQ. nx) then
+      return
+    end if
+    a(i,j) = 1.0_r_size
+    @end parallelRegion
+  end subroutine
+
+  subroutine main()
+    implicit none
+    call run()
+    stop 3
+  end subroutine
+"""
+    code = _gen(body)
+    # a kernel thread's return is counted like the launch guard (exec_launch)
+    assert "atomicAdd(hfc_ret, 1ULL); return;" in code
+    assert "throw HfcStop{3};" in code
+    with pytest.raises(GenError):  # stop inside device code
+        _gen(_region("    stop"))
