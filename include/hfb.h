@@ -212,6 +212,9 @@ hfb_status hfb_nccl_unique_id(void* out128);
  * sum the ranks' partials in rank order (deterministic). */
 hfb_status hfb_peer_export(hfb_ctx* ctx, void* buf, size_t cap, size_t* len);
 hfb_status hfb_peer_attach(hfb_ctx* ctx, int n, const void* const* blobs, const size_t* lens);
+/* Teardown: a rank's last dycore step still stores halo cells into its neighbours'
+ * buffers, so every rank must have returned from its last hfb_run / hfb_synchronize
+ * (e.g. a torch.distributed barrier) before any rank calls hfb_destroy. */
 /* halo updates so far: by the push kernel / handed off by the previous step's epilogue
  * (consecutive dycore steps store their edge outputs into the neighbours' halo rings) */
 hfb_status hfb_peer_stats(hfb_ctx* ctx, int64_t* pushes, int64_t* handoffs);
