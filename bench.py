@@ -7,6 +7,7 @@ Workload (BASELINE.json configs[1]): 512 x 512 x 58 per GPU, fp64, synthetic sta
 (nx*ny*nz / t_step, whole job) and the HBM-roofline fraction of the dominant kernel.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--strong] [--transport peer|nccl]
 
 N > 1 runs under torchrun, one rank per GPU: a 2-D (px x py) horizontal block
 decomposition, WEAK scaling (a 512 x 512 x 58 tile per GPU). The halo exchange uses the
@@ -33,6 +34,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 NX, NY, NZ = 512, 512, 58
+C4_NX, C4_NY = 1581, 1301  # the production domain (BASELINE configs[3], strong scaling)
 METRIC = "grid-point updates/sec per timestep"
 UNIT = "grid-point updates/s"
 GRIDS = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
@@ -136,10 +138,9 @@ def decompose(eng, d, n, transport, dist):
         eng.set_decomposition(d)
 
 
-def make_state(eng, d, px, py):
+def make_state(eng, d, gnx, gny):
     """Bind the synthetic state of this rank's tile (global-flat-indexed fields)."""
     from paper_1710_08616_b200 import synthetic
-    gnx, gny = NX * px, NY * py
     box = [(0, NZ), (d.i0, d.i0 + d.nx), (d.j0, d.j0 + d.ny)]
     arrs = {k: synthetic.field((NZ, gnx, gny), *v, box=box, order="F")
             for k, v in synthetic.DYCORE_FILLS.items()}
@@ -265,9 +266,11 @@ def bench_ours(args):
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     eng = hfb.Engine("dycore", device=local)
-    d = hfb.decomp_init(NX * px, NY * py, NZ, px, py, rank, halo=2)
+    # weak scaling (default): a 512 x 512 tile per GPU; --strong: the C4 grid split
+    gnx, gny = (C4_NX, C4_NY) if args.strong else (NX * px, NY * py)
+    d = hfb.decomp_init(gnx, gny, NZ, px, py, rank, halo=2)
     decompose(eng, d, n, args.transport, dist)
-    arrs = make_state(eng, d, px, py)
+    arrs = make_state(eng, d, gnx, gny)
     if n > 1 and args.transport == "peer":
         eng.attach_peers()
     for k in arrs:
@@ -306,7 +309,7 @@ def bench_ours(args):
         t = torch.tensor([ms], device="cpu" if one_gpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    pts_step = NX * NY * NZ * n
+    pts_step = gnx * gny * NZ
     value = pts_step * args.steps / (ms / 1e3)
 
     # ---- roofline of the dominant kernel (live CUDA events over the timed region) -------
@@ -343,12 +346,12 @@ def bench_ours(args):
     e2e_nsteps = 100
     eng2 = hfb.Engine("dycore", device=local)
     decompose(eng2, d, n, args.transport, dist)
-    arrs2 = make_state(eng2, d, px, py)
+    arrs2 = make_state(eng2, d, gnx, gny)
     if n > 1 and args.transport == "peer":
         eng2.attach_peers()
     eng2.set("nsteps", e2e_nsteps)
     eng2.run("main")  # warm-up call
-    arrs2 = make_state(eng2, d, px, py)
+    arrs2 = make_state(eng2, d, gnx, gny)
     eng2.set("nsteps", e2e_nsteps)
     e2e_calls = max(1, min(3, args.steps // 10))
     barrier()
@@ -377,10 +380,13 @@ def bench_ours(args):
         out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": n,
                "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+               "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
+               "dtype": "f64",
                "data": "synthetic (SplitMix64 fields, SURVEY §8(d))",
-               "config": {"workload": f"dycore+HE-VI {NX}x{NY}x{NZ} per GPU (BASELINE configs[1])",
-                          "global_grid": [NX * px, NY * py, NZ], "decomposition": f"{px}x{py}",
+               "config": {"workload": (f"dycore+HE-VI {C4_NX}x{C4_NY}x{NZ} split over {n} GPU(s) "
+                                       "(BASELINE configs[3], strong)") if args.strong else
+                          f"dycore+HE-VI {NX}x{NY}x{NZ} per GPU (BASELINE configs[1])",
+                          "global_grid": [gnx, gny, NZ], "decomposition": f"{px}x{py}",
                           "transport": args.transport if n > 1 else None,
                           "l2": f"inputs larger than L2: {6 * NX * NY * NZ * 8 / 2**30:.2f} GiB "
                                 f"state + {5 * NX * NY * NZ * 8 / 2**30:.2f} GiB outputs per step "
@@ -461,6 +467,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling of the 1581x1301x58 grid (default: weak, 512x512 per GPU)")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="halo exchange for N > 1 (peer: P2P stores + flags; nccl: send/recv)")
     ap.add_argument("--no-secondary", action="store_true",
