@@ -1,7 +1,4 @@
-timeout 300 python -m pytest tests/test_gpu_parity.py tests/test_gpu_decomp.py -q -x -k "diffusion" 2>&1 | tail -1
-for r in 1 2 3; do
-  for L in ab/libhfb_now.so ab/libhfb_diff2.so; do
-    echo -n "$L C4 diff: "; HFB_LIB=$L timeout 120 python tools/time_step.py 1581 1301 58 diffusion 2>&1 | tail -1
-  done
+for v in "HFB_DEBUG_SKIP=0" "HFB_DEBUG_SKIP=1" "HFB_DEBUG_SKIP=2" "HFB_DEBUG_SKIP=3"; do
+  echo -n "[$v] dyc "; env $v timeout 120 python tools/time_step.py 512 512 58 2>&1 | tail -1
+  echo -n "[$v] full "; env $v timeout 120 python tools/time_step.py 512 512 58 full 2>&1 | tail -1
 done
-echo -n "512 diff: "; timeout 120 python tools/time_step.py 512 512 58 diffusion 2>&1 | tail -1
