@@ -590,6 +590,9 @@ __global__ void __launch_bounds__(kWsThreads, 2)
   __shared__ uint32_t tmem_base_slot;
   double* ring = smem;
   double* ps_s = smem + kWsStages * kFStageDoubles;  // nz x 128 (ps of each column)
+  // kPhys: theta' of levels k-1 / k (parity), handed from the advection warps to the
+  // acoustic warps, which accumulate the column sums (the halves stay balanced)
+  double* thv_s = ps_s + a.nz * kThreads;
 
   const int lane = threadIdx.x, warp = threadIdx.y;  // blockDim = (32, 8)
   const bool acoustic = warp < kTY;
@@ -837,6 +840,11 @@ __global__ void __launch_bounds__(kWsThreads, 2)
       remote(rem.u, k, unk);
       remote(rem.v, k, vnk);
       ps_s[k * kThreads + t] = psk;
+      if (kPhys && (kMid || k >= 1)) {  // column sums of level k-1, in level order
+        const double thp = thv_s[((k - 1) & 1) * kThreads + t];
+        phys_cs = phys_cs + rho_prev * thp;
+        phys_cm = phys_cm + rho_prev;
+      }
       // The Thomas recursion for face f = k-2 (its coefficients were formed in the
       // previous iteration) runs here, independent of this iteration's coefficient
       // formation for face k-1: the two division chains overlap instead of adding up.
@@ -907,9 +915,7 @@ __global__ void __launch_bounds__(kWsThreads, 2)
           const double tsfc_ij = active ? a.tsfc[(j - 1) * W + (i - 1)] : 0.0;
           thv = thv + a.dt_ch * wspd * (tsfc_ij - thv) * c.rdz / S[kFOffRho + row * kSW + lane];
         }
-        const double rhok = S[kFOffRho + row * kSW + lane];
-        phys_cs = phys_cs + rhok * thv;
-        phys_cm = phys_cm + rhok;
+        thv_s[(k & 1) * kThreads + t] = thv;
       }
       if (kIn || active) *out_a = thv;
       remote(rem.th, k, thv);
@@ -959,7 +965,15 @@ __global__ void __launch_bounds__(kWsThreads, 2)
     thomas_commit(nz - 2, cpk, dpk);
   }
   sm100::cp_async_wait<0>();
-  if (kPhys && !acoustic && active) a.colm[(j - 1) * W + (i - 1)] = phys_cs / phys_cm;
+  if (kPhys) {  // the last level's column-sum terms, then the new column mean
+    __syncthreads();
+    if (acoustic) {
+      const double thp = thv_s[((nz - 1) & 1) * kThreads + t];
+      phys_cs = phys_cs + rho_prev * thp;
+      phys_cm = phys_cm + rho_prev;
+      if (active) a.colm[(j - 1) * W + (i - 1)] = phys_cs / phys_cm;
+    }
+  }
 
   if (acoustic) {
     sm100::tmem_wait_st();
@@ -1011,7 +1025,8 @@ cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, i
   if (phys && base) return cudaErrorInvalidValue;
   if (remote && base) return cudaErrorInvalidValue;  // RK stages exchange by push
   const size_t smem = std::max<size_t>((static_cast<size_t>(kWsStages) * kFStageDoubles +
-                                        static_cast<size_t>(nz) * kThreads) * sizeof(double),
+                                        static_cast<size_t>(nz) * kThreads +
+                                        (phys ? 2 * kThreads : 0)) * sizeof(double),
                                        80 * 1024);
   const int variant = (phys ? 1 : base ? 2 : 0) + (remote ? 3 : 0);
   void (*kern)(StepTmemArgs, RemoteHalo) = variant == 1   ? k_dyn_step_ws<true, false, false>
