@@ -80,41 +80,66 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
-            time.sleep(0.3)
+            # nvidia-smi may take a while to start: wait for its first sample so the
+            # timed region is bracketed by samples
+            deadline = time.perf_counter() + 10.0
+            while not self.rows and time.perf_counter() < deadline and self.proc.poll() is None:
+                time.sleep(0.01)
         except FileNotFoundError:
             self.proc = None
+        self.t0 = self.t1 = time.perf_counter()
         return self
+
+    def start(self):  # the timed region begins (after the ranks' barrier)
+        self.t0 = time.perf_counter()
+
+    def stop(self):  # the timed region ended (after the device synchronize)
+        self.t1 = time.perf_counter()
 
     def _read(self):
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) == 6:
-                self.rows.append(parts)
+                self.rows.append((time.perf_counter(), parts))
 
     def __exit__(self, *a):
         if self.proc:
-            time.sleep(0.1)
+            # at least one sample after the region ended
+            deadline = self.t1 + 2.0
+            while (not self.rows or self.rows[-1][0] <= self.t1) and \
+                    time.perf_counter() < deadline and self.proc.poll() is None:
+                time.sleep(0.01)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
+    def window(self):
+        """Samples inside the timed region plus the nearest one on each side (the region
+        can be shorter than the sampling interval)."""
+        inside = [r for t, r in self.rows if self.t0 <= t <= self.t1]
+        before = [r for t, r in self.rows if t < self.t0][-1:]
+        after = [r for t, r in self.rows if t > self.t1][:1]
+        return before + inside + after
+
     def summary(self):
-        if not self.rows:
+        rows = self.window()
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[q] for r in self.rows for q in range(4)
+        reasons = sorted({names[q] for r in rows for q in range(4)
                           if r[2 + q].lower().startswith("active")})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(rows),
+                "window_ms": round((self.t1 - self.t0) * 1e3, 2)}
 
 
 def dist_env():
@@ -293,13 +318,15 @@ def bench_ours(args):
     t_ev0 = torch.cuda.Event(enable_timing=True)
     t_ev1 = torch.cuda.Event(enable_timing=True)
     launches = 0
-    barrier()
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local) as clocks:  # nvidia-smi running before the region starts
+        barrier()
+        clocks.start()
         t_ev0.record(stream)
         for _ in range(args.steps):
             launches += eng.enqueue("dycore_step").native_launches
         t_ev1.record(stream)
         eng.synchronize()
+        clocks.stop()
     barrier()
     ms = t_ev0.elapsed_time(t_ev1)
     eng.profile(False)
