@@ -417,3 +417,29 @@ def test_layout_invariance_all_host_orders(app):
     _, out, _, _ = load_golden(case.name)
     for k in APPS[case.app].outputs:
         assert bits_equal(results[0][k], out[k]), k
+
+
+def test_transfer_state_machine_matches_reference():
+    """hfrt_device_allocate / copy_to_device / copy_from_device against the reference's
+    exec_transfer (interp.cpp:1369-1415): error kinds and texts, residency after each."""
+    case, arrs, eng = _diffusion_engine(nsteps=1)
+    with pytest.raises(hfb.HfbError) as e:
+        eng.copy_from_device("t_new")
+    assert e.value.kind == "residency" and "never transferred to the device" in str(e.value)
+    eng.device_allocate("t_new")  # a device copy; residency unchanged (still host)
+    assert eng.residency("t_new") == ("host", True)
+    eng.device_allocate("t_new")  # idempotent
+    with pytest.raises(hfb.HfbError) as e:
+        eng.copy_from_device("t_new")
+    assert e.value.kind == "residency" and "would overwrite newer host data" in str(e.value)
+    eng.copy_to_device("t_old")
+    assert eng.residency("t_old") == ("both", True)
+    eng.run("diffuse_step")  # writes both on the device
+    assert eng.residency("t_new") == ("device", True)
+    with pytest.raises(hfb.HfbError) as e:
+        eng.copy_to_device("t_new")
+    assert e.value.kind == "residency" and "would overwrite newer device data" in str(e.value)
+    eng.copy_from_device("t_new")
+    assert eng.residency("t_new") == ("both", True)
+    eng.copy_to_device("t_new")  # both -> both: allowed
+    eng.close()
