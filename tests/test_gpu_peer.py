@@ -185,3 +185,80 @@ def test_peer_ordered_reduction_bit_exact(px, py):
     accsim = run_oracle(case, {k: v.copy() for k, v in garr.items()})["total_accsim"]
     for p in parts:
         assert np.float64(p[3]).view(np.uint64) == np.float64(accsim).view(np.uint64)
+
+
+def ckpt_worker(rank, world, port, px, py, phase, tmpdir, q):
+    """phase 0: 2 steps then an HFBSTAT1 image per rank; phase 1: restore, 1 more step."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        case = PEER_CASES["dycore"]
+        gnx, gny = global_extent(case)
+        d = hfb.decomp_init(gnx, gny, case.ints["nz"], px, py, rank, halo=2)
+        img = os.path.join(tmpdir, f"rank{rank}.hfbstate")
+        if phase == 0:
+            garr = make_inputs(case)
+            eng = hfb.Engine("dycore", device=0)
+            eng.set_decomposition(d)
+            ints = dict(tile_ints(case, d), nsteps=2)
+            for k, v in ints.items():
+                eng.set(k, int(v))
+            for k, v in case.reals.items():
+                eng.set(k, float(v))
+            for n, a in garr.items():
+                eng.bind(n, np.ascontiguousarray(a[tile_slices(case.app, n, a, d)]))
+            eng.attach_peers()
+            eng.run("main")
+            eng.save_state(img)
+            q.put((rank, None, None))
+        else:
+            eng = hfb.Engine.from_state(img, device=0)
+            eng.set("nsteps", 1)
+            eng.set_decomposition(d)
+            eng.attach_peers()
+            eng.run("main")
+            q.put((rank, {n: eng.array(n).copy() for n in ("th", "u", "v", "w", "p")}, None))
+        dist.barrier()
+        eng.close()
+    except Exception as e:
+        q.put((rank, None, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_checkpoint_resume_per_rank(tmp_path):
+    """Each rank writes its tile's MachineState image after 2 decomposed steps; fresh
+    processes restore them, re-attach the peer transport and run 1 more step: the
+    assembled tiles equal 3 undecomposed steps bit for bit."""
+    px, py, world = 2, 2, 4
+    ctx = mp.get_context("spawn")
+    parts = None
+    for phase in (0, 1):
+        q = ctx.Queue()
+        port = free_port()
+        procs = [ctx.Process(target=ckpt_worker, args=(r, world, port, px, py, phase,
+                                                       str(tmp_path), q)) for r in range(world)]
+        for p in procs:
+            p.start()
+        try:
+            parts = [q.get(timeout=300) for _ in range(world)]
+            for p in procs:
+                p.join(timeout=120)
+        finally:
+            for p in procs:
+                if p.is_alive():
+                    p.kill()
+        errors = [e for *_, e in parts if e]
+        assert not errors, errors
+    case = PEER_CASES["dycore"]
+    garr = make_inputs(case)
+    ref = {k: v.copy() for k, v in garr.items()}
+    ref_case = Case("ck", "dycore", dict(case.ints, nsteps=3), case.reals, case.fills)
+    run_oracle(ref_case, ref)
+    gnx, gny = global_extent(case)
+    for rank, tiles, _ in parts:
+        d = hfb.decomp_init(gnx, gny, case.ints["nz"], px, py, rank, halo=2)
+        for k, t in tiles.items():
+            want = ref[k][tile_slices(case.app, k, ref[k], d)]
+            assert bits_equal(t.reshape(want.shape), want), (rank, k)
