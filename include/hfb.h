@@ -200,6 +200,8 @@ void hfb_group_destroy(hfb_group* group);
 hfb_status hfb_group_run(hfb_group* group, const char* entry, hfb_launch_stats* stats);
 /* halo bytes moved by this context so far (for NVLink accounting) */
 int64_t hfb_halo_bytes(hfb_ctx* ctx);
+/* host->device and device->host bytes transferred by this context so far */
+hfb_status hfb_transfer_bytes(hfb_ctx* ctx, int64_t* h2d, int64_t* d2h);
 /* 128-byte ncclUniqueId for hfb_set_decomposition (rank 0 creates, all ranks share) */
 hfb_status hfb_nccl_unique_id(void* out128);
 /* Peer-memory transport (one process per rank, NVLink/NVSwitch P2P; replaces NCCL for

@@ -285,6 +285,7 @@ struct hfb_ctx {
   double* red_cols = nullptr;
   size_t red_cols_cap = 0;
   int64_t halo_bytes = 0;
+  int64_t h2d_bytes = 0, d2h_bytes = 0;  // host <-> device transfer bytes (hfb_transfer_bytes)
   // NCCL (multi-process decomposition)
   void* nccl_comm = nullptr;
   double* halo_send = nullptr;
@@ -470,6 +471,7 @@ void do_copy_to_device(hfb_ctx* c, Slot& s) {
   ensure_staging(c, bytes);
   cuda_check(cudaMemcpyAsync(c->staging, s.host, bytes, cudaMemcpyHostToDevice, c->stream),
              "cudaMemcpyAsync(H2D)");
+  c->h2d_bytes += static_cast<int64_t>(bytes);
   cuda_check(launch_relayout(c->staging, s.d(), relayout_of(s), true, c->stream),
              "relayout(H2D)");
   s.has_device = true;
@@ -490,7 +492,17 @@ void do_copy_from_device(hfb_ctx* c, Slot& s) {
   cuda_check(cudaMemcpyAsync(s.host, c->staging, bytes, cudaMemcpyDeviceToHost, c->stream),
              "cudaMemcpyAsync(D2H)");
   cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  c->d2h_bytes += static_cast<int64_t>(bytes);
   s.res = kBoth;
+}
+
+// The copy-out at the end of an entry that copied the array in itself (transferHere,
+// codegen.cpp:570-600): an array the entry never wrote on the device — residency still
+// Both since that copy-in — already equals its host copy inside this synchronous call,
+// so the transfer is skipped (same bytes, same residency; e.g. the dycore's rho)
+void entry_copy_out(hfb_ctx* c, Slot& s) {
+  if (s.has_device && s.res == kBoth) return;
+  do_copy_from_device(c, s);
 }
 
 // device-code access checks (slot_side, interp.cpp:397-411)
@@ -685,7 +697,7 @@ void diffusion_entry(hfb_ctx* c, const std::string& r, Stats& st) {
     int64_t nsteps = ival(c, "nsteps");
     for (const char* n : {"t_new", "t_old"}) do_copy_to_device(c, slot(c, n));
     for (int64_t s = 0; s < nsteps; ++s) diffusion_step(c, st, s == nsteps - 1);
-    for (const char* n : {"t_new", "t_old"}) do_copy_from_device(c, slot(c, n));
+    for (const char* n : {"t_new", "t_old"}) entry_copy_out(c, slot(c, n));
   } else if (r == "diffuse_step") {
     diffusion_step(c, st, true);
   } else {
@@ -719,7 +731,7 @@ void damping_entry(hfb_ctx* c, const std::string& r, Stats& st) {
   if (r == "main") {
     for (const char* n : names) do_copy_to_device(c, slot(c, n));
     damping_kernel(c, st);
-    for (const char* n : names) do_copy_from_device(c, slot(c, n));
+    for (const char* n : names) entry_copy_out(c, slot(c, n));
   } else if (r == "lateral_and_upper_damping") {
     damping_kernel(c, st);
   } else {
@@ -752,7 +764,7 @@ void bounded_entry(hfb_ctx* c, const std::string& r, Stats& st) {
   if (r == "main" || r == "simulation_run") {
     for (const char* n : {"a", "b"}) do_copy_to_device(c, slot(c, n));
     bounded_kernel(c, st);
-    for (const char* n : {"a", "b"}) do_copy_from_device(c, slot(c, n));
+    for (const char* n : {"a", "b"}) entry_copy_out(c, slot(c, n));
   } else if (r == "interior_update") {
     bounded_kernel(c, st);
   } else {
@@ -791,9 +803,10 @@ void sf_entry(hfb_ctx* c, const std::string& r, Stats& st) {
       int64_t nx = ival(c, "nx"), ny = ival(c, "ny");
       launch(c, st, "sf_setup", [&] { return launch_sf_setup(cf.d(), grid_of(cf), ival(c, "ntlm"), full_span(c, nx, ny),
                                c->stream); });
+      dev_written(c, "cover_frac");
     }
     sf_tile_kernel(c, st);
-    for (const char* n : names) do_copy_from_device(c, slot(c, n));
+    for (const char* n : names) entry_copy_out(c, slot(c, n));
   } else if (r == "physics_run" || r == "sf_slab_flx_tile_run" || r == "physics_main") {
     sf_tile_kernel(c, st);
   } else {
@@ -877,7 +890,7 @@ void reduction_entry(hfb_ctx* c, const std::string& r, Stats& st) {
     tot.r = 0.0;  // reduction.h90:34 `total = 0.0_r_size`
     tot.init = true;
     reduction_kernel(c, st);
-    do_copy_from_device(c, slot(c, "y"));
+    entry_copy_out(c, slot(c, "y"));
   } else if (r == "grid_total") {
     reduction_kernel(c, st);
   } else {
@@ -1060,7 +1073,7 @@ void dycore_entry(hfb_ctx* c, const std::string& r, Stats& st) {
     int64_t nsteps = ival(c, "nsteps");
     for (const char* n : names) do_copy_to_device(c, slot(c, n));
     for (int64_t s = 0; s < nsteps; ++s) dycore_step(c, st);
-    for (const char* n : names) do_copy_from_device(c, slot(c, n));
+    for (const char* n : names) entry_copy_out(c, slot(c, n));
   } else if (r == "dycore_step") {
     dycore_step(c, st);
   } else if (r == "main_full" || r == "simulation_run_full") {
@@ -1068,7 +1081,7 @@ void dycore_entry(hfb_ctx* c, const std::string& r, Stats& st) {
     const char* full_names[] = {"colm", "p", "rho", "th", "tsfc", "u", "v", "w"};
     for (const char* n : full_names) do_copy_to_device(c, slot(c, n));
     for (int64_t s = 0; s < nsteps; ++s) dycore_step(c, st, true);
-    for (const char* n : full_names) do_copy_from_device(c, slot(c, n));
+    for (const char* n : full_names) entry_copy_out(c, slot(c, n));
   } else if (r == "full_step") {
     dycore_step(c, st, true);
   } else if (r == "rk3_step") {
@@ -1077,7 +1090,7 @@ void dycore_entry(hfb_ctx* c, const std::string& r, Stats& st) {
     int64_t nsteps = ival(c, "nsteps");
     for (const char* n : names) do_copy_to_device(c, slot(c, n));
     for (int64_t s = 0; s < nsteps; ++s) rk3_step(c, st);
-    for (const char* n : names) do_copy_from_device(c, slot(c, n));
+    for (const char* n : names) entry_copy_out(c, slot(c, n));
   } else if (r == "column_physics") {
     column_physics(c, st);
   } else {
@@ -2117,6 +2130,14 @@ hfb_status hfb_set_decomposition(hfb_ctx* c, const hfb_decomp* d, const void* nc
 }
 
 int64_t hfb_halo_bytes(hfb_ctx* c) { return c ? c->halo_bytes : 0; }
+
+hfb_status hfb_transfer_bytes(hfb_ctx* c, int64_t* h2d, int64_t* d2h) {
+  return guarded([&] {
+    if (!c) fail(HFB_CONFIG, "null context");
+    if (h2d) *h2d = c->h2d_bytes;
+    if (d2h) *d2h = c->d2h_bytes;
+  });
+}
 
 hfb_status hfb_group_create(hfb_ctx* const* ctxs, int n, hfb_group** out) {
   return guarded([&] {

@@ -44,7 +44,7 @@ EXPORTS = [
     "hfb_load_state", "hfb_host_array", "hfb_array_checksum", "hfb_run_scenario",
     "hfb_set_reduction_order", "hfb_program_name", "hfb_program_module", "hfb_plugin_prepare",
     "hfb_plugin_written", "hfb_plugin_view", "hfb_plugin_scratch", "hfb_plugin_host", "hfb_plugin_host_ref",
-    "hfb_peer_export", "hfb_peer_attach", "hfb_peer_stats",
+    "hfb_peer_export", "hfb_peer_attach", "hfb_peer_stats", "hfb_transfer_bytes",
 ]
 
 # module of each built-in program (the apps' state modules)
@@ -146,6 +146,7 @@ def lib():
         L.hfb_peer_export.argtypes = [P, P, c.c_size_t, c.POINTER(c.c_size_t)]
         L.hfb_peer_attach.argtypes = [P, c.c_int, c.POINTER(P), c.POINTER(c.c_size_t)]
         L.hfb_peer_stats.argtypes = [P, c.POINTER(i64), c.POINTER(i64)]
+        L.hfb_transfer_bytes.argtypes = [P, c.POINTER(i64), c.POINTER(i64)]
         _lib = L
     return _lib
 
@@ -375,6 +376,12 @@ class Engine:
         dist.all_gather_object(blobs, mine, group=group)
         self.peer_attach(blobs)
         dist.barrier(group)
+
+    def transfer_bytes(self):
+        """(host->device, device->host) bytes this context transferred so far"""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().hfb_transfer_bytes(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
 
     def peer_stats(self):
         """(halo updates by push kernel, halo updates handed off by the step epilogue)"""

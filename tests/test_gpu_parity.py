@@ -443,3 +443,28 @@ def test_transfer_state_machine_matches_reference():
     assert eng.residency("t_new") == ("both", True)
     eng.copy_to_device("t_new")  # both -> both: allowed
     eng.close()
+
+
+def test_entry_copy_out_skips_untouched_arrays():
+    """`main` copies the six dycore fields in and, at the end, out — except rho, which no
+    step writes: residency is still Both, the host already holds the device's bytes, so
+    no D2H happens (and the result is unchanged)."""
+    case = Case("x", "dycore", dict(nx=40, ny=24, nz=12, nsteps=2), dict(DYCORE_SCALARS),
+                dict(DYCORE_FILLS))
+    arrs = make_inputs(case)
+    ref = {k: v.copy() for k, v in arrs.items()}
+    run_oracle(case, ref)
+    with hfb.Engine("dycore") as eng:
+        for k, v in case.ints.items():
+            eng.set(k, int(v))
+        for k, v in case.reals.items():
+            eng.set(k, float(v))
+        for name, a in arrs.items():
+            eng.bind(name, a)
+        eng.run("main")
+        h2d, d2h = eng.transfer_bytes()
+        assert eng.residency("rho") == ("both", True)
+    field = 12 * 40 * 24 * 8
+    assert h2d == 6 * field and d2h == 5 * field
+    for k in ("th", "u", "v", "w", "p", "rho"):
+        assert bits_equal(arrs[k], ref[k]), k
