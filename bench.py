@@ -80,7 +80,8 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "20"],
+                 "--format=csv,noheader,nounits", "-lms",
+                 os.environ.get("HFB_BENCH_SMI_MS", "20")],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -307,8 +308,6 @@ def bench_ours(args):
     for _ in range(args.warmup):
         eng.enqueue("dycore_step")
     eng.synchronize()
-    eng.profile(True, clear=True)
-    eng.profile(True)
 
     def barrier():
         if n > 1:
@@ -329,9 +328,20 @@ def bench_ours(args):
         clocks.stop()
     barrier()
     ms = t_ev0.elapsed_time(t_ev1)
+    # per-kernel device times from a second pass of the same K steps with CUDA events
+    # around every launch (hfb_profile); kept out of the timed region, whose events
+    # would otherwise add ~2% to the step
+    eng.profile(True, clear=True)
+    eng.profile(True)
+    barrier()
+    for _ in range(args.steps):
+        eng.enqueue("dycore_step")
+    eng.synchronize()
+    barrier()
     eng.profile(False)
     kt = {k: eng.kernel_time(k) for k in BYTES_PER_POINT}
     kt = {k: v for k, v in kt.items() if v[1] > 0}
+    ms_local = ms
     if n > 1:
         t = torch.tensor([ms], device="cpu" if one_gpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -348,7 +358,13 @@ def bench_ours(args):
     # strips (decomposed, halo exchange overlapped): the kernel's device time per STEP
     # moves the tile's algorithmic bytes
     alg_bytes = BYTES_PER_POINT[dom] * pts_local
-    per_step = dom_ms / args.steps
+    per_step_prof = dom_ms / args.steps
+    if dom_n == args.steps:  # the step is this one launch: the timed region's CUDA events
+        per_step = ms_local / args.steps  # (launch stream) / launches — conservative, it
+        timing = "timed-region events / launches"  # includes the gaps between launches
+    else:
+        per_step = per_step_prof
+        timing = "per-launch events (profiled pass)"
     achieved = alg_bytes / (per_step / 1e3) / 1e9
     traffic = None
     tp = ROOT / "profiles" / "traffic.json"
@@ -359,8 +375,9 @@ def bench_ours(args):
                 "frac_of_nominal_8TBps": round(achieved / 8000.0, 4),
                 "peak_source": src, "algorithmic_bytes_per_launch": alg_bytes,
                 "launches_per_step": dom_n // args.steps,
-                "kernel_ms_avg": round(per_step, 5),
-                "share_of_step": round(dom_ms / ms, 3),
+                "kernel_ms_avg": round(per_step, 5), "timing": timing,
+                "kernel_ms_profiled": round(per_step_prof, 5),
+                "share_of_step": round(min(1.0, per_step_prof / (ms_local / args.steps)), 3),
                 "kernels": {k: {"ms_avg": round(v[0] / args.steps, 5),
                                 "GBps": round(BYTES_PER_POINT[k] * pts_local /
                                               (v[0] / args.steps / 1e3) / 1e9, 1)}

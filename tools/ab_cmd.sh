@@ -1,7 +1,5 @@
-HFB_LIB=ab/libhfb_nobr.so timeout 100 python tools/debug_tma.py 70 45 58 | tr '\n' ' '; echo
 for r in 1 2; do
-  for L in ab/libhfb_now.so ab/libhfb_nobr.so; do
-    echo -n "$L 512: "; HFB_LIB=$L timeout 120 python tools/time_step.py 512 512 58 2>&1 | tail -1
-    echo -n "$L C4 full: "; HFB_LIB=$L timeout 120 python tools/time_step.py 1581 1301 58 full 2>&1 | tail -1
-  done
+for ms in 20 100 1000; do
+  echo -n "smi $ms: "; HFB_BENCH_SMI_MS=$ms timeout 600 python bench.py --no-secondary 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['roofline']['frac'], d['clocks']['samples'])"
+done
 done
