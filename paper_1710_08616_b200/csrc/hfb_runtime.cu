@@ -309,6 +309,9 @@ struct hfb_ctx {
   // `stream`; the boundary strips follow the exchange (HFB_NO_OVERLAP=1 serialises)
   cudaStream_t comm = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+  // the stream step kernels go to (nullptr: `stream`); exchange_and_run points it at
+  // `comm` for the boundary strips, which then overlap the interior launch
+  cudaStream_t run_stream = nullptr;
   bool overlap = getenv("HFB_NO_OVERLAP") == nullptr;
   // CUDA graph cache for hfb_run_graph
   cudaGraphExec_t graph_exec = nullptr;
@@ -576,6 +579,9 @@ cudaEvent_t take_event(hfb_ctx* c) {
 
 // Launch one native kernel (or a fixed group of `n`), with optional CUDA-event timing
 // on the context stream (never during graph capture).
+// the stream a step kernel is launched on (see hfb_ctx::run_stream)
+cudaStream_t ks(hfb_ctx* c) { return c->run_stream ? c->run_stream : c->stream; }
+
 template <class F>
 void launch(hfb_ctx* c, Stats& st, const char* name, F&& f, int n = 1) {
   NvtxRange nr(name);
@@ -583,12 +589,12 @@ void launch(hfb_ctx* c, Stats& st, const char* name, F&& f, int n = 1) {
   cudaEvent_t a = nullptr, b = nullptr;
   if (timed) {
     a = take_event(c);
-    cuda_check(cudaEventRecord(a, c->stream), "cudaEventRecord");
+    cuda_check(cudaEventRecord(a, ks(c)), "cudaEventRecord");
   }
   cuda_check(f(), name);
   if (timed) {
     b = take_event(c);
-    cuda_check(cudaEventRecord(b, c->stream), "cudaEventRecord");
+    cuda_check(cudaEventRecord(b, ks(c)), "cudaEventRecord");
     c->pending.push_back({name, a, b});
   }
   st.native += n;
@@ -651,9 +657,10 @@ void exchange_and_run(hfb_ctx* c, const std::vector<const char*>& fields, int r,
   cuda_check(cudaEventRecord(c->ev_ready, c->stream), "cudaEventRecord");
   cuda_check(cudaStreamWaitEvent(c->comm, c->ev_ready, 0), "cudaStreamWaitEvent");
   halo_exchange(c, fields, r, c->comm);
-  cuda_check(cudaEventRecord(c->ev_halo, c->comm), "cudaEventRecord");
   run(in, false);
-  cuda_check(cudaStreamWaitEvent(c->stream, c->ev_halo, 0), "cudaStreamWaitEvent");
+  // the boundary strips follow the halo wait on the communication stream, so they run
+  // alongside the interior launch (disjoint output columns, read-only inputs) instead of
+  // after it; the compute stream joins them before the step ends
   Span south = full, north = full, west = full, east = full;
   south.jhi = r;
   north.jlo = ny - r + 1;
@@ -661,7 +668,16 @@ void exchange_and_run(hfb_ctx* c, const std::vector<const char*>& fields, int r,
   west.jhi = east.jhi = ny - r;
   west.ihi = r;
   east.ilo = east_lo;
-  for (const Span& sp : {south, north, west, east}) run(sp, true);
+  c->run_stream = c->comm;
+  try {
+    for (const Span& sp : {south, north, west, east}) run(sp, true);
+  } catch (...) {
+    c->run_stream = nullptr;
+    throw;
+  }
+  c->run_stream = nullptr;
+  cuda_check(cudaEventRecord(c->ev_halo, c->comm), "cudaEventRecord");
+  cuda_check(cudaStreamWaitEvent(c->stream, c->ev_halo, 0), "cudaStreamWaitEvent");
 }
 
 // ---------------------------------------------------------------------------
@@ -680,9 +696,9 @@ void diffusion_step(hfb_ctx* c, Stats& st, bool write_t_new) {
     launch(c, st, "hfk0_diffuse_step", [&] {
       if (c->force_generic)
         return launch_diffusion(to.d(), to.d_alt(), write_t_new ? tn.d() : nullptr,
-                                grid_of(to), nz, coef, sp, c->stream);
+                                grid_of(to), nz, coef, sp, ks(c));
       return launch_diffusion_ring(to.d(), to.d_alt(), write_t_new ? tn.d() : nullptr,
-                                   grid_of(to), nz, to.lay.nj, coef, sp, c->stream);
+                                   grid_of(to), nz, to.lay.nj, coef, sp, ks(c));
     });
   });
   to.cur = to.alt();
@@ -963,32 +979,32 @@ void dycore_step(hfb_ctx* c, Stats& st, bool with_physics = false) {
     if (fused) {
       if (c->force_single_role)
         launch(c, st, "dycore_step", [&] {
-          return launch_dycore_step_tmem(in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
+          return launch_dycore_step_tmem(in, out, grid_of(th), nz, th.lay.nj, k, sp, ks(c));
         });
       else if (fused_physics)
         launch(c, st, "full_step", [&] {
           return rem ? launch_dycore_step_ws(in, out, grid_of(th), nz, th.lay.nj, k, sp,
-                                             c->stream, &ph, nullptr, rem)
-                     : launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream, &ph);
+                                             ks(c), &ph, nullptr, rem)
+                     : launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, ks(c), &ph);
         });
       else
         launch(c, st, "dycore_step", [&] {
           return rem ? launch_dycore_step_ws(in, out, grid_of(th), nz, th.lay.nj, k, sp,
-                                             c->stream, nullptr, nullptr, rem)
-                     : launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream);
+                                             ks(c), nullptr, nullptr, rem)
+                     : launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, ks(c));
         });
     } else {
       launch(c, st, "dycore_advect", [&] {
-        return launch_dycore_advect(in, out.th, grid_of(th), nz, k, sp, c->stream);
+        return launch_dycore_advect(in, out.th, grid_of(th), nz, k, sp, ks(c));
       });
       if (dycore_acoustic_tmem_fits(nz) && !c->force_generic)
         launch(c, st, "dycore_acoustic", [&] {
           return launch_dycore_acoustic_tmem(in, out, grid_of(th), nz, th.lay.nj, k, sp,
-                                             c->stream);
+                                             ks(c));
         });
       else
         launch(c, st, "dycore_acoustic", [&] {
-          return launch_dycore_acoustic(in, out, grid_of(th), nz, k, sp, c->stream);
+          return launch_dycore_acoustic(in, out, grid_of(th), nz, k, sp, ks(c));
         });
     }
   });
@@ -1055,7 +1071,7 @@ void rk3_step(hfb_ctx* c, Stats& st) {
     const DynOut out = outs(out_of[g]);
     exchange_and_run(c, {"th", "u", "v", "p"}, kHalo, nx, ny, true, [&](const Span& sp, bool) {
       launch(c, st, "rk3_stage", [&] {
-        return launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, c->stream, nullptr,
+        return launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, ks(c), nullptr,
                            g == 0 ? nullptr : &base);
       });
     });
