@@ -1,8 +1,8 @@
 // hfb_diffusion.cu — the reference's 7-point diffusion step (diffusion.h90:23-41, hfk0 +
 // the fused-away hfk1 copy) with shared-memory plane staging.
 //
-// A CTA owns a 32 x 8 tile of (i,j) columns and marches K. Each K-plane of t_old the tile
-// needs (the tile plus its one-cell ring, rows j0-1..j0+8, 36 columns from the even
+// A CTA owns a 32 x 16 tile of (i,j) columns and marches K. Each K-plane of t_old the tile
+// needs (the tile plus its one-cell ring, rows j0-1..j0+16, 36 columns from the even
 // column at or left of i0-1 so the 16-B copy chunks stay aligned for any span start) is
 // staged by LDGSTS into a kStages-deep ring; the
 // vertical neighbours ride in registers (k-1, k rotate; k+1 is the next plane's centre).
@@ -25,10 +25,10 @@ namespace hfb {
 
 namespace {
 
-constexpr int kTX = 32, kTY = 8, kThreads = kTX * kTY;
-constexpr int kPW = kTX + 4, kPR = kTY + 2;  // plane tile 36 x 10
-constexpr int kPlane = kPW * kPR;            // 360 doubles
-constexpr int kChunks = kPlane / 2;          // 180 16-B chunks (one per thread)
+constexpr int kTX = 32, kTY = 16, kThreads = kTX * kTY;  // 32x16: 32x8 was 1.9% slower
+constexpr int kPW = kTX + 4, kPR = kTY + 2;  // plane tile 36 x 18
+constexpr int kPlane = kPW * kPR;            // 648 doubles
+constexpr int kChunks = kPlane / 2;          // 324 16-B chunks (one per thread)
 constexpr int kStages = 6;
 
 struct RingArgs {
@@ -42,7 +42,7 @@ struct RingArgs {
   Span sp;
 };
 
-__global__ void __launch_bounds__(kThreads, 4) k_diffusion_ring(RingArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) k_diffusion_ring(RingArgs a) {
   __shared__ __align__(16) double ring[kStages * kPlane];
   const int lane = threadIdx.x, row = threadIdx.y, tid = row * kTX + lane;
   const int64_t i0 = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * kTX;  // 1-based local
