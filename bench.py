@@ -7,7 +7,7 @@ Workload (BASELINE.json configs[1]): 512 x 512 x 58 per GPU, fp64, synthetic sta
 (nx*ny*nz / t_step, whole job) and the HBM-roofline fraction of the dominant kernel.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--strong] [--transport peer|nccl]
+                  [--strong | --c4-tiles] [--transport peer|nccl]
 
 N > 1 runs under torchrun, one rank per GPU: a 2-D (px x py) horizontal block
 decomposition, WEAK scaling (a 512 x 512 x 58 tile per GPU). The halo exchange uses the
@@ -293,7 +293,8 @@ def bench_ours(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     eng = hfb.Engine("dycore", device=local)
     # weak scaling (default): a 512 x 512 tile per GPU; --strong: the C4 grid split
-    gnx, gny = (C4_NX, C4_NY) if args.strong else (NX * px, NY * py)
+    tnx, tny = (C4_NX, C4_NY) if args.c4_tiles else (NX, NY)  # weak-scaling tile
+    gnx, gny = (C4_NX, C4_NY) if args.strong else (tnx * px, tny * py)
     d = hfb.decomp_init(gnx, gny, NZ, px, py, rank, halo=2)
     decompose(eng, d, n, args.transport, dist)
     arrs = make_state(eng, d, gnx, gny)
@@ -433,7 +434,9 @@ def bench_ours(args):
                "data": "synthetic (SplitMix64 fields, SURVEY §8(d))",
                "config": {"workload": (f"dycore+HE-VI {C4_NX}x{C4_NY}x{NZ} split over {n} GPU(s) "
                                        "(BASELINE configs[3], strong)") if args.strong else
-                          f"dycore+HE-VI {NX}x{NY}x{NZ} per GPU (BASELINE configs[1])",
+                          (f"dycore+HE-VI {tnx}x{tny}x{NZ} per GPU (BASELINE configs[4], weak)"
+                           if args.c4_tiles else
+                           f"dycore+HE-VI {NX}x{NY}x{NZ} per GPU (BASELINE configs[1])"),
                           "global_grid": [gnx, gny, NZ], "decomposition": f"{px}x{py}",
                           "transport": args.transport if n > 1 else None,
                           "l2": f"inputs larger than L2: {6 * NX * NY * NZ * 8 / 2**30:.2f} GiB "
@@ -517,6 +520,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling of the 1581x1301x58 grid (default: weak, 512x512 per GPU)")
+    ap.add_argument("--c4-tiles", action="store_true",
+                    help="weak scaling with a 1581x1301x58 tile per GPU (BASELINE configs[4])")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="halo exchange for N > 1 (peer: P2P stores + flags; nccl: send/recv)")
     ap.add_argument("--no-secondary", action="store_true",
