@@ -439,9 +439,9 @@ def bench_ours(args):
                            f"dycore+HE-VI {NX}x{NY}x{NZ} per GPU (BASELINE configs[1])"),
                           "global_grid": [gnx, gny, NZ], "decomposition": f"{px}x{py}",
                           "transport": args.transport if n > 1 else None,
-                          "l2": f"inputs larger than L2: {6 * NX * NY * NZ * 8 / 2**30:.2f} GiB "
-                                f"state + {5 * NX * NY * NZ * 8 / 2**30:.2f} GiB outputs per step "
-                                f"vs 126 MB L2"},
+                          "l2": f"inputs larger than L2: {6 * pts_local * 8 / 2**30:.2f} GiB "
+                                f"state + {5 * pts_local * 8 / 2**30:.2f} GiB outputs per step "
+                                f"and GPU vs 126 MB L2"},
                "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
                "clocks": clocks.summary(), "halo_bytes": halo}
         if n > 1:  # rank 0's halo traffic (sent + received) per step and its rate
