@@ -1,21 +1,27 @@
 #!/usr/bin/env python3
-"""Benchmark: one ASUCA-style dry dynamical-core timestep (flux-limited advection,
-pressure gradient + divergence, HE-VI vertically implicit Thomas solve) per step.
+"""Benchmark: one full ASUCA-style timestep per step — the fused dynamical core
+(flux-limited advection, pressure gradient + divergence, HE-VI vertically implicit Thomas
+solve) plus the column physics (`full_step`, apps/dycore/dycore.h90).
 
-Workload (BASELINE.json configs[1]): 512 x 512 x 58 per GPU, fp64, synthetic state
-(SURVEY §8(d) SplitMix64 fields). Metric: grid-point updates per second per timestep
-(nx*ny*nz / t_step, whole job) and the HBM-roofline fraction of the dominant kernel.
+Workload (north_star; BASELINE configs[3] at N=1, configs[4] per GPU for N > 1): a
+1581 x 1301 x 58 grid per GPU, fp64, synthetic state (SURVEY §8(d) SplitMix64 fields).
+Metric: grid-point updates per second per timestep (nx*ny*nz / t_step, whole job) and the
+HBM-roofline fraction of the dominant kernel.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--strong | --c4-tiles] [--transport peer|nccl]
+                  [--strong | --tile512] [--entry full_step|dycore_step]
+                  [--transport peer|nccl]
 
 N > 1 runs under torchrun, one rank per GPU: a 2-D (px x py) horizontal block
-decomposition, WEAK scaling (a 512 x 512 x 58 tile per GPU). The halo exchange uses the
-peer-memory transport (push kernels storing into the neighbours' halo rings over
-NVLink/NVSwitch, CUDA IPC-mapped buffers, release/acquire flags); `--transport nccl`
-selects NCCL send/recv instead.
+decomposition, WEAK scaling (a 1581 x 1301 x 58 tile per GPU, configs[4]); `--strong`
+splits the one 1581 x 1301 x 58 grid (configs[3]). The halo exchange uses the peer-memory
+transport (push kernels storing into the neighbours' halo rings over NVLink/NVSwitch,
+CUDA IPC-mapped buffers, release/acquire flags); `--transport nccl` selects NCCL
+send/recv instead.
 `--impl reference` times the reference's own CPU path (oracle/_ref/hft_ref: the
 reference interpreter built from /root/reference/proj/src) on the host cores.
+The bench reads no HFB_* environment variable and refuses to run if one is set: every
+switch is a command-line flag, so a result cannot depend on a hidden knob.
 """
 import argparse
 import json
@@ -33,17 +39,24 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-NX, NY, NZ = 512, 512, 58
-C4_NX, C4_NY = 1581, 1301  # the production domain (BASELINE configs[3], strong scaling)
+NX, NY, NZ = 1581, 1301, 58  # the production domain (north_star; BASELINE configs[3]/[4])
+C2_NX, C2_NY = 512, 512     # BASELINE configs[1] (--tile512)
 METRIC = "grid-point updates/sec per timestep"
 UNIT = "grid-point updates/s"
 GRIDS = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
-# compulsory HBM bytes per grid point and step of each native kernel (DESIGN.md):
-# the fused step reads rho,th,u,v,w,p and writes th',u',v',w',p' (11 x 8 B); the split
+# compulsory HBM bytes per grid point and step of each native kernel (DESIGN.md §4):
+# the fused step reads rho,th,u,v,w,p and writes th',u',v',w',p' (11 x 8 B); the full
+# step adds, per COLUMN, tsfc and colm read and colm written (3 x 8 B); the split
 # variant's advect reads th,u,v,w / writes th' (5 x 8 B) and acoustic reads
 # rho,th,u,v,w,p / writes u',v',w',p' (10 x 8 B)
 BYTES_PER_POINT = {"dycore_step": 88, "full_step": 88, "dycore_advect": 40,
                    "dycore_acoustic": 80, "hfk0_diffuse_step": 24}
+BYTES_PER_COLUMN = {"full_step": 24}
+
+
+def alg_bytes(kernel, nx, ny, nz):
+    """algorithmic (compulsory) HBM bytes of one launch over an nx x ny x nz tile"""
+    return BYTES_PER_POINT[kernel] * nx * ny * nz + BYTES_PER_COLUMN.get(kernel, 0) * nx * ny
 L2_BYTES = 126 * 2**20
 
 
@@ -71,8 +84,9 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device):
+    def __init__(self, device, interval_ms=20):
         self.device = device
+        self.interval_ms = interval_ms
         self.rows = []
         self.proc = None
 
@@ -80,8 +94,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms",
-                 os.environ.get("HFB_BENCH_SMI_MS", "20")],
+                 "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -164,36 +177,43 @@ def decompose(eng, d, n, transport, dist):
         eng.set_decomposition(d)
 
 
-def make_state(eng, d, gnx, gny):
-    """Bind the synthetic state of this rank's tile (global-flat-indexed fields)."""
+def make_state(eng, d, gnx, gny, physics):
+    """Bind the synthetic state of this rank's tile (global-flat-indexed fields, pinned
+    host buffers); `physics` adds the column-physics fields of the full timestep."""
     from paper_1710_08616_b200 import synthetic
     box = [(0, NZ), (d.i0, d.i0 + d.nx), (d.j0, d.j0 + d.ny)]
     arrs = {k: synthetic.field((NZ, gnx, gny), *v, box=box, order="F")
             for k, v in synthetic.DYCORE_FILLS.items()}
+    scalars = dict(synthetic.DYCORE_SCALARS)
+    if physics:
+        box2 = box[1:]
+        arrs.update({k: synthetic.field((gnx, gny), *v, box=box2, order="F")
+                     for k, v in synthetic.PHYS_FILLS.items()})
+        scalars.update(synthetic.PHYS_SCALARS)
     for k, v in dict(nx=int(d.nx), ny=int(d.ny), nz=NZ, nsteps=1).items():
         eng.set(k, v)
-    for k, v in synthetic.DYCORE_SCALARS.items():
+    for k, v in scalars.items():
         eng.set(k, v)
     for k, a in arrs.items():
         eng.bind(k, a, pin=True)
     return arrs
 
 
-def secondary(local, steps=10, warmup=3):
+def secondary(local, steps=20, warmup=5):
     """Single-GPU, device-resident timings of the other BASELINE configs (reported beside
-    the headline; same CUDA-event method, per-kernel times from hfb_profile)."""
+    the headline; same CUDA-event method over `steps` back-to-back steps)."""
     import torch
     import paper_1710_08616_b200 as hfb
     from paper_1710_08616_b200 import synthetic
     hbm, _ = peaks()
     out = {}
-    runs = [("C1 dycore step 128x128x58", "dycore", "dycore_step", 128, 128),
+    runs = [("C1 dycore step 128x128x58 (BASELINE configs[0])", "dycore", "dycore_step", 128, 128),
+            ("C2 dycore step 512x512x58 (BASELINE configs[1])", "dycore", "dycore_step", 512, 512),
             ("C2 dycore with Wicker-Skamarock RK3 (3 stages) 512x512x58", "dycore", "rk3_step",
              512, 512),
-            ("C3 full timestep + column physics 1024x1024x58", "dycore", "full_step", 1024, 1024),
-            ("C4 dycore step 1581x1301x58 (1 GPU)", "dycore", "dycore_step", 1581, 1301),
-            ("north star: full timestep (dycore + HE-VI + column physics) 1581x1301x58 "
-             "(1 GPU)", "dycore", "full_step", 1581, 1301),
+            ("C3 full timestep + column physics 1024x1024x58 (BASELINE configs[2])", "dycore",
+             "full_step", 1024, 1024),
+            ("C4 dycore step without physics 1581x1301x58", "dycore", "dycore_step", 1581, 1301),
             ("reference kernel: diffusion step 1581x1301x58", "diffusion", "diffuse_step",
              1581, 1301)]
     for label, prog, entry, nx, ny in runs:
@@ -202,21 +222,22 @@ def secondary(local, steps=10, warmup=3):
         for k, v in dict(nx=nx, ny=ny, nz=NZ, nsteps=1).items():
             eng.set(k, v)
         if prog == "dycore":
-            for k, v in dict(synthetic.DYCORE_SCALARS, ch=0.05, rrelax=0.01).items():
+            for k, v in dict(synthetic.DYCORE_SCALARS, **synthetic.PHYS_SCALARS).items():
                 eng.set(k, v)
             arrs = {k: synthetic.field(shape, *v, order="F")
                     for k, v in synthetic.DYCORE_FILLS.items()}
             if entry == "full_step":
-                arrs["tsfc"] = synthetic.field((nx, ny), 13, 300.0, 2.0, order="F")
-                arrs["colm"] = synthetic.field((nx, ny), 14, 300.0, 0.5, order="F")
+                arrs.update({k: synthetic.field((nx, ny), *v, order="F")
+                             for k, v in synthetic.PHYS_FILLS.items()})
             # RK3: stage 1 as the single step (88 B/pt); stages 2-3 also read the base
             # th, u, v, w, p (128 B/pt each)
-            bpp = 88 + 2 * 128 if entry == "rk3_step" else 88
+            abytes = (88 + 2 * 128) * nx * ny * NZ if entry == "rk3_step" else \
+                alg_bytes(entry, nx, ny, NZ)
         else:
             eng.set("coef", 0.1)
             arrs = {"t_old": synthetic.field(shape, 1, 280.0, 10.0, order="F"),
                     "t_new": np.zeros(shape, order="F")}
-            bpp = 24
+            abytes = alg_bytes("hfk0_diffuse_step", nx, ny, NZ)
         for k, a in arrs.items():
             eng.bind(k, a)
             eng.copy_to_device(k)
@@ -232,12 +253,12 @@ def secondary(local, steps=10, warmup=3):
         eng.synchronize()
         ms = e0.elapsed_time(e1) / steps
         pts = nx * ny * NZ
-        out[label] = {"ms_per_step": round(ms, 4), "value": round(pts / (ms / 1e3), 1),
-                      "unit": UNIT, "alg_bytes_per_point": bpp,
-                      "achieved_GBps": round(bpp * pts / (ms / 1e3) / 1e9, 1),
-                      "frac_of_measured_hbm": round(bpp * pts / (ms / 1e3) / 1e9 / hbm, 4),
-                      "frac_of_nominal_8TBps": round(bpp * pts / (ms / 1e3) / 1e9 / 8000.0, 4),
-                      "steps": steps}
+        gbs = abytes / (ms / 1e3) / 1e9
+        out[label] = {"entry": entry, "ms_per_step": round(ms, 4),
+                      "value": round(pts / (ms / 1e3), 1), "unit": UNIT,
+                      "alg_bytes_per_step": abytes, "achieved_GBps": round(gbs, 1),
+                      "frac_of_measured_hbm": round(gbs / hbm, 4),
+                      "frac_of_nominal_8TBps": round(gbs / 8000.0, 4), "steps": steps}
         eng.close()
         del arrs
     return out
@@ -245,27 +266,34 @@ def secondary(local, steps=10, warmup=3):
 
 def cpu_baseline_port(seconds_budget=20.0):
     """The C restatement (oracle/, KIJ storage, OpenMP over j on every host core) timed on
-    a bounded sample of the same workload: whole 512x512x58 dycore steps."""
+    a bounded sample of the same workload: whole full timesteps of a 512x512x58 block
+    (the per-point cost does not depend on the block size; the C4 grid would need ~20 GB
+    of host memory for the oracle's state and scratch)."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle
     from paper_1710_08616_b200 import synthetic
     cores = os.cpu_count() or 1
     oracle.set_threads(cores)
-    a = {k: synthetic.field((NZ, NX, NY), *v, order="F") for k, v in synthetic.DYCORE_FILLS.items()}
-    oracle.dycore_run(1, synthetic.DYCORE_SCALARS, a["rho"], a["th"], a["u"], a["v"], a["w"],
-                      a["p"])  # warm (scratch allocation, page faults)
+    sx, sy = C2_NX, C2_NY
+    a = {k: synthetic.field((NZ, sx, sy), *v, order="F") for k, v in synthetic.DYCORE_FILLS.items()}
+    a.update({k: synthetic.field((sx, sy), *v, order="F") for k, v in synthetic.PHYS_FILLS.items()})
+    prm = dict(synthetic.DYCORE_SCALARS, **synthetic.PHYS_SCALARS)
+
+    def one():
+        oracle.full_run(1, prm, a["rho"], a["th"], a["u"], a["v"], a["w"], a["p"], a["tsfc"],
+                        a["colm"])
+    one()  # warm (scratch allocation, page faults)
     steps, t0 = 0, time.perf_counter()
     while True:
-        oracle.dycore_run(1, synthetic.DYCORE_SCALARS, a["rho"], a["th"], a["u"], a["v"],
-                          a["w"], a["p"])
+        one()
         steps += 1
         el = time.perf_counter() - t0
         if el > seconds_budget / 2 or steps >= 20:
             break
-    return {"value": NX * NY * NZ * steps / el, "unit": UNIT, "cores": cores, "kind": "port",
+    return {"value": sx * sy * NZ * steps / el, "unit": UNIT, "cores": cores, "kind": "port",
             "cpu_model": cpu_model(),
-            "sample": f"{steps} full dycore steps of {NX}x{NY}x{NZ} (oracle/hfb_oracle.c, "
-                      f"KIJ order, OpenMP {cores} threads), {el:.2f} s"}
+            "sample": f"{steps} full timesteps (full_step) of a {sx}x{sy}x{NZ} block "
+                      f"(oracle/hfb_oracle.c, KIJ order, OpenMP {cores} threads), {el:.2f} s"}
 
 
 def bench_ours(args):
@@ -280,9 +308,11 @@ def bench_ours(args):
     if n not in GRIDS:
         raise SystemExit("--gpus must be 1, 2, 4 or 8")
     px, py = GRIDS[n]
-    # HFB_BENCH_ONE_GPU=1 (testing only): every rank on cuda:0, gloo for the host-side
+    entry = args.entry
+    physics = entry == "full_step"
+    # --one-gpu-test (testing only): every rank on cuda:0, gloo for the host-side
     # collectives — exercises the multi-rank path (peer transport) on a one-GPU box
-    one_gpu = os.environ.get("HFB_BENCH_ONE_GPU") == "1"
+    one_gpu = args.one_gpu_test
     if one_gpu:
         local = 0
     torch.cuda.set_device(local)
@@ -292,38 +322,51 @@ def bench_ours(args):
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     eng = hfb.Engine("dycore", device=local)
-    # weak scaling (default): a 512 x 512 tile per GPU; --strong: the C4 grid split
-    tnx, tny = (C4_NX, C4_NY) if args.c4_tiles else (NX, NY)  # weak-scaling tile
-    gnx, gny = (C4_NX, C4_NY) if args.strong else (tnx * px, tny * py)
+    # weak scaling (default): a 1581 x 1301 tile per GPU; --strong: the C4 grid split
+    tnx, tny = (C2_NX, C2_NY) if args.tile512 else (NX, NY)  # weak-scaling tile
+    gnx, gny = (NX, NY) if args.strong else (tnx * px, tny * py)
     d = hfb.decomp_init(gnx, gny, NZ, px, py, rank, halo=2)
     decompose(eng, d, n, args.transport, dist)
-    arrs = make_state(eng, d, gnx, gny)
+    arrs = make_state(eng, d, gnx, gny, physics)
     if n > 1 and args.transport == "peer":
         eng.attach_peers()
     for k in arrs:
         eng.copy_to_device(k)
     eng.synchronize()
 
-    # ---- device-resident timed region: K timesteps ------------------------------------
     stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
-    for _ in range(args.warmup):
-        eng.enqueue("dycore_step")
-    eng.synchronize()
 
     def barrier():
         if n > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
+    # ---- warm-up: W steps, extended to >= 0.4 s of back-to-back steps so the timed
+    # region sees the SUSTAINED (power-capped) clock state, not the burst one ------------
+    for _ in range(args.warmup):
+        eng.enqueue(entry)
+    eng.synchronize()
+    w0 = time.perf_counter()
+    for _ in range(args.warmup):
+        eng.enqueue(entry)
+    eng.synchronize()
+    per = (time.perf_counter() - w0) / max(1, args.warmup)
+    extra = max(0, int(0.4 / max(per, 1e-6)) - args.warmup)
+    for _ in range(extra):
+        eng.enqueue(entry)
+    warmup_run = 2 * args.warmup + extra
+    eng.synchronize()
+
+    # ---- device-resident timed region: K timesteps ------------------------------------
     t_ev0 = torch.cuda.Event(enable_timing=True)
     t_ev1 = torch.cuda.Event(enable_timing=True)
     launches = 0
-    with ClockSampler(local) as clocks:  # nvidia-smi running before the region starts
+    with ClockSampler(local, args.smi_ms) as clocks:  # nvidia-smi running before the region
         barrier()
         clocks.start()
         t_ev0.record(stream)
         for _ in range(args.steps):
-            launches += eng.enqueue("dycore_step").native_launches
+            launches += eng.enqueue(entry).native_launches
         t_ev1.record(stream)
         eng.synchronize()
         clocks.stop()
@@ -336,7 +379,7 @@ def bench_ours(args):
     eng.profile(True)
     barrier()
     for _ in range(args.steps):
-        eng.enqueue("dycore_step")
+        eng.enqueue(entry)
     eng.synchronize()
     barrier()
     eng.profile(False)
@@ -354,11 +397,11 @@ def bench_ours(args):
     hbm, src = peaks()
     dom = max(kt, key=lambda k: kt[k][0])
     dom_ms, dom_n = kt[dom]
-    pts_local = int(d.nx) * int(d.ny) * NZ
+    tnx_l, tny_l = int(d.nx), int(d.ny)
     # one step of the tile is one launch (N=1) or the interior launch plus four boundary
     # strips (decomposed, halo exchange overlapped): the kernel's device time per STEP
     # moves the tile's algorithmic bytes
-    alg_bytes = BYTES_PER_POINT[dom] * pts_local
+    abytes = alg_bytes(dom, tnx_l, tny_l, NZ)
     per_step_prof = dom_ms / args.steps
     if dom_n == args.steps:  # the step is this one launch: the timed region's CUDA events
         per_step = ms_local / args.steps  # (launch stream) / launches — conservative, it
@@ -366,44 +409,52 @@ def bench_ours(args):
     else:
         per_step = per_step_prof
         timing = "per-launch events (profiled pass)"
-    achieved = alg_bytes / (per_step / 1e3) / 1e9
+    achieved = abytes / (per_step / 1e3) / 1e9
+    # measured DRAM traffic of this kernel on THIS tile shape (ncu --set full capture,
+    # profiles/traffic.json keyed by "<kernel> <nx>x<ny>x<nz>"); null when not captured
     traffic = None
+    tkey = f"{dom} {tnx_l}x{tny_l}x{NZ}"
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists():
-        traffic = json.loads(tp.read_text()).get(dom)
+        rec = json.loads(tp.read_text()).get(tkey)
+        traffic = rec["dram_bytes"] if isinstance(rec, dict) else None
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": traffic, "kernel": dom,
-                "frac_of_nominal_8TBps": round(achieved / 8000.0, 4),
-                "peak_source": src, "algorithmic_bytes_per_launch": alg_bytes,
+                "frac": round(achieved / hbm, 4), "traffic": traffic, "traffic_key": tkey,
+                "kernel": dom, "frac_of_nominal_8TBps": round(achieved / 8000.0, 4),
+                "peak_source": src, "algorithmic_bytes_per_launch": abytes,
+                "algorithmic_bytes": f"{BYTES_PER_POINT[dom]} B/point x {tnx_l}x{tny_l}x{NZ}"
+                                     + (f" + {BYTES_PER_COLUMN[dom]} B/column x {tnx_l}x{tny_l}"
+                                        if dom in BYTES_PER_COLUMN else ""),
                 "launches_per_step": dom_n // args.steps,
                 "kernel_ms_avg": round(per_step, 5), "timing": timing,
                 "kernel_ms_profiled": round(per_step_prof, 5),
                 "share_of_step": round(min(1.0, per_step_prof / (ms_local / args.steps)), 3),
                 "kernels": {k: {"ms_avg": round(v[0] / args.steps, 5),
-                                "GBps": round(BYTES_PER_POINT[k] * pts_local /
+                                "GBps": round(alg_bytes(k, tnx_l, tny_l, NZ) /
                                               (v[0] / args.steps / 1e3) / 1e9, 1)}
                             for k, v in kt.items()}}
 
     # ---- end to end through the public API with host buffers --------------------------
-    # one e2e step = one call of the program's `main` entry (transferHere copy-in of the six
+    # one e2e step = one call of the program's main entry (transferHere copy-in of the
     # state arrays from pinned host memory, `nsteps` timesteps, copy-out), as the
     # generated host code does (codegen.cpp:570-600)
+    main_entry = "main_full" if physics else "main"
     e2e_nsteps = 100
     eng2 = hfb.Engine("dycore", device=local)
     decompose(eng2, d, n, args.transport, dist)
-    arrs2 = make_state(eng2, d, gnx, gny)
+    arrs2 = make_state(eng2, d, gnx, gny, physics)
     if n > 1 and args.transport == "peer":
         eng2.attach_peers()
     eng2.set("nsteps", e2e_nsteps)
-    eng2.run("main")  # warm-up call
-    arrs2 = make_state(eng2, d, gnx, gny)
+    eng2.run(main_entry)  # warm-up call
+    arrs2 = make_state(eng2, d, gnx, gny, physics)
     eng2.set("nsteps", e2e_nsteps)
     e2e_calls = max(1, min(3, args.steps // 10))
     xb0 = eng2.transfer_bytes()
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_calls):
-        eng2.run("main")
+        eng2.run(main_entry)
     t1 = time.perf_counter()
     xb1 = eng2.transfer_bytes()
     e2e_s = t1 - t0
@@ -411,41 +462,50 @@ def bench_ours(args):
         t = torch.tensor([e2e_s], device="cpu" if one_gpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    # bytes the runtime actually moved per call (rank 0's tile): the six fields in; out,
-    # the five the steps rewrote (rho is untouched on the device, so its copy-out is a
-    # no-op: host and device already hold the same bytes)
+    # bytes the runtime actually moved per call (rank 0's tile): every state field in; out,
+    # the ones the steps rewrote (rho and tsfc are untouched on the device, so their
+    # copy-out is a no-op: host and device already hold the same bytes)
     h2d = (xb1[0] - xb0[0]) // e2e_calls
     d2h = (xb1[1] - xb0[1]) // e2e_calls
     e2e = {"value": pts_step * e2e_nsteps * e2e_calls / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-           "step": f"one `main` call through the C ABI: copy-in of the 6 pinned host "
-                   f"fields, {e2e_nsteps} timesteps, copy-out", "timesteps_per_step": e2e_nsteps,
-           "calls": e2e_calls}
+           "step": f"one `{main_entry}` call through the C ABI: copy-in of the {len(arrs2)} "
+                   f"pinned host fields, {e2e_nsteps} timesteps, copy-out",
+           "timesteps_per_step": e2e_nsteps, "calls": e2e_calls}
     halo = eng.halo_bytes()
     eng2.close()
     eng.close()
 
     if rank == 0:
+        what = ("full timestep (dycore + HE-VI + column physics)" if physics
+                else "dycore step (advection + HE-VI)")
+        if args.strong:
+            wl = f"{what} {NX}x{NY}x{NZ} split over {n} GPU(s) (BASELINE configs[3], strong)"
+        elif args.tile512:
+            wl = f"{what} {tnx}x{tny}x{NZ} per GPU (BASELINE configs[1] grid)"
+        elif n == 1:
+            wl = f"{what} {NX}x{NY}x{NZ} on 1 GPU (north_star; BASELINE configs[3] at N=1)"
+        else:
+            wl = f"{what} {tnx}x{tny}x{NZ} per GPU (BASELINE configs[4], weak)"
         out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": n,
                "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
                "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
                "dtype": "f64",
                "data": "synthetic (SplitMix64 fields, SURVEY §8(d))",
-               "config": {"workload": (f"dycore+HE-VI {C4_NX}x{C4_NY}x{NZ} split over {n} GPU(s) "
-                                       "(BASELINE configs[3], strong)") if args.strong else
-                          (f"dycore+HE-VI {tnx}x{tny}x{NZ} per GPU (BASELINE configs[4], weak)"
-                           if args.c4_tiles else
-                           f"dycore+HE-VI {NX}x{NY}x{NZ} per GPU (BASELINE configs[1])"),
+               "config": {"workload": wl, "entry": entry,
                           "global_grid": [gnx, gny, NZ], "decomposition": f"{px}x{py}",
                           "transport": args.transport if n > 1 else None,
-                          "l2": f"inputs larger than L2: {6 * pts_local * 8 / 2**30:.2f} GiB "
-                                f"state + {5 * pts_local * 8 / 2**30:.2f} GiB outputs per step "
-                                f"and GPU vs 126 MB L2"},
+                          "warmup_steps_run": warmup_run,
+                          "timed_region_ms": round(ms, 3),
+                          "l2": f"inputs larger than L2: "
+                                f"{6 * tnx_l * tny_l * NZ * 8 / 2**30:.2f} GiB state + "
+                                f"{5 * tnx_l * tny_l * NZ * 8 / 2**30:.2f} GiB outputs per "
+                                f"step and GPU vs 126 MB L2 (no flush needed)"},
                "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
                "clocks": clocks.summary(), "halo_bytes": halo}
         if n > 1:  # rank 0's halo traffic (sent + received) per step and its rate
-            hps = halo / (args.warmup + args.steps)
+            hps = halo / (warmup_run + 2 * args.steps)
             out["halo"] = {"bytes_per_step_rank0": int(hps),
                            "GBps_rank0": round(hps / (ms / args.steps / 1e3) / 1e9, 2)}
         out["cpu_baseline"] = cpu_baseline_port() if n == 1 else None
@@ -459,10 +519,11 @@ def bench_ours(args):
 def bench_reference(args):
     """The reference's own CPU path: its binary64 interpreter (oracle/_ref/hft_ref, compiled
     from /root/reference/proj/src) running this repo's dycore app (apps/dycore, the
-    reference dialect) through run_reference. It is single-threaded by design
-    (SPEC.md:476), so every host core runs one independent interpreter over its own
-    SAMPLE_NX x SAMPLE_NY x 58 column block of the workload; a step is one timestep of
-    all blocks."""
+    reference dialect) through run_reference, entry main_full with nsteps = 1 (the full
+    timestep). It is single-threaded by design, so every host core runs one
+    independent interpreter over its own SAMPLE_NX x SAMPLE_NY x 58 column block of the
+    workload. A step's time is the slowest interpreter's own run_reference time
+    (the harness times the call; process start-up and .h90 parsing are excluded)."""
     rank, world, local = dist_env()
     if rank != 0:
         return
@@ -472,39 +533,50 @@ def bench_reference(args):
     from paper_1710_08616_b200 import synthetic
     cores = os.cpu_count() or 1
     sx, sy = 16, 16
+    physics = args.entry == "full_step"
     tmp = Path(tempfile.mkdtemp(prefix="hftref_"))
     scen = tmp / "dycore.sc"
     lines = [f"source {ROOT / 'apps/dycore/dyn_state.h90'}",
-             f"source {ROOT / 'apps/dycore/dycore.h90'}", "mode ref", "entry main",
+             f"source {ROOT / 'apps/dycore/dycore.h90'}", "mode ref",
+             f"entry {'main_full' if physics else 'main'}",
              "max_steps 2000000000", f"int dyn_state nx {sx}", f"int dyn_state ny {sy}",
              f"int dyn_state nz {NZ}", "int dyn_state nsteps 1"]
-    lines += [f"real dyn_state {k} {float(v).hex()}" for k, v in synthetic.DYCORE_SCALARS.items()]
+    scal = dict(synthetic.DYCORE_SCALARS, **(synthetic.PHYS_SCALARS if physics else {}))
+    fills = dict(synthetic.DYCORE_FILLS, **(synthetic.PHYS_FILLS if physics else {}))
+    lines += [f"real dyn_state {k} {float(v).hex()}" for k, v in scal.items()]
     lines += [f"fill dyn_state {k} {s} {float(o).hex()} {float(c).hex()}"
-              for k, (s, o, c) in synthetic.DYCORE_FILLS.items()]
+              for k, (s, o, c) in fills.items()]
     scen.write_text("\n".join(lines) + "\n")
 
     def one_step():
-        procs = [subprocess.Popen([str(hft), str(scen)], stdout=subprocess.DEVNULL)
+        procs = [subprocess.Popen([str(hft), str(scen)], stdout=subprocess.PIPE, text=True)
                  for _ in range(cores)]
+        secs = []
         for p in procs:
-            if p.wait() != 0:
+            out, _ = p.communicate()
+            if p.returncode != 0:
                 raise RuntimeError("reference interpreter failed")
+            rec = [json.loads(ln) for ln in out.splitlines() if ln.startswith('{"seconds"')]
+            secs.append(rec[-1]["seconds"])
+        return max(secs)  # the interpreters run concurrently: the slowest one's run time
 
     for _ in range(args.warmup):
         one_step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        one_step()
-    el = time.perf_counter() - t0
+    el = sum(one_step() for _ in range(args.steps))
     value = cores * sx * sy * NZ * args.steps / el
     sample = (f"{cores} concurrent reference interpreters (run_reference, 1 thread each), "
-              f"each one timestep of a {sx}x{sy}x{NZ} block of the {NX}x{NY}x{NZ} workload")
+              f"each one {'full timestep (main_full)' if physics else 'dycore step'} of its "
+              f"own {sx}x{sy}x{NZ} block of the {NX}x{NY}x{NZ} workload; time = the slowest "
+              f"interpreter's run_reference call (process start and .h90 parsing excluded)")
     out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (SplitMix64 fields, SURVEY §8(d))", "impl": "reference",
-           "config": {"workload": f"dycore+HE-VI {NX}x{NY}x{NZ} per GPU (BASELINE configs[1])"},
+           "config": {"workload": f"{'full timestep' if physics else 'dycore step'} "
+                                  f"{NX}x{NY}x{NZ} (north_star), sampled as {cores} blocks of "
+                                  f"{sx}x{sy}x{NZ}", "entry": args.entry,
+                      "sample": f"{cores} x {sx}x{sy}x{NZ} blocks"},
            "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cores,
                             "kind": "reference", "sample": sample},
            "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -513,19 +585,30 @@ def bench_reference(args):
 
 
 def main():
+    bad = sorted(k for k in os.environ if k.startswith("HFB_"))
+    if bad:
+        raise SystemExit(f"bench.py refuses to run with HFB_* environment variables set "
+                         f"({', '.join(bad)}): every switch is a command-line flag")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--entry", default="full_step", choices=["full_step", "dycore_step"],
+                    help="the timestep: full (dycore + column physics, default) or dycore only")
     ap.add_argument("--strong", action="store_true",
-                    help="strong scaling of the 1581x1301x58 grid (default: weak, 512x512 per GPU)")
-    ap.add_argument("--c4-tiles", action="store_true",
-                    help="weak scaling with a 1581x1301x58 tile per GPU (BASELINE configs[4])")
+                    help="strong scaling of the 1581x1301x58 grid (default: weak, a "
+                         "1581x1301x58 tile per GPU)")
+    ap.add_argument("--tile512", action="store_true",
+                    help="a 512x512x58 tile per GPU (BASELINE configs[1] grid)")
+    ap.add_argument("--c4-tiles", action="store_true", help=argparse.SUPPRESS)  # the default
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="halo exchange for N > 1 (peer: P2P stores + flags; nccl: send/recv)")
     ap.add_argument("--no-secondary", action="store_true",
                     help="skip the single-GPU timings of the other BASELINE configs")
+    ap.add_argument("--one-gpu-test", action="store_true",
+                    help="testing only: every rank on cuda:0 (multi-rank path on one GPU)")
+    ap.add_argument("--smi-ms", type=int, default=20, help="nvidia-smi sampling interval")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -231,6 +231,19 @@ hfb_status hfb_peer_stats(hfb_ctx* ctx, int64_t* pushes, int64_t* handoffs);
  * partials are assembled in global order on every rank). */
 hfb_status hfb_set_reduction_order(hfb_ctx* ctx, int ordered);
 
+/* --- per-context options (explicit; the library reads no environment variables) ------
+ * "variant": which kernels run the dycore steps — "product" (default: the fused
+ *   warp-specialised step), "generic" (portable kernels), "split" (advect + acoustic
+ *   kernels), "single_role" (fused, one role per warp); "tma" and "ws2" (measured-slower
+ *   alternatives) exist only in the A/B build libhfb_variants.so, elsewhere HFB_CONFIG.
+ * "overlap": "1" (default) overlaps the halo exchange with the interior columns, "0"
+ *   serialises (both orders are bit-identical).
+ * "debug_skip": A/B build only, timing experiments (1 = no advection, 2 = no acoustic).
+ * Every variant gives bit-identical results. */
+hfb_status hfb_set_option(hfb_ctx* ctx, const char* key, const char* value);
+/* 1 in the A/B build (libhfb_variants.so), 0 in the product library */
+int hfb_variants_build(void);
+
 /* --- state images and scenario files ------------------ */
 /* HFBSTAT1 image of the context's MachineState: program, every scalar (with its set
  * flag), every bound array in the reference's ArrayValue order (row-major, last subscript

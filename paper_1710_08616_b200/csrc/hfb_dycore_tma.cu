@@ -460,7 +460,8 @@ bool make_box_map(CUtensorMap* m, const double* origin, Grid3 g, int64_t nj, int
 
 cudaError_t launch_dycore_step_tma(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                    int64_t nj, const DynConst& c, const Span& sp,
-                                   cudaStream_t s, const PhysArgs* phys, const DynIn* base) {
+                                   cudaStream_t s, const PhysArgs* phys, const DynIn* base,
+                                   int debug_skip) {
   if (sp.ihi < sp.ilo || sp.jhi < sp.jlo) return cudaSuccess;
   if (!dycore_step_tmem_fits(nz)) return cudaErrorInvalidValue;
   if (phys && base) return cudaErrorInvalidValue;
@@ -485,7 +486,6 @@ cudaError_t launch_dycore_step_tma(const DynIn& in, const DynOut& out, Grid3 g, 
     cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
   }
-  static const int debug_skip = getenv("HFB_DEBUG_SKIP") ? atoi(getenv("HFB_DEBUG_SKIP")) : 0;
   TmaStepArgs a{out, g, static_cast<int>(nz), debug_skip,
                 phys ? phys->tsfc : nullptr, phys ? phys->colm : nullptr,
                 phys ? phys->dt_rrelax : 0.0, phys ? phys->dt_ch : 0.0,

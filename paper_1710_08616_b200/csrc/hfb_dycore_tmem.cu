@@ -31,6 +31,13 @@
 
 namespace hfb {
 
+// timing experiments (A/B build only): skip one role's arithmetic
+#ifdef HFB_VARIANTS
+#define HFB_SKIP(a, bit) (((a).debug_skip & (bit)) != 0)
+#else
+#define HFB_SKIP(a, bit) false
+#endif
+
 namespace {
 
 constexpr int kTX = 32, kTY = 4, kThreads = kTX * kTY;
@@ -819,7 +826,7 @@ __global__ void __launch_bounds__(kWsThreads, 2)
     const double* Vp = S + kFOffV + (row + 1) * kVW + lane;
     const double vj = Vp[0], vjm1 = Vp[-kVW];
     const double wk = S[kFOffW + row * kSW + lane];
-    if (acoustic && (a.debug_skip & 2) == 0) {
+    if (acoustic && !HFB_SKIP(a, 2)) {
       const double* Pp = S + kFOffP + (row + 1) * kPW + (lane + 2);
       const double pk = Pp[0], pe = Pp[1], pw = Pp[-1], pnn = Pp[kPW], psth = Pp[-kPW];
       const double rhok = S[kFOffRho + row * kSW + lane];
@@ -879,7 +886,7 @@ __global__ void __launch_bounds__(kWsThreads, 2)
       rho_prev = rhok;
       ps_prev = psk;
       if (kRK) wb_prev = bcur.w;
-    } else if (!acoustic && (a.debug_skip & 1) == 0) {
+    } else if (!acoustic && !HFB_SKIP(a, 1)) {
       const double* T0 = S + kFOffTh + thc;
       const double tkp1 =
           (kMid || kk + 1 <= nz) ? ring[s1 * kFStageDoubles + kFOffTh + thc] : 0.0;
@@ -1019,7 +1026,7 @@ __global__ void __launch_bounds__(kWsThreads, 2)
 cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                   int64_t nj, const DynConst& c, const Span& sp,
                                   cudaStream_t s, const PhysArgs* phys, const DynIn* base,
-                                  const RemoteHalo* remote) {
+                                  const RemoteHalo* remote, int debug_skip) {
   if (sp.ihi < sp.ilo || sp.jhi < sp.jlo) return cudaSuccess;
   if (!dycore_step_tmem_fits(nz)) return cudaErrorInvalidValue;
   if (phys && base) return cudaErrorInvalidValue;
@@ -1038,7 +1045,9 @@ cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, i
     cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
   }
-  static const int debug_skip = getenv("HFB_DEBUG_SKIP") ? atoi(getenv("HFB_DEBUG_SKIP")) : 0;
+#ifndef HFB_VARIANTS
+  debug_skip = 0;
+#endif
   StepTmemArgs a{in, out, g, static_cast<int>(nz), debug_skip,
                  phys ? phys->tsfc : nullptr, phys ? phys->colm : nullptr,
                  phys ? phys->dt_rrelax : 0.0, phys ? phys->dt_ch : 0.0,

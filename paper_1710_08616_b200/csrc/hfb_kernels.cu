@@ -223,14 +223,8 @@ cudaError_t launch_diffusion(const double* t_old, double* out1, double* out2, Gr
   int kchunk = static_cast<int>((nz + kchunks - 1) / kchunks);
   kchunks = static_cast<int>((nz + kchunk - 1) / kchunk);
   DiffArgs a{t_old, out1, out2, g, static_cast<int>(nz), kchunk, coef, sp};
-  static const int chunk = getenv("HFB_DIFF_CHUNK") ? atoi(getenv("HFB_DIFF_CHUNK")) : 2;
   dim3 grid = span_grid(sp, block, kchunks);
-  switch (chunk) {
-    case 1: k_diffusion<1><<<grid, block, 0, s>>>(a); break;
-    case 4: k_diffusion<4><<<grid, block, 0, s>>>(a); break;
-    case 8: k_diffusion<8><<<grid, block, 0, s>>>(a); break;
-    default: k_diffusion<2><<<grid, block, 0, s>>>(a); break;
-  }
+  k_diffusion<2><<<grid, block, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -126,18 +126,22 @@ cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, i
                                   int64_t nj, const DynConst& c, const Span& sp,
                                   cudaStream_t s, const PhysArgs* phys = nullptr,
                                   const DynIn* base = nullptr,
-                                  const RemoteHalo* remote = nullptr);
-// the same step fed by TMA through mbarriers (hfb_dycore_tma.cu): measured slower than the
-// cp.async-fed launch_dycore_step_ws, kept as the HFB_TMA_STEP=1 variant
+                                  const RemoteHalo* remote = nullptr, int debug_skip = 0);
+#ifdef HFB_VARIANTS
+// Measured-slower alternatives, compiled only into the A/B build (make variants ->
+// libhfb_variants.so; selected with hfb_set_option(ctx, "variant", "tma" | "ws2")).
+// debug_skip (timing experiments): 1 = no advection, 2 = no acoustic arithmetic.
+// the same step fed by TMA through mbarriers (hfb_dycore_tma.cu)
 cudaError_t launch_dycore_step_tma(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                    int64_t nj, const DynConst& c, const Span& sp,
-                                   cudaStream_t s, const PhysArgs* phys = nullptr,
-                                   const DynIn* base = nullptr);
+                                   cudaStream_t s, const PhysArgs* phys, const DynIn* base,
+                                   int debug_skip);
 // two columns per thread, one CTA (32 x 8 tile) per SM (hfb_dycore_ws2.cu)
 cudaError_t launch_dycore_step_ws2(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                    int64_t nj, const DynConst& c, const Span& sp,
-                                   cudaStream_t s, const PhysArgs* phys = nullptr,
-                                   const DynIn* base = nullptr);
+                                   cudaStream_t s, const PhysArgs* phys, const DynIn* base,
+                                   int debug_skip);
+#endif
 // standalone column physics on the current state (th updated in place)
 cudaError_t launch_column_physics(const double* rho, double* th, const double* u,
                                   const double* v, Grid3 g, int64_t nz, const DynConst& c,

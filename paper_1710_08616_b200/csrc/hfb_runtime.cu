@@ -312,18 +312,21 @@ struct hfb_ctx {
   // the stream step kernels go to (nullptr: `stream`); exchange_and_run points it at
   // `comm` for the boundary strips, which then overlap the interior launch
   cudaStream_t run_stream = nullptr;
-  bool overlap = getenv("HFB_NO_OVERLAP") == nullptr;
+  bool overlap = true;  // hfb_set_option(ctx, "overlap", "0") serialises
   // CUDA graph cache for hfb_run_graph
   cudaGraphExec_t graph_exec = nullptr;
   std::string graph_key;
   hfb_launch_stats graph_stats{};
   std::map<std::string, int> graph_cur0, graph_cur1;
-  // A/B switches: portable kernels only / the two-kernel (advect + acoustic) split
-  bool force_generic = getenv("HFB_GENERIC_KERNELS") != nullptr;
-  bool force_split = getenv("HFB_SPLIT_STEP") != nullptr;
-  bool force_single_role = getenv("HFB_SINGLE_ROLE") != nullptr;
-  bool force_tma = getenv("HFB_TMA_STEP") != nullptr;
-  bool force_ws2 = getenv("HFB_WS2_STEP") != nullptr;
+  // kernel variant (hfb_set_option "variant"; explicit per context, never from the
+  // environment): the portable kernels only / the two-kernel (advect + acoustic) split /
+  // the single-role fused kernel; tma / ws2 exist only in the A/B build (make variants)
+  bool force_generic = false;
+  bool force_split = false;
+  bool force_single_role = false;
+  bool force_tma = false;
+  bool force_ws2 = false;
+  int debug_skip = 0;  // A/B build only: 1 = no advection, 2 = no acoustic (timing)
   // per-kernel CUDA-event timing (hfb_profile)
   bool prof = false;
   bool capturing = false;
@@ -943,9 +946,16 @@ void column_physics(hfb_ctx* c, Stats& st) {
 cudaError_t launch_step(hfb_ctx* c, const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                         int64_t nj, const DynConst& k, const Span& sp, cudaStream_t s,
                         const PhysArgs* phys = nullptr, const DynIn* base = nullptr) {
-  if (c->force_ws2) return launch_dycore_step_ws2(in, out, g, nz, nj, k, sp, s, phys, base);
-  return c->force_tma ? launch_dycore_step_tma(in, out, g, nz, nj, k, sp, s, phys, base)
-                      : launch_dycore_step_ws(in, out, g, nz, nj, k, sp, s, phys, base);
+#ifdef HFB_VARIANTS
+  if (c->force_ws2)
+    return launch_dycore_step_ws2(in, out, g, nz, nj, k, sp, s, phys, base, c->debug_skip);
+  if (c->force_tma)
+    return launch_dycore_step_tma(in, out, g, nz, nj, k, sp, s, phys, base, c->debug_skip);
+  return launch_dycore_step_ws(in, out, g, nz, nj, k, sp, s, phys, base, nullptr,
+                               c->debug_skip);
+#else
+  return launch_dycore_step_ws(in, out, g, nz, nj, k, sp, s, phys, base);
+#endif
 }
 
 void dycore_step(hfb_ctx* c, Stats& st, bool with_physics = false) {
@@ -2301,6 +2311,53 @@ const char* hfb_program_module(hfb_ctx* c) {
 }
 
 const char* hfb_program_name(hfb_ctx* c) { return c && c->app ? c->app->app.c_str() : nullptr; }
+
+hfb_status hfb_set_option(hfb_ctx* c, const char* key, const char* value) {
+  return guarded([&] {
+    if (!c) fail(HFB_CONFIG, "null context");
+    const std::string k = key ? key : "", v = value ? value : "";
+    if (k == "variant") {
+      c->force_generic = v == "generic";
+      c->force_split = v == "split";
+      c->force_single_role = v == "single_role";
+      c->force_tma = v == "tma";
+      c->force_ws2 = v == "ws2";
+      const bool known = v == "product" || v == "generic" || v == "split" ||
+                         v == "single_role" || v == "tma" || v == "ws2";
+      if (!known) {
+        c->force_tma = c->force_ws2 = false;
+        fail(HFB_CONFIG, "unknown kernel variant '%s' (product, generic, split, single_role, "
+             "tma, ws2)", v.c_str());
+      }
+#ifndef HFB_VARIANTS
+      if (c->force_tma || c->force_ws2) {
+        c->force_tma = c->force_ws2 = false;
+        fail(HFB_CONFIG, "kernel variant '%s' is not compiled into this library (A/B build: "
+             "make -C csrc variants -> libhfb_variants.so)", v.c_str());
+      }
+#endif
+    } else if (k == "overlap") {
+      if (v != "0" && v != "1") fail(HFB_CONFIG, "option overlap takes 0 or 1, got '%s'", v.c_str());
+      c->overlap = v == "1";
+    } else if (k == "debug_skip") {
+#ifdef HFB_VARIANTS
+      c->debug_skip = std::atoi(v.c_str());
+#else
+      fail(HFB_CONFIG, "option debug_skip exists only in the A/B build (libhfb_variants.so)");
+#endif
+    } else {
+      fail(HFB_CONFIG, "unknown option '%s' (variant, overlap, debug_skip)", k.c_str());
+    }
+  });
+}
+
+int hfb_variants_build(void) {
+#ifdef HFB_VARIANTS
+  return 1;
+#else
+  return 0;
+#endif
+}
 
 hfb_status hfb_set_reduction_order(hfb_ctx* c, int ordered) {
   return guarded([&] {

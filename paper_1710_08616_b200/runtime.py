@@ -23,8 +23,10 @@ from pathlib import Path
 import numpy as np
 
 PKG = Path(__file__).resolve().parent
-# HFB_LIB: another build of the library (A/B timing of kernel variants)
+# HFB_LIB: another build of the library — the A/B build libhfb_variants.so (make -C csrc
+# variants), which adds the measured-slower kernel variants; bench.py refuses it
 LIB_PATH = Path(os.environ["HFB_LIB"]) if os.environ.get("HFB_LIB") else PKG / "libhfb.so"
+VARIANTS_LIB = PKG / "libhfb_variants.so"
 CSRC = PKG / "csrc"
 
 KINDS = {0: "ok", 10: "config", 15: "runtime", 16: "residency", 17: "race", 18: "validation",
@@ -45,6 +47,7 @@ EXPORTS = [
     "hfb_set_reduction_order", "hfb_program_name", "hfb_program_module", "hfb_plugin_prepare",
     "hfb_plugin_written", "hfb_plugin_view", "hfb_plugin_scratch", "hfb_plugin_host", "hfb_plugin_host_ref",
     "hfb_peer_export", "hfb_peer_attach", "hfb_peer_stats", "hfb_transfer_bytes",
+    "hfb_set_option", "hfb_variants_build",
 ]
 
 # module of each built-in program (the apps' state modules)
@@ -147,6 +150,8 @@ def lib():
         L.hfb_peer_attach.argtypes = [P, c.c_int, c.POINTER(P), c.POINTER(c.c_size_t)]
         L.hfb_peer_stats.argtypes = [P, c.POINTER(i64), c.POINTER(i64)]
         L.hfb_transfer_bytes.argtypes = [P, c.POINTER(i64), c.POINTER(i64)]
+        L.hfb_set_option.argtypes = [P, S, S]
+        L.hfb_variants_build.restype = c.c_int
         _lib = L
     return _lib
 
@@ -284,6 +289,11 @@ class Engine:
         flat = np.ctypeslib.as_array(p, shape=(count,))
         strides = tuple(8 * (st[d] if shape[d] > 1 else 1) for d in range(rank.value))
         return np.lib.stride_tricks.as_strided(flat, shape=shape, strides=strides)
+
+    def set_option(self, key, value):
+        """Per-context option (hfb_set_option): "variant" (product | generic | split |
+        single_role; tma | ws2 in the A/B build), "overlap" ("0" | "1")."""
+        _check(lib().hfb_set_option(self._h, _b(key), _b(str(value))))
 
     def set_reduction_order(self, ordered=True):
         """Ordered reductions: bit-identical to the reference's acc-simulated order
@@ -429,6 +439,11 @@ class Group:
 
     def __exit__(self, *a):
         self.close()
+
+
+def variants_build():
+    """True when the loaded library is the A/B build (libhfb_variants.so)."""
+    return bool(lib().hfb_variants_build())
 
 
 def nccl_unique_id():

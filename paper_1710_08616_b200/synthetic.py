@@ -47,3 +47,6 @@ DYCORE_SCALARS = {"dt": 0.1, "rdx": 2.0, "rdy": 2.0, "rdz": 20.0, "cs2": 1.0,
                   "grav": 0.0327, "th0": 300.0}
 DYCORE_FILLS = {"rho": (7, 1.0, 0.1), "th": (8, 300.0, 1.0), "u": (9, -0.01, 0.02),
                 "v": (10, -0.01, 0.02), "w": (11, -0.002, 0.004), "p": (12, -0.005, 0.01)}
+# column physics of the full timestep (dyn_state.tsfc / colm, dycore.h90 column_physics)
+PHYS_SCALARS = {"ch": 0.05, "rrelax": 0.01}
+PHYS_FILLS = {"tsfc": (13, 300.0, 2.0), "colm": (14, 300.0, 0.5)}

@@ -51,7 +51,7 @@ def global_extent(case):
     return case.ints["nx"], case.ints["ny"]
 
 
-def run_decomposed(case, px, py, entry=None, halo=2, ordered=False):
+def run_decomposed(case, px, py, entry=None, halo=2, ordered=False, options=None):
     entry = entry or APPS[case.app].entry
     garr = make_inputs(case)
     gnx, gny = global_extent(case)
@@ -61,6 +61,8 @@ def run_decomposed(case, px, py, entry=None, halo=2, ordered=False):
         d = hfb.decomp_init(gnx, gny, nz, px, py, r, halo=halo)
         eng = hfb.Engine(APPS[case.app].prog)
         eng.set_decomposition(d)
+        for k, v in (options or {}).items():
+            eng.set_option(k, v)
         if ordered:
             eng.set_reduction_order(True)
         ints = tile_ints(case, d)
@@ -117,11 +119,10 @@ def test_full_step_decomposed_equals_single():
         assert bits_equal(out[k], ref[k]), k
 
 
-def test_dycore_decomposed_ragged_tiles_generic_kernel(monkeypatch):
+def test_dycore_decomposed_ragged_tiles_generic_kernel():
     """Uneven tiles (remainders) and the portable kernel under decomposition."""
-    monkeypatch.setenv("HFB_GENERIC_KERNELS", "1")
     case = dyc(37, 23, 80, 2)
-    garr, out, _, _, _ = run_decomposed(case, 3, 3)
+    garr, out, _, _, _ = run_decomposed(case, 3, 3, options={"variant": "generic"})
     ref = {k: v.copy() for k, v in garr.items()}
     run_oracle(case, ref)
     for k in ("th", "u", "v", "w", "p"):
@@ -178,12 +179,10 @@ def test_reduction_decomposed_ordered_bit_exact(px, py):
 
 @pytest.mark.parametrize("overlap", [True, False])
 @pytest.mark.parametrize("app", ["dycore", "dycore_full", "diffusion"])
-def test_overlapped_exchange_equals_serial(monkeypatch, app, overlap):
+def test_overlapped_exchange_equals_serial(app, overlap):
     """Decomposed stencil steps run the interior columns while the halos travel, then the
-    boundary strips (HFB_NO_OVERLAP=1: exchange first, one full launch). Both are
+    boundary strips (option overlap=0: exchange first, one full launch). Both are
     bit-identical to the undecomposed oracle."""
-    if not overlap:
-        monkeypatch.setenv("HFB_NO_OVERLAP", "1")
     if app == "diffusion":
         case = Case("d", "diffusion", dict(nx=70, ny=45, nz=20, nsteps=3), dict(coef=0.1),
                     {"t_old": (1, 280.0, 10.0)}, unset=["t_new"])
@@ -193,7 +192,7 @@ def test_overlapped_exchange_equals_serial(monkeypatch, app, overlap):
         fills = dict(DYCORE_FILLS, **PHYS_FILLS) if app == "dycore_full" else dict(DYCORE_FILLS)
         case = Case("x", app, dict(nx=70, ny=45, nz=20, nsteps=2), reals, fills)
         names = APPS[app].outputs
-    garr, out, _, stats, _ = run_decomposed(case, 2, 2)
+    garr, out, _, stats, _ = run_decomposed(case, 2, 2, options={"overlap": int(overlap)})
     ref = {k: v.copy() for k, v in garr.items()}
     run_oracle(case, ref)
     for k in names:

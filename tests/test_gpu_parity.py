@@ -18,10 +18,12 @@ from golden_io import bits_equal, decl, load_golden, make_inputs, run_oracle
 pytestmark = pytest.mark.gpu
 
 
-def run_engine(case, arrs, entry=None):
+def run_engine(case, arrs, entry=None, options=None):
     app = APPS[case.app]
     entry = entry or app.entry
     with hfb.Engine(app.prog) as eng:
+        for k, v in (options or {}).items():
+            eng.set_option(k, v)
         for k, v in case.ints.items():
             eng.set(k, int(v))
         for k, v in case.reals.items():
@@ -55,11 +57,11 @@ def test_golden_case(case, order):
     assert stats.native_launches > 0
 
 
-def _oracle_vs_gpu(case, order="C"):
+def _oracle_vs_gpu(case, order="C", options=None):
     a_gpu = make_inputs(case, order=order)
     a_ora = {k: v.copy(order="A") for k, v in a_gpu.items()}
     run_oracle(case, a_ora)
-    run_engine(case, a_gpu)
+    run_engine(case, a_gpu, options=options)
     for name in APPS[case.app].outputs:
         if name in a_gpu:
             assert bits_equal(a_gpu[name], a_ora[name]), f"{case.name}: {name} differs"
@@ -152,18 +154,17 @@ def test_reduction_large_tolerance():
     assert abs(scal["total"] - ref["total"]) <= 1e-12 * abs(ref["total"])
 
 
-def test_split_step_matches(monkeypatch):
-    """The two-kernel step (advect + TMEM acoustic; HFB_SPLIT_STEP=1) gives the same bits."""
-    monkeypatch.setenv("HFB_SPLIT_STEP", "1")
+def test_split_step_matches():
+    """The two-kernel step (advect + TMEM acoustic; variant split) gives the same bits."""
     _oracle_vs_gpu(Case("dycore_70x45x58_s2", "dycore", dict(nx=70, ny=45, nz=58, nsteps=2),
-                        dict(DYCORE_SCALARS), dict(DYCORE_FILLS)))
+                        dict(DYCORE_SCALARS), dict(DYCORE_FILLS)), options={"variant": "split"})
 
 
-def test_full_step_split_path_matches(monkeypatch):
-    """dycore kernels + the standalone column-physics kernel (HFB_SPLIT_STEP=1)."""
-    monkeypatch.setenv("HFB_SPLIT_STEP", "1")
+def test_full_step_split_path_matches():
+    """dycore kernels + the standalone column-physics kernel (variant split)."""
     _oracle_vs_gpu(Case("full_70x45x58_s2", "dycore_full", dict(nx=70, ny=45, nz=58, nsteps=2),
-                        dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS)))
+                        dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS)),
+                   options={"variant": "split"})
 
 
 def test_full_size_full_timestep_c3():
@@ -173,23 +174,53 @@ def test_full_size_full_timestep_c3():
                         dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS)))
 
 
-def test_single_role_fused_matches(monkeypatch):
-    """The single-role fused kernel (HFB_SINGLE_ROLE=1) gives the same bits."""
-    monkeypatch.setenv("HFB_SINGLE_ROLE", "1")
+def test_single_role_fused_matches():
+    """The single-role fused kernel (variant single_role) gives the same bits."""
     _oracle_vs_gpu(Case("dycore_70x45x58_s2", "dycore", dict(nx=70, ny=45, nz=58, nsteps=2),
-                        dict(DYCORE_SCALARS), dict(DYCORE_FILLS)))
+                        dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
+                   options={"variant": "single_role"})
+
+
+def test_ab_variants_not_in_product_library():
+    """The measured-slower variants (tma, ws2) and the timing switches are compiled only
+    into the A/B build; the product library refuses them (no hidden knobs)."""
+    if hfb.variants_build():
+        pytest.skip("running against the A/B build")
+    with hfb.Engine("dycore") as eng:
+        for k, v in (("variant", "tma"), ("variant", "ws2"), ("debug_skip", "1"),
+                     ("variant", "nonsense"), ("no_such_option", "1")):
+            with pytest.raises(hfb.HfbError) as e:
+                eng.set_option(k, v)
+            assert e.value.kind == "config"
 
 
 @pytest.mark.parametrize("app", ["dycore", "dycore_full", "dycore_rk3"])
-@pytest.mark.parametrize("variant", ["HFB_TMA_STEP", "HFB_WS2_STEP"])
-def test_step_variant_matches(monkeypatch, app, variant):
+@pytest.mark.parametrize("variant", ["tma", "ws2"])
+def test_step_variant_matches(app, variant):
     """The measured alternatives of the fused step give the same bits: the TMA-fed twin
-    (HFB_TMA_STEP=1) and the two-columns-per-thread kernel (HFB_WS2_STEP=1)."""
-    monkeypatch.setenv(variant, "1")
+    (tma) and the two-columns-per-thread kernel (ws2). They live in the A/B build
+    (libhfb_variants.so), run here in a child process that loads it."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    lib = hfb.runtime.VARIANTS_LIB
+    if not lib.exists():
+        pytest.skip("A/B build not present (make -C paper_1710_08616_b200/csrc variants)")
+    here = Path(__file__).resolve().parent
+    code = ("import sys; sys.path[:0] = [%r, %r, %r]\n"
+            "import paper_1710_08616_b200 as hfb; assert hfb.variants_build()\n"
+            "from test_gpu_parity import _variant_case, _oracle_vs_gpu\n"
+            "_oracle_vs_gpu(_variant_case(%r), options={'variant': %r})\n"
+            % (str(here.parent), str(here), str(here.parent / "oracle"), app, variant))
+    r = subprocess.run([sys.executable, "-c", code], env=dict(__import__("os").environ,
+                       HFB_LIB=str(lib)), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+def _variant_case(app):
     reals = dict(DYCORE_SCALARS, **PHYS_SCALARS) if app == "dycore_full" else dict(DYCORE_SCALARS)
     fills = dict(DYCORE_FILLS, **PHYS_FILLS) if app == "dycore_full" else dict(DYCORE_FILLS)
-    _oracle_vs_gpu(Case(f"{app}_70x45x58_s2", app, dict(nx=70, ny=45, nz=58, nsteps=2),
-                        reals, fills))
+    return Case(f"{app}_70x45x58_s2", app, dict(nx=70, ny=45, nz=58, nsteps=2), reals, fills)
 
 
 @pytest.mark.parametrize("app", ["dycore", "dycore_rk3"])
@@ -214,27 +245,50 @@ def test_division_fast_path_edges(app, edge):
                         reals, fills))
 
 
-def test_generic_diffusion_kernel_matches(monkeypatch):
-    """The L1-cached diffusion kernel (HFB_GENERIC_KERNELS=1; the product kernel stages
-    planes in shared memory, hfb_diffusion.cu) gives the same bits."""
-    monkeypatch.setenv("HFB_GENERIC_KERNELS", "1")
+def test_generic_diffusion_kernel_matches():
+    """The L1-cached diffusion kernel (variant generic; the product kernel stages planes
+    in shared memory, hfb_diffusion.cu) gives the same bits."""
     _oracle_vs_gpu(Case("diffusion_333x77x58_s3", "diffusion", dict(nx=333, ny=77, nz=58, nsteps=3),
-                        dict(coef=0.1), {"t_old": (1, 280.0, 10.0)}, unset=["t_new"]))
+                        dict(coef=0.1), {"t_old": (1, 280.0, 10.0)}, unset=["t_new"]),
+                   options={"variant": "generic"})
 
 
-def test_generic_kernels_match(monkeypatch):
-    """The portable acoustic kernel (HFB_GENERIC_KERNELS=1) gives the same bits."""
-    monkeypatch.setenv("HFB_GENERIC_KERNELS", "1")
+def test_generic_kernels_match():
+    """The portable acoustic kernel (variant generic) gives the same bits."""
     _oracle_vs_gpu(Case("dycore_70x45x58_s2", "dycore", dict(nx=70, ny=45, nz=58, nsteps=2),
-                        dict(DYCORE_SCALARS), dict(DYCORE_FILLS)))
+                        dict(DYCORE_SCALARS), dict(DYCORE_FILLS)), options={"variant": "generic"})
 
 
-@pytest.mark.parametrize("nx,ny", [(512, 512)])
+@pytest.mark.parametrize("nx,ny", [(512, 512), (1581, 1301)])
 def test_full_size_dycore_step(nx, ny):
-    """BASELINE configs C2 / C4: one full step, bit-exact against the oracle."""
+    """BASELINE configs C2 / C4: one dycore step, bit-exact against the oracle."""
     case = Case(f"dycore_{nx}x{ny}x58_s1", "dycore", dict(nx=nx, ny=ny, nz=58, nsteps=1),
                 dict(DYCORE_SCALARS), dict(DYCORE_FILLS))
     _oracle_vs_gpu(case)
+
+
+def test_north_star_full_timestep_c4():
+    """north_star: one full timestep (dycore + HE-VI + column physics, `full_step`) on the
+    1581 x 1301 x 58 production grid — the bench's headline workload — bit-exact against
+    the oracle in every prognostic field and the column means."""
+    _oracle_vs_gpu(Case("full_1581x1301x58_s1", "dycore_full",
+                        dict(nx=1581, ny=1301, nz=58, nsteps=1),
+                        dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS)))
+
+
+def test_full_size_rk3_step_c2():
+    """BASELINE configs[1] grid with the Wicker-Skamarock RK3 long step (three fused
+    stages), one step, bit-exact against the oracle."""
+    _oracle_vs_gpu(Case("rk3_512x512x58_s1", "dycore_rk3", dict(nx=512, ny=512, nz=58, nsteps=1),
+                        dict(DYCORE_SCALARS), dict(DYCORE_FILLS)))
+
+
+def test_c2_dycore_100_steps():
+    """BASELINE configs[1] as stated: dycore + HE-VI, 512 x 512 x 58 for 100 steps (one
+    `main` call: copy-in, 100 fused steps, copy-out), bit-exact against the oracle after
+    all 100 steps — no drift envelope is needed because every step is bit-identical."""
+    _oracle_vs_gpu(Case("dycore_512x512x58_s100", "dycore", dict(nx=512, ny=512, nz=58, nsteps=100),
+                        dict(DYCORE_SCALARS), dict(DYCORE_FILLS)))
 
 
 def test_full_size_diffusion_step():

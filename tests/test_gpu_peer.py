@@ -50,7 +50,7 @@ def free_port():
         return s.getsockname()[1]
 
 
-def worker(rank, world, port, name, px, py, q, per_step=False, ordered=False):
+def worker(rank, world, port, name, px, py, q, per_step=False, ordered=False, options=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -60,6 +60,8 @@ def worker(rank, world, port, name, px, py, q, per_step=False, ordered=False):
         d = hfb.decomp_init(gnx, gny, case.ints.get("nz", 1), px, py, rank, halo=HALO[name])
         eng = hfb.Engine(APPS[case.app].prog, device=0)
         eng.set_decomposition(d)
+        for k, v in (options or {}).items():
+            eng.set_option(k, v)
         if ordered:
             eng.set_reduction_order(True)
         ints = tile_ints(case, d)
@@ -95,12 +97,12 @@ def worker(rank, world, port, name, px, py, q, per_step=False, ordered=False):
         dist.destroy_process_group()
 
 
-def run_peer(name, px, py, per_step=False, ordered=False):
+def run_peer(name, px, py, per_step=False, ordered=False, options=None):
     world = px * py
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=worker, args=(r, world, port, name, px, py, q, per_step, ordered))
+    procs = [ctx.Process(target=worker, args=(r, world, port, name, px, py, q, per_step, ordered, options))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -160,14 +162,13 @@ def test_peer_reduction_is_rank_ordered_and_identical_everywhere():
 
 
 @pytest.mark.parametrize("overlap", [True, False])
-def test_peer_fused_halo_hand_off_per_step_entries(monkeypatch, overlap):
+def test_peer_fused_halo_hand_off_per_step_entries(overlap):
     """Consecutive dycore_step entries hand the halos over in the step kernel's epilogue
     (boundary strips store into the neighbours' next-step halo rings; the next exchange
     only waits for their flags). Without overlap the single full-span launch carries the
     remote epilogue. Both equal the undecomposed oracle bit for bit."""
-    if not overlap:
-        monkeypatch.setenv("HFB_NO_OVERLAP", "1")
-    case, garr, out, parts = run_peer("dycore", 2, 2, per_step=True)
+    case, garr, out, parts = run_peer("dycore", 2, 2, per_step=True,
+                                      options={"overlap": int(overlap)})
     ref = {k: v.copy() for k, v in garr.items()}
     run_oracle(case, ref)
     for k in ("th", "u", "v", "w", "p"):
@@ -262,3 +263,81 @@ def test_peer_checkpoint_resume_per_rank(tmp_path):
         for k, t in tiles.items():
             want = ref[k][tile_slices(case.app, k, ref[k], d)]
             assert bits_equal(t.reshape(want.shape), want), (rank, k)
+
+
+def c4_worker(rank, world, port, px, py, tmpdir, q):
+    """One rank of the north-star grid split 4 x 2 (tiles 396 x 651 / 395 x 650): builds
+    only its own tile of the synthetic state (global flat indices), runs `main_full`
+    (copy-in, 2 full timesteps: one push, one epilogue hand-off, copy-out) and saves the
+    tile's outputs for the parent."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1710_08616_b200 import synthetic
+        gnx, gny, nz = C4
+        d = hfb.decomp_init(gnx, gny, nz, px, py, rank, halo=2)
+        eng = hfb.Engine("dycore", device=0)
+        eng.set_decomposition(d)
+        for k, v in dict(nx=int(d.nx), ny=int(d.ny), nz=nz, nsteps=2).items():
+            eng.set(k, v)
+        for k, v in dict(DYCORE_SCALARS, **PHYS_SCALARS).items():
+            eng.set(k, float(v))
+        box3 = [(0, nz), (d.i0, d.i0 + d.nx), (d.j0, d.j0 + d.ny)]
+        tiles = {k: synthetic.field((nz, gnx, gny), *v, box=box3) for k, v in DYCORE_FILLS.items()}
+        tiles.update({k: synthetic.field((gnx, gny), *v, box=box3[1:])
+                      for k, v in PHYS_FILLS.items()})
+        for n, a in tiles.items():
+            eng.bind(n, a)
+        eng.attach_peers()
+        eng.run("main_full")
+        for n, a in tiles.items():
+            np.save(os.path.join(tmpdir, f"r{rank}_{n}.npy"), a)
+        q.put((rank, eng.peer_stats(), (int(d.i0), int(d.j0), int(d.nx), int(d.ny)), None))
+        dist.barrier()
+        eng.close()
+    except Exception as e:
+        q.put((rank, None, None, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+C4 = (1581, 1301, 58)
+
+
+def test_peer_c4_strong_scaling_tiles_4x2(tmp_path):
+    """BASELINE configs[3] at 8 GPUs: the 1581 x 1301 x 58 grid as 4 x 2 tiles (396 x 651),
+    one process per rank over the peer transport, two full timesteps (north_star step:
+    dycore + HE-VI + column physics). The assembled tiles equal the undecomposed oracle
+    bit for bit."""
+    px, py = 4, 2
+    world = px * py
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=c4_worker, args=(r, world, port, px, py, str(tmp_path), q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        parts = [q.get(timeout=600) for _ in range(world)]
+        for p in procs:
+            p.join(timeout=120)
+    finally:
+        for p in procs:
+            if p.is_alive():
+                p.kill()
+    errors = [e for *_, e in parts if e]
+    assert not errors, errors
+    assert sorted((r[2][2], r[2][3]) for r in parts)[-1] == (396, 651)
+    assert all(p[1] == (1, 1) for p in parts), [p[1] for p in parts]
+    case = Case("c4_full", "dycore_full", dict(nx=C4[0], ny=C4[1], nz=C4[2], nsteps=2),
+                dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS))
+    ref = make_inputs(case)
+    run_oracle(case, ref)
+    for rank, _, (i0, j0, nx, ny), _ in parts:
+        for n in ("th", "u", "v", "w", "p", "colm"):
+            t = np.load(tmp_path / f"r{rank}_{n}.npy")
+            want = ref[n][..., i0:i0 + nx, j0:j0 + ny] if ref[n].ndim == 3 else \
+                ref[n][i0:i0 + nx, j0:j0 + ny]
+            assert bits_equal(t, want), f"rank {rank}: {n} differs"
