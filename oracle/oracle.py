@@ -34,6 +34,15 @@ class DynParams(ctypes.Structure):
                 ("th0", ctypes.c_double)]
 
 
+class AsucaParams(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int64), ("ny", ctypes.c_int64), ("nz", ctypes.c_int64),
+                ("dt", ctypes.c_double), ("rdx", ctypes.c_double), ("rdy", ctypes.c_double),
+                ("rdz", ctypes.c_double), ("cs2", ctypes.c_double), ("grav", ctypes.c_double),
+                ("th0", ctypes.c_double), ("nsound", ctypes.c_int64), ("nbnd", ctypes.c_int64),
+                ("kdmp", ctypes.c_int64), ("rdmp", ctypes.c_double), ("rnbnd", ctypes.c_double),
+                ("rnzd", ctypes.c_double)]
+
+
 _lib = None
 
 
@@ -58,6 +67,8 @@ def lib():
         L.ora_dycore_run.argtypes = [i64, ctypes.POINTER(DynParams), V, V, V, V, V, V]
         L.ora_dycore_run.restype = ctypes.c_int
         L.ora_rk3_run.argtypes = [i64, ctypes.POINTER(DynParams), V, V, V, V, V, V]
+        L.ora_asuca_run.argtypes = [i64, ctypes.POINTER(AsucaParams), V, V, V, V, V, V]
+        L.ora_asuca_run.restype = ctypes.c_int
         L.ora_rk3_run.restype = ctypes.c_int
         L.ora_full_run.argtypes = [i64, ctypes.POINTER(DynParams), dbl, dbl] + [V] * 8
         L.ora_full_run.restype = ctypes.c_int
@@ -169,3 +180,17 @@ def rk3_run(nsteps, params, rho, th, u, v, w, p):
                            view(w), view(p))
     if rc:
         raise RuntimeError(f"ora_rk3_run failed ({rc})")
+
+
+def asuca_run(nsteps, params, ints, rho, th, u, v, w, p):
+    """simulation_run_asuca: nsteps x asuca_step (apps/dycore/asuca.h90). `params` holds
+    the dyn_state reals (dt..th0, rdmp, rnbnd, rnzd), `ints` nsound, nbnd, kdmp."""
+    nz, nx, ny = th.shape
+    prm = AsucaParams(nx, ny, nz, params["dt"], params["rdx"], params["rdy"], params["rdz"],
+                      params["cs2"], params["grav"], params["th0"], ints["nsound"],
+                      ints["nbnd"], ints["kdmp"], params["rdmp"], params["rnbnd"],
+                      params["rnzd"])
+    rc = lib().ora_asuca_run(nsteps, ctypes.byref(prm), view(rho), view(th), view(u), view(v),
+                             view(w), view(p))
+    if rc:
+        raise RuntimeError(f"ora_asuca_run failed ({rc})")

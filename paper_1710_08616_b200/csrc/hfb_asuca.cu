@@ -1,0 +1,662 @@
+// hfb_asuca.cu — the ASUCA time scheme of apps/dycore/asuca.h90 on sm_100a.
+//
+// One asuca_step = three RK3 stages; each stage is
+//   k_asu_tend            slow tendencies (limited advection of rho, theta, u, v, w) at the
+//                         stage state: asuca.h90 regions "theta and rho ..." through
+//                         "momentum (advective form ...)", fused into one K-march;
+//   nsm x { k_asu_acoustic<A>   RK2 first stage (h = dtau/2): the midpoint pressure pa,
+//           k_asu_acoustic<B> } RK2 second stage (dtau) + lateral/upper damping: u, v, w, p;
+//   k_asu_stage_end       theta = thb + dtf*fth, rho = rhob + dtf*frho.
+// The dialect's copies (the step's base state, the acoustic restart from it, the
+// short-step copy-back) are pointer swaps in the runtime (hfb_runtime.cu asuca_step).
+//
+// Machine organisation follows k_dyn_step_ws (hfb_dycore_tmem.cu): a CTA owns a 32 x 4
+// tile of (i,j) columns (warp = row, lane = column) and marches K; every K-plane of the
+// fields the tile reads (with the halo columns/rows its stencils need) is staged into a
+// shared-memory ring by LDGSTS (cp.async, 16-B chunks, L1 bypass) several levels ahead;
+// the acoustic passes keep the Thomas coefficients in TENSOR MEMORY (one lane per
+// thread) and ps in shared memory, so HBM traffic is the compulsory bytes: each input
+// read once, each output written once.
+//
+// Arithmetic is the dialect's, operation for operation (-fmad=false, IEEE division),
+// so results are bit-identical to the reference interpreter. Boundary cases (walls,
+// first/last faces) are evaluated as selects on GLOBAL indices; stencil values outside
+// the domain are read from the halo ring / other ring slots and discarded by those
+// selects (the dialect clamps those indices; the discarded values never matter).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "hfb_kernels.cuh"
+#include "hfb_sm100.cuh"
+
+namespace hfb {
+
+namespace {
+
+constexpr int kTX = 32, kTY = 4, kThreads = kTX * kTY;
+constexpr int kTmemCols = 256;  // cp: columns 0..127, dp: 128..255 (nz - 1 <= 64)
+constexpr int kDpCol = 128;
+
+// ---- plane staging ---------------------------------------------------------------
+// A plane spec: rows j0' + r0 .. + h - 1 and columns i0' + c0 .. + w - 1 (0-based tile
+// origin i0' = i0 - 1, j0' = j0 - 1) of one field, packed row-major at `off` doubles
+// inside a ring stage. w and c0 are even, so every 16-B chunk is aligned (tiles start at
+// odd 1-based i, rows start 128-B aligned).
+struct PlaneSpec {
+  const double* base;
+  int r0, c0, w, h, off;
+};
+
+template <int NSPEC, int NCH>
+struct Stager {
+  const double* src[NCH];
+  uint32_t dst[NCH];
+  uint32_t ok;  // bit q: chunk q exists and lies inside the allocation
+  __device__ void init(const PlaneSpec (&sp)[NSPEC], int total_chunks, int t, int64_t i0z,
+                       int64_t j0z, int64_t W, int64_t nj, int64_t row_lo, int64_t row_hi,
+                       uint32_t ring_u32) {
+    ok = 0;
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) {
+      const int ch = t + q * kThreads;
+      src[q] = sp[0].base;
+      dst[q] = ring_u32;
+      if (ch >= total_chunks) continue;
+      const int e = ch * 2;
+      int s = 0;
+#pragma unroll
+      for (int z = 1; z < NSPEC; ++z)
+        if (e >= sp[z].off) s = z;
+      const int le = e - sp[s].off;
+      const int64_t r = j0z + sp[s].r0 + le / sp[s].w;
+      const int64_t c = i0z + sp[s].c0 + le % sp[s].w;
+      if (r >= -kHalo && r <= nj - 1 + kHalo && c >= row_lo && c + 1 <= row_hi) ok |= 1u << q;
+      src[q] = sp[s].base + r * W + c;
+      dst[q] = ring_u32 + static_cast<uint32_t>(e) * 8u;
+    }
+  }
+  // stage the plane of level k (0-based) into ring byte offset `so`
+  __device__ __forceinline__ void issue(int64_t k, int64_t P, uint32_t so) const {
+#pragma unroll
+    for (int q = 0; q < NCH; ++q)
+      if (ok & (1u << q)) sm100::cp_async16(dst[q] + so, src[q] + k * P);
+  }
+};
+
+// limited upwind flux (asuca.h90 asu_flux with asu_minmod) as selects: both upwind
+// candidates' slope pairs are formed and one is chosen, so there is no divergence on the
+// sign of the face velocity. vel*(qp1 + (-0.5)*s) == vel*(qp1 - 0.5*s) bit for bit.
+__device__ __forceinline__ double asu_flux(double vel, double qm1, double q0, double qp1,
+                                           double qp2, bool lo, bool hi) {
+  const double d0 = q0 - qm1, d1 = qp1 - q0, d2 = qp2 - qp1;
+  const bool up = vel >= 0.0;
+  const double x = up ? d0 : d1, y = up ? d1 : d2;
+  const double m = fabs(x) < fabs(y) ? x : y;
+  double sl = (x * y <= 0.0) ? 0.0 : m;
+  sl = (up ? lo : hi) ? 0.0 : sl;
+  const double base = up ? q0 : qp1;
+  const double h = up ? 0.5 : -0.5;
+  return vel * (base + h * sl);
+}
+
+// ============================================================================
+// slow tendencies
+// ============================================================================
+constexpr int kTW = kTX + 4, kTR = kTY + 4;   // 36 x 8 plane tile (2-cell ring)
+constexpr int kTPlane = kTW * kTR;            // 288
+constexpr int kTStage = 5 * kTPlane;          // rho, th, u, v, w
+constexpr int kTChunks = kTStage / 2;         // 720
+constexpr int kTChPerThread = (kTChunks + kThreads - 1) / kThreads;  // 6
+constexpr int kTStages = 6;                   // levels k-1..k+2 in use, k+3 in flight
+enum { kFRho = 0, kFTh = 1, kFU = 2, kFV = 3, kFW = 4 };
+
+struct TendArgs {
+  AsuState s;
+  AsuTend f;
+  Grid3 g;
+  int nz;
+  int64_t nj, row_lo, row_hi;
+  double rdx, rdy, rdz;
+  Span sp;
+};
+
+__global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
+  extern __shared__ __align__(128) double smem[];
+  const int lane = threadIdx.x, row = threadIdx.y, t = row * kTX + lane;
+  const int64_t i0 = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * kTX;
+  const int64_t j0 = a.sp.jlo + static_cast<int64_t>(blockIdx.y) * kTY;
+  const int64_t i = i0 + lane, j = j0 + row;
+  const bool active = i <= a.sp.ihi && j <= a.sp.jhi;
+  const int nz = a.nz;
+  const int64_t P = a.g.plane, W = a.g.pitch;
+  const int64_t gi = i + a.sp.i0, gj = j + a.sp.j0, gnx = a.sp.gnx, gny = a.sp.gny;
+  const double rdx = a.rdx, rdy = a.rdy, rdz = a.rdz;
+
+  const PlaneSpec specs[5] = {{a.s.rho, -2, -2, kTW, kTR, 0 * kTPlane},
+                              {a.s.th, -2, -2, kTW, kTR, 1 * kTPlane},
+                              {a.s.u, -2, -2, kTW, kTR, 2 * kTPlane},
+                              {a.s.v, -2, -2, kTW, kTR, 3 * kTPlane},
+                              {a.s.w, -2, -2, kTW, kTR, 4 * kTPlane}};
+  Stager<5, kTChPerThread> stg;
+  stg.init(specs, kTChunks, t, i0 - 1, j0 - 1, W, a.nj, a.row_lo, a.row_hi,
+           sm100::smem_u32(smem));
+  constexpr uint32_t kStageBytes = kTStage * 8;
+  auto issue = [&](int k) {
+    if (k < nz) stg.issue(k, P, static_cast<uint32_t>((k % kTStages) * kStageBytes));
+    sm100::cp_async_commit();
+  };
+  // value of field f at level k (0-based; any k, ring slot), offset (di, dj)
+  const int cen = (row + 2) * kTW + (lane + 2);
+  auto V = [&](int f, int k, int di, int dj) -> double {
+    const int slot = ((k % kTStages) + kTStages) % kTStages;
+    return smem[slot * kTStage + f * kTPlane + cen + dj * kTW + di];
+  };
+
+  const bool east = gi == gnx, west = gi == 1, north = gj == gny, south = gj == 1;
+  const int64_t col = (j - 1) * W + (i - 1);
+
+  for (int k = 0; k < kTStages - 2; ++k) issue(k);
+
+  // carried along K (values at the bottom face / level centre of the current level)
+  double fzt_b = 0.0, fzr_b = 0.0;  // theta/rho flux through z-face kk-1/2
+  double gzu_b = 0.0, czu_b = 0.0;  // u: z-edge flux / velocity at kk-1/2
+  double gzv_b = 0.0, czv_b = 0.0;  // v
+  double gzw_b = 0.0, czw_b = 0.0;  // w: flux / velocity through level centre kk
+#pragma unroll 1
+  for (int k = 0; k < nz; ++k) {  // 0-based level; dialect level kk = k + 1
+    sm100::cp_async_wait<kTStages - 5>();  // levels <= k+2 landed (own copies)
+    __syncthreads();                        // ... everyone's; slot of level k-2 free
+    issue(k + kTStages - 2);
+    const int kk = k + 1;
+
+    // ---- theta and rho -------------------------------------------------------------
+    const double ui = V(kFU, k, 0, 0), uim1 = V(kFU, k, -1, 0);
+    const double vj = V(kFV, k, 0, 0), vjm1 = V(kFV, k, 0, -1);
+    const double wk = V(kFW, k, 0, 0), wkm1 = V(kFW, k - 1, 0, 0);
+    double fth, frho;
+    {
+      // x faces: east (face i) and west (face i-1)
+      auto xface = [&](int fld, int64_t f, int off, double vel) {  // face f = gi + off
+        return (f == 0 || f == gnx) ? 0.0
+                                    : asu_flux(vel, V(fld, k, off - 1, 0), V(fld, k, off, 0),
+                                               V(fld, k, off + 1, 0), V(fld, k, off + 2, 0),
+                                               f == 1, f + 1 == gnx);
+      };
+      auto yface = [&](int fld, int64_t f, int off, double vel) {
+        return (f == 0 || f == gny) ? 0.0
+                                    : asu_flux(vel, V(fld, k, 0, off - 1), V(fld, k, 0, off),
+                                               V(fld, k, 0, off + 1), V(fld, k, 0, off + 2),
+                                               f == 1, f + 1 == gny);
+      };
+      auto zface = [&](int fld) {  // top face kk+1/2
+        return (kk == nz) ? 0.0
+                          : asu_flux(wk, V(fld, k - 1, 0, 0), V(fld, k, 0, 0), V(fld, k + 1, 0, 0),
+                                     V(fld, k + 2, 0, 0), kk == 1, kk + 1 == nz);
+      };
+      const double ue = east ? 0.0 : ui, uw = west ? 0.0 : uim1;
+      const double vnf = north ? 0.0 : vj, vs = south ? 0.0 : vjm1;
+      const double wt = (kk == nz) ? 0.0 : wk, wb = (kk == 1) ? 0.0 : wkm1;
+      double div = rdx * (ue - uw) + rdy * (vnf - vs);
+      div = div + rdz * (wt - wb);
+      const double fzt = zface(kFTh), fzr = zface(kFRho);
+      double flux = rdx * (xface(kFTh, gi, 0, ui) - xface(kFTh, gi - 1, -1, uim1)) +
+                    rdy * (yface(kFTh, gj, 0, vj) - yface(kFTh, gj - 1, -1, vjm1));
+      flux = flux + rdz * (fzt - fzt_b);
+      fth = V(kFTh, k, 0, 0) * div - flux;
+      flux = rdx * (xface(kFRho, gi, 0, ui) - xface(kFRho, gi - 1, -1, uim1)) +
+             rdy * (yface(kFRho, gj, 0, vj) - yface(kFRho, gj - 1, -1, vjm1));
+      flux = flux + rdz * (fzr - fzr_b);
+      frho = 0.0 - flux;
+      fzt_b = fzt;
+      fzr_b = fzr;
+    }
+
+    // ---- u (x-face point i) --------------------------------------------------------
+    double fu = 0.0;
+    {
+      // centre c = gi + off between u-points c-1 and c (walls 0 and gnx are zero)
+      auto xcen = [&](int off, double& cv) {
+        const int64_t c = gi + off;
+        const double qb = (c == 1) ? 0.0 : V(kFU, k, off - 1, 0);
+        const double qc = (c == gnx) ? 0.0 : V(kFU, k, off, 0);
+        const double qa = (c <= 2) ? 0.0 : V(kFU, k, off - 2, 0);
+        const double qd = (c + 1 >= gnx) ? 0.0 : V(kFU, k, off + 1, 0);
+        cv = 0.5 * (qb + qc);
+        return asu_flux(cv, qa, qb, qc, qd, c == 1, c == gnx);
+      };
+      // y edge f = gj + off (between u(j') and u(j'+1)), velocity mean of v(i), v(i+1)
+      auto yedge = [&](int off, double& cv) {
+        const int64_t f = gj + off;
+        if (f == 0 || f == gny || east) {
+          cv = 0.0;
+          return 0.0;
+        }
+        cv = 0.5 * (V(kFV, k, 0, off) + V(kFV, k, 1, off));
+        return asu_flux(cv, V(kFU, k, 0, off - 1), V(kFU, k, 0, off), V(kFU, k, 0, off + 1),
+                        V(kFU, k, 0, off + 2), f == 1, f + 1 == gny);
+      };
+      double cxe, cxw, cyn, cys, czt;
+      const double gxe = xcen(1, cxe), gxw = xcen(0, cxw);
+      const double gyn = yedge(0, cyn), gys = yedge(-1, cys);
+      double gzt;
+      if (kk == nz || east) {
+        czt = 0.0;
+        gzt = 0.0;
+      } else {
+        czt = 0.5 * (wk + V(kFW, k, 1, 0));
+        gzt = asu_flux(czt, V(kFU, k - 1, 0, 0), ui, V(kFU, k + 1, 0, 0), V(kFU, k + 2, 0, 0),
+                       kk == 1, kk + 1 == nz);
+      }
+      if (!east) {
+        double div = rdx * (cxe - cxw) + rdy * (cyn - cys);
+        div = div + rdz * (czt - czu_b);
+        double flux = rdx * (gxe - gxw) + rdy * (gyn - gys);
+        flux = flux + rdz * (gzt - gzu_b);
+        fu = ui * div - flux;
+      }
+      gzu_b = gzt;
+      czu_b = czt;
+    }
+
+    // ---- v (y-face point j) --------------------------------------------------------
+    double fv = 0.0;
+    {
+      auto ycen = [&](int off, double& cv) {
+        const int64_t c = gj + off;
+        const double qb = (c == 1) ? 0.0 : V(kFV, k, 0, off - 1);
+        const double qc = (c == gny) ? 0.0 : V(kFV, k, 0, off);
+        const double qa = (c <= 2) ? 0.0 : V(kFV, k, 0, off - 2);
+        const double qd = (c + 1 >= gny) ? 0.0 : V(kFV, k, 0, off + 1);
+        cv = 0.5 * (qb + qc);
+        return asu_flux(cv, qa, qb, qc, qd, c == 1, c == gny);
+      };
+      auto xedge = [&](int off, double& cv) {
+        const int64_t f = gi + off;
+        if (f == 0 || f == gnx || north) {
+          cv = 0.0;
+          return 0.0;
+        }
+        cv = 0.5 * (V(kFU, k, off, 0) + V(kFU, k, off, 1));
+        return asu_flux(cv, V(kFV, k, off - 1, 0), V(kFV, k, off, 0), V(kFV, k, off + 1, 0),
+                        V(kFV, k, off + 2, 0), f == 1, f + 1 == gnx);
+      };
+      double cye, cyw, cxe, cxw, czt;
+      const double gxe = xedge(0, cxe), gxw = xedge(-1, cxw);
+      const double gyn = ycen(1, cye), gys = ycen(0, cyw);
+      double gzt;
+      if (kk == nz || north) {
+        czt = 0.0;
+        gzt = 0.0;
+      } else {
+        czt = 0.5 * (wk + V(kFW, k, 0, 1));
+        gzt = asu_flux(czt, V(kFV, k - 1, 0, 0), vj, V(kFV, k + 1, 0, 0), V(kFV, k + 2, 0, 0),
+                       kk == 1, kk + 1 == nz);
+      }
+      if (!north) {
+        double div = rdx * (cxe - cxw) + rdy * (cye - cyw);
+        div = div + rdz * (czt - czv_b);
+        double flux = rdx * (gxe - gxw) + rdy * (gyn - gys);
+        flux = flux + rdz * (gzt - gzv_b);
+        fv = vj * div - flux;
+      }
+      gzv_b = gzt;
+      czv_b = czt;
+    }
+
+    // ---- w (z-face point kk) -------------------------------------------------------
+    double fw = 0.0;
+    {
+      // level centre c between w-points c-1 and c (0 = ground and nz = lid are zero)
+      auto zcen = [&](int c, int kc, double& cv) {  // kc: 0-based level of w-point c
+        const double qb = (c == 1) ? 0.0 : V(kFW, kc - 1, 0, 0);
+        const double qc = (c == nz) ? 0.0 : V(kFW, kc, 0, 0);
+        const double qa = (c <= 2) ? 0.0 : V(kFW, kc - 2, 0, 0);
+        const double qd = (c + 1 >= nz) ? 0.0 : V(kFW, kc + 1, 0, 0);
+        cv = 0.5 * (qb + qc);
+        return asu_flux(cv, qa, qb, qc, qd, c == 1, c == nz);
+      };
+      if (kk == 1) gzw_b = zcen(1, 0, czw_b);  // the ground-side centre of the column
+      double czt;
+      const double gzt = (kk == nz) ? 0.0 : zcen(kk + 1, k + 1, czt);
+      if (kk == nz) czt = 0.0;
+      if (kk != nz) {
+        auto xedge = [&](int off, double& cv) {
+          const int64_t f = gi + off;
+          if (f == 0 || f == gnx) {
+            cv = 0.0;
+            return 0.0;
+          }
+          cv = 0.5 * (V(kFU, k, off, 0) + V(kFU, k + 1, off, 0));
+          return asu_flux(cv, V(kFW, k, off - 1, 0), V(kFW, k, off, 0), V(kFW, k, off + 1, 0),
+                          V(kFW, k, off + 2, 0), f == 1, f + 1 == gnx);
+        };
+        auto yedge = [&](int off, double& cv) {
+          const int64_t f = gj + off;
+          if (f == 0 || f == gny) {
+            cv = 0.0;
+            return 0.0;
+          }
+          cv = 0.5 * (V(kFV, k, 0, off) + V(kFV, k + 1, 0, off));
+          return asu_flux(cv, V(kFW, k, 0, off - 1), V(kFW, k, 0, off), V(kFW, k, 0, off + 1),
+                          V(kFW, k, 0, off + 2), f == 1, f + 1 == gny);
+        };
+        double cxe, cxw, cyn, cys;
+        const double gxe = xedge(0, cxe), gxw = xedge(-1, cxw);
+        const double gyn = yedge(0, cyn), gys = yedge(-1, cys);
+        double div = rdx * (cxe - cxw) + rdy * (cyn - cys);
+        div = div + rdz * (czt - czw_b);
+        double flux = rdx * (gxe - gxw) + rdy * (gyn - gys);
+        flux = flux + rdz * (gzt - gzw_b);
+        fw = wk * div - flux;
+      }
+      gzw_b = gzt;
+      czw_b = czt;
+    }
+
+    if (active) {
+      const int64_t o = col + static_cast<int64_t>(k) * P;
+      a.f.fth[o] = fth;
+      a.f.frho[o] = frho;
+      a.f.fu[o] = fu;
+      a.f.fv[o] = fv;
+      a.f.fw[o] = fw;
+    }
+  }
+  sm100::cp_async_wait<0>();
+}
+
+// ============================================================================
+// acoustic RK2 passes
+// ============================================================================
+// pass A (kB = false) planes: p (i-1..i+1, j-1..j+1), u, fu (i-1), v, fv (j-1), w, rho,
+// th, fw. Pass B (kB = true): pa in place of p's neighbourhood, p at the column only.
+constexpr int kAW = kTX + 4;  // 36 (x-halo planes, even start 2 columns left)
+constexpr int kAStages = 4;   // level k in use, k+1..k+3 in flight
+
+struct AcoArgs {
+  AsuState s;        // current u, v, w, p; stage rho, th
+  const double *fu, *fv, *fw;
+  const double* pa;  // pass B: the midpoint pressure
+  double* pa_out;    // pass A
+  double *un, *vn, *wn, *pn;  // pass B
+  Grid3 g;
+  int nz;
+  int64_t nj, row_lo, row_hi;
+  AsuAcoConst c;
+  Span sp;
+};
+
+template <bool kB>
+__global__ void __launch_bounds__(kThreads, 2) k_asu_acoustic(AcoArgs a) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ uint32_t tmem_base_slot;
+  // stage layout (doubles)
+  constexpr int oP = 0;                          // p or pa: 36 x 6
+  constexpr int oU = oP + kAW * (kTY + 2);       // u: 36 x 4
+  constexpr int oFU = oU + kAW * kTY;            // fu: 36 x 4
+  constexpr int oV = oFU + kAW * kTY;            // v: 32 x 5
+  constexpr int oFV = oV + kTX * (kTY + 1);      // fv: 32 x 5
+  constexpr int oW = oFV + kTX * (kTY + 1);      // w, rho, th, fw: 32 x 4 each
+  constexpr int oRho = oW + kTX * kTY;
+  constexpr int oTh = oRho + kTX * kTY;
+  constexpr int oFW = oTh + kTX * kTY;
+  constexpr int oPc = oFW + kTX * kTY;           // pass B: p at the column, 32 x 4
+  constexpr int kStage = kB ? oPc + kTX * kTY : oPc;
+  constexpr int kChunks = kStage / 2;
+  constexpr int kChPer = (kChunks + kThreads - 1) / kThreads;
+  double* ring = smem;
+  double* ps_s = smem + kAStages * kStage;  // nz x 128
+
+  const int lane = threadIdx.x, row = threadIdx.y, t = row * kTX + lane;
+  const int64_t i0 = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * kTX;
+  const int64_t j0 = a.sp.jlo + static_cast<int64_t>(blockIdx.y) * kTY;
+  const int64_t i = i0 + lane, j = j0 + row;
+  const bool active = i <= a.sp.ihi && j <= a.sp.jhi;
+  const int nz = a.nz;
+  const int64_t P = a.g.plane, W = a.g.pitch;
+  const int64_t gi = i + a.sp.i0, gj = j + a.sp.j0;
+  const AsuAcoConst& c = a.c;
+
+  if (row == 0) sm100::tmem_alloc(&tmem_base_slot, kTmemCols);
+  sm100::tmem_fence_before();
+  __syncthreads();
+  sm100::tmem_fence_after();
+  const uint32_t tmem = tmem_base_slot + (static_cast<uint32_t>(32 * row) << 16);
+
+  constexpr int NS = 10;  // pass A's chunks end before the last spec (p at the column)
+  PlaneSpec specs[NS] = {{kB ? a.pa : a.s.p, -1, -2, kAW, kTY + 2, oP},
+                         {a.s.u, 0, -2, kAW, kTY, oU},
+                         {a.fu, 0, -2, kAW, kTY, oFU},
+                         {a.s.v, -1, 0, kTX, kTY + 1, oV},
+                         {a.fv, -1, 0, kTX, kTY + 1, oFV},
+                         {a.s.w, 0, 0, kTX, kTY, oW},
+                         {a.s.rho, 0, 0, kTX, kTY, oRho},
+                         {a.s.th, 0, 0, kTX, kTY, oTh},
+                         {a.fw, 0, 0, kTX, kTY, oFW},
+                         {a.s.p, 0, 0, kTX, kTY, oPc}};
+  Stager<NS, kChPer> stg;
+  stg.init(specs, kChunks, t, i0 - 1, j0 - 1, W, a.nj, a.row_lo, a.row_hi, sm100::smem_u32(ring));
+  constexpr uint32_t kStageBytes = kStage * 8;
+  auto issue = [&](int k) {
+    if (k < nz) stg.issue(k, P, static_cast<uint32_t>((k % kAStages) * kStageBytes));
+    sm100::cp_async_commit();
+  };
+
+  const bool east = gi == a.sp.gnx, west = gi == 1, north = gj == a.sp.gny, south = gj == 1;
+  const int64_t col = (j - 1) * W + (i - 1);
+  // damping (pass B): lateral ramp of this column; the upper ramp per level
+  double axy = 0.0;
+  if (kB) {
+    const int64_t nb = c.nbnd;
+    auto ramp = [&](int64_t q, int64_t n) {  // max(0, max(nbnd + 1 - q, q - n + nbnd))
+      const int64_t l = nb + 1 - q, r = q - n + nb;
+      const int64_t m = r > l ? r : l;
+      return static_cast<double>(m > 0 ? m : 0);
+    };
+    const double ax = ramp(gi, a.sp.gnx) * c.rnbnd;
+    const double ay = ramp(gj, a.sp.gny) * c.rnbnd;
+    axy = ay > ax ? ay : ax;  // interp.cpp max: the first unless a later one is greater
+  }
+  auto tau_at = [&](int kk) {  // dtau * rdmp * max(max(ax, ay), az) at 1-based level kk
+    const double az = static_cast<double>(kk - c.kdmp > 0 ? kk - c.kdmp : 0) * c.rnzd;
+    return c.dtau_rdmp * (az > axy ? az : axy);
+  };
+
+  for (int k = 0; k < kAStages - 1; ++k) issue(k);
+
+  double rho_p = 0.0, th_p = 0.0, w_p = 0.0, fw_p = 0.0, ps_p = 0.0, cp_p = 0.0, dp_p = 0.0;
+#pragma unroll 1
+  for (int k = 0; k < nz; ++k) {
+    sm100::cp_async_wait<kAStages - 2>();  // level k landed (own copies)
+    __syncthreads();                        // everyone's; the slot of level k-1 is free
+    issue(k + kAStages - 1);
+    const double* S = ring + (k % kAStages) * kStage;
+    const double* Pp = S + oP + (row + 1) * kAW + (lane + 2);
+    const double pk = Pp[0], pe = Pp[1], pw = Pp[-1], pnn = Pp[kAW], psth = Pp[-kAW];
+    const double uk = S[oU + row * kAW + lane + 2], ukw = S[oU + row * kAW + lane + 1];
+    const double fuk = S[oFU + row * kAW + lane + 2], fukw = S[oFU + row * kAW + lane + 1];
+    const double vk = S[oV + (row + 1) * kTX + lane], vks = S[oV + row * kTX + lane];
+    const double fvk = S[oFV + (row + 1) * kTX + lane], fvks = S[oFV + row * kTX + lane];
+    const double wk = S[oW + t], rhok = S[oRho + t], thk = S[oTh + t], fwk = S[oFW + t];
+    const double pc = kB ? S[oPc + t] : pk;  // p at the column (the RK2 base)
+
+    // PGF at p (A) / pa (B) applied to the current momentum, plus h * slow tendency
+    const double unk = east ? 0.0 : uk - c.h_rdx * (pe - pk) + c.h * fuk;
+    const double vnk = north ? 0.0 : vk - c.h_rdy * (pnn - pk) + c.h * fvk;
+    const double uw = west ? 0.0 : ukw - c.h_rdx * (pk - pw) + c.h * fukw;
+    const double vs = south ? 0.0 : vks - c.h_rdy * (pk - psth) + c.h * fvks;
+    const double psk = pc - c.h_cs2 * (c.rdx * (unk - uw) + c.rdy * (vnk - vs));
+    ps_s[k * kThreads + t] = psk;
+    if (kB && active) {  // damped momentum of the short step
+      const double tau = tau_at(k + 1);
+      const int64_t o = col + static_cast<int64_t>(k) * P;
+      a.un[o] = unk - tau * unk;
+      a.vn[o] = vnk - tau * vnk;
+    }
+    if (k >= 1) {  // forward elimination for the face between levels k-1 and k
+      const int f = k - 1;
+      const double rf = 0.5 * (rho_p + rhok);
+      const double beta = c.beta_num / rf;
+      double dd = w_p - c.h_rdz * (psk - ps_p) / rf;
+      dd = dd + c.h_grav * (0.5 * (th_p + thk) - c.th0) / c.th0;
+      dd = dd + c.h * fw_p;
+      const double bb = 1.0 + 2.0 * beta;
+      double cpk, dpk;
+      if (f == 0) {
+        cpk = -beta / bb;
+        dpk = dd / bb;
+      } else {
+        const double m = bb + beta * cp_p;
+        cpk = -beta / m;
+        dpk = (dd + beta * dp_p) / m;
+      }
+      sm100::tmem_st_f64(tmem + 2 * f, cpk);
+      sm100::tmem_st_f64(tmem + kDpCol + 2 * f, dpk);
+      cp_p = cpk;
+      dp_p = dpk;
+    }
+    rho_p = rhok;
+    th_p = thk;
+    w_p = wk;
+    fw_p = fwk;
+    ps_p = psk;
+  }
+  sm100::cp_async_wait<0>();
+  sm100::tmem_wait_st();
+
+  // back substitution (faces nz-2 .. 0, w(nz) = 0 is the lid), four per TMEM load, then
+  // the pressure update (pass B: the damped w of the short step)
+  double* pout = kB ? a.pn : a.pa_out;
+  if (kB && active) a.wn[col + static_cast<int64_t>(nz - 1) * P] = 0.0 - tau_at(nz) * 0.0;
+  double wk1 = 0.0;
+  const int nf = nz - 1;
+#pragma unroll 1
+  for (int cb = (nf - 1) / 4; cb >= 0; --cb) {
+    double cpv[4], dpv[4];
+    sm100::tmem_ld_4f64(tmem + 8 * cb, cpv);
+    sm100::tmem_ld_4f64(tmem + kDpCol + 8 * cb, dpv);
+#pragma unroll
+    for (int q = 3; q >= 0; --q) {
+      const int f = 4 * cb + q;  // face f = w-point f+1 (1-based) at 0-based level f
+      if (f >= nf) continue;
+      const double wkk = (f == nf - 1) ? dpv[q] : dpv[q] - cpv[q] * wk1;
+      const double pk1 = ps_s[(f + 1) * kThreads + t] - c.h_cs2_rdz * (wk1 - wkk);
+      if (active) {
+        pout[col + static_cast<int64_t>(f + 1) * P] = pk1;
+        if (kB) a.wn[col + static_cast<int64_t>(f) * P] = wkk - tau_at(f + 1) * wkk;
+      }
+      wk1 = wkk;
+    }
+  }
+  if (active) pout[col] = ps_s[t] - c.h_cs2_rdz * wk1;
+  sm100::tmem_fence_before();
+  __syncthreads();
+  if (row == 0) sm100::tmem_dealloc(tmem_base_slot, kTmemCols);
+}
+
+// theta = thb + dtf * fth, rho = rhob + dtf * frho over the span (asuca.h90 stage end)
+__global__ void k_asu_stage_end(const double* thb, const double* fth, const double* rhob,
+                                const double* frho, double* th, double* rho, Grid3 g, int nz,
+                                double dtf, Span sp) {
+  const int64_t i = sp.ilo + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t j = sp.jlo + blockIdx.y;
+  if (i > sp.ihi) return;
+  int64_t o = (j - 1) * g.pitch + (i - 1);
+  for (int k = 0; k < nz; ++k, o += g.plane) {
+    th[o] = thb[o] + dtf * fth[o];
+    rho[o] = rhob[o] + dtf * frho[o];
+  }
+}
+
+}  // namespace
+
+AsuAcoConst make_asu_aco_const(double h, double dtau, double rdx, double rdy, double rdz,
+                               double cs2, double grav, double th0, double rdmp, int64_t nbnd,
+                               int64_t kdmp, double rnbnd, double rnzd) {
+  AsuAcoConst c;
+  c.h = h;
+  c.rdx = rdx;
+  c.rdy = rdy;
+  c.th0 = th0;
+  c.h_rdx = h * rdx;                     // `h * rdx * (...)`
+  c.h_rdy = h * rdy;
+  c.h_rdz = h * rdz;                     // `h * rdz * (...) / rf`
+  c.h_cs2 = h * cs2;                     // `h * cs2 * (...)`
+  c.h_cs2_rdz = h * cs2 * rdz;           // `h * cs2 * rdz * (...)`
+  c.beta_num = h * h * cs2 * rdz * rdz;  // `h * h * cs2 * rdz * rdz / rf`
+  c.h_grav = h * grav;                   // `h * grav * (...) / th0`
+  c.dtau_rdmp = dtau * rdmp;             // `dtau * rdmp * max(...)`
+  c.nbnd = nbnd;
+  c.kdmp = kdmp;
+  c.rnbnd = rnbnd;
+  c.rnzd = rnzd;
+  return c;
+}
+
+bool asuca_fits(int64_t nz) { return nz >= 2 && nz - 1 <= 64; }
+
+cudaError_t launch_asu_tend(const AsuState& s, const AsuTend& f, Grid3 g, int64_t nz, int64_t nj,
+                            double rdx, double rdy, double rdz, const Span& sp, cudaStream_t st) {
+  if (sp.ihi < sp.ilo || sp.jhi < sp.jlo) return cudaSuccess;
+  const size_t smem = static_cast<size_t>(kTStages) * kTStage * sizeof(double);
+  {
+    cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(k_asu_tend), smem);
+    if (e != cudaSuccess) return e;
+  }
+  TendArgs a{s, f, g, static_cast<int>(nz), nj, -kIOff, g.pitch - kIOff - 1, rdx, rdy, rdz, sp};
+  dim3 block(kTX, kTY);
+  dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
+            static_cast<unsigned>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY));
+  k_asu_tend<<<grid, block, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_asu_acoustic(bool pass_b, const AsuState& s, const double* fu,
+                                const double* fv, const double* fw, const double* pa,
+                                double* pa_out, double* un, double* vn, double* wn, double* pn,
+                                Grid3 g, int64_t nz, int64_t nj, const AsuAcoConst& c,
+                                const Span& sp, cudaStream_t st) {
+  if (sp.ihi < sp.ilo || sp.jhi < sp.jlo) return cudaSuccess;
+  if (!asuca_fits(nz)) return cudaErrorInvalidValue;
+  const int stage = pass_b ? (kAW * (kTY + 2) + 2 * kAW * kTY + 2 * kTX * (kTY + 1) +
+                              5 * kTX * kTY)
+                           : (kAW * (kTY + 2) + 2 * kAW * kTY + 2 * kTX * (kTY + 1) +
+                              4 * kTX * kTY);
+  // two CTAs per SM share the SM's 512 TMEM columns; pad small-nz launches so a third
+  // CTA never blocks in tcgen05.alloc
+  const size_t smem = std::max<size_t>(
+      (static_cast<size_t>(kAStages) * stage + static_cast<size_t>(nz) * kThreads) * sizeof(double),
+      80 * 1024);
+  const void* kern = pass_b ? reinterpret_cast<const void*>(k_asu_acoustic<true>)
+                            : reinterpret_cast<const void*>(k_asu_acoustic<false>);
+  {
+    cudaError_t e = ensure_dynamic_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+  }
+  AcoArgs a{s, fu, fv, fw, pa, pa_out, un, vn, wn, pn, g, static_cast<int>(nz), nj,
+            -kIOff, g.pitch - kIOff - 1, c, sp};
+  dim3 block(kTX, kTY);
+  dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
+            static_cast<unsigned>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY));
+  if (pass_b)
+    k_asu_acoustic<true><<<grid, block, smem, st>>>(a);
+  else
+    k_asu_acoustic<false><<<grid, block, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_asu_stage_end(const double* thb, const double* fth, const double* rhob,
+                                 const double* frho, double* th, double* rho, Grid3 g,
+                                 int64_t nz, double dtf, const Span& sp, cudaStream_t st) {
+  if (sp.ihi < sp.ilo || sp.jhi < sp.jlo) return cudaSuccess;
+  dim3 block(128);
+  dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + 127) / 128),
+            static_cast<unsigned>(sp.jhi - sp.jlo + 1));
+  k_asu_stage_end<<<grid, block, 0, st>>>(thb, fth, rhob, frho, th, rho, g, static_cast<int>(nz),
+                                          dtf, sp);
+  return cudaGetLastError();
+}
+
+}  // namespace hfb

@@ -31,13 +31,6 @@
 
 namespace hfb {
 
-// timing experiments (A/B build only): skip one role's arithmetic
-#ifdef HFB_VARIANTS
-#define HFB_SKIP(a, bit) (((a).debug_skip & (bit)) != 0)
-#else
-#define HFB_SKIP(a, bit) false
-#endif
-
 namespace {
 
 constexpr int kTX = 32, kTY = 4, kThreads = kTX * kTY;
@@ -310,7 +303,11 @@ struct StepTmemArgs {
   DynOut out;
   Grid3 g;
   int nz;
-  int debug_skip;  // profiling experiments only: 1 = no advection, 2 = no acoustic, 3 = neither
+  // roles this launch computes: bit 0 = advection, bit 1 = acoustic/HE-VI. Always 3 in
+  // the product (launch_dycore_step_ws); the A/B build's timing experiments clear one
+  // (hfb_set_option debug_skip). A runtime value on purpose: folding it to a constant
+  // changes the register allocation of the 128-register kernel and costs ~2%.
+  int roles;
   // column physics fused into the advection warps (full_step); null when off
   const double* tsfc;
   double* colm;
@@ -535,7 +532,7 @@ cudaError_t launch_dycore_step_tmem(const DynIn& in, const DynOut& out, Grid3 g,
     cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(k_dyn_step_tmem), smem);
     if (e != cudaSuccess) return e;
   }
-  StepTmemArgs a{in,  out,     g,      static_cast<int>(nz), 0, nullptr, nullptr, 0.0, 0.0,
+  StepTmemArgs a{in,  out,     g,      static_cast<int>(nz), 3, nullptr, nullptr, 0.0, 0.0,
                  DynIn{}, nj, -kIOff, g.pitch - kIOff - 1, c, sp};
   dim3 block(kTX, kTY);
   dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
@@ -558,6 +555,10 @@ cudaError_t launch_dycore_step_tmem(const DynIn& in, const DynOut& out, Grid3 g,
 namespace {
 
 constexpr int kWsThreads = 2 * kThreads;  // 256
+#ifndef HFB_MID_UNROLL
+#define HFB_MID_UNROLL 1
+#endif
+constexpr int kMidUnroll = HFB_MID_UNROLL;  // mid-column K loop unrolling
 // ring depth: 6 planes x 8.25 KB (+ ps, nz x 1 KB, in shared memory: measured faster than
 // an L2 round trip of ps with a 10-deep ring)
 constexpr int kWsStages = 6;
@@ -826,7 +827,7 @@ __global__ void __launch_bounds__(kWsThreads, 2)
     const double* Vp = S + kFOffV + (row + 1) * kVW + lane;
     const double vj = Vp[0], vjm1 = Vp[-kVW];
     const double wk = S[kFOffW + row * kSW + lane];
-    if (acoustic && !HFB_SKIP(a, 2)) {
+    if (acoustic && (a.roles & 2) != 0) {
       const double* Pp = S + kFOffP + (row + 1) * kPW + (lane + 2);
       const double pk = Pp[0], pe = Pp[1], pw = Pp[-1], pnn = Pp[kPW], psth = Pp[-kPW];
       const double rhok = S[kFOffRho + row * kSW + lane];
@@ -886,7 +887,7 @@ __global__ void __launch_bounds__(kWsThreads, 2)
       rho_prev = rhok;
       ps_prev = psk;
       if (kRK) wb_prev = bcur.w;
-    } else if (!acoustic && !HFB_SKIP(a, 1)) {
+    } else if (!acoustic && (a.roles & 1) != 0) {
       const double* T0 = S + kFOffTh + thc;
       const double tkp1 =
           (kMid || kk + 1 <= nz) ? ring[s1 * kFStageDoubles + kFOffTh + thc] : 0.0;
@@ -951,7 +952,7 @@ __global__ void __launch_bounds__(kWsThreads, 2)
     int k = 0;
 #pragma unroll 1
     for (; k < mid_lo; ++k) step(k, in_tag, std::false_type{});
-#pragma unroll 1
+#pragma unroll kMidUnroll
     for (; k < mid_hi; ++k) step(k, in_tag, std::true_type{});
 #pragma unroll 1
     for (; k < nz; ++k) step(k, in_tag, std::false_type{});
@@ -1046,9 +1047,9 @@ cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, i
     if (e != cudaSuccess) return e;
   }
 #ifndef HFB_VARIANTS
-  debug_skip = 0;
+  debug_skip = 0;  // the product computes both roles
 #endif
-  StepTmemArgs a{in, out, g, static_cast<int>(nz), debug_skip,
+  StepTmemArgs a{in, out, g, static_cast<int>(nz), 3 & ~debug_skip,
                  phys ? phys->tsfc : nullptr, phys ? phys->colm : nullptr,
                  phys ? phys->dt_rrelax : 0.0, phys ? phys->dt_ch : 0.0,
                  base ? *base : DynIn{}, nj, -kIOff, g.pitch - kIOff - 1, c, sp};

@@ -192,4 +192,37 @@ struct PeerReduce {
 };
 cudaError_t launch_peer_allreduce(const PeerReduce& r, cudaStream_t s);
 
+// ---- apps/dycore/asuca.h90 (hfb_asuca.cu): the ASUCA time scheme ------------------
+struct AsuState {
+  const double *rho, *th, *u, *v, *w, *p;
+};
+struct AsuTend {
+  double *frho, *fth, *fu, *fv, *fw;
+};
+// one RK2 acoustic pass of step h (dtau/2 or dtau), products formed as the dialect
+// evaluates them (left-associative)
+struct AsuAcoConst {
+  double h, rdx, rdy, th0;
+  double h_rdx, h_rdy, h_rdz, h_cs2, h_cs2_rdz, beta_num, h_grav;
+  double dtau_rdmp, rnbnd, rnzd;
+  int64_t nbnd, kdmp;
+};
+AsuAcoConst make_asu_aco_const(double h, double dtau, double rdx, double rdy, double rdz,
+                               double cs2, double grav, double th0, double rdmp, int64_t nbnd,
+                               int64_t kdmp, double rnbnd, double rnzd);
+bool asuca_fits(int64_t nz);
+// slow tendencies at the stage state (rho, th, u, v, w; p unused)
+cudaError_t launch_asu_tend(const AsuState& s, const AsuTend& f, Grid3 g, int64_t nz, int64_t nj,
+                            double rdx, double rdy, double rdz, const Span& sp, cudaStream_t st);
+// pass A (pass_b false): pa_out = the RK2 midpoint pressure; pass B: un, vn, wn (damped),
+// pn from the state s (u, v, w, p current; rho, th of the stage) and the midpoint pa
+cudaError_t launch_asu_acoustic(bool pass_b, const AsuState& s, const double* fu,
+                                const double* fv, const double* fw, const double* pa,
+                                double* pa_out, double* un, double* vn, double* wn, double* pn,
+                                Grid3 g, int64_t nz, int64_t nj, const AsuAcoConst& c,
+                                const Span& sp, cudaStream_t st);
+cudaError_t launch_asu_stage_end(const double* thb, const double* fth, const double* rhob,
+                                 const double* frho, double* th, double* rho, Grid3 g,
+                                 int64_t nz, double dtf, const Span& sp, cudaStream_t st);
+
 }  // namespace hfb

@@ -177,7 +177,9 @@ const std::vector<AppDecl>& app_table() {
                   {"nsteps", SType::Int}, {"dt", SType::Real}, {"rdx", SType::Real},
                   {"rdy", SType::Real}, {"rdz", SType::Real}, {"cs2", SType::Real},
                   {"grav", SType::Real}, {"th0", SType::Real}, {"ch", SType::Real},
-                  {"rrelax", SType::Real}},
+                  {"rrelax", SType::Real}, {"nsound", SType::Int}, {"nbnd", SType::Int},
+                  {"kdmp", SType::Int}, {"rdmp", SType::Real}, {"rnbnd", SType::Real},
+                  {"rnzd", SType::Real}},
                  {{"rho", dims3("nz", "nx", "ny"), KIJ, false},
                   {"th", dims3("nz", "nx", "ny"), KIJ, true},
                   {"u", dims3("nz", "nx", "ny"), KIJ, true},
@@ -292,6 +294,10 @@ struct hfb_ctx {
   double* halo_recv = nullptr;
   size_t halo_cap = 0;
   std::map<std::string, Scratch> scratch;  // generated programs' routine-local arrays
+  // asuca_step: the stage's slow tendencies (frho, fth, fu, fv, fw) and the RK2 midpoint
+  // pressure pa, in the prognostic fields' device layout
+  double* asu[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  int64_t asu_elems = 0;
   // peer-memory halo transport (hfb_peer_export / hfb_peer_attach): halos are stored
   // straight into the neighbours' buffers over NVLink, flags signal their arrival
   bool peer = false;
@@ -1093,6 +1099,122 @@ void rk3_step(hfb_ctx* c, Stats& st) {
   for (const char* n : {"th", "u", "v", "w", "p"}) dev_written(c, n);
 }
 
+// apps/dycore/asuca.h90 asuca_step: the ASUCA time scheme (hfb_asuca.cu). Buffers per
+// field: u, v, w, p — the state at the start of the step (base, left intact: every RK3
+// stage restarts its acoustic sub-steps from it) and two that the short steps ping-pong
+// between; theta, rho — base and the stage state (the stage end writes thb + dtf*fth in
+// place of the previous stage's). The dialect's copies are these pointer choices.
+void asuca_prepare(hfb_ctx* c) {
+  for (const char* n : {"u", "v", "w", "p"}) ensure_device(c, slot(c, n), true, 3);
+  for (const char* n : {"th", "rho"}) ensure_device(c, slot(c, n), true, 2);
+  const int64_t elems = slot(c, "th").lay.alloc_elems;
+  if (c->asu_elems != elems) {
+    for (double*& q : c->asu) {
+      if (q) cudaFree(q);
+      q = nullptr;
+    }
+    c->asu_elems = 0;
+  }
+  for (double*& q : c->asu) {
+    if (q) continue;
+    const size_t bytes = static_cast<size_t>(elems) * sizeof(double);
+    cuda_check(cudaMalloc(&q, bytes), "cudaMalloc(asuca scratch)");
+    cuda_check(cudaMemsetAsync(q, 0, bytes, c->stream), "cudaMemsetAsync");
+  }
+  c->asu_elems = elems;
+}
+
+void asuca_step(hfb_ctx* c, Stats& st) {
+  const int64_t nx = ival(c, "nx"), ny = ival(c, "ny"), nz = ival(c, "nz");
+  if (!asuca_fits(nz))
+    fail(HFB_CONFIG, "asuca_step is implemented for 2 <= nz <= 65 (got %lld)", (long long)nz);
+  if (c->decomposed && c->decomp.px * c->decomp.py > 1)
+    fail(HFB_CONFIG, "asuca_step runs single-domain (no halo exchange between its passes yet)");
+  const int64_t nsound = ival(c, "nsound"), nbnd = ival(c, "nbnd"), kdmp = ival(c, "kdmp");
+  const double dt = rval(c, "dt"), rdx = rval(c, "rdx"), rdy = rval(c, "rdy"),
+               rdz = rval(c, "rdz"), cs2 = rval(c, "cs2"), grav = rval(c, "grav"),
+               th0 = rval(c, "th0"), rdmp = rval(c, "rdmp"), rnbnd = rval(c, "rnbnd"),
+               rnzd = rval(c, "rnzd");
+  if (nsound < 1) fail(HFB_RUNTIME, "nsound must be >= 1 (got %lld)", (long long)nsound);
+  for (const char* n : {"th", "u", "v", "w", "p", "rho"}) dev_read(c, n);
+  asuca_prepare(c);
+  Slot &rho = slot(c, "rho"), &th = slot(c, "th"), &u = slot(c, "u"), &v = slot(c, "v"),
+       &w = slot(c, "w"), &p = slot(c, "p");
+  const int b = u.cur;
+  for (Slot* s : {&v, &w, &p})
+    if (s->cur != b) fail(HFB_RUNTIME, "prognostic buffers out of step");
+  const int tb = th.cur, rb = rho.cur, tx = 1 - tb, rx = 1 - rb;
+  const int x = (b + 1) % 3, y = (b + 2) % 3;
+  const Grid3 g = grid_of(th);
+  const int64_t nj = th.lay.nj;
+  const Span sp = full_span(c, nx, ny);
+  double** A = c->asu;
+  const AsuTend F{A[0], A[1], A[2], A[3], A[4]};
+  double* pa = A[5];
+  const double dtau = dt / static_cast<double>(nsound);  // asuca.h90 `dt / real(nsound)`
+  const AsuAcoConst ca = make_asu_aco_const(0.5 * dtau, dtau, rdx, rdy, rdz, cs2, grav, th0,
+                                            rdmp, nbnd, kdmp, rnbnd, rnzd);
+  const AsuAcoConst cb = make_asu_aco_const(dtau, dtau, rdx, rdy, rdz, cs2, grav, th0, rdmp,
+                                            nbnd, kdmp, rnbnd, rnzd);
+  count_launch(st, nx, ny);  // the base-state copy region
+  const double* thS = th.d_buf(tb);
+  const double* rhoS = rho.d_buf(rb);
+  int us = b;  // buffer of the stage state's u, v, w (p's is unused by the tendencies)
+  for (int stg = 1; stg <= 3; ++stg) {
+    const double dtf = stg == 1 ? dt / 3.0 : stg == 2 ? dt / 2.0 : dt;
+    const int64_t nsm = stg == 1 ? nsound / 3 : stg == 2 ? nsound / 2 : nsound;
+    const AsuState S{rhoS, thS, u.d_buf(us), v.d_buf(us), w.d_buf(us), p.d_buf(us)};
+    launch(c, st, "asuca_tend", [&] {
+      return launch_asu_tend(S, F, g, nz, nj, rdx, rdy, rdz, sp, ks(c));
+    });
+    // the reference's launches: 12 flux regions (4 of them over an extra face row or
+    // column), the theta/rho and the momentum tendencies, the acoustic restart copy
+    count_launch(st, nx + 1, ny);
+    count_launch(st, nx, ny + 1);
+    count_launch(st, nx, ny);
+    count_launch(st, nx, ny);
+    count_launch(st, nx, ny + 1);
+    count_launch(st, nx, ny);
+    count_launch(st, nx + 1, ny);
+    count_launch(st, nx, ny);
+    count_launch(st, nx, ny);
+    count_launch(st, nx + 1, ny);
+    count_launch(st, nx, ny + 1);
+    count_launch(st, nx, ny);
+    count_launch(st, nx, ny);
+    count_launch(st, nx, ny);
+    count_launch(st, nx, ny);
+    int cur = b, nxt = x;
+    for (int64_t ss = 0; ss < nsm; ++ss) {
+      const AsuState C{rhoS, thS, u.d_buf(cur), v.d_buf(cur), w.d_buf(cur), p.d_buf(cur)};
+      launch(c, st, "asuca_acoustic_a", [&] {
+        return launch_asu_acoustic(false, C, F.fu, F.fv, F.fw, nullptr, pa, nullptr, nullptr,
+                                   nullptr, nullptr, g, nz, nj, ca, sp, ks(c));
+      });
+      launch(c, st, "asuca_acoustic_b", [&] {
+        return launch_asu_acoustic(true, C, F.fu, F.fv, F.fw, pa, nullptr, u.d_buf(nxt),
+                                   v.d_buf(nxt), w.d_buf(nxt), p.d_buf(nxt), g, nz, nj, cb, sp,
+                                   ks(c));
+      });
+      for (int r = 0; r < 7; ++r) count_launch(st, nx, ny);
+      cur = nxt;
+      nxt = nxt == x ? y : x;
+    }
+    us = cur;
+    launch(c, st, "asuca_stage_end", [&] {
+      return launch_asu_stage_end(th.d_buf(tb), F.fth, rho.d_buf(rb), F.frho, th.d_buf(tx),
+                                  rho.d_buf(rx), g, nz, dtf, sp, ks(c));
+    });
+    count_launch(st, nx, ny);
+    thS = th.d_buf(tx);
+    rhoS = rho.d_buf(rx);
+  }
+  for (Slot* s : {&u, &v, &w, &p}) s->cur = us;
+  th.cur = tx;
+  rho.cur = rx;
+  for (const char* n : {"rho", "th", "u", "v", "w", "p"}) dev_written(c, n);
+}
+
 void dycore_entry(hfb_ctx* c, const std::string& r, Stats& st) {
   const char* names[] = {"p", "rho", "th", "u", "v", "w"};
   if (r == "main" || r == "simulation_run") {
@@ -1119,6 +1241,13 @@ void dycore_entry(hfb_ctx* c, const std::string& r, Stats& st) {
     for (const char* n : names) entry_copy_out(c, slot(c, n));
   } else if (r == "column_physics") {
     column_physics(c, st);
+  } else if (r == "asuca_step") {
+    asuca_step(c, st);
+  } else if (r == "main_asuca" || r == "simulation_run_asuca") {
+    int64_t nsteps = ival(c, "nsteps");
+    for (const char* n : names) do_copy_to_device(c, slot(c, n));
+    for (int64_t s = 0; s < nsteps; ++s) asuca_step(c, st);
+    for (const char* n : names) entry_copy_out(c, slot(c, n));
   } else {
     fail(HFB_CONFIG, "program 'dycore' has no entry '%s'", r.c_str());
   }
@@ -1158,7 +1287,8 @@ bool entry_has_transfers(const AppDecl* d, const std::string& r) {
   }
   const std::string& app = d->app;
   if (r == "main" || r == "simulation_run" || r == "main_full" || r == "simulation_run_full" ||
-      r == "main_rk3" || r == "simulation_run_rk3")
+      r == "main_rk3" || r == "simulation_run_rk3" || r == "main_asuca" ||
+      r == "simulation_run_asuca")
     return true;
   (void)app;
   return false;
@@ -1663,6 +1793,8 @@ void hfb_destroy(hfb_ctx* c) {
   if (c->red_cols) cudaFree(c->red_cols);
   for (auto& kv : c->scratch)
     if (kv.second.dev) cudaFree(kv.second.dev);
+  for (double* p : c->asu)
+    if (p) cudaFree(p);
   if (c->red_host) cudaFreeHost(c->red_host);
   if (c->halo_send) cudaFree(c->halo_send);
   if (c->halo_recv) cudaFree(c->halo_recv);
@@ -1915,6 +2047,7 @@ hfb_status hfb_run_graph(hfb_ctx* c, const char* entry, int64_t steps, hfb_launc
     // no allocation may happen during capture: materialise every buffer first
     for (auto& [n, s] : c->slots)
       if (s.decl->pingpong && s.has_device) ensure_device(c, s, true, r == "rk3_step" ? 3 : 0);
+    if (r == "asuca_step" && c->app->app == "dycore" && !c->app->plugin) asuca_prepare(c);
     cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
     std::map<std::string, int> cur0;
     for (auto& [n, s] : c->slots) cur0[n] = s.cur;

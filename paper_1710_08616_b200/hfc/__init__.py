@@ -20,7 +20,8 @@ PKG = Path(__file__).resolve().parents[1]
 GEN_DIR = PKG / "gen"  # generated plugins (built by __graft_entry__.build, git-ignored)
 # programs of this repository generated at build time: name -> sources (repo-relative)
 BUILTIN_SOURCES = {
-    "dycore_gen": ["apps/dycore/dyn_state.h90", "apps/dycore/dycore.h90"],
+    "dycore_gen": ["apps/dycore/dyn_state.h90", "apps/dycore/dycore.h90",
+                   "apps/dycore/asuca.h90"],
     "kitchen_gen": ["apps/kitchen/kit_state.h90", "apps/kitchen/kitchen.h90"],
 }
 # the reference's own application corpus (proj/tests/data/apps), compiled when the reference

@@ -73,6 +73,13 @@ APPS = {
         dict({n: ("nz", "nx", "ny") for n in ("rho", "th", "u", "v", "w", "p")},
              tsfc=("nx", "ny"), colm=("nx", "ny")),
         ["th", "u", "v", "w", "p", "colm"], entry="main_full", program="dycore"),
+    # the ASUCA time scheme: RK3 long step, RK2 HE-VI acoustic short steps with damping,
+    # limited advection of rho, theta and momentum (apps/dycore/asuca.h90, entry main_asuca)
+    "asuca": App(
+        "asuca", [("own", "dycore/dyn_state.h90"), ("own", "dycore/dycore.h90"),
+                  ("own", "dycore/asuca.h90")],
+        "dyn_state", {n: ("nz", "nx", "ny") for n in ("rho", "th", "u", "v", "w", "p")},
+        ["rho", "th", "u", "v", "w", "p"], entry="main_asuca", program="dycore"),
     # feature coverage of the code generator (hfc); not a built-in program of the engine
     "kitchen": App(
         "kitchen", [("own", "kitchen/kit_state.h90"), ("own", "kitchen/kitchen.h90")],
@@ -90,6 +97,16 @@ DYCORE_FILLS = {  # name: (seed, offset, scale)
     "v": (10, -0.01, 0.02), "w": (11, -0.002, 0.004), "p": (12, -0.005, 0.01)}
 PHYS_SCALARS = {"ch": 0.05, "rrelax": 0.01}
 PHYS_FILLS = {"tsfc": (13, 300.0, 2.0), "colm": (14, 300.0, 0.5)}
+ASUCA_RDMP = 0.2  # maximum damping rate of the lateral band / upper sponge
+
+
+def asuca_params(nz, nsound=6, nbnd=2, kdmp=None):
+    """(ints, reals) of the ASUCA scheme: nsound short steps per long step, a lateral
+    damping band of nbnd cells, the upper sponge above level kdmp (default: the top
+    quarter of the column)."""
+    kdmp = nz - max(1, nz // 4) if kdmp is None else kdmp
+    return (dict(nsound=nsound, nbnd=nbnd, kdmp=kdmp),
+            dict(rdmp=ASUCA_RDMP, rnbnd=1.0 / nbnd, rnzd=1.0 / (nz - kdmp)))
 
 
 @dataclass
@@ -123,6 +140,12 @@ def _full(name, nx, ny, nz, nsteps, gpu_check=True):
 def _rk3(name, nx, ny, nz, nsteps, gpu_check=True):
     return Case(name, "dycore_rk3", dict(nx=nx, ny=ny, nz=nz, nsteps=nsteps),
                 dict(DYCORE_SCALARS), dict(DYCORE_FILLS), gpu_check=gpu_check)
+
+
+def _asu(name, nx, ny, nz, nsteps, gpu_check=True, **kw):
+    ints, reals = asuca_params(nz, **kw)
+    return Case(name, "asuca", dict(nx=nx, ny=ny, nz=nz, nsteps=nsteps, **ints),
+                dict(DYCORE_SCALARS, **reals), dict(DYCORE_FILLS), gpu_check=gpu_check)
 
 
 CASES = [
@@ -175,6 +198,11 @@ CASES = [
     _rk3("rk3_24x20x12_s1", 24, 20, 12, 1),
     _rk3("rk3_1x5x2_s2", 1, 5, 2, 2),
     _rk3("rk3_33x3x58_s1", 33, 3, 58, 1),
+    _asu("asuca_13x7x10_s2", 13, 7, 10, 2),
+    _asu("asuca_24x20x12_s1", 24, 20, 12, 1, nbnd=3),
+    _asu("asuca_1x5x3_s1", 1, 5, 3, 1, nsound=12, nbnd=1),
+    _asu("asuca_33x3x58_s1", 33, 3, 58, 1, nbnd=4),
+    _asu("asuca_13x7x10_s20", 13, 7, 10, 20, gpu_check=False),
 ]
 CASE_BY_NAME = {c.name: c for c in CASES}
 

@@ -73,6 +73,8 @@ def run_oracle(case, arrs):
     elif case.app == "dycore_full":
         oracle.full_run(i["nsteps"], r, a["rho"], a["th"], a["u"], a["v"], a["w"], a["p"],
                         a["tsfc"], a["colm"])
+    elif case.app == "asuca":
+        oracle.asuca_run(i["nsteps"], r, i, a["rho"], a["th"], a["u"], a["v"], a["w"], a["p"])
     else:
         raise KeyError(case.app)
     return {}

@@ -13,7 +13,7 @@ from golden_io import bits_equal, decl, load_golden, make_inputs
 
 pytestmark = pytest.mark.gpu
 GEN = hfc.GEN_DIR / "dycore_gen.so"
-DYCORE_CASES = [c for c in CASES if c.app in ("dycore", "dycore_rk3", "dycore_full")]
+DYCORE_CASES = [c for c in CASES if c.app in ("dycore", "dycore_rk3", "dycore_full", "asuca")]
 
 
 def run_generated(case, arrs):

@@ -12,7 +12,7 @@ import pytest
 
 import paper_1710_08616_b200 as hfb
 from cases import (APPS, CASES, CASE_BY_NAME, DYCORE_FILLS, DYCORE_SCALARS, PHYS_FILLS,
-                   PHYS_SCALARS, Case)
+                   PHYS_SCALARS, Case, _asu)
 from golden_io import bits_equal, decl, load_golden, make_inputs, run_oracle
 
 pytestmark = pytest.mark.gpu
@@ -99,6 +99,10 @@ LARGE = [
          dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS)),
     Case("full_45x37x80_s2", "dycore_full", dict(nx=45, ny=37, nz=80, nsteps=2),
          dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS)),
+    _asu("asuca_128x96x58_s1", 128, 96, 58, 1, nbnd=6),
+    _asu("asuca_77x41x31_s2", 77, 41, 31, 2, nsound=12, nbnd=3),
+    _asu("asuca_40x36x2_s2", 40, 36, 2, 2, kdmp=1),
+    _asu("asuca_33x9x65_s1", 33, 9, 65, 1, nsound=6, nbnd=4),
 ]
 
 
@@ -274,6 +278,42 @@ def test_north_star_full_timestep_c4():
     _oracle_vs_gpu(Case("full_1581x1301x58_s1", "dycore_full",
                         dict(nx=1581, ny=1301, nz=58, nsteps=1),
                         dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS)))
+
+
+def test_asuca_step_c3():
+    """The ASUCA time scheme (RK3 long step; 11 RK2 HE-VI acoustic short steps with
+    lateral/upper damping; limited advection of rho, theta, u, v, w) on the BASELINE
+    configs[2] grid, 1024 x 1024 x 58, one step, bit-exact against the oracle."""
+    _oracle_vs_gpu(_asu("asuca_1024x1024x58_s1", 1024, 1024, 58, 1, nbnd=8))
+
+
+def test_asuca_per_step_entry_and_graph_replay():
+    """asuca_step as a per-step entry (device resident, enqueued) and replayed from a CUDA
+    graph equals main_asuca (copy-in, nsteps, copy-out)."""
+    case = _asu("asuca_70x45x20_s4", 70, 45, 20, 4, nbnd=3)
+    ref = make_inputs(case)
+    run_engine(case, ref)
+    for mode in ("enqueue", "graph"):
+        arrs = make_inputs(case)
+        with hfb.Engine("dycore") as eng:
+            for k, v in case.ints.items():
+                eng.set(k, int(v))
+            for k, v in case.reals.items():
+                eng.set(k, float(v))
+            for n, a in arrs.items():
+                eng.bind(n, a)
+                eng.copy_to_device(n)
+            if mode == "enqueue":
+                for _ in range(case.ints["nsteps"]):
+                    eng.enqueue("asuca_step")
+                eng.synchronize()
+            else:
+                eng.run_graph("asuca_step", 2)
+                eng.run_graph("asuca_step", 2)
+            for n in arrs:
+                eng.copy_from_device(n)
+        for n in ("rho", "th", "u", "v", "w", "p"):
+            assert bits_equal(arrs[n], ref[n]), f"{mode}: {n} differs"
 
 
 def test_full_size_rk3_step_c2():
