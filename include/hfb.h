@@ -116,9 +116,16 @@ hfb_status hfb_synchronize(hfb_ctx* ctx);
 /* the context's CUDA stream (cudaStream_t), for callers that time with events */
 void* hfb_stream(hfb_ctx* ctx);
 /* Capture `steps` calls of a stream-only entry into a CUDA graph and replay it
- * (launch-overhead-free timestep loop). */
+ * (launch-overhead-free timestep loop; replaces the generated host driver's per-step
+ * launches, codegen.cpp:621-670). Graphs are cached per entry, step count and starting
+ * buffer sides. Decomposed contexts on the peer transport are captured too: the halo
+ * epochs live in device memory, so every replay signals and waits on fresh epochs
+ * (every rank must replay the same sequence). hfb_run_graph synchronises;
+ * hfb_enqueue_graph only launches on the context stream. */
 hfb_status hfb_run_graph(hfb_ctx* ctx, const char* entry, int64_t steps,
                          hfb_launch_stats* stats);
+hfb_status hfb_enqueue_graph(hfb_ctx* ctx, const char* entry, int64_t steps,
+                             hfb_launch_stats* stats);
 
 /* --- generated-kernel ABI (codegen.cpp:397-519) ------------------------------------ */
 typedef struct {

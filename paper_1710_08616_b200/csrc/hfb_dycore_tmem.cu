@@ -25,6 +25,17 @@
 #include <cstring>
 #include <type_traits>
 
+// The tolerance build of this file (Makefile: -fmad=true -DHFB_ARITH_FMA): the same
+// kernels with a*b+c contracted to FMA, every entry point renamed *_fma; selected per
+// context with hfb_set_option(ctx, "arith", "fma"). Results then differ from the
+// reference's binary64 evaluation by rounding only (tests/test_gpu_tolerance.py).
+#ifdef HFB_ARITH_FMA
+#define launch_dycore_acoustic_tmem launch_dycore_acoustic_tmem_fma
+#define dycore_acoustic_tmem_fits dycore_acoustic_tmem_fits_fma
+#define launch_dycore_step_tmem launch_dycore_step_tmem_fma
+#define dycore_step_tmem_fits dycore_step_tmem_fits_fma
+#define launch_dycore_step_ws launch_dycore_step_ws_fma
+#endif
 #include "hfb_kernels.cuh"
 #include "hfb_sm100.cuh"
 #include "hfb_fp64.cuh"

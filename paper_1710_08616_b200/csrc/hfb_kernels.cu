@@ -924,15 +924,22 @@ struct FlagList {
   uint64_t* f[16];
 };
 
-__global__ void k_peer_signal(FlagList fl, int n, uint64_t epoch) {
+__global__ void k_peer_signal(FlagList fl, int n, uint64_t* epoch_ctr, uint64_t epoch_val) {
   // every push of this stream completed before this kernel started (stream order); the
   // system-scope fence makes them visible to whoever acquires the flag
+  uint64_t epoch = epoch_val;
+  if (epoch_ctr) {  // the counter is touched by this stream only
+    epoch = *epoch_ctr + 1;
+    *epoch_ctr = epoch;
+  }
   __threadfence_system();
   for (int q = 0; q < n; ++q) st_release_sys(fl.f[q], epoch);
 }
 
-__global__ void k_peer_wait(FlagList fl, int n, uint64_t epoch) {
+__global__ void k_peer_wait(FlagList fl, int n, const uint64_t* epoch_ctr, uint64_t epoch_val) {
   const int q = threadIdx.x;
+  // the counter was written by this stream's previous signal
+  const uint64_t epoch = epoch_ctr ? *epoch_ctr : epoch_val;
   if (q < n)
     while (ld_acquire_sys(fl.f[q]) < epoch) __nanosleep(128);
 }
@@ -963,22 +970,23 @@ cudaError_t launch_peer_push(const PeerPush& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_peer_signal(uint64_t* const* flags, int n, uint64_t epoch, cudaStream_t s) {
+cudaError_t launch_peer_signal(uint64_t* const* flags, int n, uint64_t* epoch, cudaStream_t s,
+                               uint64_t epoch_val) {
   if (n <= 0) return cudaSuccess;
   if (n > 16) return cudaErrorInvalidValue;
   FlagList fl{};
   for (int q = 0; q < n; ++q) fl.f[q] = flags[q];
-  k_peer_signal<<<1, 1, 0, s>>>(fl, n, epoch);
+  k_peer_signal<<<1, 1, 0, s>>>(fl, n, epoch, epoch_val);
   return cudaGetLastError();
 }
 
-cudaError_t launch_peer_wait(const uint64_t* const* flags, int n, uint64_t epoch,
-                             cudaStream_t s) {
+cudaError_t launch_peer_wait(const uint64_t* const* flags, int n, const uint64_t* epoch,
+                             cudaStream_t s, uint64_t epoch_val) {
   if (n <= 0) return cudaSuccess;
   if (n > 16) return cudaErrorInvalidValue;
   FlagList fl{};
   for (int q = 0; q < n; ++q) fl.f[q] = const_cast<uint64_t*>(flags[q]);
-  k_peer_wait<<<1, 32, 0, s>>>(fl, n, epoch);
+  k_peer_wait<<<1, 32, 0, s>>>(fl, n, epoch, epoch_val);
   return cudaGetLastError();
 }
 

@@ -127,6 +127,14 @@ cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, i
                                   cudaStream_t s, const PhysArgs* phys = nullptr,
                                   const DynIn* base = nullptr,
                                   const RemoteHalo* remote = nullptr, int debug_skip = 0);
+#ifndef HFB_ARITH_FMA
+// the same step compiled with FMA contraction (tolerance mode, hfb_set_option "arith")
+cudaError_t launch_dycore_step_ws_fma(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
+                                      int64_t nj, const DynConst& c, const Span& sp,
+                                      cudaStream_t s, const PhysArgs* phys = nullptr,
+                                      const DynIn* base = nullptr,
+                                      const RemoteHalo* remote = nullptr, int debug_skip = 0);
+#endif
 #ifdef HFB_VARIANTS
 // Measured-slower alternatives, compiled only into the A/B build (make variants ->
 // libhfb_variants.so; selected with hfb_set_option(ctx, "variant", "tma" | "ws2")).
@@ -174,11 +182,15 @@ struct PeerPush {
   int n;
 };
 cudaError_t launch_peer_push(const PeerPush& p, cudaStream_t s);
-// release `epoch` into each remote flag (system scope, after the pushes on this stream)
-cudaError_t launch_peer_signal(uint64_t* const* flags, int n, uint64_t epoch, cudaStream_t s);
-// wait until every local flag reached `epoch` (acquire, system scope)
-cudaError_t launch_peer_wait(const uint64_t* const* flags, int n, uint64_t epoch,
-                             cudaStream_t s);
+// The exchange epoch lives in DEVICE memory (`epoch`, one word of the rank's own signal
+// block), so a captured CUDA graph replays correct epochs: the signal kernel increments
+// it and releases the new value into each remote flag (system scope, after the pushes on
+// this stream); the wait kernel reads it and waits until every local flag reached it
+// (acquire, system scope). With `epoch` null the epoch is the host value epoch_val.
+cudaError_t launch_peer_signal(uint64_t* const* flags, int n, uint64_t* epoch, cudaStream_t s,
+                               uint64_t epoch_val = 0);
+cudaError_t launch_peer_wait(const uint64_t* const* flags, int n, const uint64_t* epoch,
+                             cudaStream_t s, uint64_t epoch_val = 0);
 // deterministic all-reduce of one double over n ranks through peer memory: my value goes
 // to slot [parity][rank] of every rank, then every rank sums slots 0..n-1 in rank order
 struct PeerReduce {

@@ -252,7 +252,9 @@ struct PeerRank {
 // signal block layout (uint64 words): [0, 9) halo flags by the sender's offset from the
 // receiver, [16, 80) reduction flags by sender rank, then 2 x 64 doubles of reduction
 // slots (parity of the reduction epoch)
-constexpr int kSigHalo = 0, kSigRed = 16, kSigSlots = 80, kSigWords = 80 + 128;
+// signal block words: halo flags per neighbour direction (0..8), this rank's halo epoch
+// counter (9, device side: graph replays advance it), reduction flags, reduction slots
+constexpr int kSigHalo = 0, kSigEpoch = 9, kSigRed = 16, kSigSlots = 80, kSigWords = 80 + 128;
 // device scratch of generated programs: routine-local arrays (hfb_plugin_scratch)
 struct Scratch {
   Layout lay;
@@ -320,10 +322,16 @@ struct hfb_ctx {
   cudaStream_t run_stream = nullptr;
   bool overlap = true;  // hfb_set_option(ctx, "overlap", "0") serialises
   // CUDA graph cache for hfb_run_graph
-  cudaGraphExec_t graph_exec = nullptr;
-  std::string graph_key;
-  hfb_launch_stats graph_stats{};
-  std::map<std::string, int> graph_cur0, graph_cur1;
+  // CUDA graphs of captured step sequences (hfb_run_graph / hfb_enqueue_graph), keyed by
+  // entry, step count, the buffer sides at the start and the peer hand-off state
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    hfb_launch_stats stats{};
+    std::map<std::string, int> cur1;  // buffer sides after the steps
+    bool peer_fused1 = false;         // peer hand-off state after the steps
+    int64_t pushes = 0, handoffs = 0, halo_bytes = 0, epochs = 0;  // per replay
+  };
+  std::map<std::string, GraphEntry> graphs;
   // kernel variant (hfb_set_option "variant"; explicit per context, never from the
   // environment): the portable kernels only / the two-kernel (advect + acoustic) split /
   // the single-role fused kernel; tma / ws2 exist only in the A/B build (make variants)
@@ -333,6 +341,8 @@ struct hfb_ctx {
   bool force_tma = false;
   bool force_ws2 = false;
   int debug_skip = 0;  // A/B build only: 1 = no advection, 2 = no acoustic (timing)
+  // hfb_set_option "arith": the fused step's FMA-contracted build (tolerance mode)
+  bool arith_fma = false;
   // per-kernel CUDA-event timing (hfb_profile)
   bool prof = false;
   bool capturing = false;
@@ -957,9 +967,13 @@ cudaError_t launch_step(hfb_ctx* c, const DynIn& in, const DynOut& out, Grid3 g,
     return launch_dycore_step_ws2(in, out, g, nz, nj, k, sp, s, phys, base, c->debug_skip);
   if (c->force_tma)
     return launch_dycore_step_tma(in, out, g, nz, nj, k, sp, s, phys, base, c->debug_skip);
+  if (c->arith_fma)
+    return launch_dycore_step_ws_fma(in, out, g, nz, nj, k, sp, s, phys, base, nullptr,
+                                     c->debug_skip);
   return launch_dycore_step_ws(in, out, g, nz, nj, k, sp, s, phys, base, nullptr,
                                c->debug_skip);
 #else
+  if (c->arith_fma) return launch_dycore_step_ws_fma(in, out, g, nz, nj, k, sp, s, phys, base);
   return launch_dycore_step_ws(in, out, g, nz, nj, k, sp, s, phys, base);
 #endif
 }
@@ -999,14 +1013,15 @@ void dycore_step(hfb_ctx* c, Stats& st, bool with_physics = false) {
         });
       else if (fused_physics)
         launch(c, st, "full_step", [&] {
-          return rem ? launch_dycore_step_ws(in, out, grid_of(th), nz, th.lay.nj, k, sp,
-                                             ks(c), &ph, nullptr, rem)
+          return rem ? (c->arith_fma ? launch_dycore_step_ws_fma : launch_dycore_step_ws)(
+                           in, out, grid_of(th), nz, th.lay.nj, k, sp, ks(c), &ph, nullptr, rem, 0)
                      : launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, ks(c), &ph);
         });
       else
         launch(c, st, "dycore_step", [&] {
-          return rem ? launch_dycore_step_ws(in, out, grid_of(th), nz, th.lay.nj, k, sp,
-                                             ks(c), nullptr, nullptr, rem)
+          return rem ? (c->arith_fma ? launch_dycore_step_ws_fma : launch_dycore_step_ws)(
+                           in, out, grid_of(th), nz, th.lay.nj, k, sp, ks(c), nullptr, nullptr,
+                           rem, 0)
                      : launch_step(c, in, out, grid_of(th), nz, th.lay.nj, k, sp, ks(c));
         });
     } else {
@@ -1387,17 +1402,19 @@ void peer_wait(hfb_ctx* c, cudaStream_t st) {
   std::vector<const uint64_t*> mine;
   for (const Nbr& n : peer_neighbours(c->decomp))
     mine.push_back(c->peer_sig + kSigHalo + (n.dy + 1) * 3 + (n.dx + 1));
-  cuda_check(launch_peer_wait(mine.data(), static_cast<int>(mine.size()), c->halo_epoch, st),
+  cuda_check(launch_peer_wait(mine.data(), static_cast<int>(mine.size()),
+                              c->peer_sig + kSigEpoch, st),
              "peer wait");
 }
 
 // release the next epoch to every neighbour (I am at offset (-dx, -dy) from each)
 void peer_signal(hfb_ctx* c, cudaStream_t st) {
-  const uint64_t epoch = ++c->halo_epoch;
+  ++c->halo_epoch;  // host mirror (statistics); the kernels use the device counter
   std::vector<uint64_t*> flags;
   for (const Nbr& n : peer_neighbours(c->decomp))
     flags.push_back(c->peers.at(n.rank).sig + kSigHalo + (1 - n.dy) * 3 + (1 - n.dx));
-  cuda_check(launch_peer_signal(flags.data(), static_cast<int>(flags.size()), epoch, st),
+  cuda_check(launch_peer_signal(flags.data(), static_cast<int>(flags.size()),
+                                c->peer_sig + kSigEpoch, st),
              "peer signal");
 }
 
@@ -1450,7 +1467,7 @@ void peer_exchange(hfb_ctx* c, const std::vector<const char*>& fields, cudaStrea
       }
     return;
   }
-  const uint64_t epoch = ++c->halo_epoch;
+  ++c->halo_epoch;
   ++c->peer_pushes;
   PeerPush push{};
   std::vector<uint64_t*> remote_flags;
@@ -1496,10 +1513,11 @@ void peer_exchange(hfb_ctx* c, const std::vector<const char*>& fields, cudaStrea
       my_flags.push_back(c->peer_sig + kSigHalo + (dy + 1) * 3 + (dx + 1));
     }
   cuda_check(launch_peer_push(push, st), "peer halo push");
-  cuda_check(launch_peer_signal(remote_flags.data(), static_cast<int>(remote_flags.size()), epoch,
-                                st),
+  cuda_check(launch_peer_signal(remote_flags.data(), static_cast<int>(remote_flags.size()),
+                                c->peer_sig + kSigEpoch, st),
              "peer signal");
-  cuda_check(launch_peer_wait(my_flags.data(), static_cast<int>(my_flags.size()), epoch, st),
+  cuda_check(launch_peer_wait(my_flags.data(), static_cast<int>(my_flags.size()),
+                              c->peer_sig + kSigEpoch, st),
              "peer wait");
 }
 
@@ -1669,8 +1687,8 @@ const double* peer_gather(hfb_ctx* c, int64_t nx, int64_t ny) {
     mine.push_back(c->peer_sig + kSigRed + q);
   }
   cuda_check(launch_peer_push(push, c->stream), "peer gather push");
-  cuda_check(launch_peer_signal(flags.data(), n, epoch, c->stream), "peer signal");
-  cuda_check(launch_peer_wait(mine.data(), n, epoch, c->stream), "peer wait");
+  cuda_check(launch_peer_signal(flags.data(), n, nullptr, c->stream, epoch), "peer signal");
+  cuda_check(launch_peer_wait(mine.data(), n, nullptr, c->stream, epoch), "peer wait");
   return c->peer_gather + par;
 }
 
@@ -1801,7 +1819,8 @@ void hfb_destroy(hfb_ctx* c) {
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (c->peer_sig) cudaFree(c->peer_sig);
   if (c->peer_gather) cudaFree(c->peer_gather);
-  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  for (auto& kv : c->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   if (c->nccl_comm) nccl().CommDestroy(c->nccl_comm);
   for (auto& t : c->pending) {
     cudaEventDestroy(t.a);
@@ -2031,60 +2050,97 @@ hfb_status hfb_synchronize(hfb_ctx* c) {
 
 void* hfb_stream(hfb_ctx* c) { return c ? c->stream : nullptr; }
 
-hfb_status hfb_run_graph(hfb_ctx* c, const char* entry, int64_t steps, hfb_launch_stats* stats) {
-  return guarded([&] {
-    if (!c || !c->app) fail(HFB_CONFIG, "no program loaded");
-    if (steps < 1) return;
-    cudaSetDevice(c->device);
-    std::string r = routine_name(entry);
-    if (entry_has_transfers(c->app, r))
-      fail(HFB_CONFIG, "entry '%s' performs host transfers; cannot be graph-captured", entry);
-    if (c->decomposed && c->decomp.px * c->decomp.py > 1)
-      fail(HFB_CONFIG, "graph replay of decomposed contexts is not supported");
-    // Capture `steps` steps; an even step count returns every double buffer to its
-    // starting side, so the graph can be replayed; odd counts are re-captured.
-    std::string key = r + ":" + std::to_string(steps);
-    // no allocation may happen during capture: materialise every buffer first
-    for (auto& [n, s] : c->slots)
-      if (s.decl->pingpong && s.has_device) ensure_device(c, s, true, r == "rk3_step" ? 3 : 0);
-    if (r == "asuca_step" && c->app->app == "dycore" && !c->app->plugin) asuca_prepare(c);
+// Capture `steps` calls of a stream-only entry into a CUDA graph (cached per entry, step
+// count, starting buffer sides and peer hand-off state: a graph ending on the other
+// buffer side is replayed from there by a second cached graph) and launch it.
+void graph_launch(hfb_ctx* c, const char* entry, int64_t steps, hfb_launch_stats* stats,
+                  bool sync) {
+  if (!c || !c->app) fail(HFB_CONFIG, "no program loaded");
+  if (steps < 1) return;
+  cudaSetDevice(c->device);
+  std::string r = routine_name(entry);
+  if (entry_has_transfers(c->app, r))
+    fail(HFB_CONFIG, "entry '%s' performs host transfers; cannot be graph-captured", entry);
+  const bool multi = c->decomposed && c->decomp.px * c->decomp.py > 1;
+  if (multi && !c->peer)
+    fail(HFB_CONFIG, "graph replay of a decomposed context needs the peer transport "
+         "(hfb_peer_attach); NCCL and in-process groups run the step loop");
+  if (multi && c->app->app == "reduction")
+    fail(HFB_CONFIG, "decomposed reductions gather through host-numbered epochs; run them "
+         "with hfb_run");
+  // no allocation may happen during capture: materialise every buffer first
+  for (auto& [n, s] : c->slots)
+    if (s.decl->pingpong && s.has_device) ensure_device(c, s, true, r == "rk3_step" ? 3 : 0);
+  if (r == "asuca_step" && c->app->app == "dycore" && !c->app->plugin) asuca_prepare(c);
+  std::string key = r + ":" + std::to_string(steps) + (c->peer_fused ? ":f" : ":p");
+  for (auto& [n, s] : c->slots) key += ":" + n + "=" + std::to_string(s.cur);
+  auto it = c->graphs.find(key);
+  if (it == c->graphs.end()) {
     cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
     std::map<std::string, int> cur0;
     for (auto& [n, s] : c->slots) cur0[n] = s.cur;
-    if (c->graph_key != key || c->graph_cur0 != cur0) {
-      if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
-      c->graph_exec = nullptr;
-      c->graph_key.clear();
-      Stats st;
-      cudaGraph_t g;
-      cuda_check(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal),
-                 "cudaStreamBeginCapture");
-      c->capturing = true;
-      try {
-        for (int64_t s = 0; s < steps; ++s) entry_fn(c->app)(c, r, st);
-        c->capturing = false;
-      } catch (...) {
-        c->capturing = false;
-        cudaStreamEndCapture(c->stream, &g);
-        for (auto& [n, s] : c->slots) s.cur = cur0[n];
-        throw;
-      }
-      cuda_check(cudaStreamEndCapture(c->stream, &g), "cudaStreamEndCapture");
-      cuda_check(cudaGraphInstantiate(&c->graph_exec, g, 0), "cudaGraphInstantiate");
-      cudaGraphDestroy(g);
-      c->graph_key = key;
-      c->graph_cur0 = cur0;
-      c->graph_cur1.clear();
-      for (auto& [n, s] : c->slots) c->graph_cur1[n] = s.cur;  // buffer sides after the steps
-      c->graph_stats = hfb_launch_stats{st.launches, st.threads, st.guard_returns, st.native};
-      // a graph whose steps do not return every buffer to its side is single-use
-      if (c->graph_cur1 != cur0) c->graph_key += ":once";
+    const bool fused0 = c->peer_fused;
+    const int64_t p0 = c->peer_pushes, h0 = c->peer_handoffs, b0 = c->halo_bytes,
+                  e0 = static_cast<int64_t>(c->halo_epoch);
+    Stats st;
+    cudaGraph_t g;
+    cuda_check(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal),
+               "cudaStreamBeginCapture");
+    c->capturing = true;
+    try {
+      for (int64_t s = 0; s < steps; ++s) entry_fn(c->app)(c, r, st);
+      c->capturing = false;
+    } catch (...) {
+      c->capturing = false;
+      cudaStreamEndCapture(c->stream, &g);
+      for (auto& [n, s] : c->slots) s.cur = cur0[n];
+      c->peer_fused = fused0;
+      c->peer_pushes = p0;
+      c->peer_handoffs = h0;
+      c->halo_bytes = b0;
+      c->halo_epoch = static_cast<uint64_t>(e0);
+      throw;
     }
-    cuda_check(cudaGraphLaunch(c->graph_exec, c->stream), "cudaGraphLaunch");
-    for (auto& [n, sl] : c->slots) sl.cur = c->graph_cur1[n];
-    cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
-    if (stats) *stats = c->graph_stats;
-  });
+    cuda_check(cudaStreamEndCapture(c->stream, &g), "cudaStreamEndCapture");
+    hfb_ctx::GraphEntry ge;
+    cuda_check(cudaGraphInstantiate(&ge.exec, g, 0), "cudaGraphInstantiate");
+    cudaGraphDestroy(g);
+    for (auto& [n, s] : c->slots) ge.cur1[n] = s.cur;
+    ge.stats = hfb_launch_stats{st.launches, st.threads, st.guard_returns, st.native};
+    ge.peer_fused1 = c->peer_fused;
+    ge.pushes = c->peer_pushes - p0;
+    ge.handoffs = c->peer_handoffs - h0;
+    ge.halo_bytes = c->halo_bytes - b0;
+    ge.epochs = static_cast<int64_t>(c->halo_epoch) - e0;
+    // capturing recorded the host-side effects without running anything: undo them, the
+    // launch below applies them once
+    for (auto& [n, s] : c->slots) s.cur = cur0[n];
+    c->peer_fused = fused0;
+    c->peer_pushes = p0;
+    c->peer_handoffs = h0;
+    c->halo_bytes = b0;
+    c->halo_epoch = static_cast<uint64_t>(e0);
+    it = c->graphs.emplace(key, std::move(ge)).first;
+  }
+  const hfb_ctx::GraphEntry& ge = it->second;
+  cuda_check(cudaGraphLaunch(ge.exec, c->stream), "cudaGraphLaunch");
+  for (auto& [n, sl] : c->slots) sl.cur = ge.cur1.at(n);
+  c->peer_fused = ge.peer_fused1;
+  c->peer_pushes += ge.pushes;
+  c->peer_handoffs += ge.handoffs;
+  c->halo_bytes += ge.halo_bytes;
+  c->halo_epoch += static_cast<uint64_t>(ge.epochs);
+  if (sync) cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  if (stats) *stats = ge.stats;
+}
+
+hfb_status hfb_run_graph(hfb_ctx* c, const char* entry, int64_t steps, hfb_launch_stats* stats) {
+  return guarded([&] { graph_launch(c, entry, steps, stats, true); });
+}
+
+hfb_status hfb_enqueue_graph(hfb_ctx* c, const char* entry, int64_t steps,
+                             hfb_launch_stats* stats) {
+  return guarded([&] { graph_launch(c, entry, steps, stats, false); });
 }
 
 hfb_status hfb_device_array(hfb_ctx* c, const char* module, const char* name, hfb_array* out) {
@@ -2469,6 +2525,10 @@ hfb_status hfb_set_option(hfb_ctx* c, const char* key, const char* value) {
              "make -C csrc variants -> libhfb_variants.so)", v.c_str());
       }
 #endif
+    } else if (k == "arith") {
+      if (v != "exact" && v != "fma")
+        fail(HFB_CONFIG, "option arith takes exact or fma, got '%s'", v.c_str());
+      c->arith_fma = v == "fma";
     } else if (k == "overlap") {
       if (v != "0" && v != "1") fail(HFB_CONFIG, "option overlap takes 0 or 1, got '%s'", v.c_str());
       c->overlap = v == "1";
@@ -2479,7 +2539,7 @@ hfb_status hfb_set_option(hfb_ctx* c, const char* key, const char* value) {
       fail(HFB_CONFIG, "option debug_skip exists only in the A/B build (libhfb_variants.so)");
 #endif
     } else {
-      fail(HFB_CONFIG, "unknown option '%s' (variant, overlap, debug_skip)", k.c_str());
+      fail(HFB_CONFIG, "unknown option '%s' (variant, arith, overlap, debug_skip)", k.c_str());
     }
   });
 }

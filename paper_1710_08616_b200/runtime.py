@@ -47,7 +47,7 @@ EXPORTS = [
     "hfb_set_reduction_order", "hfb_program_name", "hfb_program_module", "hfb_plugin_prepare",
     "hfb_plugin_written", "hfb_plugin_view", "hfb_plugin_scratch", "hfb_plugin_host", "hfb_plugin_host_ref",
     "hfb_peer_export", "hfb_peer_attach", "hfb_peer_stats", "hfb_transfer_bytes",
-    "hfb_set_option", "hfb_variants_build",
+    "hfb_set_option", "hfb_variants_build", "hfb_enqueue_graph",
 ]
 
 # module of each built-in program (the apps' state modules)
@@ -122,6 +122,7 @@ def lib():
         L.hfb_stream.argtypes = [P]
         L.hfb_stream.restype = P
         L.hfb_run_graph.argtypes = [P, S, i64, c.POINTER(_Stats)]
+        L.hfb_enqueue_graph.argtypes = [P, S, i64, c.POINTER(_Stats)]
         L.hfb_decomp_init.argtypes = [c.POINTER(Decomp)]
         L.hfb_decomp_faces.argtypes = [c.POINTER(Decomp), c.c_int32, c.POINTER(i64),
                                        c.POINTER(i64)]
@@ -348,6 +349,12 @@ class Engine:
     def run_graph(self, entry, steps):
         st = _Stats()
         _check(lib().hfb_run_graph(self._h, _b(entry), int(steps), ctypes.byref(st)))
+        return LaunchStats(st.launches, st.threads, st.guard_returns, st.native_launches)
+
+    def enqueue_graph(self, entry, steps):
+        """Launch (without synchronising) the cached CUDA graph of `steps` steps."""
+        st = _Stats()
+        _check(lib().hfb_enqueue_graph(self._h, _b(entry), int(steps), ctypes.byref(st)))
         return LaunchStats(st.launches, st.threads, st.guard_returns, st.native_launches)
 
     def synchronize(self):

@@ -24,6 +24,10 @@ pytestmark = pytest.mark.gpu
 PEER_CASES = {
     "dycore": Case("p_dycore", "dycore", dict(nx=70, ny=45, nz=20, nsteps=3),
                    dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
+    "dycore4": Case("p_dycore4", "dycore", dict(nx=70, ny=45, nz=20, nsteps=4),
+                    dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
+    "dycore_full4": Case("p_full4", "dycore_full", dict(nx=70, ny=45, nz=20, nsteps=4),
+                         dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS)),
     "dycore_full": Case("p_full", "dycore_full", dict(nx=70, ny=45, nz=20, nsteps=2),
                         dict(DYCORE_SCALARS, **PHYS_SCALARS),
                         dict(DYCORE_FILLS, **PHYS_FILLS)),
@@ -40,7 +44,7 @@ PEER_CASES = {
     "reduction": Case("p_red", "reduction", dict(nx=67, ny=45, nz=20), dict(total=0.0),
                       {"y": (6, 0.0, 1.0)}),
 }
-HALO = {"dycore": 2, "dycore_full": 2, "dycore_rk3": 2, "diffusion": 1, "reduction": 0,
+HALO = {"dycore": 2, "dycore4": 2, "dycore_full4": 2, "dycore_full": 2, "dycore_rk3": 2, "diffusion": 1, "reduction": 0,
         "bounded": 1, "damping": 0}
 
 
@@ -75,11 +79,16 @@ def worker(rank, world, port, name, px, py, q, per_step=False, ordered=False, op
             _, lower = decl(case.app, n, ints)
             eng.bind(n, tiles[n], lower=lower)
         eng.attach_peers()
-        if per_step:  # the bench's device-resident path: copy-in, n enqueued steps, copy-out
+        if per_step:  # the bench's device-resident path: copy-in, n steps, copy-out
+            step = "full_step" if case.app == "dycore_full" else "dycore_step"
             for n in tiles:
                 eng.copy_to_device(n)
-            for _ in range(case.ints["nsteps"]):
-                stats = eng.enqueue("dycore_step")
+            if per_step == "graph":  # CUDA graphs of 2 steps, replayed
+                for _ in range(case.ints["nsteps"] // 2):
+                    stats = eng.run_graph(step, 2)
+            else:
+                for _ in range(case.ints["nsteps"]):
+                    stats = eng.enqueue(step)
             eng.synchronize()
             for n in tiles:
                 eng.copy_from_device(n)
@@ -175,6 +184,21 @@ def test_peer_fused_halo_hand_off_per_step_entries(overlap):
         assert bits_equal(out[k], ref[k]), k
     # the first step after the copy-in pushes, the following ones are handed off
     assert all(p[1] == (1, case.ints["nsteps"] - 1) for p in parts), [p[1] for p in parts]
+
+
+@pytest.mark.parametrize("name,px,py", [("dycore4", 2, 2), ("dycore4", 4, 2), ("dycore_full4", 3, 2)])
+def test_peer_graph_replay_decomposed(name, px, py):
+    """Decomposed steps replayed from CUDA graphs (hfb_run_graph) over the peer transport:
+    the halo epochs live in device memory, so each replay of the captured push / signal /
+    wait and epilogue hand-off sequence uses fresh epochs. Two replays of a 2-step graph
+    equal the undecomposed oracle's 4 steps bit for bit; the exchanges are one push (the
+    first step after the copy-in) and three epilogue hand-offs."""
+    case, garr, out, parts = run_peer(name, px, py, per_step="graph")
+    ref = {k: v.copy() for k, v in garr.items()}
+    run_oracle(case, ref)
+    for k in APPS[case.app].outputs:
+        assert bits_equal(out[k], ref[k]), f"{name} {px}x{py}: {k} differs"
+    assert all(p[1] == (1, 3) for p in parts), [p[1] for p in parts]
 
 
 @pytest.mark.parametrize("px,py", [(2, 2), (3, 1)])

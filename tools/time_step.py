@@ -14,10 +14,14 @@ import numpy as np  # noqa: E402
 
 nx, ny, nz = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (512, 512, 58)))
 app = sys.argv[4] if len(sys.argv) > 4 else "dycore"
+arith = sys.argv[5] if len(sys.argv) > 5 else "exact"
 full = app == "full"  # the full timestep: dycore + column physics (full_step)
-if full:
+asuca = app == "asuca"  # the ASUCA time scheme (asuca_step)
+if full or asuca:
     app = "dycore"
 eng = hfb.Engine(app)
+if app == "dycore":
+    eng.set_option("arith", arith)
 for k, v in dict(nx=nx, ny=ny, nz=nz, nsteps=1).items():
     eng.set(k, v)
 if app == "dycore":
@@ -32,6 +36,13 @@ if app == "dycore":
         arrs["tsfc"] = synthetic.field((nx, ny), 13, 300.0, 2.0, order="F")
         arrs["colm"] = synthetic.field((nx, ny), 14, 300.0, 0.5, order="F")
         entry = "full_step"
+    if asuca:
+        kdmp = nz - max(1, nz // 4)
+        for k, v in dict(nsound=6, nbnd=8, kdmp=kdmp).items():
+            eng.set(k, v)
+        for k, v in dict(rdmp=0.2, rnbnd=1.0 / 8, rnzd=1.0 / (nz - kdmp)).items():
+            eng.set(k, v)
+        entry, bpp = "asuca_step", 2496
 else:
     eng.set("coef", 0.1)
     arrs = {"t_old": synthetic.field((nz, nx, ny), 1, 280.0, 10.0, order="F"),
@@ -51,5 +62,19 @@ for _ in range(n):
 e1.record(s)
 eng.synchronize()
 ms = e0.elapsed_time(e1) / n
-print(f"{app} {nx}x{ny}x{nz}: {ms:.4f} ms/step  {nx*ny*nz/ms*1e3:.3e} pt/s  "
+print(f"{entry} [{arith}] {nx}x{ny}x{nz}: {ms:.4f} ms/step  {nx*ny*nz/ms*1e3:.3e} pt/s  "
       f"{bpp*nx*ny*nz/ms/1e6:.0f} GB/s(alg)")
+if asuca:  # per-kernel device times of 3 more steps (CUDA events around every launch)
+    eng.profile(True, clear=True)
+    eng.profile(True)
+    for _ in range(3):
+        eng.enqueue(entry)
+    eng.synchronize()
+    eng.profile(False)
+    pts = nx * ny * nz
+    for kname, b in (("asuca_tend", 80), ("asuca_acoustic_a", 80), ("asuca_acoustic_b", 112),
+                     ("asuca_stage_end", 48)):
+        t, n = eng.kernel_time(kname)
+        if n:
+            print(f"  {kname}: {n // 3} launches/step, {t / n:.4f} ms each, "
+                  f"{b * pts / (t / n) / 1e6:.0f} GB/s(alg, {b} B/pt)")
