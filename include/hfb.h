@@ -85,6 +85,16 @@ hfb_status hfb_bind_array(hfb_ctx* ctx, const char* module, const char* name, in
                           const int64_t* lower, const int64_t* upper, double* host,
                           const int64_t* strides, unsigned flags);
 
+/* Element init flags of a bound array (ArrayValue::init, interp.hpp:16-28; SURVEY §8(b)
+ * `init_or_null`): one byte per element at the same element offsets (strides) as the
+ * host buffer, caller-owned like the data, NULL unbinds. When flags are bound (or the
+ * context runs checked, hfb_set_option "checked"), the device copy carries init flags:
+ * hfrt_copy_to_device uploads them, hfrt_device_allocate clears them, kernels set them
+ * for the elements they write, a read of an unset element fails with HFB_RUNTIME "read
+ * of unset element of '<name>'" (interp.cpp:505-507), and hfrt_copy_from_device writes
+ * them back. Arrays bound without flags count as fully set. */
+hfb_status hfb_bind_init(hfb_ctx* ctx, const char* module, const char* name, uint8_t* init);
+
 /* --- transfers: the generated-code runtime (codegen.cpp:580-600) ------------------ */
 /* residency of a bound array: 0 = Host, 1 = Device, 2 = Both (interp.hpp:30);
  * has_device reports whether a device copy exists */
@@ -243,6 +253,12 @@ hfb_status hfb_set_reduction_order(hfb_ctx* ctx, int ordered);
  *   warp-specialised step), "generic" (portable kernels), "split" (advect + acoustic
  *   kernels), "single_role" (fused, one role per warp); "tma" and "ws2" (measured-slower
  *   alternatives) exist only in the A/B build libhfb_variants.so, elsewhere HFB_CONFIG.
+ * "arith": "exact" (default, bit-identical to the reference's binary64 evaluation) or
+ *   "fma" (the fused step compiled with FMA contraction; within 1e-12 relative per field
+ *   after one step, tests/test_gpu_tolerance.py).
+ * "checked": "1" tracks element init flags on the device (see hfb_bind_init) — the
+ *   debug mode in which programs generated with `hfc --checked` also check every array
+ *   access against the declared bounds (interp.cpp:487-492).
  * "overlap": "1" (default) overlaps the halo exchange with the interior columns, "0"
  *   serialises (both orders are bit-identical).
  * "debug_skip": A/B build only, timing experiments (1 = no advection, 2 = no acoustic).

@@ -82,6 +82,20 @@ hfb_status hfb_plugin_host_ref(hfb_ctx* ctx, const char* name, hfb_host_ref* out
 hfb_status hfb_plugin_scratch(hfb_ctx* ctx, const char* key, int rank, const int64_t* lower,
                               const int64_t* upper, const int* roles);
 
+/* --- checked mode (programs generated with `hfc --checked`) ------------------------- */
+/* Declared bounds and element init flags of a module or scratch array, for the checked
+ * accessors: `dinit` (device, one byte per element at the data's element offsets
+ * relative to hfb_view.origin) and `hinit` (the caller's host flags bound with
+ * hfb_bind_init, at the host buffer's offsets; NULL if none). Module arrays whose init
+ * flags were never tracked count as fully set. */
+hfb_status hfb_plugin_array_info(hfb_ctx* ctx, const char* name, int* rank, int64_t lower[4],
+                                 int64_t upper[4], uint8_t** dinit, uint8_t** hinit);
+/* a routine-local array starts every routine invocation with no element set
+ * (elaborate_locals, interp.cpp:936-979) */
+hfb_status hfb_plugin_scratch_clear_init(hfb_ctx* ctx, const char* key);
+/* fail the current run with `status` and the message (the reference's texts) */
+hfb_status hfb_plugin_error(hfb_ctx* ctx, hfb_status status, const char* msg);
+
 #ifdef __cplusplus
 }
 #endif

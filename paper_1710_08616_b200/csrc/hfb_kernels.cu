@@ -119,6 +119,65 @@ cudaError_t launch_relayout(const double* src, double* dst, const Relayout& r, b
 }
 
 // ============================================================================
+// element init flags (the reference's ArrayValue::init, interp.hpp:16-28) for the
+// checked mode: one byte per element in the device layout of its array
+// ============================================================================
+namespace {
+__global__ void k_relayout_u8(const uint8_t* src, uint8_t* dst, Relayout r, bool to_device,
+                              int64_t n) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t q = e, ho = 0, dof = 0;
+    for (int role = 0; role < 4; ++role) {
+      const int64_t x = q % r.ext[role];
+      q /= r.ext[role];
+      ho += x * r.hs[role];
+      dof += x * r.ds[role];
+    }
+    if (to_device)
+      dst[dof] = src[ho];
+    else
+      dst[ho] = src[dof];
+  }
+}
+
+// mode 0: *flag = 1 if any element of the box is unset; mode 1: set every element
+__global__ void k_init_box(uint8_t* init, InitBox b, int mode, int* flag) {
+  const int64_t n = b.n[0] * b.n[1] * b.n[2] * b.n[3];
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t q = e, off = 0;
+    for (int role = 0; role < 4; ++role) {
+      off += (b.lo[role] + q % b.n[role]) * b.ds[role];
+      q /= b.n[role];
+    }
+    if (mode == 1)
+      init[off] = 1;
+    else if (!init[off])
+      *flag = 1;
+  }
+}
+}  // namespace
+
+cudaError_t launch_relayout_u8(const uint8_t* src, uint8_t* dst, const Relayout& r,
+                               bool to_device, cudaStream_t s) {
+  const int64_t n = r.ext[0] * r.ext[1] * r.ext[2] * r.ext[3];
+  if (n <= 0) return cudaSuccess;
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  k_relayout_u8<<<blocks, 256, 0, s>>>(src, dst, r, to_device, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_box(uint8_t* init, const InitBox& b, int mode, int* flag,
+                            cudaStream_t s) {
+  const int64_t n = b.n[0] * b.n[1] * b.n[2] * b.n[3];
+  if (n <= 0) return cudaSuccess;
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  k_init_box<<<blocks, 256, 0, s>>>(init, b, mode, flag);
+  return cudaGetLastError();
+}
+
+// ============================================================================
 // diffusion.h90:23-41 — 7-point stencil with the Dirichlet copy on the GLOBAL
 // boundary; K neighbours live in registers (k-1, k, k+1 rotate), I/J neighbours
 // come from L1 (each is loaded by the adjacent threads of the same warp/block).

@@ -28,6 +28,16 @@ struct Relayout {
 };
 cudaError_t launch_relayout(const double* src, double* dst, const Relayout& r, bool to_device,
                             cudaStream_t s);
+// the same for one-byte element init flags (checked mode)
+cudaError_t launch_relayout_u8(const uint8_t* src, uint8_t* dst, const Relayout& r,
+                               bool to_device, cudaStream_t s);
+// a box of device elements per role (I, J, K, L): lo (0-based), n, device strides
+struct InitBox {
+  int64_t lo[4], n[4], ds[4];
+};
+// mode 0: *flag = 1 when any element of the box is unset; mode 1: mark the box set
+cudaError_t launch_init_box(uint8_t* init, const InitBox& b, int mode, int* flag,
+                            cudaStream_t s);
 
 // ---- diffusion.h90 (hfk0 + hfk1 fused: write the step result to one or two outputs)
 cudaError_t launch_diffusion(const double* t_old, double* out1, double* out2, Grid3 g,

@@ -220,6 +220,11 @@ struct Slot {
   double* dev[3] = {nullptr, nullptr, nullptr};  // [2] only for RK3 stage states
   int cur = 0;
   int32_t has_device = 0;  // a device copy exists (bool; int32 for hfb_plugin_host_ref)
+  // element init flags (ArrayValue::init, interp.hpp:16-28): the caller's, at the host
+  // buffer's element offsets (hfb_bind_init), and the device copy's, one byte per element
+  // in the device layout (kept while the context tracks init: checked mode or bound flags)
+  uint8_t* hinit = nullptr;
+  uint8_t* dinit = nullptr;
   Residency res = kHost;
   cudaStream_t stream = nullptr;  // owning context's stream
 
@@ -259,6 +264,7 @@ constexpr int kSigHalo = 0, kSigEpoch = 9, kSigRed = 16, kSigSlots = 80, kSigWor
 struct Scratch {
   Layout lay;
   double* dev = nullptr;
+  uint8_t* dinit = nullptr;  // checked generated programs: element init flags
   int rank = 0;
   int64_t lower[4] = {1, 1, 1, 1}, upper[4] = {1, 1, 1, 1};
   Role roles[4] = {kRoleI, kRoleJ, kRoleK, kRoleL};
@@ -343,6 +349,10 @@ struct hfb_ctx {
   int debug_skip = 0;  // A/B build only: 1 = no advection, 2 = no acoustic (timing)
   // hfb_set_option "arith": the fused step's FMA-contracted build (tolerance mode)
   bool arith_fma = false;
+  // hfb_set_option "checked": track element init flags on the device and check reads
+  // (the reference's unset-read and bounds errors, interp.cpp:487-507)
+  bool checked = false;
+  int* chk_flag = nullptr;  // device word of the init-box checks
   // per-kernel CUDA-event timing (hfb_profile)
   bool prof = false;
   bool capturing = false;
@@ -474,11 +484,118 @@ Relayout relayout_of(const Slot& s) {
 // ---------------------------------------------------------------------------
 // transfers (interp.cpp:1369-1415)
 // ---------------------------------------------------------------------------
+// ---- element init flags (checked mode / bound flags) -------------------------------
+bool tracks_init(const hfb_ctx* c, const Slot& s) { return c->checked || s.hinit; }
+
+void ensure_dinit(hfb_ctx* c, Slot& s, int fill) {
+  if (s.dinit) return;
+  cuda_check(cudaMalloc(&s.dinit, static_cast<size_t>(s.lay.alloc_elems)), "cudaMalloc(init)");
+  cuda_check(cudaMemsetAsync(s.dinit, fill, static_cast<size_t>(s.lay.alloc_elems), c->stream),
+             "cudaMemsetAsync(init)");
+}
+
+// the device copy's init flags := the bound host flags (copy-in) / all set / all clear
+void dinit_upload(hfb_ctx* c, Slot& s) {
+  ensure_dinit(c, s, 1);
+  if (!s.hinit) {
+    cuda_check(cudaMemsetAsync(s.dinit, 1, static_cast<size_t>(s.lay.alloc_elems), c->stream),
+               "cudaMemsetAsync(init)");
+    return;
+  }
+  ensure_staging(c, static_cast<size_t>(s.count) * sizeof(double));
+  uint8_t* st = reinterpret_cast<uint8_t*>(c->staging);
+  cuda_check(cudaMemcpyAsync(st, s.hinit, static_cast<size_t>(s.count), cudaMemcpyHostToDevice,
+                             c->stream),
+             "cudaMemcpyAsync(init H2D)");
+  cuda_check(launch_relayout_u8(st, s.dinit + s.lay.origin_off, relayout_of(s), true, c->stream),
+             "relayout(init H2D)");
+}
+
+void dinit_download(hfb_ctx* c, Slot& s) {
+  if (!s.hinit || !s.dinit) return;
+  ensure_staging(c, static_cast<size_t>(s.count) * sizeof(double));
+  uint8_t* st = reinterpret_cast<uint8_t*>(c->staging);
+  cuda_check(launch_relayout_u8(s.dinit + s.lay.origin_off, st, relayout_of(s), false, c->stream),
+             "relayout(init D2H)");
+  cuda_check(cudaMemcpyAsync(s.hinit, st, static_cast<size_t>(s.count), cudaMemcpyDeviceToHost,
+                             c->stream),
+             "cudaMemcpyAsync(init D2H)");
+  cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+}
+
+// A built-in kernel reads / writes the elements of `s` within declared bounds [lo, hi]
+// (per declared dim; NULL = the whole array). Reads of an unset element fail with the
+// reference's text (interp.cpp:505-507); writes set the flags (write_element, :534).
+InitBox init_box(const Slot& s, const int64_t* lo, const int64_t* hi) {
+  InitBox b{};
+  for (int r = 0; r < 4; ++r) {
+    b.lo[r] = 0;
+    b.n[r] = 1;
+  }
+  b.ds[kRoleI] = 1;
+  b.ds[kRoleJ] = s.lay.pitch;
+  b.ds[kRoleK] = s.lay.plane;
+  b.ds[kRoleL] = s.lay.volume;
+  for (int d = 0; d < s.rank; ++d) {
+    const Role r = s.decl->roles[d];
+    const int64_t l = lo ? lo[d] : s.lower[d], h = hi ? hi[d] : s.upper[d];
+    b.lo[r] = l - s.lower[d];
+    b.n[r] = h - l + 1;
+  }
+  return b;
+}
+
+void init_read(hfb_ctx* c, const char* name, const int64_t* lo = nullptr,
+               const int64_t* hi = nullptr) {
+  Slot& s = slot(c, name);
+  if (!s.dinit) return;  // not tracked: the contents count as defined
+  if (!c->chk_flag) cuda_check(cudaMalloc(&c->chk_flag, sizeof(int)), "cudaMalloc(flag)");
+  cuda_check(cudaMemsetAsync(c->chk_flag, 0, sizeof(int), c->stream), "cudaMemsetAsync");
+  const InitBox b = init_box(s, lo, hi);
+  for (int q = 0; q < 4; ++q)
+    if (b.n[q] <= 0) return;
+  cuda_check(launch_init_box(s.dinit + s.lay.origin_off, b, 0, c->chk_flag, c->stream),
+             "init check");
+  int flag = 0;
+  cuda_check(cudaMemcpyAsync(&flag, c->chk_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream),
+             "cudaMemcpyAsync(flag)");
+  cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  if (flag) fail(HFB_RUNTIME, "read of unset element of '%s'", name);
+}
+
+void init_written(hfb_ctx* c, const char* name, const int64_t* lo = nullptr,
+                  const int64_t* hi = nullptr) {
+  Slot& s = slot(c, name);
+  if (!s.dinit) return;
+  const InitBox b = init_box(s, lo, hi);
+  for (int q = 0; q < 4; ++q)
+    if (b.n[q] <= 0) return;
+  cuda_check(launch_init_box(s.dinit + s.lay.origin_off, b, 1, nullptr, c->stream), "init set");
+}
+
+// every array element a prognostic read touches except the upper wall plane of one dim
+// (u(nx), v(ny), w(nz) of the C-grid are never read)
+void init_read_but_last(hfb_ctx* c, const char* name, int dim) {
+  Slot& s = slot(c, name);
+  if (!s.dinit) return;
+  int64_t lo[4], hi[4];
+  for (int d = 0; d < s.rank; ++d) {
+    lo[d] = s.lower[d];
+    hi[d] = s.upper[d] - (d == dim ? 1 : 0);
+  }
+  init_read(c, name, lo, hi);
+}
+
 void do_device_allocate(hfb_ctx* c, Slot& s) {
   check_bounds(c, s);
   if (!s.has_device) {
     ensure_device(c, s, false);
     s.has_device = true;  // init flags cleared: contents undefined until written
+    if (tracks_init(c, s)) {
+      ensure_dinit(c, s, 0);
+      cuda_check(cudaMemsetAsync(s.dinit, 0, static_cast<size_t>(s.lay.alloc_elems), c->stream),
+                 "cudaMemsetAsync(init)");
+    }
   }
 }
 
@@ -496,6 +613,7 @@ void do_copy_to_device(hfb_ctx* c, Slot& s) {
   c->h2d_bytes += static_cast<int64_t>(bytes);
   cuda_check(launch_relayout(c->staging, s.d(), relayout_of(s), true, c->stream),
              "relayout(H2D)");
+  if (tracks_init(c, s)) dinit_upload(c, s);  // after the data: the staging is reused
   s.has_device = true;
   s.res = kBoth;
 }
@@ -515,6 +633,7 @@ void do_copy_from_device(hfb_ctx* c, Slot& s) {
              "cudaMemcpyAsync(D2H)");
   cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
   c->d2h_bytes += static_cast<int64_t>(bytes);
+  dinit_download(c, s);
   s.res = kBoth;
 }
 
@@ -707,6 +826,7 @@ void diffusion_step(hfb_ctx* c, Stats& st, bool write_t_new) {
   double coef = rval(c, "coef");
   dev_read(c, "t_old");
   dev_write(c, "t_new");
+  init_read(c, "t_old");  // the stencil and the boundary copy read every element
   Slot& to = slot(c, "t_old");
   Slot& tn = slot(c, "t_new");
   ensure_device(c, to, true);
@@ -725,6 +845,8 @@ void diffusion_step(hfb_ctx* c, Stats& st, bool write_t_new) {
   count_launch(st, nx, ny);
   dev_written(c, "t_new");
   dev_written(c, "t_old");
+  init_written(c, "t_new");
+  init_written(c, "t_old");
 }
 
 void diffusion_entry(hfb_ctx* c, const std::string& r, Stats& st) {
@@ -752,6 +874,8 @@ void damping_kernel(hfb_ctx* c, Stats& st) {
   dev_read(c, "dens_ref_f");
   dev_read(c, "dens_ptb_bnd");
   dev_write(c, "dens_ptb_damp");
+  init_read(c, "dens_ref_f");
+  init_read(c, "dens_ptb_bnd");
   Slot& ref = slot(c, "dens_ref_f");
   Slot& bnd = slot(c, "dens_ptb_bnd");
   Slot& dmp = slot(c, "dens_ptb_damp");
@@ -759,6 +883,7 @@ void damping_kernel(hfb_ctx* c, Stats& st) {
   launch(c, st, "hfk0_lateral_and_upper_damping", [&] { return launch_damping(ref.d(), bnd.d(), bnd.d() + bnd.lay.volume, dmp.d(), grid_of(ref), nz,
                           m, t, sp, c->stream); });
   dev_written(c, "dens_ptb_damp");
+  init_written(c, "dens_ptb_damp");
 }
 
 void damping_entry(hfb_ctx* c, const std::string& r, Stats& st) {
@@ -784,6 +909,11 @@ void bounded_kernel(hfb_ctx* c, Stats& st) {
   dev_write(c, "b");
   Slot& a = slot(c, "a");
   Slot& b = slot(c, "b");
+  if (a.dinit && nx >= 3 && ny >= 3) {  // 5-point interior update: all but the corners of a
+    const int64_t lo1[2] = {1, 2}, hi1[2] = {nx, ny - 1}, lo2[2] = {2, 1}, hi2[2] = {nx - 1, ny};
+    init_read(c, "a", lo1, hi1);
+    init_read(c, "a", lo2, hi2);
+  }
   halo_exchange(c, {"a"}, 1);
   Span sp = full_span(c, nx, ny);
   // startAt(2,2), endAt(nx-1, ny-1) on the GLOBAL domain
@@ -793,6 +923,10 @@ void bounded_kernel(hfb_ctx* c, Stats& st) {
   sp.jhi = std::min<int64_t>(ny, sp.gny - 1 - sp.j0);
   launch(c, st, "hfk0_interior_update", [&] { return launch_bounded(a.d(), b.d(), a.lay.pitch, sp, c->stream); });
   dev_written(c, "b");
+  if (nx >= 3 && ny >= 3) {
+    const int64_t lo[2] = {2, 2}, hi[2] = {nx - 1, ny - 1};
+    init_written(c, "b", lo, hi);
+  }
 }
 
 void bounded_entry(hfb_ctx* c, const std::string& r, Stats& st) {
@@ -820,11 +954,18 @@ void sf_tile_kernel(hfb_ctx* c, Stats& st) {
     fail(HFB_RUNTIME, "index %lld out of bounds [1, %lld] in dimension 1 of 'cover_frac'",
          (long long)lt, (long long)ntlm);
   Slot& cf = slot(c, "cover_frac");
+  {
+    const int64_t lo[3] = {lt, 1, 1}, hi[3] = {lt, nx, ny};
+    init_read(c, "cover_frac", lo, hi);
+  }
   Span sp = full_span(c, nx, ny);
   launch(c, st, "hfk0_sf_slab_flx_tile_run", [&] { return launch_sf_tile(cf.d() + (lt - 1) * cf.lay.plane, slot(c, "flx_sum_x").d(),
                           slot(c, "flx_sum_y").d(), slot(c, "wind_speed").d(), cf.lay.pitch, sp,
                           c->stream); });
-  for (const char* n : {"flx_sum_x", "flx_sum_y", "wind_speed"}) dev_written(c, n);
+  for (const char* n : {"flx_sum_x", "flx_sum_y", "wind_speed"}) {
+    dev_written(c, n);
+    init_written(c, n);
+  }
 }
 
 void sf_entry(hfb_ctx* c, const std::string& r, Stats& st) {
@@ -836,6 +977,7 @@ void sf_entry(hfb_ctx* c, const std::string& r, Stats& st) {
       // right after it arrives (same final state; no host compute on the product path)
       Slot& cf = slot(c, "cover_frac");
       int64_t nx = ival(c, "nx"), ny = ival(c, "ny");
+      init_read(c, "cover_frac");
       launch(c, st, "sf_setup", [&] { return launch_sf_setup(cf.d(), grid_of(cf), ival(c, "ntlm"), full_span(c, nx, ny),
                                c->stream); });
       dev_written(c, "cover_frac");
@@ -859,6 +1001,7 @@ void reduction_kernel(hfb_ctx* c, Stats& st) {
   int64_t nx = ival(c, "nx"), ny = ival(c, "ny"), nz = ival(c, "nz");
   double total = rval(c, "total");
   dev_read(c, "y");
+  init_read(c, "y");
   Slot& y = slot(c, "y");
   if (!c->red_partials) {
     cuda_check(cudaMalloc(&c->red_partials, sizeof(double) * (reduce_partials_needed() + 2)),
@@ -945,6 +1088,12 @@ PhysArgs phys_args(hfb_ctx* c, Slot& tsfc, Slot& colm) {
 void column_physics(hfb_ctx* c, Stats& st) {
   int64_t nx = ival(c, "nx"), ny = ival(c, "ny"), nz = ival(c, "nz");
   for (const char* n : {"rho", "th", "u", "v", "tsfc", "colm"}) dev_read(c, n);
+  for (const char* n : {"rho", "th", "tsfc", "colm"}) init_read(c, n);
+  if (slot(c, "u").dinit) {  // the surface wind: u, v of the lowest level only
+    const int64_t lo[3] = {1, 1, 1}, hi[3] = {1, nx, ny};
+    init_read(c, "u", lo, hi);
+    init_read(c, "v", lo, hi);
+  }
   DynConst k = make_dyn_const(rval(c, "dt"), rval(c, "rdx"), rval(c, "rdy"), rval(c, "rdz"),
                               rval(c, "cs2"), rval(c, "grav"), rval(c, "th0"));
   Slot &rho = slot(c, "rho"), &th = slot(c, "th"), &u = slot(c, "u"), &v = slot(c, "v");
@@ -954,7 +1103,24 @@ void column_physics(hfb_ctx* c, Stats& st) {
                                  full_span(c, nx, ny), c->stream);
   });
   count_launch(st, nx, ny);
-  for (const char* n : {"th", "colm"}) dev_written(c, n);
+  for (const char* n : {"th", "colm"}) {
+    dev_written(c, n);
+    init_written(c, n);
+  }
+}
+
+// what a dynamics step reads of the prognostic state (every element except the C-grid
+// wall planes u(nx), v(ny), w(nz), which the dialect never reads) and what it writes
+void dyn_init_reads(hfb_ctx* c, bool with_physics) {
+  for (const char* n : {"rho", "th", "p"}) init_read(c, n);
+  init_read_but_last(c, "u", 1);  // (nz, nx, ny): i
+  init_read_but_last(c, "v", 2);  // j
+  init_read_but_last(c, "w", 0);  // k
+  if (with_physics)
+    for (const char* n : {"tsfc", "colm"}) init_read(c, n);
+}
+void dyn_init_writes(hfb_ctx* c, std::initializer_list<const char*> names) {
+  for (const char* n : names) init_written(c, n);
 }
 
 // the fused warp-specialised step: cp.async-fed (product) or its TMA twin (measured
@@ -989,6 +1155,7 @@ void dycore_step(hfb_ctx* c, Stats& st, bool with_physics = false) {
   for (const char* n : {"th", "u", "v", "w", "p", "rho"}) dev_read(c, n);
   if (with_physics)
     for (const char* n : {"tsfc", "colm"}) dev_read(c, n);
+  dyn_init_reads(c, with_physics);
   Slot &rho = slot(c, "rho"), &th = slot(c, "th"), &u = slot(c, "u"), &v = slot(c, "v"),
        &w = slot(c, "w"), &p = slot(c, "p");
   for (Slot* s : {&th, &u, &v, &w, &p}) ensure_device(c, *s, true);
@@ -1050,10 +1217,12 @@ void dycore_step(hfb_ctx* c, Stats& st, bool with_physics = false) {
   count_launch(st, nx, ny + 1);
   for (int r = 0; r < 6; ++r) count_launch(st, nx, ny);
   for (const char* n : {"th", "u", "v", "w", "p"}) dev_written(c, n);
+  dyn_init_writes(c, {"th", "u", "v", "w", "p"});
   if (with_physics) {
     if (fused_physics) {
       count_launch(st, nx, ny);  // the generated code's column_physics launch
       dev_written(c, "colm");
+      init_written(c, "colm");
     } else {
       column_physics(c, st);
     }
@@ -1074,6 +1243,7 @@ void rk3_step(hfb_ctx* c, Stats& st) {
                      "an in-process group");
   const double dt = rval(c, "dt");
   for (const char* n : {"th", "u", "v", "w", "p", "rho"}) dev_read(c, n);
+  dyn_init_reads(c, false);
   Slot &rho = slot(c, "rho"), &th = slot(c, "th"), &u = slot(c, "u"), &v = slot(c, "v"),
        &w = slot(c, "w"), &p = slot(c, "p");
   Slot* prog[5] = {&th, &u, &v, &w, &p};
@@ -1112,6 +1282,7 @@ void rk3_step(hfb_ctx* c, Stats& st) {
   }
   for (Slot* s : prog) s->cur = s1;
   for (const char* n : {"th", "u", "v", "w", "p"}) dev_written(c, n);
+  dyn_init_writes(c, {"th", "u", "v", "w", "p"});
 }
 
 // apps/dycore/asuca.h90 asuca_step: the ASUCA time scheme (hfb_asuca.cu). Buffers per
@@ -1152,6 +1323,7 @@ void asuca_step(hfb_ctx* c, Stats& st) {
                rnzd = rval(c, "rnzd");
   if (nsound < 1) fail(HFB_RUNTIME, "nsound must be >= 1 (got %lld)", (long long)nsound);
   for (const char* n : {"th", "u", "v", "w", "p", "rho"}) dev_read(c, n);
+  dyn_init_reads(c, false);
   asuca_prepare(c);
   Slot &rho = slot(c, "rho"), &th = slot(c, "th"), &u = slot(c, "u"), &v = slot(c, "v"),
        &w = slot(c, "w"), &p = slot(c, "p");
@@ -1163,9 +1335,11 @@ void asuca_step(hfb_ctx* c, Stats& st) {
   const Grid3 g = grid_of(th);
   const int64_t nj = th.lay.nj;
   const Span sp = full_span(c, nx, ny);
-  double** A = c->asu;
-  const AsuTend F{A[0], A[1], A[2], A[3], A[4]};
-  double* pa = A[5];
+  // the scratch fields share the prognostic fields' layout: views at their origin
+  const int64_t o = th.lay.origin_off;
+  double* const* A = c->asu;
+  const AsuTend F{A[0] + o, A[1] + o, A[2] + o, A[3] + o, A[4] + o};
+  double* pa = A[5] + o;
   const double dtau = dt / static_cast<double>(nsound);  // asuca.h90 `dt / real(nsound)`
   const AsuAcoConst ca = make_asu_aco_const(0.5 * dtau, dtau, rdx, rdy, rdz, cs2, grav, th0,
                                             rdmp, nbnd, kdmp, rnbnd, rnzd);
@@ -1228,6 +1402,7 @@ void asuca_step(hfb_ctx* c, Stats& st) {
   th.cur = tx;
   rho.cur = rx;
   for (const char* n : {"rho", "th", "u", "v", "w", "p"}) dev_written(c, n);
+  dyn_init_writes(c, {"rho", "th", "u", "v", "w", "p"});
 }
 
 void dycore_entry(hfb_ctx* c, const std::string& r, Stats& st) {
@@ -1803,14 +1978,18 @@ void hfb_destroy(hfb_ctx* c) {
   for (auto& [n, s] : c->slots) {
     for (double* p : s.dev)
       if (p) cudaFree(p);
+    if (s.dinit) cudaFree(s.dinit);
     if (s.pinned && s.host) cudaHostUnregister(s.host);
     if (s.owned) cudaFreeHost(s.owned);
   }
   if (c->staging) cudaFree(c->staging);
   if (c->red_partials) cudaFree(c->red_partials);
   if (c->red_cols) cudaFree(c->red_cols);
-  for (auto& kv : c->scratch)
+  for (auto& kv : c->scratch) {
     if (kv.second.dev) cudaFree(kv.second.dev);
+    if (kv.second.dinit) cudaFree(kv.second.dinit);
+  }
+  if (c->chk_flag) cudaFree(c->chk_flag);
   for (double* p : c->asu)
     if (p) cudaFree(p);
   if (c->red_host) cudaFreeHost(c->red_host);
@@ -1899,6 +2078,14 @@ hfb_status hfb_get_scalar_f64(hfb_ctx* c, const char* module, const char* name, 
     Scalar& s = scalar_ref(c, lower(module), lower(name));
     if (!s.init) fail(HFB_RUNTIME, "read of unset variable '%s'", name);
     *v = s.type == SType::Real ? s.r : static_cast<double>(s.i);
+  });
+}
+
+hfb_status hfb_bind_init(hfb_ctx* c, const char* module, const char* name, uint8_t* init) {
+  return guarded([&] {
+    Slot& s = slot_ref(c, lower(module), lower(name));
+    if (!s.host) fail(HFB_CONFIG, "bind the host buffer of '%s' before its init flags", name);
+    s.hinit = init;
   });
 }
 
@@ -2525,6 +2712,9 @@ hfb_status hfb_set_option(hfb_ctx* c, const char* key, const char* value) {
              "make -C csrc variants -> libhfb_variants.so)", v.c_str());
       }
 #endif
+    } else if (k == "checked") {
+      if (v != "0" && v != "1") fail(HFB_CONFIG, "option checked takes 0 or 1, got '%s'", v.c_str());
+      c->checked = v == "1";
     } else if (k == "arith") {
       if (v != "exact" && v != "fma")
         fail(HFB_CONFIG, "option arith takes exact or fma, got '%s'", v.c_str());
@@ -2539,7 +2729,8 @@ hfb_status hfb_set_option(hfb_ctx* c, const char* key, const char* value) {
       fail(HFB_CONFIG, "option debug_skip exists only in the A/B build (libhfb_variants.so)");
 #endif
     } else {
-      fail(HFB_CONFIG, "unknown option '%s' (variant, arith, overlap, debug_skip)", k.c_str());
+      fail(HFB_CONFIG, "unknown option '%s' (variant, arith, checked, overlap, debug_skip)",
+           k.c_str());
     }
   });
 }
@@ -3337,6 +3528,61 @@ hfb_status hfb_plugin_host_ref(hfb_ctx* c, const char* name, hfb_host_ref* out) 
   });
 }
 
+hfb_status hfb_plugin_array_info(hfb_ctx* c, const char* name, int* rank, int64_t lower[4],
+                                 int64_t upper[4], uint8_t** dinit, uint8_t** hinit) {
+  return guarded([&] {
+    if (is_scratch(name)) {
+      auto it = c->scratch.find(name);
+      if (it == c->scratch.end()) fail(HFB_CONFIG, "no scratch array '%s'", name);
+      Scratch& sa = it->second;
+      if (!sa.dinit) {
+        cuda_check(cudaMalloc(&sa.dinit, static_cast<size_t>(sa.lay.alloc_elems)),
+                   "cudaMalloc(init)");
+        cuda_check(cudaMemsetAsync(sa.dinit, 0, static_cast<size_t>(sa.lay.alloc_elems),
+                                   c->stream),
+                   "cudaMemsetAsync(init)");
+      }
+      *rank = sa.rank;
+      for (int q = 0; q < 4; ++q) {
+        lower[q] = q < sa.rank ? sa.lower[q] : 1;
+        upper[q] = q < sa.rank ? sa.upper[q] : 1;
+      }
+      *dinit = sa.dinit + sa.lay.origin_off;
+      *hinit = nullptr;
+      return;
+    }
+    Slot& s = slot(c, name);
+    check_bounds(c, s);
+    *rank = s.rank;
+    for (int q = 0; q < 4; ++q) {
+      lower[q] = q < s.rank ? s.lower[q] : 1;
+      upper[q] = q < s.rank ? s.upper[q] : 1;
+    }
+    *dinit = nullptr;
+    if (s.has_device) {
+      if (!s.dinit) ensure_dinit(c, s, 1);  // never tracked: defined
+      *dinit = s.dinit + s.lay.origin_off;
+    }
+    *hinit = s.hinit;
+  });
+}
+
+hfb_status hfb_plugin_scratch_clear_init(hfb_ctx* c, const char* key) {
+  return guarded([&] {
+    auto it = c->scratch.find(key);
+    if (it == c->scratch.end()) fail(HFB_CONFIG, "no scratch array '%s'", key);
+    Scratch& sa = it->second;
+    if (sa.dinit)
+      cuda_check(cudaMemsetAsync(sa.dinit, 0, static_cast<size_t>(sa.lay.alloc_elems), c->stream),
+                 "cudaMemsetAsync(init)");
+  });
+}
+
+hfb_status hfb_plugin_error(hfb_ctx* c, hfb_status status, const char* msg) {
+  (void)c;
+  return guarded([&] { fail(status, "%s", msg ? msg : "error"); });
+}
+
 hfb_status hfb_plugin_scratch(hfb_ctx* c, const char* key, int rank, const int64_t* lower,
                               const int64_t* upper, const int* roles) {
   return guarded([&] {
@@ -3352,7 +3598,9 @@ hfb_status hfb_plugin_scratch(hfb_ctx* c, const char* key, int rank, const int64
     }
     if (same) return;
     if (sa.dev) cudaFree(sa.dev);
+    if (sa.dinit) cudaFree(sa.dinit);
     sa.dev = nullptr;
+    sa.dinit = nullptr;
     sa.rank = rank;
     for (int q = 0; q < rank; ++q) {
       sa.lower[q] = lower[q];

@@ -47,7 +47,8 @@ EXPORTS = [
     "hfb_set_reduction_order", "hfb_program_name", "hfb_program_module", "hfb_plugin_prepare",
     "hfb_plugin_written", "hfb_plugin_view", "hfb_plugin_scratch", "hfb_plugin_host", "hfb_plugin_host_ref",
     "hfb_peer_export", "hfb_peer_attach", "hfb_peer_stats", "hfb_transfer_bytes",
-    "hfb_set_option", "hfb_variants_build", "hfb_enqueue_graph",
+    "hfb_set_option", "hfb_variants_build", "hfb_enqueue_graph", "hfb_bind_init",
+    "hfb_plugin_array_info", "hfb_plugin_scratch_clear_init", "hfb_plugin_error",
 ]
 
 # module of each built-in program (the apps' state modules)
@@ -152,6 +153,7 @@ def lib():
         L.hfb_peer_stats.argtypes = [P, c.POINTER(i64), c.POINTER(i64)]
         L.hfb_transfer_bytes.argtypes = [P, c.POINTER(i64), c.POINTER(i64)]
         L.hfb_set_option.argtypes = [P, S, S]
+        L.hfb_bind_init.argtypes = [P, S, S, P]
         L.hfb_variants_build.restype = c.c_int
         _lib = L
     return _lib
@@ -276,6 +278,20 @@ class Engine:
         _check(lib().hfb_bind_array(self._h, _b(self.module), _b(name), rank, lo, hi,
                                     a.ctypes.data, strides, 1 if pin else 0))
         self._bound[name] = a  # keep the buffer alive
+
+    def bind_init(self, name, init):
+        """Element init flags (uint8, the array's shape and element order) for a bound array
+        (hfb_bind_init); kept alive by the engine, written back by copy-outs."""
+        if init is None:
+            _check(lib().hfb_bind_init(self._h, _b(self.module), _b(name), None))
+            self._bound.pop("@init:" + name, None)
+            return
+        a = self._bound[name]
+        if init.dtype != np.uint8 or init.shape != a.shape or init.strides != tuple(
+                s // 8 for s in a.strides):
+            raise TypeError("init flags must be uint8 with the data array's shape and order")
+        _check(lib().hfb_bind_init(self._h, _b(self.module), _b(name), init.ctypes.data))
+        self._bound["@init:" + name] = init
 
     def array(self, name):
         """numpy view (declared bounds' shape, host order) of an array's bound host buffer:
