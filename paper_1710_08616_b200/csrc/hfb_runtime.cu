@@ -353,6 +353,7 @@ struct hfb_ctx {
   // (the reference's unset-read and bounds errors, interp.cpp:487-507)
   bool checked = false;
   int* chk_flag = nullptr;  // device word of the init-box checks
+  bool plugin_tracks_init = false;  // the loaded program is a checked build (hfc --checked)
   // per-kernel CUDA-event timing (hfb_profile)
   bool prof = false;
   bool capturing = false;
@@ -3472,7 +3473,11 @@ hfb_status hfb_plugin_prepare(hfb_ctx* c, const char* name, int mode) {
 
 hfb_status hfb_plugin_written(hfb_ctx* c, const char* name) {
   return guarded([&] {
-    if (!is_scratch(name)) dev_written(c, name);
+    if (is_scratch(name)) return;
+    dev_written(c, name);
+    // a checked program sets the flags of exactly the elements it writes; an unchecked
+    // one is only known to have written the array: count it as set
+    if (!c->plugin_tracks_init) init_written(c, name);
   });
 }
 
@@ -3553,6 +3558,7 @@ hfb_status hfb_plugin_array_info(hfb_ctx* c, const char* name, int* rank, int64_
     }
     Slot& s = slot(c, name);
     check_bounds(c, s);
+    c->plugin_tracks_init = true;
     *rank = s.rank;
     for (int q = 0; q < 4; ++q) {
       lower[q] = q < s.rank ? s.lower[q] : 1;

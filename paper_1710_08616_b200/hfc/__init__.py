@@ -46,14 +46,17 @@ def translate(paths, name):
     return generate([(str(p), Path(p).read_text()) for p in paths], name)
 
 
-def build(paths, name, out, keep_source=True):
-    """Translate and compile into the plugin `out` (.so); returns its absolute path."""
+def build(paths, name, out, keep_source=True, checked=False):
+    """Translate and compile into the plugin `out` (.so); returns its absolute path.
+    checked=True builds the debug variant: every array access is checked against the
+    declared bounds and the element init flags (the reference's runtime errors,
+    interp.cpp:487-507), reported after each launch as HFB_RUNTIME."""
     out = Path(out).resolve()
     out.parent.mkdir(parents=True, exist_ok=True)
     src = out.with_suffix(".cu")
     src.write_text(translate(paths, name))
-    cmd = [NVCC, *FLAGS, "-I", str(INCLUDE), str(src), "-o", str(out), "-L", str(PKG), "-lhfb",
-           "-Xlinker", f"-rpath={PKG}"]
+    cmd = [NVCC, *FLAGS, *(["-DHFC_CHECKED"] if checked else []), "-I", str(INCLUDE), str(src),
+           "-o", str(out), "-L", str(PKG), "-lhfb", "-Xlinker", f"-rpath={PKG}"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-4000:]}")

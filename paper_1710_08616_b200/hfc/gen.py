@@ -311,6 +311,11 @@ class Scope:
 class Emitter:
     def __init__(self, prog):
         self.p = prog
+        self.nids = {}  # array name -> id in kNames (checked accessors)
+        self.used_idiv = False
+
+    def nid(self, name):
+        return self.nids.setdefault(name, len(self.nids))
 
     def etype(self, e, sc):
         if isinstance(e, Num):
@@ -367,14 +372,22 @@ class Emitter:
         if isinstance(e, Ref):
             v = sc.get(e.name)
             if v is not None and v[0] in ("array", "xarray", "harray"):
+                write = bool(sc.get("@write"))
+                if write:  # subscripts are reads
+                    sc.names.pop("@write")
                 idx = [self.expr(a, sc) if self.etype(a, sc) == "int"
                        else f"static_cast<int64_t>({self.expr(a, sc)})" for a in e.args]
+                if write:
+                    sc.set("@write", "meta", "", True)
                 if v[0] == "xarray":  # extended local: domain iterators prepended
                     idx = list(sc.get("@iters")[2]) + idx
+                acc = "HFC_WR" if write else "HFC_RD"
+                nm = self.nid(e.name)
                 if v[0] == "harray":  # host code: the bound host buffer (cached reference)
-                    fn = "hfc_wr" if sc.get("@write") else "hfc_rd"
-                    return f"{fn}(R, {sc.get('@href:' + e.name)[2]}, {v[2]}).at({', '.join(idx)})"
-                return f"{v[2]}.at({', '.join(idx)})"
+                    fn = "hfc_wr" if write else "hfc_rd"
+                    view = f"{fn}(R, {sc.get('@href:' + e.name)[2]}, {v[2]})"
+                    return f"{acc}({view}, {nm}, {', '.join(idx)})"
+                return f"{acc}({v[2]}, {nm}, {', '.join(idx)})"
             return self.intrinsic(e, sc)
         if isinstance(e, Un):
             if e.op == ".not.":
@@ -402,6 +415,7 @@ class Emitter:
                 return f"pow({self.real(e.a, sc)}, {self.real(e.b, sc)})"
             if ta == "int" and tb == "int":
                 if op == "/":
+                    self.used_idiv = True
                     return f"hfc_idiv({self.expr(e.a, sc)}, {self.expr(e.b, sc)})"
                 return f"({self.expr(e.a, sc)} {op} {self.expr(e.b, sc)})"
             return f"({self.real(e.a, sc)} {op} {self.real(e.b, sc)})"
@@ -447,10 +461,94 @@ PRELUDE = r"""
 
 namespace {
 
+// Runtime errors of the program (the reference's rt_fail, interp.cpp:68-70): device code
+// records the first one here, the host driver turns it into HFB_RUNTIME with the
+// reference's text after the launch (checked builds) or at the end of the run.
+struct HfcErr {
+  int code;  // 1 index out of bounds, 2 read of an unset element, 3 integer division by 0
+  int name, dim;
+  long long idx, lo, hi;
+};
+__device__ HfcErr hfc_err;
+__device__ double hfc_trash;  // target of out-of-bounds writes (the error is recorded)
+__device__ __forceinline__ void hfc_report(int code, int name, int dim, long long idx,
+                                           long long lo, long long hi) {
+  if (atomicCAS(&hfc_err.code, 0, code) == 0) {
+    hfc_err.name = name;
+    hfc_err.dim = dim;
+    hfc_err.idx = idx;
+    hfc_err.lo = lo;
+    hfc_err.hi = hi;
+  }
+}
+struct HfcFail {  // a host-side runtime error: the run ends with this status and text
+  int status;
+  char msg[256];
+};
+extern const char* const kNames[];  // array names by id (checked accessors)
+inline HfcFail hfc_fail_msg(int code, int name, int dim, long long idx, long long lo,
+                            long long hi) {
+  HfcFail f{HFB_RUNTIME, {0}};
+  if (code == 1)
+    std::snprintf(f.msg, sizeof f.msg, "index %lld out of bounds [%lld, %lld] in dimension %d of '%s'",
+                  idx, lo, hi, dim, kNames[name]);
+  else if (code == 2)
+    std::snprintf(f.msg, sizeof f.msg, "read of unset element of '%s'", kNames[name]);
+  else
+    std::snprintf(f.msg, sizeof f.msg, "integer division by zero");
+  return f;
+}
+__host__ __device__ inline void hfc_fail(int code, int name, int dim, long long idx, long long lo,
+                                         long long hi) {
+#ifdef __CUDA_ARCH__
+  hfc_report(code, name, dim, idx, lo, hi);
+#else
+  throw hfc_fail_msg(code, name, dim, idx, lo, hi);
+#endif
+}
+
 struct HArr {  // device view: element(d0..d3) = o[sum (d - lo) * s]
   double* o;
   int64_t s[4];
   int64_t lo[4];
+#ifdef HFC_CHECKED
+  // checked build (hfc --checked): declared upper bounds and the element init flags (device
+  // views: the device copy's; host views: the caller's, or none)
+  int64_t hi[4];
+  uint8_t* init;
+  __host__ __device__ int64_t off(int nm, int n, const int64_t* x) const {
+    int64_t f = 0;
+    for (int d = 0; d < n; ++d) {
+      if (x[d] < lo[d] || x[d] > hi[d]) {  // interp.cpp:487-492
+        hfc_fail(1, nm, d + 1, x[d], lo[d], hi[d]);
+        return -1;
+      }
+      f += (x[d] - lo[d]) * s[d];
+    }
+    return f;
+  }
+  template <class... I>
+  __host__ __device__ double rd(int nm, I... i) const {
+    const int64_t x[] = {static_cast<int64_t>(i)...};
+    const int64_t f = off(nm, static_cast<int>(sizeof...(I)), x);
+    if (f < 0) return 0.0;
+    if (init && !init[f]) {  // interp.cpp:505-507
+      hfc_fail(2, nm, 0, 0, 0, 0);
+      return 0.0;
+    }
+    return o[f];
+  }
+  template <class... I>
+  __host__ __device__ double& wr(int nm, I... i) const {
+    const int64_t x[] = {static_cast<int64_t>(i)...};
+    const int64_t f = off(nm, static_cast<int>(sizeof...(I)), x);
+#ifdef __CUDA_ARCH__
+    if (f < 0) return hfc_trash;
+#endif
+    if (init) init[f] = 1;  // write_element sets the flag (interp.cpp:534)
+    return o[f];
+  }
+#endif
   __host__ __device__ __forceinline__ double& at(int64_t a) const { return o[(a - lo[0]) * s[0]]; }
   __host__ __device__ __forceinline__ double& at(int64_t a, int64_t b) const {
     return o[(a - lo[0]) * s[0] + (b - lo[1]) * s[1]];
@@ -475,7 +573,21 @@ __host__ __device__ __forceinline__ int64_t hfc_ipowi(int64_t b, int64_t n) {
   for (int64_t k = 0; k < n; ++k) acc *= b;
   return acc;
 }
-__host__ __device__ __forceinline__ int64_t hfc_idiv(int64_t a, int64_t b) { return b ? a / b : 0; }
+// integer division; by zero: the reference's runtime error (interp.cpp:754)
+__host__ __device__ __forceinline__ int64_t hfc_idiv(int64_t a, int64_t b) {
+  if (b == 0) {
+    hfc_fail(3, 0, 0, 0, 0, 0);
+    return 0;
+  }
+  return a / b;
+}
+#ifdef HFC_CHECKED
+#define HFC_RD(v, nm, ...) (v).rd(nm, __VA_ARGS__)
+#define HFC_WR(v, nm, ...) (v).wr(nm, __VA_ARGS__)
+#else
+#define HFC_RD(v, nm, ...) (v).at(__VA_ARGS__)
+#define HFC_WR(v, nm, ...) (v).at(__VA_ARGS__)
+#endif
 __host__ __device__ __forceinline__ int64_t hfc_iabs(int64_t a) { return a < 0 ? -a : a; }
 // interp.cpp:630-645: min/max fold, the later value replaces only on strict improvement
 __host__ __device__ __forceinline__ double hfc_fold_r(double best, double d, int is_min) {
@@ -519,6 +631,10 @@ HArr hfc_view(const hfb_view& v) {
     a.s[d] = v.stride[d];
     a.lo[d] = v.lower[d];
   }
+#ifdef HFC_CHECKED
+  for (int d = 0; d < 4; ++d) a.hi[d] = INT64_MAX;
+  a.init = nullptr;
+#endif
   return a;
 }
 
@@ -701,12 +817,12 @@ class Gen:
                 if region_ctx is not None:
                     region_ctx["written"].add(s.lhs.name)
                 rhs = em.real(s.rhs, sc)
+                sc.set("@write", "meta", "", True)
+                lhs = em.expr(s.lhs, sc)
+                sc.names.pop("@write")
                 if v[0] == "harray":  # host element write (marks the host copy newer)
-                    sc.set("@write", "meta", "", True)
-                    lhs = em.expr(s.lhs, sc)
-                    sc.names.pop("@write")
                     return [f"{ind}{{ const double hfc_v = {rhs}; {lhs} = hfc_v; }}"]
-                return [f"{ind}{em.expr(s.lhs, sc)} = {rhs};"]
+                return [f"{ind}{lhs} = {rhs};"]
             n = s.lhs.name
             v = sc.get(n)
             if v is None:
@@ -761,7 +877,12 @@ class Gen:
                                 sc.get(a.name)[0] in ("array", "xarray"):
                             if region_ctx is not None:
                                 region_ctx["written"].add(a.name)
-                            args.append(em.expr(a, sc))  # the element, by reference
+                            sc.set("@write", "meta", "", True)
+                            elem = em.expr(a, sc)  # the element, by reference
+                            sc.names.pop("@write")
+                            if d.intent == "inout":  # copy-in reads it first
+                                elem = f"((void){em.expr(a, sc)}, {elem})"
+                            args.append(elem)
                             continue
                         if not isinstance(a, Name):
                             raise GenError(f"line {s.line}: intent(out) argument must be a "
@@ -1117,6 +1238,9 @@ class Gen:
         lines = [f"// generated by paper_1710_08616_b200.hfc from program '{self.p.name}'",
                  "// (Hybrid-Fortran dialect -> CUDA C++ for sm_100a); do not edit", PRELUDE]
         lines.append("namespace {")
+        names = sorted(self.em.nids, key=self.em.nids.get) or ["?"]
+        lines.append("const char* const kNames[] = {" + ", ".join(f'"{n}"' for n in names) + "};")
+        lines.append(f"constexpr bool kDeviceErrors = {'true' if self.em.used_idiv else 'false'};")
         lines.append(HOST_HELPERS.replace("@MODULE@", self.p.state.name))
         for sig, body in self.devfns:
             lines.append(sig + " {")
@@ -1226,21 +1350,41 @@ void hfc_setl(Run& R, const char* n, bool v) { hfc_seti(R, n, v ? 1 : 0); }
 // residency checks before a kernel reads (0) or reads+writes (2) an array
 void hfc_prepare(Run& R, const char* n, int mode) { HFC_CHECK(hfb_plugin_prepare(R.ctx, n, mode)); }
 void hfc_written(Run& R, const char* n) { HFC_CHECK(hfb_plugin_written(R.ctx, n)); }
+// checked builds: the declared bounds and init flags of an array (device or host copy)
+void hfc_checked(Run& R, const char* n, HArr& a, bool device) {
+#ifdef HFC_CHECKED
+  int rank = 0;
+  int64_t lo[4], hi[4];
+  uint8_t *dinit = nullptr, *hinit = nullptr;
+  HFC_CHECK(hfb_plugin_array_info(R.ctx, n, &rank, lo, hi, &dinit, &hinit));
+  for (int d = 0; d < 4; ++d) a.hi[d] = hi[d];
+  a.init = device ? dinit : hinit;
+#else
+  (void)R, (void)n, (void)a, (void)device;
+#endif
+}
 HArr hfc_array(Run& R, const char* n) {
   hfb_view v;
   HFC_CHECK(hfb_plugin_view(R.ctx, n, &v));
-  return hfc_view(v);
+  HArr a = hfc_view(v);
+  hfc_checked(R, n, a, true);
+  return a;
 }
 void hfc_scratch(Run& R, const char* key, int rank, const int64_t* lo, const int64_t* hi,
                  const int* roles) {
   HFC_CHECK(hfb_plugin_scratch(R.ctx, key, rank, lo, hi, roles));
+#ifdef HFC_CHECKED
+  HFC_CHECK(hfb_plugin_scratch_clear_init(R.ctx, key));  // elaborate_locals: no element set
+#endif
 }
 // host-side element access (host routines): the bound host buffer; write = 1 makes the
 // host copy the newest
 HArr hfc_host(Run& R, const char* n, int write) {
   hfb_view v;
   HFC_CHECK(hfb_plugin_host(R.ctx, n, write, &v));
-  return hfc_view(v);
+  HArr a = hfc_view(v);
+  hfc_checked(R, n, a, false);
+  return a;
 }
 // per host-routine invocation: one cached reference per array, fetched on first access
 struct HRef {
@@ -1253,7 +1397,9 @@ inline HArr hfc_rd(Run& R, HRef& h, const char* n) {
     h.ok = true;
   }
   if (*h.r.residency == 1) return hfc_host(R, n, 0);  // raises the stale-copy error
-  return hfc_view(h.r.view);
+  HArr a = hfc_view(h.r.view);
+  hfc_checked(R, n, a, false);
+  return a;
 }
 inline HArr hfc_wr(Run& R, HRef& h, const char* n) {
   if (!h.ok) {
@@ -1261,7 +1407,9 @@ inline HArr hfc_wr(Run& R, HRef& h, const char* n) {
     h.ok = true;
   }
   if (*h.r.has_device) *h.r.residency = 0;  // the host copy is now the newest
-  return hfc_view(h.r.view);
+  HArr a = hfc_view(h.r.view);
+  hfc_checked(R, n, a, false);
+  return a;
 }
 // the run's early-return counter (one device word, zeroed once per run)
 unsigned long long* hfc_ret_counter(Run& R) {
@@ -1290,9 +1438,29 @@ void hfc_count(Run& R, int64_t ex, int64_t ey) {
   R.st->threads += total;
   R.st->guard_returns += total - ex * ey;
 }
+// the device error record: HFB_RUNTIME with the reference's text if a thread failed
+int hfc_check_err(Run& R) {
+  HfcErr e{};
+  if (cudaMemcpyFromSymbolAsync(&e, hfc_err, sizeof e, 0, cudaMemcpyDeviceToHost, R.stream) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(R.stream) != cudaSuccess)
+    return HFB_CUDA;
+  if (e.code == 0) return HFB_OK;
+  const HfcErr zero{};
+  cudaMemcpyToSymbolAsync(hfc_err, &zero, sizeof zero, 0, cudaMemcpyHostToDevice, R.stream);
+  cudaStreamSynchronize(R.stream);
+  const HfcFail f = hfc_fail_msg(e.code, e.name, e.dim, e.idx, e.lo, e.hi);
+  return hfb_plugin_error(R.ctx, f.status, f.msg);
+}
 int hfc_launched(Run& R) {
   R.st->native_launches += 1;
-  return cudaGetLastError() == cudaSuccess ? HFB_OK : HFB_CUDA;
+  if (cudaGetLastError() != cudaSuccess) return HFB_CUDA;
+#ifdef HFC_CHECKED
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(R.stream, &cap);
+  if (cap == cudaStreamCaptureStatusNone) return hfc_check_err(R);  // after every launch
+#endif
+  return HFB_OK;
 }
 double* hfc_red_alloc(Run& R, const char* key, int64_t n) {
   const int64_t lo[] = {1}, hi[] = {n + 1};
@@ -1328,6 +1496,19 @@ int run_entry(hfb_ctx* ctx, const char* routine, hfb_launch_stats* stats, int al
       dispatch(R, routine);
     } catch (const HfcStop&) {
       // the program stopped: the run ends here, state as left (run_program, interp.cpp)
+    } catch (const HfcFail& f) {
+      return hfb_plugin_error(ctx, f.status, f.msg);
+    }
+#ifdef HFC_CHECKED
+    constexpr bool kCheck = true;
+#else
+    constexpr bool kCheck = kDeviceErrors;  // only programs whose kernels divide integers
+#endif
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(R.stream, &cap);
+    if (kCheck && cap == cudaStreamCaptureStatusNone) {  // device-side errors of the run
+      const int rc = hfc_check_err(R);
+      if (rc != HFB_OK) return rc;
     }
     if (R.ret) {  // kernel threads that returned early count as guard returns
       unsigned long long n = 0;
