@@ -412,7 +412,11 @@ class Emitter:
                     if ta == "int":
                         return f"hfc_ipowi({self.expr(e.a, sc)}, {self.expr(e.b, sc)})"
                     return f"hfc_powi({self.real(e.a, sc)}, {self.expr(e.b, sc)})"
-                return f"pow({self.real(e.a, sc)}, {self.real(e.b, sc)})"
+                # the reference evaluates real exponents with the host's std::pow
+                # (interp.cpp:745), which device pow() matches only to 2 ulp: refused
+                # rather than silently breaking bit-exactness
+                raise GenError("real exponent in '**': only integer exponents are supported "
+                               "(device pow differs from the reference's std::pow)")
             if ta == "int" and tb == "int":
                 if op == "/":
                     self.used_idiv = True

@@ -126,6 +126,7 @@ def test_plain_region_generates():
     @end parallelRegion
   end subroutine
 """, "reduce needs"),
+    (_region("    a(i,j) = a(i,j) ** 0.5_r_size"), "real exponent"),
 ])
 def test_generator_refuses(body, msg):
     with pytest.raises(GenError) as ei:
@@ -218,3 +219,13 @@ def test_return_and_stop_statements():
     assert "throw HfcStop{3};" in code
     with pytest.raises(GenError):  # stop inside device code
         _gen(_region("    stop"))
+
+
+def test_checked_build_uses_checked_accessors():
+    """`hfc --checked` and the normal build come from one translation: array reads and
+    writes go through HFC_RD / HFC_WR, which the checked build (-DHFC_CHECKED) maps to
+    the bounds/init-checking accessors and the normal build to plain element access."""
+    code = _gen(_region("    a(i,j) = a(i,j) + 1.0_r_size"))
+    assert "HFC_WR(a, 0, i, j) = " in code and "HFC_RD(a, 0, i, j)" in code
+    assert 'kNames[] = {"a"}' in code
+    assert "#define HFC_RD(v, nm, ...) (v).at(__VA_ARGS__)" in code
