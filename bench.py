@@ -52,6 +52,14 @@ GRIDS = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
 BYTES_PER_POINT = {"dycore_step": 88, "full_step": 88, "dycore_advect": 40,
                    "dycore_acoustic": 80, "hfk0_diffuse_step": 24}
 BYTES_PER_COLUMN = {"full_step": 24}
+# asuca_step (apps/dycore/asuca.h90, nsound = 6): per RK3 stage the slow tendencies read
+# rho, th, u, v, w and write 5 tendencies (80 B); every short step's RK2 pass A reads
+# u, v, w, p, rho, th, fu, fv, fw and writes pa (80 B), pass B also reads pa and writes
+# u, v, w, p (112 B); the stage end reads thb, fth, rhob, frho and writes th, rho (48 B):
+# 3 x (80 + 48) + (2 + 3 + 6) x (80 + 112) = 2496 B per point and step
+ASUCA_KERNEL_BYTES = {"asuca_tend": 80, "asuca_acoustic_a": 80, "asuca_acoustic_b": 112,
+                      "asuca_stage_end": 48}
+ASUCA_BYTES_PER_POINT = 3 * (80 + 48) + 11 * (80 + 112)
 
 
 def alg_bytes(kernel, nx, ny, nz):
@@ -215,7 +223,9 @@ def secondary(local, steps=20, warmup=5):
              "full_step", 1024, 1024),
             ("C4 dycore step without physics 1581x1301x58", "dycore", "dycore_step", 1581, 1301),
             ("reference kernel: diffusion step 1581x1301x58", "diffusion", "diffuse_step",
-             1581, 1301)]
+             1581, 1301),
+            ("ASUCA time scheme (RK3 + 11 RK2 HE-VI acoustic short steps + damping + limited "
+             "advection of rho, theta, u, v, w) 1581x1301x58", "dycore", "asuca_step", 1581, 1301)]
     for label, prog, entry, nx, ny in runs:
         eng = hfb.Engine(prog, device=local)
         shape = (NZ, nx, ny)
@@ -229,9 +239,13 @@ def secondary(local, steps=20, warmup=5):
             if entry == "full_step":
                 arrs.update({k: synthetic.field((nx, ny), *v, order="F")
                              for k, v in synthetic.PHYS_FILLS.items()})
+            if entry == "asuca_step":
+                for k, v in synthetic.asuca_params(NZ).items():
+                    eng.set(k, v)
             # RK3: stage 1 as the single step (88 B/pt); stages 2-3 also read the base
             # th, u, v, w, p (128 B/pt each)
             abytes = (88 + 2 * 128) * nx * ny * NZ if entry == "rk3_step" else \
+                ASUCA_BYTES_PER_POINT * nx * ny * NZ if entry == "asuca_step" else \
                 alg_bytes(entry, nx, ny, NZ)
         else:
             eng.set("coef", 0.1)
@@ -242,23 +256,40 @@ def secondary(local, steps=20, warmup=5):
             eng.bind(k, a)
             eng.copy_to_device(k)
         stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
-        for _ in range(warmup):
+        nst = 5 if entry == "asuca_step" else steps  # ~0.1 s per asuca step at C4
+        for _ in range(min(warmup, nst)):
             eng.enqueue(entry)
         eng.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(steps):
+        for _ in range(nst):
             eng.enqueue(entry)
         e1.record(stream)
         eng.synchronize()
-        ms = e0.elapsed_time(e1) / steps
+        ms = e0.elapsed_time(e1) / nst
+        kern = None
+        if entry == "asuca_step":  # per-kernel device times of one more step
+            eng.profile(True, clear=True)
+            eng.profile(True)
+            eng.enqueue(entry)
+            eng.synchronize()
+            eng.profile(False)
+            kern = {}
+            for kname, b in ASUCA_KERNEL_BYTES.items():
+                t, nl = eng.kernel_time(kname)
+                if nl:
+                    kern[kname] = {"launches_per_step": nl, "ms_each": round(t / nl, 4),
+                                   "alg_bytes_per_point": b,
+                                   "GBps": round(b * nx * ny * NZ / (t / nl / 1e3) / 1e9, 1)}
         pts = nx * ny * NZ
         gbs = abytes / (ms / 1e3) / 1e9
         out[label] = {"entry": entry, "ms_per_step": round(ms, 4),
                       "value": round(pts / (ms / 1e3), 1), "unit": UNIT,
                       "alg_bytes_per_step": abytes, "achieved_GBps": round(gbs, 1),
                       "frac_of_measured_hbm": round(gbs / hbm, 4),
-                      "frac_of_nominal_8TBps": round(gbs / 8000.0, 4), "steps": steps}
+                      "frac_of_nominal_8TBps": round(gbs / 8000.0, 4), "steps": nst}
+        if kern:
+            out[label]["kernels"] = kern
         eng.close()
         del arrs
     return out
@@ -342,9 +373,22 @@ def bench_ours(args):
         torch.cuda.synchronize()
 
     # ---- warm-up: W steps, extended to >= 0.4 s of back-to-back steps so the timed
-    # region sees the SUSTAINED (power-capped) clock state, not the burst one ------------
+    # region sees the SUSTAINED (power-capped) clock state, not the burst one; the timed
+    # K steps replay ONE CUDA graph (hfb_enqueue_graph: the native host driver's steps,
+    # halo exchange included for N > 1), captured here for both buffer sides ------------
+    # (NCCL send/recv is not graph-captured: that transport keeps the launch loop)
+    use_graph = n == 1 or args.transport == "peer"
+
+    def run_steps():
+        if use_graph:
+            return eng.enqueue_graph(entry, args.steps).native_launches
+        return sum(eng.enqueue(entry).native_launches for _ in range(args.steps))
+
     for _ in range(args.warmup):
         eng.enqueue(entry)
+    eng.synchronize()
+    run_steps()  # graph capture (+ K steps)
+    run_steps()  # the other buffer side when K is odd
     eng.synchronize()
     w0 = time.perf_counter()
     for _ in range(args.warmup):
@@ -354,7 +398,7 @@ def bench_ours(args):
     extra = max(0, int(0.4 / max(per, 1e-6)) - args.warmup)
     for _ in range(extra):
         eng.enqueue(entry)
-    warmup_run = 2 * args.warmup + extra
+    warmup_run = 2 * args.warmup + extra + 2 * args.steps
     eng.synchronize()
 
     # ---- device-resident timed region: K timesteps ------------------------------------
@@ -365,8 +409,7 @@ def bench_ours(args):
         barrier()
         clocks.start()
         t_ev0.record(stream)
-        for _ in range(args.steps):
-            launches += eng.enqueue(entry).native_launches
+        launches += run_steps()
         t_ev1.record(stream)
         eng.synchronize()
         clocks.stop()
@@ -385,11 +428,31 @@ def bench_ours(args):
     eng.profile(False)
     kt = {k: eng.kernel_time(k) for k in BYTES_PER_POINT}
     kt = {k: v for k, v in kt.items() if v[1] > 0}
+    # the tolerance mode side by side (hfb_set_option "arith" "fma": the same fused step
+    # with FMA contraction, within 1e-12 per field of the reference after one step,
+    # tests/test_gpu_tolerance.py): the same K steps, graph-replayed, same clock state
+    eng.set_option("arith", "fma")
+    run_steps()
+    run_steps()
+    barrier()
+    f_ev0 = torch.cuda.Event(enable_timing=True)
+    f_ev1 = torch.cuda.Event(enable_timing=True)
+    f_ev0.record(stream)
+    run_steps()
+    f_ev1.record(stream)
+    eng.synchronize()
+    barrier()
+    eng.set_option("arith", "exact")
+    ms_fma = f_ev0.elapsed_time(f_ev1)
     ms_local = ms
     if n > 1:
         t = torch.tensor([ms], device="cpu" if one_gpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    if n > 1:
+        t = torch.tensor([ms_fma], device="cpu" if one_gpu else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_fma = float(t.item())
     pts_step = gnx * gny * NZ
     value = pts_step * args.steps / (ms / 1e3)
 
@@ -418,6 +481,15 @@ def bench_ours(args):
     if tp.exists():
         rec = json.loads(tp.read_text()).get(tkey)
         traffic = rec["dram_bytes"] if isinstance(rec, dict) else None
+    ach_fma = abytes / (ms_fma / args.steps / 1e3) / 1e9
+    tolerance_mode = {"arith": "fma", "ms_per_step": round(ms_fma / args.steps, 5),
+                      "value": round(pts_step * args.steps / (ms_fma / 1e3), 1), "unit": UNIT,
+                      "roofline_frac": round(ach_fma / hbm, 4),
+                      "achieved_GBps": round(ach_fma, 1),
+                      "tolerance": "<= 1e-12 relative (normwise) per field after one step; "
+                                   "<= 1e-10 after 100 steps (tests/test_gpu_tolerance.py)",
+                      "note": "opt-in (hfb_set_option arith=fma); the headline is the "
+                              "default, bit-exact build"}
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": traffic, "traffic_key": tkey,
                 "kernel": dom, "frac_of_nominal_8TBps": round(achieved / 8000.0, 4),
@@ -497,12 +569,15 @@ def bench_ours(args):
                           "global_grid": [gnx, gny, NZ], "decomposition": f"{px}x{py}",
                           "transport": args.transport if n > 1 else None,
                           "warmup_steps_run": warmup_run,
+                          "timed_steps": f"{args.steps} steps replayed from one CUDA graph"
+                          if use_graph else f"{args.steps} enqueued steps",
                           "timed_region_ms": round(ms, 3),
                           "l2": f"inputs larger than L2: "
                                 f"{6 * tnx_l * tny_l * NZ * 8 / 2**30:.2f} GiB state + "
                                 f"{5 * tnx_l * tny_l * NZ * 8 / 2**30:.2f} GiB outputs per "
                                 f"step and GPU vs 126 MB L2 (no flush needed)"},
-               "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
+               "roofline": roofline, "tolerance_mode": tolerance_mode, "e2e": e2e,
+               "gpu_launches": launches,
                "clocks": clocks.summary(), "halo_bytes": halo}
         if n > 1:  # rank 0's halo traffic (sent + received) per step and its rate
             hps = halo / (warmup_run + 2 * args.steps)

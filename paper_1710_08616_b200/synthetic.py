@@ -50,3 +50,11 @@ DYCORE_FILLS = {"rho": (7, 1.0, 0.1), "th": (8, 300.0, 1.0), "u": (9, -0.01, 0.0
 # column physics of the full timestep (dyn_state.tsfc / colm, dycore.h90 column_physics)
 PHYS_SCALARS = {"ch": 0.05, "rrelax": 0.01}
 PHYS_FILLS = {"tsfc": (13, 300.0, 2.0), "colm": (14, 300.0, 0.5)}
+
+
+def asuca_params(nz, nsound=6, nbnd=8, kdmp=None, rdmp=0.2):
+    """dyn_state scalars of the ASUCA scheme (asuca.h90): nsound short steps per long step,
+    lateral damping band of nbnd cells, upper sponge above kdmp (default: the top quarter)."""
+    kdmp = nz - max(1, nz // 4) if kdmp is None else kdmp
+    return {"nsound": nsound, "nbnd": nbnd, "kdmp": kdmp, "rdmp": rdmp, "rnbnd": 1.0 / nbnd,
+            "rnzd": 1.0 / (nz - kdmp)}
