@@ -215,6 +215,18 @@ typedef struct hfb_group hfb_group;
 hfb_status hfb_group_create(hfb_ctx* const* ctxs, int n, hfb_group** out);
 void hfb_group_destroy(hfb_group* group);
 hfb_status hfb_group_run(hfb_group* group, const char* entry, hfb_launch_stats* stats);
+/* The device layout of a module array (include/../csrc/hfb_layout.cuh: I fastest, 128-B
+ * aligned rows, a 2-cell I/J halo ring) and host twins of the halo pack/unpack kernels
+ * (box {ilo, ihi, jlo, jhi} in tile-local 1-based (i, j) x all nk levels, packed i fastest,
+ * then j, then k — the kernels' exact element order). `origin` is the element (1, 1, 1) of
+ * a buffer in that layout. Pure host code: used by host-staged transports and by the CPU
+ * multi-process tests (tests/test_decomp_gloo.py). */
+hfb_status hfb_layout_of(int64_t ni, int64_t nj, int64_t nk, int64_t nl, int64_t* pitch,
+                         int64_t* plane, int64_t* alloc_elems, int64_t* origin_off);
+hfb_status hfb_pack_box_host(const double* origin, int64_t pitch, int64_t plane, int64_t nk,
+                             const int64_t box[4], double* buf);
+hfb_status hfb_unpack_box_host(double* origin, int64_t pitch, int64_t plane, int64_t nk,
+                               const int64_t box[4], const double* buf);
 /* halo bytes moved by this context so far (for NVLink accounting) */
 int64_t hfb_halo_bytes(hfb_ctx* ctx);
 /* host->device and device->host bytes transferred by this context so far */

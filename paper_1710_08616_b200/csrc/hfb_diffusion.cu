@@ -142,9 +142,20 @@ cudaError_t launch_diffusion_ring(const double* t_old, double* out1, double* out
   if (sp.ihi < sp.ilo || sp.jhi < sp.jlo || nz <= 0) return cudaSuccess;
   const int64_t tiles = ((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX) *
                         ((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY);
-  // small grids: split K so that ~4 CTAs per SM exist (each chunk re-reads two planes)
+  // small grids: split K until two waves of resident CTAs exist (each chunk re-reads two
+  // planes, so no more splitting than that); residency from the occupancy calculator
+  static const int resident = [] {
+    int n = 0, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &n, reinterpret_cast<const void*>(k_diffusion_ring), kTX * kTY, 0) != cudaSuccess ||
+        n < 1)
+      n = 1;
+    return n * sms;
+  }();
   int kchunks = 1;
-  while (tiles * kchunks < 148 * 8 && nz / (kchunks * 2) >= 8) kchunks *= 2;
+  while (tiles * kchunks < 2 * resident && nz / (kchunks * 2) >= 8) kchunks *= 2;
   const int kchunk = static_cast<int>((nz + kchunks - 1) / kchunks);
   kchunks = static_cast<int>((nz + kchunk - 1) / kchunk);
   RingArgs a{t_old, out1, out2, g, static_cast<int>(nz), kchunk, coef, nj,

@@ -903,22 +903,32 @@ __global__ void __launch_bounds__(256) k_pack_box(const double* __restrict__ fie
                                                   int64_t bi0, int64_t bj0, int64_t nbi,
                                                   int64_t nbj, int64_t total) {
   for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t ii = t % nbi, rest = t / nbi, jj = rest % nbj, k = rest / nbj;
-    buf[t] = field[g.at(bi0 - 1 + ii, bj0 - 1 + jj, k)];
-  }
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    buf[t] = field[box_elem(g, bi0, bj0, nbi, nbj, t)];
 }
 __global__ void __launch_bounds__(256) k_unpack_box(double* __restrict__ field,
                                                     const double* __restrict__ buf, Grid3 g,
                                                     int64_t bi0, int64_t bj0, int64_t nbi,
                                                     int64_t nbj, int64_t total) {
   for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t ii = t % nbi, rest = t / nbi, jj = rest % nbj, k = rest / nbj;
-    field[g.at(bi0 - 1 + ii, bj0 - 1 + jj, k)] = buf[t];
-  }
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    field[box_elem(g, bi0, bj0, nbi, nbj, t)] = buf[t];
 }
 }  // namespace
+
+void pack_box_host(const double* field, double* buf, Grid3 g, int64_t nk, const int64_t box[4],
+                   bool pack) {
+  const int64_t nbi = box[1] - box[0] + 1, nbj = box[3] - box[2] + 1;
+  if (nbi <= 0 || nbj <= 0 || nk <= 0) return;
+  const int64_t total = nbi * nbj * nk;
+  for (int64_t t = 0; t < total; ++t) {
+    const int64_t e = box_elem(g, box[0], box[2], nbi, nbj, t);
+    if (pack)
+      buf[t] = field[e];
+    else
+      const_cast<double*>(field)[e] = buf[t];
+  }
+}
 
 cudaError_t launch_pack_box(const double* field, double* buf, Grid3 g, int64_t nk,
                             const int64_t box[4], bool pack, cudaStream_t s) {

@@ -166,6 +166,17 @@ cudaError_t launch_column_physics(const double* rho, double* th, const double* u
                                   const PhysArgs& ph, const Span& sp, cudaStream_t s);
 
 // ---- halo pack/unpack for the 2-D decomposition -------------------------------------
+// element t of a halo box {ilo, ihi, jlo, jhi} (local 1-based) x all K levels in its
+// packed order (i fastest, then j, then k): the one indexing of the pack/unpack kernels
+// and of their host twin
+__host__ __device__ __forceinline__ int64_t box_elem(const Grid3& g, int64_t bi0, int64_t bj0,
+                                                     int64_t nbi, int64_t nbj, int64_t t) {
+  const int64_t ii = t % nbi, rest = t / nbi, jj = rest % nbj, k = rest / nbj;
+  return g.at(bi0 - 1 + ii, bj0 - 1 + jj, k);
+}
+// the same pack (pack = true) / unpack on host memory (hfb_pack_box_host)
+void pack_box_host(const double* field, double* buf, Grid3 g, int64_t nk, const int64_t box[4],
+                   bool pack);
 cudaError_t launch_pack_box(const double* field, double* buf, Grid3 g, int64_t nk,
                             const int64_t box[4], bool pack, cudaStream_t s);
 

@@ -811,7 +811,11 @@ void exchange_and_run(hfb_ctx* c, const std::vector<const char*>& fields, int r,
   try {
     for (const Span& sp : {south, north, west, east}) run(sp, true);
   } catch (...) {
+    // the communication stream may still hold the exchange (a spinning wait) and strips:
+    // join it before the error propagates, so nothing it does outlives the buffers
     c->run_stream = nullptr;
+    cudaEventRecord(c->ev_halo, c->comm);
+    cudaStreamWaitEvent(c->stream, c->ev_halo, 0);
     throw;
   }
   c->run_stream = nullptr;
@@ -1976,6 +1980,7 @@ void hfb_destroy(hfb_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  if (c->comm) cudaStreamSynchronize(c->comm);
   for (auto& [n, s] : c->slots) {
     for (double* p : s.dev)
       if (p) cudaFree(p);
@@ -2508,6 +2513,30 @@ hfb_status hfb_decomp_faces(const hfb_decomp* d, int32_t side, int64_t send_box[
       send_box[q] = sb[q];
       recv_box[q] = rb[q];
     }
+  });
+}
+
+hfb_status hfb_layout_of(int64_t ni, int64_t nj, int64_t nk, int64_t nl, int64_t* pitch,
+                         int64_t* plane, int64_t* alloc_elems, int64_t* origin_off) {
+  return guarded([&] {
+    if (ni < 1 || nj < 1 || nk < 1 || nl < 1) fail(HFB_CONFIG, "non-positive extent");
+    const Layout L = Layout::make(ni, nj, nk, nl);
+    *pitch = L.pitch;
+    *plane = L.plane;
+    *alloc_elems = L.alloc_elems;
+    *origin_off = L.origin_off;
+  });
+}
+
+hfb_status hfb_pack_box_host(const double* origin, int64_t pitch, int64_t plane, int64_t nk,
+                             const int64_t box[4], double* buf) {
+  return guarded([&] { pack_box_host(origin, buf, Grid3{pitch, plane}, nk, box, true); });
+}
+
+hfb_status hfb_unpack_box_host(double* origin, int64_t pitch, int64_t plane, int64_t nk,
+                               const int64_t box[4], const double* buf) {
+  return guarded([&] {
+    pack_box_host(origin, const_cast<double*>(buf), Grid3{pitch, plane}, nk, box, false);
   });
 }
 

@@ -49,6 +49,7 @@ EXPORTS = [
     "hfb_peer_export", "hfb_peer_attach", "hfb_peer_stats", "hfb_transfer_bytes",
     "hfb_set_option", "hfb_variants_build", "hfb_enqueue_graph", "hfb_bind_init",
     "hfb_plugin_array_info", "hfb_plugin_scratch_clear_init", "hfb_plugin_error",
+    "hfb_layout_of", "hfb_pack_box_host", "hfb_unpack_box_host",
 ]
 
 # module of each built-in program (the apps' state modules)
@@ -154,6 +155,9 @@ def lib():
         L.hfb_transfer_bytes.argtypes = [P, c.POINTER(i64), c.POINTER(i64)]
         L.hfb_set_option.argtypes = [P, S, S]
         L.hfb_bind_init.argtypes = [P, S, S, P]
+        L.hfb_layout_of.argtypes = [i64] * 4 + [c.POINTER(i64)] * 4
+        L.hfb_pack_box_host.argtypes = [P, i64, i64, i64, c.POINTER(i64), P]
+        L.hfb_unpack_box_host.argtypes = [P, i64, i64, i64, c.POINTER(i64), P]
         L.hfb_variants_build.restype = c.c_int
         _lib = L
     return _lib
@@ -462,6 +466,49 @@ class Group:
 
     def __exit__(self, *a):
         self.close()
+
+
+class TileLayout:
+    """The device layout of an (nk, nj, ni) array (hfb_layout_of) on a host buffer, with the
+    library's host twins of the halo pack / unpack kernels."""
+
+    def __init__(self, ni, nj, nk, nl=1):
+        v = [ctypes.c_int64() for _ in range(4)]
+        _check(lib().hfb_layout_of(ni, nj, nk, nl, *[ctypes.byref(x) for x in v]))
+        self.ni, self.nj, self.nk = ni, nj, nk
+        self.pitch, self.plane, self.alloc, self.origin = (x.value for x in v)
+        self.buf = np.zeros(self.alloc)
+
+    def interior(self):
+        """(nk, nj, ni) view of the logical elements (i fastest)."""
+        v = self.buf[self.origin:self.origin + self.nk * self.plane]
+        return np.lib.stride_tricks.as_strided(
+            v, shape=(self.nk, self.nj, self.ni), strides=(8 * self.plane, 8 * self.pitch, 8))
+
+    def padded(self, h):
+        """(nk, nj + 2h, ni + 2h) view including h cells of the halo ring (h <= 2)."""
+        start = self.origin - h * self.pitch - h
+        v = self.buf[start:]
+        return np.lib.stride_tricks.as_strided(
+            v, shape=(self.nk, self.nj + 2 * h, self.ni + 2 * h),
+            strides=(8 * self.plane, 8 * self.pitch, 8))
+
+    def _ptr(self):
+        return self.buf.ctypes.data + 8 * self.origin
+
+    def pack(self, box):
+        n = (box[1] - box[0] + 1) * (box[3] - box[2] + 1) * self.nk
+        out = np.empty(max(n, 0))
+        b = (ctypes.c_int64 * 4)(*box)
+        _check(lib().hfb_pack_box_host(self._ptr(), self.pitch, self.plane, self.nk, b,
+                                       out.ctypes.data))
+        return out
+
+    def unpack(self, box, data):
+        data = np.ascontiguousarray(data, dtype=np.float64)
+        b = (ctypes.c_int64 * 4)(*box)
+        _check(lib().hfb_unpack_box_host(self._ptr(), self.pitch, self.plane, self.nk, b,
+                                         data.ctypes.data))
 
 
 def variants_build():

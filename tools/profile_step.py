@@ -37,6 +37,9 @@ if a.app == "dycore":
         eng.set(k, v)
     arrs = {k: synthetic.field(shape, *v, order="F") for k, v in synthetic.DYCORE_FILLS.items()}
     entry = a.entry
+    if entry == "asuca_step":
+        for k, v in synthetic.asuca_params(a.nz).items():
+            eng.set(k, v)
     if entry == "full_step":
         arrs.update({k: synthetic.field((a.nx, a.ny), *v, order="F")
                      for k, v in synthetic.PHYS_FILLS.items()})
