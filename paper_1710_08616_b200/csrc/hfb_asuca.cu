@@ -27,7 +27,9 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
+#include "hfb_fp64.cuh"
 #include "hfb_kernels.cuh"
 #include "hfb_sm100.cuh"
 
@@ -154,11 +156,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
     return smem[slot * kTStage + f * kTPlane + cen + dj * kTW + di];
   };
 
-  const bool east = gi == gnx, west = gi == 1, north = gj == gny, south = gj == 1;
   const int64_t col = (j - 1) * W + (i - 1);
 
   for (int k = 0; k < kTStages - 2; ++k) issue(k);
 
+  // kLat: the tile touches (or is within 2 cells of) a lateral wall and needs the wall /
+  // first-last-face cases; tiles >= 3 cells from every wall run without them
+  auto sweep = [&](auto lat_tag) {
+  constexpr bool kLat = decltype(lat_tag)::value;
+  const bool east = kLat && gi == gnx, west = kLat && gi == 1;
+  const bool north = kLat && gj == gny, south = kLat && gj == 1;
   // carried along K (values at the bottom face / level centre of the current level)
   double fzt_b = 0.0, fzr_b = 0.0;  // theta/rho flux through z-face kk-1/2
   double gzu_b = 0.0, czu_b = 0.0;  // u: z-edge flux / velocity at kk-1/2
@@ -179,16 +186,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
     {
       // x faces: east (face i) and west (face i-1)
       auto xface = [&](int fld, int64_t f, int off, double vel) {  // face f = gi + off
-        return (f == 0 || f == gnx) ? 0.0
+        return (kLat && (f == 0 || f == gnx)) ? 0.0
                                     : asu_flux(vel, V(fld, k, off - 1, 0), V(fld, k, off, 0),
                                                V(fld, k, off + 1, 0), V(fld, k, off + 2, 0),
-                                               f == 1, f + 1 == gnx);
+                                               kLat && f == 1, kLat && f + 1 == gnx);
       };
       auto yface = [&](int fld, int64_t f, int off, double vel) {
-        return (f == 0 || f == gny) ? 0.0
+        return (kLat && (f == 0 || f == gny)) ? 0.0
                                     : asu_flux(vel, V(fld, k, 0, off - 1), V(fld, k, 0, off),
                                                V(fld, k, 0, off + 1), V(fld, k, 0, off + 2),
-                                               f == 1, f + 1 == gny);
+                                               kLat && f == 1, kLat && f + 1 == gny);
       };
       auto zface = [&](int fld) {  // top face kk+1/2
         return (kk == nz) ? 0.0
@@ -219,23 +226,23 @@ __global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
       // centre c = gi + off between u-points c-1 and c (walls 0 and gnx are zero)
       auto xcen = [&](int off, double& cv) {
         const int64_t c = gi + off;
-        const double qb = (c == 1) ? 0.0 : V(kFU, k, off - 1, 0);
-        const double qc = (c == gnx) ? 0.0 : V(kFU, k, off, 0);
-        const double qa = (c <= 2) ? 0.0 : V(kFU, k, off - 2, 0);
-        const double qd = (c + 1 >= gnx) ? 0.0 : V(kFU, k, off + 1, 0);
+        const double qb = (kLat && c == 1) ? 0.0 : V(kFU, k, off - 1, 0);
+        const double qc = (kLat && c == gnx) ? 0.0 : V(kFU, k, off, 0);
+        const double qa = (kLat && c <= 2) ? 0.0 : V(kFU, k, off - 2, 0);
+        const double qd = (kLat && c + 1 >= gnx) ? 0.0 : V(kFU, k, off + 1, 0);
         cv = 0.5 * (qb + qc);
-        return asu_flux(cv, qa, qb, qc, qd, c == 1, c == gnx);
+        return asu_flux(cv, qa, qb, qc, qd, kLat && c == 1, kLat && c == gnx);
       };
       // y edge f = gj + off (between u(j') and u(j'+1)), velocity mean of v(i), v(i+1)
       auto yedge = [&](int off, double& cv) {
         const int64_t f = gj + off;
-        if (f == 0 || f == gny || east) {
+        if (kLat && (f == 0 || f == gny || east)) {
           cv = 0.0;
           return 0.0;
         }
         cv = 0.5 * (V(kFV, k, 0, off) + V(kFV, k, 1, off));
         return asu_flux(cv, V(kFU, k, 0, off - 1), V(kFU, k, 0, off), V(kFU, k, 0, off + 1),
-                        V(kFU, k, 0, off + 2), f == 1, f + 1 == gny);
+                        V(kFU, k, 0, off + 2), kLat && f == 1, kLat && f + 1 == gny);
       };
       double cxe, cxw, cyn, cys, czt;
       const double gxe = xcen(1, cxe), gxw = xcen(0, cxw);
@@ -265,22 +272,22 @@ __global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
     {
       auto ycen = [&](int off, double& cv) {
         const int64_t c = gj + off;
-        const double qb = (c == 1) ? 0.0 : V(kFV, k, 0, off - 1);
-        const double qc = (c == gny) ? 0.0 : V(kFV, k, 0, off);
-        const double qa = (c <= 2) ? 0.0 : V(kFV, k, 0, off - 2);
-        const double qd = (c + 1 >= gny) ? 0.0 : V(kFV, k, 0, off + 1);
+        const double qb = (kLat && c == 1) ? 0.0 : V(kFV, k, 0, off - 1);
+        const double qc = (kLat && c == gny) ? 0.0 : V(kFV, k, 0, off);
+        const double qa = (kLat && c <= 2) ? 0.0 : V(kFV, k, 0, off - 2);
+        const double qd = (kLat && c + 1 >= gny) ? 0.0 : V(kFV, k, 0, off + 1);
         cv = 0.5 * (qb + qc);
-        return asu_flux(cv, qa, qb, qc, qd, c == 1, c == gny);
+        return asu_flux(cv, qa, qb, qc, qd, kLat && c == 1, kLat && c == gny);
       };
       auto xedge = [&](int off, double& cv) {
         const int64_t f = gi + off;
-        if (f == 0 || f == gnx || north) {
+        if (kLat && (f == 0 || f == gnx || north)) {
           cv = 0.0;
           return 0.0;
         }
         cv = 0.5 * (V(kFU, k, off, 0) + V(kFU, k, off, 1));
         return asu_flux(cv, V(kFV, k, off - 1, 0), V(kFV, k, off, 0), V(kFV, k, off + 1, 0),
-                        V(kFV, k, off + 2, 0), f == 1, f + 1 == gnx);
+                        V(kFV, k, off + 2, 0), kLat && f == 1, kLat && f + 1 == gnx);
       };
       double cye, cyw, cxe, cxw, czt;
       const double gxe = xedge(0, cxe), gxw = xedge(-1, cxw);
@@ -324,23 +331,23 @@ __global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
       if (kk != nz) {
         auto xedge = [&](int off, double& cv) {
           const int64_t f = gi + off;
-          if (f == 0 || f == gnx) {
+          if (kLat && (f == 0 || f == gnx)) {
             cv = 0.0;
             return 0.0;
           }
           cv = 0.5 * (V(kFU, k, off, 0) + V(kFU, k + 1, off, 0));
           return asu_flux(cv, V(kFW, k, off - 1, 0), V(kFW, k, off, 0), V(kFW, k, off + 1, 0),
-                          V(kFW, k, off + 2, 0), f == 1, f + 1 == gnx);
+                          V(kFW, k, off + 2, 0), kLat && f == 1, kLat && f + 1 == gnx);
         };
         auto yedge = [&](int off, double& cv) {
           const int64_t f = gj + off;
-          if (f == 0 || f == gny) {
+          if (kLat && (f == 0 || f == gny)) {
             cv = 0.0;
             return 0.0;
           }
           cv = 0.5 * (V(kFV, k, 0, off) + V(kFV, k + 1, 0, off));
           return asu_flux(cv, V(kFW, k, 0, off - 1), V(kFW, k, 0, off), V(kFW, k, 0, off + 1),
-                          V(kFW, k, 0, off + 2), f == 1, f + 1 == gny);
+                          V(kFW, k, 0, off + 2), kLat && f == 1, kLat && f + 1 == gny);
         };
         double cxe, cxw, cyn, cys;
         const double gxe = xedge(0, cxe), gxw = xedge(-1, cxw);
@@ -364,6 +371,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
       a.f.fw[o] = fw;
     }
   }
+  };
+  const int64_t gi0 = i0 + a.sp.i0, gj0 = j0 + a.sp.j0;
+  const bool interior = gi0 >= 3 && gi0 + kTX - 1 <= gnx - 3 && i0 + kTX - 1 <= a.sp.ihi &&
+                        gj0 >= 3 && gj0 + kTY - 1 <= gny - 3 && j0 + kTY - 1 <= a.sp.jhi;
+  if (interior)
+    sweep(std::false_type{});
+  else
+    sweep(std::true_type{});
   sm100::cp_async_wait<0>();
 }
 
@@ -467,6 +482,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_asu_acoustic(AcoArgs a) {
   for (int k = 0; k < kAStages - 1; ++k) issue(k);
 
   double rho_p = 0.0, th_p = 0.0, w_p = 0.0, fw_p = 0.0, ps_p = 0.0, cp_p = 0.0, dp_p = 0.0;
+  double pend_beta = 0.0, pend_bb = 1.0, pend_dd = 0.0;  // face awaiting its recursion
+  const fp64::Recip rth0 = fp64::recip(c.th0);
 #pragma unroll 1
   for (int k = 0; k < nz; ++k) {
     sm100::cp_async_wait<kAStages - 2>();  // level k landed (own copies)
@@ -495,33 +512,81 @@ __global__ void __launch_bounds__(kThreads, 2) k_asu_acoustic(AcoArgs a) {
       a.un[o] = unk - tau * unk;
       a.vn[o] = vnk - tau * vnk;
     }
-    if (k >= 1) {  // forward elimination for the face between levels k-1 and k
-      const int f = k - 1;
+    // HE-VI forward elimination, software-pipelined: the Thomas recursion of face k-2
+    // (coefficients formed last level) runs beside the coefficient formation of face
+    // k-1, so the two division chains overlap. Quotients by the same divisor share one
+    // reciprocal (hfb_fp64.cuh): bit-identical to `/` whenever the range check passes,
+    // else the dialect's divisions are redone.
+    bool ok = true;
+    double cpk = 0.0, dpk = 0.0, beta = 0.0, dd = 0.0;
+    if (k >= 2) {
+      const bool first = k == 2;  // face 0: no previous coefficients
+      const double m = first ? pend_bb : pend_bb + pend_beta * cp_p;
+      const double num = first ? pend_dd : pend_dd + pend_beta * dp_p;
+      const fp64::Recip rm = fp64::recip(m);
+      cpk = fp64::quot(-pend_beta, rm, ok);
+      dpk = fp64::quot(num, rm, ok);
+    }
+    const double n_ps = c.h_rdz * (psk - ps_p);
+    const double n_th = c.h_grav * (0.5 * (th_p + thk) - c.th0);
+    if (k >= 1) {
       const double rf = 0.5 * (rho_p + rhok);
-      const double beta = c.beta_num / rf;
-      double dd = w_p - c.h_rdz * (psk - ps_p) / rf;
-      dd = dd + c.h_grav * (0.5 * (th_p + thk) - c.th0) / c.th0;
+      const fp64::Recip rr = fp64::recip(rf);
+      beta = fp64::quot(c.beta_num, rr, ok);
+      dd = w_p - fp64::quot(n_ps, rr, ok);
+      dd = dd + fp64::quot(n_th, rth0, ok);
       dd = dd + c.h * fw_p;
-      const double bb = 1.0 + 2.0 * beta;
-      double cpk, dpk;
-      if (f == 0) {
-        cpk = -beta / bb;
-        dpk = dd / bb;
-      } else {
-        const double m = bb + beta * cp_p;
-        cpk = -beta / m;
-        dpk = (dd + beta * dp_p) / m;
+    }
+    if (__builtin_expect(!ok, 0)) {  // a range check failed: the dialect's divisions
+      if (k >= 2) {
+        if (k == 2) {
+          cpk = -pend_beta / pend_bb;
+          dpk = pend_dd / pend_bb;
+        } else {
+          const double m = pend_bb + pend_beta * cp_p;
+          cpk = -pend_beta / m;
+          dpk = (pend_dd + pend_beta * dp_p) / m;
+        }
       }
-      sm100::tmem_st_f64(tmem + 2 * f, cpk);
-      sm100::tmem_st_f64(tmem + kDpCol + 2 * f, dpk);
+      if (k >= 1) {
+        const double rf = 0.5 * (rho_p + rhok);
+        beta = c.beta_num / rf;
+        dd = w_p - n_ps / rf;
+        dd = dd + n_th / c.th0;
+        dd = dd + c.h * fw_p;
+      }
+    }
+    if (k >= 2) {  // face k-2's coefficients to this thread's TMEM lane
+      sm100::tmem_st_f64(tmem + 2 * (k - 2), cpk);
+      sm100::tmem_st_f64(tmem + kDpCol + 2 * (k - 2), dpk);
       cp_p = cpk;
       dp_p = dpk;
+    }
+    if (k >= 1) {
+      pend_beta = beta;
+      pend_bb = 1.0 + 2.0 * beta;
+      pend_dd = dd;
     }
     rho_p = rhok;
     th_p = thk;
     w_p = wk;
     fw_p = fwk;
     ps_p = psk;
+  }
+  if (nz >= 2) {  // drain: the recursion of the last face, nz-2
+    bool ok = true;
+    const bool first = nz == 2;
+    const double m = first ? pend_bb : pend_bb + pend_beta * cp_p;
+    const double num = first ? pend_dd : pend_dd + pend_beta * dp_p;
+    const fp64::Recip rm = fp64::recip(m);
+    double cpk = fp64::quot(-pend_beta, rm, ok);
+    double dpk = fp64::quot(num, rm, ok);
+    if (!ok) {
+      cpk = -pend_beta / m;
+      dpk = num / m;
+    }
+    sm100::tmem_st_f64(tmem + 2 * (nz - 2), cpk);
+    sm100::tmem_st_f64(tmem + kDpCol + 2 * (nz - 2), dpk);
   }
   sm100::cp_async_wait<0>();
   sm100::tmem_wait_st();
