@@ -171,8 +171,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
   double gzu_b = 0.0, czu_b = 0.0;  // u: z-edge flux / velocity at kk-1/2
   double gzv_b = 0.0, czv_b = 0.0;  // v
   double gzw_b = 0.0, czw_b = 0.0;  // w: flux / velocity through level centre kk
-#pragma unroll 1
-  for (int k = 0; k < nz; ++k) {  // 0-based level; dialect level kk = k + 1
+  // kV: the level needs the vertical boundary cases (ground, lid, first/last faces);
+  // mid-column levels 3 <= kk <= nz-3 run without them
+  auto level = [&](int k, auto v_tag) {
+  constexpr bool kV = decltype(v_tag)::value;
     sm100::cp_async_wait<kTStages - 5>();  // levels <= k+2 landed (own copies)
     __syncthreads();                        // ... everyone's; slot of level k-2 free
     issue(k + kTStages - 2);
@@ -198,13 +200,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
                                                kLat && f == 1, kLat && f + 1 == gny);
       };
       auto zface = [&](int fld) {  // top face kk+1/2
-        return (kk == nz) ? 0.0
+        return (kV && kk == nz) ? 0.0
                           : asu_flux(wk, V(fld, k - 1, 0, 0), V(fld, k, 0, 0), V(fld, k + 1, 0, 0),
-                                     V(fld, k + 2, 0, 0), kk == 1, kk + 1 == nz);
+                                     V(fld, k + 2, 0, 0), kV && kk == 1, kV && kk + 1 == nz);
       };
       const double ue = east ? 0.0 : ui, uw = west ? 0.0 : uim1;
       const double vnf = north ? 0.0 : vj, vs = south ? 0.0 : vjm1;
-      const double wt = (kk == nz) ? 0.0 : wk, wb = (kk == 1) ? 0.0 : wkm1;
+      const double wt = (kV && kk == nz) ? 0.0 : wk, wb = (kV && kk == 1) ? 0.0 : wkm1;
       double div = rdx * (ue - uw) + rdy * (vnf - vs);
       div = div + rdz * (wt - wb);
       const double fzt = zface(kFTh), fzr = zface(kFRho);
@@ -248,13 +250,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
       const double gxe = xcen(1, cxe), gxw = xcen(0, cxw);
       const double gyn = yedge(0, cyn), gys = yedge(-1, cys);
       double gzt;
-      if (kk == nz || east) {
+      if ((kV && kk == nz) || east) {
         czt = 0.0;
         gzt = 0.0;
       } else {
         czt = 0.5 * (wk + V(kFW, k, 1, 0));
         gzt = asu_flux(czt, V(kFU, k - 1, 0, 0), ui, V(kFU, k + 1, 0, 0), V(kFU, k + 2, 0, 0),
-                       kk == 1, kk + 1 == nz);
+                       kV && kk == 1, kV && kk + 1 == nz);
       }
       if (!east) {
         double div = rdx * (cxe - cxw) + rdy * (cyn - cys);
@@ -293,13 +295,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
       const double gxe = xedge(0, cxe), gxw = xedge(-1, cxw);
       const double gyn = ycen(1, cye), gys = ycen(0, cyw);
       double gzt;
-      if (kk == nz || north) {
+      if ((kV && kk == nz) || north) {
         czt = 0.0;
         gzt = 0.0;
       } else {
         czt = 0.5 * (wk + V(kFW, k, 0, 1));
         gzt = asu_flux(czt, V(kFV, k - 1, 0, 0), vj, V(kFV, k + 1, 0, 0), V(kFV, k + 2, 0, 0),
-                       kk == 1, kk + 1 == nz);
+                       kV && kk == 1, kV && kk + 1 == nz);
       }
       if (!north) {
         double div = rdx * (cxe - cxw) + rdy * (cye - cyw);
@@ -317,18 +319,18 @@ __global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
     {
       // level centre c between w-points c-1 and c (0 = ground and nz = lid are zero)
       auto zcen = [&](int c, int kc, double& cv) {  // kc: 0-based level of w-point c
-        const double qb = (c == 1) ? 0.0 : V(kFW, kc - 1, 0, 0);
-        const double qc = (c == nz) ? 0.0 : V(kFW, kc, 0, 0);
-        const double qa = (c <= 2) ? 0.0 : V(kFW, kc - 2, 0, 0);
-        const double qd = (c + 1 >= nz) ? 0.0 : V(kFW, kc + 1, 0, 0);
+        const double qb = (kV && c == 1) ? 0.0 : V(kFW, kc - 1, 0, 0);
+        const double qc = (kV && c == nz) ? 0.0 : V(kFW, kc, 0, 0);
+        const double qa = (kV && c <= 2) ? 0.0 : V(kFW, kc - 2, 0, 0);
+        const double qd = (kV && c + 1 >= nz) ? 0.0 : V(kFW, kc + 1, 0, 0);
         cv = 0.5 * (qb + qc);
-        return asu_flux(cv, qa, qb, qc, qd, c == 1, c == nz);
+        return asu_flux(cv, qa, qb, qc, qd, kV && c == 1, kV && c == nz);
       };
-      if (kk == 1) gzw_b = zcen(1, 0, czw_b);  // the ground-side centre of the column
+      if (kV && kk == 1) gzw_b = zcen(1, 0, czw_b);  // the ground-side centre of the column
       double czt;
-      const double gzt = (kk == nz) ? 0.0 : zcen(kk + 1, k + 1, czt);
-      if (kk == nz) czt = 0.0;
-      if (kk != nz) {
+      const double gzt = (kV && kk == nz) ? 0.0 : zcen(kk + 1, k + 1, czt);
+      if (kV && kk == nz) czt = 0.0;
+      if (!(kV && kk == nz)) {
         auto xedge = [&](int off, double& cv) {
           const int64_t f = gi + off;
           if (kLat && (f == 0 || f == gnx)) {
@@ -370,7 +372,15 @@ __global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
       a.f.fv[o] = fv;
       a.f.fw[o] = fw;
     }
-  }
+    };
+  const int mid_lo = nz > 2 ? 2 : nz, mid_hi = nz - 3 > mid_lo ? nz - 3 : mid_lo;
+  int k = 0;
+#pragma unroll 1
+  for (; k < mid_lo; ++k) level(k, std::true_type{});
+#pragma unroll 1
+  for (; k < mid_hi; ++k) level(k, std::false_type{});
+#pragma unroll 1
+  for (; k < nz; ++k) level(k, std::true_type{});
   };
   const int64_t gi0 = i0 + a.sp.i0, gj0 = j0 + a.sp.j0;
   const bool interior = gi0 >= 3 && gi0 + kTX - 1 <= gnx - 3 && i0 + kTX - 1 <= a.sp.ihi &&
