@@ -714,10 +714,15 @@ __global__ void __launch_bounds__(kWsThreads, 2)
         if (ok[q]) sm100::cp_async16(dst[q] + so, src[q]);
         src[q] += P;
       }
+#ifdef HFB_AB_CHUNK3
+      if (ok[2]) sm100::cp_async16(dst[2] + so, src[2]);
+      src[2] += P;
+#else
       if (warp == 0) {
         if (ok[2]) sm100::cp_async16(dst[2] + so, src[2]);
         src[2] += P;
       }
+#endif
     }
     sm100::cp_async_commit();
     so = so == (kWsStages - 1) * kStageBytes ? 0u : so + kStageBytes;
@@ -767,11 +772,11 @@ __global__ void __launch_bounds__(kWsThreads, 2)
   struct BaseLevel {
     double th, u, uw, v, vs, p, w;
   };
-  auto base_load = [&](int k) {
+  auto base_load = [&](int k, auto role_tag) {
     BaseLevel b{};
     if (kRK && k < nz && active) {
       const int64_t o = col + static_cast<int64_t>(k) * P;
-      if (acoustic) {
+      if constexpr (decltype(role_tag)::value) {
         b.u = __ldg(a.base.u + o);
         b.uw = __ldg(a.base.u + o - 1);
         b.v = __ldg(a.base.v + o);
@@ -784,7 +789,8 @@ __global__ void __launch_bounds__(kWsThreads, 2)
     }
     return b;
   };
-  BaseLevel bcur = base_load(0);
+  BaseLevel bcur{};
+  if (kRK) bcur = acoustic ? base_load(0, std::true_type{}) : base_load(0, std::false_type{});
   double wb_prev = 0.0;  // base w of the previous level (RK: the HE-VI right-hand side)
   if (kPhys && !acoustic && active) {
     colm_ij = a.colm[(j - 1) * W + (i - 1)];
@@ -823,11 +829,14 @@ __global__ void __launch_bounds__(kWsThreads, 2)
 
   // kMid: 3 <= k < nz - 5 — no vertical boundary cases (faces kk+1/2 with
   // 2 <= kk <= nz-2, Thomas face k-2 >= 1) and the copy of level k+5 always exists
-  auto level = [&](int k, auto chk_tag, auto mid_tag) {
+  // kAc: the role of this warp (acoustic/HE-VI or advection) is a compile-time property of
+  // the whole K sweep, so each role's loop carries only its own state across levels
+  auto level = [&](int k, auto chk_tag, auto mid_tag, auto role_tag) {
     constexpr bool kCX = decltype(chk_tag)::x, kCY = decltype(chk_tag)::y;
     constexpr bool kIn = !kCX && !kCY;  // every lane active
     constexpr bool kMid = decltype(mid_tag)::value;
-    const BaseLevel bnext = base_load(k + 1);
+    constexpr bool kAc = decltype(role_tag)::value;
+    const BaseLevel bnext = base_load(k + 1, role_tag);
     const int kk = k + 1;
     const int s1 = s0 == kWsStages - 1 ? 0 : s0 + 1;
     const int s2 = s1 == kWsStages - 1 ? 0 : s1 + 1;
@@ -838,7 +847,7 @@ __global__ void __launch_bounds__(kWsThreads, 2)
     const double* Vp = S + kFOffV + (row + 1) * kVW + lane;
     const double vj = Vp[0], vjm1 = Vp[-kVW];
     const double wk = S[kFOffW + row * kSW + lane];
-    if (acoustic && (a.roles & 2) != 0) {
+    if (kAc && (a.roles & 2) != 0) {
       const double* Pp = S + kFOffP + (row + 1) * kPW + (lane + 2);
       const double pk = Pp[0], pe = Pp[1], pw = Pp[-1], pnn = Pp[kPW], psth = Pp[-kPW];
       const double rhok = S[kFOffRho + row * kSW + lane];
@@ -898,7 +907,7 @@ __global__ void __launch_bounds__(kWsThreads, 2)
       rho_prev = rhok;
       ps_prev = psk;
       if (kRK) wb_prev = bcur.w;
-    } else if (!acoustic && (a.roles & 1) != 0) {
+    } else if (!kAc && (a.roles & 1) != 0) {
       const double* T0 = S + kFOffTh + thc;
       const double tkp1 =
           (kMid || kk + 1 <= nz) ? ring[s1 * kFStageDoubles + kFOffTh + thc] : 0.0;
@@ -944,38 +953,45 @@ __global__ void __launch_bounds__(kWsThreads, 2)
     w_prev = wk;
     s0 = s1;
     out_a += P;
-    if (acoustic) out_v += P;
+    if (kAc) out_v += P;
     bcur = bnext;
   };
 
   // one level: levels <= k+2 have landed (own copies; issued up to k+kWsStages-2), the
   // barrier makes everyone's visible and tells that every warp has finished level k-1,
   // so its slot is refilled with level k+kWsStages-1 (one barrier per level)
-  auto step = [&](int k, auto in_tag, auto mid_tag) {
+  auto step = [&](int k, auto in_tag, auto mid_tag, auto role_tag) {
     sm100::cp_async_wait<kWsStages - 4>();
     __syncthreads();
     issue(decltype(mid_tag)::value || k + kWsStages - 1 < nz);
-    level(k, in_tag, mid_tag);
+    level(k, in_tag, mid_tag, role_tag);
   };
   // K phases: [0, 3) and [nz-5, nz) with the vertical boundary cases, [3, nz-5) without
   const int mid_lo = nz >= 3 ? 3 : nz, mid_hi = nz - 5 > mid_lo ? nz - 5 : mid_lo;
-  auto sweep = [&](auto in_tag) {
+  auto sweep = [&](auto in_tag, auto role_tag) {
     int k = 0;
 #pragma unroll 1
-    for (; k < mid_lo; ++k) step(k, in_tag, std::false_type{});
+    for (; k < mid_lo; ++k) step(k, in_tag, std::false_type{}, role_tag);
 #pragma unroll kMidUnroll
-    for (; k < mid_hi; ++k) step(k, in_tag, std::true_type{});
+    for (; k < mid_hi; ++k) step(k, in_tag, std::true_type{}, role_tag);
 #pragma unroll 1
-    for (; k < nz; ++k) step(k, in_tag, std::false_type{});
+    for (; k < nz; ++k) step(k, in_tag, std::false_type{}, role_tag);
   };
-  if (!chk_x && !chk_y)
-    sweep(Chk<false, false>{});
-  else if (!chk_y)
-    sweep(Chk<true, false>{});
-  else if (!chk_x)
-    sweep(Chk<false, true>{});
+  // the two roles run separate K loops (same barrier sequence: one bar.sync per level)
+  auto run = [&](auto role_tag) {
+    if (!chk_x && !chk_y)
+      sweep(Chk<false, false>{}, role_tag);
+    else if (!chk_y)
+      sweep(Chk<true, false>{}, role_tag);
+    else if (!chk_x)
+      sweep(Chk<false, true>{}, role_tag);
+    else
+      sweep(Chk<true, true>{}, role_tag);
+  };
+  if (acoustic)
+    run(std::true_type{});
   else
-    sweep(Chk<true, true>{});
+    run(std::false_type{});
   if (acoustic && nz >= 2) {  // drain the last face
     bool ok = true;
     double cpk, dpk;

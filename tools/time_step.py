@@ -17,7 +17,8 @@ app = sys.argv[4] if len(sys.argv) > 4 else "dycore"
 arith = sys.argv[5] if len(sys.argv) > 5 else "exact"
 full = app == "full"  # the full timestep: dycore + column physics (full_step)
 asuca = app == "asuca"  # the ASUCA time scheme (asuca_step)
-if full or asuca:
+rk3 = app == "rk3"  # Wicker-Skamarock RK3 of the dycore step (rk3_step)
+if full or asuca or rk3:
     app = "dycore"
 eng = hfb.Engine(app)
 if app == "dycore":
@@ -43,6 +44,8 @@ if app == "dycore":
         for k, v in dict(rdmp=0.2, rnbnd=1.0 / 8, rnzd=1.0 / (nz - kdmp)).items():
             eng.set(k, v)
         entry, bpp = "asuca_step", 2496
+    if rk3:
+        entry, bpp = "rk3_step", 88 + 2 * 128
 else:
     eng.set("coef", 0.1)
     arrs = {"t_old": synthetic.field((nz, nx, ny), 1, 280.0, 10.0, order="F"),
