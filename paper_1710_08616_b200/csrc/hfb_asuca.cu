@@ -51,7 +51,7 @@ struct PlaneSpec {
   int r0, c0, w, h, off;
 };
 
-template <int NSPEC, int NCH>
+template <int NSPEC, int NCH, int NT = kThreads>
 struct Stager {
   const double* src[NCH];
   uint32_t dst[NCH];
@@ -62,7 +62,7 @@ struct Stager {
     ok = 0;
 #pragma unroll
     for (int q = 0; q < NCH; ++q) {
-      const int ch = t + q * kThreads;
+      const int ch = t + q * NT;
       src[q] = sp[0].base;
       dst[q] = ring_u32;
       if (ch >= total_chunks) continue;
@@ -413,8 +413,19 @@ struct AcoArgs {
   Span sp;
 };
 
+// Warp-specialised: 8 warps per CTA over the same 32 x 4 column tile. Warps 4-7 (the
+// "horizontal" role) compute, per level k, the pressure gradient, the divergence and ps
+// (pass B: also the damped u', v'), then FORM the HE-VI coefficients of face k-1 (beta,
+// dd: one shared reciprocal of rf, three quotients) and hand them over through a
+// two-deep shared-memory buffer; warps 0-3 (the "Thomas" role, owners of the TMEM lanes)
+// run the forward recursion of face k-2 one level behind, then the back substitution
+// and the pressure update. The barrier that publishes every staged plane also publishes
+// the handed-over coefficients, so the pipeline needs no extra synchronisation. Two
+// CTAs per SM (TMEM: 256 columns each) give 16 resident warps instead of 8.
+constexpr int kAcoThreads = 2 * kThreads;
+
 template <bool kB>
-__global__ void __launch_bounds__(kThreads, 2) k_asu_acoustic(AcoArgs a) {
+__global__ void __launch_bounds__(kAcoThreads, 2) k_asu_acoustic(AcoArgs a) {
   extern __shared__ __align__(128) double smem[];
   __shared__ uint32_t tmem_base_slot;
   // stage layout (doubles)
@@ -430,21 +441,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_asu_acoustic(AcoArgs a) {
   constexpr int oPc = oFW + kTX * kTY;           // pass B: p at the column, 32 x 4
   constexpr int kStage = kB ? oPc + kTX * kTY : oPc;
   constexpr int kChunks = kStage / 2;
-  constexpr int kChPer = (kChunks + kThreads - 1) / kThreads;
+  constexpr int kChPer = (kChunks + kAcoThreads - 1) / kAcoThreads;
+  const int nz = a.nz;
   double* ring = smem;
   double* ps_s = smem + kAStages * kStage;  // nz x 128
+  double* cf_s = ps_s + nz * kThreads;      // [face parity][beta, dd] x 128
 
-  const int lane = threadIdx.x, row = threadIdx.y, t = row * kTX + lane;
+  const int lane = threadIdx.x, warp = threadIdx.y;  // blockDim = (32, 8)
+  const bool thomas = warp < kTY;
+  const int row = thomas ? warp : warp - kTY;
+  const int tid = warp * kTX + lane;  // 0..255 (copy issue)
+  const int t = row * kTX + lane;     // 0..127 (column within the tile)
   const int64_t i0 = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * kTX;
   const int64_t j0 = a.sp.jlo + static_cast<int64_t>(blockIdx.y) * kTY;
   const int64_t i = i0 + lane, j = j0 + row;
   const bool active = i <= a.sp.ihi && j <= a.sp.jhi;
-  const int nz = a.nz;
   const int64_t P = a.g.plane, W = a.g.pitch;
   const int64_t gi = i + a.sp.i0, gj = j + a.sp.j0;
   const AsuAcoConst& c = a.c;
 
-  if (row == 0) sm100::tmem_alloc(&tmem_base_slot, kTmemCols);
+  if (warp == 0) sm100::tmem_alloc(&tmem_base_slot, kTmemCols);
   sm100::tmem_fence_before();
   __syncthreads();
   sm100::tmem_fence_after();
@@ -461,8 +477,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_asu_acoustic(AcoArgs a) {
                          {a.s.th, 0, 0, kTX, kTY, oTh},
                          {a.fw, 0, 0, kTX, kTY, oFW},
                          {a.s.p, 0, 0, kTX, kTY, oPc}};
-  Stager<NS, kChPer> stg;
-  stg.init(specs, kChunks, t, i0 - 1, j0 - 1, W, a.nj, a.row_lo, a.row_hi, sm100::smem_u32(ring));
+  Stager<NS, kChPer, kAcoThreads> stg;
+  stg.init(specs, kChunks, tid, i0 - 1, j0 - 1, W, a.nj, a.row_lo, a.row_hi,
+           sm100::smem_u32(ring));
   constexpr uint32_t kStageBytes = kStage * 8;
   auto issue = [&](int k) {
     if (k < nz) stg.issue(k, P, static_cast<uint32_t>((k % kAStages) * kStageBytes));
@@ -488,147 +505,137 @@ __global__ void __launch_bounds__(kThreads, 2) k_asu_acoustic(AcoArgs a) {
     const double az = static_cast<double>(kk - c.kdmp > 0 ? kk - c.kdmp : 0) * c.rnzd;
     return c.dtau_rdmp * (az > axy ? az : axy);
   };
+  double* const cf_beta = cf_s + t;  // + (f & 1) * 256
+  double* const cf_dd = cf_s + kThreads + t;
 
   for (int k = 0; k < kAStages - 1; ++k) issue(k);
 
-  double rho_p = 0.0, th_p = 0.0, w_p = 0.0, fw_p = 0.0, ps_p = 0.0, cp_p = 0.0, dp_p = 0.0;
-  double pend_beta = 0.0, pend_bb = 1.0, pend_dd = 0.0;  // face awaiting its recursion
-  const fp64::Recip rth0 = fp64::recip(c.th0);
-#pragma unroll 1
-  for (int k = 0; k < nz; ++k) {
-    sm100::cp_async_wait<kAStages - 2>();  // level k landed (own copies)
-    __syncthreads();                        // everyone's; the slot of level k-1 is free
-    issue(k + kAStages - 1);
-    const double* S = ring + (k % kAStages) * kStage;
-    const double* Pp = S + oP + (row + 1) * kAW + (lane + 2);
-    const double pk = Pp[0], pe = Pp[1], pw = Pp[-1], pnn = Pp[kAW], psth = Pp[-kAW];
-    const double uk = S[oU + row * kAW + lane + 2], ukw = S[oU + row * kAW + lane + 1];
-    const double fuk = S[oFU + row * kAW + lane + 2], fukw = S[oFU + row * kAW + lane + 1];
-    const double vk = S[oV + (row + 1) * kTX + lane], vks = S[oV + row * kTX + lane];
-    const double fvk = S[oFV + (row + 1) * kTX + lane], fvks = S[oFV + row * kTX + lane];
-    const double wk = S[oW + t], rhok = S[oRho + t], thk = S[oTh + t], fwk = S[oFW + t];
-    const double pc = kB ? S[oPc + t] : pk;  // p at the column (the RK2 base)
-
-    // PGF at p (A) / pa (B) applied to the current momentum, plus h * slow tendency
-    const double unk = east ? 0.0 : uk - c.h_rdx * (pe - pk) + c.h * fuk;
-    const double vnk = north ? 0.0 : vk - c.h_rdy * (pnn - pk) + c.h * fvk;
-    const double uw = west ? 0.0 : ukw - c.h_rdx * (pk - pw) + c.h * fukw;
-    const double vs = south ? 0.0 : vks - c.h_rdy * (pk - psth) + c.h * fvks;
-    const double psk = pc - c.h_cs2 * (c.rdx * (unk - uw) + c.rdy * (vnk - vs));
-    ps_s[k * kThreads + t] = psk;
-    if (kB && active) {  // damped momentum of the short step
-      const double tau = tau_at(k + 1);
-      const int64_t o = col + static_cast<int64_t>(k) * P;
-      a.un[o] = unk - tau * unk;
-      a.vn[o] = vnk - tau * vnk;
-    }
-    // HE-VI forward elimination, software-pipelined: the Thomas recursion of face k-2
-    // (coefficients formed last level) runs beside the coefficient formation of face
-    // k-1, so the two division chains overlap. Quotients by the same divisor share one
-    // reciprocal (hfb_fp64.cuh): bit-identical to `/` whenever the range check passes,
-    // else the dialect's divisions are redone.
+  // Thomas forward recursion of face f from its handed-over (beta, dd); quotients by m
+  // share one reciprocal (hfb_fp64.cuh), else the dialect's divisions
+  double cp_p = 0.0, dp_p = 0.0;
+  auto recursion = [&](int f) {
+    const double beta = cf_beta[(f & 1) * 2 * kThreads];
+    const double dd = cf_dd[(f & 1) * 2 * kThreads];
+    const double bb = 1.0 + 2.0 * beta;
+    const bool first = f == 0;  // face 0: no previous coefficients
+    const double m = first ? bb : bb + beta * cp_p;
+    const double num = first ? dd : dd + beta * dp_p;
     bool ok = true;
-    double cpk = 0.0, dpk = 0.0, beta = 0.0, dd = 0.0;
-    if (k >= 2) {
-      const bool first = k == 2;  // face 0: no previous coefficients
-      const double m = first ? pend_bb : pend_bb + pend_beta * cp_p;
-      const double num = first ? pend_dd : pend_dd + pend_beta * dp_p;
-      const fp64::Recip rm = fp64::recip(m);
-      cpk = fp64::quot(-pend_beta, rm, ok);
-      dpk = fp64::quot(num, rm, ok);
-    }
-    const double n_ps = c.h_rdz * (psk - ps_p);
-    const double n_th = c.h_grav * (0.5 * (th_p + thk) - c.th0);
-    if (k >= 1) {
-      const double rf = 0.5 * (rho_p + rhok);
-      const fp64::Recip rr = fp64::recip(rf);
-      beta = fp64::quot(c.beta_num, rr, ok);
-      dd = w_p - fp64::quot(n_ps, rr, ok);
-      dd = dd + fp64::quot(n_th, rth0, ok);
-      dd = dd + c.h * fw_p;
-    }
-    if (__builtin_expect(!ok, 0)) {  // a range check failed: the dialect's divisions
-      if (k >= 2) {
-        if (k == 2) {
-          cpk = -pend_beta / pend_bb;
-          dpk = pend_dd / pend_bb;
-        } else {
-          const double m = pend_bb + pend_beta * cp_p;
-          cpk = -pend_beta / m;
-          dpk = (pend_dd + pend_beta * dp_p) / m;
-        }
-      }
-      if (k >= 1) {
-        const double rf = 0.5 * (rho_p + rhok);
-        beta = c.beta_num / rf;
-        dd = w_p - n_ps / rf;
-        dd = dd + n_th / c.th0;
-        dd = dd + c.h * fw_p;
-      }
-    }
-    if (k >= 2) {  // face k-2's coefficients to this thread's TMEM lane
-      sm100::tmem_st_f64(tmem + 2 * (k - 2), cpk);
-      sm100::tmem_st_f64(tmem + kDpCol + 2 * (k - 2), dpk);
-      cp_p = cpk;
-      dp_p = dpk;
-    }
-    if (k >= 1) {
-      pend_beta = beta;
-      pend_bb = 1.0 + 2.0 * beta;
-      pend_dd = dd;
-    }
-    rho_p = rhok;
-    th_p = thk;
-    w_p = wk;
-    fw_p = fwk;
-    ps_p = psk;
-  }
-  if (nz >= 2) {  // drain: the recursion of the last face, nz-2
-    bool ok = true;
-    const bool first = nz == 2;
-    const double m = first ? pend_bb : pend_bb + pend_beta * cp_p;
-    const double num = first ? pend_dd : pend_dd + pend_beta * dp_p;
     const fp64::Recip rm = fp64::recip(m);
-    double cpk = fp64::quot(-pend_beta, rm, ok);
+    double cpk = fp64::quot(-beta, rm, ok);
     double dpk = fp64::quot(num, rm, ok);
-    if (!ok) {
-      cpk = -pend_beta / m;
+    if (__builtin_expect(!ok, 0)) {
+      cpk = -beta / m;
       dpk = num / m;
     }
-    sm100::tmem_st_f64(tmem + 2 * (nz - 2), cpk);
-    sm100::tmem_st_f64(tmem + kDpCol + 2 * (nz - 2), dpk);
-  }
-  sm100::cp_async_wait<0>();
-  sm100::tmem_wait_st();
+    sm100::tmem_st_f64(tmem + 2 * f, cpk);
+    sm100::tmem_st_f64(tmem + kDpCol + 2 * f, dpk);
+    cp_p = cpk;
+    dp_p = dpk;
+  };
 
-  // back substitution (faces nz-2 .. 0, w(nz) = 0 is the lid), four per TMEM load, then
-  // the pressure update (pass B: the damped w of the short step)
-  double* pout = kB ? a.pn : a.pa_out;
-  if (kB && active) a.wn[col + static_cast<int64_t>(nz - 1) * P] = 0.0 - tau_at(nz) * 0.0;
-  double wk1 = 0.0;
-  const int nf = nz - 1;
+  // one role's K sweep (the role is compile-time per loop: no cross-role live state)
+  auto sweep = [&](auto role_tag) {
+    constexpr bool kThomas = decltype(role_tag)::value;
+    double rho_p = 0.0, th_p = 0.0, w_p = 0.0, fw_p = 0.0, ps_p = 0.0;
+    const fp64::Recip rth0 = fp64::recip(c.th0);
 #pragma unroll 1
-  for (int cb = (nf - 1) / 4; cb >= 0; --cb) {
-    double cpv[4], dpv[4];
-    sm100::tmem_ld_4f64(tmem + 8 * cb, cpv);
-    sm100::tmem_ld_4f64(tmem + kDpCol + 8 * cb, dpv);
-#pragma unroll
-    for (int q = 3; q >= 0; --q) {
-      const int f = 4 * cb + q;  // face f = w-point f+1 (1-based) at 0-based level f
-      if (f >= nf) continue;
-      const double wkk = (f == nf - 1) ? dpv[q] : dpv[q] - cpv[q] * wk1;
-      const double pk1 = ps_s[(f + 1) * kThreads + t] - c.h_cs2_rdz * (wk1 - wkk);
-      if (active) {
-        pout[col + static_cast<int64_t>(f + 1) * P] = pk1;
-        if (kB) a.wn[col + static_cast<int64_t>(f) * P] = wkk - tau_at(f + 1) * wkk;
+    for (int k = 0; k < nz; ++k) {
+      sm100::cp_async_wait<kAStages - 2>();  // level k landed (own copies)
+      __syncthreads();  // everyone's; the slot of level k-1 is free; face k-2's (beta, dd)
+      issue(k + kAStages - 1);
+      if constexpr (kThomas) {
+        if (k >= 2) recursion(k - 2);
+      } else {
+        const double* S = ring + (k % kAStages) * kStage;
+        const double* Pp = S + oP + (row + 1) * kAW + (lane + 2);
+        const double pk = Pp[0], pe = Pp[1], pw = Pp[-1], pnn = Pp[kAW], psth = Pp[-kAW];
+        const double uk = S[oU + row * kAW + lane + 2], ukw = S[oU + row * kAW + lane + 1];
+        const double fuk = S[oFU + row * kAW + lane + 2], fukw = S[oFU + row * kAW + lane + 1];
+        const double vk = S[oV + (row + 1) * kTX + lane], vks = S[oV + row * kTX + lane];
+        const double fvk = S[oFV + (row + 1) * kTX + lane], fvks = S[oFV + row * kTX + lane];
+        const double wk = S[oW + t], rhok = S[oRho + t], thk = S[oTh + t], fwk = S[oFW + t];
+        const double pc = kB ? S[oPc + t] : pk;  // p at the column (the RK2 base)
+
+        // PGF at p (A) / pa (B) applied to the current momentum, plus h * slow tendency
+        const double unk = east ? 0.0 : uk - c.h_rdx * (pe - pk) + c.h * fuk;
+        const double vnk = north ? 0.0 : vk - c.h_rdy * (pnn - pk) + c.h * fvk;
+        const double uw = west ? 0.0 : ukw - c.h_rdx * (pk - pw) + c.h * fukw;
+        const double vs = south ? 0.0 : vks - c.h_rdy * (pk - psth) + c.h * fvks;
+        const double psk = pc - c.h_cs2 * (c.rdx * (unk - uw) + c.rdy * (vnk - vs));
+        ps_s[k * kThreads + t] = psk;
+        if (kB && active) {  // damped momentum of the short step
+          const double tau = tau_at(k + 1);
+          const int64_t o = col + static_cast<int64_t>(k) * P;
+          a.un[o] = unk - tau * unk;
+          a.vn[o] = vnk - tau * vnk;
+        }
+        if (k >= 1) {  // HE-VI coefficients of face k-1 (between levels k-1 and k)
+          bool ok = true;
+          const double n_ps = c.h_rdz * (psk - ps_p);
+          const double n_th = c.h_grav * (0.5 * (th_p + thk) - c.th0);
+          const double rf = 0.5 * (rho_p + rhok);
+          const fp64::Recip rr = fp64::recip(rf);
+          double beta = fp64::quot(c.beta_num, rr, ok);
+          double dd = w_p - fp64::quot(n_ps, rr, ok);
+          dd = dd + fp64::quot(n_th, rth0, ok);
+          dd = dd + c.h * fw_p;
+          if (__builtin_expect(!ok, 0)) {  // a range check failed: the dialect's divisions
+            beta = c.beta_num / rf;
+            dd = w_p - n_ps / rf;
+            dd = dd + n_th / c.th0;
+            dd = dd + c.h * fw_p;
+          }
+          cf_beta[((k - 1) & 1) * 2 * kThreads] = beta;
+          cf_dd[((k - 1) & 1) * 2 * kThreads] = dd;
+        }
+        rho_p = rhok;
+        th_p = thk;
+        w_p = wk;
+        fw_p = fwk;
+        ps_p = psk;
       }
-      wk1 = wkk;
     }
+  };
+  if (thomas)
+    sweep(std::true_type{});
+  else
+    sweep(std::false_type{});
+  sm100::cp_async_wait<0>();
+  __syncthreads();  // face nz-2's coefficients and every ps are visible
+
+  if (thomas) {
+    recursion(nz - 2);  // drain: the last face
+    sm100::tmem_wait_st();
+    // back substitution (faces nz-2 .. 0, w(nz) = 0 is the lid), four per TMEM load,
+    // then the pressure update (pass B: the damped w of the short step)
+    double* pout = kB ? a.pn : a.pa_out;
+    if (kB && active) a.wn[col + static_cast<int64_t>(nz - 1) * P] = 0.0 - tau_at(nz) * 0.0;
+    double wk1 = 0.0;
+    const int nf = nz - 1;
+#pragma unroll 1
+    for (int cb = (nf - 1) / 4; cb >= 0; --cb) {
+      double cpv[4], dpv[4];
+      sm100::tmem_ld_4f64(tmem + 8 * cb, cpv);
+      sm100::tmem_ld_4f64(tmem + kDpCol + 8 * cb, dpv);
+#pragma unroll
+      for (int q = 3; q >= 0; --q) {
+        const int f = 4 * cb + q;  // face f = w-point f+1 (1-based) at 0-based level f
+        if (f >= nf) continue;
+        const double wkk = (f == nf - 1) ? dpv[q] : dpv[q] - cpv[q] * wk1;
+        const double pk1 = ps_s[(f + 1) * kThreads + t] - c.h_cs2_rdz * (wk1 - wkk);
+        if (active) {
+          pout[col + static_cast<int64_t>(f + 1) * P] = pk1;
+          if (kB) a.wn[col + static_cast<int64_t>(f) * P] = wkk - tau_at(f + 1) * wkk;
+        }
+        wk1 = wkk;
+      }
+    }
+    if (active) pout[col] = ps_s[t] - c.h_cs2_rdz * wk1;
   }
-  if (active) pout[col] = ps_s[t] - c.h_cs2_rdz * wk1;
   sm100::tmem_fence_before();
   __syncthreads();
-  if (row == 0) sm100::tmem_dealloc(tmem_base_slot, kTmemCols);
+  if (warp == 0) sm100::tmem_dealloc(tmem_base_slot, kTmemCols);
 }
 
 // theta = thb + dtf * fth, rho = rhob + dtf * frho over the span (asuca.h90 stage end)
@@ -702,7 +709,8 @@ cudaError_t launch_asu_acoustic(bool pass_b, const AsuState& s, const double* fu
   // two CTAs per SM share the SM's 512 TMEM columns; pad small-nz launches so a third
   // CTA never blocks in tcgen05.alloc
   const size_t smem = std::max<size_t>(
-      (static_cast<size_t>(kAStages) * stage + static_cast<size_t>(nz) * kThreads) * sizeof(double),
+      (static_cast<size_t>(kAStages) * stage + static_cast<size_t>(nz + 4) * kThreads) *
+          sizeof(double),
       80 * 1024);
   const void* kern = pass_b ? reinterpret_cast<const void*>(k_asu_acoustic<true>)
                             : reinterpret_cast<const void*>(k_asu_acoustic<false>);
@@ -712,7 +720,7 @@ cudaError_t launch_asu_acoustic(bool pass_b, const AsuState& s, const double* fu
   }
   AcoArgs a{s, fu, fv, fw, pa, pa_out, un, vn, wn, pn, g, static_cast<int>(nz), nj,
             -kIOff, g.pitch - kIOff - 1, c, sp};
-  dim3 block(kTX, kTY);
+  dim3 block(kTX, 2 * kTY);
   dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
             static_cast<unsigned>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY));
   if (pass_b)
