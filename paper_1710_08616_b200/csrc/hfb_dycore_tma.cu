@@ -424,39 +424,7 @@ __global__ void __launch_bounds__(kThreadsTma, 2)
 
 }  // namespace
 
-// ---- host: tensor maps ------------------------------------------------------------
-namespace {
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      p = nullptr;
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }();
-  return fn;
-}
-
-}  // namespace
-
-bool make_box_map(CUtensorMap* m, const double* origin, Grid3 g, int64_t nj, int64_t nz, int bw,
-                  int bh) {
-  auto fn = encode_fn();
-  if (!fn) return false;
-  const double* base = origin - (kHalo * g.pitch + kIOff);
-  cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.pitch), static_cast<cuuint64_t>(nj + 2 * kHalo),
-                        static_cast<cuuint64_t>(nz)};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.pitch * 8),
-                           static_cast<cuuint64_t>(g.plane * 8)};
-  cuuint32_t box[3] = {static_cast<cuuint32_t>(bw), static_cast<cuuint32_t>(bh), 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box,
-            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
+// make_box_map (hfb_tmap.cuh) is defined with the product step in hfb_dycore_tmem.cu
 
 cudaError_t launch_dycore_step_tma(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                    int64_t nj, const DynConst& c, const Span& sp,

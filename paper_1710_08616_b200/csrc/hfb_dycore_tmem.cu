@@ -36,9 +36,13 @@
 #define dycore_step_tmem_fits dycore_step_tmem_fits_fma
 #define launch_dycore_step_ws launch_dycore_step_ws_fma
 #endif
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "hfb_kernels.cuh"
 #include "hfb_sm100.cuh"
 #include "hfb_fp64.cuh"
+#include "hfb_tmap.cuh"
 
 namespace hfb {
 
@@ -566,6 +570,17 @@ cudaError_t launch_dycore_step_tmem(const DynIn& in, const DynOut& out, Grid3 g,
 namespace {
 
 constexpr int kWsThreads = 2 * kThreads;  // 256
+// ring stage layout: the six plane tiles of a level (th, u, v, w, p, rho), each starting
+// 128-B aligned (the TMA destination rule; the cp.async feed uses the same layout)
+constexpr int pad16(int n) { return (n + 15) / 16 * 16; }
+constexpr int kWOffTh = 0;
+constexpr int kWOffU = kWOffTh + pad16(kFThW * kFThR);
+constexpr int kWOffV = kWOffU + pad16(kUW * kUR);
+constexpr int kWOffW = kWOffV + pad16(kVW * kVR);
+constexpr int kWOffP = kWOffW + pad16(kSW * kSR);
+constexpr int kWOffRho = kWOffP + pad16(kPW * kPR);
+constexpr int kWStageDoubles = kWOffRho + pad16(kSW * kSR);  // 1072
+constexpr uint32_t kWStageTx = kFStageDoubles * 8;            // bytes landing per level
 #ifndef HFB_MID_UNROLL
 #define HFB_MID_UNROLL 1
 #endif
@@ -601,14 +616,35 @@ struct Chk {
   static constexpr bool x = kX, y = kY;
 };
 
+// The ring feed: cp.async (LDGSTS, every thread copies 2-3 16-B chunks per level and
+// waits for its own) or, with HFB_WS_TMA, TMA (six 3-D box loads per level issued by one
+// lane each of warps 0-5, completion on the slot's mbarrier; one waiter warp observes it
+// and the per-level CTA barrier publishes it).
+#ifdef HFB_WS_TMA
+constexpr bool kTmaFeed = true;
+#else
+constexpr bool kTmaFeed = false;
+#endif
+constexpr int kWaitWarp = 4;  // TMA feed: the warp that waits on the slot barriers
+
 template <bool kPhys, bool kRK, bool kRemote>
 __global__ void __launch_bounds__(kWsThreads, 2)
-    k_dyn_step_ws(StepTmemArgs a, const __grid_constant__ RemoteHalo rem) {
+    k_dyn_step_ws(const __grid_constant__ StepMaps maps, StepTmemArgs a,
+                  const __grid_constant__ RemoteHalo rem) {
+  // (the tensor maps come first: a CUtensorMap must sit 64-B aligned in parameter space)
   static_assert(!(kPhys && kRK), "column physics is not fused into RK stages");
-  extern __shared__ __align__(128) double smem[];
-  __shared__ uint32_t tmem_base_slot;
-  double* ring = smem;
-  double* ps_s = smem + kWsStages * kFStageDoubles;  // nz x 128 (ps of each column)
+  extern __shared__ __align__(128) double smem_raw[];
+  // static shared memory: the slot barriers and the TMEM address, 64 B in total, so the
+  // dynamic segment starts 16-B aligned and the 128-B alignment below is exact
+  __shared__ __align__(16) uint64_t sbar[8];
+  static_assert(kWsStages < 8, "slot barriers");
+  uint64_t* const full_bar = sbar;
+  uint32_t& tmem_base_slot = *reinterpret_cast<uint32_t*>(&sbar[7]);
+  // the ring starts 128-B aligned (TMA destinations; the launch adds the slack)
+  // (offset arithmetic on the __shared__ array keeps the loads in the shared window)
+  const uint32_t raw_u32 = sm100::smem_u32(smem_raw);
+  double* ring = smem_raw + ((((raw_u32 + 127u) & ~127u) - raw_u32) >> 3);
+  double* ps_s = ring + kWsStages * kWStageDoubles;  // nz x 128 (ps of each column)
   // kPhys: theta' of levels k-1 / k (parity), handed from the advection warps to the
   // acoustic warps, which accumulate the column sums (the halves stay balanced)
   double* thv_s = ps_s + a.nz * kThreads;
@@ -663,11 +699,35 @@ __global__ void __launch_bounds__(kWsThreads, 2)
   const bool chk_x = !(gi0 >= 3 && gi0 + kTX - 1 <= gnx - 2 && i0 + kTX - 1 <= a.sp.ihi);
   const bool chk_y = !(gj0 >= 3 && gj0 + kTY - 1 <= gny - 2 && j0 + kTY - 1 <= a.sp.jhi);
 
+  const uint32_t full0 = sm100::smem_u32(full_bar);
   if (warp == 0) sm100::tmem_alloc(&tmem_base_slot, kTmemCols);
+  if (kTmaFeed && warp == 0 && lane == 0) {
+    for (int q = 0; q < kWsStages; ++q) sm100::mbar_init(full0 + 8 * q, 1);
+    sm100::mbar_fence_init();
+  }
+  if (kTmaFeed && warp < 6 && lane == 0) sm100::tma_prefetch_desc(&maps.m[warp]);
   sm100::tmem_fence_before();
   __syncthreads();
   sm100::tmem_fence_after();
   const uint32_t tmem = tmem_base_slot + (static_cast<uint32_t>(32 * row) << 16);
+
+  // TMA feed: lane 0 of warp f (f < 6) loads field f's box (th, u, v, w, p, rho order);
+  // box origins in allocation coordinates (x = kIOff + i', y = kHalo + j', z = k)
+  const bool tma_lane = kTmaFeed && lane == 0 && warp < 6;
+  int f_off = kWOffTh, f_dx = -2, f_dy = -2;
+  switch (warp) {
+    case 1: f_off = kWOffU; f_dx = -2; f_dy = 0; break;
+    case 2: f_off = kWOffV; f_dx = 0; f_dy = -1; break;
+    case 3: f_off = kWOffW; f_dx = 0; f_dy = 0; break;
+    case 4: f_off = kWOffP; f_dx = -2; f_dy = -1; break;
+    case 5: f_off = kWOffRho; f_dx = 0; f_dy = 0; break;
+    default: break;
+  }
+  const CUtensorMap* f_map = &maps.m[warp < 6 ? warp : 0];
+  const int box_x = static_cast<int>(kIOff + (i0 - 1)) + f_dx;
+  const int box_y = static_cast<int>(kHalo + (j0 - 1)) + f_dy;
+  const uint32_t f_dst = sm100::smem_u32(ring) + static_cast<uint32_t>(f_off * 8);
+  int tma_k = 0;  // the next level this lane loads
 
   const double* src[kWsChunksPerThread];
   uint32_t dst[kWsChunksPerThread];
@@ -680,25 +740,31 @@ __global__ void __launch_bounds__(kWsThreads, 2)
     src[q] = a.in.p;
     dst[q] = 0;
     if (ch >= kFChunks) continue;
-    const int e = ch * 2;
+    const int e = ch * 2;  // packed index of the chunk's first double in the stage
     const double* base;
     int64_t r, cc;  // 0-based local (j', i') of the chunk start
+    int d;          // padded offset of the chunk's field minus its packed offset
     if (e < kFOffU) {
-      base = a.in.th; r = (j0 - 3) + e / kFThW; cc = (i0 - 3) + e % kFThW;
+      base = a.in.th; r = (j0 - 3) + e / kFThW; cc = (i0 - 3) + e % kFThW; d = kWOffTh - kFOffTh;
     } else if (e < kFOffV) {
       base = a.in.u; r = (j0 - 1) + (e - kFOffU) / kUW; cc = (i0 - 3) + (e - kFOffU) % kUW;
+      d = kWOffU - kFOffU;
     } else if (e < kFOffW) {
       base = a.in.v; r = (j0 - 2) + (e - kFOffV) / kVW; cc = (i0 - 1) + (e - kFOffV) % kVW;
+      d = kWOffV - kFOffV;
     } else if (e < kFOffP) {
       base = a.in.w; r = (j0 - 1) + (e - kFOffW) / kSW; cc = (i0 - 1) + (e - kFOffW) % kSW;
+      d = kWOffW - kFOffW;
     } else if (e < kFOffRho) {
       base = a.in.p; r = (j0 - 2) + (e - kFOffP) / kPW; cc = (i0 - 3) + (e - kFOffP) % kPW;
+      d = kWOffP - kFOffP;
     } else {
       base = a.in.rho; r = (j0 - 1) + (e - kFOffRho) / kSW; cc = (i0 - 1) + (e - kFOffRho) % kSW;
+      d = kWOffRho - kFOffRho;
     }
     ok[q] = r >= -kHalo && r <= a.nj - 1 + kHalo && cc >= a.row_lo && cc + 1 <= a.row_hi;
     src[q] = base + r * W + cc;
-    dst[q] = ring_u32 + static_cast<uint32_t>(e) * 8u;
+    dst[q] = ring_u32 + static_cast<uint32_t>(e + d) * 8u;
   }
   // levels are issued in order, once each: sources advance by one plane per call and the
   // ring offset rotates (no per-level multiplies or modulo). 528 chunks per level over
@@ -706,23 +772,28 @@ __global__ void __launch_bounds__(kWsThreads, 2)
   // other warps carry no third pointer).
   static_assert(kFChunks > 2 * kWsThreads && kFChunks <= 2 * kWsThreads + kTX, "chunk split");
   uint32_t so = 0;
-  constexpr uint32_t kStageBytes = kFStageDoubles * 8;
+  constexpr uint32_t kStageBytes = kWStageDoubles * 8;
   auto issue = [&](bool copy) {
+    if constexpr (kTmaFeed) {
+      if (copy && tma_lane) {
+        const uint32_t fb = full0 + 8 * static_cast<uint32_t>(so / kStageBytes);
+        if (warp == 0) sm100::mbar_arrive_expect_tx(fb, kWStageTx);
+        sm100::tma_load_3d(f_dst + so, f_map, fb, box_x, box_y, tma_k);
+      }
+      ++tma_k;
+      so = so == (kWsStages - 1) * kStageBytes ? 0u : so + kStageBytes;
+      return;
+    }
     if (copy) {
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         if (ok[q]) sm100::cp_async16(dst[q] + so, src[q]);
         src[q] += P;
       }
-#ifdef HFB_AB_CHUNK3
-      if (ok[2]) sm100::cp_async16(dst[2] + so, src[2]);
-      src[2] += P;
-#else
       if (warp == 0) {
         if (ok[2]) sm100::cp_async16(dst[2] + so, src[2]);
         src[2] += P;
       }
-#endif
     }
     sm100::cp_async_commit();
     so = so == (kWsStages - 1) * kStageBytes ? 0u : so + kStageBytes;
@@ -762,6 +833,8 @@ __global__ void __launch_bounds__(kWsThreads, 2)
 
 #pragma unroll 1
   for (int k = 0; k < kWsStages - 1; ++k) issue(k < nz);
+  if (kTmaFeed && warp == kWaitWarp)
+    for (int l = 0; l < 3 && l < nz; ++l) sm100::mbar_wait(full0 + 8 * l, 0);
 
   // role state carried along K
   double th_prev = 0.0, w_prev = 0.0;              // both roles
@@ -840,17 +913,17 @@ __global__ void __launch_bounds__(kWsThreads, 2)
     const int kk = k + 1;
     const int s1 = s0 == kWsStages - 1 ? 0 : s0 + 1;
     const int s2 = s1 == kWsStages - 1 ? 0 : s1 + 1;
-    const double* S = ring + s0 * kFStageDoubles;
-    const double tk = S[kFOffTh + thc];
-    const double* Up = S + kFOffU + row * kUW + (lane + 2);
+    const double* S = ring + s0 * kWStageDoubles;
+    const double tk = S[kWOffTh + thc];
+    const double* Up = S + kWOffU + row * kUW + (lane + 2);
     const double ui = Up[0], uim1 = Up[-1];
-    const double* Vp = S + kFOffV + (row + 1) * kVW + lane;
+    const double* Vp = S + kWOffV + (row + 1) * kVW + lane;
     const double vj = Vp[0], vjm1 = Vp[-kVW];
-    const double wk = S[kFOffW + row * kSW + lane];
+    const double wk = S[kWOffW + row * kSW + lane];
     if (kAc && (a.roles & 2) != 0) {
-      const double* Pp = S + kFOffP + (row + 1) * kPW + (lane + 2);
+      const double* Pp = S + kWOffP + (row + 1) * kPW + (lane + 2);
       const double pk = Pp[0], pe = Pp[1], pw = Pp[-1], pnn = Pp[kPW], psth = Pp[-kPW];
-      const double rhok = S[kFOffRho + row * kSW + lane];
+      const double rhok = S[kWOffRho + row * kSW + lane];
       // PGF applied to the base momentum (RK) or the current one (single stage)
       const double unk0 = (kRK ? bcur.u : ui) - c.dt_rdx * (pe - pk);
       const double vnk0 = (kRK ? bcur.v : vj) - c.dt_rdy * (pnn - pk);
@@ -908,11 +981,11 @@ __global__ void __launch_bounds__(kWsThreads, 2)
       ps_prev = psk;
       if (kRK) wb_prev = bcur.w;
     } else if (!kAc && (a.roles & 1) != 0) {
-      const double* T0 = S + kFOffTh + thc;
+      const double* T0 = S + kWOffTh + thc;
       const double tkp1 =
-          (kMid || kk + 1 <= nz) ? ring[s1 * kFStageDoubles + kFOffTh + thc] : 0.0;
+          (kMid || kk + 1 <= nz) ? ring[s1 * kWStageDoubles + kWOffTh + thc] : 0.0;
       const double tkp2 =
-          (kMid || kk + 2 <= nz) ? ring[s2 * kFStageDoubles + kFOffTh + thc] : 0.0;
+          (kMid || kk + 2 <= nz) ? ring[s2 * kWStageDoubles + kWOffTh + thc] : 0.0;
       const double xm2 = T0[-2], xm1 = T0[-1], xp1 = T0[1], xp2 = T0[2];
       const double ym2 = T0[-2 * kFThW], ym1 = T0[-kFThW], yp1 = T0[kFThW], yp2 = T0[2 * kFThW];
       const double fzk = face_flux_up<!kMid>(kk, nz, wk, th_prev, tk, tkp1, tkp2);
@@ -936,12 +1009,12 @@ __global__ void __launch_bounds__(kWsThreads, 2)
         // (only the first K phase holds level 1: the mid instantiation carries no branch, and
         // tsfc is read where it is used instead of living in a register for the sweep)
         if (!kMid && kk == 1) {  // new u, v at the lowest level (region 5), from the plane
-          const double* Pp = S + kFOffP + (row + 1) * kPW + (lane + 2);
+          const double* Pp = S + kWOffP + (row + 1) * kPW + (lane + 2);
           const double un1 = (kCX && east) ? 0.0 : ui - c.dt_rdx * (Pp[1] - Pp[0]);
           const double vn1 = (kCY && north) ? 0.0 : vj - c.dt_rdy * (Pp[kPW] - Pp[0]);
           const double wspd = sqrt(un1 * un1 + vn1 * vn1);
           const double tsfc_ij = active ? a.tsfc[(j - 1) * W + (i - 1)] : 0.0;
-          thv = thv + a.dt_ch * wspd * (tsfc_ij - thv) * c.rdz / S[kFOffRho + row * kSW + lane];
+          thv = thv + a.dt_ch * wspd * (tsfc_ij - thv) * c.rdz / S[kWOffRho + row * kSW + lane];
         }
         thv_s[(k & 1) * kThreads + t] = thv;
       }
@@ -960,11 +1033,25 @@ __global__ void __launch_bounds__(kWsThreads, 2)
   // one level: levels <= k+2 have landed (own copies; issued up to k+kWsStages-2), the
   // barrier makes everyone's visible and tells that every warp has finished level k-1,
   // so its slot is refilled with level k+kWsStages-1 (one barrier per level)
+  // TMA feed: the waiter warp observes level k+3 at the END of level k (its own work
+  // done, so the mbarrier latency overlaps the other warps' arithmetic); the barrier at
+  // the top of level k+1 publishes it (mbarrier acquire, then bar.sync)
+  uint32_t wslot = 3 % kWsStages, wpar = 0;  // slot / phase parity of the awaited level
+  auto wait_level = [&]() {
+    sm100::mbar_wait(full0 + 8 * wslot, wpar);
+    if (++wslot == kWsStages) {
+      wslot = 0;
+      wpar ^= 1u;
+    }
+  };
   auto step = [&](int k, auto in_tag, auto mid_tag, auto role_tag) {
-    sm100::cp_async_wait<kWsStages - 4>();
+    if constexpr (!kTmaFeed) sm100::cp_async_wait<kWsStages - 4>();
     __syncthreads();
     issue(decltype(mid_tag)::value || k + kWsStages - 1 < nz);
     level(k, in_tag, mid_tag, role_tag);
+    if constexpr (kTmaFeed && !decltype(role_tag)::value) {
+      if (warp == kWaitWarp && (decltype(mid_tag)::value || k + 3 < nz)) wait_level();
+    }
   };
   // K phases: [0, 3) and [nz-5, nz) with the vertical boundary cases, [3, nz-5) without
   const int mid_lo = nz >= 3 ? 3 : nz, mid_hi = nz - 5 > mid_lo ? nz - 5 : mid_lo;
@@ -1051,6 +1138,40 @@ __global__ void __launch_bounds__(kWsThreads, 2)
 
 }  // namespace
 
+#ifndef HFB_ARITH_FMA
+// ---- host: TMA tensor maps over hfb-layout device arrays (hfb_tmap.cuh) -------------
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+}  // namespace
+
+bool make_box_map(CUtensorMap* m, const double* origin, Grid3 g, int64_t nj, int64_t nz, int bw,
+                  int bh) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const double* base = origin - (kHalo * g.pitch + kIOff);
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.pitch), static_cast<cuuint64_t>(nj + 2 * kHalo),
+                        static_cast<cuuint64_t>(nz)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.pitch * 8),
+                           static_cast<cuuint64_t>(g.plane * 8)};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(bw), static_cast<cuuint32_t>(bh), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+#endif
+
 cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                   int64_t nj, const DynConst& c, const Span& sp,
                                   cudaStream_t s, const PhysArgs* phys, const DynIn* base,
@@ -1059,12 +1180,22 @@ cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, i
   if (!dycore_step_tmem_fits(nz)) return cudaErrorInvalidValue;
   if (phys && base) return cudaErrorInvalidValue;
   if (remote && base) return cudaErrorInvalidValue;  // RK stages exchange by push
-  const size_t smem = std::max<size_t>((static_cast<size_t>(kWsStages) * kFStageDoubles +
+  const size_t smem = std::max<size_t>((static_cast<size_t>(kWsStages) * kWStageDoubles +
                                         static_cast<size_t>(nz) * kThreads +
-                                        (phys ? 2 * kThreads : 0)) * sizeof(double),
+                                        (phys ? 2 * kThreads : 0)) * sizeof(double) + 128,
                                        80 * 1024);
   const int variant = (phys ? 1 : base ? 2 : 0) + (remote ? 3 : 0);
-  void (*kern)(StepTmemArgs, RemoteHalo) = variant == 1   ? k_dyn_step_ws<true, false, false>
+  StepMaps maps{};
+  if (kTmaFeed) {
+    const bool ok = make_box_map(&maps.m[0], in.th, g, nj, nz, kFThW, kFThR) &&
+                    make_box_map(&maps.m[1], in.u, g, nj, nz, kUW, kUR) &&
+                    make_box_map(&maps.m[2], in.v, g, nj, nz, kVW, kVR) &&
+                    make_box_map(&maps.m[3], in.w, g, nj, nz, kSW, kSR) &&
+                    make_box_map(&maps.m[4], in.p, g, nj, nz, kPW, kPR) &&
+                    make_box_map(&maps.m[5], in.rho, g, nj, nz, kSW, kSR);
+    if (!ok) return cudaErrorInvalidValue;
+  }
+  void (*kern)(StepMaps, StepTmemArgs, RemoteHalo) = variant == 1   ? k_dyn_step_ws<true, false, false>
                                            : variant == 2 ? k_dyn_step_ws<false, true, false>
                                            : variant == 3 ? k_dyn_step_ws<false, false, true>
                                            : variant == 4 ? k_dyn_step_ws<true, false, true>
@@ -1103,7 +1234,7 @@ cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, i
   dim3 block(kTX, 2 * kTY);
   dim3 grid(static_cast<unsigned>(ntx * nty));
   static const RemoteHalo none{};
-  kern<<<grid, block, smem, s>>>(a, remote ? *remote : none);
+  kern<<<grid, block, smem, s>>>(maps, a, remote ? *remote : none);
   return cudaGetLastError();
 }
 
