@@ -425,13 +425,14 @@ struct AcoArgs {
 
 // Warp-specialised: 8 warps per CTA over the same 32 x 4 column tile. Warps 4-7 (the
 // "horizontal" role) compute, per level k, the pressure gradient, the divergence and ps
-// (pass B: also the damped u', v'), then FORM the HE-VI coefficients of face k-1 (beta,
-// dd: one shared reciprocal of rf, three quotients) and hand them over through a
-// two-deep shared-memory buffer; warps 0-3 (the "Thomas" role, owners of the TMEM lanes)
-// run the forward recursion of face k-2 one level behind, then the back substitution
-// and the pressure update. The barrier that publishes every staged plane also publishes
-// the handed-over coefficients, so the pipeline needs no extra synchronisation. Two
-// CTAs per SM (TMEM: 256 columns each) give 16 resident warps instead of 8.
+// (pass B: also the damped u', v') and leave ps in shared memory; warps 0-3 (the
+// "Thomas" role, owners of the TMEM lanes) form the HE-VI coefficients of face k-2 one
+// level behind (its upper ps was published by this level's barrier; rho, th, w, fw come
+// from the ring at their own level and stay in registers for two levels) beside the
+// forward recursion of face k-3, then run the back substitution and the pressure update.
+// The barrier that publishes every staged plane also publishes ps, so the pipeline needs
+// no extra synchronisation. Two CTAs per SM (TMEM: 256 columns each) give 16 resident
+// warps instead of 8; the roles carry about the same instruction count per level.
 constexpr int kAcoThreads = 2 * kThreads;
 
 template <bool kB>
@@ -455,7 +456,6 @@ __global__ void __launch_bounds__(kAcoThreads, 2) k_asu_acoustic(AcoArgs a) {
   const int nz = a.nz;
   double* ring = smem;
   double* ps_s = smem + kAStages * kStage;  // nz x 128
-  double* cf_s = ps_s + nz * kThreads;      // [face parity][beta, dd] x 128
 
   const int lane = threadIdx.x, warp = threadIdx.y;  // blockDim = (32, 8)
   const bool thomas = warp < kTY;
@@ -515,17 +515,39 @@ __global__ void __launch_bounds__(kAcoThreads, 2) k_asu_acoustic(AcoArgs a) {
     const double az = static_cast<double>(kk - c.kdmp > 0 ? kk - c.kdmp : 0) * c.rnzd;
     return c.dtau_rdmp * (az > axy ? az : axy);
   };
-  double* const cf_beta = cf_s + t;  // + (f & 1) * 256
-  double* const cf_dd = cf_s + kThreads + t;
-
   for (int k = 0; k < kAStages - 1; ++k) issue(k);
 
-  // Thomas forward recursion of face f from its handed-over (beta, dd); quotients by m
-  // share one reciprocal (hfb_fp64.cuh), else the dialect's divisions
-  double cp_p = 0.0, dp_p = 0.0;
-  auto recursion = [&](int f) {
-    const double beta = cf_beta[(f & 1) * 2 * kThreads];
-    const double dd = cf_dd[(f & 1) * 2 * kThreads];
+  // Thomas role state: rho/th/w/fw of the last two levels (read from the ring at their
+  // own level), the coefficients of the face awaiting its recursion step, cp/dp of the
+  // face below
+  double rho_1 = 0.0, th_1 = 0.0, w_1 = 0.0, fw_1 = 0.0;  // level k-1
+  double rho_2 = 0.0, th_2 = 0.0, w_2 = 0.0, fw_2 = 0.0;  // level k-2
+  double pend_beta = 0.0, pend_dd = 0.0, cp_p = 0.0, dp_p = 0.0;
+  const fp64::Recip rth0 = fp64::recip(c.th0);
+  const double* ps_t = ps_s + t;
+  // coefficient formation of face f (levels f, f+1: rho/th/w/fw from registers, ps from
+  // shared memory); quotients by rf share one reciprocal (hfb_fp64.cuh), else the
+  // dialect's divisions
+  auto formation = [&](int f, double rho_lo, double rho_hi, double th_lo, double th_hi,
+                       double w_lo, double fw_lo, double& beta, double& dd, bool& ok) {
+    const double n_ps = c.h_rdz * (ps_t[(f + 1) * kThreads] - ps_t[f * kThreads]);
+    const double n_th = c.h_grav * (0.5 * (th_lo + th_hi) - c.th0);
+    const double rf = 0.5 * (rho_lo + rho_hi);
+    const fp64::Recip rr = fp64::recip(rf);
+    beta = fp64::quot(c.beta_num, rr, ok);
+    dd = w_lo - fp64::quot(n_ps, rr, ok);
+    dd = dd + fp64::quot(n_th, rth0, ok);
+    dd = dd + c.h * fw_lo;
+    if (__builtin_expect(!ok, 0)) {
+      beta = c.beta_num / rf;
+      dd = w_lo - n_ps / rf;
+      dd = dd + n_th / c.th0;
+      dd = dd + c.h * fw_lo;
+    }
+  };
+  // forward recursion of face f from its coefficients; quotients by m share one
+  // reciprocal
+  auto recursion = [&](int f, double beta, double dd) {
     const double bb = 1.0 + 2.0 * beta;
     const bool first = f == 0;  // face 0: no previous coefficients
     const double m = first ? bb : bb + beta * cp_p;
@@ -544,27 +566,37 @@ __global__ void __launch_bounds__(kAcoThreads, 2) k_asu_acoustic(AcoArgs a) {
     dp_p = dpk;
   };
 
-  // one role's K sweep (the role is compile-time per loop: no cross-role live state)
+  // one role's K sweep (the role is compile-time per loop: no cross-role live state).
+  // Horizontal warps: ps of level k (pass B: u', v'). Thomas warps: formation of face
+  // k-2 (its upper ps, of level k-1, was published by this level's barrier) beside the
+  // recursion of face k-3, so the two division chains overlap.
   auto sweep = [&](auto role_tag) {
     constexpr bool kThomas = decltype(role_tag)::value;
-    double rho_p = 0.0, th_p = 0.0, w_p = 0.0, fw_p = 0.0, ps_p = 0.0;
-    const fp64::Recip rth0 = fp64::recip(c.th0);
 #pragma unroll 1
     for (int k = 0; k < nz; ++k) {
       sm100::cp_async_wait<kAStages - 2>();  // level k landed (own copies)
-      __syncthreads();  // everyone's; the slot of level k-1 is free; face k-2's (beta, dd)
+      __syncthreads();  // everyone's; the slot of level k-1 is free; ps of level k-1
       issue(k + kAStages - 1);
+      const double* S = ring + (k % kAStages) * kStage;
       if constexpr (kThomas) {
-        if (k >= 2) recursion(k - 2);
+        const double wk = S[oW + t], rhok = S[oRho + t], thk = S[oTh + t], fwk = S[oFW + t];
+        if (k >= 2) {
+          bool ok = true;
+          double beta, dd;
+          formation(k - 2, rho_2, rho_1, th_2, th_1, w_2, fw_2, beta, dd, ok);
+          if (k >= 3) recursion(k - 3, pend_beta, pend_dd);
+          pend_beta = beta;
+          pend_dd = dd;
+        }
+        rho_2 = rho_1, th_2 = th_1, w_2 = w_1, fw_2 = fw_1;
+        rho_1 = rhok, th_1 = thk, w_1 = wk, fw_1 = fwk;
       } else {
-        const double* S = ring + (k % kAStages) * kStage;
         const double* Pp = S + oP + (row + 1) * kAW + (lane + 2);
         const double pk = Pp[0], pe = Pp[1], pw = Pp[-1], pnn = Pp[kAW], psth = Pp[-kAW];
         const double uk = S[oU + row * kAW + lane + 2], ukw = S[oU + row * kAW + lane + 1];
         const double fuk = S[oFU + row * kAW + lane + 2], fukw = S[oFU + row * kAW + lane + 1];
         const double vk = S[oV + (row + 1) * kTX + lane], vks = S[oV + row * kTX + lane];
         const double fvk = S[oFV + (row + 1) * kTX + lane], fvks = S[oFV + row * kTX + lane];
-        const double wk = S[oW + t], rhok = S[oRho + t], thk = S[oTh + t], fwk = S[oFW + t];
         const double pc = kB ? S[oPc + t] : pk;  // p at the column (the RK2 base)
 
         // PGF at p (A) / pa (B) applied to the current momentum, plus h * slow tendency
@@ -580,30 +612,6 @@ __global__ void __launch_bounds__(kAcoThreads, 2) k_asu_acoustic(AcoArgs a) {
           a.un[o] = unk - tau * unk;
           a.vn[o] = vnk - tau * vnk;
         }
-        if (k >= 1) {  // HE-VI coefficients of face k-1 (between levels k-1 and k)
-          bool ok = true;
-          const double n_ps = c.h_rdz * (psk - ps_p);
-          const double n_th = c.h_grav * (0.5 * (th_p + thk) - c.th0);
-          const double rf = 0.5 * (rho_p + rhok);
-          const fp64::Recip rr = fp64::recip(rf);
-          double beta = fp64::quot(c.beta_num, rr, ok);
-          double dd = w_p - fp64::quot(n_ps, rr, ok);
-          dd = dd + fp64::quot(n_th, rth0, ok);
-          dd = dd + c.h * fw_p;
-          if (__builtin_expect(!ok, 0)) {  // a range check failed: the dialect's divisions
-            beta = c.beta_num / rf;
-            dd = w_p - n_ps / rf;
-            dd = dd + n_th / c.th0;
-            dd = dd + c.h * fw_p;
-          }
-          cf_beta[((k - 1) & 1) * 2 * kThreads] = beta;
-          cf_dd[((k - 1) & 1) * 2 * kThreads] = dd;
-        }
-        rho_p = rhok;
-        th_p = thk;
-        w_p = wk;
-        fw_p = fwk;
-        ps_p = psk;
       }
     }
   };
@@ -612,10 +620,18 @@ __global__ void __launch_bounds__(kAcoThreads, 2) k_asu_acoustic(AcoArgs a) {
   else
     sweep(std::false_type{});
   sm100::cp_async_wait<0>();
-  __syncthreads();  // face nz-2's coefficients and every ps are visible
+  __syncthreads();  // every ps is visible
 
   if (thomas) {
-    recursion(nz - 2);  // drain: the last face
+    // drain: formation of the last face nz-2 (levels nz-2, nz-1 are in registers), the
+    // recursions of faces nz-3 and nz-2
+    if (nz >= 2) {
+      bool ok = true;
+      double beta, dd;
+      formation(nz - 2, rho_2, rho_1, th_2, th_1, w_2, fw_2, beta, dd, ok);
+      if (nz >= 3) recursion(nz - 3, pend_beta, pend_dd);
+      recursion(nz - 2, beta, dd);
+    }
     sm100::tmem_wait_st();
     // back substitution (faces nz-2 .. 0, w(nz) = 0 is the lid), four per TMEM load,
     // then the pressure update (pass B: the damped w of the short step)
@@ -719,7 +735,7 @@ cudaError_t launch_asu_acoustic(bool pass_b, const AsuState& s, const double* fu
   // two CTAs per SM share the SM's 512 TMEM columns; pad small-nz launches so a third
   // CTA never blocks in tcgen05.alloc
   const size_t smem = std::max<size_t>(
-      (static_cast<size_t>(kAStages) * stage + static_cast<size_t>(nz + 4) * kThreads) *
+      (static_cast<size_t>(kAStages) * stage + static_cast<size_t>(nz) * kThreads) *
           sizeof(double),
       80 * 1024);
   const void* kern = pass_b ? reinterpret_cast<const void*>(k_asu_acoustic<true>)

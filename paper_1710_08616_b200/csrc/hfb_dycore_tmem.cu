@@ -616,16 +616,20 @@ struct Chk {
   static constexpr bool x = kX, y = kY;
 };
 
-// The ring feed: cp.async (LDGSTS, every thread copies 2-3 16-B chunks per level and
-// waits for its own) or, with HFB_WS_TMA, TMA (six 3-D box loads per level issued by one
-// lane each of warps 0-5, completion on the slot's mbarrier; one waiter warp observes it
-// and the per-level CTA barrier publishes it).
-#ifdef HFB_WS_TMA
-constexpr bool kTmaFeed = true;
-#else
+// The ring feed: TMA (the product: six 3-D box loads per level, one field each, issued by
+// lane 0 of warps 0-5; completion on the slot's mbarrier, observed by one advection warp
+// at the end of its level, published to every warp by the per-level CTA barrier) or, in
+// the A/B build flag HFB_WS_CPASYNC, cp.async (LDGSTS: every thread copies 2-3 16-B
+// chunks per level and waits for its own; ~45 more instructions per warp and level).
+#ifdef HFB_WS_CPASYNC
 constexpr bool kTmaFeed = false;
+#else
+constexpr bool kTmaFeed = true;
 #endif
-constexpr int kWaitWarp = 4;  // TMA feed: the warp that waits on the slot barriers
+#ifndef HFB_WAIT_WARP
+#define HFB_WAIT_WARP 4
+#endif
+constexpr int kWaitWarp = HFB_WAIT_WARP;  // TMA feed: the warp that waits on the slots
 
 template <bool kPhys, bool kRK, bool kRemote>
 __global__ void __launch_bounds__(kWsThreads, 2)
@@ -633,7 +637,10 @@ __global__ void __launch_bounds__(kWsThreads, 2)
                   const __grid_constant__ RemoteHalo rem) {
   // (the tensor maps come first: a CUtensorMap must sit 64-B aligned in parameter space)
   static_assert(!(kPhys && kRK), "column physics is not fused into RK stages");
-  extern __shared__ __align__(128) double smem_raw[];
+  // (declared 16-B aligned only: the runtime places the dynamic segment right after the
+  // 64 B of static shared memory, and a larger declared alignment would let the compiler
+  // fold the 128-B round-up below to zero)
+  extern __shared__ __align__(16) double smem_raw[];
   // static shared memory: the slot barriers and the TMEM address, 64 B in total, so the
   // dynamic segment starts 16-B aligned and the 128-B alignment below is exact
   __shared__ __align__(16) uint64_t sbar[8];
@@ -772,16 +779,19 @@ __global__ void __launch_bounds__(kWsThreads, 2)
   // other warps carry no third pointer).
   static_assert(kFChunks > 2 * kWsThreads && kFChunks <= 2 * kWsThreads + kTX, "chunk split");
   uint32_t so = 0;
+  uint32_t tma_bar = 0;  // TMA feed: byte offset of the slot's barrier
   constexpr uint32_t kStageBytes = kWStageDoubles * 8;
   auto issue = [&](bool copy) {
     if constexpr (kTmaFeed) {
       if (copy && tma_lane) {
-        const uint32_t fb = full0 + 8 * static_cast<uint32_t>(so / kStageBytes);
+        const uint32_t fb = full0 + tma_bar;
         if (warp == 0) sm100::mbar_arrive_expect_tx(fb, kWStageTx);
         sm100::tma_load_3d(f_dst + so, f_map, fb, box_x, box_y, tma_k);
       }
       ++tma_k;
-      so = so == (kWsStages - 1) * kStageBytes ? 0u : so + kStageBytes;
+      const bool wrap = so == (kWsStages - 1) * kStageBytes;
+      so = wrap ? 0u : so + kStageBytes;
+      tma_bar = wrap ? 0u : tma_bar + 8u;
       return;
     }
     if (copy) {
@@ -1049,7 +1059,7 @@ __global__ void __launch_bounds__(kWsThreads, 2)
     __syncthreads();
     issue(decltype(mid_tag)::value || k + kWsStages - 1 < nz);
     level(k, in_tag, mid_tag, role_tag);
-    if constexpr (kTmaFeed && !decltype(role_tag)::value) {
+    if constexpr (kTmaFeed && decltype(role_tag)::value == (kWaitWarp < kTY)) {
       if (warp == kWaitWarp && (decltype(mid_tag)::value || k + 3 < nz)) wait_level();
     }
   };
