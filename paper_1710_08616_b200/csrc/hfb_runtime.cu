@@ -306,6 +306,7 @@ struct hfb_ctx {
   // pressure pa, in the prognostic fields' device layout
   double* asu[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   int64_t asu_elems = 0;
+  bool asu_exported = false;  // fu, fv, pa are mapped by the peers (hfb_peer_export)
   // peer-memory halo transport (hfb_peer_export / hfb_peer_attach): halos are stored
   // straight into the neighbours' buffers over NVLink, flags signal their arrival
   bool peer = false;
@@ -753,6 +754,26 @@ void resolve_timings(hfb_ctx* c) {
   c->pending.clear();
 }
 
+// one array to exchange: its name on every rank (a module array, or "asu:<name>" for the
+// ASUCA scheme's exchanged scratch), which of its buffers, this rank's origin of that
+// buffer and its layout
+struct XField {
+  std::string name;
+  int buf = 0;
+  double* origin = nullptr;
+  Grid3 g{};
+  int64_t nk = 1;  // K extent times the trailing dimension
+};
+XField xfield(hfb_ctx* c, const char* name, int buf) {
+  Slot& sl = slot(c, name);
+  return XField{name, buf, sl.d_buf(buf), grid_of(sl), sl.lay.nk * sl.lay.nl};
+}
+std::vector<XField> xfields(hfb_ctx* c, const std::vector<const char*>& names) {
+  std::vector<XField> v;
+  for (const char* n : names) v.push_back(xfield(c, n, slot(c, n).cur));
+  return v;
+}
+void halo_exchange_x(hfb_ctx* c, const std::vector<XField>& fields, cudaStream_t st);
 void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width,
                    cudaStream_t s = nullptr);
 RemoteHalo remote_halo(hfb_ctx* c, const std::vector<Slot*>& f4);
@@ -1300,6 +1321,9 @@ void asuca_prepare(hfb_ctx* c) {
   for (const char* n : {"th", "rho"}) ensure_device(c, slot(c, n), true, 2);
   const int64_t elems = slot(c, "th").lay.alloc_elems;
   if (c->asu_elems != elems) {
+    if (c->asu_exported)
+      fail(HFB_CONFIG, "asuca_step: the layout changed after hfb_peer_export mapped the "
+           "scheme's scratch arrays");
     for (double*& q : c->asu) {
       if (q) cudaFree(q);
       q = nullptr;
@@ -1319,8 +1343,21 @@ void asuca_step(hfb_ctx* c, Stats& st) {
   const int64_t nx = ival(c, "nx"), ny = ival(c, "ny"), nz = ival(c, "nz");
   if (!asuca_fits(nz))
     fail(HFB_CONFIG, "asuca_step is implemented for 2 <= nz <= 65 (got %lld)", (long long)nz);
-  if (c->decomposed && c->decomp.px * c->decomp.py > 1)
-    fail(HFB_CONFIG, "asuca_step runs single-domain (no halo exchange between its passes yet)");
+  // decomposed: every pass's stencil inputs are exchanged first (peer or NCCL transport;
+  // push + signal + wait per exchange, 28 per step with nsound = 6), then the pass runs
+  // over the whole tile
+  const bool multi = c->decomposed && c->decomp.px * c->decomp.py > 1;
+  if (multi) {
+    if (c->group)
+      fail(HFB_CONFIG, "asuca_step on a decomposed context needs the peer or NCCL transport "
+           "(in-process groups exchange module arrays only)");
+    if (c->decomp.halo < 2)
+      fail(HFB_CONFIG, "asuca_step needs a halo of 2 cells (decomposition halo %lld)",
+           (long long)c->decomp.halo);
+    if (c->peer && !c->asu_exported)
+      fail(HFB_CONFIG, "asuca_step with the peer transport: set nsound before "
+           "hfb_peer_export so the scheme's exchanged scratch arrays are mapped");
+  }
   const int64_t nsound = ival(c, "nsound"), nbnd = ival(c, "nbnd"), kdmp = ival(c, "kdmp");
   const double dt = rval(c, "dt"), rdx = rval(c, "rdx"), rdy = rval(c, "rdy"),
                rdz = rval(c, "rdz"), cs2 = rval(c, "cs2"), grav = rval(c, "grav"),
@@ -1354,10 +1391,20 @@ void asuca_step(hfb_ctx* c, Stats& st) {
   const double* thS = th.d_buf(tb);
   const double* rhoS = rho.d_buf(rb);
   int us = b;  // buffer of the stage state's u, v, w (p's is unused by the tendencies)
+  int ts = tb, rs = rb;  // buffers of the stage state's theta, rho
+  // the exchanged scratch: every rank's origin of the same array (layout of th)
+  auto xscratch = [&](const char* name, double* origin) {
+    return XField{name, 0, origin, g, th.lay.nk * th.lay.nl};
+  };
+  if (multi) c->peer_fused = false;  // every exchange of the scheme is a push
   for (int stg = 1; stg <= 3; ++stg) {
     const double dtf = stg == 1 ? dt / 3.0 : stg == 2 ? dt / 2.0 : dt;
     const int64_t nsm = stg == 1 ? nsound / 3 : stg == 2 ? nsound / 2 : nsound;
     const AsuState S{rhoS, thS, u.d_buf(us), v.d_buf(us), w.d_buf(us), p.d_buf(us)};
+    if (multi)  // the tendencies' stencils: the stage state with a 2-cell ring
+      halo_exchange_x(c, {xfield(c, "rho", rs), xfield(c, "th", ts), xfield(c, "u", us),
+                          xfield(c, "v", us), xfield(c, "w", us)},
+                      ks(c));
     launch(c, st, "asuca_tend", [&] {
       return launch_asu_tend(S, F, g, nz, nj, rdx, rdy, rdz, sp, ks(c));
     });
@@ -1378,13 +1425,19 @@ void asuca_step(hfb_ctx* c, Stats& st) {
     count_launch(st, nx, ny);
     count_launch(st, nx, ny);
     count_launch(st, nx, ny);
+    if (multi)  // the acoustic passes read fu(i-1), fv(j-1)
+      halo_exchange_x(c, {xscratch("asu:fu", F.fu), xscratch("asu:fv", F.fv)}, ks(c));
     int cur = b, nxt = x;
     for (int64_t ss = 0; ss < nsm; ++ss) {
       const AsuState C{rhoS, thS, u.d_buf(cur), v.d_buf(cur), w.d_buf(cur), p.d_buf(cur)};
+      if (multi)  // pass A: p with its ring, u(i-1), v(j-1) of the short-step state
+        halo_exchange_x(c, {xfield(c, "p", cur), xfield(c, "u", cur), xfield(c, "v", cur)},
+                        ks(c));
       launch(c, st, "asuca_acoustic_a", [&] {
         return launch_asu_acoustic(false, C, F.fu, F.fv, F.fw, nullptr, pa, nullptr, nullptr,
                                    nullptr, nullptr, g, nz, nj, ca, sp, ks(c));
       });
+      if (multi) halo_exchange_x(c, {xscratch("asu:pa", pa)}, ks(c));  // pass B: pa's ring
       launch(c, st, "asuca_acoustic_b", [&] {
         return launch_asu_acoustic(true, C, F.fu, F.fv, F.fw, pa, nullptr, u.d_buf(nxt),
                                    v.d_buf(nxt), w.d_buf(nxt), p.d_buf(nxt), g, nz, nj, cb, sp,
@@ -1402,6 +1455,8 @@ void asuca_step(hfb_ctx* c, Stats& st) {
     count_launch(st, nx, ny);
     thS = th.d_buf(tx);
     rhoS = rho.d_buf(rx);
+    ts = tx;
+    rs = rx;
   }
   for (Slot* s : {&u, &v, &w, &p}) s->cur = us;
   th.cur = tx;
@@ -1631,6 +1686,8 @@ RemoteHalo remote_halo(hfb_ctx* c, const std::vector<Slot*>& f4) {
   return rh;
 }
 
+void peer_push_exchange(hfb_ctx* c, const std::vector<XField>& fields, cudaStream_t st);
+
 void peer_exchange(hfb_ctx* c, const std::vector<const char*>& fields, cudaStream_t st) {
   NvtxRange nr("halo:peer");
   const hfb_decomp& d = c->decomp;
@@ -1647,6 +1704,16 @@ void peer_exchange(hfb_ctx* c, const std::vector<const char*>& fields, cudaStrea
       }
     return;
   }
+  peer_push_exchange(c, xfields(c, fields), st);
+}
+
+// one push + signal + wait exchange of the given buffers. Safe to reuse a buffer's halo
+// ring at every exchange: a neighbour's last reads of that ring precede (in its stream
+// order) its push of some exchange this rank waited for before pushing again
+void peer_push_exchange(hfb_ctx* c, const std::vector<XField>& fields, cudaStream_t st) {
+  const hfb_decomp& d = c->decomp;
+  const int64_t H = d.halo;
+  if (H == 0) return;
   ++c->halo_epoch;
   ++c->peer_pushes;
   PeerPush push{};
@@ -1666,18 +1733,17 @@ void peer_exchange(hfb_ctx* c, const std::vector<const char*>& fields, cudaStrea
       const int64_t sj0 = dy < 0 ? 1 : dy == 0 ? 1 : d.ny - H + 1;
       const int64_t nbj = dy == 0 ? d.ny : H;
       const int64_t dj0 = dy < 0 ? pr.ny + 1 : dy == 0 ? 1 : 1 - H;
-      for (const char* f : fields) {
-        Slot& sl = slot(c, f);
-        auto it = pr.fields.find(f);
-        if (it == pr.fields.end() || sl.cur >= it->second.nbuf || !it->second.base[sl.cur])
+      for (const XField& f : fields) {
+        auto it = pr.fields.find(f.name);
+        if (it == pr.fields.end() || f.buf >= it->second.nbuf || !it->second.base[f.buf])
           fail(HFB_CONFIG, "peer transport: buffer %d of '%s' on rank %d is not mapped "
-               "(export after binding every array)", sl.cur, f, nr);
+               "(export after binding every array)", f.buf, f.name.c_str(), nr);
         if (push.n == kMaxPeerBoxes) fail(HFB_CONFIG, "peer transport: too many halo boxes");
         const PeerField& rf = it->second;
         PeerBox& b = push.box[push.n++];
-        b.src = sl.d();
-        b.dst = rf.base[sl.cur] + rf.origin_off;
-        b.gs = grid_of(sl);
+        b.src = f.origin;
+        b.dst = rf.base[f.buf] + rf.origin_off;
+        b.gs = f.g;
         b.gd = Grid3{rf.pitch, rf.plane};
         b.si0 = si0;
         b.sj0 = sj0;
@@ -1685,7 +1751,7 @@ void peer_exchange(hfb_ctx* c, const std::vector<const char*>& fields, cudaStrea
         b.dj0 = dj0;
         b.nbi = nbi;
         b.nbj = nbj;
-        b.nk = sl.lay.nk * sl.lay.nl;
+        b.nk = f.nk;
         c->halo_bytes += 2 * nbi * nbj * b.nk * static_cast<int64_t>(sizeof(double));
       }
       // I am at offset (-dx, -dy) from the receiver
@@ -1701,6 +1767,8 @@ void peer_exchange(hfb_ctx* c, const std::vector<const char*>& fields, cudaStrea
              "peer wait");
 }
 
+void nccl_exchange(hfb_ctx* c, const std::vector<XField>& fields, cudaStream_t st);
+
 void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width,
                    cudaStream_t st) {
   if (!c->decomposed || c->decomp.px * c->decomp.py <= 1) return;
@@ -1713,9 +1781,27 @@ void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width
     group_pull(c, fields, st);
     return;
   }
+  (void)width;  // the face boxes always carry the full halo ring (kHalo)
+  nccl_exchange(c, xfields(c, fields), st);
+}
+
+// exchange of explicit buffers (peer or NCCL transport; in-process groups pull by name)
+void halo_exchange_x(hfb_ctx* c, const std::vector<XField>& fields, cudaStream_t st) {
+  if (!c->decomposed || c->decomp.px * c->decomp.py <= 1) return;
+  if (c->peer) {
+    NvtxRange nr("halo:peer");
+    peer_push_exchange(c, fields, st);
+    return;
+  }
+  if (c->group) fail(HFB_CONFIG, "in-process groups exchange module arrays only");
+  nccl_exchange(c, fields, st);
+}
+
+// NCCL transport: two phases (west/east faces, then south/north spanning the I halo so
+// the corners travel), all fields' boxes packed per side, grouped send/recv, unpack
+void nccl_exchange(hfb_ctx* c, const std::vector<XField>& fields, cudaStream_t st) {
   if (!c->nccl_comm) fail(HFB_CONFIG, "decomposed context without a communicator");
   NvtxRange nr("halo:nccl");
-  (void)width;  // the face boxes always carry the full halo ring (kHalo)
   NcclApi& api = nccl();
   const hfb_decomp& d = c->decomp;
   const int nbr[4] = {d.west, d.east, d.south, d.north};
@@ -1727,12 +1813,9 @@ void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width
     for (int s = 2 * phase; s < 2 * phase + 2; ++s) {
       hfb_decomp_faces(&d, s, sbox[s], rbox[s]);
       if (nbr[s] < 0) continue;
-      for (const char* f : fields) {
-        Slot& sl = slot(c, f);
-        int64_t nk = sl.lay.nk * sl.lay.nl;
+      for (const XField& f : fields)
         count[s] += static_cast<size_t>((sbox[s][1] - sbox[s][0] + 1) *
-                                        (sbox[s][3] - sbox[s][2] + 1) * nk);
-      }
+                                        (sbox[s][3] - sbox[s][2] + 1) * f.nk);
       need += count[s];
     }
     if (need == 0) continue;
@@ -1748,14 +1831,11 @@ void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width
     for (int s = 2 * phase; s < 2 * phase + 2; ++s) {
       base[s] = off;
       if (nbr[s] < 0) continue;
-      for (const char* f : fields) {
-        Slot& sl = slot(c, f);
-        int64_t fk = sl.lay.nk * sl.lay.nl;
-        cuda_check(launch_pack_box(sl.d(), c->halo_send + off, grid_of(sl), fk, sbox[s], true,
-                                   st),
+      for (const XField& f : fields) {
+        cuda_check(launch_pack_box(f.origin, c->halo_send + off, f.g, f.nk, sbox[s], true, st),
                    "halo pack");
         off += static_cast<size_t>((sbox[s][1] - sbox[s][0] + 1) * (sbox[s][3] - sbox[s][2] + 1) *
-                                   fk);
+                                   f.nk);
       }
     }
     nccl_check(api.GroupStart(), "ncclGroupStart");
@@ -1772,14 +1852,11 @@ void halo_exchange(hfb_ctx* c, const std::vector<const char*>& fields, int width
     for (int s = 2 * phase; s < 2 * phase + 2; ++s) {
       if (nbr[s] < 0) continue;
       size_t o = base[s];
-      for (const char* f : fields) {
-        Slot& sl = slot(c, f);
-        int64_t fk = sl.lay.nk * sl.lay.nl;
-        cuda_check(launch_pack_box(sl.d(), c->halo_recv + o, grid_of(sl), fk, rbox[s], false,
-                                   st),
+      for (const XField& f : fields) {
+        cuda_check(launch_pack_box(f.origin, c->halo_recv + o, f.g, f.nk, rbox[s], false, st),
                    "halo unpack");
         o += static_cast<size_t>((rbox[s][1] - rbox[s][0] + 1) * (rbox[s][3] - rbox[s][2] + 1) *
-                                 fk);
+                                 f.nk);
       }
       c->halo_bytes += static_cast<int64_t>(2 * count[s] * sizeof(double));
     }
@@ -2868,6 +2945,27 @@ hfb_status hfb_peer_export(hfb_ctx* c, void* buf, size_t cap, size_t* len) {
       f.plane = s.lay.plane;
       f.origin_off = s.lay.origin_off;
       fs.push_back(f);
+    }
+    // the ASUCA scheme's exchanged scratch (fu, fv: the slow momentum tendencies, pa: the
+    // RK2 midpoint pressure), when the scheme's parameters are set: allocated now so the
+    // neighbours map them before the first step
+    auto ns = c->scalars.find("nsound");
+    if (c->app->app == "dycore" && !c->app->plugin && ns != c->scalars.end() && ns->second.init) {
+      asuca_prepare(c);
+      const Slot& th = slot(c, "th");
+      const std::pair<const char*, double*> scr[3] = {
+          {"asu:fu", c->asu[2]}, {"asu:fv", c->asu[3]}, {"asu:pa", c->asu[5]}};
+      for (const auto& [nm, base] : scr) {
+        PeerBlobField f{};
+        std::strncpy(f.name, nm, sizeof f.name - 1);
+        cuda_check(cudaIpcGetMemHandle(&f.h[0], base), "cudaIpcGetMemHandle");
+        f.nbuf = 1;
+        f.pitch = th.lay.pitch;
+        f.plane = th.lay.plane;
+        f.origin_off = th.lay.origin_off;
+        fs.push_back(f);
+      }
+      c->asu_exported = true;
     }
     cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
     PeerBlobHead h{};

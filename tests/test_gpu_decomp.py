@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import paper_1710_08616_b200 as hfb
-from cases import APPS, DYCORE_FILLS, DYCORE_SCALARS, PHYS_FILLS, PHYS_SCALARS, Case
+from cases import APPS, DYCORE_FILLS, DYCORE_SCALARS, PHYS_FILLS, PHYS_SCALARS, Case, _asu
 from golden_io import bits_equal, decl, make_inputs, run_oracle
 
 pytestmark = pytest.mark.gpu
@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 # which declared dims are (i, j) for each array of an app
 IJ_DIMS = {"diffusion": (1, 2), "dycore": (1, 2), "reduction": (1, 2), "bounded": (0, 1),
            "damping": (1, 2), "surface_flux": None, "dycore_full": (1, 2),
-           "dycore_rk3": (1, 2)}
+           "dycore_rk3": (1, 2), "asuca": (1, 2)}
 
 
 def tile_slices(app, name, arr, d):
@@ -199,3 +199,12 @@ def test_overlapped_exchange_equals_serial(app, overlap):
         assert bits_equal(out[k], ref[k]), k
     steps = case.ints["nsteps"]
     assert stats.native_launches == 4 * steps * (5 if overlap else 1)
+
+
+def test_group_refuses_the_asuca_scheme():
+    """The ASUCA scheme's exchanges include scratch arrays that in-process groups cannot
+    pull by name: a decomposed asuca_step in a group fails with HFB_CONFIG (the peer and
+    NCCL transports run it, tests/test_gpu_peer.py) instead of computing without halos."""
+    case = _asu("g_asuca", 40, 30, 10, 1, nbnd=2)
+    with pytest.raises(hfb.HfbError, match="peer or NCCL"):
+        run_decomposed(case, 2, 1)

@@ -15,7 +15,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import paper_1710_08616_b200 as hfb
-from cases import APPS, DYCORE_FILLS, DYCORE_SCALARS, PHYS_FILLS, PHYS_SCALARS, Case
+from cases import APPS, DYCORE_FILLS, DYCORE_SCALARS, PHYS_FILLS, PHYS_SCALARS, Case, _asu
 from golden_io import bits_equal, decl, make_inputs, run_oracle
 from test_gpu_decomp import global_extent, tile_ints, tile_slices
 
@@ -33,6 +33,9 @@ PEER_CASES = {
                         dict(DYCORE_FILLS, **PHYS_FILLS)),
     "dycore_rk3": Case("p_rk3", "dycore_rk3", dict(nx=70, ny=45, nz=20, nsteps=2),
                        dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
+    # the ASUCA scheme: 28 exchanges per step (stage state, fu/fv, p/u/v, pa), nbnd = 3
+    # damping band across the tile edges; 2 short steps in stage 1 (nsound = 6)
+    "asuca": _asu("p_asuca", 70, 45, 20, 2, nbnd=3),
     "diffusion": Case("p_diff", "diffusion", dict(nx=40, ny=36, nz=12, nsteps=3),
                       dict(coef=0.1), {"t_old": (1, 280.0, 10.0)}, unset=["t_new"]),
     "bounded": Case("p_bnd", "bounded", dict(nx=37, ny=21), {},
@@ -44,7 +47,7 @@ PEER_CASES = {
     "reduction": Case("p_red", "reduction", dict(nx=67, ny=45, nz=20), dict(total=0.0),
                       {"y": (6, 0.0, 1.0)}),
 }
-HALO = {"dycore": 2, "dycore4": 2, "dycore_full4": 2, "dycore_full": 2, "dycore_rk3": 2, "diffusion": 1, "reduction": 0,
+HALO = {"asuca": 2, "dycore": 2, "dycore4": 2, "dycore_full4": 2, "dycore_full": 2, "dycore_rk3": 2, "diffusion": 1, "reduction": 0,
         "bounded": 1, "damping": 0}
 
 
@@ -80,7 +83,8 @@ def worker(rank, world, port, name, px, py, q, per_step=False, ordered=False, op
             eng.bind(n, tiles[n], lower=lower)
         eng.attach_peers()
         if per_step:  # the bench's device-resident path: copy-in, n steps, copy-out
-            step = "full_step" if case.app == "dycore_full" else "dycore_step"
+            step = {"dycore_full": "full_step", "asuca": "asuca_step"}.get(case.app,
+                                                                          "dycore_step")
             for n in tiles:
                 eng.copy_to_device(n)
             if per_step == "graph":  # CUDA graphs of 2 steps, replayed
@@ -365,3 +369,30 @@ def test_peer_c4_strong_scaling_tiles_4x2(tmp_path):
             want = ref[n][..., i0:i0 + nx, j0:j0 + ny] if ref[n].ndim == 3 else \
                 ref[n][i0:i0 + nx, j0:j0 + ny]
             assert bits_equal(t, want), f"rank {rank}: {n} differs"
+
+
+@pytest.mark.parametrize("px,py", [(2, 1), (2, 2), (3, 2)])
+def test_peer_asuca_scheme_equals_single_domain(px, py):
+    """The complete ASUCA step on a decomposed context (peer transport, one process per
+    rank): each pass's stencil inputs are pushed into the neighbours' halo rings first —
+    the stage state before the tendencies, fu/fv after them, p/u/v before every first
+    acoustic pass, pa before every second — and the assembled tiles equal the
+    undecomposed oracle bit for bit (the lateral damping band crosses tile edges)."""
+    case, garr, out, parts = run_peer("asuca", px, py)
+    ref = {k: v.copy() for k, v in garr.items()}
+    run_oracle(case, ref)
+    for k in APPS[case.app].outputs:
+        assert bits_equal(out[k], ref[k]), f"asuca {px}x{py}: {k} differs"
+    # nsound = 6: per step 3 stage-state exchanges, 3 fu/fv, 11 p/u/v, 11 pa
+    n = case.ints["nsteps"]
+    assert all(p[1] == (28 * n, 0) for p in parts), [p[1] for p in parts]
+
+
+def test_peer_asuca_graph_replay():
+    """asuca_step replayed from a CUDA graph on the decomposed context (device-side halo
+    epochs): equal to the undecomposed oracle."""
+    case, garr, out, parts = run_peer("asuca", 2, 2, per_step="graph")
+    ref = {k: v.copy() for k, v in garr.items()}
+    run_oracle(case, ref)
+    for k in APPS[case.app].outputs:
+        assert bits_equal(out[k], ref[k]), k
