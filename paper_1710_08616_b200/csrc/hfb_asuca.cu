@@ -13,7 +13,8 @@
 // Machine organisation follows k_dyn_step_ws (hfb_dycore_tmem.cu): a CTA owns a 32 x 4
 // tile of (i,j) columns (warp = row, lane = column) and marches K; every K-plane of the
 // fields the tile reads (with the halo columns/rows its stencils need) is staged into a
-// shared-memory ring by LDGSTS (cp.async, 16-B chunks, L1 bypass) several levels ahead;
+// shared-memory ring by TMA (one 3-D box load per field and level, completion on the
+// slot's mbarrier) several levels ahead;
 // the acoustic passes keep the Thomas coefficients in TENSOR MEMORY (one lane per
 // thread) and ps in shared memory, so HBM traffic is the compulsory bytes: each input
 // read once, each output written once.
@@ -29,9 +30,12 @@
 #include <cstdint>
 #include <type_traits>
 
+#include <cuda.h>
+
 #include "hfb_fp64.cuh"
 #include "hfb_kernels.cuh"
 #include "hfb_sm100.cuh"
+#include "hfb_tmap.cuh"
 
 namespace hfb {
 
@@ -40,62 +44,6 @@ namespace {
 constexpr int kTX = 32, kTY = 4, kThreads = kTX * kTY;
 constexpr int kTmemCols = 256;  // cp: columns 0..127, dp: 128..255 (nz - 1 <= 64)
 constexpr int kDpCol = 128;
-
-// ---- plane staging ---------------------------------------------------------------
-// A plane spec: rows j0' + r0 .. + h - 1 and columns i0' + c0 .. + w - 1 (0-based tile
-// origin i0' = i0 - 1, j0' = j0 - 1) of one field, packed row-major at `off` doubles
-// inside a ring stage. w and c0 are even, so every 16-B chunk is aligned (tiles start at
-// odd 1-based i, rows start 128-B aligned).
-struct PlaneSpec {
-  const double* base;
-  int r0, c0, w, h, off;
-};
-
-template <int NSPEC, int NCH, int NT = kThreads>
-struct Stager {
-  const double* src[NCH];
-  uint32_t dst[NCH];
-  uint32_t ok;  // bit q: chunk q exists and lies inside the allocation
-  __device__ void init(const PlaneSpec (&sp)[NSPEC], int total_chunks, int t, int64_t i0z,
-                       int64_t j0z, int64_t W, int64_t nj, int64_t row_lo, int64_t row_hi,
-                       uint32_t ring_u32) {
-    ok = 0;
-#pragma unroll
-    for (int q = 0; q < NCH; ++q) {
-      const int ch = t + q * NT;
-      src[q] = sp[0].base;
-      dst[q] = ring_u32;
-      if (ch >= total_chunks) continue;
-      const int e = ch * 2;
-      // the chunk's plane: the last spec starting at or before e, selected with
-      // compile-time indices only (a runtime index into `sp` would put the specs in local
-      // memory: ~1.3 GB of DRAM writes per launch at 1581 x 1301)
-      const double* base = sp[0].base;
-      int r0 = sp[0].r0, c0 = sp[0].c0, w = sp[0].w, off = sp[0].off;
-#pragma unroll
-      for (int z = 1; z < NSPEC; ++z)
-        if (e >= sp[z].off) {
-          base = sp[z].base;
-          r0 = sp[z].r0;
-          c0 = sp[z].c0;
-          w = sp[z].w;
-          off = sp[z].off;
-        }
-      const int le = e - off;
-      const int64_t r = j0z + r0 + le / w;
-      const int64_t c = i0z + c0 + le % w;
-      if (r >= -kHalo && r <= nj - 1 + kHalo && c >= row_lo && c + 1 <= row_hi) ok |= 1u << q;
-      src[q] = base + r * W + c;
-      dst[q] = ring_u32 + static_cast<uint32_t>(e) * 8u;
-    }
-  }
-  // stage the plane of level k (0-based) into ring byte offset `so`
-  __device__ __forceinline__ void issue(int64_t k, int64_t P, uint32_t so) const {
-#pragma unroll
-    for (int q = 0; q < NCH; ++q)
-      if (ok & (1u << q)) sm100::cp_async16(dst[q] + so, src[q] + k * P);
-  }
-};
 
 // limited upwind flux (asuca.h90 asu_flux with asu_minmod) as selects: both upwind
 // candidates' slope pairs are formed and one is chosen, so there is no divergence on the
@@ -119,8 +67,6 @@ __device__ __forceinline__ double asu_flux(double vel, double qm1, double q0, do
 constexpr int kTW = kTX + 4, kTR = kTY + 4;   // 36 x 8 plane tile (2-cell ring)
 constexpr int kTPlane = kTW * kTR;            // 288
 constexpr int kTStage = 5 * kTPlane;          // rho, th, u, v, w
-constexpr int kTChunks = kTStage / 2;         // 720
-constexpr int kTChPerThread = (kTChunks + kThreads - 1) / kThreads;  // 6
 constexpr int kTStages = 6;                   // levels k-1..k+2 in use, k+3 in flight
 enum { kFRho = 0, kFTh = 1, kFU = 2, kFV = 3, kFW = 4 };
 
@@ -134,8 +80,23 @@ struct TendArgs {
   Span sp;
 };
 
-__global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
-  extern __shared__ __align__(128) double smem[];
+// The ring is fed by TMA: five 36 x 8 box loads per level (rho, th, u, v, w with their
+// 2-cell ring), issued by lane 0 of warps 0-3 (warp 0 also the fifth), completion on the
+// slot's mbarrier; warp kTendWaitWarp observes level k+3 at the end of its level k and
+// the per-level CTA barrier publishes it.
+struct TendMaps {
+  CUtensorMap m[5];
+};
+constexpr int kTendWaitWarp = 3;
+
+__global__ void __launch_bounds__(kThreads, 3)
+    k_asu_tend(const __grid_constant__ TendMaps maps, TendArgs a) {
+  // (maps first: 64-B aligned parameters; the dynamic segment declared 16-B aligned so
+  // the round-up to 128 B is not folded away)
+  extern __shared__ __align__(16) double smem_raw[];
+  __shared__ __align__(16) uint64_t sbar[8];  // slot barriers
+  const uint32_t raw_u32 = sm100::smem_u32(smem_raw);
+  double* const smem = smem_raw + ((((raw_u32 + 127u) & ~127u) - raw_u32) >> 3);
   const int lane = threadIdx.x, row = threadIdx.y, t = row * kTX + lane;
   const int64_t i0 = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * kTX;
   const int64_t j0 = a.sp.jlo + static_cast<int64_t>(blockIdx.y) * kTY;
@@ -146,18 +107,33 @@ __global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
   const int64_t gi = i + a.sp.i0, gj = j + a.sp.j0, gnx = a.sp.gnx, gny = a.sp.gny;
   const double rdx = a.rdx, rdy = a.rdy, rdz = a.rdz;
 
-  const PlaneSpec specs[5] = {{a.s.rho, -2, -2, kTW, kTR, 0 * kTPlane},
-                              {a.s.th, -2, -2, kTW, kTR, 1 * kTPlane},
-                              {a.s.u, -2, -2, kTW, kTR, 2 * kTPlane},
-                              {a.s.v, -2, -2, kTW, kTR, 3 * kTPlane},
-                              {a.s.w, -2, -2, kTW, kTR, 4 * kTPlane}};
-  Stager<5, kTChPerThread> stg;
-  stg.init(specs, kTChunks, t, i0 - 1, j0 - 1, W, a.nj, a.row_lo, a.row_hi,
-           sm100::smem_u32(smem));
+  static_assert(kTStages <= 8, "slot barriers");
+  const uint32_t full0 = sm100::smem_u32(sbar);
+  if (t == 0) {
+    for (int q = 0; q < kTStages; ++q) sm100::mbar_init(full0 + 8 * q, 1);
+    sm100::mbar_fence_init();
+  }
+  if (lane == 0) {
+    sm100::tma_prefetch_desc(&maps.m[row]);
+    if (row == 0) sm100::tma_prefetch_desc(&maps.m[4]);
+  }
+  __syncthreads();
   constexpr uint32_t kStageBytes = kTStage * 8;
-  auto issue = [&](int k) {
-    if (k < nz) stg.issue(k, P, static_cast<uint32_t>((k % kTStages) * kStageBytes));
-    sm100::cp_async_commit();
+  const uint32_t ring_u32 = sm100::smem_u32(smem);
+  // box origin in allocation coordinates (x = kIOff + i', y = kHalo + j'), 2-cell ring
+  const int xo = static_cast<int>(kIOff + (i0 - 1)) - 2, yo = static_cast<int>(kHalo + (j0 - 1)) - 2;
+  auto issue = [&](int k) {  // level k into slot k % kTStages (lane 0 of every warp)
+    if (lane != 0 || k >= nz) return;
+    const uint32_t slot = static_cast<uint32_t>(k % kTStages);
+    const uint32_t fb = full0 + 8 * slot;
+    const uint32_t so = ring_u32 + slot * kStageBytes;
+    if (row == 0) sm100::mbar_arrive_expect_tx(fb, kStageBytes);
+    sm100::tma_load_3d(so + row * kTPlane * 8, &maps.m[row], fb, xo, yo, k);
+    if (row == 0) sm100::tma_load_3d(so + 4 * kTPlane * 8, &maps.m[4], fb, xo, yo, k);
+  };
+  auto wait_level = [&](int l) {
+    sm100::mbar_wait(full0 + 8 * static_cast<uint32_t>(l % kTStages),
+                     static_cast<uint32_t>((l / kTStages) & 1));
   };
   // value of field f at level k (0-based; any k, ring slot), offset (di, dj)
   const int cen = (row + 2) * kTW + (lane + 2);
@@ -169,6 +145,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
   const int64_t col = (j - 1) * W + (i - 1);
 
   for (int k = 0; k < kTStages - 2; ++k) issue(k);
+  if (row == kTendWaitWarp)
+    for (int l = 0; l < 3 && l < nz; ++l) wait_level(l);
 
   // kLat: the tile touches (or is within 2 cells of) a lateral wall and needs the wall /
   // first-last-face cases; tiles >= 3 cells from every wall run without them
@@ -185,8 +163,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
   // mid-column levels 3 <= kk <= nz-3 run without them
   auto level = [&](int k, auto v_tag) {
   constexpr bool kV = decltype(v_tag)::value;
-    sm100::cp_async_wait<kTStages - 5>();  // levels <= k+2 landed (own copies)
-    __syncthreads();                        // ... everyone's; slot of level k-2 free
+    __syncthreads();  // levels <= k+2 landed (observed by the waiter); slot of level k-2 free
     issue(k + kTStages - 2);
     const int kk = k + 1;
 
@@ -382,6 +359,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
       a.f.fv[o] = fv;
       a.f.fw[o] = fw;
     }
+    if (row == kTendWaitWarp && k + 3 < nz) wait_level(k + 3);
     };
   const int mid_lo = nz > 2 ? 2 : nz, mid_hi = nz - 3 > mid_lo ? nz - 3 : mid_lo;
   int k = 0;
@@ -399,7 +377,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_asu_tend(TendArgs a) {
     sweep(std::false_type{});
   else
     sweep(std::true_type{});
-  sm100::cp_async_wait<0>();
 }
 
 // ============================================================================
@@ -434,28 +411,66 @@ struct AcoArgs {
 // no extra synchronisation. Two CTAs per SM (TMEM: 256 columns each) give 16 resident
 // warps instead of 8; the roles carry about the same instruction count per level.
 constexpr int kAcoThreads = 2 * kThreads;
+// The plane ring is fed by TMA: one 3-D box load per field and level (10 in pass B, 9 in
+// pass A), issued by lane 0 of warps 0-7 (warps 0-1 take a second box), completion on
+// the slot's mbarrier; one horizontal warp (the lighter role) observes level k+1's
+// barrier at the end of its level k, and the per-level CTA barrier publishes it. Plane
+// tiles start 128-B aligned inside a slot.
+__host__ __device__ constexpr int pad16(int n) { return (n + 15) / 16 * 16; }
+constexpr int kAoP = 0;                                   // p or pa: 36 x 6
+constexpr int kAoU = kAoP + pad16(kAW * (kTY + 2));       // u: 36 x 4
+constexpr int kAoFU = kAoU + pad16(kAW * kTY);            // fu: 36 x 4
+constexpr int kAoV = kAoFU + pad16(kAW * kTY);            // v: 32 x 5
+constexpr int kAoFV = kAoV + pad16(kTX * (kTY + 1));      // fv: 32 x 5
+constexpr int kAoW = kAoFV + pad16(kTX * (kTY + 1));      // w, rho, th, fw: 32 x 4 each
+constexpr int kAoRho = kAoW + kTX * kTY;
+constexpr int kAoTh = kAoRho + kTX * kTY;
+constexpr int kAoFW = kAoTh + kTX * kTY;
+constexpr int kAoPc = kAoFW + kTX * kTY;                  // pass B: p at the column
+constexpr int kAcoWaitWarp = 4;
+// box of field f: smem offset, origin offset (dx, dy) from the tile, extent (bw, bh)
+struct AcoBox {
+  int off, dx, dy, bw, bh;
+};
+constexpr AcoBox kAcoBox[10] = {{kAoP, -2, -1, kAW, kTY + 2},  {kAoU, -2, 0, kAW, kTY},
+                                {kAoFU, -2, 0, kAW, kTY},      {kAoV, 0, -1, kTX, kTY + 1},
+                                {kAoFV, 0, -1, kTX, kTY + 1},  {kAoW, 0, 0, kTX, kTY},
+                                {kAoRho, 0, 0, kTX, kTY},      {kAoTh, 0, 0, kTX, kTY},
+                                {kAoFW, 0, 0, kTX, kTY},       {kAoPc, 0, 0, kTX, kTY}};
+// (device code reads the table through its __constant__ copy)
+__constant__ AcoBox kAcoBoxDev[10] = {{kAoP, -2, -1, kAW, kTY + 2},  {kAoU, -2, 0, kAW, kTY},
+                                      {kAoFU, -2, 0, kAW, kTY},      {kAoV, 0, -1, kTX, kTY + 1},
+                                      {kAoFV, 0, -1, kTX, kTY + 1},  {kAoW, 0, 0, kTX, kTY},
+                                      {kAoRho, 0, 0, kTX, kTY},      {kAoTh, 0, 0, kTX, kTY},
+                                      {kAoFW, 0, 0, kTX, kTY},       {kAoPc, 0, 0, kTX, kTY}};
+__host__ __device__ constexpr uint32_t aco_tx(int nb) {
+  uint32_t b = 0;
+  const int words[10] = {kAW * (kTY + 2), kAW * kTY, kAW * kTY, kTX * (kTY + 1),
+                        kTX * (kTY + 1), kTX * kTY, kTX * kTY, kTX * kTY, kTX * kTY, kTX * kTY};
+  for (int f = 0; f < nb; ++f) b += words[f] * 8;
+  return b;
+}
+struct AcoMaps {
+  CUtensorMap m[10];
+};
 
 template <bool kB>
-__global__ void __launch_bounds__(kAcoThreads, 2) k_asu_acoustic(AcoArgs a) {
-  extern __shared__ __align__(128) double smem[];
-  __shared__ uint32_t tmem_base_slot;
-  // stage layout (doubles)
-  constexpr int oP = 0;                          // p or pa: 36 x 6
-  constexpr int oU = oP + kAW * (kTY + 2);       // u: 36 x 4
-  constexpr int oFU = oU + kAW * kTY;            // fu: 36 x 4
-  constexpr int oV = oFU + kAW * kTY;            // v: 32 x 5
-  constexpr int oFV = oV + kTX * (kTY + 1);      // fv: 32 x 5
-  constexpr int oW = oFV + kTX * (kTY + 1);      // w, rho, th, fw: 32 x 4 each
-  constexpr int oRho = oW + kTX * kTY;
-  constexpr int oTh = oRho + kTX * kTY;
-  constexpr int oFW = oTh + kTX * kTY;
-  constexpr int oPc = oFW + kTX * kTY;           // pass B: p at the column, 32 x 4
+__global__ void __launch_bounds__(kAcoThreads, 2)
+    k_asu_acoustic(const __grid_constant__ AcoMaps maps, AcoArgs a) {
+  // (the tensor maps come first: a CUtensorMap must sit 64-B aligned in parameter space;
+  // the dynamic segment is declared 16-B aligned so the round-up below is not folded)
+  extern __shared__ __align__(16) double smem_raw[];
+  __shared__ __align__(16) uint64_t sbar[8];  // slot barriers, TMEM address (64 B)
+  uint32_t& tmem_base_slot = *reinterpret_cast<uint32_t*>(&sbar[7]);
+  const uint32_t raw_u32 = sm100::smem_u32(smem_raw);
+  double* const ring = smem_raw + ((((raw_u32 + 127u) & ~127u) - raw_u32) >> 3);
+  constexpr int oP = kAoP, oU = kAoU, oFU = kAoFU, oV = kAoV, oFV = kAoFV, oW = kAoW,
+                oRho = kAoRho, oTh = kAoTh, oFW = kAoFW, oPc = kAoPc;
+  constexpr int kNB = kB ? 10 : 9;  // boxes per level
   constexpr int kStage = kB ? oPc + kTX * kTY : oPc;
-  constexpr int kChunks = kStage / 2;
-  constexpr int kChPer = (kChunks + kAcoThreads - 1) / kAcoThreads;
+  constexpr uint32_t kTx = aco_tx(kNB);
   const int nz = a.nz;
-  double* ring = smem;
-  double* ps_s = smem + kAStages * kStage;  // nz x 128
+  double* ps_s = ring + kAStages * kStage;  // nz x 128
 
   const int lane = threadIdx.x, warp = threadIdx.y;  // blockDim = (32, 8)
   const bool thomas = warp < kTY;
@@ -470,30 +485,42 @@ __global__ void __launch_bounds__(kAcoThreads, 2) k_asu_acoustic(AcoArgs a) {
   const int64_t gi = i + a.sp.i0, gj = j + a.sp.j0;
   const AsuAcoConst& c = a.c;
 
+  const uint32_t full0 = sm100::smem_u32(sbar);
   if (warp == 0) sm100::tmem_alloc(&tmem_base_slot, kTmemCols);
+  if (warp == 0 && lane == 0) {
+    for (int q = 0; q < kAStages; ++q) sm100::mbar_init(full0 + 8 * q, 1);
+    sm100::mbar_fence_init();
+  }
+  if (lane == 0) {
+    sm100::tma_prefetch_desc(&maps.m[warp]);
+    if (warp + 8 < kNB) sm100::tma_prefetch_desc(&maps.m[warp + 8]);
+  }
   sm100::tmem_fence_before();
   __syncthreads();
   sm100::tmem_fence_after();
   const uint32_t tmem = tmem_base_slot + (static_cast<uint32_t>(32 * row) << 16);
 
-  constexpr int NS = 10;  // pass A's chunks end before the last spec (p at the column)
-  PlaneSpec specs[NS] = {{kB ? a.pa : a.s.p, -1, -2, kAW, kTY + 2, oP},
-                         {a.s.u, 0, -2, kAW, kTY, oU},
-                         {a.fu, 0, -2, kAW, kTY, oFU},
-                         {a.s.v, -1, 0, kTX, kTY + 1, oV},
-                         {a.fv, -1, 0, kTX, kTY + 1, oFV},
-                         {a.s.w, 0, 0, kTX, kTY, oW},
-                         {a.s.rho, 0, 0, kTX, kTY, oRho},
-                         {a.s.th, 0, 0, kTX, kTY, oTh},
-                         {a.fw, 0, 0, kTX, kTY, oFW},
-                         {a.s.p, 0, 0, kTX, kTY, oPc}};
-  Stager<NS, kChPer, kAcoThreads> stg;
-  stg.init(specs, kChunks, tid, i0 - 1, j0 - 1, W, a.nj, a.row_lo, a.row_hi,
-           sm100::smem_u32(ring));
+  // this warp's boxes (lane 0 issues): field `warp`, and `warp + 8` for warps 0-1 in
+  // pass B / warp 0 in pass A; allocation coordinates x = kIOff + i', y = kHalo + j'
+  const uint32_t ring_u32 = sm100::smem_u32(ring);
+  const int xo = static_cast<int>(kIOff + (i0 - 1)), yo = static_cast<int>(kHalo + (j0 - 1));
+  const AcoBox b0 = kAcoBoxDev[warp];
+  const AcoBox b1 = kAcoBoxDev[warp + 8 < kNB ? warp + 8 : 0];
+  const bool two = warp + 8 < kNB;
   constexpr uint32_t kStageBytes = kStage * 8;
-  auto issue = [&](int k) {
-    if (k < nz) stg.issue(k, P, static_cast<uint32_t>((k % kAStages) * kStageBytes));
-    sm100::cp_async_commit();
+  auto issue = [&](int k) {  // level k into slot k % kAStages
+    if (lane != 0 || k >= nz) return;
+    const uint32_t slot = static_cast<uint32_t>(k % kAStages);
+    const uint32_t fb = full0 + 8 * slot;
+    const uint32_t so = ring_u32 + slot * kStageBytes;
+    if (warp == 0) sm100::mbar_arrive_expect_tx(fb, kTx);
+    sm100::tma_load_3d(so + b0.off * 8, &maps.m[warp], fb, xo + b0.dx, yo + b0.dy, k);
+    if (two) sm100::tma_load_3d(so + b1.off * 8, &maps.m[warp + 8], fb, xo + b1.dx, yo + b1.dy, k);
+  };
+  // the waiter (a horizontal warp) observes level l's slot barrier
+  auto wait_level = [&](int l) {
+    sm100::mbar_wait(full0 + 8 * static_cast<uint32_t>(l % kAStages),
+                     static_cast<uint32_t>((l / kAStages) & 1));
   };
 
   const bool east = gi == a.sp.gnx, west = gi == 1, north = gj == a.sp.gny, south = gj == 1;
@@ -516,6 +543,7 @@ __global__ void __launch_bounds__(kAcoThreads, 2) k_asu_acoustic(AcoArgs a) {
     return c.dtau_rdmp * (az > axy ? az : axy);
   };
   for (int k = 0; k < kAStages - 1; ++k) issue(k);
+  if (warp == kAcoWaitWarp) wait_level(0);
 
   // Thomas role state: rho/th/w/fw of the last two levels (read from the ring at their
   // own level), the coefficients of the face awaiting its recursion step, cp/dp of the
@@ -574,8 +602,8 @@ __global__ void __launch_bounds__(kAcoThreads, 2) k_asu_acoustic(AcoArgs a) {
     constexpr bool kThomas = decltype(role_tag)::value;
 #pragma unroll 1
     for (int k = 0; k < nz; ++k) {
-      sm100::cp_async_wait<kAStages - 2>();  // level k landed (own copies)
-      __syncthreads();  // everyone's; the slot of level k-1 is free; ps of level k-1
+      __syncthreads();  // level k landed (observed by the waiter); the slot of level k-1
+                        // is free; ps of level k-1 is visible
       issue(k + kAStages - 1);
       const double* S = ring + (k % kAStages) * kStage;
       if constexpr (kThomas) {
@@ -612,6 +640,7 @@ __global__ void __launch_bounds__(kAcoThreads, 2) k_asu_acoustic(AcoArgs a) {
           a.un[o] = unk - tau * unk;
           a.vn[o] = vnk - tau * vnk;
         }
+        if (warp == kAcoWaitWarp && k + 1 < nz) wait_level(k + 1);
       }
     }
   };
@@ -619,7 +648,6 @@ __global__ void __launch_bounds__(kAcoThreads, 2) k_asu_acoustic(AcoArgs a) {
     sweep(std::true_type{});
   else
     sweep(std::false_type{});
-  sm100::cp_async_wait<0>();
   __syncthreads();  // every ps is visible
 
   if (thomas) {
@@ -708,16 +736,20 @@ bool asuca_fits(int64_t nz) { return nz >= 2 && nz - 1 <= 64; }
 cudaError_t launch_asu_tend(const AsuState& s, const AsuTend& f, Grid3 g, int64_t nz, int64_t nj,
                             double rdx, double rdy, double rdz, const Span& sp, cudaStream_t st) {
   if (sp.ihi < sp.ilo || sp.jhi < sp.jlo) return cudaSuccess;
-  const size_t smem = static_cast<size_t>(kTStages) * kTStage * sizeof(double);
+  const size_t smem = static_cast<size_t>(kTStages) * kTStage * sizeof(double) + 128;
   {
     cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(k_asu_tend), smem);
     if (e != cudaSuccess) return e;
   }
+  TendMaps maps{};
+  const double* fld[5] = {s.rho, s.th, s.u, s.v, s.w};
+  for (int q = 0; q < 5; ++q)
+    if (!make_box_map(&maps.m[q], fld[q], g, nj, nz, kTW, kTR)) return cudaErrorInvalidValue;
   TendArgs a{s, f, g, static_cast<int>(nz), nj, -kIOff, g.pitch - kIOff - 1, rdx, rdy, rdz, sp};
   dim3 block(kTX, kTY);
   dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
             static_cast<unsigned>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY));
-  k_asu_tend<<<grid, block, smem, st>>>(a);
+  k_asu_tend<<<grid, block, smem, st>>>(maps, a);
   return cudaGetLastError();
 }
 
@@ -728,16 +760,20 @@ cudaError_t launch_asu_acoustic(bool pass_b, const AsuState& s, const double* fu
                                 const Span& sp, cudaStream_t st) {
   if (sp.ihi < sp.ilo || sp.jhi < sp.jlo) return cudaSuccess;
   if (!asuca_fits(nz)) return cudaErrorInvalidValue;
-  const int stage = pass_b ? (kAW * (kTY + 2) + 2 * kAW * kTY + 2 * kTX * (kTY + 1) +
-                              5 * kTX * kTY)
-                           : (kAW * (kTY + 2) + 2 * kAW * kTY + 2 * kTX * (kTY + 1) +
-                              4 * kTX * kTY);
+  const int stage = pass_b ? kAoPc + kTX * kTY : kAoPc;  // padded plane tiles
   // two CTAs per SM share the SM's 512 TMEM columns; pad small-nz launches so a third
-  // CTA never blocks in tcgen05.alloc
+  // CTA never blocks in tcgen05.alloc (+128 B: the ring's 128-B round-up)
   const size_t smem = std::max<size_t>(
       (static_cast<size_t>(kAStages) * stage + static_cast<size_t>(nz) * kThreads) *
-          sizeof(double),
+              sizeof(double) + 128,
       80 * 1024);
+  AcoMaps maps{};
+  {
+    const double* fld[10] = {pass_b ? pa : s.p, s.u, fu, s.v, fv, s.w, s.rho, s.th, fw, s.p};
+    for (int f = 0; f < (pass_b ? 10 : 9); ++f)
+      if (!make_box_map(&maps.m[f], fld[f], g, nj, nz, kAcoBox[f].bw, kAcoBox[f].bh))
+        return cudaErrorInvalidValue;
+  }
   const void* kern = pass_b ? reinterpret_cast<const void*>(k_asu_acoustic<true>)
                             : reinterpret_cast<const void*>(k_asu_acoustic<false>);
   {
@@ -750,9 +786,9 @@ cudaError_t launch_asu_acoustic(bool pass_b, const AsuState& s, const double* fu
   dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
             static_cast<unsigned>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY));
   if (pass_b)
-    k_asu_acoustic<true><<<grid, block, smem, st>>>(a);
+    k_asu_acoustic<true><<<grid, block, smem, st>>>(maps, a);
   else
-    k_asu_acoustic<false><<<grid, block, smem, st>>>(a);
+    k_asu_acoustic<false><<<grid, block, smem, st>>>(maps, a);
   return cudaGetLastError();
 }
 
