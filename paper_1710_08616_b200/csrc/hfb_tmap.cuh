@@ -19,6 +19,7 @@ bool make_box_map(CUtensorMap* m, const double* origin, Grid3 g, int64_t nj, int
 // ring (th, u, v, w, p, rho)
 struct StepMaps {
   CUtensorMap m[6];
+  CUtensorMap base[5];  // RK stages: the base state's th, u, v, w, p (L2 prefetch boxes)
 };
 
 }  // namespace hfb
