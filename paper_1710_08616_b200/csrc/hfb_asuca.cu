@@ -42,8 +42,8 @@ namespace hfb {
 namespace {
 
 constexpr int kTX = 32, kTY = 4, kThreads = kTX * kTY;
-constexpr int kTmemCols = 256;  // cp: columns 0..127, dp: 128..255 (nz - 1 <= 64)
-constexpr int kDpCol = 128;
+// TMEM per acoustic CTA: cp in columns [0, n/2), dp in [n/2, n); n = 256 (two CTAs per SM)
+// up to 64 faces, 512 (one CTA per SM) up to 128
 
 // limited upwind flux (asuca.h90 asu_flux with asu_minmod) as selects: both upwind
 // candidates' slope pairs are formed and one is chosen, so there is no divergence on the
@@ -486,7 +486,9 @@ __global__ void __launch_bounds__(kAcoThreads, 2)
   const AsuAcoConst& c = a.c;
 
   const uint32_t full0 = sm100::smem_u32(sbar);
-  if (warp == 0) sm100::tmem_alloc(&tmem_base_slot, kTmemCols);
+  const uint32_t tmem_cols = a.nz - 1 <= 64 ? 256u : 512u;
+  const uint32_t dp_col = tmem_cols / 2;
+  if (warp == 0) sm100::tmem_alloc(&tmem_base_slot, tmem_cols);
   if (warp == 0 && lane == 0) {
     for (int q = 0; q < kAStages; ++q) sm100::mbar_init(full0 + 8 * q, 1);
     sm100::mbar_fence_init();
@@ -589,7 +591,7 @@ __global__ void __launch_bounds__(kAcoThreads, 2)
       dpk = num / m;
     }
     sm100::tmem_st_f64(tmem + 2 * f, cpk);
-    sm100::tmem_st_f64(tmem + kDpCol + 2 * f, dpk);
+    sm100::tmem_st_f64(tmem + dp_col + 2 * f, dpk);
     cp_p = cpk;
     dp_p = dpk;
   };
@@ -671,7 +673,7 @@ __global__ void __launch_bounds__(kAcoThreads, 2)
     for (int cb = (nf - 1) / 4; cb >= 0; --cb) {
       double cpv[4], dpv[4];
       sm100::tmem_ld_4f64(tmem + 8 * cb, cpv);
-      sm100::tmem_ld_4f64(tmem + kDpCol + 8 * cb, dpv);
+      sm100::tmem_ld_4f64(tmem + dp_col + 8 * cb, dpv);
 #pragma unroll
       for (int q = 3; q >= 0; --q) {
         const int f = 4 * cb + q;  // face f = w-point f+1 (1-based) at 0-based level f
@@ -689,7 +691,7 @@ __global__ void __launch_bounds__(kAcoThreads, 2)
   }
   sm100::tmem_fence_before();
   __syncthreads();
-  if (warp == 0) sm100::tmem_dealloc(tmem_base_slot, kTmemCols);
+  if (warp == 0) sm100::tmem_dealloc(tmem_base_slot, tmem_cols);
 }
 
 // theta = thb + dtf * fth, rho = rhob + dtf * frho over the span (asuca.h90 stage end)
@@ -731,7 +733,7 @@ AsuAcoConst make_asu_aco_const(double h, double dtau, double rdx, double rdy, do
   return c;
 }
 
-bool asuca_fits(int64_t nz) { return nz >= 2 && nz - 1 <= 64; }
+bool asuca_fits(int64_t nz) { return nz >= 2 && nz - 1 <= 128; }
 
 cudaError_t launch_asu_tend(const AsuState& s, const AsuTend& f, Grid3 g, int64_t nz, int64_t nj,
                             double rdx, double rdy, double rdz, const Span& sp, cudaStream_t st) {

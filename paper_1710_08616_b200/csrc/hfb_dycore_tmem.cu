@@ -34,6 +34,7 @@
 #define dycore_acoustic_tmem_fits dycore_acoustic_tmem_fits_fma
 #define launch_dycore_step_tmem launch_dycore_step_tmem_fma
 #define dycore_step_tmem_fits dycore_step_tmem_fits_fma
+#define dycore_step_ws_fits dycore_step_ws_fits_fma
 #define launch_dycore_step_ws launch_dycore_step_ws_fma
 #endif
 #include <cuda.h>
@@ -534,6 +535,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_dyn_step_tmem(StepTmemArgs a) {
 }  // namespace
 
 bool dycore_step_tmem_fits(int64_t nz) { return nz >= 2 && nz - 1 <= 64; }
+// the warp-specialised step: 256 TMEM columns per CTA up to 64 faces, 512 up to 128 (the
+// shared memory of such a column, ps included, then keeps one CTA per SM as well)
+bool dycore_step_ws_fits(int64_t nz) { return nz >= 2 && nz - 1 <= 128; }
 
 cudaError_t launch_dycore_step_tmem(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                     int64_t nj, const DynConst& c, const Span& sp,
@@ -707,7 +711,11 @@ __global__ void __launch_bounds__(kWsThreads, 2)
   const bool chk_y = !(gj0 >= 3 && gj0 + kTY - 1 <= gny - 2 && j0 + kTY - 1 <= a.sp.jhi);
 
   const uint32_t full0 = sm100::smem_u32(full_bar);
-  if (warp == 0) sm100::tmem_alloc(&tmem_base_slot, kTmemCols);
+  // TMEM: cp in columns [0, ncols/2), dp in [ncols/2, ncols); 256 columns (two CTAs per SM)
+  // up to 64 faces, 512 (one CTA per SM) up to 128
+  const uint32_t tmem_cols = a.nz - 1 <= 64 ? 256u : 512u;
+  const uint32_t dp_col = tmem_cols / 2;
+  if (warp == 0) sm100::tmem_alloc(&tmem_base_slot, tmem_cols);
   if (kTmaFeed && warp == 0 && lane == 0) {
     for (int q = 0; q < kWsStages; ++q) sm100::mbar_init(full0 + 8 * q, 1);
     sm100::mbar_fence_init();
@@ -913,7 +921,7 @@ __global__ void __launch_bounds__(kWsThreads, 2)
   // cp/dp of face f go to this thread's TMEM lane
   auto thomas_commit = [&](int f, double cpk, double dpk) {
     sm100::tmem_st_f64(tmem + 2 * f, cpk);
-    sm100::tmem_st_f64(tmem + kDpCol + 2 * f, dpk);
+    sm100::tmem_st_f64(tmem + dp_col + 2 * f, dpk);
     cp_prev = cpk;
     dp_prev = dpk;
   };
@@ -1127,7 +1135,7 @@ __global__ void __launch_bounds__(kWsThreads, 2)
     for (int cb = (nf - 1) / 4; cb >= 0; --cb) {
       double cpv[4], dpv[4];
       sm100::tmem_ld_4f64(tmem + 8 * cb, cpv);
-      sm100::tmem_ld_4f64(tmem + kDpCol + 8 * cb, dpv);
+      sm100::tmem_ld_4f64(tmem + dp_col + 8 * cb, dpv);
 #pragma unroll
       for (int q = 3; q >= 0; --q) {
         const int f = 4 * cb + q;
@@ -1151,7 +1159,7 @@ __global__ void __launch_bounds__(kWsThreads, 2)
   }
   sm100::tmem_fence_before();
   __syncthreads();
-  if (warp == 0) sm100::tmem_dealloc(tmem_base_slot, kTmemCols);
+  if (warp == 0) sm100::tmem_dealloc(tmem_base_slot, tmem_cols);
 }
 
 }  // namespace
@@ -1195,7 +1203,7 @@ cudaError_t launch_dycore_step_ws(const DynIn& in, const DynOut& out, Grid3 g, i
                                   cudaStream_t s, const PhysArgs* phys, const DynIn* base,
                                   const RemoteHalo* remote, int debug_skip) {
   if (sp.ihi < sp.ilo || sp.jhi < sp.jlo) return cudaSuccess;
-  if (!dycore_step_tmem_fits(nz)) return cudaErrorInvalidValue;
+  if (!dycore_step_ws_fits(nz)) return cudaErrorInvalidValue;
   if (phys && base) return cudaErrorInvalidValue;
   if (remote && base) return cudaErrorInvalidValue;  // RK stages exchange by push
   const size_t smem = std::max<size_t>((static_cast<size_t>(kWsStages) * kWStageDoubles +

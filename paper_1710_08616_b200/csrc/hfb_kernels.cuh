@@ -105,6 +105,7 @@ cudaError_t launch_dycore_acoustic_tmem(const DynIn& in, const DynOut& out, Grid
                                         const Span& sp, cudaStream_t s);
 // the whole timestep in one kernel (advection + acoustic), same budget
 bool dycore_step_tmem_fits(int64_t nz);
+bool dycore_step_ws_fits(int64_t nz);  // the product step kernel (nz - 1 <= 128)
 cudaError_t launch_dycore_step_tmem(const DynIn& in, const DynOut& out, Grid3 g, int64_t nz,
                                     int64_t nj, const DynConst& c, const Span& sp,
                                     cudaStream_t s);

@@ -1187,7 +1187,11 @@ void dycore_step(hfb_ctx* c, Stats& st, bool with_physics = false) {
   for (Slot* s : {&th, &u, &v, &w, &p}) ensure_device(c, *s, true);
   DynIn in{rho.d(), th.d(), u.d(), v.d(), w.d(), p.d()};
   DynOut out{th.d_alt(), u.d_alt(), v.d_alt(), w.d_alt(), p.d_alt()};
-  const bool fused = dycore_step_tmem_fits(nz) && !c->force_generic && !c->force_split;
+  // the product kernel takes nz - 1 <= 128; the A/B variants (single role, TMA twin, two
+  // columns per thread) keep their 64-face TMEM budget
+  const bool variant = c->force_single_role || c->force_tma || c->force_ws2;
+  const bool fused = (variant ? dycore_step_tmem_fits(nz) : dycore_step_ws_fits(nz)) &&
+                     !c->force_generic && !c->force_split;
   const bool fused_physics = fused && !c->force_single_role && with_physics;
   PhysArgs ph{};
   if (fused_physics) ph = phys_args(c, slot(c, "tsfc"), slot(c, "colm"));
@@ -1260,8 +1264,8 @@ void dycore_step(hfb_ctx* c, Stats& st, bool with_physics = false) {
 // s1 and s2 (stage states); the new state ends in s1.
 void rk3_step(hfb_ctx* c, Stats& st) {
   int64_t nx = ival(c, "nx"), ny = ival(c, "ny"), nz = ival(c, "nz");
-  if (!dycore_step_tmem_fits(nz))
-    fail(HFB_CONFIG, "rk3_step is implemented for 2 <= nz <= 65 (got %lld)", (long long)nz);
+  if (!dycore_step_ws_fits(nz))
+    fail(HFB_CONFIG, "rk3_step is implemented for 2 <= nz <= 129 (got %lld)", (long long)nz);
   if (c->decomposed && c->decomp.px * c->decomp.py > 1 && c->decomp.halo < 2)
     fail(HFB_CONFIG, "rk3_step needs a halo of 2 cells, got %d", c->decomp.halo);
   if (c->group)  // stage states are overwritten within a step: needs true rank lockstep
@@ -1342,7 +1346,7 @@ void asuca_prepare(hfb_ctx* c) {
 void asuca_step(hfb_ctx* c, Stats& st) {
   const int64_t nx = ival(c, "nx"), ny = ival(c, "ny"), nz = ival(c, "nz");
   if (!asuca_fits(nz))
-    fail(HFB_CONFIG, "asuca_step is implemented for 2 <= nz <= 65 (got %lld)", (long long)nz);
+    fail(HFB_CONFIG, "asuca_step is implemented for 2 <= nz <= 129 (got %lld)", (long long)nz);
   // decomposed: every pass's stencil inputs are exchanged first (peer or NCCL transport;
   // push + signal + wait per exchange, 28 per step with nsound = 6), then the pass runs
   // over the whole tile

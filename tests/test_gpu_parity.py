@@ -84,8 +84,15 @@ LARGE = [
          dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
     Case("dycore_77x203x31_s3", "dycore", dict(nx=77, ny=203, nz=31, nsteps=3),
          dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
-    # nz - 1 > 64: beyond the TMEM budget, served by the generic (L2 round-trip) kernel
+    # nz - 1 > 64: 512 TMEM columns per CTA (one CTA per SM) up to nz = 129; beyond that
+    # the generic (L2 round-trip) kernels
     Case("dycore_40x30x80_s2", "dycore", dict(nx=40, ny=30, nz=80, nsteps=2),
+         dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
+    Case("dycore_37x21x129_s2", "dycore", dict(nx=37, ny=21, nz=129, nsteps=2),
+         dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
+    Case("dycore_35x9x140_s1", "dycore", dict(nx=35, ny=9, nz=140, nsteps=1),
+         dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
+    Case("rk3_40x30x100_s2", "dycore_rk3", dict(nx=40, ny=30, nz=100, nsteps=2),
          dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
     Case("dycore_33x9x65_s2", "dycore", dict(nx=33, ny=9, nz=65, nsteps=2),
          dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
@@ -103,6 +110,7 @@ LARGE = [
     _asu("asuca_77x41x31_s2", 77, 41, 31, 2, nsound=12, nbnd=3),
     _asu("asuca_40x36x2_s2", 40, 36, 2, 2, kdmp=1),
     _asu("asuca_33x9x65_s1", 33, 9, 65, 1, nsound=6, nbnd=4),
+    _asu("asuca_33x21x100_s1", 33, 21, 100, 1, nsound=6, nbnd=4),
 ]
 
 
@@ -562,3 +570,14 @@ def test_entry_copy_out_skips_untouched_arrays():
     assert h2d == 6 * field and d2h == 5 * field
     for k in ("th", "u", "v", "w", "p", "rho"):
         assert bits_equal(arrs[k], ref[k]), k
+
+
+@pytest.mark.parametrize("nz,fused", [(58, True), (100, True), (129, True), (140, False)])
+def test_tall_columns_take_the_fused_kernel(nz, fused):
+    """Columns of up to 128 faces run the fused step kernel (512 TMEM columns, one CTA per
+    SM, above 64 faces): one native launch per step. Taller ones fall back to the portable
+    kernels (advection + acoustic launches, the dialect's intermediates through L2)."""
+    case = Case(f"tall_{nz}", "dycore", dict(nx=40, ny=12, nz=nz, nsteps=2),
+                dict(DYCORE_SCALARS), dict(DYCORE_FILLS))
+    stats, _ = run_engine(case, make_inputs(case))
+    assert (stats.native_launches == 2) == fused, stats
