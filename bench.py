@@ -572,6 +572,9 @@ def bench_ours(args):
                           "timed_steps": f"{args.steps} steps replayed from one CUDA graph"
                           if use_graph else f"{args.steps} enqueued steps",
                           "timed_region_ms": round(ms, 3),
+                          "column_sums": "thread per column, the K sum in the dialect's "
+                                         "left-to-right order inside the fused step (bit-exact; "
+                                         "no warp-level tree reduction)" if physics else None,
                           "l2": f"inputs larger than L2: "
                                 f"{6 * tnx_l * tny_l * NZ * 8 / 2**30:.2f} GiB state + "
                                 f"{5 * tnx_l * tny_l * NZ * 8 / 2**30:.2f} GiB outputs per "
