@@ -25,7 +25,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import paper_1710_08616_b200 as hfb
-from cases import APPS, DYCORE_FILLS, DYCORE_SCALARS, PHYS_FILLS, PHYS_SCALARS, Case
+from cases import APPS, DYCORE_FILLS, DYCORE_SCALARS, PHYS_FILLS, PHYS_SCALARS, Case, _asu
 from golden_io import bits_equal, decl, make_inputs, run_oracle
 from test_gpu_decomp import global_extent, tile_ints, tile_slices
 
@@ -43,8 +43,9 @@ CASES = {
                       dict(coef=0.1), {"t_old": (1, 280.0, 10.0)}, unset=["t_new"]),
     "reduction": Case("m_red", "reduction", dict(nx=67, ny=45, nz=20), dict(total=0.0),
                       {"y": (6, 0.0, 1.0)}),
+    "asuca": _asu("m_asuca", 70, 45, 20, 1, nbnd=3),
 }
-HALO = {"dycore": 2, "dycore_full": 2, "diffusion": 1, "reduction": 0}
+HALO = {"dycore": 2, "dycore_full": 2, "diffusion": 1, "reduction": 0, "asuca": 2}
 
 
 def free_port():
@@ -144,12 +145,12 @@ def run(name, px, py, transport, mode="main"):
     return parts
 
 
-@pytest.mark.parametrize("name", ["dycore", "dycore_full", "diffusion", "reduction"])
+@pytest.mark.parametrize("name", ["dycore", "dycore_full", "diffusion", "reduction", "asuca"])
 def test_nccl_transport_two_gpus(name):
     run(name, 2, 1, "nccl")
 
 
-@pytest.mark.parametrize("name", ["dycore", "diffusion", "reduction"])
+@pytest.mark.parametrize("name", ["dycore", "diffusion", "reduction", "asuca"])
 def test_peer_transport_across_devices(name):
     run(name, 2, 1, "peer")
 
