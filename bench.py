@@ -334,6 +334,11 @@ def bench_ours(args):
 
     rank, world, local = dist_env()
     n = args.gpus
+
+    def trace(what):  # --trace: phase markers on stderr (debugging multi-rank runs)
+        if args.trace:
+            print(f"[bench rank {rank}] {what} t={time.perf_counter():.2f}", file=sys.stderr,
+                  flush=True)
     if world != n:
         raise SystemExit(f"--gpus {n} but WORLD_SIZE={world}")
     if n not in GRIDS:
@@ -352,6 +357,7 @@ def bench_ours(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    trace("process group up")
     eng = hfb.Engine("dycore", device=local)
     # weak scaling (default): a 1581 x 1301 tile per GPU; --strong: the C4 grid split
     tnx, tny = (C2_NX, C2_NY) if args.tile512 else (NX, NY)  # weak-scaling tile
@@ -361,6 +367,7 @@ def bench_ours(args):
     arrs = make_state(eng, d, gnx, gny, physics)
     if n > 1 and args.transport == "peer":
         eng.attach_peers()
+    trace("state bound, peers attached")
     for k in arrs:
         eng.copy_to_device(k)
     eng.synchronize()
@@ -387,19 +394,27 @@ def bench_ours(args):
     for _ in range(args.warmup):
         eng.enqueue(entry)
     eng.synchronize()
+    trace("warm-up steps done")
     run_steps()  # graph capture (+ K steps)
     run_steps()  # the other buffer side when K is odd
     eng.synchronize()
+    trace("graphs captured")
     w0 = time.perf_counter()
     for _ in range(args.warmup):
         eng.enqueue(entry)
     eng.synchronize()
     per = (time.perf_counter() - w0) / max(1, args.warmup)
+    if n > 1:  # every rank must run the same number of steps (the exchanges pair up)
+        t = torch.tensor([per], device="cpu" if one_gpu else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        per = float(t.item())
     extra = max(0, int(0.4 / max(per, 1e-6)) - args.warmup)
+    trace(f"per-step {per * 1e3:.3f} ms, {extra} more warm-up steps")
     for _ in range(extra):
         eng.enqueue(entry)
     warmup_run = 2 * args.warmup + extra + 2 * args.steps
     eng.synchronize()
+    trace("sustained warm-up done")
 
     # ---- device-resident timed region: K timesteps ------------------------------------
     t_ev0 = torch.cuda.Event(enable_timing=True)
@@ -407,6 +422,7 @@ def bench_ours(args):
     launches = 0
     with ClockSampler(local, args.smi_ms) as clocks:  # nvidia-smi running before the region
         barrier()
+        trace("timed region starts")
         clocks.start()
         t_ev0.record(stream)
         launches += run_steps()
@@ -415,6 +431,7 @@ def bench_ours(args):
         clocks.stop()
     barrier()
     ms = t_ev0.elapsed_time(t_ev1)
+    trace("timed region done")
     # per-kernel device times from a second pass of the same K steps with CUDA events
     # around every launch (hfb_profile); kept out of the timed region, whose events
     # would otherwise add ~2% to the step
@@ -444,6 +461,7 @@ def bench_ours(args):
     barrier()
     eng.set_option("arith", "exact")
     ms_fma = f_ev0.elapsed_time(f_ev1)
+    trace("tolerance-mode region done")
     ms_local = ms
     if n > 1:
         t = torch.tensor([ms], device="cpu" if one_gpu else "cuda")
@@ -518,7 +536,9 @@ def bench_ours(args):
     if n > 1 and args.transport == "peer":
         eng2.attach_peers()
     eng2.set("nsteps", e2e_nsteps)
+    trace("e2e engine ready")
     eng2.run(main_entry)  # warm-up call
+    trace("e2e warm-up call done")
     arrs2 = make_state(eng2, d, gnx, gny, physics)
     eng2.set("nsteps", e2e_nsteps)
     e2e_calls = max(1, min(3, args.steps // 10))
@@ -687,6 +707,7 @@ def main():
     ap.add_argument("--one-gpu-test", action="store_true",
                     help="testing only: every rank on cuda:0 (multi-rank path on one GPU)")
     ap.add_argument("--smi-ms", type=int, default=20, help="nvidia-smi sampling interval")
+    ap.add_argument("--trace", action="store_true", help="phase markers on stderr")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

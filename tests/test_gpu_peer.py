@@ -396,3 +396,26 @@ def test_peer_asuca_graph_replay():
     run_oracle(case, ref)
     for k in APPS[case.app].outputs:
         assert bits_equal(out[k], ref[k]), k
+
+
+def test_bench_multi_rank_path_on_one_gpu():
+    """bench.py's multi-rank path (torchrun, 2 ranks, peer transport, graph-replayed timed
+    region, e2e) with both ranks on this one GPU (--one-gpu-test): it must finish and print
+    one JSON line — every rank runs the same number of steps (the warm-up count is agreed
+    over the ranks), or the pairwise exchanges deadlock."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = {k: v for k, v in os.environ.items() if not k.startswith("HFB_")}
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        str(free_port()), str(root / "bench.py"), "--gpus", "2", "--steps", "4",
+                        "--warmup", "3", "--tile512", "--one-gpu-test", "--no-secondary"],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["halo"]["bytes_per_step_rank0"] > 0
