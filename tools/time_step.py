@@ -23,8 +23,10 @@ if full or asuca or rk3:
 eng = hfb.Engine(app)
 if app == "dycore":
     eng.set_option("arith", arith)
-    if len(sys.argv) > 6:  # A/B build only (libhfb_variants.so): 1 = no advection, 2 = no acoustic
-        eng.set_option("debug_skip", sys.argv[6])
+    if len(sys.argv) > 7:  # kernel variant (hfb_set_option "variant")
+        eng.set_option("variant", sys.argv[7])
+    if len(sys.argv) > 6 and sys.argv[6] != "0":  # A/B build only (libhfb_variants.so):
+        eng.set_option("debug_skip", sys.argv[6])     # 1 = no advection, 2 = no acoustic
 for k, v in dict(nx=nx, ny=ny, nz=nz, nsteps=1).items():
     eng.set(k, v)
 if app == "dycore":
