@@ -365,8 +365,26 @@ def bench_ours(args):
     d = hfb.decomp_init(gnx, gny, NZ, px, py, rank, halo=2)
     decompose(eng, d, n, args.transport, dist)
     arrs = make_state(eng, d, gnx, gny, physics)
+    transport_note = None
     if n > 1 and args.transport == "peer":
-        eng.attach_peers()
+        # the peer transport maps the neighbours' buffers by CUDA IPC; if that fails on any
+        # rank (e.g. no peer access between the devices), every rank falls back to NCCL
+        err = ""
+        try:
+            eng.attach_peers()
+        except Exception as e:  # noqa: BLE001 - reported in the JSON line
+            err = repr(e)[:200]
+        t = torch.tensor([0.0 if err else 1.0], device="cpu" if one_gpu else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if t.item() < 1.0:
+            if one_gpu:
+                raise SystemExit(f"peer attach failed on one GPU: {err}")
+            eng.close()
+            args.transport = "nccl"
+            transport_note = f"peer transport unavailable ({err or 'on another rank'}): NCCL"
+            eng = hfb.Engine("dycore", device=local)
+            decompose(eng, d, n, "nccl", dist)
+            arrs = make_state(eng, d, gnx, gny, physics)
     trace("state bound, peers attached")
     for k in arrs:
         eng.copy_to_device(k)
@@ -588,6 +606,7 @@ def bench_ours(args):
                "config": {"workload": wl, "entry": entry,
                           "global_grid": [gnx, gny, NZ], "decomposition": f"{px}x{py}",
                           "transport": args.transport if n > 1 else None,
+                          "transport_note": transport_note,
                           "warmup_steps_run": warmup_run,
                           "timed_steps": f"{args.steps} steps replayed from one CUDA graph"
                           if use_graph else f"{args.steps} enqueued steps",
