@@ -621,7 +621,7 @@ struct Chk {
 };
 
 // The ring feed: TMA (the product: six 3-D box loads per level, one field each, issued by
-// lane 0 of warps 0-5; completion on the slot's mbarrier, observed by one advection warp
+// lane 0 of the acoustic warps 0-3; completion on the slot's mbarrier, observed by one advection warp
 // at the end of its level, published to every warp by the per-level CTA barrier) or, in
 // the A/B build flag HFB_WS_CPASYNC, cp.async (LDGSTS: every thread copies 2-3 16-B
 // chunks per level and waits for its own; ~45 more instructions per warp and level).
@@ -720,7 +720,17 @@ __global__ void __launch_bounds__(kWsThreads, 2)
     for (int q = 0; q < kWsStages; ++q) sm100::mbar_init(full0 + 8 * q, 1);
     sm100::mbar_fence_init();
   }
-  if (kTmaFeed && warp < 6 && lane == 0) sm100::tma_prefetch_desc(&maps.m[warp]);
+  // TMA issue: which boxes this warp's lane 0 loads per level (-1: none). The acoustic
+  // warps issue (warp 0 th + u, 1 v + w, 2 p, 3 rho; warp 0 arms the slot barrier), an
+  // advection warp waits: the advection role is the one whose per-level instruction
+  // stream sets the pace (issuing from warps 0-5 instead: 2.68-2.71 vs 2.65 ms; waiting on
+  // an acoustic warp: 2.75-2.79 ms, tools/gpu_r2zf.sh, gpu_r2zg.sh)
+  const int f0 = warp == 0 ? 0 : warp == 1 ? 2 : warp == 2 ? 4 : warp == 3 ? 5 : -1;
+  const int f1 = warp == 0 ? 1 : warp == 1 ? 3 : -1;
+  if (kTmaFeed && lane == 0) {
+    if (f0 >= 0) sm100::tma_prefetch_desc(&maps.m[f0]);
+    if (f1 >= 0) sm100::tma_prefetch_desc(&maps.m[f1]);
+  }
   sm100::tmem_fence_before();
   __syncthreads();
   sm100::tmem_fence_after();
@@ -728,24 +738,20 @@ __global__ void __launch_bounds__(kWsThreads, 2)
 
   // TMA feed: lane 0 of warp f (f < 6) loads field f's box (th, u, v, w, p, rho order);
   // box origins in allocation coordinates (x = kIOff + i', y = kHalo + j', z = k)
-  const bool tma_lane = kTmaFeed && lane == 0 && warp < 6;
-  int f_off = kWOffTh, f_dx = -2, f_dy = -2;
-  switch (warp) {
-    case 1: f_off = kWOffU; f_dx = -2; f_dy = 0; break;
-    case 2: f_off = kWOffV; f_dx = 0; f_dy = -1; break;
-    case 3: f_off = kWOffW; f_dx = 0; f_dy = 0; break;
-    case 4: f_off = kWOffP; f_dx = -2; f_dy = -1; break;
-    case 5: f_off = kWOffRho; f_dx = 0; f_dy = 0; break;
-    default: break;
-  }
-  const CUtensorMap* f_map = &maps.m[warp < 6 ? warp : 0];
-  const int box_x = static_cast<int>(kIOff + (i0 - 1)) + f_dx;
-  const int box_y = static_cast<int>(kHalo + (j0 - 1)) + f_dy;
-  const uint32_t f_dst = sm100::smem_u32(ring) + static_cast<uint32_t>(f_off * 8);
+  const bool tma_lane = kTmaFeed && lane == 0 && f0 >= 0;
+  auto box_of = [&](int f, int& off, int& dx, int& dy) {
+    off = f == 0 ? kWOffTh : f == 1 ? kWOffU : f == 2 ? kWOffV : f == 3 ? kWOffW
+        : f == 4 ? kWOffP : kWOffRho;
+    dx = (f == 0 || f == 1 || f == 4) ? -2 : 0;
+    dy = f == 0 ? -2 : (f == 2 || f == 4) ? -1 : 0;
+  };
+  const int x00 = static_cast<int>(kIOff + (i0 - 1)), y00 = static_cast<int>(kHalo + (j0 - 1));
+  int off0 = 0, dx0 = 0, dy0 = 0, off1 = 0, dx1 = 0, dy1 = 0;
+  box_of(f0 < 0 ? 0 : f0, off0, dx0, dy0);
+  box_of(f1 < 0 ? 0 : f1, off1, dx1, dy1);
+  const uint32_t dst0 = sm100::smem_u32(ring) + static_cast<uint32_t>(off0 * 8);
+  const uint32_t dst1 = sm100::smem_u32(ring) + static_cast<uint32_t>(off1 * 8);
   int tma_k = 0;  // the next level this lane loads
-  // base-state prefetch boxes (RK stages): th 32x4, u 34x4 (i-2..), v 32x5 (j-1..), w, p
-  const int base_x = static_cast<int>(kIOff + (i0 - 1)) + (warp == 1 ? -2 : 0);
-  const int base_y = static_cast<int>(kHalo + (j0 - 1)) + (warp == 2 ? -1 : 0);
 
   const double* src[kWsChunksPerThread];
   uint32_t dst[kWsChunksPerThread];
@@ -797,12 +803,20 @@ __global__ void __launch_bounds__(kWsThreads, 2)
       if (copy && tma_lane) {
         const uint32_t fb = full0 + tma_bar;
         if (warp == 0) sm100::mbar_arrive_expect_tx(fb, kWStageTx);
-        sm100::tma_load_3d(f_dst + so, f_map, fb, box_x, box_y, tma_k);
+        sm100::tma_load_3d(dst0 + so, &maps.m[f0], fb, x00 + dx0, y00 + dy0, tma_k);
+        if (f1 >= 0)
+          sm100::tma_load_3d(dst1 + so, &maps.m[f1], fb, x00 + dx1, y00 + dy1, tma_k);
         // RK stages: the base state of the same level into L2 (TMA prefetch boxes), so
         // the per-thread base loads one level ahead hit L2 instead of DRAM (C2 RK3 step
-        // 1.41 -> 1.17 ms)
-        if (kRK && warp < 5)
-          sm100::tma_prefetch_l2_3d(&maps.base[warp], base_x, base_y, tma_k);
+        // 1.41 -> 1.17 ms); boxes th 32x4, u 34x4 (i-2..), v 32x5 (j-1..), w, p
+        if constexpr (kRK) {
+          if (f0 < 5)
+            sm100::tma_prefetch_l2_3d(&maps.base[f0], x00 + (f0 == 1 ? -2 : 0),
+                                      y00 + (f0 == 2 ? -1 : 0), tma_k);
+          if (f1 >= 0 && f1 < 5)
+            sm100::tma_prefetch_l2_3d(&maps.base[f1], x00 + (f1 == 1 ? -2 : 0),
+                                      y00 + (f1 == 2 ? -1 : 0), tma_k);
+        }
       }
       ++tma_k;
       const bool wrap = so == (kWsStages - 1) * kStageBytes;
