@@ -185,9 +185,11 @@ def decompose(eng, d, n, transport, dist):
         eng.set_decomposition(d)
 
 
-def make_state(eng, d, gnx, gny, physics):
+def make_state(eng, d, gnx, gny, physics, asuca=False):
     """Bind the synthetic state of this rank's tile (global-flat-indexed fields, pinned
-    host buffers); `physics` adds the column-physics fields of the full timestep."""
+    host buffers); `physics` adds the column-physics fields of the full timestep, `asuca`
+    the ASUCA scheme's scalars (set before the peers are attached: the export then maps
+    the scheme's exchanged scratch)."""
     from paper_1710_08616_b200 import synthetic
     box = [(0, NZ), (d.i0, d.i0 + d.nx), (d.j0, d.j0 + d.ny)]
     arrs = {k: synthetic.field((NZ, gnx, gny), *v, box=box, order="F")
@@ -198,6 +200,8 @@ def make_state(eng, d, gnx, gny, physics):
         arrs.update({k: synthetic.field((gnx, gny), *v, box=box2, order="F")
                      for k, v in synthetic.PHYS_FILLS.items()})
         scalars.update(synthetic.PHYS_SCALARS)
+    if asuca:
+        scalars.update(synthetic.asuca_params(NZ))
     for k, v in dict(nx=int(d.nx), ny=int(d.ny), nz=NZ, nsteps=1).items():
         eng.set(k, v)
     for k, v in scalars.items():
@@ -301,22 +305,29 @@ def secondary(local, steps=20, warmup=5):
     return out
 
 
-def cpu_baseline_port(seconds_budget=20.0):
+def cpu_baseline_port(seconds_budget=20.0, asuca=False):
     """The C restatement (oracle/, KIJ storage, OpenMP over j on every host core) timed on
     a bounded sample of the same workload: whole full timesteps of a 512x512x58 block
     (the per-point cost does not depend on the block size; the C4 grid would need ~20 GB
-    of host memory for the oracle's state and scratch)."""
+    of host memory for the oracle's state and scratch); ASUCA steps of a 128x128x58 block
+    for --entry asuca_step."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle
     from paper_1710_08616_b200 import synthetic
     cores = os.cpu_count() or 1
     oracle.set_threads(cores)
-    sx, sy = C2_NX, C2_NY
+    sx, sy = (128, 128) if asuca else (C2_NX, C2_NY)
     a = {k: synthetic.field((NZ, sx, sy), *v, order="F") for k, v in synthetic.DYCORE_FILLS.items()}
     a.update({k: synthetic.field((sx, sy), *v, order="F") for k, v in synthetic.PHYS_FILLS.items()})
     prm = dict(synthetic.DYCORE_SCALARS, **synthetic.PHYS_SCALARS)
+    ap = synthetic.asuca_params(NZ)
+    prm.update({k: v for k, v in ap.items() if isinstance(v, float)})
+    ints = {k: v for k, v in ap.items() if isinstance(v, int)}
 
     def one():
+        if asuca:
+            oracle.asuca_run(1, prm, ints, a["rho"], a["th"], a["u"], a["v"], a["w"], a["p"])
+            return
         oracle.full_run(1, prm, a["rho"], a["th"], a["u"], a["v"], a["w"], a["p"], a["tsfc"],
                         a["colm"])
     one()  # warm (scratch allocation, page faults)
@@ -329,7 +340,8 @@ def cpu_baseline_port(seconds_budget=20.0):
             break
     return {"value": sx * sy * NZ * steps / el, "unit": UNIT, "cores": cores, "kind": "port",
             "cpu_model": cpu_model(),
-            "sample": f"{steps} full timesteps (full_step) of a {sx}x{sy}x{NZ} block "
+            "sample": f"{steps} {'ASUCA steps (asuca_step)' if asuca else 'full timesteps (full_step)'}"
+                      f" of a {sx}x{sy}x{NZ} block "
                       f"(oracle/hfb_oracle.c, KIJ order, OpenMP {cores} threads), {el:.2f} s"}
 
 
@@ -352,6 +364,7 @@ def bench_ours(args):
     px, py = GRIDS[n]
     entry = args.entry
     physics = entry == "full_step"
+    asuca = entry == "asuca_step"
     # --one-gpu-test (testing only): every rank on cuda:0, gloo for the host-side
     # collectives — exercises the multi-rank path (peer transport) on a one-GPU box
     one_gpu = args.one_gpu_test
@@ -370,7 +383,7 @@ def bench_ours(args):
     gnx, gny = (NX, NY) if args.strong else (tnx * px, tny * py)
     d = hfb.decomp_init(gnx, gny, NZ, px, py, rank, halo=2)
     decompose(eng, d, n, args.transport, dist)
-    arrs = make_state(eng, d, gnx, gny, physics)
+    arrs = make_state(eng, d, gnx, gny, physics, asuca)
     transport_note = None
     if n > 1 and args.transport == "peer":
         # the peer transport maps the neighbours' buffers by CUDA IPC; if that fails on any
@@ -390,7 +403,7 @@ def bench_ours(args):
             transport_note = f"peer transport unavailable ({err or 'on another rank'}): NCCL"
             eng = hfb.Engine("dycore", device=local)
             decompose(eng, d, n, "nccl", dist)
-            arrs = make_state(eng, d, gnx, gny, physics)
+            arrs = make_state(eng, d, gnx, gny, physics, asuca)
     trace("state bound, peers attached")
     for k in arrs:
         eng.copy_to_device(k)
@@ -467,7 +480,8 @@ def bench_ours(args):
     eng.synchronize()
     barrier()
     eng.profile(False)
-    kt = {k: eng.kernel_time(k) for k in BYTES_PER_POINT}
+    kernel_bytes = ASUCA_KERNEL_BYTES if asuca else BYTES_PER_POINT
+    kt = {k: eng.kernel_time(k) for k in kernel_bytes}
     kt = {k: v for k, v in kt.items() if v[1] > 0}
     # the tolerance mode side by side (hfb_set_option "arith" "fma": the same fused step
     # with FMA contraction, within 1e-12 per field of the reference after one step,
@@ -482,12 +496,15 @@ def bench_ours(args):
         eng.synchronize()
         barrier()
         return e0.elapsed_time(e1)
-    ms_exact2 = timed_region()
-    eng.set_option("arith", "fma")
-    run_steps()
-    run_steps()
-    ms_fma = timed_region()
-    eng.set_option("arith", "exact")
+    if asuca:  # the tolerance build exists for the fused dycore step only
+        ms_exact2 = ms_fma = ms
+    else:
+        ms_exact2 = timed_region()
+        eng.set_option("arith", "fma")
+        run_steps()
+        run_steps()
+        ms_fma = timed_region()
+        eng.set_option("arith", "exact")
     trace("tolerance-mode region done")
     ms_local = ms
     if n > 1:
@@ -509,9 +526,13 @@ def bench_ours(args):
     # one step of the tile is one launch (N=1) or the interior launch plus four boundary
     # strips (decomposed, halo exchange overlapped): the kernel's device time per STEP
     # moves the tile's algorithmic bytes
-    abytes = alg_bytes(dom, tnx_l, tny_l, NZ)
+    abytes = (ASUCA_KERNEL_BYTES[dom] * tnx_l * tny_l * NZ if asuca
+              else alg_bytes(dom, tnx_l, tny_l, NZ))
     per_step_prof = dom_ms / args.steps
-    if dom_n == args.steps:  # the step is this one launch: the timed region's CUDA events
+    if asuca:  # several launches of the dominant pass per step: its time per LAUNCH
+        per_step = dom_ms / dom_n
+        timing = "per-launch events (profiled pass), per launch"
+    elif dom_n == args.steps:  # the step is this one launch: the timed region's CUDA events
         per_step = ms_local / args.steps  # (launch stream) / launches — conservative, it
         timing = "timed-region events / launches"  # includes the gaps between launches
     else:
@@ -540,34 +561,44 @@ def bench_ours(args):
                 "frac": round(achieved / hbm, 4), "traffic": traffic, "traffic_key": tkey,
                 "kernel": dom, "frac_of_nominal_8TBps": round(achieved / 8000.0, 4),
                 "peak_source": src, "algorithmic_bytes_per_launch": abytes,
-                "algorithmic_bytes": f"{BYTES_PER_POINT[dom]} B/point x {tnx_l}x{tny_l}x{NZ}"
+                "algorithmic_bytes": f"{kernel_bytes[dom]} B/point x {tnx_l}x{tny_l}x{NZ}"
                                      + (f" + {BYTES_PER_COLUMN[dom]} B/column x {tnx_l}x{tny_l}"
-                                        if dom in BYTES_PER_COLUMN else ""),
+                                        if dom in BYTES_PER_COLUMN else "")
+                                     + (" per launch" if asuca else ""),
                 "launches_per_step": dom_n // args.steps,
+                "algorithmic_bytes_per_step": (ASUCA_BYTES_PER_POINT * tnx_l * tny_l * NZ
+                                               if asuca else abytes),
+                "step_frac": round(ASUCA_BYTES_PER_POINT * tnx_l * tny_l * NZ /
+                                   (ms_local / args.steps / 1e3) / 1e9 / hbm, 4)
+                if asuca else None,
                 "kernel_ms_avg": round(per_step, 5), "timing": timing,
                 "kernel_ms_profiled": round(per_step_prof, 5),
                 "share_of_step": round(min(1.0, per_step_prof / (ms_local / args.steps)), 3),
                 "kernels": {k: {"ms_avg": round(v[0] / args.steps, 5),
-                                "GBps": round(alg_bytes(k, tnx_l, tny_l, NZ) /
-                                              (v[0] / args.steps / 1e3) / 1e9, 1)}
+                                "launches_per_step": v[1] // args.steps,
+                                "GBps": round(kernel_bytes[k] * tnx_l * tny_l * NZ * v[1] /
+                                              args.steps / (v[0] / args.steps / 1e3) / 1e9, 1)
+                                if asuca else
+                                round(alg_bytes(k, tnx_l, tny_l, NZ) /
+                                      (v[0] / args.steps / 1e3) / 1e9, 1)}
                             for k, v in kt.items()}}
 
     # ---- end to end through the public API with host buffers --------------------------
     # one e2e step = one call of the program's main entry (transferHere copy-in of the
     # state arrays from pinned host memory, `nsteps` timesteps, copy-out), as the
     # generated host code does (codegen.cpp:570-600)
-    main_entry = "main_full" if physics else "main"
-    e2e_nsteps = 100
+    main_entry = "main_full" if physics else "main_asuca" if asuca else "main"
+    e2e_nsteps = 10 if asuca else 100
     eng2 = hfb.Engine("dycore", device=local)
     decompose(eng2, d, n, args.transport, dist)
-    arrs2 = make_state(eng2, d, gnx, gny, physics)
+    arrs2 = make_state(eng2, d, gnx, gny, physics, asuca)
     if n > 1 and args.transport == "peer":
         eng2.attach_peers()
     eng2.set("nsteps", e2e_nsteps)
     trace("e2e engine ready")
     eng2.run(main_entry)  # warm-up call
     trace("e2e warm-up call done")
-    arrs2 = make_state(eng2, d, gnx, gny, physics)
+    arrs2 = make_state(eng2, d, gnx, gny, physics, asuca)
     eng2.set("nsteps", e2e_nsteps)
     e2e_calls = max(1, min(3, args.steps // 10))
     xb0 = eng2.transfer_bytes()
@@ -598,6 +629,8 @@ def bench_ours(args):
 
     if rank == 0:
         what = ("full timestep (dycore + HE-VI + column physics)" if physics
+                else "ASUCA time scheme (RK3 + 11 RK2 HE-VI acoustic short steps + damping + "
+                     "limited advection of rho, theta, u, v, w; 2496 B/pt)" if asuca
                 else "dycore step (advection + HE-VI)")
         if args.strong:
             wl = f"{what} {NX}x{NY}x{NZ} split over {n} GPU(s) (BASELINE configs[3], strong)"
@@ -628,14 +661,15 @@ def bench_ours(args):
                                 f"{6 * tnx_l * tny_l * NZ * 8 / 2**30:.2f} GiB state + "
                                 f"{5 * tnx_l * tny_l * NZ * 8 / 2**30:.2f} GiB outputs per "
                                 f"step and GPU vs 126 MB L2 (no flush needed)"},
-               "roofline": roofline, "tolerance_mode": tolerance_mode, "e2e": e2e,
+               "roofline": roofline, "tolerance_mode": None if asuca else tolerance_mode,
+               "e2e": e2e,
                "gpu_launches": launches,
                "clocks": clocks.summary(), "halo_bytes": halo}
         if n > 1:  # rank 0's halo traffic (sent + received) per step and its rate
             hps = halo / (warmup_run + 2 * args.steps)
             out["halo"] = {"bytes_per_step_rank0": int(hps),
                            "GBps_rank0": round(hps / (ms / args.steps / 1e3) / 1e9, 2)}
-        out["cpu_baseline"] = cpu_baseline_port() if n == 1 else None
+        out["cpu_baseline"] = cpu_baseline_port(asuca=asuca) if n == 1 else None
         if n == 1 and not args.no_secondary:
             out["other_configs"] = secondary(local)
         print(json.dumps(out), flush=True)
@@ -659,16 +693,24 @@ def bench_reference(args):
         subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "ref"], check=True)
     from paper_1710_08616_b200 import synthetic
     cores = os.cpu_count() or 1
-    sx, sy = 16, 16
     physics = args.entry == "full_step"
+    asuca = args.entry == "asuca_step"
+    sx, sy = (8, 8) if asuca else (16, 16)  # an ASUCA step is ~30x a full step's work
     tmp = Path(tempfile.mkdtemp(prefix="hftref_"))
     scen = tmp / "dycore.sc"
     lines = [f"source {ROOT / 'apps/dycore/dyn_state.h90'}",
-             f"source {ROOT / 'apps/dycore/dycore.h90'}", "mode ref",
-             f"entry {'main_full' if physics else 'main'}",
-             "max_steps 2000000000", f"int dyn_state nx {sx}", f"int dyn_state ny {sy}",
-             f"int dyn_state nz {NZ}", "int dyn_state nsteps 1"]
+             f"source {ROOT / 'apps/dycore/dycore.h90'}"]
+    if asuca:
+        lines.append(f"source {ROOT / 'apps/dycore/asuca.h90'}")
+    lines += ["mode ref",
+              f"entry {'main_full' if physics else 'main_asuca' if asuca else 'main'}",
+              "max_steps 2000000000", f"int dyn_state nx {sx}", f"int dyn_state ny {sy}",
+              f"int dyn_state nz {NZ}", "int dyn_state nsteps 1"]
     scal = dict(synthetic.DYCORE_SCALARS, **(synthetic.PHYS_SCALARS if physics else {}))
+    if asuca:
+        ap = synthetic.asuca_params(NZ)
+        lines += [f"int dyn_state {k} {v}" for k, v in ap.items() if isinstance(v, int)]
+        scal.update({k: v for k, v in ap.items() if isinstance(v, float)})
     fills = dict(synthetic.DYCORE_FILLS, **(synthetic.PHYS_FILLS if physics else {}))
     lines += [f"real dyn_state {k} {float(v).hex()}" for k, v in scal.items()]
     lines += [f"fill dyn_state {k} {s} {float(o).hex()} {float(c).hex()}"
@@ -692,7 +734,7 @@ def bench_reference(args):
     el = sum(one_step() for _ in range(args.steps))
     value = cores * sx * sy * NZ * args.steps / el
     sample = (f"{cores} concurrent reference interpreters (run_reference, 1 thread each), "
-              f"each one {'full timestep (main_full)' if physics else 'dycore step'} of its "
+              f"each one {'full timestep (main_full)' if physics else 'ASUCA step (main_asuca)' if asuca else 'dycore step'} of its "
               f"own {sx}x{sy}x{NZ} block of the {NX}x{NY}x{NZ} workload; time = the slowest "
               f"interpreter's run_reference call (process start and .h90 parsing excluded)")
     out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": args.gpus,
@@ -700,7 +742,7 @@ def bench_reference(args):
            "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (SplitMix64 fields, SURVEY §8(d))", "impl": "reference",
-           "config": {"workload": f"{'full timestep' if physics else 'dycore step'} "
+           "config": {"workload": f"{'full timestep' if physics else 'ASUCA step' if asuca else 'dycore step'} "
                                   f"{NX}x{NY}x{NZ} (north_star), sampled as {cores} blocks of "
                                   f"{sx}x{sy}x{NZ}", "entry": args.entry,
                       "sample": f"{cores} x {sx}x{sy}x{NZ} blocks"},
@@ -721,8 +763,10 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--entry", default="full_step", choices=["full_step", "dycore_step"],
-                    help="the timestep: full (dycore + column physics, default) or dycore only")
+    ap.add_argument("--entry", default="full_step",
+                    choices=["full_step", "dycore_step", "asuca_step"],
+                    help="the timestep: full (dycore + column physics, default), dycore only, "
+                         "or the ASUCA time scheme (use --steps 10: ~0.07 s per step at C4)")
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling of the 1581x1301x58 grid (default: weak, a "
                          "1581x1301x58 tile per GPU)")
