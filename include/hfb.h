@@ -116,8 +116,11 @@ typedef struct {
 } hfb_launch_stats;
 
 /* Entries are the app's routine names with or without the generated `hfd_` prefix
- * (e.g. "main", "hfd_main", "simulation_run", "diffuse_step", "dycore_step").
- * Runs to completion on the context's stream and synchronises before returning. */
+ * (e.g. "main", "hfd_main", "simulation_run", "diffuse_step", "dycore_step"). The dycore
+ * program's per-step entries: "dycore_step", "full_step" (+ column physics), "rk3_step"
+ * and "asuca_step" (the ASUCA time scheme, apps/dycore/asuca.h90); the fused kernels take
+ * columns of up to 129 levels. Runs to completion on the context's stream and
+ * synchronises before returning. */
 hfb_status hfb_run(hfb_ctx* ctx, const char* entry, hfb_launch_stats* stats);
 /* Same, asynchronously on the context's stream (no host synchronisation); only for
  * entries without transfers. */
