@@ -29,3 +29,20 @@ def test_reference_arm_json_line():
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
     assert "workload" in d["config"]
+
+
+@pytest.mark.skipif(not (ROOT / "oracle" / "_ref" / "hft_ref").exists(),
+                    reason="oracle/_ref/hft_ref not built")
+def test_reference_arm_asuca_entry():
+    """--entry asuca_step: the reference interpreter runs main_asuca (apps/dycore/asuca.h90)
+    on its sample blocks; same contract keys."""
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
+                        "--entry", "asuca_step", "--steps", "1", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["config"]["entry"] == "asuca_step"
+    assert d["value"] > 0 and "ASUCA" in d["config"]["workload"]
+    assert d["cpu_baseline"]["kind"] == "reference"
