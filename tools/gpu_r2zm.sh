@@ -1,0 +1,1 @@
+timeout 1500 python -m pytest tests/test_gpu_sanitizer.py -q -p no:cacheprovider 2>&1 | tail -3
