@@ -1,6 +1,7 @@
 // hfb_dycore_tma.cu — the whole dycore timestep (dycore.h90 regions 1-8) in one kernel,
-// fed by TMA: the TMA twin of k_dyn_step_ws (hfb_dycore_tmem.cu, fed by cp.async), kept
-// as a measured alternative (HFB_TMA_STEP=1; see MEASURED below).
+// fed by TMA: round 1's TMA twin of k_dyn_step_ws (then fed by cp.async; since round 2 the
+// product kernel is TMA-fed itself, with role-split loops and a different waiter), kept
+// as a measured alternative (hfb_set_option "variant" "tma" in the A/B build; see MEASURED below).
 //
 // Machine organisation (one CTA per 32 x 4 tile of (i,j) columns, marching K):
 //   * per K level, six threads issue six 3-D TMA box loads (th with its 2-cell ring, u
@@ -19,7 +20,7 @@
 //   * MEASURED (512x512x58, B200): this kernel is SLOWER than its cp.async twin (0.414 vs
 //     0.379 ms per step) although its data-movement skeleton is faster (0.219 vs 0.235
 //     ms with both roles' arithmetic skipped), so the cp.async kernel stays the product
-//     path and this one is the HFB_TMA_STEP=1 variant. Also measured and dropped: a
+//     path and this one is the "tma" variant. Also measured and dropped: a
 //     dedicated producer warp with empty/full barrier pairs (0.430 ms: a ninth warp
 //     cuts the register budget to 96) and refills by the last warp out of a slot through
 //     an acq_rel arrival counter, no CTA barrier (0.441 ms).

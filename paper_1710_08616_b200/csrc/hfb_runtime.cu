@@ -321,7 +321,7 @@ struct hfb_ctx {
   std::vector<void*> ipc_opened;
   // halo exchange overlapped with the interior columns (decomposed stencil steps): the
   // exchange runs on `comm` while the columns that never read the halo ring run on
-  // `stream`; the boundary strips follow the exchange (HFB_NO_OVERLAP=1 serialises)
+  // `stream`; the boundary strips follow the exchange (hfb_set_option "overlap" "0" serialises)
   cudaStream_t comm = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
   // the stream step kernels go to (nullptr: `stream`); exchange_and_run points it at
