@@ -64,8 +64,10 @@ __device__ __forceinline__ double asu_flux(double vel, double qm1, double q0, do
 // ============================================================================
 // slow tendencies
 // ============================================================================
-constexpr int kTW = kTX + 4, kTR = kTY + 4;   // 36 x 8 plane tile (2-cell ring)
-constexpr int kTPlane = kTW * kTR;            // 288
+// 38 x 8 plane tile: the 2-cell ring around the 32 lanes plus one column, because a TMA
+// box must start 16-B aligned (an even x) and the 31-column tiles (below) alternate parity
+constexpr int kTW = kTX + 6, kTR = kTY + 4;
+constexpr int kTPlane = kTW * kTR;            // 304
 constexpr int kTStage = 5 * kTPlane;          // rho, th, u, v, w
 constexpr int kTStages = 6;                   // levels k-1..k+2 in use, k+3 in flight
 enum { kFRho = 0, kFTh = 1, kFU = 2, kFV = 3, kFW = 4 };
@@ -80,7 +82,7 @@ struct TendArgs {
   Span sp;
 };
 
-// The ring is fed by TMA: five 36 x 8 box loads per level (rho, th, u, v, w with their
+// The ring is fed by TMA: five 38 x 8 box loads per level (rho, th, u, v, w with their
 // 2-cell ring), issued by lane 0 of warps 0-3 (warp 0 also the fifth), completion on the
 // slot's mbarrier; warp kTendWaitWarp observes level k+3 at the end of its level k and
 // the per-level CTA barrier publishes it.
@@ -88,6 +90,13 @@ struct TendMaps {
   CUtensorMap m[5];
 };
 constexpr int kTendWaitWarp = 3;
+// x faces are shared between neighbouring lanes: every lane evaluates the EAST face (or
+// x-centre / x-edge) of its point and takes the west one from lane - 1 by a shuffle, so
+// each horizontal x flux is evaluated once instead of twice. Lane 0 is therefore a ghost
+// column (the point west of the tile: it supplies lane 1's west faces and stores nothing)
+// and a tile owns 31 columns.
+constexpr int kTXo = kTX - 1;
+__device__ __forceinline__ double from_west(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
 
 __global__ void __launch_bounds__(kThreads, 3)
     k_asu_tend(const __grid_constant__ TendMaps maps, TendArgs a) {
@@ -98,10 +107,10 @@ __global__ void __launch_bounds__(kThreads, 3)
   const uint32_t raw_u32 = sm100::smem_u32(smem_raw);
   double* const smem = smem_raw + ((((raw_u32 + 127u) & ~127u) - raw_u32) >> 3);
   const int lane = threadIdx.x, row = threadIdx.y, t = row * kTX + lane;
-  const int64_t i0 = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * kTX;
+  const int64_t i0 = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * kTXo;  // lane 1's column
   const int64_t j0 = a.sp.jlo + static_cast<int64_t>(blockIdx.y) * kTY;
-  const int64_t i = i0 + lane, j = j0 + row;
-  const bool active = i <= a.sp.ihi && j <= a.sp.jhi;
+  const int64_t i = i0 - 1 + lane, j = j0 + row;
+  const bool active = lane > 0 && i <= a.sp.ihi && j <= a.sp.jhi;
   const int nz = a.nz;
   const int64_t P = a.g.plane, W = a.g.pitch;
   const int64_t gi = i + a.sp.i0, gj = j + a.sp.j0, gnx = a.sp.gnx, gny = a.sp.gny;
@@ -121,7 +130,9 @@ __global__ void __launch_bounds__(kThreads, 3)
   constexpr uint32_t kStageBytes = kTStage * 8;
   const uint32_t ring_u32 = sm100::smem_u32(smem);
   // box origin in allocation coordinates (x = kIOff + i', y = kHalo + j'), 2-cell ring
-  const int xo = static_cast<int>(kIOff + (i0 - 1)) - 2, yo = static_cast<int>(kHalo + (j0 - 1)) - 2;
+  // box origin: 2 columns left of lane 0 (local i0 - 2, 0-based), rounded down to even
+  const int xo_l = static_cast<int>(kIOff + (i0 - 2)) - 2, xpar = xo_l & 1;
+  const int xo = xo_l - xpar, yo = static_cast<int>(kHalo + (j0 - 1)) - 2;
   auto issue = [&](int k) {  // level k into slot k % kTStages (lane 0 of every warp)
     if (lane != 0 || k >= nz) return;
     const uint32_t slot = static_cast<uint32_t>(k % kTStages);
@@ -136,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                      static_cast<uint32_t>((l / kTStages) & 1));
   };
   // value of field f at level k (0-based; any k, ring slot), offset (di, dj)
-  const int cen = (row + 2) * kTW + (lane + 2);
+  const int cen = (row + 2) * kTW + (lane + 2 + xpar);
   auto V = [&](int f, int k, int di, int dj) -> double {
     const int slot = ((k % kTStages) + kTStages) % kTStages;
     return smem[slot * kTStage + f * kTPlane + cen + dj * kTW + di];
@@ -197,12 +208,12 @@ __global__ void __launch_bounds__(kThreads, 3)
       double div = rdx * (ue - uw) + rdy * (vnf - vs);
       div = div + rdz * (wt - wb);
       const double fzt = zface(kFTh), fzr = zface(kFRho);
-      double flux = rdx * (xface(kFTh, gi, 0, ui) - xface(kFTh, gi - 1, -1, uim1)) +
-                    rdy * (yface(kFTh, gj, 0, vj) - yface(kFTh, gj - 1, -1, vjm1));
+      const double fxt = xface(kFTh, gi, 0, ui), fxr = xface(kFRho, gi, 0, ui);
+      const double fxt_w = from_west(fxt), fxr_w = from_west(fxr);  // faces gi - 1
+      double flux = rdx * (fxt - fxt_w) + rdy * (yface(kFTh, gj, 0, vj) - yface(kFTh, gj - 1, -1, vjm1));
       flux = flux + rdz * (fzt - fzt_b);
       fth = V(kFTh, k, 0, 0) * div - flux;
-      flux = rdx * (xface(kFRho, gi, 0, ui) - xface(kFRho, gi - 1, -1, uim1)) +
-             rdy * (yface(kFRho, gj, 0, vj) - yface(kFRho, gj - 1, -1, vjm1));
+      flux = rdx * (fxr - fxr_w) + rdy * (yface(kFRho, gj, 0, vj) - yface(kFRho, gj - 1, -1, vjm1));
       flux = flux + rdz * (fzr - fzr_b);
       frho = 0.0 - flux;
       fzt_b = fzt;
@@ -234,7 +245,9 @@ __global__ void __launch_bounds__(kThreads, 3)
                         V(kFU, k, 0, off + 2), kLat && f == 1, kLat && f + 1 == gny);
       };
       double cxe, cxw, cyn, cys, czt;
-      const double gxe = xcen(1, cxe), gxw = xcen(0, cxw);
+      const double gxe = xcen(1, cxe);
+      const double gxw = from_west(gxe);  // centre gi
+      cxw = from_west(cxe);
       const double gyn = yedge(0, cyn), gys = yedge(-1, cys);
       double gzt;
       if ((kV && kk == nz) || east) {
@@ -279,7 +292,9 @@ __global__ void __launch_bounds__(kThreads, 3)
                         V(kFV, k, off + 2, 0), kLat && f == 1, kLat && f + 1 == gnx);
       };
       double cye, cyw, cxe, cxw, czt;
-      const double gxe = xedge(0, cxe), gxw = xedge(-1, cxw);
+      const double gxe = xedge(0, cxe);
+      const double gxw = from_west(gxe);  // edge gi - 1
+      cxw = from_west(cxe);
       const double gyn = ycen(1, cye), gys = ycen(0, cyw);
       double gzt;
       if ((kV && kk == nz) || north) {
@@ -339,7 +354,9 @@ __global__ void __launch_bounds__(kThreads, 3)
                           V(kFW, k, 0, off + 2), kLat && f == 1, kLat && f + 1 == gny);
         };
         double cxe, cxw, cyn, cys;
-        const double gxe = xedge(0, cxe), gxw = xedge(-1, cxw);
+        const double gxe = xedge(0, cxe);
+        const double gxw = from_west(gxe);  // edge gi - 1
+        cxw = from_west(cxe);
         const double gyn = yedge(0, cyn), gys = yedge(-1, cys);
         double div = rdx * (cxe - cxw) + rdy * (cyn - cys);
         div = div + rdz * (czt - czw_b);
@@ -370,8 +387,8 @@ __global__ void __launch_bounds__(kThreads, 3)
 #pragma unroll 1
   for (; k < nz; ++k) level(k, std::true_type{});
   };
-  const int64_t gi0 = i0 + a.sp.i0, gj0 = j0 + a.sp.j0;
-  const bool interior = gi0 >= 3 && gi0 + kTX - 1 <= gnx - 3 && i0 + kTX - 1 <= a.sp.ihi &&
+  const int64_t gi0 = i0 - 1 + a.sp.i0, gj0 = j0 + a.sp.j0;  // lane 0 (the ghost) included
+  const bool interior = gi0 >= 3 && gi0 + kTX - 1 <= gnx - 3 && i0 - 1 + kTX - 1 <= a.sp.ihi &&
                         gj0 >= 3 && gj0 + kTY - 1 <= gny - 3 && j0 + kTY - 1 <= a.sp.jhi;
   if (interior)
     sweep(std::false_type{});
@@ -749,7 +766,7 @@ cudaError_t launch_asu_tend(const AsuState& s, const AsuTend& f, Grid3 g, int64_
     if (!make_box_map(&maps.m[q], fld[q], g, nj, nz, kTW, kTR)) return cudaErrorInvalidValue;
   TendArgs a{s, f, g, static_cast<int>(nz), nj, -kIOff, g.pitch - kIOff - 1, rdx, rdy, rdz, sp};
   dim3 block(kTX, kTY);
-  dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTX - 1) / kTX),
+  dim3 grid(static_cast<unsigned>((sp.ihi - sp.ilo + 1 + kTXo - 1) / kTXo),
             static_cast<unsigned>((sp.jhi - sp.jlo + 1 + kTY - 1) / kTY));
   k_asu_tend<<<grid, block, smem, st>>>(maps, a);
   return cudaGetLastError();
