@@ -492,7 +492,6 @@ __global__ void __launch_bounds__(kAcoThreads, 2)
   const int lane = threadIdx.x, warp = threadIdx.y;  // blockDim = (32, 8)
   const bool thomas = warp < kTY;
   const int row = thomas ? warp : warp - kTY;
-  const int tid = warp * kTX + lane;  // 0..255 (copy issue)
   const int t = row * kTX + lane;     // 0..127 (column within the tile)
   const int64_t i0 = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * kTX;
   const int64_t j0 = a.sp.jlo + static_cast<int64_t>(blockIdx.y) * kTY;
