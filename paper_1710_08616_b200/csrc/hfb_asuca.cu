@@ -11,7 +11,8 @@
 // short-step copy-back) are pointer swaps in the runtime (hfb_runtime.cu asuca_step).
 //
 // Machine organisation follows k_dyn_step_ws (hfb_dycore_tmem.cu): a CTA owns a 32 x 4
-// tile of (i,j) columns (warp = row, lane = column) and marches K; every K-plane of the
+// tile of (i,j) columns (warp = row, lane = column; the tendency pass: 31 x 4 plus a ghost
+// lane that supplies the shared x faces) and marches K; every K-plane of the
 // fields the tile reads (with the halo columns/rows its stencils need) is staged into a
 // shared-memory ring by TMA (one 3-D box load per field and level, completion on the
 // slot's mbarrier) several levels ahead;
