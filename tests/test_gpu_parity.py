@@ -111,6 +111,11 @@ LARGE = [
     _asu("asuca_40x36x2_s2", 40, 36, 2, 2, kdmp=1),
     _asu("asuca_33x9x65_s1", 33, 9, 65, 1, nsound=6, nbnd=4),
     _asu("asuca_33x21x100_s1", 33, 21, 100, 1, nsound=6, nbnd=4),
+    # the tendency pass tiles x by 31 columns (+ a ghost lane): exact multiples, one past,
+    # and interior tiles of both box parities
+    _asu("asuca_93x11x12_s1", 93, 11, 12, 1, nbnd=3),
+    _asu("asuca_94x13x12_s1", 94, 13, 12, 1, nbnd=3),
+    _asu("asuca_190x14x9_s1", 190, 14, 9, 1, nbnd=2),
 ]
 
 
