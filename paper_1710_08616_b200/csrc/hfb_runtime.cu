@@ -784,10 +784,10 @@ void peer_signal(hfb_ctx* c, cudaStream_t st);
 // the tile — they never read the halo ring — are launched at once on the compute stream;
 // the four boundary strips follow once the halos landed. Every column is computed from
 // the same inputs either way, so the split is bit-identical to one full-span launch.
-// `run(span)` launches the step kernel over a span of the tile.
-template <class F>
-void exchange_and_run(hfb_ctx* c, const std::vector<const char*>& fields, int r, int64_t nx,
-                      int64_t ny, bool odd_ilo, F&& run) {
+// `run(span)` launches the step kernel over a span of the tile; `xchg(stream)` enqueues
+// the exchange (module arrays by name, or the ASUCA scheme's explicit buffers).
+template <class X, class F>
+void overlap_run(hfb_ctx* c, X&& xchg, int r, int64_t nx, int64_t ny, bool odd_ilo, F&& run) {
   const Span full = full_span(c, nx, ny);
   const bool multi = c->decomposed && c->decomp.px * c->decomp.py > 1;
   if (!multi) {
@@ -805,7 +805,7 @@ void exchange_and_run(hfb_ctx* c, const std::vector<const char*>& fields, int r,
   in.jhi = ny - r;
   if (!c->overlap || c->capturing || (odd_ilo && in.ilo % 2 == 0) || in.ihi < in.ilo ||
       in.jhi < in.jlo) {
-    halo_exchange(c, fields, r);
+    xchg(c->stream);
     run(full, true);
     return;
   }
@@ -816,7 +816,7 @@ void exchange_and_run(hfb_ctx* c, const std::vector<const char*>& fields, int r,
   }
   cuda_check(cudaEventRecord(c->ev_ready, c->stream), "cudaEventRecord");
   cuda_check(cudaStreamWaitEvent(c->comm, c->ev_ready, 0), "cudaStreamWaitEvent");
-  halo_exchange(c, fields, r, c->comm);
+  xchg(c->comm);
   run(in, false);
   // the boundary strips follow the halo wait on the communication stream, so they run
   // alongside the interior launch (disjoint output columns, read-only inputs) instead of
@@ -842,6 +842,12 @@ void exchange_and_run(hfb_ctx* c, const std::vector<const char*>& fields, int r,
   c->run_stream = nullptr;
   cuda_check(cudaEventRecord(c->ev_halo, c->comm), "cudaEventRecord");
   cuda_check(cudaStreamWaitEvent(c->stream, c->ev_halo, 0), "cudaStreamWaitEvent");
+}
+template <class F>
+void exchange_and_run(hfb_ctx* c, const std::vector<const char*>& fields, int r, int64_t nx,
+                      int64_t ny, bool odd_ilo, F&& run) {
+  overlap_run(c, [&](cudaStream_t s) { halo_exchange(c, fields, r, s); }, r, nx, ny, odd_ilo,
+              std::forward<F>(run));
 }
 
 // ---------------------------------------------------------------------------
@@ -1347,9 +1353,10 @@ void asuca_step(hfb_ctx* c, Stats& st) {
   const int64_t nx = ival(c, "nx"), ny = ival(c, "ny"), nz = ival(c, "nz");
   if (!asuca_fits(nz))
     fail(HFB_CONFIG, "asuca_step is implemented for 2 <= nz <= 129 (got %lld)", (long long)nz);
-  // decomposed: every pass's stencil inputs are exchanged first (peer or NCCL transport;
-  // push + signal + wait per exchange, 28 per step with nsound = 6), then the pass runs
-  // over the whole tile
+  // decomposed: every pass's stencil inputs are exchanged (peer or NCCL transport; push +
+  // signal + wait per exchange, 28 per step with nsound = 6) on the communication stream
+  // while the pass runs over the columns >= 2 cells inside the tile; the boundary strips
+  // follow the halo wait (overlap_run; serial under graph capture or overlap=0)
   const bool multi = c->decomposed && c->decomp.px * c->decomp.py > 1;
   if (multi) {
     if (c->group)
@@ -1405,13 +1412,19 @@ void asuca_step(hfb_ctx* c, Stats& st) {
     const double dtf = stg == 1 ? dt / 3.0 : stg == 2 ? dt / 2.0 : dt;
     const int64_t nsm = stg == 1 ? nsound / 3 : stg == 2 ? nsound / 2 : nsound;
     const AsuState S{rhoS, thS, u.d_buf(us), v.d_buf(us), w.d_buf(us), p.d_buf(us)};
-    if (multi)  // the tendencies' stencils: the stage state with a 2-cell ring
-      halo_exchange_x(c, {xfield(c, "rho", rs), xfield(c, "th", ts), xfield(c, "u", us),
-                          xfield(c, "v", us), xfield(c, "w", us)},
-                      ks(c));
-    launch(c, st, "asuca_tend", [&] {
-      return launch_asu_tend(S, F, g, nz, nj, rdx, rdy, rdz, sp, ks(c));
-    });
+    // the tendencies' stencils: the stage state with a 2-cell ring
+    overlap_run(
+        c,
+        [&](cudaStream_t s) {
+          halo_exchange_x(c, {xfield(c, "rho", rs), xfield(c, "th", ts), xfield(c, "u", us),
+                              xfield(c, "v", us), xfield(c, "w", us)},
+                          s);
+        },
+        2, nx, ny, true, [&](const Span& q, bool) {
+          launch(c, st, "asuca_tend", [&] {
+            return launch_asu_tend(S, F, g, nz, nj, rdx, rdy, rdz, q, ks(c));
+          });
+        });
     // the reference's launches: 12 flux regions (4 of them over an extra face row or
     // column), the theta/rho and the momentum tendencies, the acoustic restart copy
     count_launch(st, nx + 1, ny);
@@ -1429,24 +1442,37 @@ void asuca_step(hfb_ctx* c, Stats& st) {
     count_launch(st, nx, ny);
     count_launch(st, nx, ny);
     count_launch(st, nx, ny);
-    if (multi)  // the acoustic passes read fu(i-1), fv(j-1)
-      halo_exchange_x(c, {xscratch("asu:fu", F.fu), xscratch("asu:fv", F.fv)}, ks(c));
+    // the acoustic passes read fu(i-1), fv(j-1): exchanged with the first pass A
+    bool fuv_pending = multi;
     int cur = b, nxt = x;
     for (int64_t ss = 0; ss < nsm; ++ss) {
       const AsuState C{rhoS, thS, u.d_buf(cur), v.d_buf(cur), w.d_buf(cur), p.d_buf(cur)};
-      if (multi)  // pass A: p with its ring, u(i-1), v(j-1) of the short-step state
-        halo_exchange_x(c, {xfield(c, "p", cur), xfield(c, "u", cur), xfield(c, "v", cur)},
-                        ks(c));
-      launch(c, st, "asuca_acoustic_a", [&] {
-        return launch_asu_acoustic(false, C, F.fu, F.fv, F.fw, nullptr, pa, nullptr, nullptr,
-                                   nullptr, nullptr, g, nz, nj, ca, sp, ks(c));
-      });
-      if (multi) halo_exchange_x(c, {xscratch("asu:pa", pa)}, ks(c));  // pass B: pa's ring
-      launch(c, st, "asuca_acoustic_b", [&] {
-        return launch_asu_acoustic(true, C, F.fu, F.fv, F.fw, pa, nullptr, u.d_buf(nxt),
-                                   v.d_buf(nxt), w.d_buf(nxt), p.d_buf(nxt), g, nz, nj, cb, sp,
-                                   ks(c));
-      });
+      // pass A: p with its ring, u(i-1), v(j-1) of the short-step state
+      overlap_run(
+          c,
+          [&](cudaStream_t s) {
+            if (fuv_pending)
+              halo_exchange_x(c, {xscratch("asu:fu", F.fu), xscratch("asu:fv", F.fv)}, s);
+            halo_exchange_x(c, {xfield(c, "p", cur), xfield(c, "u", cur), xfield(c, "v", cur)},
+                            s);
+          },
+          2, nx, ny, true, [&](const Span& q, bool) {
+            launch(c, st, "asuca_acoustic_a", [&] {
+              return launch_asu_acoustic(false, C, F.fu, F.fv, F.fw, nullptr, pa, nullptr,
+                                         nullptr, nullptr, nullptr, g, nz, nj, ca, q, ks(c));
+            });
+          });
+      fuv_pending = false;
+      // pass B: pa's ring
+      overlap_run(
+          c, [&](cudaStream_t s) { halo_exchange_x(c, {xscratch("asu:pa", pa)}, s); }, 2, nx,
+          ny, true, [&](const Span& q, bool) {
+            launch(c, st, "asuca_acoustic_b", [&] {
+              return launch_asu_acoustic(true, C, F.fu, F.fv, F.fw, pa, nullptr, u.d_buf(nxt),
+                                         v.d_buf(nxt), w.d_buf(nxt), p.d_buf(nxt), g, nz, nj, cb,
+                                         q, ks(c));
+            });
+          });
       for (int r = 0; r < 7; ++r) count_launch(st, nx, ny);
       cur = nxt;
       nxt = nxt == x ? y : x;

@@ -371,14 +371,16 @@ def test_peer_c4_strong_scaling_tiles_4x2(tmp_path):
             assert bits_equal(t, want), f"rank {rank}: {n} differs"
 
 
-@pytest.mark.parametrize("px,py", [(2, 1), (2, 2), (3, 2)])
-def test_peer_asuca_scheme_equals_single_domain(px, py):
+@pytest.mark.parametrize("px,py,overlap", [(2, 1, 1), (2, 2, 1), (3, 2, 1), (2, 2, 0)])
+def test_peer_asuca_scheme_equals_single_domain(px, py, overlap):
     """The complete ASUCA step on a decomposed context (peer transport, one process per
-    rank): each pass's stencil inputs are pushed into the neighbours' halo rings first —
-    the stage state before the tendencies, fu/fv after them, p/u/v before every first
-    acoustic pass, pa before every second — and the assembled tiles equal the
-    undecomposed oracle bit for bit (the lateral damping band crosses tile edges)."""
-    case, garr, out, parts = run_peer("asuca", px, py)
+    rank): each pass's stencil inputs are pushed into the neighbours' halo rings — the
+    stage state for the tendencies, fu/fv and p/u/v for every first acoustic pass, pa for
+    every second — on the communication stream while the pass runs over the columns 2
+    cells inside the tile, then the boundary strips (overlap=0: exchange first, one
+    full-span launch); the assembled tiles equal the undecomposed oracle bit for bit (the
+    lateral damping band crosses tile edges)."""
+    case, garr, out, parts = run_peer("asuca", px, py, options={"overlap": overlap})
     ref = {k: v.copy() for k, v in garr.items()}
     run_oracle(case, ref)
     for k in APPS[case.app].outputs:
@@ -386,6 +388,10 @@ def test_peer_asuca_scheme_equals_single_domain(px, py):
     # nsound = 6: per step 3 stage-state exchanges, 3 fu/fv, 11 p/u/v, 11 pa
     n = case.ints["nsteps"]
     assert all(p[1] == (28 * n, 0) for p in parts), [p[1] for p in parts]
+    # per step 3 tendency passes, 22 acoustic passes (interior + 4 strips each when
+    # overlapped) and 3 stage ends
+    per_pass = 5 if overlap else 1
+    assert all(p[5] == n * (25 * per_pass + 3) for p in parts), [p[5] for p in parts]
 
 
 def test_peer_asuca_graph_replay():
