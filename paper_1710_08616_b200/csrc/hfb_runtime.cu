@@ -794,15 +794,24 @@ void overlap_run(hfb_ctx* c, X&& xchg, int r, int64_t nx, int64_t ny, bool odd_i
     run(full, false);
     return;
   }
-  // odd_ilo: spans must start at odd i (the fused dycore kernel's 16-B copy chunks begin
-  // 2 columns left of a tile: i - 3 must be even), so the east strip may be one column
+  // The strips are whole tiles where the tile is large enough (32 columns, 4 rows: the
+  // step kernels' CTA tile, so a strip launch does not run mostly idle lanes through the
+  // whole K march; the interior is then whole tiles too), else r cells wide.
+  // odd_ilo: spans must start at odd i (the step kernels' TMA boxes begin 2 columns left
+  // of a tile and must start 16-B aligned), so an r-wide east strip may be one column
   // wider and an even interior start falls back to the serial order
-  const int64_t east_lo = (!odd_ilo || (nx - r + 1) % 2 == 1) ? nx - r + 1 : nx - r;
+  constexpr int64_t kTileI = 32, kTileJ = 4;
   Span in = full;
-  in.ilo = r + 1;
-  in.ihi = east_lo - 1;
-  in.jlo = r + 1;
-  in.jhi = ny - r;
+  auto split = [&](int64_t n, int64_t t, int64_t& lo, int64_t& hi) {
+    lo = std::max<int64_t>(r, t) + 1;
+    hi = lo - 1 + (n - r - (lo - 1)) / t * t;  // whole tiles, >= r short of the far edge
+    if (hi >= lo && n - r - (lo - 1) > 0) return true;
+    lo = r + 1;
+    hi = n - r;
+    return false;
+  };
+  if (!split(nx, kTileI, in.ilo, in.ihi) && odd_ilo && (nx - r + 1) % 2 == 0) --in.ihi;
+  split(ny, kTileJ, in.jlo, in.jhi);
   if (!c->overlap || c->capturing || (odd_ilo && in.ilo % 2 == 0) || in.ihi < in.ilo ||
       in.jhi < in.jlo) {
     xchg(c->stream);
@@ -822,12 +831,12 @@ void overlap_run(hfb_ctx* c, X&& xchg, int r, int64_t nx, int64_t ny, bool odd_i
   // alongside the interior launch (disjoint output columns, read-only inputs) instead of
   // after it; the compute stream joins them before the step ends
   Span south = full, north = full, west = full, east = full;
-  south.jhi = r;
-  north.jlo = ny - r + 1;
-  west.jlo = east.jlo = r + 1;
-  west.jhi = east.jhi = ny - r;
-  west.ihi = r;
-  east.ilo = east_lo;
+  south.jhi = in.jlo - 1;
+  north.jlo = in.jhi + 1;
+  west.jlo = east.jlo = in.jlo;
+  west.jhi = east.jhi = in.jhi;
+  west.ihi = in.ilo - 1;
+  east.ilo = in.ihi + 1;
   c->run_stream = c->comm;
   try {
     for (const Span& sp : {south, north, west, east}) run(sp, true);

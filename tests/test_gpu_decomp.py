@@ -201,6 +201,26 @@ def test_overlapped_exchange_equals_serial(app, overlap):
     assert stats.native_launches == 4 * steps * (5 if overlap else 1)
 
 
+@pytest.mark.parametrize("app", ["dycore_full", "diffusion"])
+def test_overlapped_exchange_whole_tile_strips(app):
+    """Tiles wide and tall enough for whole-tile boundary strips (32 columns, 4 rows): the
+    interior is whole tiles too, and the split is still bit-identical to the oracle."""
+    if app == "diffusion":
+        case = Case("d", "diffusion", dict(nx=150, ny=30, nz=12, nsteps=3), dict(coef=0.1),
+                    {"t_old": (1, 280.0, 10.0)}, unset=["t_new"])
+        names = ("t_old", "t_new")
+    else:
+        case = Case("x", app, dict(nx=150, ny=30, nz=20, nsteps=2),
+                    dict(DYCORE_SCALARS, **PHYS_SCALARS), dict(DYCORE_FILLS, **PHYS_FILLS))
+        names = APPS[app].outputs
+    garr, out, _, stats, _ = run_decomposed(case, 2, 2, options={"overlap": 1})
+    ref = {k: v.copy() for k, v in garr.items()}
+    run_oracle(case, ref)
+    for k in names:
+        assert bits_equal(out[k], ref[k]), k
+    assert stats.native_launches == 4 * case.ints["nsteps"] * 5
+
+
 def test_group_refuses_the_asuca_scheme():
     """The ASUCA scheme's exchanges include scratch arrays that in-process groups cannot
     pull by name: a decomposed asuca_step in a group fails with HFB_CONFIG (the peer and

@@ -36,6 +36,11 @@ PEER_CASES = {
     # the ASUCA scheme: 28 exchanges per step (stage state, fu/fv, p/u/v, pa), nbnd = 3
     # damping band across the tile edges; 2 short steps in stage 1 (nsound = 6)
     "asuca": _asu("p_asuca", 70, 45, 20, 2, nbnd=3),
+    # tiles wide enough for whole-tile boundary strips (32 columns, 4 rows) in both
+    # directions when the exchange is overlapped
+    "asuca_wide": _asu("p_asuca_w", 150, 30, 12, 1, nbnd=3),
+    "dycore_wide": Case("p_dyn_w", "dycore", dict(nx=150, ny=30, nz=20, nsteps=3),
+                        dict(DYCORE_SCALARS), dict(DYCORE_FILLS)),
     "diffusion": Case("p_diff", "diffusion", dict(nx=40, ny=36, nz=12, nsteps=3),
                       dict(coef=0.1), {"t_old": (1, 280.0, 10.0)}, unset=["t_new"]),
     "bounded": Case("p_bnd", "bounded", dict(nx=37, ny=21), {},
@@ -47,7 +52,7 @@ PEER_CASES = {
     "reduction": Case("p_red", "reduction", dict(nx=67, ny=45, nz=20), dict(total=0.0),
                       {"y": (6, 0.0, 1.0)}),
 }
-HALO = {"asuca": 2, "dycore": 2, "dycore4": 2, "dycore_full4": 2, "dycore_full": 2, "dycore_rk3": 2, "diffusion": 1, "reduction": 0,
+HALO = {"asuca": 2, "asuca_wide": 2, "dycore_wide": 2, "dycore": 2, "dycore4": 2, "dycore_full4": 2, "dycore_full": 2, "dycore_rk3": 2, "diffusion": 1, "reduction": 0,
         "bounded": 1, "damping": 0}
 
 
@@ -174,13 +179,14 @@ def test_peer_reduction_is_rank_ordered_and_identical_everywhere():
     assert abs(totals[0] - ref) <= 1e-12 * abs(ref)
 
 
-@pytest.mark.parametrize("overlap", [True, False])
-def test_peer_fused_halo_hand_off_per_step_entries(overlap):
+@pytest.mark.parametrize("name,overlap", [("dycore", True), ("dycore", False),
+                                           ("dycore_wide", True)])
+def test_peer_fused_halo_hand_off_per_step_entries(name, overlap):
     """Consecutive dycore_step entries hand the halos over in the step kernel's epilogue
     (boundary strips store into the neighbours' next-step halo rings; the next exchange
     only waits for their flags). Without overlap the single full-span launch carries the
     remote epilogue. Both equal the undecomposed oracle bit for bit."""
-    case, garr, out, parts = run_peer("dycore", 2, 2, per_step=True,
+    case, garr, out, parts = run_peer(name, 2, 2, per_step=True,
                                       options={"overlap": int(overlap)})
     ref = {k: v.copy() for k, v in garr.items()}
     run_oracle(case, ref)
@@ -371,8 +377,10 @@ def test_peer_c4_strong_scaling_tiles_4x2(tmp_path):
             assert bits_equal(t, want), f"rank {rank}: {n} differs"
 
 
-@pytest.mark.parametrize("px,py,overlap", [(2, 1, 1), (2, 2, 1), (3, 2, 1), (2, 2, 0)])
-def test_peer_asuca_scheme_equals_single_domain(px, py, overlap):
+@pytest.mark.parametrize("name,px,py,overlap", [("asuca", 2, 1, 1), ("asuca", 2, 2, 1),
+                                                ("asuca", 3, 2, 1), ("asuca", 2, 2, 0),
+                                                ("asuca_wide", 2, 2, 1)])
+def test_peer_asuca_scheme_equals_single_domain(name, px, py, overlap):
     """The complete ASUCA step on a decomposed context (peer transport, one process per
     rank): each pass's stencil inputs are pushed into the neighbours' halo rings — the
     stage state for the tendencies, fu/fv and p/u/v for every first acoustic pass, pa for
@@ -380,7 +388,7 @@ def test_peer_asuca_scheme_equals_single_domain(px, py, overlap):
     cells inside the tile, then the boundary strips (overlap=0: exchange first, one
     full-span launch); the assembled tiles equal the undecomposed oracle bit for bit (the
     lateral damping band crosses tile edges)."""
-    case, garr, out, parts = run_peer("asuca", px, py, options={"overlap": overlap})
+    case, garr, out, parts = run_peer(name, px, py, options={"overlap": overlap})
     ref = {k: v.copy() for k, v in garr.items()}
     run_oracle(case, ref)
     for k in APPS[case.app].outputs:
