@@ -430,7 +430,7 @@ struct AcoArgs {
 // warps instead of 8; the roles carry about the same instruction count per level.
 constexpr int kAcoThreads = 2 * kThreads;
 // The plane ring is fed by TMA: one 3-D box load per field and level (10 in pass B, 9 in
-// pass A), issued by lane 0 of warps 0-7 (warps 0-1 take a second box), completion on
+// pass A), issued by lane 0 of the horizontal warps 4-7 in pass A, of every warp in pass B, completion on
 // the slot's mbarrier; one horizontal warp (the lighter role) observes level k+1's
 // barrier at the end of its level k, and the per-level CTA barrier publishes it. Plane
 // tiles start 128-B aligned inside a slot.
@@ -519,22 +519,36 @@ __global__ void __launch_bounds__(kAcoThreads, 2)
   sm100::tmem_fence_after();
   const uint32_t tmem = tmem_base_slot + (static_cast<uint32_t>(32 * row) << 16);
 
-  // this warp's boxes (lane 0 issues): field `warp`, and `warp + 8` for warps 0-1 in
-  // pass B / warp 0 in pass A; allocation coordinates x = kIOff + i', y = kHalo + j'
+  // Who issues the boxes (lane 0 of each issuing warp). Pass A: the horizontal warps only
+  // (the lighter role there: the Thomas warps' K loop carries no issue code; warp 4 + h
+  // issues fields h, h + 4 and h + 8 < kNB): 2.39 -> 2.23 ms at C4. Pass B, whose
+  // horizontal warps also store the damped u', v', is ~0.5-1% faster with every warp
+  // issuing (field `warp`, warps 0-1 also `warp + 8`) than with either role alone
+  // (tools/gpu_r2zt.sh, gpu_r2zu.sh). Allocation coordinates x = kIOff + i', y = kHalo + j'.
+  // issuing role: 0 every warp, 1 the horizontal warps, 2 the Thomas warps
+  constexpr int kIssue = kB ? 0 : 1;
   const uint32_t ring_u32 = sm100::smem_u32(ring);
   const int xo = static_cast<int>(kIOff + (i0 - 1)), yo = static_cast<int>(kHalo + (j0 - 1));
-  const AcoBox b0 = kAcoBoxDev[warp];
-  const AcoBox b1 = kAcoBoxDev[warp + 8 < kNB ? warp + 8 : 0];
-  const bool two = warp + 8 < kNB;
+  const int f0 = kIssue == 0 ? warp : kIssue == 1 ? (thomas ? 0 : warp - kTY) : (thomas ? warp : 0);
+  const int fstep = kIssue == 0 ? 8 : 4;
+  const int nbox = (f0 + 2 * fstep < kNB) ? 3 : (f0 + fstep < kNB) ? 2 : 1;
+  const AcoBox b0 = kAcoBoxDev[f0];
+  const AcoBox b1 = kAcoBoxDev[nbox > 1 ? f0 + fstep : 0];
+  const AcoBox b2 = kAcoBoxDev[nbox > 2 ? f0 + 2 * fstep : 0];
+  const bool issuer = kIssue == 0 || (kIssue == 1) != thomas;
   constexpr uint32_t kStageBytes = kStage * 8;
   auto issue = [&](int k) {  // level k into slot k % kAStages
-    if (lane != 0 || k >= nz) return;
+    if (!issuer || lane != 0 || k >= nz) return;
     const uint32_t slot = static_cast<uint32_t>(k % kAStages);
     const uint32_t fb = full0 + 8 * slot;
     const uint32_t so = ring_u32 + slot * kStageBytes;
-    if (warp == 0) sm100::mbar_arrive_expect_tx(fb, kTx);
-    sm100::tma_load_3d(so + b0.off * 8, &maps.m[warp], fb, xo + b0.dx, yo + b0.dy, k);
-    if (two) sm100::tma_load_3d(so + b1.off * 8, &maps.m[warp + 8], fb, xo + b1.dx, yo + b1.dy, k);
+    if (f0 == 0) sm100::mbar_arrive_expect_tx(fb, kTx);
+    sm100::tma_load_3d(so + b0.off * 8, &maps.m[f0], fb, xo + b0.dx, yo + b0.dy, k);
+    if (nbox > 1)
+      sm100::tma_load_3d(so + b1.off * 8, &maps.m[f0 + fstep], fb, xo + b1.dx, yo + b1.dy, k);
+    if (nbox > 2)
+      sm100::tma_load_3d(so + b2.off * 8, &maps.m[f0 + 2 * fstep], fb, xo + b2.dx, yo + b2.dy,
+                         k);
   };
   // the waiter (a horizontal warp) observes level l's slot barrier
   auto wait_level = [&](int l) {
@@ -623,7 +637,7 @@ __global__ void __launch_bounds__(kAcoThreads, 2)
     for (int k = 0; k < nz; ++k) {
       __syncthreads();  // level k landed (observed by the waiter); the slot of level k-1
                         // is free; ps of level k-1 is visible
-      issue(k + kAStages - 1);
+      if constexpr (kIssue == 0 || (kIssue == 1) != kThomas) issue(k + kAStages - 1);
       const double* S = ring + (k % kAStages) * kStage;
       if constexpr (kThomas) {
         const double wk = S[oW + t], rhok = S[oRho + t], thk = S[oTh + t], fwk = S[oFW + t];
