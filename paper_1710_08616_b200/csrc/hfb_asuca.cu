@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kThreads, 3)
   __shared__ __align__(16) uint64_t sbar[8];  // slot barriers
   const uint32_t raw_u32 = sm100::smem_u32(smem_raw);
   double* const smem = smem_raw + ((((raw_u32 + 127u) & ~127u) - raw_u32) >> 3);
-  const int lane = threadIdx.x, row = threadIdx.y, t = row * kTX + lane;
+  const int lane = threadIdx.x, row = sm100::warp_uniform(threadIdx.y), t = row * kTX + lane;
   const int64_t i0 = a.sp.ilo + static_cast<int64_t>(blockIdx.x) * kTXo;  // lane 1's column
   const int64_t j0 = a.sp.jlo + static_cast<int64_t>(blockIdx.y) * kTY;
   const int64_t i = i0 - 1 + lane, j = j0 + row;
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(kAcoThreads, 2)
   const int nz = a.nz;
   double* ps_s = ring + kAStages * kStage;  // nz x 128
 
-  const int lane = threadIdx.x, warp = threadIdx.y;  // blockDim = (32, 8)
+  const int lane = threadIdx.x, warp = sm100::warp_uniform(threadIdx.y);  // blockDim = (32, 8)
   const bool thomas = warp < kTY;
   const int row = thomas ? warp : warp - kTY;
   const int t = row * kTX + lane;     // 0..127 (column within the tile)

@@ -660,7 +660,12 @@ __global__ void __launch_bounds__(kWsThreads, 2)
   // acoustic warps, which accumulate the column sums (the halves stay balanced)
   double* thv_s = ps_s + a.nz * kThreads;
 
-  const int lane = threadIdx.x, warp = threadIdx.y;  // blockDim = (32, 8)
+  // blockDim = (32, 8); the warp index shuffled from lane 0 is known warp-uniform: the
+  // role branches are uniform and the TMA issue operands live in uniform registers (no
+  // per-lane ELECT / R2UR.BROADCAST / BRA.U.ANY loop around UTMALDG; the allocation fell
+  // from 124 to 102 registers in the dycore-step instantiation): C4 dycore step 2.557 ->
+  // 2.478 ms, RK3 512^2 1.176 -> 1.123 ms (tools/gpu_r2zv.sh)
+  const int lane = threadIdx.x, warp = sm100::warp_uniform(threadIdx.y);
   const bool acoustic = warp < kTY;
   const int row = acoustic ? warp : warp - kTY;       // tile row served by this warp
   const int tid = warp * kTX + lane;                  // 0..255 (copy issue)

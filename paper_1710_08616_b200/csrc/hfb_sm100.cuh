@@ -12,6 +12,19 @@
 namespace hfb {
 namespace sm100 {
 
+// The warp index as a value the compiler knows to be warp-uniform (shuffled from lane 0):
+// branches on it are uniform, and values derived from it (TMA box coordinates, ring
+// offsets) live in uniform registers, so a TMA issue needs no per-lane waterfall loop
+// (ELECT / R2UR.BROADCAST / BRA.U.ANY) around UTMALDG.
+__device__ __forceinline__ int warp_uniform(int v) { return __shfl_sync(0xffffffffu, v, 0); }
+// one elected lane of a converged warp (elect.sync)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e = 0;
+  asm volatile(
+      "{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n selp.u32 %0, 1, 0, P;\n}\n"
+      : "=r"(e));
+  return e != 0;
+}
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
