@@ -743,7 +743,6 @@ __global__ void __launch_bounds__(kWsThreads, 2)
 
   // TMA feed: lane 0 of warp f (f < 6) loads field f's box (th, u, v, w, p, rho order);
   // box origins in allocation coordinates (x = kIOff + i', y = kHalo + j', z = k)
-  const bool tma_lane = kTmaFeed && lane == 0 && f0 >= 0;
   auto box_of = [&](int f, int& off, int& dx, int& dy) {
     off = f == 0 ? kWOffTh : f == 1 ? kWOffU : f == 2 ? kWOffV : f == 3 ? kWOffW
         : f == 4 ? kWOffP : kWOffRho;
@@ -805,22 +804,27 @@ __global__ void __launch_bounds__(kWsThreads, 2)
   constexpr uint32_t kStageBytes = kWStageDoubles * 8;
   auto issue = [&](bool copy) {
     if constexpr (kTmaFeed) {
-      if (copy && tma_lane) {
-        const uint32_t fb = full0 + tma_bar;
+      if (copy && f0 >= 0) {  // (warp-uniform) the ring cursor shuffled from lane 0 is
+        // known uniform, so the issue needs no per-lane waterfall loop around UTMALDG
+        const uint32_t so_u = __shfl_sync(0xffffffffu, so, 0);
+        const uint32_t fb = full0 + __shfl_sync(0xffffffffu, tma_bar, 0);
+        const int k_u = __shfl_sync(0xffffffffu, tma_k, 0);
+        if (lane == 0) {
         if (warp == 0) sm100::mbar_arrive_expect_tx(fb, kWStageTx);
-        sm100::tma_load_3d(dst0 + so, &maps.m[f0], fb, x00 + dx0, y00 + dy0, tma_k);
+        sm100::tma_load_3d(dst0 + so_u, &maps.m[f0], fb, x00 + dx0, y00 + dy0, k_u);
         if (f1 >= 0)
-          sm100::tma_load_3d(dst1 + so, &maps.m[f1], fb, x00 + dx1, y00 + dy1, tma_k);
+          sm100::tma_load_3d(dst1 + so_u, &maps.m[f1], fb, x00 + dx1, y00 + dy1, k_u);
         // RK stages: the base state of the same level into L2 (TMA prefetch boxes), so
         // the per-thread base loads one level ahead hit L2 instead of DRAM (C2 RK3 step
         // 1.41 -> 1.17 ms); boxes th 32x4, u 34x4 (i-2..), v 32x5 (j-1..), w, p
         if constexpr (kRK) {
           if (f0 < 5)
             sm100::tma_prefetch_l2_3d(&maps.base[f0], x00 + (f0 == 1 ? -2 : 0),
-                                      y00 + (f0 == 2 ? -1 : 0), tma_k);
+                                      y00 + (f0 == 2 ? -1 : 0), k_u);
           if (f1 >= 0 && f1 < 5)
             sm100::tma_prefetch_l2_3d(&maps.base[f1], x00 + (f1 == 1 ? -2 : 0),
-                                      y00 + (f1 == 2 ? -1 : 0), tma_k);
+                                      y00 + (f1 == 2 ? -1 : 0), k_u);
+        }
         }
       }
       ++tma_k;
