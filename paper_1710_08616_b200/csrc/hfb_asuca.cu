@@ -430,7 +430,7 @@ struct AcoArgs {
 // warps instead of 8; the roles carry about the same instruction count per level.
 constexpr int kAcoThreads = 2 * kThreads;
 // The plane ring is fed by TMA: one 3-D box load per field and level (10 in pass B, 9 in
-// pass A), issued by lane 0 of the horizontal warps 4-7 in pass A, of every warp in pass B, completion on
+// pass A), issued by lane 0 of the horizontal warps 4-7 in pass A, of the Thomas warps 0-3 in pass B, completion on
 // the slot's mbarrier; one horizontal warp (the lighter role) observes level k+1's
 // barrier at the end of its level k, and the per-level CTA barrier publishes it. Plane
 // tiles start 128-B aligned inside a slot.
@@ -519,14 +519,14 @@ __global__ void __launch_bounds__(kAcoThreads, 2)
   sm100::tmem_fence_after();
   const uint32_t tmem = tmem_base_slot + (static_cast<uint32_t>(32 * row) << 16);
 
-  // Who issues the boxes (lane 0 of each issuing warp). Pass A: the horizontal warps only
-  // (the lighter role there: the Thomas warps' K loop carries no issue code; warp 4 + h
-  // issues fields h, h + 4 and h + 8 < kNB): 2.39 -> 2.23 ms at C4. Pass B, whose
-  // horizontal warps also store the damped u', v', is ~0.5-1% faster with every warp
-  // issuing (field `warp`, warps 0-1 also `warp + 8`) than with either role alone
-  // (tools/gpu_r2zt.sh, gpu_r2zu.sh). Allocation coordinates x = kIOff + i', y = kHalo + j'.
+  // Who issues the boxes (lane 0 of each issuing warp; warp w of the issuing role loads
+  // fields w, w + 4 and w + 8 < kNB). Pass A: the horizontal warps (the lighter role there:
+  // the Thomas warps' K loop carries no issue code): 2.39 -> 2.23 ms at C4. Pass B, whose
+  // horizontal warps also store the damped u', v': the Thomas warps (with the warp-uniform
+  // index: 2.60 vs 2.63 ms every warp, 2.65 the horizontal ones; tools/gpu_r2zt.sh,
+  // gpu_r2zu.sh, gpu_r2zz.sh). Allocation coordinates x = kIOff + i', y = kHalo + j'.
   // issuing role: 0 every warp, 1 the horizontal warps, 2 the Thomas warps
-  constexpr int kIssue = kB ? 0 : 1;
+  constexpr int kIssue = kB ? 2 : 1;
   const uint32_t ring_u32 = sm100::smem_u32(ring);
   const int xo = static_cast<int>(kIOff + (i0 - 1)), yo = static_cast<int>(kHalo + (j0 - 1));
   const int f0 = kIssue == 0 ? warp : kIssue == 1 ? (thomas ? 0 : warp - kTY) : (thomas ? warp : 0);
