@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kThreads, 3)
   const int xo_l = static_cast<int>(kIOff + (i0 - 2)) - 2, xpar = xo_l & 1;
   const int xo = xo_l - xpar, yo = static_cast<int>(kHalo + (j0 - 1)) - 2;
   auto issue = [&](int k) {  // level k into slot k % kTStages (lane 0 of every warp)
-    if (lane != 0 || k >= nz) return;
+    if (k >= nz || !sm100::elect_one()) return;  // (k warp-uniform: the warp is converged)
     const uint32_t slot = static_cast<uint32_t>(k % kTStages);
     const uint32_t fb = full0 + 8 * slot;
     const uint32_t so = ring_u32 + slot * kStageBytes;
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(kAcoThreads, 2)
   const bool issuer = kIssue == 0 || (kIssue == 1) != thomas;
   constexpr uint32_t kStageBytes = kStage * 8;
   auto issue = [&](int k) {  // level k into slot k % kAStages
-    if (!issuer || lane != 0 || k >= nz) return;
+    if (!issuer || k >= nz || !sm100::elect_one()) return;  // (issuer, k warp-uniform)
     const uint32_t slot = static_cast<uint32_t>(k % kAStages);
     const uint32_t fb = full0 + 8 * slot;
     const uint32_t so = ring_u32 + slot * kStageBytes;

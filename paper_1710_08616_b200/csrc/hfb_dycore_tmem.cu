@@ -809,7 +809,8 @@ __global__ void __launch_bounds__(kWsThreads, 2)
         const uint32_t so_u = __shfl_sync(0xffffffffu, so, 0);
         const uint32_t fb = full0 + __shfl_sync(0xffffffffu, tma_bar, 0);
         const int k_u = __shfl_sync(0xffffffffu, tma_k, 0);
-        if (lane == 0) {
+        if (sm100::elect_one()) {  // (not lane == 0: with elect.sync the compiler emits no
+          // per-active-lane BRA.U.ANY loop around the UTMALDGs)
         if (warp == 0) sm100::mbar_arrive_expect_tx(fb, kWStageTx);
         sm100::tma_load_3d(dst0 + so_u, &maps.m[f0], fb, x00 + dx0, y00 + dy0, k_u);
         if (f1 >= 0)
